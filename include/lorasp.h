@@ -1,0 +1,161 @@
+/*
+ * liblorasp — B200-native (sm_100a) LoRaSp level sweep: the hierarchical
+ * low-rank approximate LU of a sparse matrix of arxiv 1510.07363
+ * ("LoRaSp"), used as a direct solver or as a Krylov preconditioner.
+ *
+ * C ABI: plain pointers and sizes, no torch / C++ types.  Every entry point
+ * returns an lorasp_status (0 = OK, > 0 soft, < 0 hard error); the message of
+ * the last error is available from lorasp_last_error().  Hard errors leave the
+ * handle valid but unfactored.
+ *
+ * Pointers that carry numeric data (values, b, x) may be HOST or DEVICE
+ * pointers: the library inspects them with cudaPointerGetAttributes and copies
+ * host buffers through its own device staging (the "e2e" path).  Device
+ * pointers must live on the handle's device.  Caller-owned memory is only
+ * borrowed for the duration of the call; the library owns everything it
+ * allocates and frees it in lorasp_destroy().
+ *
+ * Citations: "P:l.N" = line N of the paper text.
+ */
+#ifndef LORASP_H
+#define LORASP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lorasp_ctx *lorasp_handle;  /* opaque, owned by the library */
+
+typedef enum {
+  LORASP_OK = 0,
+  LORASP_NOT_CONVERGED = 1,     /* soft: Krylov hit max_it; x holds the last iterate      */
+  LORASP_E_ARG = -1,            /* bad argument (null pointer, size, flag)                */
+  LORASP_E_PATTERN = -2,        /* pattern not usable (asymmetric structure, bad CSR)     */
+  LORASP_E_SINGULAR_PIVOT = -3, /* a pivot's signed Cholesky failed (node in last_error)  */
+  LORASP_E_EIG_NOCONV = -4,     /* Jacobi eigen-solver did not converge                   */
+  LORASP_E_CUDA = -5,           /* CUDA runtime error                                     */
+  LORASP_E_OOM = -6,            /* device allocation failed                               */
+  LORASP_E_NCCL = -7,           /* reserved for the multi-GPU exchange                    */
+  LORASP_E_STATE = -8           /* call out of order (e.g. apply before factor)           */
+} lorasp_status;
+
+/* analyze flags */
+#define LORASP_SPD            0x1u  /* symmetric input: symmetric block store, SPD path  */
+#define LORASP_ORDER_NATURAL  0x2u  /* ascending cluster order, one node per wave (debug:
+                                       the paper's literal Alg. 1 loop, P:l.281)         */
+
+/* Krylov methods for lorasp_krylov_ex */
+#define LORASP_CG     0
+#define LORASP_GMRES  1
+
+/*
+ * lorasp_analyze — symbolic phase (host only; no device work).
+ *   Builds the nested partitionings P_0..P_depth by recursive coordinate
+ *   bisection (Def. nested partitionings, P:l.214-216), the quotient graphs of
+ *   A at every level (Def. adjacency graph P:l.73-76, adjacent clusters
+ *   P:l.247-249), a distance-2 colouring per level (the order within a level
+ *   is free, P:l.843), and replays Alg. 1 (P:l.265-289) symbolically: per
+ *   super-node the well-separated partners, the neighbours it is eliminated
+ *   against and every block that fill creates (Theorem, P:l.515-521).
+ *
+ *   n         number of unknowns (> 0)
+ *   row_ptr   host, n+1 int64, CSR row pointers of A (row_ptr[0] = 0)
+ *   col_idx   host, nnz int64, column indices, sorted within each row; the
+ *             pattern must be structurally symmetric (else LORASP_E_PATTERN)
+ *   dim       coordinate dimension (1..3)
+ *   coords    host, n*dim float64, row-major point coordinates
+ *   leaf_size target dofs per leaf red cluster (used when depth <= 0)
+ *   depth     H-tree depth l; <= 0 means round(log2(n / leaf_size))
+ *   eps       truncation threshold of Eq. cutOff1 (P:l.580-584): keep
+ *             sigma_k >= eps * sigma_0; eps = 0 keeps everything (exact)
+ *   flags     LORASP_SPD (required in this version: the SPD path) |
+ *             LORASP_ORDER_NATURAL
+ *   device    CUDA device ordinal the handle will use
+ *   out       receives the handle
+ *   The pattern and coordinates are copied; the caller keeps ownership.
+ */
+int lorasp_analyze(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                   int dim, const double *coords, int leaf_size, int depth,
+                   double eps, unsigned flags, int device, lorasp_handle *out);
+
+/*
+ * lorasp_factor — numeric phase: Alg. 1 (P:l.265-289) on the device.
+ *   values  nnz float64 in the CSR order given to analyze (host or device).
+ *   Per level: MergeRedNodes (P:l.295-313); per distance-2 colour wave:
+ *   Compress (P:l.319-394: batched Gram + Jacobi eigen-solver, rank
+ *   sigma_k >= eps sigma_0, R_k = A_k V, five edge rules) and the fused
+ *   elimination of s and b (P:l.396-399, P:l.101-106).  Re-callable with new
+ *   values on the same pattern.  Returns LORASP_E_SINGULAR_PIVOT /
+ *   LORASP_E_EIG_NOCONV on numerical failure.
+ */
+int lorasp_factor(lorasp_handle h, const double *values);
+
+/*
+ * lorasp_apply — x = Ã b: Alg. 2-4 (P:l.401-500), forward and backward
+ *   substitution over the frozen factors in elimination order.
+ *   b, x: n float64 (host or device, both of the same kind); x must not alias b.
+ */
+int lorasp_apply(lorasp_handle h, const double *b, double *x);
+
+/*
+ * lorasp_gmres — right-preconditioned GMRES(50) with Ã (P:l.651-669):
+ *   x (in: ignored, x0 = 0; out: solution) until ||b - A x|| / ||b|| <= tol
+ *   or 500 iterations (LORASP_NOT_CONVERGED).
+ */
+int lorasp_gmres(lorasp_handle h, const double *b, double *x, double tol);
+
+/*
+ * lorasp_krylov_ex — the full form: method LORASP_CG (preconditioned CG,
+ *   P:l.652) or LORASP_GMRES; restart (GMRES), max_it; outputs the number of
+ *   iterations (A-products) and the final true relative residual
+ *   ||b - A x||_2 / ||b||_2 (Eq. accres, P:l.585-589).  iters / relres may be NULL.
+ */
+int lorasp_krylov_ex(lorasp_handle h, const double *b, double *x, double tol,
+                     int method, int restart, int max_it, int *iters, double *relres);
+
+/* Use an existing cudaStream_t (passed as void*) for all device work; NULL = default. */
+int lorasp_set_stream(lorasp_handle h, void *cuda_stream);
+
+/* Structure queries (valid after analyze): depth l and, for level i (1..l),
+ * the number of clusters 2^(i-1) and the processing order of those clusters
+ * (order[k] = cluster processed k-th) and its colour waves (wave[c]). */
+int lorasp_get_depth(lorasp_handle h, int *depth);
+int lorasp_get_level_order(lorasp_handle h, int level, int *order, int *wave, int cap);
+
+/* Numeric queries (valid after factor): per-node retained rank r of s_c^[i]
+ * (c = 0..2^(i-1)-1), and per-level super-node sizes m_c. */
+int lorasp_get_ranks(lorasp_handle h, int level, int *ranks, int cap);
+int lorasp_get_sizes(lorasp_handle h, int level, int *sizes, int cap);
+
+/* JSON statistics (ranks per level, algorithmic flops, phase times, bytes)
+ * into buf (NUL-terminated, truncated to cap). Returns the full length needed
+ * through *len if len != NULL. */
+int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len);
+
+/* Number of kernel launches issued by the last factor / apply / krylov call. */
+int lorasp_get_launch_count(lorasp_handle h, int64_t *factor_launches,
+                            int64_t *apply_launches, int64_t *krylov_launches);
+
+/*
+ * Kernel-level test hooks (host buffers, run on `device`, synchronous).
+ * lorasp_test_eig: the Compress eigen-solver on one symmetric PSD Gram matrix
+ *   G (m x m, column-major): sigma (m, descending sqrt-eigenvalues), rank
+ *   r = #{sigma_k >= eps sigma_0}, V (m x r, column-major) the leading
+ *   eigenvectors (P:l.333-359, Eq. cutOff1).
+ * lorasp_test_pivot: the fused (s, b) pivot kernel on K = [[S, V], [V^T, 0]]
+ *   (n = m + r, column-major, lower triangle read): overwrites K with L^{-1}
+ *   where K = L diag(I_m, -I_r) L^T.  Returns LORASP_E_SINGULAR_PIVOT on failure.
+ */
+int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, double *sigma, int *rank);
+int lorasp_test_pivot(int device, double *K, int m, int r);
+
+const char *lorasp_last_error(lorasp_handle h);
+void lorasp_destroy(lorasp_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LORASP_H */

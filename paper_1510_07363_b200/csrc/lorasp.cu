@@ -1,0 +1,1275 @@
+// liblorasp: host orchestration of the level sweep + the C ABI (include/lorasp.h).
+//
+// factor(): for each level i = l..1 (Alg. 1, P:l.265-289)
+//   level start : exact super-node sizes m_c (from the ranks of level i+1),
+//                 bound-allocated block slots in a per-level arena, zeroed;
+//                 MergeRedNodes (P:l.295-313) = leaf scatter (i = l) or copies
+//                 of the level-(i+1) red-red blocks;
+//   per colour wave (distance-2 colouring => all nodes of a wave touch
+//   disjoint blocks, so the wave is one batch):
+//     Compress (P:l.319-394): Gram of the stacked well-separated blocks
+//       (k_gemm) -> Jacobi eigen-solver + rank (k_jacobi) -> host reads the
+//       ranks -> R_k = A_k V written to the new P(b) <-> p_k blocks (k_gemm);
+//     Eliminate s then b (P:l.101-106, l.396-399), fused: gather the pivot
+//       K = [[S, V], [V^T, 0]] and coupling C into the node's record F
+//       (k_copy), K = L D L^T and L^{-1} (k_pivot), Z = L^{-1} C (k_gemm),
+//       Schur update T_ab -= Z_a^T D Z_b into the target blocks (k_gemm).
+//   The frozen records F = [L^{-1} | Z] are the factor used by apply().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.cuh"
+#include "lorasp.h"
+
+namespace lorasp {
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess) {                                                           \
+      throw Err(LORASP_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));      \
+    }                                                                                  \
+  } while (0)
+
+struct Err {
+  int code;
+  std::string msg;
+  Err(int c, std::string m) : code(c), msg(std::move(m)) {}
+};
+
+static const int SMEM_LIMIT = 226 * 1024;  // dynamic; leaves room for static smem
+
+// growable device buffer; growth synchronises the stream first (no in-flight use)
+struct DevBuf {
+  void *p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes, cudaStream_t st) {
+    if (bytes <= cap) return;
+    if (p) {
+      CK(cudaStreamSynchronize(st));
+      CK(cudaFree(p));
+      p = nullptr;
+      cap = 0;
+    }
+    size_t nb = std::max<size_t>(bytes + bytes / 4, 1 << 20);
+    if (cudaMalloc(&p, nb) != cudaSuccess) {
+      cudaGetLastError();
+      throw Err(LORASP_E_OOM, "device allocation of " + std::to_string(nb) + " bytes failed");
+    }
+    cap = nb;
+  }
+  template <class T>
+  T *as() const { return reinterpret_cast<T *>(p); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// bump pool of device chunks for the frozen factor records
+struct Pool {
+  struct Chunk {
+    double *p;
+    size_t cap;
+  };
+  std::vector<Chunk> chunks;
+  size_t ci = 0, used = 0, total_used = 0;
+  double *alloc(size_t nd) {
+    nd = (nd + 31) & ~size_t(31);
+    while (ci < chunks.size() && used + nd > chunks[ci].cap) {
+      ++ci;
+      used = 0;
+    }
+    if (ci == chunks.size()) {
+      size_t cap = std::max<size_t>(nd, size_t(32) << 20);  // >= 256 MB
+      double *p = nullptr;
+      if (cudaMalloc(&p, cap * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();
+        throw Err(LORASP_E_OOM, "factor pool allocation failed");
+      }
+      chunks.push_back({p, cap});
+      used = 0;
+    }
+    double *r = chunks[ci].p + used;
+    used += nd;
+    total_used += nd;
+    return r;
+  }
+  void reset() { ci = 0; used = 0; total_used = 0; }
+  void release() {
+    for (auto &c : chunks) cudaFree(c.p);
+    chunks.clear();
+    reset();
+  }
+};
+
+// host-side pinned staging + device mirror for task descriptors
+struct Staging {
+  char *h = nullptr;
+  DevBuf d;
+  size_t cap = 0, used = 0;
+  void init(size_t bytes, cudaStream_t st) {
+    if (h) cudaFreeHost(h);
+    CK(cudaMallocHost(&h, bytes));
+    cap = bytes;
+    d.ensure(bytes, st);
+    used = 0;
+  }
+  // make room for a group of pushes that one launch consumes together
+  void reserve(size_t bytes, cudaStream_t st) {
+    size_t need = bytes + 4096;
+    if (used + need <= cap) return;
+    CK(cudaStreamSynchronize(st));
+    used = 0;
+    if (need > cap) init(std::max(need, cap * 2), st);
+  }
+  // copy `bytes` of src into staging and enqueue the H2D copy; returns device ptr
+  void *push(const void *src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return d.p;
+    size_t need = (bytes + 255) & ~size_t(255);
+    if (used + need > cap) {
+      CK(cudaStreamSynchronize(st));
+      used = 0;
+      if (need > cap) init(std::max(need, cap * 2), st);
+    }
+    std::memcpy(h + used, src, bytes);
+    void *dp = d.as<char>() + used;
+    CK(cudaMemcpyAsync(dp, h + used, bytes, cudaMemcpyHostToDevice, st));
+    used += need;
+    return dp;
+  }
+  void reset() { used = 0; }  // only after a stream sync
+  void release() {
+    if (h) cudaFreeHost(h);
+    h = nullptr;
+    d.release();
+  }
+};
+
+struct NodeRec {  // one eliminated (s, b) pair, for apply + stats
+  int level, c, m, r, W;
+  double *F;
+  std::vector<int> T;  // level node ids (S: c', P: K + c')
+  std::vector<int> w;  // widths
+};
+
+}  // namespace lorasp
+
+using namespace lorasp;
+
+struct lorasp_ctx {
+  Plan plan;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  bool factored = false;
+  bool mem_ready = false;
+  // numeric state
+  std::vector<std::vector<int>> msz, rnk;  // [level][cluster]
+  std::vector<std::vector<double>> sigma0; // unused placeholder for stats
+  DevBuf d_values, d_rowptr, d_colidx, d_dest, arena[2], ws_G, ws_V, ws_sig, ws_X, ws_ctr, d_ranks,
+      d_status, d_vec, d_y, d_perm, d_b, d_x, d_kry, d_apnodes, d_apsegs, d_dotpart;
+  int *h_ranks = nullptr;
+  int *h_status = nullptr;
+  double *h_dot = nullptr;
+  Pool fpool;
+  Staging stg;
+  std::vector<NodeRec> recs;
+  // apply plan
+  std::vector<int> ap_wave_begin;  // in recs order (factor order), per wave
+  size_t ap_fwd_smem = 0, ap_bwd_smem = 0;
+  int64_t vec_len = 0;
+  bool dest_ready = false;
+  std::vector<int64_t> leaf_soff;  // leaf-level slot offsets used for d_dest
+  // stats
+  double flops_model = 0, t_factor_ms = 0;
+  int64_t launches_factor = 0, launches_apply = 0, launches_krylov = 0;
+  int64_t f_doubles = 0;
+  bool debug = getenv("LORASP_DEBUG") != nullptr;
+};
+
+namespace {
+
+inline dim3 grid1(int64_t n, int bs = 256) {
+  int64_t g = (n + bs - 1) / bs;
+  return dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16)));
+}
+
+bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void ensure_mem(lorasp_ctx *h) {
+  if (h->mem_ready) return;
+  CK(cudaSetDevice(h->device));
+  const Plan &pl = h->plan;
+  h->d_rowptr.ensure((pl.n + 1) * sizeof(int64_t), h->stream);
+  h->d_colidx.ensure(std::max<int64_t>(1, pl.nnz) * sizeof(int64_t), h->stream);
+  CK(cudaMemcpy(h->d_rowptr.p, pl.row_ptr.data(), (pl.n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_colidx.p, pl.col_idx.data(), pl.nnz * sizeof(int64_t), cudaMemcpyHostToDevice));
+  h->d_values.ensure(std::max<int64_t>(1, pl.nnz) * sizeof(double), h->stream);
+  h->d_status.ensure(64, h->stream);
+  CK(cudaMallocHost(&h->h_ranks, sizeof(int) * (1 << 20)));
+  CK(cudaMallocHost(&h->h_status, 64));
+  CK(cudaMallocHost(&h->h_dot, 64 * sizeof(double)));
+  h->d_dotpart.ensure((DOT_BLOCKS + 64) * sizeof(double), h->stream);
+  h->stg.init(size_t(64) << 20, h->stream);
+  CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_apply_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  h->mem_ready = true;
+}
+
+template <class T>
+T *push(lorasp_ctx *h, const std::vector<T> &v) {
+  return reinterpret_cast<T *>(h->stg.push(v.data(), v.size() * sizeof(T), h->stream));
+}
+
+void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::vector<GemmSeg> &segs) {
+  if (tasks.empty()) return;
+  h->stg.reserve(segs.size() * sizeof(GemmSeg) + tasks.size() * sizeof(GemmTask), h->stream);
+  GemmSeg *ds = push(h, segs);
+  GemmTask *dt = push(h, tasks);
+  const size_t maxg = 65535 * 32;
+  for (size_t o = 0; o < tasks.size(); o += maxg) {
+    unsigned nb = (unsigned)std::min(maxg, tasks.size() - o);
+    k_gemm<<<nb, 256, 0, h->stream>>>(dt + o, ds);
+    ++h->launches_factor;
+  }
+  CK(cudaGetLastError());
+}
+
+void launch_copy(lorasp_ctx *h, const std::vector<CopyTask> &tasks) {
+  if (tasks.empty()) return;
+  CopyTask *dt = push(h, tasks);
+  k_copy<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt);
+  ++h->launches_factor;
+  CK(cudaGetLastError());
+}
+
+// tile a logical M x N product into 64x64 tasks
+void add_tiles(std::vector<GemmTask> &tasks, GemmTask base, int kmax_by_row = 0) {
+  (void)kmax_by_row;
+  for (int tn = 0; tn < base.N; tn += GT)
+    for (int tm = 0; tm < base.M; tm += GT) {
+      GemmTask t = base;
+      t.tm = tm;
+      t.tn = tn;
+      tasks.push_back(t);
+    }
+}
+
+double node_flops(int m, int r, int R, int W) {
+  // SURVEY §8(d) algorithmic work (SPD path): compress + fused elimination
+  double f = 0;
+  if (R > 0) f += (double)R * m * m + 9.0 * m * m * (double)m + 2.0 * R * m * (double)r;
+  f += ((double)m * m * m + (double)r * r * r) / 3.0 + ((double)m * m + (double)r * r) * (W + r) +
+       (double)(m + r) * (W + r) * (W + r);
+  return f;
+}
+
+void factor_impl(lorasp_ctx *h, const double *values) {
+  ensure_mem(h);
+  const Plan &pl = h->plan;
+  cudaStream_t st = h->stream;
+  const int L = pl.depth;
+  h->launches_factor = 0;
+  h->flops_model = 0;
+  h->factored = false;
+  // values -> device
+  if (is_device_ptr(values)) {
+    CK(cudaMemcpyAsync(h->d_values.p, values, pl.nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  } else {
+    CK(cudaMemcpyAsync(h->d_values.p, values, pl.nnz * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemsetAsync(h->d_status.p, 0, 64, st));
+  h->fpool.reset();
+  h->recs.clear();
+  h->msz.assign(L + 2, {});
+  h->rnk.assign(L + 2, {});
+  std::vector<int64_t> prev_soff;
+  std::vector<int> prev_sld;
+  h->stg.reset();
+  CK(cudaStreamSynchronize(st));
+
+  for (int i = L; i >= 1; --i) {
+    const SymLevel &lv = pl.lev[i];
+    const int K = lv.K;
+    std::vector<int> &m = h->msz[i];
+    std::vector<int> &r = h->rnk[i];
+    m.assign(K, 0);
+    r.assign(K, 0);
+    for (int c = 0; c < K; ++c)
+      m[c] = (i == L) ? pl.leaf_size[2 * c] + pl.leaf_size[2 * c + 1]
+                      : h->rnk[i + 1][2 * c] + h->rnk[i + 1][2 * c + 1];
+    auto bound = [&](int id) { return id < K ? m[id] : (lv.node[id - K].aux ? m[id - K] : 0); };
+    auto size = [&](int id) { return id < K ? m[id] : r[id - K]; };
+    // slot layout (bound sizes; P-node ranks are not known yet)
+    std::vector<int64_t> soff(lv.slots.size());
+    std::vector<int> sld(lv.slots.size());
+    int64_t tot = 0;
+    for (size_t s = 0; s < lv.slots.size(); ++s) {
+      int rows = bound(lv.slots[s].row), cols = bound(lv.slots[s].col);
+      sld[s] = std::max(1, rows);
+      soff[s] = tot;
+      tot += ((int64_t)rows * cols + 31) & ~int64_t(31);
+    }
+    DevBuf &ar = h->arena[i & 1];
+    ar.ensure(std::max<int64_t>(tot, 32) * sizeof(double), st);
+    CK(cudaMemsetAsync(ar.p, 0, tot * sizeof(double), st));
+    double *base = ar.as<double>();
+    auto slot_ptr = [&](int s) { return base + soff[s]; };
+
+    // ---- MergeRedNodes ------------------------------------------------------
+    if (i == L) {
+      if (!h->dest_ready || h->leaf_soff != soff) {
+        std::vector<int64_t> dest(pl.nnz, -1);
+        for (int64_t k = 0; k < pl.nnz; ++k)
+          if (pl.nnz_slot[k] >= 0)
+            dest[k] = soff[pl.nnz_slot[k]] + pl.nnz_r[k] + (int64_t)pl.nnz_c[k] * sld[pl.nnz_slot[k]];
+        h->d_dest.ensure(std::max<int64_t>(1, pl.nnz) * sizeof(int64_t), st);
+        CK(cudaMemcpy(h->d_dest.p, dest.data(), pl.nnz * sizeof(int64_t), cudaMemcpyHostToDevice));
+        h->leaf_soff = soff;
+        h->dest_ready = true;
+      }
+      k_leaf_scatter<<<grid1(pl.nnz), 256, 0, st>>>(h->d_values.as<double>(), h->d_dest.as<int64_t>(),
+                                                    pl.nnz, base);
+      ++h->launches_factor;
+      CK(cudaGetLastError());
+    } else {
+      const std::vector<int> &rp = h->rnk[i + 1];  // sizes of the level-i reds
+      double *pbase = h->arena[(i + 1) & 1].as<double>();
+      std::vector<CopyTask> ct;
+      for (const MergeSrc &ms : lv.merge) {
+        int rows = rp[ms.src_cluster_r], cols = rp[ms.src_cluster_c];
+        if (rows == 0 || cols == 0) continue;
+        int ro = (ms.src_cluster_r & 1) ? rp[ms.src_cluster_r - 1] : 0;
+        int co = (ms.src_cluster_c & 1) ? rp[ms.src_cluster_c - 1] : 0;
+        CopyTask t{};
+        t.src = pbase + prev_soff[ms.src_slot];
+        t.lds = prev_sld[ms.src_slot];
+        t.dst = slot_ptr(ms.dst_slot) + ro + (int64_t)co * sld[ms.dst_slot];
+        t.ldd = sld[ms.dst_slot];
+        t.rows = rows;
+        t.cols = cols;
+        t.mode = 0;
+        t.trans = ms.trans ? 1 : 0;
+        t.alpha = 1.0;
+        ct.push_back(t);
+      }
+      launch_copy(h, ct);
+    }
+
+    // ---- colour waves ---------------------------------------------------------
+    for (size_t w = 0; w + 1 < lv.wave_begin.size(); ++w) {
+      std::vector<int> comp, elim;
+      for (int t = lv.wave_begin[w]; t < lv.wave_begin[w + 1]; ++t) {
+        int c = lv.order[t];
+        const SymNode &nd = lv.node[c];
+        if (!nd.exists || m[c] == 0) continue;
+        elim.push_back(c);
+        if (nd.aux) comp.push_back(c);
+      }
+      if (elim.empty()) continue;
+      // --- Compress: Gram + Jacobi + rank ---
+      std::vector<int64_t> goff(K, 0);
+      if (!comp.empty()) {
+        int64_t gtot = 0, stot = 0, xtot = 0;
+        for (int c : comp) {
+          goff[c] = gtot;
+          gtot += (int64_t)m[c] * m[c];
+          stot += m[c];
+          if ((int64_t)m[c] * m[c] + 2 * m[c] > SMEM_LIMIT / 8) xtot += (int64_t)m[c] * m[c];
+        }
+        h->ws_G.ensure(gtot * 8 + 256, st);
+        h->ws_V.ensure(gtot * 8 + 256, st);
+        h->ws_sig.ensure(stot * 8 + 256, st);
+        h->ws_X.ensure(xtot * 8 + 256, st);
+        h->d_ranks.ensure(comp.size() * sizeof(int) + 64, st);
+        std::vector<GemmTask> gt;
+        std::vector<GemmSeg> gs;
+        std::vector<EigTask> et;
+        int64_t soff_sig = 0, xoff = 0;
+        int max_m = 0;
+        for (size_t q = 0; q < comp.size(); ++q) {
+          const int c = comp[q];
+          const SymNode &nd = lv.node[c];
+          const int mc = m[c];
+          max_m = std::max(max_m, mc);
+          GemmTask b{};
+          b.C = h->ws_G.as<double>() + goff[c];
+          b.ldc = mc;
+          b.M = b.N = mc;
+          b.ta = 0;
+          b.tb = 1;
+          b.tc = 0;
+          b.beta = 0;
+          b.seg0 = (int)gs.size();
+          int R = 0;
+          for (size_t k = 0; k < nd.partners.size(); ++k) {
+            int p = nd.partners[k], sl = nd.pslot_src[k];
+            int mk = size(p);
+            if (mk == 0) continue;
+            GemmSeg g{};
+            g.A = slot_ptr(sl);
+            g.B = slot_ptr(sl);
+            g.lda = g.ldb = sld[sl];
+            g.K = mk;
+            g.alpha = 1.0;
+            gs.push_back(g);
+            R += mk;
+          }
+          b.nseg = (int)gs.size() - b.seg0;
+          add_tiles(gt, b);
+          EigTask e{};
+          e.G = b.C;
+          e.V = h->ws_V.as<double>() + goff[c];
+          e.sig = h->ws_sig.as<double>() + soff_sig;
+          soff_sig += mc;
+          if ((int64_t)mc * mc + 2 * mc > SMEM_LIMIT / 8) {
+            e.work = h->ws_X.as<double>() + xoff;
+            xoff += (int64_t)mc * mc;
+          }
+          e.m = mc;
+          e.node = c;
+          e.rank_out = h->d_ranks.as<int>() + q;
+          et.push_back(e);
+        }
+        launch_gemm(h, gt, gs);
+        EigTask *de = push(h, et);
+        int64_t want = (int64_t)max_m * max_m + 2 * max_m;
+        int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
+        cap = std::max(cap, 2 * max_m);
+        k_jacobi<<<(unsigned)et.size(), 512, cap * 8, st>>>(de, pl.eps, cap, h->d_status.as<int>());
+        ++h->launches_factor;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h->h_ranks, h->d_ranks.p, comp.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        h->stg.reset();
+        if (h->h_status[0] != 0) {
+          throw Err(h->h_status[0], std::string(h->h_status[0] == LORASP_E_EIG_NOCONV
+                                                    ? "Jacobi eigen-solver did not converge"
+                                                    : "singular pivot") +
+                                        " at level " + std::to_string(i) + " node " +
+                                        std::to_string(h->h_status[1]));
+        }
+        for (size_t q = 0; q < comp.size(); ++q) r[comp[q]] = h->h_ranks[q];
+      }
+      // --- project, assemble, pivot, Z, Schur ---
+      std::vector<GemmTask> pt, zt, stt;
+      std::vector<GemmSeg> ps, zs, ss;
+      std::vector<CopyTask> ct;
+      std::vector<PivTask> pv;
+      int64_t ctr_tot = 0;
+      std::vector<int64_t> ctr_off(elim.size());
+      std::vector<int> Wn(elim.size());
+      for (size_t e = 0; e < elim.size(); ++e) {
+        const int c = elim[e];
+        const SymNode &nd = lv.node[c];
+        int W = 0;
+        for (int u : nd.n1) W += size(u);
+        if (nd.aux) W += r[c];
+        Wn[e] = W;
+        ctr_off[e] = ctr_tot;
+        ctr_tot += ((int64_t)(m[c] + r[c]) * W + 31) & ~int64_t(31);
+      }
+      h->ws_ctr.ensure(std::max<int64_t>(ctr_tot, 32) * 8, st);
+      int max_n = 0;
+      for (size_t e = 0; e < elim.size(); ++e) {
+        const int c = elim[e];
+        const SymNode &nd = lv.node[c];
+        const int mc = m[c], rc = r[c], n = mc + rc, W = Wn[e];
+        max_n = std::max(max_n, n);
+        double *V = h->ws_V.as<double>() + goff[c];
+        // project: R_k = A_k V  into  P(b) <-> p_k  (edge rules 2/3, P:l.385-386)
+        int R = 0;
+        if (nd.aux && rc > 0) {
+          for (size_t k = 0; k < nd.partners.size(); ++k) {
+            int p = nd.partners[k];
+            int mk = size(p);
+            R += mk;
+            if (mk == 0) continue;
+            int s1 = nd.pslot_src[k], s2 = nd.pslot_dst[k];
+            GemmTask b{};
+            b.C = slot_ptr(s2);
+            b.ldc = sld[s2];
+            b.M = mk;
+            b.N = rc;
+            b.ta = 1;
+            b.tb = 0;
+            b.tc = (lv.slots[s2].row == p) ? 0 : 1;
+            b.beta = 0;
+            b.seg0 = (int)ps.size();
+            b.nseg = 1;
+            GemmSeg g{};
+            g.A = slot_ptr(s1);
+            g.lda = sld[s1];
+            g.B = V;
+            g.ldb = mc;
+            g.K = mc;
+            g.alpha = 1.0;
+            ps.push_back(g);
+            add_tiles(pt, b);
+          }
+        } else if (nd.aux) {
+          for (int p : nd.partners) R += size(p);
+        }
+        // record F = [L^{-1} | Z]  (n x (n + W))
+        double *F = h->fpool.alloc((size_t)n * (n + W));
+        double *ctr = h->ws_ctr.as<double>() + ctr_off[e];
+        h->f_doubles += (int64_t)n * (n + W);
+        NodeRec rec;
+        rec.level = i;
+        rec.c = c;
+        rec.m = mc;
+        rec.r = rc;
+        rec.W = W;
+        rec.F = F;
+        // assemble pivot K = [[S, V], [V^T, 0]] (lower part used)
+        CopyTask t{};
+        t.src = slot_ptr(nd.self_slot);
+        t.lds = sld[nd.self_slot];
+        t.dst = F;
+        t.ldd = n;
+        t.rows = mc;
+        t.cols = mc;
+        t.mode = 0;
+        t.trans = 0;
+        t.alpha = 1.0;
+        ct.push_back(t);
+        if (rc > 0) {
+          t = CopyTask{};
+          t.src = V;
+          t.lds = mc;
+          t.dst = F + mc;
+          t.ldd = n;
+          t.rows = rc;
+          t.cols = mc;
+          t.mode = 0;
+          t.trans = 1;
+          t.alpha = 1.0;
+          ct.push_back(t);  // V^T (s -> b, rule 4)
+          t = CopyTask{};
+          t.dst = F + mc + (int64_t)mc * n;
+          t.ldd = n;
+          t.rows = rc;
+          t.cols = rc;
+          t.mode = 1;
+          t.alpha = 0.0;
+          ct.push_back(t);  // b has no self block (reading Z13)
+        }
+        // coupling C: rows (s; b), columns T = N1(s) + [P(b)]
+        int zc = 0;
+        for (size_t k = 0; k < nd.n1.size(); ++k) {
+          int u = nd.n1[k], wu = size(u);
+          rec.T.push_back(u);
+          rec.w.push_back(wu);
+          if (wu > 0) {
+            t = CopyTask{};
+            t.src = slot_ptr(nd.n1_slot[k]);
+            t.lds = sld[nd.n1_slot[k]];
+            t.dst = ctr + (int64_t)zc * n;
+            t.ldd = n;
+            t.rows = mc;
+            t.cols = wu;
+            t.mode = 0;
+            t.alpha = 1.0;
+            ct.push_back(t);
+          }
+          zc += wu;
+        }
+        if (rc > 0 && zc > 0) {
+          t = CopyTask{};
+          t.dst = ctr + mc;
+          t.ldd = n;
+          t.rows = rc;
+          t.cols = zc;
+          t.mode = 1;
+          t.alpha = 0.0;
+          ct.push_back(t);
+        }
+        if (nd.aux) {
+          rec.T.push_back(K + c);
+          rec.w.push_back(rc);
+          if (rc > 0) {
+            t = CopyTask{};
+            t.dst = ctr + (int64_t)zc * n;
+            t.ldd = n;
+            t.rows = mc;
+            t.cols = rc;
+            t.mode = 1;
+            t.alpha = 0.0;
+            ct.push_back(t);
+            t = CopyTask{};
+            t.dst = ctr + (int64_t)zc * n + mc;
+            t.ldd = n;
+            t.rows = rc;
+            t.cols = rc;
+            t.mode = 2;
+            t.alpha = -1.0;
+            ct.push_back(t);  // b <-> P(b): -I_r (rule 5)
+          }
+        }
+        // pivot
+        pv.push_back(PivTask{F, n, mc, rc, c});
+        // Z = L^{-1} C  (L^{-1} lower triangular: row tile tm needs k < tm + 64)
+        if (W > 0) {
+          for (int tn = 0; tn < W; tn += GT)
+            for (int tm = 0; tm < n; tm += GT) {
+              GemmTask b{};
+              b.C = F + (int64_t)n * n;
+              b.ldc = n;
+              b.M = n;
+              b.N = W;
+              b.tm = tm;
+              b.tn = tn;
+              b.beta = 0;
+              b.seg0 = (int)zs.size();
+              b.nseg = 1;
+              GemmSeg g{};
+              g.A = F;
+              g.lda = n;
+              g.B = ctr;
+              g.ldb = n;
+              g.K = std::min(n, tm + GT);
+              g.alpha = 1.0;
+              zs.push_back(g);
+              zt.push_back(b);
+            }
+        }
+        // Schur: T_a,b -= Z_a^T D Z_b   (D = diag(I_m, -I_r))
+        {
+          const std::vector<int> &T = rec.T;
+          std::vector<int> zoff(T.size() + 1, 0);
+          for (size_t a = 0; a < T.size(); ++a) zoff[a + 1] = zoff[a] + rec.w[a];
+          const double *Z = F + (int64_t)n * n;
+          size_t idx = 0;
+          for (size_t a = 0; a < T.size(); ++a)
+            for (size_t bb = 0; bb <= a; ++bb, ++idx) {
+              int wa = rec.w[a], wb = rec.w[bb];
+              if (wa == 0 || wb == 0) continue;
+              int sl = nd.tslot[idx];
+              GemmTask b{};
+              b.C = slot_ptr(sl);
+              b.ldc = sld[sl];
+              b.M = wa;
+              b.N = wb;
+              b.ta = 1;
+              b.tb = 0;
+              b.tc = (a != bb && lv.slots[sl].row != T[a]) ? 1 : 0;
+              b.beta = 1;
+              b.seg0 = (int)ss.size();
+              GemmSeg g{};
+              g.A = Z + (int64_t)zoff[a] * n;
+              g.B = Z + (int64_t)zoff[bb] * n;
+              g.lda = g.ldb = n;
+              g.K = mc;
+              g.alpha = -1.0;
+              ss.push_back(g);
+              if (rc > 0) {
+                g.A += mc;
+                g.B += mc;
+                g.K = rc;
+                g.alpha = 1.0;
+                ss.push_back(g);
+              }
+              b.nseg = (int)ss.size() - b.seg0;
+              add_tiles(stt, b);
+            }
+        }
+        h->flops_model += node_flops(mc, rc, nd.aux ? R : 0, W);
+        h->recs.push_back(std::move(rec));
+      }
+      launch_gemm(h, pt, ps);
+      launch_copy(h, ct);
+      {
+        PivTask *dp = push(h, pv);
+        int64_t want = (int64_t)max_n * max_n + max_n;
+        int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
+        cap = std::max(cap, max_n);
+        k_pivot<<<(unsigned)pv.size(), 512, cap * 8, st>>>(dp, cap, h->d_status.as<int>());
+        ++h->launches_factor;
+        CK(cudaGetLastError());
+      }
+      launch_gemm(h, zt, zs);
+      launch_gemm(h, stt, ss);
+      if (h->debug) {
+        CK(cudaStreamSynchronize(st));
+        CK(cudaMemcpy(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "[lorasp] level %d wave %zu: %zu nodes, %zu compressed, status %d (node %d); ranks:",
+                i, w, elim.size(), comp.size(), h->h_status[0], h->h_status[1]);
+        for (int c : elim) fprintf(stderr, " %d:%d/%d", c, r[c], m[c]);
+        fprintf(stderr, "\n");
+      }
+    }
+    prev_soff.swap(soff);
+    prev_sld.swap(sld);
+  }
+  CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->stg.reset();
+  if (h->h_status[0] != 0)
+    throw Err(h->h_status[0], std::string(h->h_status[0] == LORASP_E_EIG_NOCONV
+                                              ? "Jacobi eigen-solver did not converge"
+                                              : "singular pivot (signed Cholesky failed)") +
+                                  " at node " + std::to_string(h->h_status[1]));
+
+  // ---- apply plan: vector layout over red nodes of every level --------------
+  std::vector<std::vector<int64_t>> voff(L + 1);
+  int64_t tot = 0;
+  for (int k = L; k >= 0; --k) {
+    int ncl = 1 << k;
+    voff[k].assign(ncl, 0);
+    for (int c = 0; c < ncl; ++c) {
+      voff[k][c] = tot;
+      tot += (k == L) ? pl.leaf_size[c] : h->rnk[k + 1][c];
+    }
+  }
+  h->vec_len = tot;
+  std::vector<ApNode> an;
+  std::vector<ApSeg> as;
+  int64_t ytot = 0;
+  std::vector<int64_t> yoff;
+  for (auto &rc : h->recs) {
+    yoff.push_back(ytot);
+    ytot += ((int64_t)(rc.m + rc.r) + 3) & ~int64_t(3);
+  }
+  h->d_y.ensure(std::max<int64_t>(ytot, 8) * 8, st);
+  h->ap_wave_begin.clear();
+  size_t fwd = 0, bwd = 0;
+  int prev_level = -1, prev_wave = -1;
+  for (size_t q = 0; q < h->recs.size(); ++q) {
+    const NodeRec &rc = h->recs[q];
+    const SymLevel &lv = pl.lev[rc.level];
+    int wv = lv.node[rc.c].wave;
+    if (rc.level != prev_level || wv != prev_wave) h->ap_wave_begin.push_back((int)q);
+    prev_level = rc.level;
+    prev_wave = wv;
+    ApNode a{};
+    a.F = rc.F;
+    a.y = h->d_y.as<double>() + yoff[q];
+    a.off_s = voff[rc.level][2 * rc.c];
+    a.m = rc.m;
+    a.r = rc.r;
+    a.W = rc.W;
+    a.seg0 = (int)as.size();
+    int zc = 0;
+    const int K = lv.K;
+    for (size_t k = 0; k < rc.T.size(); ++k) {
+      int u = rc.T[k];
+      ApSeg sgm{};
+      sgm.voff = (u < K) ? voff[rc.level][2 * u] : voff[rc.level - 1][u - K];
+      sgm.w = rc.w[k];
+      sgm.zc = zc;
+      zc += rc.w[k];
+      if (sgm.w > 0) as.push_back(sgm);
+    }
+    a.nseg = (int)as.size() - a.seg0;
+    an.push_back(a);
+    int n = rc.m + rc.r;
+    fwd = std::max(fwd, (size_t)(rc.m + n));
+    bwd = std::max(bwd, (size_t)(n + rc.W));
+  }
+  h->ap_wave_begin.push_back((int)h->recs.size());
+  h->ap_fwd_smem = fwd * 8;
+  h->ap_bwd_smem = bwd * 8;
+  if (h->ap_fwd_smem > (size_t)SMEM_LIMIT || h->ap_bwd_smem > (size_t)SMEM_LIMIT)
+    throw Err(LORASP_E_ARG, "apply: node record too large for the shared-memory apply kernel");
+  h->d_apnodes.ensure(std::max<size_t>(1, an.size()) * sizeof(ApNode), st);
+  h->d_apsegs.ensure(std::max<size_t>(1, as.size()) * sizeof(ApSeg), st);
+  CK(cudaMemcpy(h->d_apnodes.p, an.data(), an.size() * sizeof(ApNode), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(h->d_apsegs.p, as.data(), as.size() * sizeof(ApSeg), cudaMemcpyHostToDevice));
+  std::vector<int64_t> perm(pl.n);
+  for (int64_t q = 0; q < pl.n; ++q) perm[q] = voff[L][pl.leaf_of[q]] + pl.leaf_pos[q];
+  h->d_perm.ensure(pl.n * sizeof(int64_t), st);
+  CK(cudaMemcpy(h->d_perm.p, perm.data(), pl.n * sizeof(int64_t), cudaMemcpyHostToDevice));
+  h->d_vec.ensure(std::max<int64_t>(tot, 8) * 8, st);
+  h->d_b.ensure(pl.n * 8, st);
+  h->d_x.ensure(pl.n * 8, st);
+  h->factored = true;
+}
+
+// x = Ã b on device buffers
+void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
+  cudaStream_t st = h->stream;
+  const Plan &pl = h->plan;
+  CK(cudaMemsetAsync(h->d_vec.p, 0, h->vec_len * 8, st));
+  k_set_rhs<<<grid1(pl.n), 256, 0, st>>>(b, h->d_perm.as<int64_t>(), pl.n, h->d_vec.as<double>());
+  const ApNode *nodes = h->d_apnodes.as<ApNode>();
+  const ApSeg *segs = h->d_apsegs.as<ApSeg>();
+  const int nw = (int)h->ap_wave_begin.size() - 1;
+  for (int w = 0; w < nw; ++w) {
+    int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
+    k_apply_fwd<<<b1 - b0, 256, h->ap_fwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>());
+  }
+  for (int w = nw - 1; w >= 0; --w) {
+    int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
+    k_apply_bwd<<<b1 - b0, 256, h->ap_bwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>());
+  }
+  k_get_x<<<grid1(pl.n), 256, 0, st>>>(h->d_vec.as<double>(), h->d_perm.as<int64_t>(), pl.n, x);
+  *counter += 2 * nw + 2;
+  CK(cudaGetLastError());
+}
+
+double dot_dev(lorasp_ctx *h, const double *a, const double *b) {
+  cudaStream_t st = h->stream;
+  k_dot_partial<<<DOT_BLOCKS, 256, 0, st>>>(h->plan.n, a, b, h->d_dotpart.as<double>());
+  k_dot_final<<<1, 256, 0, st>>>(h->d_dotpart.as<double>(), DOT_BLOCKS,
+                                 h->d_dotpart.as<double>() + DOT_BLOCKS);
+  CK(cudaMemcpyAsync(h->h_dot, h->d_dotpart.as<double>() + DOT_BLOCKS, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  h->launches_krylov += 2;
+  return h->h_dot[0];
+}
+
+void spmv_dev(lorasp_ctx *h, const double *x, double *y) {
+  const Plan &pl = h->plan;
+  k_spmv<<<grid1(pl.n), 256, 0, h->stream>>>(pl.n, h->d_rowptr.as<int64_t>(), h->d_colidx.as<int64_t>(),
+                                            h->d_values.as<double>(), x, y);
+  ++h->launches_krylov;
+}
+
+void axpby(lorasp_ctx *h, double a, const double *x, double b, double *y) {
+  k_axpby<<<grid1(h->plan.n), 256, 0, h->stream>>>(h->plan.n, a, x, b, y);
+  ++h->launches_krylov;
+}
+
+// preconditioned CG (P:l.652; readings Z21/Z24/Z27); device vectors b, x
+int pcg_dev(lorasp_ctx *h, const double *b, double *x, double tol, int maxit, int *iters, double *relres) {
+  const int64_t n = h->plan.n;
+  h->d_kry.ensure(4 * n * 8, h->stream);
+  double *r = h->d_kry.as<double>(), *z = r + n, *p = z + n, *q = p + n;
+  cudaStream_t st = h->stream;
+  CK(cudaMemsetAsync(x, 0, n * 8, st));
+  CK(cudaMemcpyAsync(r, b, n * 8, cudaMemcpyDeviceToDevice, st));
+  double nb = std::sqrt(dot_dev(h, b, b));
+  if (nb == 0.0) {
+    if (iters) *iters = 0;
+    if (relres) *relres = 0;
+    return LORASP_OK;
+  }
+  apply_dev(h, r, z, &h->launches_krylov);
+  CK(cudaMemcpyAsync(p, z, n * 8, cudaMemcpyDeviceToDevice, st));
+  double rz = dot_dev(h, r, z);
+  int it = 0;
+  bool conv = false;
+  for (it = 1; it <= maxit; ++it) {
+    spmv_dev(h, p, q);
+    double pq = dot_dev(h, p, q);
+    if (!(pq > 0) || !(rz > 0)) {
+      it -= 1;
+      break;  // breakdown (reading Z24)
+    }
+    double alpha = rz / pq;
+    axpby(h, alpha, p, 1.0, x);
+    axpby(h, -alpha, q, 1.0, r);
+    double rel = std::sqrt(dot_dev(h, r, r)) / nb;
+    if (rel <= tol) {
+      conv = true;
+      break;
+    }
+    apply_dev(h, r, z, &h->launches_krylov);
+    double rz2 = dot_dev(h, r, z);
+    axpby(h, 1.0, z, rz2 / rz, p);
+    rz = rz2;
+  }
+  if (it > maxit) it = maxit;
+  // true residual
+  spmv_dev(h, x, q);
+  k_sub<<<grid1(n), 256, 0, st>>>(n, b, q, r);
+  ++h->launches_krylov;
+  double rr = std::sqrt(dot_dev(h, r, r)) / nb;
+  if (iters) *iters = it;
+  if (relres) *relres = rr;
+  return (conv || rr <= tol) ? LORASP_OK : LORASP_NOT_CONVERGED;
+}
+
+// right-preconditioned GMRES(restart) with MGS + Givens (reading Z21)
+int gmres_dev(lorasp_ctx *h, const double *b, double *x, double tol, int restart, int maxit, int *iters,
+              double *relres) {
+  const int64_t n = h->plan.n;
+  cudaStream_t st = h->stream;
+  h->d_kry.ensure((size_t)(2 * restart + 3) * n * 8, h->stream);
+  double *Vb = h->d_kry.as<double>();            // (restart+1) x n
+  double *Zb = Vb + (int64_t)(restart + 1) * n;  // restart x n
+  double *w = Zb + (int64_t)restart * n;         // n
+  double *r = w + n;                             // n
+  CK(cudaMemsetAsync(x, 0, n * 8, st));
+  double nb = std::sqrt(dot_dev(h, b, b));
+  if (nb == 0.0) {
+    if (iters) *iters = 0;
+    if (relres) *relres = 0;
+    return LORASP_OK;
+  }
+  int it = 0;
+  bool conv = false;
+  std::vector<double> H((restart + 1) * restart), cs(restart), sn(restart), g(restart + 1);
+  while (it < maxit && !conv) {
+    spmv_dev(h, x, w);
+    k_sub<<<grid1(n), 256, 0, st>>>(n, b, w, r);
+    ++h->launches_krylov;
+    double beta = std::sqrt(dot_dev(h, r, r));
+    if (beta / nb <= tol) {
+      conv = true;
+      break;
+    }
+    axpby(h, 1.0 / beta, r, 0.0, Vb);
+    std::fill(H.begin(), H.end(), 0.0);
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int k_used = 0;
+    for (int k = 0; k < restart && it < maxit; ++k) {
+      apply_dev(h, Vb + (int64_t)k * n, Zb + (int64_t)k * n, &h->launches_krylov);
+      spmv_dev(h, Zb + (int64_t)k * n, w);
+      for (int j = 0; j <= k; ++j) {
+        double hj = dot_dev(h, w, Vb + (int64_t)j * n);
+        H[j + k * (restart + 1)] = hj;
+        axpby(h, -hj, Vb + (int64_t)j * n, 1.0, w);
+      }
+      double hn = std::sqrt(dot_dev(h, w, w));
+      H[k + 1 + k * (restart + 1)] = hn;
+      for (int j = 0; j < k; ++j) {
+        double a = H[j + k * (restart + 1)], bb = H[j + 1 + k * (restart + 1)];
+        H[j + k * (restart + 1)] = cs[j] * a + sn[j] * bb;
+        H[j + 1 + k * (restart + 1)] = -sn[j] * a + cs[j] * bb;
+      }
+      double a = H[k + k * (restart + 1)], bb = H[k + 1 + k * (restart + 1)];
+      double den = std::hypot(a, bb);
+      cs[k] = den == 0 ? 1.0 : a / den;
+      sn[k] = den == 0 ? 0.0 : bb / den;
+      H[k + k * (restart + 1)] = cs[k] * a + sn[k] * bb;
+      H[k + 1 + k * (restart + 1)] = 0;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      ++it;
+      k_used = k + 1;
+      if (std::fabs(g[k + 1]) / nb <= tol) {
+        conv = true;
+        break;
+      }
+      if (hn == 0) break;
+      if (k + 1 < restart || true) axpby(h, 1.0 / hn, w, 0.0, Vb + (int64_t)(k + 1) * n);
+    }
+    // y = H^{-1} g (upper triangular)
+    std::vector<double> y(k_used);
+    for (int j = k_used - 1; j >= 0; --j) {
+      double s = g[j];
+      for (int q = j + 1; q < k_used; ++q) s -= H[j + q * (restart + 1)] * y[q];
+      y[j] = s / H[j + j * (restart + 1)];
+    }
+    for (int j = 0; j < k_used; ++j) axpby(h, y[j], Zb + (int64_t)j * n, 1.0, x);
+  }
+  spmv_dev(h, x, w);
+  k_sub<<<grid1(n), 256, 0, st>>>(n, b, w, r);
+  ++h->launches_krylov;
+  double rr = std::sqrt(dot_dev(h, r, r)) / nb;
+  if (iters) *iters = it;
+  if (relres) *relres = rr;
+  return (rr <= tol) ? LORASP_OK : LORASP_NOT_CONVERGED;
+}
+
+template <class F>
+int guarded(lorasp_ctx *h, F &&f) {
+  if (!h) return LORASP_E_ARG;
+  try {
+    return f();
+  } catch (const Err &e) {
+    h->last_error = e.msg;
+    return e.code;
+  } catch (const std::exception &e) {
+    h->last_error = e.what();
+    return LORASP_E_ARG;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int lorasp_analyze(int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int dim, const double *coords,
+                   int leaf_size, int depth, double eps, unsigned flags, int device, lorasp_handle *out) {
+  if (!out) return LORASP_E_ARG;
+  *out = nullptr;
+  if (!(flags & LORASP_SPD)) return LORASP_E_ARG;  // only the SPD path in this version
+  auto *h = new lorasp_ctx();
+  h->device = device;
+  std::string err;
+  int rc = build_plan(h->plan, n, row_ptr, col_idx, dim, coords, leaf_size, depth, eps, flags, err);
+  if (rc != 0) {
+    delete h;
+    return rc == -1 ? LORASP_E_ARG : LORASP_E_PATTERN;
+  }
+  *out = h;
+  return LORASP_OK;
+}
+
+int lorasp_factor(lorasp_handle h, const double *values) {
+  return guarded(h, [&]() {
+    if (!values) return (int)LORASP_E_ARG;
+    CK(cudaSetDevice(h->device));
+    auto t0 = std::chrono::steady_clock::now();
+    h->f_doubles = 0;
+    factor_impl(h, values);
+    h->t_factor_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return (int)LORASP_OK;
+  });
+}
+
+int lorasp_apply(lorasp_handle h, const double *b, double *x) {
+  return guarded(h, [&]() {
+    if (!b || !x || b == x) return (int)LORASP_E_ARG;
+    if (!h->factored) return (int)LORASP_E_STATE;
+    CK(cudaSetDevice(h->device));
+    const int64_t n = h->plan.n;
+    h->launches_apply = 0;
+    if (is_device_ptr(b)) {
+      apply_dev(h, b, x, &h->launches_apply);
+      CK(cudaStreamSynchronize(h->stream));
+    } else {
+      CK(cudaMemcpyAsync(h->d_b.p, b, n * 8, cudaMemcpyHostToDevice, h->stream));
+      apply_dev(h, h->d_b.as<double>(), h->d_x.as<double>(), &h->launches_apply);
+      CK(cudaMemcpyAsync(x, h->d_x.p, n * 8, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    }
+    return (int)LORASP_OK;
+  });
+}
+
+int lorasp_krylov_ex(lorasp_handle h, const double *b, double *x, double tol, int method, int restart,
+                     int max_it, int *iters, double *relres) {
+  return guarded(h, [&]() {
+    if (!b || !x || b == x || tol < 0 || max_it < 0) return (int)LORASP_E_ARG;
+    if (!h->factored) return (int)LORASP_E_STATE;
+    CK(cudaSetDevice(h->device));
+    if (restart <= 0) restart = 50;
+    const int64_t n = h->plan.n;
+    h->launches_krylov = 0;
+    bool dev = is_device_ptr(b);
+    const double *bd = b;
+    double *xd = x;
+    if (!dev) {
+      CK(cudaMemcpyAsync(h->d_b.p, b, n * 8, cudaMemcpyHostToDevice, h->stream));
+      bd = h->d_b.as<double>();
+      xd = h->d_x.as<double>();
+    }
+    int rc = (method == LORASP_CG) ? pcg_dev(h, bd, xd, tol, max_it, iters, relres)
+                                   : gmres_dev(h, bd, xd, tol, restart, max_it, iters, relres);
+    if (!dev) CK(cudaMemcpyAsync(x, xd, n * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return rc;
+  });
+}
+
+int lorasp_gmres(lorasp_handle h, const double *b, double *x, double tol) {
+  return lorasp_krylov_ex(h, b, x, tol, LORASP_GMRES, 50, 500, nullptr, nullptr);
+}
+
+int lorasp_set_stream(lorasp_handle h, void *s) {
+  if (!h) return LORASP_E_ARG;
+  h->stream = reinterpret_cast<cudaStream_t>(s);
+  return LORASP_OK;
+}
+
+int lorasp_get_depth(lorasp_handle h, int *depth) {
+  if (!h || !depth) return LORASP_E_ARG;
+  *depth = h->plan.depth;
+  return LORASP_OK;
+}
+
+int lorasp_get_level_order(lorasp_handle h, int level, int *order, int *wave, int cap) {
+  if (!h || level < 1 || level > h->plan.depth) return LORASP_E_ARG;
+  const SymLevel &lv = h->plan.lev[level];
+  if (cap < lv.K) return LORASP_E_ARG;
+  for (int t = 0; t < lv.K; ++t) {
+    if (order) order[t] = lv.order[t];
+    if (wave) wave[lv.order[t]] = lv.node[lv.order[t]].wave;
+  }
+  return LORASP_OK;
+}
+
+int lorasp_get_ranks(lorasp_handle h, int level, int *ranks, int cap) {
+  if (!h || !ranks || level < 1 || level > h->plan.depth) return LORASP_E_ARG;
+  if (!h->factored) return LORASP_E_STATE;
+  const auto &r = h->rnk[level];
+  if (cap < (int)r.size()) return LORASP_E_ARG;
+  std::copy(r.begin(), r.end(), ranks);
+  return LORASP_OK;
+}
+
+int lorasp_get_sizes(lorasp_handle h, int level, int *sizes, int cap) {
+  if (!h || !sizes || level < 1 || level > h->plan.depth) return LORASP_E_ARG;
+  if (!h->factored) return LORASP_E_STATE;
+  const auto &m = h->msz[level];
+  if (cap < (int)m.size()) return LORASP_E_ARG;
+  std::copy(m.begin(), m.end(), sizes);
+  return LORASP_OK;
+}
+
+int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
+  if (!h) return LORASP_E_ARG;
+  std::ostringstream o;
+  const Plan &pl = h->plan;
+  o << "{\"n\":" << pl.n << ",\"nnz\":" << pl.nnz << ",\"depth\":" << pl.depth << ",\"eps\":" << pl.eps
+    << ",\"waves\":" << pl.total_waves << ",\"max_edge_distance\":" << pl.max_edge_distance
+    << ",\"factored\":" << (h->factored ? "true" : "false");
+  if (h->factored) {
+    o << ",\"flops_model\":" << h->flops_model << ",\"factor_bytes\":" << h->f_doubles * 8
+      << ",\"t_factor_host_ms\":" << h->t_factor_ms << ",\"launches_factor\":" << h->launches_factor
+      << ",\"aux_vars\":";
+    int64_t aux = 0;
+    for (int i = 1; i <= pl.depth; ++i)
+      for (int r : h->rnk[i]) aux += 2 * r;
+    o << aux << ",\"levels\":[";
+    for (int i = pl.depth; i >= 1; --i) {
+      int64_t rs = 0, ms = 0;
+      int rmax = 0, mmax = 0, nr = 0;
+      for (size_t c = 0; c < h->rnk[i].size(); ++c) {
+        rs += h->rnk[i][c];
+        rmax = std::max(rmax, h->rnk[i][c]);
+        ms += h->msz[i][c];
+        mmax = std::max(mmax, h->msz[i][c]);
+        nr += pl.lev[i].node[c].aux;
+      }
+      o << "{\"level\":" << i << ",\"supers\":" << h->rnk[i].size() << ",\"compressed\":" << nr
+        << ",\"rank_sum\":" << rs << ",\"rank_max\":" << rmax << ",\"size_sum\":" << ms
+        << ",\"size_max\":" << mmax << ",\"waves\":" << pl.lev[i].wave_begin.size() - 1
+        << ",\"lattice\":" << (pl.lev[i].lattice ? "true" : "false") << "}" << (i > 1 ? "," : "");
+    }
+    o << "]";
+  }
+  o << "}";
+  std::string s = o.str();
+  if (len) *len = s.size() + 1;
+  if (buf && cap > 0) {
+    size_t k = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), k);
+    buf[k] = 0;
+  }
+  return LORASP_OK;
+}
+
+int lorasp_get_launch_count(lorasp_handle h, int64_t *f, int64_t *a, int64_t *k) {
+  if (!h) return LORASP_E_ARG;
+  if (f) *f = h->launches_factor;
+  if (a) *a = h->launches_apply;
+  if (k) *k = h->launches_krylov;
+  return LORASP_OK;
+}
+
+int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, double *sigma, int *rank) {
+  if (!G || !V || !sigma || !rank || m <= 0) return LORASP_E_ARG;
+  try {
+    CK(cudaSetDevice(device));
+    CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+    double *dG, *dV, *dS, *dW;
+    int *dr, *dst;
+    size_t mm = (size_t)m * m;
+    CK(cudaMalloc(&dG, mm * 8));
+    CK(cudaMalloc(&dV, mm * 8));
+    CK(cudaMalloc(&dS, m * 8));
+    CK(cudaMalloc(&dW, mm * 8));
+    CK(cudaMalloc(&dr, 64));
+    dst = dr + 4;
+    CK(cudaMemset(dr, 0, 64));
+    CK(cudaMemset(dV, 0, mm * 8));
+    CK(cudaMemcpy(dG, G, mm * 8, cudaMemcpyHostToDevice));
+    EigTask e{};
+    e.G = dG;
+    e.V = dV;
+    e.sig = dS;
+    e.work = dW;
+    e.m = m;
+    e.node = 0;
+    e.rank_out = dr;
+    EigTask *de;
+    CK(cudaMalloc(&de, sizeof(EigTask)));
+    CK(cudaMemcpy(de, &e, sizeof(EigTask), cudaMemcpyHostToDevice));
+    int cap = (int)std::min<int64_t>((int64_t)m * m + 2 * m, SMEM_LIMIT / 8);
+    cap = std::max(cap, 2 * m);
+    k_jacobi<<<1, 512, cap * 8>>>(de, eps, cap, dst);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    int st[2];
+    CK(cudaMemcpy(rank, dr, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(st, dst, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sigma, dS, m * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(V, dV, (size_t)m * (*rank) * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dG); cudaFree(dV); cudaFree(dS); cudaFree(dW); cudaFree(dr); cudaFree(de);
+    return st[0];
+  } catch (const Err &e) {
+    return e.code;
+  }
+}
+
+int lorasp_test_pivot(int device, double *K, int m, int r) {
+  if (!K || m < 0 || r < 0 || m + r == 0) return LORASP_E_ARG;
+  try {
+    CK(cudaSetDevice(device));
+    CK(cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+    const int n = m + r;
+    double *dK;
+    int *dst;
+    CK(cudaMalloc(&dK, (size_t)n * n * 8));
+    CK(cudaMalloc(&dst, 64));
+    CK(cudaMemset(dst, 0, 64));
+    CK(cudaMemcpy(dK, K, (size_t)n * n * 8, cudaMemcpyHostToDevice));
+    PivTask t{dK, n, m, r, 0};
+    PivTask *dt;
+    CK(cudaMalloc(&dt, sizeof(PivTask)));
+    CK(cudaMemcpy(dt, &t, sizeof(PivTask), cudaMemcpyHostToDevice));
+    int cap = (int)std::min<int64_t>((int64_t)n * n + n, SMEM_LIMIT / 8);
+    cap = std::max(cap, n);
+    k_pivot<<<1, 512, cap * 8>>>(dt, cap, dst);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    int st[2];
+    CK(cudaMemcpy(st, dst, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(K, dK, (size_t)n * n * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dK); cudaFree(dst); cudaFree(dt);
+    return st[0];
+  } catch (const Err &e) {
+    return e.code;
+  }
+}
+
+const char *lorasp_last_error(lorasp_handle h) { return h ? h->last_error.c_str() : "null handle"; }
+
+void lorasp_destroy(lorasp_handle h) {
+  if (!h) return;
+  if (h->mem_ready) {
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    DevBuf *bufs[] = {&h->d_values, &h->d_rowptr, &h->d_colidx, &h->d_dest, &h->arena[0], &h->arena[1],
+                      &h->ws_G, &h->ws_V, &h->ws_sig, &h->ws_X, &h->ws_ctr, &h->d_ranks, &h->d_status,
+                      &h->d_vec, &h->d_y, &h->d_perm, &h->d_b, &h->d_x, &h->d_kry, &h->d_apnodes,
+                      &h->d_apsegs, &h->d_dotpart};
+    for (DevBuf *b : bufs) b->release();
+    h->fpool.release();
+    h->stg.release();
+    if (h->h_ranks) cudaFreeHost(h->h_ranks);
+    if (h->h_status) cudaFreeHost(h->h_status);
+    if (h->h_dot) cudaFreeHost(h->h_dot);
+  }
+  delete h;
+}
+
+}  // extern "C"
