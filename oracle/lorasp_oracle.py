@@ -38,6 +38,11 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 import scipy.linalg as sla
+from threadpoolctl import threadpool_limits
+
+# The oracle is sequential, like the paper's implementation (P:l.794): BLAS runs
+# on one thread (multi-threaded BLAS on these small blocks is ~20x slower).
+ORACLE_THREADS = 1
 
 # Node ids are tuples:  ('r', k, c)  red node of cluster c of P_k
 #                       ('s', i, c)  super-node s_c^[i]  (cluster c of P_{i-1})
@@ -337,7 +342,8 @@ class _Factorizer:
         A = [self.M.get((s, p), np.zeros((self.size[p], m))) for p in partners]
         B = [self.M.get((p, s), np.zeros((m, self.size[p]))).T for p in partners]
         stack = np.vstack(A if self.symmetric_stack else A + B)
-        _, sig, Vt = np.linalg.svd(stack, full_matrices=True)
+        # thin SVD when the stack has >= m rows (V is m x m either way)
+        _, sig, Vt = np.linalg.svd(stack, full_matrices=stack.shape[0] < m)
         sig0 = float(sig[0]) if sig.size else 0.0
         if sig0 == 0.0:
             r = 0                                   # reading Z4
@@ -424,6 +430,11 @@ class _Factorizer:
 def factorize(n, row_ptr, col_idx, values, coords, depth, eps, order="coloured",
               symmetric_stack=False, trace=False) -> Factorization:
     """Alg. 1 on the CSR matrix A (row_ptr, col_idx, values) with point coordinates."""
+    with threadpool_limits(ORACLE_THREADS):
+        return _factorize(n, row_ptr, col_idx, values, coords, depth, eps, order, symmetric_stack, trace)
+
+
+def _factorize(n, row_ptr, col_idx, values, coords, depth, eps, order, symmetric_stack, trace):
     return _Factorizer(n, np.asarray(row_ptr, np.int64), np.asarray(col_idx, np.int64),
                        np.asarray(values, np.float64), coords, depth, eps, order=order,
                        symmetric_stack=symmetric_stack, trace=trace).run()
@@ -440,6 +451,11 @@ def _ord(f: Factorization, q: Node) -> float:
 
 def solve(f: Factorization, b: np.ndarray) -> np.ndarray:
     """x ~= A^{-1} b by Alg. 2 (forward SolveL / backward SolveU in Order)."""
+    with threadpool_limits(ORACLE_THREADS):
+        return _solve(f, b)
+
+
+def _solve(f: Factorization, b: np.ndarray) -> np.ndarray:
     l = f.depth
     rhs: Dict[Node, np.ndarray] = {}
     var: Dict[Node, np.ndarray] = {}
