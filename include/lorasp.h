@@ -135,6 +135,11 @@ int lorasp_get_sizes(lorasp_handle h, int level, int *sizes, int cap);
  * through *len if len != NULL. */
 int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len);
 
+/* Per-kernel-class CUDA-event timing on the handle's stream: enable != 0
+ * resets and starts accumulating (ms, launches, algorithmic flops and bytes
+ * per class, reported under "kernels" by lorasp_get_stats); 0 stops. */
+int lorasp_set_timing(lorasp_handle h, int enable);
+
 /* Number of kernel launches issued by the last factor / apply / krylov call. */
 int lorasp_get_launch_count(lorasp_handle h, int64_t *factor_launches,
                             int64_t *apply_launches, int64_t *krylov_launches);

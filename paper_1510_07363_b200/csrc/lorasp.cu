@@ -158,6 +158,27 @@ struct Staging {
   }
 };
 
+// per-kernel-class CUDA-event timing (enabled with lorasp_set_timing)
+enum KClass {
+  K_SCATTER, K_MERGE, K_GRAM, K_JACOBI, K_PROJECT, K_ASSEMBLE, K_PIVOT, K_ZGEMM, K_SCHUR,
+  K_APPLY_FWD, K_APPLY_BWD, K_SPMV, K_DOT, K_VEC, K_NCLASS
+};
+static const char *KNAME[K_NCLASS] = {"leaf_scatter", "merge_copy", "gram_gemm", "jacobi_eig",
+                                      "project_gemm", "assemble_copy", "pivot_chol_inv", "trsm_gemm",
+                                      "schur_gemm", "apply_fwd", "apply_bwd", "spmv", "dot", "vec"};
+static const char *KKERNEL[K_NCLASS] = {"k_leaf_scatter", "k_copy", "k_gemm", "k_jacobi", "k_gemm", "k_copy",
+                                        "k_pivot", "k_gemm", "k_gemm", "k_apply_fwd", "k_apply_bwd",
+                                        "k_spmv", "k_dot_partial+k_dot_final", "k_axpby/k_sub/k_set_rhs/k_get_x"};
+struct KStat {
+  double ms = 0, flops = 0, bytes = 0;
+  int64_t launches = 0;
+};
+struct TimedEv {
+  int cls;
+  cudaEvent_t a, b;
+  double flops, bytes;
+};
+
 struct NodeRec {  // one eliminated (s, b) pair, for apply + stats
   int level, c, m, r, W;
   double *F;
@@ -189,6 +210,7 @@ struct lorasp_ctx {
   std::vector<NodeRec> recs;
   // apply plan
   std::vector<int> ap_wave_begin;  // in recs order (factor order), per wave
+  std::vector<double> ap_wave_flops, ap_wave_bytes;  // per wave, one pass (fwd or bwd)
   size_t ap_fwd_smem = 0, ap_bwd_smem = 0;
   int64_t vec_len = 0;
   bool dest_ready = false;
@@ -198,6 +220,11 @@ struct lorasp_ctx {
   int64_t launches_factor = 0, launches_apply = 0, launches_krylov = 0;
   int64_t f_doubles = 0;
   bool debug = getenv("LORASP_DEBUG") != nullptr;
+  // kernel timing
+  bool timing = false;
+  std::vector<cudaEvent_t> evpool;
+  std::vector<TimedEv> pend;
+  KStat kst[K_NCLASS];
 };
 
 namespace {
@@ -205,6 +232,39 @@ namespace {
 inline dim3 grid1(int64_t n, int bs = 256) {
   int64_t g = (n + bs - 1) / bs;
   return dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16)));
+}
+
+int tbeg(lorasp_ctx *h, int cls) {
+  if (!h->timing) return -1;
+  size_t need = 2 * (h->pend.size() + 1);
+  while (h->evpool.size() < need) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    h->evpool.push_back(e);
+  }
+  TimedEv t{cls, h->evpool[need - 2], h->evpool[need - 1], 0, 0};
+  CK(cudaEventRecord(t.a, h->stream));
+  h->pend.push_back(t);
+  return (int)h->pend.size() - 1;
+}
+void tend(lorasp_ctx *h, int idx, double flops, double bytes) {
+  if (idx < 0) return;
+  CK(cudaEventRecord(h->pend[idx].b, h->stream));
+  h->pend[idx].flops = flops;
+  h->pend[idx].bytes = bytes;
+}
+// after a stream sync: fold the recorded launches into the per-class totals
+void tflush(lorasp_ctx *h) {
+  for (const TimedEv &t : h->pend) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, t.a, t.b));
+    KStat &k = h->kst[t.cls];
+    k.ms += ms;
+    k.flops += t.flops;
+    k.bytes += t.bytes;
+    k.launches += 1;
+  }
+  h->pend.clear();
 }
 
 bool is_device_ptr(const void *p) {
@@ -243,24 +303,27 @@ T *push(lorasp_ctx *h, const std::vector<T> &v) {
   return reinterpret_cast<T *>(h->stg.push(v.data(), v.size() * sizeof(T), h->stream));
 }
 
-void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::vector<GemmSeg> &segs) {
+void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::vector<GemmSeg> &segs,
+                 int cls, double flops, double bytes) {
   if (tasks.empty()) return;
   h->stg.reserve(segs.size() * sizeof(GemmSeg) + tasks.size() * sizeof(GemmTask), h->stream);
   GemmSeg *ds = push(h, segs);
   GemmTask *dt = push(h, tasks);
-  const size_t maxg = 65535 * 32;
-  for (size_t o = 0; o < tasks.size(); o += maxg) {
-    unsigned nb = (unsigned)std::min(maxg, tasks.size() - o);
-    k_gemm<<<nb, 256, 0, h->stream>>>(dt + o, ds);
-    ++h->launches_factor;
-  }
+  int ev = tbeg(h, cls);
+  k_gemm<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt, ds);
+  tend(h, ev, flops, bytes);
+  ++h->launches_factor;
   CK(cudaGetLastError());
 }
 
-void launch_copy(lorasp_ctx *h, const std::vector<CopyTask> &tasks) {
+void launch_copy(lorasp_ctx *h, const std::vector<CopyTask> &tasks, int cls) {
   if (tasks.empty()) return;
   CopyTask *dt = push(h, tasks);
+  double bytes = 0;
+  for (const CopyTask &t : tasks) bytes += (t.mode == 0 ? 16.0 : 8.0) * t.rows * t.cols;
+  int ev = tbeg(h, cls);
   k_copy<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt);
+  tend(h, ev, 0, bytes);
   ++h->launches_factor;
   CK(cudaGetLastError());
 }
@@ -350,8 +413,10 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         h->leaf_soff = soff;
         h->dest_ready = true;
       }
+      int ev = tbeg(h, K_SCATTER);
       k_leaf_scatter<<<grid1(pl.nnz), 256, 0, st>>>(h->d_values.as<double>(), h->d_dest.as<int64_t>(),
                                                     pl.nnz, base);
+      tend(h, ev, 0, 24.0 * pl.nnz);
       ++h->launches_factor;
       CK(cudaGetLastError());
     } else {
@@ -375,7 +440,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         t.alpha = 1.0;
         ct.push_back(t);
       }
-      launch_copy(h, ct);
+      launch_copy(h, ct, K_MERGE);
     }
 
     // ---- colour waves ---------------------------------------------------------
@@ -409,6 +474,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         std::vector<EigTask> et;
         int64_t soff_sig = 0, xoff = 0;
         int max_m = 0;
+        double f_gram = 0, b_gram = 0, f_eig = 0, b_eig = 0;
         for (size_t q = 0; q < comp.size(); ++q) {
           const int c = comp[q];
           const SymNode &nd = lv.node[c];
@@ -439,6 +505,10 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           }
           b.nseg = (int)gs.size() - b.seg0;
           add_tiles(gt, b);
+          f_gram += (double)R * mc * mc;
+          b_gram += 8.0 * R * mc + 8.0 * mc * mc;
+          f_eig += 9.0 * mc * (double)mc * mc;
+          b_eig += 16.0 * mc * mc;
           EigTask e{};
           e.G = b.C;
           e.V = h->ws_V.as<double>() + goff[c];
@@ -453,12 +523,14 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           e.rank_out = h->d_ranks.as<int>() + q;
           et.push_back(e);
         }
-        launch_gemm(h, gt, gs);
+        launch_gemm(h, gt, gs, K_GRAM, f_gram, b_gram);
         EigTask *de = push(h, et);
         int64_t want = (int64_t)max_m * max_m + 2 * max_m;
         int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
         cap = std::max(cap, 2 * max_m);
+        int ev = tbeg(h, K_JACOBI);
         k_jacobi<<<(unsigned)et.size(), 512, cap * 8, st>>>(de, pl.eps, cap, h->d_status.as<int>());
+        tend(h, ev, f_eig, b_eig);
         ++h->launches_factor;
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h->h_ranks, h->d_ranks.p, comp.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -494,6 +566,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
       }
       h->ws_ctr.ensure(std::max<int64_t>(ctr_tot, 32) * 8, st);
       int max_n = 0;
+      double f_proj = 0, b_proj = 0, f_piv = 0, b_piv = 0, f_z = 0, b_z = 0, f_s = 0, b_s = 0;
       for (size_t e = 0; e < elim.size(); ++e) {
         const int c = elim[e];
         const SymNode &nd = lv.node[c];
@@ -697,21 +770,31 @@ void factor_impl(lorasp_ctx *h, const double *values) {
             }
         }
         h->flops_model += node_flops(mc, rc, nd.aux ? R : 0, W);
+        f_proj += 2.0 * R * mc * rc;
+        b_proj += 8.0 * ((double)R * mc + (double)R * rc + (double)mc * rc);
+        f_piv += ((double)mc * mc * mc + (double)rc * rc * rc) / 3.0;
+        b_piv += 16.0 * n * n;
+        f_z += ((double)mc * mc + (double)rc * rc) * W;
+        b_z += 8.0 * ((double)n * n + 2.0 * n * W);
+        f_s += (double)(mc + rc) * W * W;
+        b_s += 8.0 * (2.0 * n * W + (double)W * W);
         h->recs.push_back(std::move(rec));
       }
-      launch_gemm(h, pt, ps);
-      launch_copy(h, ct);
+      launch_gemm(h, pt, ps, K_PROJECT, f_proj, b_proj);
+      launch_copy(h, ct, K_ASSEMBLE);
       {
         PivTask *dp = push(h, pv);
         int64_t want = (int64_t)max_n * max_n + max_n;
         int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
         cap = std::max(cap, max_n);
+        int ev = tbeg(h, K_PIVOT);
         k_pivot<<<(unsigned)pv.size(), 512, cap * 8, st>>>(dp, cap, h->d_status.as<int>());
+        tend(h, ev, f_piv, b_piv);
         ++h->launches_factor;
         CK(cudaGetLastError());
       }
-      launch_gemm(h, zt, zs);
-      launch_gemm(h, stt, ss);
+      launch_gemm(h, zt, zs, K_ZGEMM, f_z, b_z);
+      launch_gemm(h, stt, ss, K_SCHUR, f_s, b_s);
       if (h->debug) {
         CK(cudaStreamSynchronize(st));
         CK(cudaMemcpy(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost));
@@ -727,6 +810,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
   CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   h->stg.reset();
+  tflush(h);
   if (h->h_status[0] != 0)
     throw Err(h->h_status[0], std::string(h->h_status[0] == LORASP_E_EIG_NOCONV
                                               ? "Jacobi eigen-solver did not converge"
@@ -790,6 +874,17 @@ void factor_impl(lorasp_ctx *h, const double *values) {
     bwd = std::max(bwd, (size_t)(n + rc.W));
   }
   h->ap_wave_begin.push_back((int)h->recs.size());
+  h->ap_wave_flops.assign(h->ap_wave_begin.size() - 1, 0.0);
+  h->ap_wave_bytes.assign(h->ap_wave_begin.size() - 1, 0.0);
+  for (size_t w = 0; w + 1 < h->ap_wave_begin.size(); ++w)
+    for (int q = h->ap_wave_begin[w]; q < h->ap_wave_begin[w + 1]; ++q) {
+      const NodeRec &rc = h->recs[q];
+      double n = rc.m + rc.r;
+      // one pass reads L^{-1} (lower half) and Z once: 2 flops / element read
+      double elems = n * (n + 1) / 2 + n * rc.W;
+      h->ap_wave_flops[w] += 2.0 * elems;
+      h->ap_wave_bytes[w] += 8.0 * elems + 8.0 * 2 * (n + rc.W);
+    }
   h->ap_fwd_smem = fwd * 8;
   h->ap_bwd_smem = bwd * 8;
   if (h->ap_fwd_smem > (size_t)SMEM_LIMIT || h->ap_bwd_smem > (size_t)SMEM_LIMIT)
@@ -813,28 +908,38 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
   cudaStream_t st = h->stream;
   const Plan &pl = h->plan;
   CK(cudaMemsetAsync(h->d_vec.p, 0, h->vec_len * 8, st));
+  int ev = tbeg(h, K_VEC);
   k_set_rhs<<<grid1(pl.n), 256, 0, st>>>(b, h->d_perm.as<int64_t>(), pl.n, h->d_vec.as<double>());
+  tend(h, ev, 0, 24.0 * pl.n);
   const ApNode *nodes = h->d_apnodes.as<ApNode>();
   const ApSeg *segs = h->d_apsegs.as<ApSeg>();
   const int nw = (int)h->ap_wave_begin.size() - 1;
   for (int w = 0; w < nw; ++w) {
     int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
+    ev = tbeg(h, K_APPLY_FWD);
     k_apply_fwd<<<b1 - b0, 256, h->ap_fwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>());
+    tend(h, ev, h->ap_wave_flops[w], h->ap_wave_bytes[w]);
   }
   for (int w = nw - 1; w >= 0; --w) {
     int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
+    ev = tbeg(h, K_APPLY_BWD);
     k_apply_bwd<<<b1 - b0, 256, h->ap_bwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>());
+    tend(h, ev, h->ap_wave_flops[w], h->ap_wave_bytes[w]);
   }
+  ev = tbeg(h, K_VEC);
   k_get_x<<<grid1(pl.n), 256, 0, st>>>(h->d_vec.as<double>(), h->d_perm.as<int64_t>(), pl.n, x);
+  tend(h, ev, 0, 24.0 * pl.n);
   *counter += 2 * nw + 2;
   CK(cudaGetLastError());
 }
 
 double dot_dev(lorasp_ctx *h, const double *a, const double *b) {
   cudaStream_t st = h->stream;
+  int ev = tbeg(h, K_DOT);
   k_dot_partial<<<DOT_BLOCKS, 256, 0, st>>>(h->plan.n, a, b, h->d_dotpart.as<double>());
   k_dot_final<<<1, 256, 0, st>>>(h->d_dotpart.as<double>(), DOT_BLOCKS,
                                  h->d_dotpart.as<double>() + DOT_BLOCKS);
+  tend(h, ev, 2.0 * h->plan.n, 16.0 * h->plan.n);
   CK(cudaMemcpyAsync(h->h_dot, h->d_dotpart.as<double>() + DOT_BLOCKS, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   h->launches_krylov += 2;
@@ -843,13 +948,17 @@ double dot_dev(lorasp_ctx *h, const double *a, const double *b) {
 
 void spmv_dev(lorasp_ctx *h, const double *x, double *y) {
   const Plan &pl = h->plan;
+  int ev = tbeg(h, K_SPMV);
   k_spmv<<<grid1(pl.n), 256, 0, h->stream>>>(pl.n, h->d_rowptr.as<int64_t>(), h->d_colidx.as<int64_t>(),
                                             h->d_values.as<double>(), x, y);
+  tend(h, ev, 2.0 * pl.nnz, 20.0 * pl.nnz + 16.0 * pl.n);
   ++h->launches_krylov;
 }
 
 void axpby(lorasp_ctx *h, double a, const double *x, double b, double *y) {
+  int ev = tbeg(h, K_VEC);
   k_axpby<<<grid1(h->plan.n), 256, 0, h->stream>>>(h->plan.n, a, x, b, y);
+  tend(h, ev, 3.0 * h->plan.n, 24.0 * h->plan.n);
   ++h->launches_krylov;
 }
 
@@ -1050,6 +1159,7 @@ int lorasp_apply(lorasp_handle h, const double *b, double *x) {
       CK(cudaMemcpyAsync(x, h->d_x.p, n * 8, cudaMemcpyDeviceToHost, h->stream));
       CK(cudaStreamSynchronize(h->stream));
     }
+    tflush(h);
     return (int)LORASP_OK;
   });
 }
@@ -1075,6 +1185,7 @@ int lorasp_krylov_ex(lorasp_handle h, const double *b, double *x, double tol, in
                                    : gmres_dev(h, bd, xd, tol, restart, max_it, iters, relres);
     if (!dev) CK(cudaMemcpyAsync(x, xd, n * 8, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+    tflush(h);
     return rc;
   });
 }
@@ -1087,6 +1198,16 @@ int lorasp_set_stream(lorasp_handle h, void *s) {
   if (!h) return LORASP_E_ARG;
   h->stream = reinterpret_cast<cudaStream_t>(s);
   return LORASP_OK;
+}
+
+int lorasp_set_timing(lorasp_handle h, int enable) {
+  return guarded(h, [&]() {
+    CK(cudaSetDevice(h->device));
+    h->timing = enable != 0;
+    for (auto &k : h->kst) k = KStat();
+    h->pend.clear();
+    return (int)LORASP_OK;
+  });
 }
 
 int lorasp_get_depth(lorasp_handle h, int *depth) {
@@ -1156,7 +1277,16 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
     }
     o << "]";
   }
-  o << "}";
+  o << ",\"kernels\":{";
+  bool first = true;
+  for (int c = 0; c < K_NCLASS; ++c) {
+    const KStat &k = h->kst[c];
+    if (k.launches == 0) continue;
+    o << (first ? "" : ",") << "\"" << KNAME[c] << "\":{\"kernel\":\"" << KKERNEL[c] << "\",\"ms\":" << k.ms
+      << ",\"launches\":" << k.launches << ",\"alg_flops\":" << k.flops << ",\"alg_bytes\":" << k.bytes << "}";
+    first = false;
+  }
+  o << "}}";
   std::string s = o.str();
   if (len) *len = s.size() + 1;
   if (buf && cap > 0) {
@@ -1263,6 +1393,7 @@ void lorasp_destroy(lorasp_handle h) {
                       &h->d_vec, &h->d_y, &h->d_perm, &h->d_b, &h->d_x, &h->d_kry, &h->d_apnodes,
                       &h->d_apsegs, &h->d_dotpart};
     for (DevBuf *b : bufs) b->release();
+    for (cudaEvent_t e : h->evpool) cudaEventDestroy(e);
     h->fpool.release();
     h->stg.release();
     if (h->h_ranks) cudaFreeHost(h->h_ranks);

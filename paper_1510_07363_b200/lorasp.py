@@ -32,7 +32,7 @@ STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "E_ARG", -2: "E_PATTERN", -3: "E_SING
 
 # every symbol include/lorasp.h declares
 SYMBOLS = ["lorasp_analyze", "lorasp_factor", "lorasp_apply", "lorasp_gmres", "lorasp_krylov_ex",
-           "lorasp_set_stream", "lorasp_get_depth", "lorasp_get_level_order", "lorasp_get_ranks",
+           "lorasp_set_stream", "lorasp_set_timing", "lorasp_get_depth", "lorasp_get_level_order", "lorasp_get_ranks",
            "lorasp_get_sizes", "lorasp_get_stats", "lorasp_get_launch_count", "lorasp_test_eig",
            "lorasp_test_pivot", "lorasp_last_error", "lorasp_destroy"]
 
@@ -64,6 +64,7 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lorasp_krylov_ex.argtypes = [P, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
     lib.lorasp_set_stream.argtypes = [P, P]
+    lib.lorasp_set_timing.argtypes = [P, ctypes.c_int]
     lib.lorasp_get_depth.argtypes = [P, ctypes.POINTER(ctypes.c_int)]
     lib.lorasp_get_level_order.argtypes = [P, ctypes.c_int, P, P, ctypes.c_int]
     lib.lorasp_get_ranks.argtypes = [P, ctypes.c_int, P, ctypes.c_int]
@@ -144,6 +145,9 @@ class Handle:
 
     def set_stream(self, stream_ptr: int):
         return self._check(self._lib.lorasp_set_stream(self.h, ctypes.c_void_p(stream_ptr)), "set_stream")
+
+    def set_timing(self, enable: bool):
+        return self._check(self._lib.lorasp_set_timing(self.h, int(bool(enable))), "set_timing")
 
     def level_order(self, level):
         K = 2 ** (level - 1)
