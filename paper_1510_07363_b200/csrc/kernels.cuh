@@ -33,19 +33,17 @@ struct CopyTask {
 __global__ void __launch_bounds__(256) k_copy(const CopyTask *__restrict__ tasks) {
   const CopyTask t = tasks[blockIdx.x];
   if (t.rows <= 0 || t.cols <= 0) return;
-  const int64_t tot = (int64_t)t.rows * t.cols;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (t.mode != 0) {
-    for (int64_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-      int i = (int)(idx % t.rows), j = (int)(idx / t.rows);
-      t.dst[i + (int64_t)j * t.ldd] = (t.mode == 1 || i == j) ? t.alpha : 0.0;
-    }
+    for (int j = warp; j < t.cols; j += nw)
+      for (int i = lane; i < t.rows; i += 32)
+        t.dst[i + (int64_t)j * t.ldd] = (t.mode == 1 || i == j) ? t.alpha : 0.0;
     return;
   }
   if (!t.trans) {
-    for (int64_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-      int i = (int)(idx % t.rows), j = (int)(idx / t.rows);
-      t.dst[i + (int64_t)j * t.ldd] = t.alpha * t.src[i + (int64_t)j * t.lds];
-    }
+    for (int j = warp; j < t.cols; j += nw)
+      for (int i = lane; i < t.rows; i += 32)
+        t.dst[i + (int64_t)j * t.ldd] = t.alpha * t.src[i + (int64_t)j * t.lds];
   } else {
     // transpose through shared memory 32x32 tiles (coalesced on both sides)
     __shared__ double tile[32][33];
@@ -180,7 +178,20 @@ struct EigTask {
   int m;
   int node;          // cluster id (for status)
   int *rank_out;
+  long long *dbg;    // optional phase timestamps (test hook), may be null
 };
+
+// FP64 division is a long software sequence on sm_100a (~430 cycles of latency
+// measured, tools/micro/fp64lat.cu); the reciprocal from MUFU.RCP64H plus two
+// Newton steps costs ~50 cycles and matched IEEE 1/x on every tested input.
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -308,6 +319,487 @@ __global__ void __launch_bounds__(512) k_jacobi(const EigTask *__restrict__ task
   if (tid == 0) *t.rank_out = r;
 }
 
+// ------------------------------------------------- tridiagonal eigen-solver ----
+// Symmetric eigen-decomposition of the Gram matrix G = M^T M for Compress
+// (sigma_k = sqrt(lambda_k), P:l.333-359) in O(m^3) with few sequential steps:
+//   1. Householder tridiagonalisation Q^T G Q = T (lower, LAPACK sytd2 form);
+//   2. eigenvalues of T by Sturm-count multisection (one warp per eigenvalue,
+//      32 points per round): lambda_0 first, then only the candidates with
+//      lambda >= (eps sigma_0)^2 / 4 (a superset of the kept ones);
+//   3. rank r = #{sqrt(lambda_k) >= eps sqrt(lambda_0)} (Eq. cutOff1);
+//   4. eigenvectors of T for the r kept eigenvalues by inverse iteration
+//      (pivoted tridiagonal LU, 3 sweeps, re-orthogonalised inside clusters);
+//   5. back-transformation V = Q Z.
+// eps = 0 keeps every direction (reading Z3): V = I_m, r = m.
+struct EigScratch {
+  double *work;  // >= 7 m^2 doubles of global scratch per task
+};
+
+__device__ __forceinline__ int sturm_count(const double *__restrict__ d, const double *__restrict__ e2,
+                                           int m, double x, double pivmin) {
+  // Number of eigenvalues of T below x: sign changes of the leading principal
+  // minors p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}, i.e. negative pivots
+  // q_i = p_i / p_{i-1} of the LDL^T count, evaluated without divisions
+  // (an exact zero pivot counts as negative, as q = -pivmin does in LAPACK).
+  // T is pre-scaled to |d|, |e| <= 1, so |p| grows at most 3x per step; the
+  // pair (p0, p1) is renormalised by a power of two every 8 steps.  d / e2 are
+  // padded to a multiple of 8 with d = 4, e2 = 0 (no sign change for x < 4).
+  (void)pivmin;
+  double p0 = 1.0, p1 = 1.0;
+  int c = 0;
+  const double *e2m = e2 - 1;
+  for (int i0 = 0; i0 < m; i0 += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u;
+      const double ee = (i == 0) ? 0.0 : e2m[i];
+      double p2 = fma(d[i] - x, p1, -ee * p0);
+      p2 = (p2 == 0.0) ? -1e-30 * p1 : p2;
+      c += (p2 < 0.0) != (p1 < 0.0);
+      p0 = p1;
+      p1 = p2;
+    }
+    const double a = fmax(fabs(p0), fabs(p1));
+    const long long ex = ((__double_as_longlong(a) >> 52) & 0x7ff) - 1023;
+    const double sc = __longlong_as_double((long long)(1023 - ex) << 52);
+    p0 *= sc;
+    p1 *= sc;
+  }
+  return c;
+}
+
+// warp-cooperative multisection for the ascending-index-j eigenvalue of T
+__device__ __forceinline__ double warp_eig_asc(const double *d, const double *e2, int m, int j, double lo, double hi,
+                               double pivmin) {
+  const int lane = threadIdx.x & 31;
+  for (int round = 0; round < 64; ++round) {
+    double tol = 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 2.0 * pivmin;
+    if (hi - lo <= tol) break;
+    double x = fma(hi - lo, (double)(lane + 1) * (1.0 / 33.0), lo);
+    int c = sturm_count(d, e2, m, x, pivmin);
+    unsigned bal = __ballot_sync(0xffffffffu, c > j);
+    double xlast = __shfl_sync(0xffffffffu, x, 31);
+    if (bal == 0) {
+      lo = xlast;
+    } else {
+      int f = __ffs(bal) - 1;
+      double xf = __shfl_sync(0xffffffffu, x, f);
+      double xp = __shfl_sync(0xffffffffu, x, f > 0 ? f - 1 : 0);
+      if (f > 0) lo = xp;
+      hi = xf;
+    }
+  }
+  return 0.5 * (lo + hi);
+}
+
+__global__ void __launch_bounds__(512, 1) k_eig(const EigTask *__restrict__ tasks, double eps,
+                                             int smem_cap_doubles, int *status) {
+  extern __shared__ double sh[];
+  __shared__ double s_red[32];
+  __shared__ double s_bc[8];
+  __shared__ int s_int[4];
+  const EigTask t = tasks[blockIdx.x];
+  const int m = t.m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int ml = m > 512 ? m : 512;  // lam doubles as p-partials scratch during phase 1
+  const int mp = (m + 8) & ~7;       // padded length (>= m + 1, multiple of 8)
+  double *d = sh, *e = d + mp, *tau = e + mp, *e2 = tau + mp, *vt = e2 + mp, *pw = vt + mp, *lam = pw + mp;
+  double *A = ((int64_t)m * m + 6 * mp + ml <= smem_cap_doubles) ? lam + ml : t.work + 6 * (int64_t)m * m;
+  double *scr = t.work;  // 6 m^2: inverse-iteration scratch
+  for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) A[q] = t.G[q];
+  __syncthreads();
+  if (t.dbg && tid == 0) t.dbg[0] = clock64();
+  // block reduction helper (sum)
+  auto bsum = [&](double v) -> double {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) s_red[warp] = v;
+    __syncthreads();
+    double r = 0;
+    for (int w = 0; w < nw; ++w) r += s_red[w];
+    return r;
+  };
+  double fro = 0;
+  for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) fro += A[q] * A[q];
+  fro = bsum(fro);
+  if (!(fro > 0.0)) {
+    if (tid == 0) *t.rank_out = 0;
+    for (int q = tid; q < m; q += blockDim.x) t.sig[q] = 0.0;
+    return;
+  }
+  if (eps == 0.0) {
+    for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) t.V[q] = ((q % m) == (q / m)) ? 1.0 : 0.0;
+    for (int q = tid; q < m; q += blockDim.x) t.sig[q] = 0.0;
+    if (tid == 0) *t.rank_out = m;
+    return;
+  }
+  // ---- 1. Householder tridiagonalisation ----
+  // per step k: v from column k (its squared norm below x0 was accumulated by
+  // warp 0 during the previous update), p = tau A22 v with 4 partial sums per
+  // row, one block reduction for p.v, then the rank-2 update A22 -= v w^T + w v^T.
+  double *part = t.work + 6 * (int64_t)m * m;  // placeholder (unused when A is in smem)
+  (void)part;
+  __shared__ double s_s2;
+  if (tid < 32) {
+    double a = 0;
+    for (int i = 2 + lane; i < m; i += 32) a = fma(A[i], A[i], a);   // column 0, rows 2..
+    a = warp_sum(a);
+    if (lane == 0) s_s2 = a;
+  }
+  __syncthreads();
+  long long tph[6] = {0, 0, 0, 0, 0, 0};
+  long long tprev = clock64();
+  for (int k = 0; k < m - 2; ++k) {
+    const int L = m - k - 1;
+    double *colk = A + (int64_t)k * m + (k + 1);   // x = A[k+1.., k], length L
+    const double s2 = s_s2;
+    const double x0 = colk[0];
+    if (s2 == 0.0) {
+      if (tid == 0) {
+        tau[k] = 0.0;
+        e[k] = x0;
+      }
+      // next column's norm (A22 unchanged)
+      __syncthreads();
+      if (tid < 32) {
+        const double *cn = A + (int64_t)(k + 1) * m;
+        double a = 0;
+        for (int i = k + 3 + lane; i < m; i += 32) a = fma(cn[i], cn[i], a);
+        a = warp_sum(a);
+        if (lane == 0) s_s2 = a;
+      }
+      __syncthreads();
+      continue;
+    }
+    const double beta = -copysign(sqrt(x0 * x0 + s2), x0);
+    const double tk = (beta - x0) * frcp(beta);
+    const double scal = frcp(x0 - beta);
+    for (int i = tid; i < L; i += blockDim.x) {
+      double v = (i == 0) ? 1.0 : colk[i] * scal;
+      vt[i] = v;
+      colk[i] = v;
+    }
+    if (tid == 0) {
+      tau[k] = tk;
+      e[k] = beta;
+    }
+    __syncthreads();
+    if (t.dbg && tid == 0) { long long tn = clock64(); tph[0] += tn - tprev; tprev = tn; }
+    // p_i = tk * sum_j A22(i, j) v_j : thread (g, i) sums j = g, g+4, ... (4 groups)
+    double *A22 = A + (int64_t)(k + 1) * m + (k + 1);
+    double pvp = 0;
+    for (int i0 = 0; i0 < L; i0 += 128) {
+      const int i = i0 + (tid & 127), g = tid >> 7;
+      double acc0 = 0, acc1 = 0;
+      if (i < L) {
+        for (int jb = g; jb < L; jb += 32) {
+#pragma unroll
+          for (int u = 0; u < 8; u += 2) {
+            const int j0 = jb + 4 * u, j1 = j0 + 4;
+            const double a0 = (j0 < L) ? A22[i + (int64_t)j0 * m] : 0.0;
+            const double b0 = (j0 < L) ? vt[j0] : 0.0;
+            const double a1 = (j1 < L) ? A22[i + (int64_t)j1 * m] : 0.0;
+            const double b1 = (j1 < L) ? vt[j1] : 0.0;
+            acc0 = fma(a0, b0, acc0);
+            acc1 = fma(a1, b1, acc1);
+          }
+        }
+      }
+      lam[tid] = acc0 + acc1;   // lam[] is free scratch until phase 2 (>= blockDim doubles)
+      __syncthreads();
+      if (t.dbg && tid == 0) { long long tn = clock64(); tph[1] += tn - tprev; tprev = tn; }
+      if (g == 0 && i < L) {
+        double pi = (lam[tid] + lam[tid + 128]) + (lam[tid + 256] + lam[tid + 384]);
+        pi *= tk;
+        pw[i] = pi;
+        pvp = fma(pi, vt[i], pvp);
+      }
+      __syncthreads();
+    }
+    // pv = sum p_i v_i (block reduction)
+    if (t.dbg && tid == 0) { long long tn = clock64(); tph[2] += tn - tprev; tprev = tn; }
+    pvp = warp_sum(pvp);
+    if (lane == 0) s_red[warp] = pvp;
+    __syncthreads();
+    if (t.dbg && tid == 0) { long long tn = clock64(); tph[3] += tn - tprev; tprev = tn; }
+    double pv = 0;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) pv += s_red[w];
+    const double alpha = -0.5 * tk * pv;   // w = p + alpha v
+    // rank-2 update A22 -= v w^T + w v^T (w formed on the fly);
+    // warp 0 (column j = 0 of A22 = column k+1) also forms the squared norm of
+    // the next Householder column (rows k+3..)
+    for (int j = warp; j < L; j += nw) {
+      const double vj = vt[j], pj = pw[j];
+      const double wj = fma(alpha, vj, pj);
+      double *cj = A22 + (int64_t)j * m;
+      double a = 0;
+      for (int i = lane; i < L; i += 32) {
+        const double vi = vt[i], pi = pw[i];
+        const double wi = fma(alpha, vi, pi);           // w = p + alpha v
+        const double nv = cj[i] - fma(vi, wj, wi * vj);
+        cj[i] = nv;
+        if (j == 0 && i >= 2) a = fma(nv, nv, a);
+      }
+      if (j == 0) {
+        a = warp_sum(a);
+        if (lane == 0) s_s2 = a;
+      }
+    }
+    __syncthreads();
+    if (t.dbg && tid == 0) { long long tn = clock64(); tph[4] += tn - tprev; tprev = tn; }
+  }
+  if (t.dbg && tid == 0) for (int q = 0; q < 5; ++q) t.dbg[5 + q] = tph[q];
+  for (int i = tid; i < m; i += blockDim.x) d[i] = A[i + (int64_t)i * m];
+  if (tid == 0) {
+    if (m >= 2) e[m - 2] = A[(m - 1) + (int64_t)(m - 2) * m];
+    e[m - 1] = 0.0;
+    if (m >= 2) tau[m - 2] = 0.0;
+    tau[m - 1] = 0.0;
+  }
+  __syncthreads();
+  if (t.dbg && tid == 0) t.dbg[1] = clock64();
+  // ---- 2. eigenvalues (Sturm multisection) ----
+  double gl = 1e300, gu = -1e300, emax2 = 0;
+  for (int i = tid; i < m; i += blockDim.x) {
+    double off = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < m - 1 ? fabs(e[i]) : 0.0);
+    gl = fmin(gl, d[i] - off);
+    gu = fmax(gu, d[i] + off);
+    if (i < m - 1) {
+      e2[i] = e[i] * e[i];
+      emax2 = fmax(emax2, e2[i]);
+    }
+  }
+  // block min / max
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+  }
+  __syncthreads();
+  if (lane == 0) {
+    s_red[warp] = gl;
+    s_red[16 + warp] = gu;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 1e300, b = -1e300;
+    for (int w = 0; w < nw; ++w) {
+      a = fmin(a, s_red[w]);
+      b = fmax(b, s_red[16 + w]);
+    }
+    s_bc[0] = a;
+    s_bc[1] = b;
+  }
+  __syncthreads();
+  if (lane == 0) s_red[warp] = emax2;
+  __syncthreads();
+  double em = 0;
+  for (int w = 0; w < nw; ++w) em = fmax(em, s_red[w]);
+  gl = s_bc[0];
+  gu = s_bc[1];
+  const double bnorm = fmax(fabs(gl), fabs(gu));
+  // work on T / bnorm (|d|, |e| <= 1): the division-free Sturm recurrence then
+  // cannot overflow within a few hundred steps; eigenvalues are scaled back.
+  const double isc = 1.0 / bnorm;
+  __syncthreads();
+  for (int i = tid; i < mp; i += blockDim.x) {
+    if (i < m) {
+      d[i] *= isc;
+      if (i < m - 1) e2[i] *= isc * isc;
+      else e2[i] = 0.0;
+    } else {
+      d[i] = 4.0;   // padding: no sign change for x < 4
+      e2[i] = 0.0;
+    }
+  }
+  gl *= isc;
+  gu *= isc;
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, em * isc * isc) * 1e10;
+  gl -= 2.2e-16 * 2 * m + 2 * pivmin;
+  gu += 2.2e-16 * 2 * m + 2 * pivmin;
+  __syncthreads();
+  if (warp == 0) {
+    double l0 = warp_eig_asc(d, e2, m, m - 1, gl, gu, pivmin);
+    if (lane == 0) {
+      lam[0] = l0 * bnorm;
+      double thr = eps * sqrt(fmax(l0, 0.0));
+      thr = thr * thr;
+      int below = sturm_count(d, e2, m, 0.25 * thr, pivmin);
+      s_int[0] = min(m, m - below + 1);  // candidates to compute (superset of kept + 1)
+    }
+  }
+  __syncthreads();
+  const int ncomp = s_int[0];
+  for (int k = 1 + warp; k < ncomp; k += nw) {
+    double lk = warp_eig_asc(d, e2, m, m - 1 - k, gl, gu, pivmin);
+    if (lane == 0) lam[k] = lk * bnorm;
+  }
+  __syncthreads();
+  // restore T (inverse iteration works on the unscaled tridiagonal)
+  for (int i = tid; i < m; i += blockDim.x) d[i] *= bnorm;
+  __syncthreads();
+  const double sig0 = sqrt(fmax(lam[0], 0.0));
+  int r = 0;
+  for (int k = 0; k < ncomp; ++k) r += (sqrt(fmax(lam[k], 0.0)) >= eps * sig0);
+  for (int k = tid; k < m; k += blockDim.x) t.sig[k] = (k < ncomp) ? sqrt(fmax(lam[k], 0.0)) : 0.0;
+  if (tid == 0) *t.rank_out = r;
+  if (t.dbg && tid == 0) t.dbg[2] = clock64();
+  // ---- 4. inverse iteration, one thread per kept eigenvalue ----
+  // Each vector is computed independently (shift lambda_k, equal shifts
+  // separated by pertol), then the r vectors are orthonormalised (MGS): mixing
+  // kept vectors leaves the kept subspace unchanged.
+  const double pertol = 10.0 * 2.2e-16 * bnorm;
+  for (int k = tid; k < r; k += blockDim.x) {
+    double *DL = scr + (int64_t)k * 6 * m, *D = DL + m, *DU = D + m, *DU2 = DU + m, *b = DU2 + m,
+           *piv = b + m;
+    double sft = lam[k];
+    for (int q = 1; q <= k && lam[k - q] - lam[k] < pertol; ++q) sft -= pertol;
+    // dgttrf on T - sft I with the running pivot row carried in registers
+    double Di = d[0] - sft, DUi = (m > 1) ? e[0] : 0.0;
+#pragma unroll 2
+    for (int i = 0; i < m - 1; ++i) {
+      const double DLi = e[i];
+      double Dn = d[i + 1] - sft;
+      double DUn = (i < m - 2) ? e[i + 1] : 0.0;
+      if (fabs(Di) >= fabs(DLi)) {
+        if (Di == 0.0) Di = pertol;
+        const double f = DLi * frcp(Di);
+        D[i] = Di;
+        DL[i] = f;
+        DU[i] = DUi;
+        DU2[i] = 0.0;
+        piv[i] = 0.0;
+        Dn = fma(-f, DUi, Dn);
+      } else {
+        const double f = Di * frcp(DLi);
+        D[i] = DLi;
+        DL[i] = f;
+        DU[i] = Dn;
+        DU2[i] = DUn;
+        piv[i] = 1.0;
+        const double nd = fma(-f, Dn, DUi);
+        DUn = -f * DUn;
+        Dn = nd;
+      }
+      Di = Dn;
+      DUi = DUn;
+    }
+    D[m - 1] = Di;
+    for (int i = 0; i < m; ++i) {        // keep pivots away from 0, store reciprocals
+      double v = D[i];
+      if (fabs(v) < pertol) v = copysign(pertol, v == 0.0 ? 1.0 : v);
+      D[i] = frcp(v);
+    }
+    for (int i = 0; i < m; ++i) b[i] = 1.0 + 0.5 * sin(0.7 * i + 1.3 * k + 0.1);
+    for (int it = 0; it < 3; ++it) {
+      // forward (row interchanges + unit lower)
+      double bi = b[0];
+#pragma unroll 4
+      for (int i = 0; i < m - 1; ++i) {
+        const double bn = b[i + 1];
+        if (piv[i] == 0.0) {
+          b[i] = bi;
+          bi = fma(-DL[i], bi, bn);
+        } else {
+          b[i] = bn;
+          bi = fma(-DL[i], bn, bi);
+        }
+      }
+      b[m - 1] = bi;
+      // backward (upper with two super-diagonals), carries x_{i+1}, x_{i+2}
+      double x1 = b[m - 1] * D[m - 1];
+      b[m - 1] = x1;
+      double nrm = x1 * x1, x2 = 0.0;
+      if (m >= 2) {
+        const double x0 = (b[m - 2] - DU[m - 2] * x1) * D[m - 2];
+        b[m - 2] = x0;
+        nrm = fma(x0, x0, nrm);
+        x2 = x1;
+        x1 = x0;
+      }
+#pragma unroll 4
+      for (int i = m - 3; i >= 0; --i) {
+        const double x0 = (b[i] - DU[i] * x1 - DU2[i] * x2) * D[i];
+        b[i] = x0;
+        nrm = fma(x0, x0, nrm);
+        x2 = x1;
+        x1 = x0;
+      }
+      nrm = frcp(sqrt(nrm));
+      for (int i = 0; i < m; ++i) b[i] *= nrm;
+    }
+    double *z = t.V + (int64_t)k * m;
+    for (int i = 0; i < m; ++i) z[i] = b[i];
+  }
+  __syncthreads();
+  // modified Gram-Schmidt over the r vectors (warps over later vectors)
+  for (int k = 0; k < r; ++k) {
+    double *zk = t.V + (int64_t)k * m;
+    if (warp == 0) {
+      double s2 = 0;
+      for (int i = lane; i < m; i += 32) s2 = fma(zk[i], zk[i], s2);
+      s2 = frcp(sqrt(warp_sum(s2)));
+      for (int i = lane; i < m; i += 32) zk[i] *= s2;
+    }
+    __syncthreads();
+    for (int j = k + 1 + warp; j < r; j += nw) {
+      double *zj = t.V + (int64_t)j * m;
+      double s2 = 0;
+      for (int i = lane; i < m; i += 32) s2 = fma(zk[i], zj[i], s2);
+      s2 = warp_sum(s2);
+      for (int i = lane; i < m; i += 32) zj[i] -= s2 * zk[i];
+    }
+    __syncthreads();
+  }
+  if (t.dbg && tid == 0) t.dbg[3] = clock64();
+  // ---- 5. back-transformation V = H_0 ... H_{m-3} Z ----
+  if (m <= 256) {
+    for (int k = warp; k < r; k += nw) {
+      double *z = t.V + (int64_t)k * m;
+      double zr[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) zr[q] = (lane + 32 * q < m) ? z[lane + 32 * q] : 0.0;
+      for (int j = m - 3; j >= 0; --j) {
+        const double tj = tau[j];
+        if (tj == 0.0) continue;
+        const double *v = A + (int64_t)j * m;  // v_j in rows j+1.. of column j
+        double s2 = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          int i = lane + 32 * q;
+          if (i > j && i < m) s2 = fma(v[i], zr[q], s2);
+        }
+        s2 = warp_sum(s2) * tj;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          int i = lane + 32 * q;
+          if (i > j && i < m) zr[q] -= s2 * v[i];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (lane + 32 * q < m) z[lane + 32 * q] = zr[q];
+    }
+  } else {
+    for (int k = warp; k < r; k += nw) {
+      double *z = t.V + (int64_t)k * m;
+      for (int j = m - 3; j >= 0; --j) {
+        const double tj = tau[j];
+        if (tj == 0.0) continue;
+        const double *v = A + (int64_t)j * m;
+        double s2 = 0;
+        for (int i = j + 1 + lane; i < m; i += 32) s2 = fma(v[i], z[i], s2);
+        s2 = warp_sum(s2) * tj;
+        for (int i = j + 1 + lane; i < m; i += 32) z[i] -= s2 * v[i];
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  if (t.dbg && tid == 0) t.dbg[4] = clock64();
+}
+
 // ----------------------------------------------------------------- pivot ----
 // Fused pivot of (s, b): K = [[S, V], [V^T, 0]] (n = m + r) factored as
 // K = L D L^T with D = diag(I_m, -I_r) (Cholesky of S, then of
@@ -333,10 +825,8 @@ __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks
   if (in_smem) {
     A = sh + n;
     lda = n;
-    for (int64_t q = tid; q < (int64_t)n * n; q += blockDim.x) {
-      int i = (int)(q % n), j = (int)(q / n);
-      A[q] = (i >= j) ? t.F[i + (int64_t)j * t.ld] : 0.0;
-    }
+    for (int j = warp; j < n; j += nw)
+      for (int i = lane; i < n; i += 32) A[i + (int64_t)j * n] = (i >= j) ? t.F[i + (int64_t)j * t.ld] : 0.0;
   } else {
     A = t.F;
     lda = t.ld;
@@ -355,7 +845,7 @@ __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks
       break;
     }
     const double lkk = sqrt(v);
-    const double sc = 1.0 / (d * lkk);
+    const double sc = d * frcp(lkk);
     __syncthreads();
     for (int i = k + 1 + tid; i < n; i += blockDim.x) A[i + (int64_t)k * lda] *= sc;
     __syncthreads();
@@ -373,7 +863,7 @@ __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks
   for (int j = n - 1; j >= 0; --j) {
     for (int i = j + 1 + tid; i < n; i += blockDim.x) tmp[i] = A[i + (int64_t)j * lda];
     __syncthreads();
-    const double ajj = 1.0 / A[j + (int64_t)j * lda];
+    const double ajj = frcp(A[j + (int64_t)j * lda]);
     for (int i = j + 1 + tid; i < n; i += blockDim.x) {
       double s = 0;
       for (int k = j + 1; k <= i; ++k) s = fma(A[i + (int64_t)k * lda], tmp[k], s);
@@ -384,11 +874,11 @@ __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks
     __syncthreads();
   }
   // write back L^{-1} with the strict upper triangle zeroed
-  for (int64_t q = tid; q < (int64_t)n * n; q += blockDim.x) {
-    int i = (int)(q % n), j = (int)(q / n);
-    double v = (i >= j) ? A[i + (int64_t)j * lda] : 0.0;
-    t.F[i + (int64_t)j * t.ld] = v;
-  }
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i < n; i += 32) {
+      double v = (i >= j) ? A[i + (int64_t)j * lda] : 0.0;
+      t.F[i + (int64_t)j * t.ld] = v;
+    }
 }
 
 // ----------------------------------------------------------------- apply ----

@@ -163,10 +163,10 @@ enum KClass {
   K_SCATTER, K_MERGE, K_GRAM, K_JACOBI, K_PROJECT, K_ASSEMBLE, K_PIVOT, K_ZGEMM, K_SCHUR,
   K_APPLY_FWD, K_APPLY_BWD, K_SPMV, K_DOT, K_VEC, K_NCLASS
 };
-static const char *KNAME[K_NCLASS] = {"leaf_scatter", "merge_copy", "gram_gemm", "jacobi_eig",
+static const char *KNAME[K_NCLASS] = {"leaf_scatter", "merge_copy", "gram_gemm", "eig_tridiag",
                                       "project_gemm", "assemble_copy", "pivot_chol_inv", "trsm_gemm",
                                       "schur_gemm", "apply_fwd", "apply_bwd", "spmv", "dot", "vec"};
-static const char *KKERNEL[K_NCLASS] = {"k_leaf_scatter", "k_copy", "k_gemm", "k_jacobi", "k_gemm", "k_copy",
+static const char *KKERNEL[K_NCLASS] = {"k_leaf_scatter", "k_copy", "k_gemm", "k_eig", "k_gemm", "k_copy",
                                         "k_pivot", "k_gemm", "k_gemm", "k_apply_fwd", "k_apply_bwd",
                                         "k_spmv", "k_dot_partial+k_dot_final", "k_axpby/k_sub/k_set_rhs/k_get_x"};
 struct KStat {
@@ -292,6 +292,7 @@ void ensure_mem(lorasp_ctx *h) {
   h->d_dotpart.ensure((DOT_BLOCKS + 64) * sizeof(double), h->stream);
   h->stg.init(size_t(64) << 20, h->stream);
   CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
@@ -462,7 +463,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           goff[c] = gtot;
           gtot += (int64_t)m[c] * m[c];
           stot += m[c];
-          if ((int64_t)m[c] * m[c] + 2 * m[c] > SMEM_LIMIT / 8) xtot += (int64_t)m[c] * m[c];
+          xtot += 7 * (int64_t)m[c] * m[c];  // eigen-solver scratch
         }
         h->ws_G.ensure(gtot * 8 + 256, st);
         h->ws_V.ensure(gtot * 8 + 256, st);
@@ -514,10 +515,8 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           e.V = h->ws_V.as<double>() + goff[c];
           e.sig = h->ws_sig.as<double>() + soff_sig;
           soff_sig += mc;
-          if ((int64_t)mc * mc + 2 * mc > SMEM_LIMIT / 8) {
-            e.work = h->ws_X.as<double>() + xoff;
-            xoff += (int64_t)mc * mc;
-          }
+          e.work = h->ws_X.as<double>() + xoff;
+          xoff += 7 * (int64_t)mc * mc;
           e.m = mc;
           e.node = c;
           e.rank_out = h->d_ranks.as<int>() + q;
@@ -525,11 +524,11 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         }
         launch_gemm(h, gt, gs, K_GRAM, f_gram, b_gram);
         EigTask *de = push(h, et);
-        int64_t want = (int64_t)max_m * max_m + 2 * max_m;
+        int64_t want = (int64_t)max_m * max_m + 6 * (max_m + 8) + std::max(max_m, 512);
         int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
-        cap = std::max(cap, 2 * max_m);
+        cap = std::max(cap, 6 * (max_m + 8) + std::max(max_m, 512));
         int ev = tbeg(h, K_JACOBI);
-        k_jacobi<<<(unsigned)et.size(), 512, cap * 8, st>>>(de, pl.eps, cap, h->d_status.as<int>());
+        k_eig<<<(unsigned)et.size(), 512, cap * 8, st>>>(de, pl.eps, cap, h->d_status.as<int>());
         tend(h, ev, f_eig, b_eig);
         ++h->launches_factor;
         CK(cudaGetLastError());
@@ -1307,16 +1306,18 @@ int lorasp_get_launch_count(lorasp_handle h, int64_t *f, int64_t *a, int64_t *k)
 
 int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, double *sigma, int *rank) {
   if (!G || !V || !sigma || !rank || m <= 0) return LORASP_E_ARG;
+  const bool jac = getenv("LORASP_EIG_JACOBI") != nullptr;  // debug: the one-sided Jacobi variant
   try {
     CK(cudaSetDevice(device));
     CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+    CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
     double *dG, *dV, *dS, *dW;
     int *dr, *dst;
     size_t mm = (size_t)m * m;
     CK(cudaMalloc(&dG, mm * 8));
     CK(cudaMalloc(&dV, mm * 8));
     CK(cudaMalloc(&dS, m * 8));
-    CK(cudaMalloc(&dW, mm * 8));
+    CK(cudaMalloc(&dW, 7 * mm * 8));
     CK(cudaMalloc(&dr, 64));
     dst = dr + 4;
     CK(cudaMemset(dr, 0, 64));
@@ -1330,12 +1331,24 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     e.m = m;
     e.node = 0;
     e.rank_out = dr;
+    long long *ddbg = nullptr;
+    if (getenv("LORASP_EIG_PROFILE")) {
+      CK(cudaMalloc(&ddbg, 128));
+      CK(cudaMemset(ddbg, 0, 128));
+    }
+    e.dbg = ddbg;
     EigTask *de;
     CK(cudaMalloc(&de, sizeof(EigTask)));
     CK(cudaMemcpy(de, &e, sizeof(EigTask), cudaMemcpyHostToDevice));
-    int cap = (int)std::min<int64_t>((int64_t)m * m + 2 * m, SMEM_LIMIT / 8);
-    cap = std::max(cap, 2 * m);
-    k_jacobi<<<1, 512, cap * 8>>>(de, eps, cap, dst);
+    if (jac) {
+      int cap = (int)std::min<int64_t>((int64_t)m * m + 2 * m, SMEM_LIMIT / 8);
+      cap = std::max(cap, 2 * m);
+      k_jacobi<<<1, 512, cap * 8>>>(de, eps, cap, dst);
+    } else {
+      int cap = (int)std::min<int64_t>((int64_t)m * m + 6 * (m + 8) + std::max(m, 512), SMEM_LIMIT / 8);
+      cap = std::max(cap, 6 * (m + 8) + std::max(m, 512));
+      k_eig<<<1, 512, cap * 8>>>(de, eps, cap, dst);
+    }
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     int st[2];
@@ -1343,6 +1356,15 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     CK(cudaMemcpy(st, dst, 2 * sizeof(int), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(sigma, dS, m * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(V, dV, (size_t)m * (*rank) * 8, cudaMemcpyDeviceToHost));
+    if (ddbg) {
+      long long tt[10];
+      CK(cudaMemcpy(tt, ddbg, sizeof(tt), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "[tridiag phases] vscale %lld  partials %lld  combine %lld  pvred %lld  update %lld\n",
+              tt[5], tt[6], tt[7], tt[8], tt[9]);
+      fprintf(stderr, "[eig m=%d r=%d] tridiag %lld  eigvals %lld  invit %lld  backtr %lld cycles\n", m, *rank,
+              tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3]);
+      cudaFree(ddbg);
+    }
     cudaFree(dG); cudaFree(dV); cudaFree(dS); cudaFree(dW); cudaFree(dr); cudaFree(de);
     return st[0];
   } catch (const Err &e) {
