@@ -887,10 +887,10 @@ __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks
 // forward:  y = L^{-1} [rhs_s; 0];  rhs_q -= Z_q^T D y           (q in T)
 // backward: u = y - Z x_T;  [x_s; x_b] = L^{-T} D u               (P:l.487-495)
 struct ApNode {
-  const double *F;
+  const double *F; // [L^{-1} | Z], column-major, leading dimension ld (even)
   double *y;       // n doubles, kept between the two passes
   int64_t off_s;   // vector offset of Var/RHS(s)
-  int m, r, W;
+  int m, r, W, ld;
   int seg0, nseg;
 };
 struct ApSeg {
@@ -898,67 +898,217 @@ struct ApSeg {
   int w, zc;      // width, column offset inside Z
 };
 
+// ---- bulk-async (TMA 1D) streaming helpers --------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Column-chunk streamer: a node's record F (column-major, ld n) is consumed as
+// runs of whole columns [c0, c1) copied into a 2-stage shared-memory ring with
+// cp.async.bulk by thread 0; completion through mbarriers.  Chunk c lives in
+// stage c & 1; its parity flips every second use.
+struct ColStream {
+  const double *base;  // first column of the run
+  int n, ncol, cc;     // rows, columns in the run, columns per chunk
+  double *buf[2];
+  uint64_t *bar;       // 2 mbarriers
+  __device__ int nchunks() const { return (ncol + cc - 1) / cc; }
+  __device__ void issue(int c) const {
+    const int c0 = c * cc, c1 = min(ncol, c0 + cc);
+    const uint32_t bytes = (uint32_t)((int64_t)(c1 - c0) * n * 8);   // n = ld (even)
+    fence_proxy_async();
+    mbar_expect_tx(&bar[c & 1], bytes);
+    bulk_g2s(buf[c & 1], base + (int64_t)c0 * n, bytes, &bar[c & 1]);
+  }
+};
+
+// One CTA per node: the node's record streams through shared memory once per
+// pass (forward reads L^{-1}[:, :m] and Z, backward reads Z and L^{-1}[:, :m]).
 __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ nodes,
                                                    const ApSeg *__restrict__ segs,
-                                                   double *__restrict__ vec) {
-  extern __shared__ double sh[];
+                                                   double *__restrict__ vec, int chunk_doubles) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) uint64_t bars[2];
   const ApNode nd = nodes[blockIdx.x];
   const int n = nd.m + nd.r;
   if (n == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  double *rhs = sh;      // m
-  double *dy = sh + nd.m;  // n
-  for (int i = tid; i < nd.m; i += blockDim.x) rhs[i] = vec[nd.off_s + i];
-  __syncthreads();
-  for (int i = tid; i < n; i += blockDim.x) {
-    double s = 0;
-    const int kmax = min(i, nd.m - 1);
-    for (int k = 0; k <= kmax; ++k) s = fma(nd.F[i + (int64_t)k * n], rhs[k], s);
-    nd.y[i] = s;
-    dy[i] = (i < nd.m) ? s : -s;
+  double *stage0 = sh, *stage1 = sh + chunk_doubles;
+  double *rhs = stage1 + chunk_doubles;  // m
+  double *dy = rhs + nd.m;               // n (accumulates y)
+  double *zo = dy + n;                   // W: Z^T D y, written back once at the end
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  for (int i = tid; i < nd.m; i += blockDim.x) rhs[i] = vec[nd.off_s + i];
+  for (int i = tid; i < n; i += blockDim.x) dy[i] = 0.0;
   __syncthreads();
-  const double *Z = nd.F + (int64_t)n * n;
+  const int ld = nd.ld;
+  int cc = max(1, chunk_doubles / ld);
+  // ---- y = L^{-1}[:, :m] rhs ----
+  ColStream A{nd.F, ld, nd.m, cc, {stage0, stage1}, bars};
+  const int na = A.nchunks();
+  const double *Z = nd.F + (int64_t)ld * n;
+  ColStream B{Z, ld, nd.W, cc, {stage0, stage1}, bars};
+  const int nb = B.nchunks();
+  const int ntot = na + nb;
+  if (tid == 0) {
+    if (ntot > 0) (0 < na ? A : B).issue(0 < na ? 0 : 0);
+  }
+  for (int c = 0; c < ntot; ++c) {
+    if (tid == 0 && c + 1 < ntot) {
+      if (c + 1 < na) A.issue(c + 1);
+      else {
+        // B chunk index (c+1-na) must land in stage (c+1)&1: reuse issue with a shifted parity
+        const int cb = c + 1 - na;
+        const int c0 = cb * cc, c1 = min(nd.W, c0 + cc);
+        uint32_t bytes = (uint32_t)((int64_t)(c1 - c0) * ld * 8);
+        fence_proxy_async();
+        mbar_expect_tx(&bars[(c + 1) & 1], bytes);
+        bulk_g2s(((c + 1) & 1) ? stage1 : stage0, Z + (int64_t)c0 * ld, bytes, &bars[(c + 1) & 1]);
+      }
+    }
+    mbar_wait(&bars[c & 1], (c >> 1) & 1);
+    const double *buf = (c & 1) ? stage1 : stage0;
+    if (c < na) {
+      const int k0 = c * cc, k1 = min(nd.m, k0 + cc);
+      for (int i = tid; i < n; i += blockDim.x) {
+        double sacc = 0;
+        const int kl = min(k1 - 1, i);
+        for (int k = k0; k <= kl; ++k) sacc = fma(buf[(int64_t)(k - k0) * ld + i], rhs[k], sacc);
+        dy[i] += sacc;
+      }
+      if (c == na - 1) {
+        __syncthreads();
+        for (int i = tid; i < n; i += blockDim.x) {
+          const double y = dy[i];
+          nd.y[i] = y;
+          dy[i] = (i < nd.m) ? y : -y;
+        }
+      }
+    } else {
+      const int j0 = (c - na) * cc, j1 = min(nd.W, j0 + cc);
+      for (int j = j0 + warp; j < j1; j += nw) {
+        const double *col = buf + (int64_t)(j - j0) * ld;
+        double sacc = 0;
+        for (int k = lane; k < n; k += 32) sacc = fma(col[k], dy[k], sacc);
+        sacc = warp_sum(sacc);
+        if (lane == 0) zo[j] = sacc;
+      }
+    }
+    __syncthreads();   // stage (c & 1) is free for chunk c + 2
+  }
+  // rhs_q -= Z_q^T D y for every target segment (coalesced read-modify-write)
   for (int sg = 0; sg < nd.nseg; ++sg) {
     const ApSeg S = segs[nd.seg0 + sg];
-    for (int j = warp; j < S.w; j += nw) {
-      const double *zc = Z + (int64_t)(S.zc + j) * n;
-      double s = 0;
-      for (int k = lane; k < n; k += 32) s = fma(zc[k], dy[k], s);
-      s = warp_sum(s);
-      if (lane == 0) vec[S.voff + j] -= s;
-    }
+    for (int j = tid; j < S.w; j += blockDim.x) vec[S.voff + j] -= zo[S.zc + j];
+  }
+  if (na == 0) {  // m == 0 cannot happen for a recorded node; keep y defined
+    for (int i = tid; i < n; i += blockDim.x) nd.y[i] = 0.0;
   }
 }
 
 __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ nodes,
                                                    const ApSeg *__restrict__ segs,
-                                                   double *__restrict__ vec) {
-  extern __shared__ double sh[];
+                                                   double *__restrict__ vec, int chunk_doubles) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) uint64_t bars[2];
   const ApNode nd = nodes[blockIdx.x];
   const int n = nd.m + nd.r;
   if (n == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  double *u = sh;           // n
-  double *xt = sh + n;      // W
+  double *stage0 = sh, *stage1 = sh + chunk_doubles;
+  double *u = stage1 + chunk_doubles;  // n
+  double *xt = u + n;                  // W
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int sg = 0; sg < nd.nseg; ++sg) {
     const ApSeg S = segs[nd.seg0 + sg];
     for (int j = tid; j < S.w; j += blockDim.x) xt[S.zc + j] = vec[S.voff + j];
   }
+  for (int i = tid; i < n; i += blockDim.x) u[i] = nd.y[i];
   __syncthreads();
-  const double *Z = nd.F + (int64_t)n * n;
-  for (int k = tid; k < n; k += blockDim.x) {
-    double s = nd.y[k];
-    for (int j = 0; j < nd.W; ++j) s = fma(-Z[k + (int64_t)j * n], xt[j], s);
-    u[k] = (k < nd.m) ? s : -s;  // D u
-  }
-  __syncthreads();
-  for (int i = warp; i < nd.m; i += nw) {
-    const double *li = nd.F + (int64_t)i * n;  // column i of L^{-1}: rows >= i
-    double s = 0;
-    for (int k = i + lane; k < n; k += 32) s = fma(li[k], u[k], s);
-    s = warp_sum(s);
-    if (lane == 0) vec[nd.off_s + i] = s;
+  const int ld = nd.ld;
+  int cc = max(1, chunk_doubles / ld);
+  const double *Z = nd.F + (int64_t)ld * n;
+  const int nb = (nd.W + cc - 1) / cc;     // Z chunks first
+  const int na = (nd.m + cc - 1) / cc;     // then L^{-1}[:, :m]
+  const int ntot = nb + na;
+  auto issue = [&](int c) {
+    const double *src;
+    int c0, c1;
+    if (c < nb) {
+      c0 = c * cc;
+      c1 = min(nd.W, c0 + cc);
+      src = Z + (int64_t)c0 * ld;
+    } else {
+      c0 = (c - nb) * cc;
+      c1 = min(nd.m, c0 + cc);
+      src = nd.F + (int64_t)c0 * ld;
+    }
+    uint32_t bytes = (uint32_t)((int64_t)(c1 - c0) * ld * 8);
+    fence_proxy_async();
+    mbar_expect_tx(&bars[c & 1], bytes);
+    bulk_g2s((c & 1) ? stage1 : stage0, src, bytes, &bars[c & 1]);
+  };
+  if (tid == 0 && ntot > 0) issue(0);
+  for (int c = 0; c < ntot; ++c) {
+    if (tid == 0 && c + 1 < ntot) issue(c + 1);
+    mbar_wait(&bars[c & 1], (c >> 1) & 1);
+    const double *buf = (c & 1) ? stage1 : stage0;
+    if (c < nb) {
+      const int j0 = c * cc, j1 = min(nd.W, j0 + cc);
+      for (int i = tid; i < n; i += blockDim.x) {
+        double sacc = 0;
+        for (int j = j0; j < j1; ++j) sacc = fma(buf[(int64_t)(j - j0) * ld + i], xt[j], sacc);
+        u[i] -= sacc;
+      }
+      if (c == nb - 1) {
+        __syncthreads();
+        for (int i = nd.m + tid; i < n; i += blockDim.x) u[i] = -u[i];   // D u
+      }
+    } else {
+      if (nb == 0 && c == 0) {
+        for (int i = nd.m + tid; i < n; i += blockDim.x) u[i] = -u[i];
+        __syncthreads();
+      }
+      const int i0 = (c - nb) * cc, i1 = min(nd.m, i0 + cc);
+      for (int i = i0 + warp; i < i1; i += nw) {
+        const double *col = buf + (int64_t)(i - i0) * ld;
+        double sacc = 0;
+        for (int k = i + lane; k < n; k += 32) sacc = fma(col[k], u[k], sacc);
+        sacc = warp_sum(sacc);
+        if (lane == 0) vec[nd.off_s + i] = sacc;
+      }
+    }
+    __syncthreads();
   }
 }
 

@@ -180,7 +180,7 @@ struct TimedEv {
 };
 
 struct NodeRec {  // one eliminated (s, b) pair, for apply + stats
-  int level, c, m, r, W;
+  int level, c, m, r, W, ld;
   double *F;
   std::vector<int> T;  // level node ids (S: c', P: K + c')
   std::vector<int> w;  // widths
@@ -212,11 +212,12 @@ struct lorasp_ctx {
   std::vector<int> ap_wave_begin;  // in recs order (factor order), per wave
   std::vector<double> ap_wave_flops, ap_wave_bytes;  // per wave, one pass (fwd or bwd)
   size_t ap_fwd_smem = 0, ap_bwd_smem = 0;
+  int ap_chunk = 0;
   int64_t vec_len = 0;
   bool dest_ready = false;
   std::vector<int64_t> leaf_soff;  // leaf-level slot offsets used for d_dest
   // stats
-  double flops_model = 0, t_factor_ms = 0;
+  double flops_model = 0, t_factor_ms = 0, t_host_ms = 0, t_sync_ms = 0;
   int64_t launches_factor = 0, launches_apply = 0, launches_krylov = 0;
   int64_t f_doubles = 0;
   bool debug = getenv("LORASP_DEBUG") != nullptr;
@@ -357,6 +358,8 @@ void factor_impl(lorasp_ctx *h, const double *values) {
   const int L = pl.depth;
   h->launches_factor = 0;
   h->flops_model = 0;
+  h->t_host_ms = 0;
+  h->t_sync_ms = 0;
   h->factored = false;
   // values -> device
   if (is_device_ptr(values)) {
@@ -534,7 +537,9 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h->h_ranks, h->d_ranks.p, comp.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        auto ts0 = std::chrono::steady_clock::now();
         CK(cudaStreamSynchronize(st));
+        h->t_sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts0).count();
         h->stg.reset();
         if (h->h_status[0] != 0) {
           throw Err(h->h_status[0], std::string(h->h_status[0] == LORASP_E_EIG_NOCONV
@@ -546,6 +551,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         for (size_t q = 0; q < comp.size(); ++q) r[comp[q]] = h->h_ranks[q];
       }
       // --- project, assemble, pivot, Z, Schur ---
+      auto th0 = std::chrono::steady_clock::now();
       std::vector<GemmTask> pt, zt, stt;
       std::vector<GemmSeg> ps, zs, ss;
       std::vector<CopyTask> ct;
@@ -605,10 +611,12 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         } else if (nd.aux) {
           for (int p : nd.partners) R += size(p);
         }
-        // record F = [L^{-1} | Z]  (n x (n + W))
-        double *F = h->fpool.alloc((size_t)n * (n + W));
+        // record F = [L^{-1} | Z]  (n x (n + W), leading dimension ldF = n rounded up to
+        // even so that every column starts 16-byte aligned for the bulk-copy apply)
+        const int ldF = n + (n & 1);
+        double *F = h->fpool.alloc((size_t)ldF * (n + W) + 2);  // +16 B: bulk copies round up
         double *ctr = h->ws_ctr.as<double>() + ctr_off[e];
-        h->f_doubles += (int64_t)n * (n + W);
+        h->f_doubles += (int64_t)ldF * (n + W);
         NodeRec rec;
         rec.level = i;
         rec.c = c;
@@ -616,12 +624,13 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         rec.r = rc;
         rec.W = W;
         rec.F = F;
+        rec.ld = ldF;
         // assemble pivot K = [[S, V], [V^T, 0]] (lower part used)
         CopyTask t{};
         t.src = slot_ptr(nd.self_slot);
         t.lds = sld[nd.self_slot];
         t.dst = F;
-        t.ldd = n;
+        t.ldd = ldF;
         t.rows = mc;
         t.cols = mc;
         t.mode = 0;
@@ -633,7 +642,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           t.src = V;
           t.lds = mc;
           t.dst = F + mc;
-          t.ldd = n;
+          t.ldd = ldF;
           t.rows = rc;
           t.cols = mc;
           t.mode = 0;
@@ -641,8 +650,8 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           t.alpha = 1.0;
           ct.push_back(t);  // V^T (s -> b, rule 4)
           t = CopyTask{};
-          t.dst = F + mc + (int64_t)mc * n;
-          t.ldd = n;
+          t.dst = F + mc + (int64_t)mc * ldF;
+          t.ldd = ldF;
           t.rows = rc;
           t.cols = rc;
           t.mode = 1;
@@ -702,14 +711,14 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           }
         }
         // pivot
-        pv.push_back(PivTask{F, n, mc, rc, c});
+        pv.push_back(PivTask{F, ldF, mc, rc, c});
         // Z = L^{-1} C  (L^{-1} lower triangular: row tile tm needs k < tm + 64)
         if (W > 0) {
           for (int tn = 0; tn < W; tn += GT)
             for (int tm = 0; tm < n; tm += GT) {
               GemmTask b{};
-              b.C = F + (int64_t)n * n;
-              b.ldc = n;
+              b.C = F + (int64_t)ldF * n;
+              b.ldc = ldF;
               b.M = n;
               b.N = W;
               b.tm = tm;
@@ -719,7 +728,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
               b.nseg = 1;
               GemmSeg g{};
               g.A = F;
-              g.lda = n;
+              g.lda = ldF;
               g.B = ctr;
               g.ldb = n;
               g.K = std::min(n, tm + GT);
@@ -733,7 +742,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           const std::vector<int> &T = rec.T;
           std::vector<int> zoff(T.size() + 1, 0);
           for (size_t a = 0; a < T.size(); ++a) zoff[a + 1] = zoff[a] + rec.w[a];
-          const double *Z = F + (int64_t)n * n;
+          const double *Z = F + (int64_t)ldF * n;
           size_t idx = 0;
           for (size_t a = 0; a < T.size(); ++a)
             for (size_t bb = 0; bb <= a; ++bb, ++idx) {
@@ -751,9 +760,9 @@ void factor_impl(lorasp_ctx *h, const double *values) {
               b.beta = 1;
               b.seg0 = (int)ss.size();
               GemmSeg g{};
-              g.A = Z + (int64_t)zoff[a] * n;
-              g.B = Z + (int64_t)zoff[bb] * n;
-              g.lda = g.ldb = n;
+              g.A = Z + (int64_t)zoff[a] * ldF;
+              g.B = Z + (int64_t)zoff[bb] * ldF;
+              g.lda = g.ldb = ldF;
               g.K = mc;
               g.alpha = -1.0;
               ss.push_back(g);
@@ -779,6 +788,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         b_s += 8.0 * (2.0 * n * W + (double)W * W);
         h->recs.push_back(std::move(rec));
       }
+      h->t_host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
       launch_gemm(h, pt, ps, K_PROJECT, f_proj, b_proj);
       launch_copy(h, ct, K_ASSEMBLE);
       {
@@ -838,7 +848,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
   }
   h->d_y.ensure(std::max<int64_t>(ytot, 8) * 8, st);
   h->ap_wave_begin.clear();
-  size_t fwd = 0, bwd = 0;
+  size_t fwd = 0, bwd = 0, max_col = 0;
   int prev_level = -1, prev_wave = -1;
   for (size_t q = 0; q < h->recs.size(); ++q) {
     const NodeRec &rc = h->recs[q];
@@ -854,6 +864,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
     a.m = rc.m;
     a.r = rc.r;
     a.W = rc.W;
+    a.ld = rc.ld;
     a.seg0 = (int)as.size();
     int zc = 0;
     const int K = lv.K;
@@ -869,8 +880,9 @@ void factor_impl(lorasp_ctx *h, const double *values) {
     a.nseg = (int)as.size() - a.seg0;
     an.push_back(a);
     int n = rc.m + rc.r;
-    fwd = std::max(fwd, (size_t)(rc.m + n));
-    bwd = std::max(bwd, (size_t)(n + rc.W));
+    fwd = std::max(fwd, (size_t)(rc.m + n + rc.W + 2));   // rhs, y, Z^T D y
+    bwd = std::max(bwd, (size_t)(n + rc.W + 2));
+    max_col = std::max(max_col, (size_t)rc.ld);
   }
   h->ap_wave_begin.push_back((int)h->recs.size());
   h->ap_wave_flops.assign(h->ap_wave_begin.size() - 1, 0.0);
@@ -884,10 +896,18 @@ void factor_impl(lorasp_ctx *h, const double *values) {
       h->ap_wave_flops[w] += 2.0 * elems;
       h->ap_wave_bytes[w] += 8.0 * elems + 8.0 * 2 * (n + rc.W);
     }
-  h->ap_fwd_smem = fwd * 8;
-  h->ap_bwd_smem = bwd * 8;
-  if (h->ap_fwd_smem > (size_t)SMEM_LIMIT || h->ap_bwd_smem > (size_t)SMEM_LIMIT)
-    throw Err(LORASP_E_ARG, "apply: node record too large for the shared-memory apply kernel");
+  // 2-stage streaming ring: as large as fits (<= 2 x 48 KB), >= 2 columns per stage
+  {
+    size_t fixed = std::max(fwd, bwd) * 8 + 256;
+    size_t room = fixed < (size_t)SMEM_LIMIT ? ((size_t)SMEM_LIMIT - fixed) / 2 : 0;
+    size_t ch = std::min<size_t>(room, 48 * 1024) / 8;
+    ch &= ~size_t(1);
+    if (ch < 2 * max_col + 2)
+      throw Err(LORASP_E_ARG, "apply: node record too large for the shared-memory apply kernel");
+    h->ap_chunk = (int)ch;
+    h->ap_fwd_smem = fwd * 8 + 2 * ch * 8 + 64;
+    h->ap_bwd_smem = bwd * 8 + 2 * ch * 8 + 64;
+  }
   h->d_apnodes.ensure(std::max<size_t>(1, an.size()) * sizeof(ApNode), st);
   h->d_apsegs.ensure(std::max<size_t>(1, as.size()) * sizeof(ApSeg), st);
   CK(cudaMemcpy(h->d_apnodes.p, an.data(), an.size() * sizeof(ApNode), cudaMemcpyHostToDevice));
@@ -916,13 +936,13 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
   for (int w = 0; w < nw; ++w) {
     int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
     ev = tbeg(h, K_APPLY_FWD);
-    k_apply_fwd<<<b1 - b0, 256, h->ap_fwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>());
+    k_apply_fwd<<<b1 - b0, 256, h->ap_fwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>(), h->ap_chunk);
     tend(h, ev, h->ap_wave_flops[w], h->ap_wave_bytes[w]);
   }
   for (int w = nw - 1; w >= 0; --w) {
     int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
     ev = tbeg(h, K_APPLY_BWD);
-    k_apply_bwd<<<b1 - b0, 256, h->ap_bwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>());
+    k_apply_bwd<<<b1 - b0, 256, h->ap_bwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>(), h->ap_chunk);
     tend(h, ev, h->ap_wave_flops[w], h->ap_wave_bytes[w]);
   }
   ev = tbeg(h, K_VEC);
@@ -1253,7 +1273,8 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
     << ",\"factored\":" << (h->factored ? "true" : "false");
   if (h->factored) {
     o << ",\"flops_model\":" << h->flops_model << ",\"factor_bytes\":" << h->f_doubles * 8
-      << ",\"t_factor_host_ms\":" << h->t_factor_ms << ",\"launches_factor\":" << h->launches_factor
+      << ",\"t_factor_host_ms\":" << h->t_factor_ms << ",\"t_task_build_ms\":" << h->t_host_ms
+      << ",\"t_rank_sync_wait_ms\":" << h->t_sync_ms << ",\"launches_factor\":" << h->launches_factor
       << ",\"aux_vars\":";
     int64_t aux = 0;
     for (int i = 1; i <= pl.depth; ++i)
