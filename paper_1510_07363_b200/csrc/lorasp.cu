@@ -200,7 +200,7 @@ struct lorasp_ctx {
   // numeric state
   std::vector<std::vector<int>> msz, rnk;  // [level][cluster]
   std::vector<std::vector<double>> sigma0; // unused placeholder for stats
-  DevBuf d_values, d_rowptr, d_colidx, d_dest, arena[2], ws_G, ws_V, ws_sig, ws_X, ws_ctr, d_ranks,
+  DevBuf d_values, d_rowptr, d_colidx, d_dest, arena[2], ws_G, ws_V, ws_sig, ws_X, ws_ctr, ws_piv, d_ranks,
       d_status, d_vec, d_y, d_perm, d_b, d_x, d_kry, d_apnodes, d_apsegs, d_dotpart;
   int *h_ranks = nullptr;
   int *h_status = nullptr;
@@ -311,7 +311,7 @@ void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::v
   h->stg.reserve(segs.size() * sizeof(GemmSeg) + tasks.size() * sizeof(GemmTask), h->stream);
   GemmSeg *ds = push(h, segs);
   GemmTask *dt = push(h, tasks);
-  int ev = tbeg(h, cls);
+  int ev = cls >= 0 ? tbeg(h, cls) : -1;
   k_gemm<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt, ds);
   tend(h, ev, flops, bytes);
   ++h->launches_factor;
@@ -323,7 +323,7 @@ void launch_copy(lorasp_ctx *h, const std::vector<CopyTask> &tasks, int cls) {
   CopyTask *dt = push(h, tasks);
   double bytes = 0;
   for (const CopyTask &t : tasks) bytes += (t.mode == 0 ? 16.0 : 8.0) * t.rows * t.cols;
-  int ev = tbeg(h, cls);
+  int ev = cls >= 0 ? tbeg(h, cls) : -1;
   k_copy<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt);
   tend(h, ev, 0, bytes);
   ++h->launches_factor;
@@ -349,6 +349,176 @@ double node_flops(int m, int r, int R, int W) {
   f += ((double)m * m * m + (double)r * r * r) / 3.0 + ((double)m * m + (double)r * r) * (W + r) +
        (double)(m + r) * (W + r) * (W + r);
   return f;
+}
+
+// Fused pivots of one wave: nodes whose pivot fits one CTA's shared memory go
+// through k_pivot; larger ones through the blocked path (k_pivdiag + k_gemm).
+static const int PIV_SMALL_N = 160;
+
+void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double b_piv) {
+  cudaStream_t st = h->stream;
+  std::vector<PivTask> small, big;
+  int max_n = 0;
+  for (const PivTask &t : pv) {
+    const int n = t.m + t.r;
+    if (n <= PIV_SMALL_N) {
+      small.push_back(t);
+      max_n = std::max(max_n, n);
+    } else {
+      big.push_back(t);
+    }
+  }
+  int ev = tbeg(h, K_PIVOT);
+  if (!small.empty()) {
+    PivTask *dp = push(h, small);
+    int64_t want = (int64_t)max_n * max_n + max_n;
+    int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
+    cap = std::max(cap, max_n);
+    k_pivot<<<(unsigned)small.size(), 512, cap * 8, st>>>(dp, cap, h->d_status.as<int>());
+    ++h->launches_factor;
+    CK(cudaGetLastError());
+  }
+  if (!big.empty()) {
+    // scratch per node: X (n x n) | S (n x 64) | T (n x 64) | Wt (64 x 64)
+    std::vector<int64_t> off(big.size());
+    int64_t tot = 0;
+    int np_max = 0;
+    for (size_t q = 0; q < big.size(); ++q) {
+      const int n = big[q].m + big[q].r;
+      off[q] = tot;
+      tot += (int64_t)n * n + (int64_t)n * 64 + (int64_t)((n + 63) / 64) * 4096 + 4096;
+      np_max = std::max(np_max, (n + 63) / 64);
+    }
+    h->ws_piv.ensure(tot * 8 + 256, st);
+    CK(cudaMemsetAsync(h->ws_piv.p, 0, tot * 8, st));
+    double *wb = h->ws_piv.as<double>();
+    auto Xp = [&](size_t q) { return wb + off[q]; };
+    auto Sp = [&](size_t q) { const int n = big[q].m + big[q].r; return wb + off[q] + (int64_t)n * n; };
+    auto Tp = [&](size_t q) { const int n = big[q].m + big[q].r; return wb + off[q] + (int64_t)n * n + (int64_t)n * 64; };
+    auto Wp = [&](size_t q) {
+      const int n = big[q].m + big[q].r;
+      return wb + off[q] + (int64_t)n * n + (int64_t)n * 64 + (int64_t)((n + 63) / 64) * 4096;
+    };
+    for (int p = 0; p < np_max; ++p) {
+      std::vector<PivDiagTask> dt;
+      std::vector<CopyTask> ct;
+      std::vector<GemmTask> g1, g2;
+      std::vector<GemmSeg> s1, s2;
+      for (size_t q = 0; q < big.size(); ++q) {
+        const PivTask &t = big[q];
+        const int n = t.m + t.r, j0 = 64 * p;
+        if (j0 >= n) continue;
+        const int b = std::min(64, n - j0), j1 = j0 + b, rest = n - j1;
+        dt.push_back(PivDiagTask{t.F, Xp(q), Wp(q), t.ld, n, j0, b, t.m, t.node});
+        if (rest == 0) continue;
+        CopyTask c{};
+        c.src = t.F + j1 + (int64_t)j0 * t.ld;
+        c.lds = t.ld;
+        c.dst = Sp(q);
+        c.ldd = n;
+        c.rows = rest;
+        c.cols = b;
+        c.mode = 0;
+        c.alpha = 1.0;
+        ct.push_back(c);
+        // L21 = S Wt
+        GemmTask g{};
+        g.C = t.F + j1 + (int64_t)j0 * t.ld;
+        g.ldc = t.ld;
+        g.M = rest;
+        g.N = b;
+        g.beta = 0;
+        g.seg0 = (int)s1.size();
+        g.nseg = 1;
+        s1.push_back(GemmSeg{Sp(q), Wp(q), n, 64, b, 1.0});
+        add_tiles(g1, g);
+        // K22 -= L21 D1 L21^T (lower tiles)
+        const int spos = std::max(0, std::min(b, t.m - j0));
+        const double *L21 = t.F + j1 + (int64_t)j0 * t.ld;
+        GemmTask u{};
+        u.C = t.F + j1 + (int64_t)j1 * t.ld;
+        u.ldc = t.ld;
+        u.M = rest;
+        u.N = rest;
+        u.tb = 1;
+        u.beta = 1;
+        u.seg0 = (int)s2.size();
+        if (spos > 0) s2.push_back(GemmSeg{L21, L21, t.ld, t.ld, spos, -1.0});
+        if (spos < b) s2.push_back(GemmSeg{L21 + (int64_t)spos * t.ld, L21 + (int64_t)spos * t.ld, t.ld, t.ld,
+                                           b - spos, 1.0});
+        u.nseg = (int)s2.size() - u.seg0;
+        for (int tn = 0; tn < rest; tn += GT)
+          for (int tm = tn; tm < rest; tm += GT) {
+            GemmTask x = u;
+            x.tm = tm;
+            x.tn = tn;
+            g2.push_back(x);
+          }
+      }
+      if (!dt.empty()) {
+        PivDiagTask *dd = push(h, dt);
+        k_pivdiag<<<(unsigned)dt.size(), 256, 0, st>>>(dd, h->d_status.as<int>());
+        ++h->launches_factor;
+        CK(cudaGetLastError());
+      }
+      launch_copy(h, ct, -1);
+      launch_gemm(h, g1, s1, -1, 0, 0);
+      launch_gemm(h, g2, s2, -1, 0, 0);
+    }
+    // blocked inversion: X_ip = -X_ii * sum_{k=p}^{i-1} L_ik X_kp
+    for (int i = 1; i < np_max; ++i) {
+      std::vector<GemmTask> g1, g2;
+      std::vector<GemmSeg> s1, s2;
+      for (size_t q = 0; q < big.size(); ++q) {
+        const PivTask &t = big[q];
+        const int n = t.m + t.r, i0 = 64 * i;
+        if (i0 >= n) continue;
+        const int bi = std::min(64, n - i0);
+        for (int p = 0; p < i; ++p) {
+          const int p0 = 64 * p, bp = 64;
+          GemmTask g{};
+          g.C = Tp(q) + (int64_t)p * 4096;   // T_ip: bi x 64, ld 64, slot p
+          g.ldc = 64;
+          g.M = bi;
+          g.N = bp;
+          g.beta = 0;
+          g.seg0 = (int)s1.size();
+          g.nseg = 1;
+          s1.push_back(GemmSeg{t.F + i0 + (int64_t)p0 * t.ld, Xp(q) + p0 + (int64_t)p0 * n, t.ld, n, i0 - p0, 1.0});
+          add_tiles(g1, g);
+          GemmTask x{};
+          x.C = Xp(q) + i0 + (int64_t)p0 * n;
+          x.ldc = n;
+          x.M = bi;
+          x.N = bp;
+          x.beta = 0;
+          x.seg0 = (int)s2.size();
+          x.nseg = 1;
+          s2.push_back(GemmSeg{Xp(q) + i0 + (int64_t)i0 * n, Tp(q) + (int64_t)p * 4096, n, 64, bi, -1.0});
+          add_tiles(g2, x);
+        }
+      }
+      launch_gemm(h, g1, s1, -1, 0, 0);
+      launch_gemm(h, g2, s2, -1, 0, 0);
+    }
+    std::vector<CopyTask> ct;
+    for (size_t q = 0; q < big.size(); ++q) {
+      const PivTask &t = big[q];
+      const int n = t.m + t.r;
+      CopyTask c{};
+      c.src = Xp(q);
+      c.lds = n;
+      c.dst = t.F;
+      c.ldd = t.ld;
+      c.rows = n;
+      c.cols = n;
+      c.mode = 0;
+      c.alpha = 1.0;
+      ct.push_back(c);
+    }
+    launch_copy(h, ct, -1);
+  }
+  tend(h, ev, f_piv, b_piv);
 }
 
 void factor_impl(lorasp_ctx *h, const double *values) {
@@ -791,17 +961,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
       h->t_host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
       launch_gemm(h, pt, ps, K_PROJECT, f_proj, b_proj);
       launch_copy(h, ct, K_ASSEMBLE);
-      {
-        PivTask *dp = push(h, pv);
-        int64_t want = (int64_t)max_n * max_n + max_n;
-        int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
-        cap = std::max(cap, max_n);
-        int ev = tbeg(h, K_PIVOT);
-        k_pivot<<<(unsigned)pv.size(), 512, cap * 8, st>>>(dp, cap, h->d_status.as<int>());
-        tend(h, ev, f_piv, b_piv);
-        ++h->launches_factor;
-        CK(cudaGetLastError());
-      }
+      pivots(h, pv, f_piv, b_piv);
       launch_gemm(h, zt, zs, K_ZGEMM, f_z, b_z);
       launch_gemm(h, stt, ss, K_SCHUR, f_s, b_s);
       if (h->debug) {
@@ -1432,7 +1592,8 @@ void lorasp_destroy(lorasp_handle h) {
     cudaSetDevice(h->device);
     cudaStreamSynchronize(h->stream);
     DevBuf *bufs[] = {&h->d_values, &h->d_rowptr, &h->d_colidx, &h->d_dest, &h->arena[0], &h->arena[1],
-                      &h->ws_G, &h->ws_V, &h->ws_sig, &h->ws_X, &h->ws_ctr, &h->d_ranks, &h->d_status,
+                      &h->ws_G, &h->ws_V, &h->ws_sig, &h->ws_X, &h->ws_ctr, &h->ws_piv, &h->d_ranks,
+                      &h->d_status,
                       &h->d_vec, &h->d_y, &h->d_perm, &h->d_b, &h->d_x, &h->d_kry, &h->d_apnodes,
                       &h->d_apsegs, &h->d_dotpart};
     for (DevBuf *b : bufs) b->release();

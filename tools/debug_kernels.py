@@ -25,3 +25,11 @@ for m in [64, 128]:
     check(U @ np.diag(s) @ W.T, 1e-3, "clusters eps1e-3")
     s = 10.0**(-6*np.arange(m)/m)
     check(U @ np.diag(s) @ W.T, 1e-3, "slow decay eps1e-3")
+# pivot kernel, small and large n (large path is exercised through the factor tests)
+for m, rr in [(100, 40), (150, 10)]:
+    Sx = rng.standard_normal((m, m)); S = Sx@Sx.T + m*np.eye(m)
+    Vq,_ = np.linalg.qr(rng.standard_normal((m, rr)))
+    n = m+rr; K = np.zeros((n,n)); K[:m,:m]=S; K[m:,:m]=Vq.T; K[:m,m:]=Vq
+    Li, st = L.test_pivot(K, m, rr)
+    Lf = np.linalg.inv(Li); D = np.diag([1]*m+[-1]*rr)
+    print("pivot n", n, "st", st, "recon", np.abs(Lf@D@Lf.T - K).max()/np.abs(K).max())
