@@ -339,33 +339,40 @@ __device__ __forceinline__ int sturm_count(const double *__restrict__ d, const d
                                            int m, double x, double pivmin) {
   // Number of eigenvalues of T below x: sign changes of the leading principal
   // minors p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}, i.e. negative pivots
-  // q_i = p_i / p_{i-1} of the LDL^T count, evaluated without divisions
-  // (an exact zero pivot counts as negative, as q = -pivmin does in LAPACK).
-  // T is pre-scaled to |d|, |e| <= 1, so |p| grows at most 3x per step; the
-  // pair (p0, p1) is renormalised by a power of two every 8 steps.  d / e2 are
+  // q_i = p_i / p_{i-1} of the LDL^T count, evaluated without divisions.  T is
+  // pre-scaled to |d|, |e| <= 1, so |p| grows at most 3x per step; the pair
+  // (p0, p1) is renormalised by a power of two every 8 steps.  d / e2 are
   // padded to a multiple of 8 with d = 4, e2 = 0 (no sign change for x < 4).
+  // An exact zero minor (x an eigenvalue of a leading block) is detected off
+  // the dependency chain and the count is redone at the next double above x.
   (void)pivmin;
-  double p0 = 1.0, p1 = 1.0;
-  int c = 0;
   const double *e2m = e2 - 1;
-  for (int i0 = 0; i0 < m; i0 += 8) {
+  for (int attempt = 0; attempt < 4; ++attempt) {
+    double p0 = 1.0, p1 = 1.0;
+    int c = 0;
+    bool zero = false;
+    for (int i0 = 0; i0 < m; i0 += 8) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int i = i0 + u;
-      const double ee = (i == 0) ? 0.0 : e2m[i];
-      double p2 = fma(d[i] - x, p1, -ee * p0);
-      p2 = (p2 == 0.0) ? -1e-30 * p1 : p2;
-      c += (p2 < 0.0) != (p1 < 0.0);
-      p0 = p1;
-      p1 = p2;
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u;
+        const double ee = (i == 0) ? 0.0 : e2m[i];
+        const double p2 = fma(d[i] - x, p1, -ee * p0);
+        const long long b2 = __double_as_longlong(p2), b1 = __double_as_longlong(p1);
+        zero |= (b2 << 1) == 0;                 // +-0
+        c += (int)((unsigned long long)(b2 ^ b1) >> 63);   // sign change
+        p0 = p1;
+        p1 = p2;
+      }
+      const double a = fmax(fabs(p0), fabs(p1));
+      const long long ex = ((__double_as_longlong(a) >> 52) & 0x7ff) - 1023;
+      const double sc = __longlong_as_double((long long)(1023 - ex) << 52);
+      p0 *= sc;
+      p1 *= sc;
     }
-    const double a = fmax(fabs(p0), fabs(p1));
-    const long long ex = ((__double_as_longlong(a) >> 52) & 0x7ff) - 1023;
-    const double sc = __longlong_as_double((long long)(1023 - ex) << 52);
-    p0 *= sc;
-    p1 *= sc;
+    if (!zero) return c;
+    x = nextafter(x, 1e300);
   }
-  return c;
+  return 0;
 }
 
 // warp-cooperative multisection for the ascending-index-j eigenvalue of T
@@ -392,8 +399,12 @@ __device__ __forceinline__ double warp_eig_asc(const double *d, const double *e2
   return 0.5 * (lo + hi);
 }
 
-__global__ void __launch_bounds__(512, 1) k_eig(const EigTask *__restrict__ tasks, double eps,
-                                             int smem_cap_doubles, int *status) {
+constexpr int EIG_THREADS = 256;      // generic path
+constexpr int EIG_REG_THREADS = 512;  // register-tile path (m <= 128)
+constexpr int EIG_REG_M = 128;
+template <bool REG>
+__global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
+    k_eig_t(const EigTask *__restrict__ tasks, double eps, int smem_cap_doubles, int *status) {
   extern __shared__ double sh[];
   __shared__ double s_red[32];
   __shared__ double s_bc[8];
@@ -404,10 +415,23 @@ __global__ void __launch_bounds__(512, 1) k_eig(const EigTask *__restrict__ task
   const int ml = m > 512 ? m : 512;  // lam doubles as p-partials scratch during phase 1
   const int mp = (m + 8) & ~7;       // padded length (>= m + 1, multiple of 8)
   double *d = sh, *e = d + mp, *tau = e + mp, *e2 = tau + mp, *vt = e2 + mp, *pw = vt + mp, *lam = pw + mp;
-  double *A = ((int64_t)m * m + 6 * mp + ml <= smem_cap_doubles) ? lam + ml : t.work + 6 * (int64_t)m * m;
+  double *A = (REG || (int64_t)m * m + 6 * mp + ml <= smem_cap_doubles) ? lam + ml
+                                                                        : t.work + 6 * (int64_t)m * m;
   double *scr = t.work;  // 6 m^2: inverse-iteration scratch
-  for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) A[q] = t.G[q];
-  __syncthreads();
+  // REG: thread (warp w, lane) holds the 4 x 8 tile a[q][u] = G(4 lane + q, 8 w + u)
+  double a[4][8];
+  if constexpr (REG) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = 4 * lane + q, c = 8 * warp + u;
+        a[q][u] = (r < m && c < m) ? t.G[r + (int64_t)c * m] : 0.0;
+      }
+  } else {
+    for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) A[q] = t.G[q];
+    __syncthreads();
+  }
   if (t.dbg && tid == 0) t.dbg[0] = clock64();
   // block reduction helper (sum)
   auto bsum = [&](double v) -> double {
@@ -420,7 +444,14 @@ __global__ void __launch_bounds__(512, 1) k_eig(const EigTask *__restrict__ task
     return r;
   };
   double fro = 0;
-  for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) fro += A[q] * A[q];
+  if constexpr (REG) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) fro = fma(a[q][u], a[q][u], fro);
+  } else {
+    for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) fro += A[q] * A[q];
+  }
   fro = bsum(fro);
   if (!(fro > 0.0)) {
     if (tid == 0) *t.rank_out = 0;
@@ -433,123 +464,213 @@ __global__ void __launch_bounds__(512, 1) k_eig(const EigTask *__restrict__ task
     if (tid == 0) *t.rank_out = m;
     return;
   }
-  // ---- 1. Householder tridiagonalisation ----
-  // per step k: v from column k (its squared norm below x0 was accumulated by
-  // warp 0 during the previous update), p = tau A22 v with 4 partial sums per
-  // row, one block reduction for p.v, then the rank-2 update A22 -= v w^T + w v^T.
-  double *part = t.work + 6 * (int64_t)m * m;  // placeholder (unused when A is in smem)
-  (void)part;
-  __shared__ double s_s2;
-  if (tid < 32) {
-    double a = 0;
-    for (int i = 2 + lane; i < m; i += 32) a = fma(A[i], A[i], a);   // column 0, rows 2..
-    a = warp_sum(a);
-    if (lane == 0) s_s2 = a;
+  if constexpr (REG) {
+  // ---- 1 (register tile). Householder tridiagonalisation, m <= 128 ----
+  // A lives in registers (4 x 8 per thread, 512 threads); per step k the warp
+  // owning column k forms v (written to shared memory, double-buffered, and
+  // into column k of A_sm for the back-transformation), every thread forms its
+  // 4 partial row sums of A v, rows reduce over the 16 column strips, and the
+  // rank-2 update is register-only.  v and p vanish outside rows/cols > k, so
+  // no predication is needed.  3 barriers per step.
+  double *vsm0 = vt, *vsm1 = pw;                     // v (two buffers)
+  double *psm0 = lam, *psm1 = lam + 128;             // p (two buffers)
+  double *psum = t.work + 6 * (int64_t)m * m;        // unused (register path uses smem below)
+  (void)psum;
+  __shared__ double ps_part[16][EIG_REG_M + 1];
+  for (int k = 0; k < m - 2; ++k) {
+    double *vs = (k & 1) ? vsm1 : vsm0;
+    double *ps = (k & 1) ? psm1 : psm0;
+    const int wk = k >> 3, uk = k & 7;
+    double tk = 0.0;
+    if (warp == wk) {
+      double col[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        col[q] = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (u == uk) col[q] = a[q][u];
+      }
+      double s2 = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = 4 * lane + q;
+        if (r >= k + 2 && r < m) s2 = fma(col[q], col[q], s2);
+      }
+      s2 = warp_sum(s2);
+      const int rx = k + 1;
+      double x0 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * lane + q == rx) x0 = col[q];
+      x0 = __shfl_sync(0xffffffffu, x0, rx >> 2);
+      double beta = x0, scal = 0.0;
+      if (s2 != 0.0) {
+        beta = -copysign(sqrt(x0 * x0 + s2), x0);
+        tk = (beta - x0) * frcp(beta);
+        scal = frcp(x0 - beta);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = 4 * lane + q;
+        double v = 0.0;
+        if (s2 != 0.0) v = (r == rx) ? 1.0 : ((r > rx && r < m) ? col[q] * scal : 0.0);
+        vs[r] = v;
+        if (r > k && r < m) A[r + (int64_t)k * m] = v;
+      }
+      if (lane == 0) {
+        tau[k] = tk;
+        e[k] = beta;
+      }
+    }
+    __syncthreads();                                              // (1) v visible
+    tk = tau[k];
+    // partial row sums over this warp's 8 columns
+    double vc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) vc[u] = vs[8 * warp + u];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double sacc = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sacc = fma(a[q][u], vc[u], sacc);
+      ps_part[warp][4 * lane + q] = sacc;
+    }
+    __syncthreads();                                              // (2) partials visible
+    double pvp = 0;
+    if (tid < EIG_REG_M) {
+      double sacc = 0;
+#pragma unroll
+      for (int w = 0; w < 16; ++w) sacc += ps_part[w][tid];
+      const double pi = (tid > k && tid < m) ? tk * sacc : 0.0;
+      ps[tid] = pi;
+      pvp = pi * vs[tid];
+    }
+    pvp = warp_sum(pvp);
+    if (lane == 0) s_red[warp] = pvp;
+    __syncthreads();                                              // (3) p, p.v visible
+    double pv = 0;
+#pragma unroll
+    for (int w = 0; w < 16; ++w) pv += s_red[w];
+    const double alpha = -0.5 * tk * pv;
+    double wc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) wc[u] = fma(alpha, vc[u], ps[8 * warp + u]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = 4 * lane + q;
+      const double vr = vs[r], wr = fma(alpha, vr, ps[r]);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[q][u] -= fma(vr, wc[u], wr * vc[u]);
+    }
+  }
+  // diagonal and last sub-diagonal from the register tiles
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = 4 * lane + q, c = 8 * warp + u;
+      if (r < m && r == c) d[r] = a[q][u];
+      if (m >= 2 && r == m - 1 && c == m - 2) e[m - 2] = a[q][u];
+    }
+  if (tid == 0) {
+    e[m - 1] = 0.0;
+    if (m >= 2) tau[m - 2] = 0.0;
+    tau[m - 1] = 0.0;
   }
   __syncthreads();
-  long long tph[6] = {0, 0, 0, 0, 0, 0};
+  } else {
+  // ---- 1. Householder tridiagonalisation (thread per row) ----
+  // step k: v from column k (its squared norm below x0 comes from the previous
+  // step), p = tau A22 v (thread i owns row i: sum over columns, conflict-free
+  // shared-memory reads), alpha from p.v, A22 -= v w^T + w v^T with
+  // w = p + alpha v formed on the fly, and the next column's norm; 3 barriers.
+  __shared__ double s_red2[32];
+  {
+    double a = 0;
+    for (int i = 2 + tid; i < m; i += blockDim.x) a = fma(A[i], A[i], a);
+    a = warp_sum(a);
+    if (lane == 0) s_red2[warp] = a;
+    __syncthreads();
+  }
+  long long tph[4] = {0, 0, 0, 0};
   long long tprev = clock64();
   for (int k = 0; k < m - 2; ++k) {
     const int L = m - k - 1;
     double *colk = A + (int64_t)k * m + (k + 1);   // x = A[k+1.., k], length L
-    const double s2 = s_s2;
+    double *A22 = A + (int64_t)(k + 1) * m + (k + 1);
+    double s2 = 0;                      // squared norm below x0 (partials of the last step)
+    for (int w = 0; w < nw; ++w) s2 += s_red2[w];
     const double x0 = colk[0];
-    if (s2 == 0.0) {
-      if (tid == 0) {
-        tau[k] = 0.0;
-        e[k] = x0;
+    double beta = x0, tk = 0.0, scal = 0.0;
+    const bool refl = s2 != 0.0;
+    if (refl) {
+      beta = -copysign(sqrt(x0 * x0 + s2), x0);
+      tk = (beta - x0) * frcp(beta);
+      scal = frcp(x0 - beta);
+      for (int i = tid; i < L; i += blockDim.x) {
+        const double v = (i == 0) ? 1.0 : colk[i] * scal;
+        vt[i] = v;
+        colk[i] = v;
       }
-      // next column's norm (A22 unchanged)
-      __syncthreads();
-      if (tid < 32) {
-        const double *cn = A + (int64_t)(k + 1) * m;
-        double a = 0;
-        for (int i = k + 3 + lane; i < m; i += 32) a = fma(cn[i], cn[i], a);
-        a = warp_sum(a);
-        if (lane == 0) s_s2 = a;
-      }
-      __syncthreads();
-      continue;
-    }
-    const double beta = -copysign(sqrt(x0 * x0 + s2), x0);
-    const double tk = (beta - x0) * frcp(beta);
-    const double scal = frcp(x0 - beta);
-    for (int i = tid; i < L; i += blockDim.x) {
-      double v = (i == 0) ? 1.0 : colk[i] * scal;
-      vt[i] = v;
-      colk[i] = v;
     }
     if (tid == 0) {
       tau[k] = tk;
       e[k] = beta;
     }
-    __syncthreads();
+    __syncthreads();                                              // (1) v visible
     if (t.dbg && tid == 0) { long long tn = clock64(); tph[0] += tn - tprev; tprev = tn; }
-    // p_i = tk * sum_j A22(i, j) v_j : thread (g, i) sums j = g, g+4, ... (4 groups)
-    double *A22 = A + (int64_t)(k + 1) * m + (k + 1);
     double pvp = 0;
-    for (int i0 = 0; i0 < L; i0 += 128) {
-      const int i = i0 + (tid & 127), g = tid >> 7;
-      double acc0 = 0, acc1 = 0;
-      if (i < L) {
-        for (int jb = g; jb < L; jb += 32) {
-#pragma unroll
-          for (int u = 0; u < 8; u += 2) {
-            const int j0 = jb + 4 * u, j1 = j0 + 4;
-            const double a0 = (j0 < L) ? A22[i + (int64_t)j0 * m] : 0.0;
-            const double b0 = (j0 < L) ? vt[j0] : 0.0;
-            const double a1 = (j1 < L) ? A22[i + (int64_t)j1 * m] : 0.0;
-            const double b1 = (j1 < L) ? vt[j1] : 0.0;
-            acc0 = fma(a0, b0, acc0);
-            acc1 = fma(a1, b1, acc1);
-          }
+    if (refl) {
+      for (int i = tid; i < L; i += blockDim.x) {
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        int j = 0;
+        for (; j + 3 < L; j += 4) {
+          a0 = fma(A22[i + (int64_t)j * m], vt[j], a0);
+          a1 = fma(A22[i + (int64_t)(j + 1) * m], vt[j + 1], a1);
+          a2 = fma(A22[i + (int64_t)(j + 2) * m], vt[j + 2], a2);
+          a3 = fma(A22[i + (int64_t)(j + 3) * m], vt[j + 3], a3);
         }
-      }
-      lam[tid] = acc0 + acc1;   // lam[] is free scratch until phase 2 (>= blockDim doubles)
-      __syncthreads();
-      if (t.dbg && tid == 0) { long long tn = clock64(); tph[1] += tn - tprev; tprev = tn; }
-      if (g == 0 && i < L) {
-        double pi = (lam[tid] + lam[tid + 128]) + (lam[tid + 256] + lam[tid + 384]);
-        pi *= tk;
+        for (; j < L; ++j) a0 = fma(A22[i + (int64_t)j * m], vt[j], a0);
+        const double pi = tk * ((a0 + a1) + (a2 + a3));
         pw[i] = pi;
         pvp = fma(pi, vt[i], pvp);
       }
-      __syncthreads();
     }
-    // pv = sum p_i v_i (block reduction)
-    if (t.dbg && tid == 0) { long long tn = clock64(); tph[2] += tn - tprev; tprev = tn; }
     pvp = warp_sum(pvp);
     if (lane == 0) s_red[warp] = pvp;
-    __syncthreads();
-    if (t.dbg && tid == 0) { long long tn = clock64(); tph[3] += tn - tprev; tprev = tn; }
-    double pv = 0;
-#pragma unroll
-    for (int w = 0; w < 16; ++w) pv += s_red[w];
-    const double alpha = -0.5 * tk * pv;   // w = p + alpha v
-    // rank-2 update A22 -= v w^T + w v^T (w formed on the fly);
-    // warp 0 (column j = 0 of A22 = column k+1) also forms the squared norm of
-    // the next Householder column (rows k+3..)
-    for (int j = warp; j < L; j += nw) {
-      const double vj = vt[j], pj = pw[j];
-      const double wj = fma(alpha, vj, pj);
-      double *cj = A22 + (int64_t)j * m;
-      double a = 0;
-      for (int i = lane; i < L; i += 32) {
-        const double vi = vt[i], pi = pw[i];
-        const double wi = fma(alpha, vi, pi);           // w = p + alpha v
-        const double nv = cj[i] - fma(vi, wj, wi * vj);
-        cj[i] = nv;
-        if (j == 0 && i >= 2) a = fma(nv, nv, a);
+    __syncthreads();                                              // (2) p, partials visible
+    if (t.dbg && tid == 0) { long long tn = clock64(); tph[1] += tn - tprev; tprev = tn; }
+    double nxt = 0;
+    if (refl) {
+      double pv = 0;
+      for (int w = 0; w < nw; ++w) pv += s_red[w];
+      const double alpha = -0.5 * tk * pv;
+      for (int i = tid; i < L; i += blockDim.x) {
+        const double vi = vt[i], wi = fma(alpha, vi, pw[i]);
+        int j = 0;
+        for (; j + 1 < L; j += 2) {
+          const double vj0 = vt[j], wj0 = fma(alpha, vj0, pw[j]);
+          const double vj1 = vt[j + 1], wj1 = fma(alpha, vj1, pw[j + 1]);
+          double *c0 = A22 + i + (int64_t)j * m, *c1 = c0 + m;
+          *c0 -= fma(vi, wj0, wi * vj0);
+          *c1 -= fma(vi, wj1, wi * vj1);
+        }
+        if (j < L) {
+          const double vj0 = vt[j], wj0 = fma(alpha, vj0, pw[j]);
+          A22[i + (int64_t)j * m] -= fma(vi, wj0, wi * vj0);
+        }
+        if (i >= 2) nxt = fma(A22[i], A22[i], nxt);   // column 0 of A22 = next column
       }
-      if (j == 0) {
-        a = warp_sum(a);
-        if (lane == 0) s_s2 = a;
-      }
+    } else {
+      for (int i = 2 + tid; i < L; i += blockDim.x) nxt = fma(A22[i], A22[i], nxt);
     }
-    __syncthreads();
-    if (t.dbg && tid == 0) { long long tn = clock64(); tph[4] += tn - tprev; tprev = tn; }
+    nxt = warp_sum(nxt);
+    if (lane == 0) s_red2[warp] = nxt;   // read by every thread at the next step's start
+    __syncthreads();                                              // (3) A22, partials
+    if (t.dbg && tid == 0) { long long tn = clock64(); tph[2] += tn - tprev; tprev = tn; }
   }
-  if (t.dbg && tid == 0) for (int q = 0; q < 5; ++q) t.dbg[5 + q] = tph[q];
+  if (t.dbg && tid == 0) for (int q = 0; q < 3; ++q) t.dbg[5 + q] = tph[q];
   for (int i = tid; i < m; i += blockDim.x) d[i] = A[i + (int64_t)i * m];
   if (tid == 0) {
     if (m >= 2) e[m - 2] = A[(m - 1) + (int64_t)(m - 2) * m];
@@ -558,6 +679,7 @@ __global__ void __launch_bounds__(512, 1) k_eig(const EigTask *__restrict__ task
     tau[m - 1] = 0.0;
   }
   __syncthreads();
+  }
   if (t.dbg && tid == 0) t.dbg[1] = clock64();
   // ---- 2. eigenvalues (Sturm multisection) ----
   double gl = 1e300, gu = -1e300, emax2 = 0;
@@ -651,8 +773,10 @@ __global__ void __launch_bounds__(512, 1) k_eig(const EigTask *__restrict__ task
   // kept vectors leaves the kept subspace unchanged.
   const double pertol = 10.0 * 2.2e-16 * bnorm;
   for (int k = tid; k < r; k += blockDim.x) {
-    double *DL = scr + (int64_t)k * 6 * m, *D = DL + m, *DU = D + m, *DU2 = DU + m, *b = DU2 + m,
-           *piv = b + m;
+    // interleaved scratch: element i of vector k at [i * r + k] (coalesced across threads)
+    const int64_t RR = r;
+    double *DL = scr + k, *D = DL + m * RR, *DU = D + m * RR, *DU2 = DU + m * RR, *b = DU2 + m * RR,
+           *piv = b + m * RR;
     double sft = lam[k];
     for (int q = 1; q <= k && lam[k - q] - lam[k] < pertol; ++q) sft -= pertol;
     // dgttrf on T - sft I with the running pivot row carried in registers
@@ -665,19 +789,19 @@ __global__ void __launch_bounds__(512, 1) k_eig(const EigTask *__restrict__ task
       if (fabs(Di) >= fabs(DLi)) {
         if (Di == 0.0) Di = pertol;
         const double f = DLi * frcp(Di);
-        D[i] = Di;
-        DL[i] = f;
-        DU[i] = DUi;
-        DU2[i] = 0.0;
-        piv[i] = 0.0;
+        D[(i) * RR] = Di;
+        DL[(i) * RR] = f;
+        DU[(i) * RR] = DUi;
+        DU2[(i) * RR] = 0.0;
+        piv[(i) * RR] = 0.0;
         Dn = fma(-f, DUi, Dn);
       } else {
         const double f = Di * frcp(DLi);
-        D[i] = DLi;
-        DL[i] = f;
-        DU[i] = Dn;
-        DU2[i] = DUn;
-        piv[i] = 1.0;
+        D[(i) * RR] = DLi;
+        DL[(i) * RR] = f;
+        DU[(i) * RR] = Dn;
+        DU2[(i) * RR] = DUn;
+        piv[(i) * RR] = 1.0;
         const double nd = fma(-f, Dn, DUi);
         DUn = -f * DUn;
         Dn = nd;
@@ -685,52 +809,52 @@ __global__ void __launch_bounds__(512, 1) k_eig(const EigTask *__restrict__ task
       Di = Dn;
       DUi = DUn;
     }
-    D[m - 1] = Di;
+    D[(m - 1) * RR] = Di;
     for (int i = 0; i < m; ++i) {        // keep pivots away from 0, store reciprocals
-      double v = D[i];
+      double v = D[(i) * RR];
       if (fabs(v) < pertol) v = copysign(pertol, v == 0.0 ? 1.0 : v);
-      D[i] = frcp(v);
+      D[(i) * RR] = frcp(v);
     }
-    for (int i = 0; i < m; ++i) b[i] = 1.0 + 0.5 * sin(0.7 * i + 1.3 * k + 0.1);
+    for (int i = 0; i < m; ++i) b[(i) * RR] = 1.0 + 0.5 * (double)((i * 7919u + k * 104729u + 13u) % 1024u) * (1.0 / 1024.0);
     for (int it = 0; it < 3; ++it) {
       // forward (row interchanges + unit lower)
-      double bi = b[0];
+      double bi = b[(0) * RR];
 #pragma unroll 4
       for (int i = 0; i < m - 1; ++i) {
-        const double bn = b[i + 1];
-        if (piv[i] == 0.0) {
-          b[i] = bi;
-          bi = fma(-DL[i], bi, bn);
+        const double bn = b[(i + 1) * RR];
+        if (piv[(i) * RR] == 0.0) {
+          b[(i) * RR] = bi;
+          bi = fma(-DL[(i) * RR], bi, bn);
         } else {
-          b[i] = bn;
-          bi = fma(-DL[i], bn, bi);
+          b[(i) * RR] = bn;
+          bi = fma(-DL[(i) * RR], bn, bi);
         }
       }
-      b[m - 1] = bi;
+      b[(m - 1) * RR] = bi;
       // backward (upper with two super-diagonals), carries x_{i+1}, x_{i+2}
-      double x1 = b[m - 1] * D[m - 1];
-      b[m - 1] = x1;
+      double x1 = b[(m - 1) * RR] * D[(m - 1) * RR];
+      b[(m - 1) * RR] = x1;
       double nrm = x1 * x1, x2 = 0.0;
       if (m >= 2) {
-        const double x0 = (b[m - 2] - DU[m - 2] * x1) * D[m - 2];
-        b[m - 2] = x0;
+        const double x0 = (b[(m - 2) * RR] - DU[(m - 2) * RR] * x1) * D[(m - 2) * RR];
+        b[(m - 2) * RR] = x0;
         nrm = fma(x0, x0, nrm);
         x2 = x1;
         x1 = x0;
       }
 #pragma unroll 4
       for (int i = m - 3; i >= 0; --i) {
-        const double x0 = (b[i] - DU[i] * x1 - DU2[i] * x2) * D[i];
-        b[i] = x0;
+        const double x0 = (b[(i) * RR] - DU[(i) * RR] * x1 - DU2[(i) * RR] * x2) * D[(i) * RR];
+        b[(i) * RR] = x0;
         nrm = fma(x0, x0, nrm);
         x2 = x1;
         x1 = x0;
       }
       nrm = frcp(sqrt(nrm));
-      for (int i = 0; i < m; ++i) b[i] *= nrm;
+      for (int i = 0; i < m; ++i) b[(i) * RR] *= nrm;
     }
     double *z = t.V + (int64_t)k * m;
-    for (int i = 0; i < m; ++i) z[i] = b[i];
+    for (int i = 0; i < m; ++i) z[i] = b[(i) * RR];
   }
   __syncthreads();
   // modified Gram-Schmidt over the r vectors (warps over later vectors)
@@ -801,6 +925,8 @@ __global__ void __launch_bounds__(512, 1) k_eig(const EigTask *__restrict__ task
 }
 
 // ----------------------------------------------------------------- pivot ----
+// (k_eig_t<true> for m <= 128, k_eig_t<false> otherwise)
+
 // Fused pivot of (s, b): K = [[S, V], [V^T, 0]] (n = m + r) factored as
 // K = L D L^T with D = diag(I_m, -I_r) (Cholesky of S, then of
 // W = V^T S^{-1} V for the black node, P:l.396-399), then overwritten by

@@ -293,7 +293,8 @@ void ensure_mem(lorasp_ctx *h) {
   h->d_dotpart.ensure((DOT_BLOCKS + 64) * sizeof(double), h->stream);
   h->stg.init(size_t(64) << 20, h->stream);
   CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-  CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
@@ -316,6 +317,35 @@ void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::v
   tend(h, ev, flops, bytes);
   ++h->launches_factor;
   CK(cudaGetLastError());
+}
+
+// eigen tasks: m <= 128 -> register-tile kernel (512 threads), else the generic one
+// eigen tasks: 64 < m <= 128 -> register-tile kernel (512 threads); otherwise
+// the generic shared/global-memory kernel (faster for small m, measured with
+// tools/eig_cmp.py)
+static const int EIG_REG_MIN = 65;
+
+void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int max_m, int cap) {
+  std::vector<EigTask> small, big;
+  for (const EigTask &e : et) ((e.m >= EIG_REG_MIN && e.m <= EIG_REG_M) ? small : big).push_back(e);
+  if (!small.empty()) {
+    EigTask *ds = big.empty() ? de : push(h, small);
+    int m1 = 0;
+    for (auto &e : small) m1 = std::max(m1, e.m);
+    size_t sm = (size_t)(6 * (m1 + 8) + 512 + (int64_t)m1 * m1) * 8;
+    k_eig_t<true><<<(unsigned)small.size(), EIG_REG_THREADS, sm, h->stream>>>(ds, h->plan.eps, (int)(sm / 8),
+                                                                               h->d_status.as<int>());
+    ++h->launches_factor;
+    CK(cudaGetLastError());
+  }
+  if (!big.empty()) {
+    EigTask *db = small.empty() ? de : push(h, big);
+    k_eig_t<false><<<(unsigned)big.size(), EIG_THREADS, cap * 8, h->stream>>>(db, h->plan.eps, cap,
+                                                                             h->d_status.as<int>());
+    ++h->launches_factor;
+    CK(cudaGetLastError());
+  }
+  (void)max_m;
 }
 
 void launch_copy(lorasp_ctx *h, const std::vector<CopyTask> &tasks, int cls) {
@@ -701,7 +731,28 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
         cap = std::max(cap, 6 * (max_m + 8) + std::max(max_m, 512));
         int ev = tbeg(h, K_JACOBI);
-        k_eig<<<(unsigned)et.size(), 512, cap * 8, st>>>(de, pl.eps, cap, h->d_status.as<int>());
+        cudaEvent_t dbg_e0 = nullptr, dbg_e1 = nullptr;
+        if (h->debug) {
+          cudaEventCreate(&dbg_e0);
+          cudaEventCreate(&dbg_e1);
+          cudaEventRecord(dbg_e0, st);
+        }
+        launch_eig(h, et, de, max_m, cap);
+        if (h->debug) {
+          cudaEventRecord(dbg_e1, st);
+          cudaEventSynchronize(dbg_e1);
+          float ms = 0;
+          cudaEventElapsedTime(&ms, dbg_e0, dbg_e1);
+          int mmin = 1 << 30, mmax = 0;
+          for (auto &e : et) {
+            mmin = std::min(mmin, e.m);
+            mmax = std::max(mmax, e.m);
+          }
+          fprintf(stderr, "[lorasp] level %d wave %zu eig: %zu tasks m in [%d, %d]: %.3f ms\n", i, w, et.size(), mmin,
+                  mmax, ms);
+          cudaEventDestroy(dbg_e0);
+          cudaEventDestroy(dbg_e1);
+        }
         tend(h, ev, f_eig, b_eig);
         ++h->launches_factor;
         CK(cudaGetLastError());
@@ -1491,7 +1542,8 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
   try {
     CK(cudaSetDevice(device));
     CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-    CK(cudaFuncSetAttribute(k_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+    CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
     double *dG, *dV, *dS, *dW;
     int *dr, *dst;
     size_t mm = (size_t)m * m;
@@ -1528,7 +1580,10 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     } else {
       int cap = (int)std::min<int64_t>((int64_t)m * m + 6 * (m + 8) + std::max(m, 512), SMEM_LIMIT / 8);
       cap = std::max(cap, 6 * (m + 8) + std::max(m, 512));
-      k_eig<<<1, 512, cap * 8>>>(de, eps, cap, dst);
+      if (m >= EIG_REG_MIN && m <= EIG_REG_M && !getenv("LORASP_EIG_GENERIC"))
+        k_eig_t<true><<<1, EIG_REG_THREADS, cap * 8>>>(de, eps, cap, dst);
+      else
+        k_eig_t<false><<<1, EIG_THREADS, cap * 8>>>(de, eps, cap, dst);
     }
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
@@ -1540,8 +1595,7 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     if (ddbg) {
       long long tt[10];
       CK(cudaMemcpy(tt, ddbg, sizeof(tt), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[tridiag phases] vscale %lld  partials %lld  combine %lld  pvred %lld  update %lld\n",
-              tt[5], tt[6], tt[7], tt[8], tt[9]);
+      fprintf(stderr, "[tridiag phases] v %lld  matvec %lld  update %lld\n", tt[5], tt[6], tt[7]);
       fprintf(stderr, "[eig m=%d r=%d] tridiag %lld  eigvals %lld  invit %lld  backtr %lld cycles\n", m, *rank,
               tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3]);
       cudaFree(ddbg);
@@ -1549,6 +1603,7 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     cudaFree(dG); cudaFree(dV); cudaFree(dS); cudaFree(dW); cudaFree(dr); cudaFree(de);
     return st[0];
   } catch (const Err &e) {
+    fprintf(stderr, "lorasp_test_eig: %s\n", e.msg.c_str());
     return e.code;
   }
 }
