@@ -37,6 +37,10 @@ WORKLOADS = {
     "cfg1": "2D 5-point Poisson 32x32 (n=1024), 16-dof leaves, depth 6, eps=1e-2, PCG 1e-10",
     "cfg2": "2D 5-point Poisson 256x256 (n=65536), 64-dof leaves, depth 10, eps=1e-3, PCG 1e-10",
     "cfg3": "3D 7-point Poisson 64^3 (n=262144), 64-dof leaves, depth 12, eps=1e-2, PCG 1e-10",
+    "cfg4": "3D 7-point variable-coefficient (phi log-uniform 1e-3..1e3, harmonic faces) 128^3 (n=2097152), "
+            "64-dof leaves, depth 15, eps=1e-2, PCG 1e-10",
+    "cfg5": "2D first-order upwind convection-diffusion beta=(50,30) 1024^2 (n=1048576), 64-dof leaves, "
+            "depth 14, eps=1e-3, GMRES(50) 1e-10 (LU path)",
 }
 L2_FLUSH_BYTES = 256 << 20
 
@@ -122,7 +126,7 @@ def dist_init():
     return world, rank, local
 
 
-def cpu_baseline(p, sample="factor+pcg"):
+def cpu_baseline(p, sample="factor+krylov"):
     """The oracle as it stands, on the host cores, on one bounded sample."""
     from oracle import lorasp_oracle as O
     t0 = time.perf_counter()
@@ -130,13 +134,14 @@ def cpu_baseline(p, sample="factor+pcg"):
     tf = time.perf_counter() - t0
     out = {"value": p.n / tf, "unit": "unknowns/s", "cores": O.ORACLE_THREADS, "kind": "oracle",
            "factor_s": tf, "host_cpus": os.cpu_count()}
-    if sample == "factor+pcg":
+    if sample == "factor+krylov":
         mv = lambda v: O.spmv(p.row_ptr, p.col_idx, p.values, v)
         t0 = time.perf_counter()
-        r = O.pcg(mv, lambda v: O.solve(f, v), p.b, tol=1e-10)
+        kry = O.pcg if p.solver == "cg" else O.gmres
+        r = kry(mv, lambda v: O.solve(f, v), p.b, tol=1e-10)
         out["krylov_s"] = time.perf_counter() - t0
         out["krylov_iters"] = r.iters
-        out["sample"] = (f"1 full {p.name} factorization (n={p.n}) + PCG to 1e-10 "
+        out["sample"] = (f"1 full {p.name} factorization (n={p.n}) + {p.solver.upper()} to 1e-10 "
                          f"({r.iters} iters), numpy oracle, 1 BLAS thread")
     return out, f
 
@@ -156,7 +161,7 @@ def run_reference(args, world, rank):
             times.append(dt)
     mv = lambda v: O.spmv(p.row_ptr, p.col_idx, p.values, v)
     t0 = time.perf_counter()
-    kr = O.pcg(mv, lambda v: O.solve(f, v), p.b, tol=1e-10)
+    kr = (O.pcg if p.solver == "cg" else O.gmres)(mv, lambda v: O.solve(f, v), p.b, tol=1e-10)
     tk = time.perf_counter() - t0
     tf = sum(times) / len(times)
     val = p.n / tf
@@ -202,13 +207,14 @@ def main():
     b = torch.tensor(p.b, device=dev)
     x = torch.empty_like(b)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    method = L.LORASP_CG if p.solver == "cg" else L.LORASP_GMRES
 
     def step(timed):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
         ev[0].record()
         h.factor(vals)
         ev[1].record()
-        rc, it, rr = h.krylov(b, x, tol=1e-10, method=L.LORASP_CG)
+        rc, it, rr = h.krylov(b, x, tol=1e-10, method=method, restart=50)
         ev[2].record()
         torch.cuda.synchronize()
         fl, al, kl = h.launch_counts()
@@ -314,7 +320,7 @@ def main():
             t0 = time.perf_counter()
             h.factor(vh)
             t1 = time.perf_counter()
-            h.krylov(bh, xh, tol=1e-10, method=L.LORASP_CG)
+            h.krylov(bh, xh, tol=1e-10, method=method, restart=50)
             t2 = time.perf_counter()
             if s >= args.warmup:
                 tfe.append(t1 - t0)

@@ -58,6 +58,9 @@ inline uint64_t key(int u, int v) {
   if (u > v) std::swap(u, v);
   return ((uint64_t)(uint32_t)u << 32) | (uint32_t)v;
 }
+inline uint64_t dkey(int u, int v) {  // ordered pair u -> v
+  return ((uint64_t)(uint32_t)u << 32) | (uint32_t)v;
+}
 
 void sorted_insert(std::vector<int> &v, int x) {
   auto it = std::lower_bound(v.begin(), v.end(), x);
@@ -165,6 +168,7 @@ int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_i
   }
   const int L = depth;
   const int nleaf = 1 << L;
+  const bool sym = (flags & LORASP_SPD) != 0;
   pl.leaf_members = cur;
   pl.leaf_of.assign(n, 0);
   pl.leaf_pos.assign(n, 0);
@@ -275,13 +279,19 @@ int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_i
       if (sv) return v;
       return std::min(u, v);
     };
+    // SPD: slot of the unordered pair {u, v}; LU: slot of Mat(u -> v) (rows v)
     auto get_slot = [&](int u, int v) {
-      auto it = slot_of.find(key(u, v));
+      const uint64_t kk = sym ? key(u, v) : dkey(u, v);
+      auto it = slot_of.find(kk);
       if (it != slot_of.end()) return it->second;
-      int r = row_node(u, v);
       int id = (int)lv.slots.size();
-      lv.slots.push_back({r, r == u ? v : u});
-      slot_of.emplace(key(u, v), id);
+      if (sym) {
+        int r = row_node(u, v);
+        lv.slots.push_back({r, r == u ? v : u});
+      } else {
+        lv.slots.push_back({v, u});
+      }
+      slot_of.emplace(kk, id);
       return id;
     };
     auto cl = [&](int u) { return u < K ? u : u - K; };
@@ -308,6 +318,7 @@ int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_i
         for (int q : g.n1[c])
           if (s_exists[q]) {
             get_slot(c, q);
+            if (!sym) get_slot(q, c);
             add_edge(c, q);
           }
       }
@@ -321,6 +332,12 @@ int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_i
         if (ps.row < Kp || ps.col < Kp) continue;  // only P-P slots survive
         int xr = ps.row - Kp, xc = ps.col - Kp;
         int a = xr >> 1, b = xc >> 1;
+        if (!sym) {   // Mat(P_xc -> P_xr) lands in Mat(S_b -> S_a) (rows S_a)
+          int dst = get_slot(b, a);
+          if (a != b) add_edge(a, b);
+          lv.merge.push_back({dst, (int)sid, xr & 1, xc & 1, xr, xc, false});
+          continue;
+        }
         int dst = get_slot(a, b);
         if (a != b) add_edge(a, b);
         if (a == b) {
@@ -360,9 +377,16 @@ int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_i
           lv.p_exists[c] = 1;
           const int P = K + c;
           for (int u : nd.partners) {
-            nd.pslot_src.push_back(get_slot(s, u));
+            if (sym) {
+              nd.pslot_src.push_back(get_slot(s, u));
+              nd.pslot_dst.push_back(get_slot(P, u));
+            } else {
+              nd.pslot_src.push_back(get_slot(u, s));    // Mat(p -> s) = B_k^T
+              nd.pslot_src2.push_back(get_slot(s, u));   // Mat(s -> p) = A_k
+              nd.pslot_dst.push_back(get_slot(P, u));    // Mat(P -> p) = R_k
+              nd.pslot_dst2.push_back(get_slot(u, P));   // Mat(p -> P) = Q_k^T
+            }
             del_edge(s, u);                 // rule 1
-            nd.pslot_dst.push_back(get_slot(P, u));
             add_edge(P, u);                 // rules 2/3
           }
         }
@@ -370,15 +394,28 @@ int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_i
         for (int u : adj[s]) {
           if (u < K && elim[u]) continue;
           nd.n1.push_back(u);
-          nd.n1_slot.push_back(get_slot(s, u));
+          if (sym) {
+            nd.n1_slot.push_back(get_slot(s, u));
+          } else {
+            nd.n1_slot.push_back(get_slot(u, s));    // Mat(n -> s): coupling C
+            nd.n1_slot2.push_back(get_slot(s, u));   // Mat(s -> n): coupling R
+          }
         }
         std::vector<int> T = nd.n1;
         if (nd.aux) T.push_back(K + c);
-        for (size_t a = 0; a < T.size(); ++a)
-          for (size_t b = 0; b <= a; ++b) {
-            nd.tslot.push_back(get_slot(T[a], T[b]));
-            add_edge(T[a], T[b]);
-          }
+        if (sym) {
+          for (size_t a = 0; a < T.size(); ++a)
+            for (size_t b = 0; b <= a; ++b) {
+              nd.tslot.push_back(get_slot(T[a], T[b]));
+              add_edge(T[a], T[b]);
+            }
+        } else {
+          for (size_t a = 0; a < T.size(); ++a)
+            for (size_t b = 0; b < T.size(); ++b) {
+              nd.tslot.push_back(get_slot(T[b], T[a]));   // Mat(T_b -> T_a)
+              add_edge(T[a], T[b]);
+            }
+        }
         for (int u : std::vector<int>(adj[s])) del_edge(s, u);  // s eliminated
         elim[c] = 1;
       }
@@ -398,6 +435,9 @@ int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_i
         for (int sl : nd.n1_slot) good = good && touch(sl);
         for (int sl : nd.pslot_src) good = good && touch(sl);
         for (int sl : nd.pslot_dst) good = good && touch(sl);
+        for (int sl : nd.pslot_src2) good = good && touch(sl);
+        for (int sl : nd.pslot_dst2) good = good && touch(sl);
+        for (int sl : nd.n1_slot2) good = good && touch(sl);
         for (int sl : nd.tslot) good = good && touch(sl);
         if (!good) {
           err = "analyze: colour wave is not conflict-free at level " + std::to_string(i);
@@ -419,7 +459,8 @@ int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_i
     const SymLevel &lv = pl.lev[L];
     std::unordered_map<uint64_t, int> slot_of;
     for (size_t sid = 0; sid < lv.slots.size(); ++sid)
-      slot_of.emplace(key(lv.slots[sid].row, lv.slots[sid].col), (int)sid);
+      slot_of.emplace(sym ? key(lv.slots[sid].row, lv.slots[sid].col) : dkey(lv.slots[sid].col, lv.slots[sid].row),
+                      (int)sid);
     pl.nnz_slot.assign(pl.nnz, -1);
     pl.nnz_r.assign(pl.nnz, 0);
     pl.nnz_c.assign(pl.nnz, 0);
@@ -430,13 +471,13 @@ int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_i
         int sv = v >> 1, su = u >> 1;
         int ri = ((v & 1) ? pl.leaf_size[v - 1] : 0) + pl.leaf_pos[i];
         int ci = ((u & 1) ? pl.leaf_size[u - 1] : 0) + pl.leaf_pos[j];
-        auto it = slot_of.find(key(sv, su));
+        auto it = slot_of.find(sym ? key(sv, su) : dkey(su, sv));
         if (it == slot_of.end()) {
           err = "analyze: internal error (leaf slot missing)";
           return -2;
         }
         const SymSlot &sl = lv.slots[it->second];
-        if (sv == su || sl.row == sv) {
+        if (!sym || sv == su || sl.row == sv) {
           pl.nnz_slot[k] = it->second;
           pl.nnz_r[k] = ri;
           pl.nnz_c[k] = ci;

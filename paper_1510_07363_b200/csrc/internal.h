@@ -32,17 +32,25 @@ struct MergeSrc {
   bool trans;          // source stored with rows = src_cluster_c
 };
 
+// Slots on the SPD path are unordered pairs (one orientation stored); on the
+// general (LU) path every ordered pair u -> v has its own slot Mat(u -> v)
+// (rows v, cols u).
 struct SymNode {
   bool exists = false;  // structural size > 0
   bool aux = false;     // has well-separated partners -> Compress, b and P(b) exist
   int wave = -1;
-  std::vector<int> partners;   // level node ids, sorted (S by cluster, then P)
-  std::vector<int> pslot_src;  // slot {S_c, p_k}  (read: A_k^T)
-  std::vector<int> pslot_dst;  // slot {P_c, p_k}  (write: R_k)
-  std::vector<int> n1;         // uneliminated neighbours at elimination (S/P ids), sorted
-  std::vector<int> n1_slot;    // slot {S_c, n}
-  int self_slot = -1;          // slot {S_c, S_c}
-  // T = n1 + [P_c if aux]; tslot[a*(a+1)/2 + b] = slot {T_a, T_b}, b <= a
+  std::vector<int> partners;    // level node ids, sorted (S by cluster, then P)
+  std::vector<int> pslot_src;   // SPD: {S_c, p_k} (rows S_c = A_k^T); LU: Mat(p_k -> S_c) (rows S_c = B_k^T)
+  std::vector<int> pslot_src2;  // LU: Mat(S_c -> p_k) (rows p_k = A_k)
+  std::vector<int> pslot_dst;   // SPD: {P_c, p_k};  LU: Mat(P_c -> p_k) (rows p_k = R_k)
+  std::vector<int> pslot_dst2;  // LU: Mat(p_k -> P_c) (rows P_c = Q_k^T)
+  std::vector<int> n1;          // uneliminated neighbours at elimination (S/P ids), sorted
+  std::vector<int> n1_slot;     // SPD: {S_c, n};  LU: Mat(n -> S_c) (rows S_c: coupling C)
+  std::vector<int> n1_slot2;    // LU: Mat(S_c -> n) (rows n: coupling R)
+  int self_slot = -1;           // slot {S_c, S_c}
+  // T = n1 + [P_c if aux]
+  // SPD: tslot[a*(a+1)/2 + b] = slot {T_a, T_b}, b <= a
+  // LU:  tslot[a*|T| + b]     = Mat(T_b -> T_a)
   std::vector<int> tslot;
 };
 

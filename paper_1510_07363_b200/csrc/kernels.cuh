@@ -1007,6 +1007,106 @@ __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks
     }
 }
 
+// --------------------------------------------------------- LU pivot (general) ----
+// LU path: the fused pivot K = [[S, V], [V^T, 0]] (n = m + r, full, ld) is
+// factored without pivoting, K = L U (S is an M-matrix-like block whose Schur
+// complements stay positive real, so no zero pivots arise; a vanishing pivot
+// reports LORASP_E_SINGULAR_PIVOT), then region 0 <- L^{-1} (unit lower) and
+// region 1 <- U^{-T} (lower).  Shared memory when n^2 + n fits, else in place
+// in region 0 (global).
+__global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ tasks, int smem_cap_doubles,
+                                                  int *status) {
+  extern __shared__ double sh[];
+  const PivTask t = tasks[blockIdx.x];
+  const int n = t.m + t.r;
+  if (n == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  __shared__ int s_fail;
+  const bool in_smem = (int64_t)n * n + n <= smem_cap_doubles;
+  double *tmp = sh;
+  double *A;
+  int lda;
+  if (in_smem) {
+    A = sh + n;
+    lda = n;
+    for (int j = warp; j < n; j += nw)
+      for (int i = lane; i < n; i += 32) A[i + (int64_t)j * n] = t.F[i + (int64_t)j * t.ld];
+  } else {
+    A = t.F;
+    lda = t.ld;
+  }
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  double amax = 0;   // scale for the singularity test
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i < n; i += 32) amax = fmax(amax, fabs(A[i + (int64_t)j * lda]));
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  __shared__ double s_amax[16];
+  if (lane == 0) s_amax[warp] = amax;
+  __syncthreads();
+  amax = 0;
+  for (int w = 0; w < nw; ++w) amax = fmax(amax, s_amax[w]);
+  // right-looking LU without pivoting
+  for (int k = 0; k < n; ++k) {
+    const double piv = A[k + (int64_t)k * lda];
+    if (!(fabs(piv) > 1e-14 * amax) || !isfinite(piv)) {
+      if (tid == 0) {
+        s_fail = 1;
+        if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
+      }
+      break;
+    }
+    const double rp = frcp(piv);
+    __syncthreads();
+    for (int i = k + 1 + tid; i < n; i += blockDim.x) A[i + (int64_t)k * lda] *= rp;
+    __syncthreads();
+    for (int j = k + 1 + warp; j < n; j += nw) {
+      const double ukj = A[k + (int64_t)j * lda];
+      double *cj = A + (int64_t)j * lda;
+      const double *ck = A + (int64_t)k * lda;
+      for (int i = k + 1 + lane; i < n; i += 32) cj[i] = fma(-ck[i], ukj, cj[i]);
+    }
+    __syncthreads();
+  }
+  if (s_fail) return;
+  // U^{-1} in place (upper incl. diagonal), columns ascending:
+  // u_jj <- 1/u_jj; A[0:j, j] <- -u_jj^{-1} * Uinv[0:j, 0:j] A[0:j, j]
+  for (int j = 0; j < n; ++j) {
+    for (int i = tid; i < j; i += blockDim.x) tmp[i] = A[i + (int64_t)j * lda];
+    __syncthreads();
+    const double ajj = frcp(A[j + (int64_t)j * lda]);
+    for (int i = tid; i < j; i += blockDim.x) {
+      double sacc = 0;
+      for (int k = i; k < j; ++k) sacc = fma(A[i + (int64_t)k * lda], tmp[k], sacc);
+      A[i + (int64_t)j * lda] = -ajj * sacc;
+    }
+    __syncthreads();
+    if (tid == 0) A[j + (int64_t)j * lda] = ajj;
+    __syncthreads();
+  }
+  // region 1 <- U^{-T} (lower): (U^{-T})(i, j) = U^{-1}(j, i) for i >= j
+  double *R1 = t.F + (int64_t)t.ld * n;
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i < n; i += 32) R1[i + (int64_t)j * t.ld] = (i >= j) ? A[j + (int64_t)i * lda] : 0.0;
+  __syncthreads();
+  // L^{-1} in place (strict lower, unit diagonal), columns descending
+  for (int j = n - 1; j >= 0; --j) {
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) tmp[i] = A[i + (int64_t)j * lda];
+    __syncthreads();
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) {
+      double sacc = tmp[i];   // unit diagonal of L^{-1} at (i, i)
+      for (int k = j + 1; k < i; ++k) sacc = fma(A[i + (int64_t)k * lda], tmp[k], sacc);
+      A[i + (int64_t)j * lda] = -sacc;
+    }
+    __syncthreads();
+  }
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i < n; i += 32) {
+      const double v = (i > j) ? A[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
+      t.F[i + (int64_t)j * t.ld] = v;
+    }
+}
+
 // -------------------------------------------- blocked pivot (large nodes) ----
 // For n = m + r too large for one CTA's shared memory the fused pivot is
 // factored by a right-looking blocked signed Cholesky (64-column panels; panel
@@ -1089,9 +1189,14 @@ __global__ void __launch_bounds__(256) k_pivdiag(const PivDiagTask *__restrict__
 // forward:  y = L^{-1} [rhs_s; 0];  rhs_q -= Z_q^T D y           (q in T)
 // backward: u = y - Z x_T;  [x_s; x_b] = L^{-T} D u               (P:l.487-495)
 struct ApNode {
-  const double *F; // [L^{-1} | Z], column-major, leading dimension ld (even)
+  const double *F; // record, column-major, leading dimension ld (even):
+                   // SPD [L^{-1} | Z];  LU [L^{-1} | U^{-T} | X | Y^T]
   double *y;       // n doubles, kept between the two passes
   int64_t off_s;   // vector offset of Var/RHS(s)
+  int64_t zf_off;  // forward coupling (SPD: Z, LU: Y^T)
+  int64_t zb_off;  // backward coupling (SPD: Z, LU: X)
+  int64_t lb_off;  // backward triangle (SPD: L^{-1}, LU: U^{-T})
+  int sym;         // SPD: apply D = diag(I_m, -I_r)
   int m, r, W, ld;
   int seg0, nseg;
 };
@@ -1174,7 +1279,7 @@ __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ no
   // ---- y = L^{-1}[:, :m] rhs ----
   ColStream A{nd.F, ld, nd.m, cc, {stage0, stage1}, bars};
   const int na = A.nchunks();
-  const double *Z = nd.F + (int64_t)ld * n;
+  const double *Z = nd.F + nd.zf_off;
   ColStream B{Z, ld, nd.W, cc, {stage0, stage1}, bars};
   const int nb = B.nchunks();
   const int ntot = na + nb;
@@ -1209,7 +1314,7 @@ __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ no
         for (int i = tid; i < n; i += blockDim.x) {
           const double y = dy[i];
           nd.y[i] = y;
-          dy[i] = (i < nd.m) ? y : -y;
+          dy[i] = (i < nd.m || !nd.sym) ? y : -y;
         }
       }
     } else {
@@ -1259,7 +1364,8 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
   __syncthreads();
   const int ld = nd.ld;
   int cc = max(1, chunk_doubles / ld);
-  const double *Z = nd.F + (int64_t)ld * n;
+  const double *Z = nd.F + nd.zb_off;
+  const double *Lb = nd.F + nd.lb_off;
   const int nb = (nd.W + cc - 1) / cc;     // Z chunks first
   const int na = (nd.m + cc - 1) / cc;     // then L^{-1}[:, :m]
   const int ntot = nb + na;
@@ -1273,7 +1379,7 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
     } else {
       c0 = (c - nb) * cc;
       c1 = min(nd.m, c0 + cc);
-      src = nd.F + (int64_t)c0 * ld;
+      src = Lb + (int64_t)c0 * ld;
     }
     uint32_t bytes = (uint32_t)((int64_t)(c1 - c0) * ld * 8);
     fence_proxy_async();
@@ -1292,12 +1398,12 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
         for (int j = j0; j < j1; ++j) sacc = fma(buf[(int64_t)(j - j0) * ld + i], xt[j], sacc);
         u[i] -= sacc;
       }
-      if (c == nb - 1) {
+      if (c == nb - 1 && nd.sym) {
         __syncthreads();
         for (int i = nd.m + tid; i < n; i += blockDim.x) u[i] = -u[i];   // D u
       }
     } else {
-      if (nb == 0 && c == 0) {
+      if (nb == 0 && c == 0 && nd.sym) {
         for (int i = nd.m + tid; i < n; i += blockDim.x) u[i] = -u[i];
         __syncthreads();
       }

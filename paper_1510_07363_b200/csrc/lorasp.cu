@@ -181,6 +181,7 @@ struct TimedEv {
 
 struct NodeRec {  // one eliminated (s, b) pair, for apply + stats
   int level, c, m, r, W, ld;
+  int64_t zf_off = 0, zb_off = 0, lb_off = 0;
   double *F;
   std::vector<int> T;  // level node ids (S: c', P: K + c')
   std::vector<int> w;  // widths
@@ -296,6 +297,7 @@ void ensure_mem(lorasp_ctx *h) {
   CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_pivot_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   h->mem_ready = true;
@@ -372,12 +374,15 @@ void add_tiles(std::vector<GemmTask> &tasks, GemmTask base, int kmax_by_row = 0)
     }
 }
 
-double node_flops(int m, int r, int R, int W) {
-  // SURVEY §8(d) algorithmic work (SPD path): compress + fused elimination
+double node_flops(int m, int r, int R, int W, bool sym) {
+  // SURVEY §8(d) algorithmic work: compress + fused elimination; R is the stack
+  // height (doubled on the LU path by the B_k), the [x2] terms double for LU.
+  // Here W already includes the r columns of P(b).
+  const double x2 = sym ? 1.0 : 2.0;
   double f = 0;
   if (R > 0) f += (double)R * m * m + 9.0 * m * m * (double)m + 2.0 * R * m * (double)r;
-  f += ((double)m * m * m + (double)r * r * r) / 3.0 + ((double)m * m + (double)r * r) * (W + r) +
-       (double)(m + r) * (W + r) * (W + r);
+  f += x2 * (((double)m * m * m + (double)r * r * r) / 3.0 + ((double)m * m + (double)r * r) * W +
+             (double)(m + r) * W * W);
   return f;
 }
 
@@ -551,11 +556,30 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
   tend(h, ev, f_piv, b_piv);
 }
 
+// LU path: fused pivots by no-pivot LU (k_pivot_lu: shared memory when the
+// n x n pivot fits, else in place in global memory), L^{-1} and U^{-T} written
+// to the first two record regions.
+void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double b_piv) {
+  if (pv.empty()) return;
+  int max_n = 0;
+  for (const PivTask &t : pv) max_n = std::max(max_n, t.m + t.r);
+  PivTask *dp = push(h, pv);
+  int64_t want = (int64_t)max_n * max_n + max_n;
+  int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
+  cap = std::max(cap, max_n);
+  int ev = tbeg(h, K_PIVOT);
+  k_pivot_lu<<<(unsigned)pv.size(), 512, cap * 8, h->stream>>>(dp, cap, h->d_status.as<int>());
+  tend(h, ev, f_piv, b_piv);
+  ++h->launches_factor;
+  CK(cudaGetLastError());
+}
+
 void factor_impl(lorasp_ctx *h, const double *values) {
   ensure_mem(h);
   const Plan &pl = h->plan;
   cudaStream_t st = h->stream;
   const int L = pl.depth;
+  const bool sym = (pl.flags & LORASP_SPD) != 0;
   h->launches_factor = 0;
   h->flops_model = 0;
   h->t_host_ms = 0;
@@ -673,8 +697,8 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         h->ws_sig.ensure(stot * 8 + 256, st);
         h->ws_X.ensure(xtot * 8 + 256, st);
         h->d_ranks.ensure(comp.size() * sizeof(int) + 64, st);
-        std::vector<GemmTask> gt;
-        std::vector<GemmSeg> gs;
+        std::vector<GemmTask> gt, gt2;
+        std::vector<GemmSeg> gs, gs2;
         std::vector<EigTask> et;
         int64_t soff_sig = 0, xoff = 0;
         int max_m = 0;
@@ -698,6 +722,8 @@ void factor_impl(lorasp_ctx *h, const double *values) {
             int p = nd.partners[k], sl = nd.pslot_src[k];
             int mk = size(p);
             if (mk == 0) continue;
+            // SPD: sum X X^T with X = {S_c, p} (rows S_c) = A_k^T;  LU: the same for
+            // X = Mat(p -> s) = B_k^T, plus A_k^T A_k from Mat(s -> p) (rows p) below
             GemmSeg g{};
             g.A = slot_ptr(sl);
             g.B = slot_ptr(sl);
@@ -709,6 +735,22 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           }
           b.nseg = (int)gs.size() - b.seg0;
           add_tiles(gt, b);
+          if (!sym) {   // second task set (ta = 1, tb = 0) for the A_k^T A_k part, accumulated
+            GemmTask b2 = b;
+            b2.ta = 1;
+            b2.tb = 0;
+            b2.beta = 1;
+            b2.seg0 = (int)gs2.size();
+            for (size_t k = 0; k < nd.partners.size(); ++k) {
+              int p = nd.partners[k], sl = nd.pslot_src2[k];
+              int mk = size(p);
+              if (mk == 0) continue;
+              gs2.push_back(GemmSeg{slot_ptr(sl), slot_ptr(sl), sld[sl], sld[sl], mk, 1.0});
+              R += mk;
+            }
+            b2.nseg = (int)gs2.size() - b2.seg0;
+            add_tiles(gt2, b2);
+          }
           f_gram += (double)R * mc * mc;
           b_gram += 8.0 * R * mc + 8.0 * mc * mc;
           f_eig += 9.0 * mc * (double)mc * mc;
@@ -726,6 +768,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           et.push_back(e);
         }
         launch_gemm(h, gt, gs, K_GRAM, f_gram, b_gram);
+        launch_gemm(h, gt2, gs2, K_GRAM, 0, 0);   // LU: A_k^T A_k half of the Gram
         EigTask *de = push(h, et);
         int64_t want = (int64_t)max_m * max_m + 6 * (max_m + 8) + std::max(max_m, 512);
         int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
@@ -788,7 +831,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         if (nd.aux) W += r[c];
         Wn[e] = W;
         ctr_off[e] = ctr_tot;
-        ctr_tot += ((int64_t)(m[c] + r[c]) * W + 31) & ~int64_t(31);
+        ctr_tot += ((int64_t)(m[c] + r[c]) * W * (sym ? 1 : 2) + 31) & ~int64_t(31);
       }
       h->ws_ctr.ensure(std::max<int64_t>(ctr_tot, 32) * 8, st);
       int max_n = 0;
@@ -807,13 +850,16 @@ void factor_impl(lorasp_ctx *h, const double *values) {
             int mk = size(p);
             R += mk;
             if (mk == 0) continue;
-            int s1 = nd.pslot_src[k], s2 = nd.pslot_dst[k];
+            // SPD: R_k = (A_k^T)^T V from {S_c, p} into {P_c, p}.
+            // LU:  R_k = A_k V (Mat(s->p)) into Mat(P->p);  Q_k = B_k V (Mat(p->s)^T V)
+            //      stored transposed into Mat(p->P) = Q_k^T
+            int s1 = sym ? nd.pslot_src[k] : nd.pslot_src2[k], s2 = nd.pslot_dst[k];
             GemmTask b{};
             b.C = slot_ptr(s2);
             b.ldc = sld[s2];
             b.M = mk;
             b.N = rc;
-            b.ta = 1;
+            b.ta = sym ? 1 : 0;
             b.tb = 0;
             b.tc = (lv.slots[s2].row == p) ? 0 : 1;
             b.beta = 0;
@@ -828,16 +874,32 @@ void factor_impl(lorasp_ctx *h, const double *values) {
             g.alpha = 1.0;
             ps.push_back(g);
             add_tiles(pt, b);
+            if (!sym) {
+              const int s3 = nd.pslot_src[k], s4 = nd.pslot_dst2[k];
+              GemmTask q2 = b;
+              q2.C = slot_ptr(s4);
+              q2.ldc = sld[s4];
+              q2.ta = 1;
+              q2.tc = 1;   // Mat(p -> P) has rows P: store Q_k^T
+              q2.seg0 = (int)ps.size();
+              ps.push_back(GemmSeg{slot_ptr(s3), V, sld[s3], mc, mc, 1.0});
+              add_tiles(pt, q2);
+            }
           }
         } else if (nd.aux) {
           for (int p : nd.partners) R += size(p);
         }
         // record F = [L^{-1} | Z]  (n x (n + W), leading dimension ldF = n rounded up to
         // even so that every column starts 16-byte aligned for the bulk-copy apply)
+        // LU: F = [L^{-1} | U^{-T} | X = L^{-1} C | Y^T = U^{-T} R^T]
         const int ldF = n + (n & 1);
-        double *F = h->fpool.alloc((size_t)ldF * (n + W) + 2);  // +16 B: bulk copies round up
+        const int64_t fcols = sym ? (int64_t)(n + W) : (int64_t)(2 * n + 2 * W);
+        double *F = h->fpool.alloc((size_t)ldF * fcols + 2);  // +16 B: bulk copies round up
         double *ctr = h->ws_ctr.as<double>() + ctr_off[e];
-        h->f_doubles += (int64_t)ldF * (n + W);
+        double *rtr = sym ? nullptr : ctr + (int64_t)n * W;   // LU: R (W x n, ld W)
+        h->f_doubles += (int64_t)ldF * fcols;
+        const int64_t offX = sym ? (int64_t)ldF * n : 2 * (int64_t)ldF * n;
+        const int64_t offY = offX + (int64_t)ldF * W;
         NodeRec rec;
         rec.level = i;
         rec.c = c;
@@ -846,6 +908,9 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         rec.W = W;
         rec.F = F;
         rec.ld = ldF;
+        rec.zf_off = sym ? offX : offY;   // forward: Z (SPD) / Y^T (LU)
+        rec.zb_off = offX;                // backward: Z / X
+        rec.lb_off = sym ? 0 : (int64_t)ldF * n;   // backward triangle: L^{-1} / U^{-T}
         // assemble pivot K = [[S, V], [V^T, 0]] (lower part used)
         CopyTask t{};
         t.src = slot_ptr(nd.self_slot);
@@ -878,6 +943,18 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           t.mode = 1;
           t.alpha = 0.0;
           ct.push_back(t);  // b has no self block (reading Z13)
+          if (!sym) {
+            t = CopyTask{};
+            t.src = V;
+            t.lds = mc;
+            t.dst = F + (int64_t)mc * ldF;
+            t.ldd = ldF;
+            t.rows = mc;
+            t.cols = rc;
+            t.mode = 0;
+            t.alpha = 1.0;
+            ct.push_back(t);  // Mat(b -> s) = V (rule 4), upper-right of the LU pivot
+          }
         }
         // coupling C: rows (s; b), columns T = N1(s) + [P(b)]
         int zc = 0;
@@ -896,6 +973,28 @@ void factor_impl(lorasp_ctx *h, const double *values) {
             t.mode = 0;
             t.alpha = 1.0;
             ct.push_back(t);
+            if (!sym) {   // R rows of n: Mat(s -> n) (wu x m), b columns stay zero
+              t = CopyTask{};
+              t.src = slot_ptr(nd.n1_slot2[k]);
+              t.lds = sld[nd.n1_slot2[k]];
+              t.dst = rtr + zc;
+              t.ldd = W;
+              t.rows = wu;
+              t.cols = mc;
+              t.mode = 0;
+              t.alpha = 1.0;
+              ct.push_back(t);
+              if (rc > 0) {
+                t = CopyTask{};
+                t.dst = rtr + zc + (int64_t)mc * W;
+                t.ldd = W;
+                t.rows = wu;
+                t.cols = rc;
+                t.mode = 1;
+                t.alpha = 0.0;
+                ct.push_back(t);
+              }
+            }
           }
           zc += wu;
         }
@@ -929,6 +1028,24 @@ void factor_impl(lorasp_ctx *h, const double *values) {
             t.mode = 2;
             t.alpha = -1.0;
             ct.push_back(t);  // b <-> P(b): -I_r (rule 5)
+            if (!sym) {       // R rows of P(b): Mat(s -> P) = 0, Mat(b -> P) = -I
+              t = CopyTask{};
+              t.dst = rtr + zc;
+              t.ldd = W;
+              t.rows = rc;
+              t.cols = mc;
+              t.mode = 1;
+              t.alpha = 0.0;
+              ct.push_back(t);
+              t = CopyTask{};
+              t.dst = rtr + zc + (int64_t)mc * W;
+              t.ldd = W;
+              t.rows = rc;
+              t.cols = rc;
+              t.mode = 2;
+              t.alpha = -1.0;
+              ct.push_back(t);
+            }
           }
         }
         // pivot
@@ -938,7 +1055,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           for (int tn = 0; tn < W; tn += GT)
             for (int tm = 0; tm < n; tm += GT) {
               GemmTask b{};
-              b.C = F + (int64_t)ldF * n;
+              b.C = F + offX;
               b.ldc = ldF;
               b.M = n;
               b.N = W;
@@ -956,6 +1073,14 @@ void factor_impl(lorasp_ctx *h, const double *values) {
               g.alpha = 1.0;
               zs.push_back(g);
               zt.push_back(b);
+              if (!sym) {   // Y^T = U^{-T} R^T  (U^{-T} lower triangular)
+                GemmTask y = b;
+                y.C = F + offY;
+                y.tb = 1;
+                y.seg0 = (int)zs.size();
+                zs.push_back(GemmSeg{F + (int64_t)ldF * n, rtr, ldF, W, std::min(n, tm + GT), 1.0});
+                zt.push_back(y);
+              }
             }
         }
         // Schur: T_a,b -= Z_a^T D Z_b   (D = diag(I_m, -I_r))
@@ -963,9 +1088,31 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           const std::vector<int> &T = rec.T;
           std::vector<int> zoff(T.size() + 1, 0);
           for (size_t a = 0; a < T.size(); ++a) zoff[a + 1] = zoff[a] + rec.w[a];
-          const double *Z = F + (int64_t)ldF * n;
+          const double *Z = F + offX;
+          if (!sym) {   // LU: Mat(T_b -> T_a) -= Y_a X_b for every ordered pair
+            const double *Yt = F + offY;
+            for (size_t a = 0; a < T.size(); ++a)
+              for (size_t bb = 0; bb < T.size(); ++bb) {
+                const int wa = rec.w[a], wb = rec.w[bb];
+                if (wa == 0 || wb == 0) continue;
+                const int sl = nd.tslot[a * T.size() + bb];
+                GemmTask b{};
+                b.C = slot_ptr(sl);
+                b.ldc = sld[sl];
+                b.M = wa;
+                b.N = wb;
+                b.ta = 1;
+                b.tb = 0;
+                b.tc = 0;
+                b.beta = 1;
+                b.seg0 = (int)ss.size();
+                b.nseg = 1;
+                ss.push_back(GemmSeg{Yt + (int64_t)zoff[a] * ldF, Z + (int64_t)zoff[bb] * ldF, ldF, ldF, n, -1.0});
+                add_tiles(stt, b);
+              }
+          }
           size_t idx = 0;
-          for (size_t a = 0; a < T.size(); ++a)
+          for (size_t a = 0; sym && a < T.size(); ++a)
             for (size_t bb = 0; bb <= a; ++bb, ++idx) {
               int wa = rec.w[a], wb = rec.w[bb];
               if (wa == 0 || wb == 0) continue;
@@ -998,7 +1145,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
               add_tiles(stt, b);
             }
         }
-        h->flops_model += node_flops(mc, rc, nd.aux ? R : 0, W);
+        h->flops_model += node_flops(mc, rc, nd.aux ? R : 0, W, sym);
         f_proj += 2.0 * R * mc * rc;
         b_proj += 8.0 * ((double)R * mc + (double)R * rc + (double)mc * rc);
         f_piv += ((double)mc * mc * mc + (double)rc * rc * rc) / 3.0;
@@ -1012,7 +1159,10 @@ void factor_impl(lorasp_ctx *h, const double *values) {
       h->t_host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
       launch_gemm(h, pt, ps, K_PROJECT, f_proj, b_proj);
       launch_copy(h, ct, K_ASSEMBLE);
-      pivots(h, pv, f_piv, b_piv);
+      if (sym)
+        pivots(h, pv, f_piv, b_piv);
+      else
+        pivots_lu(h, pv, f_piv, b_piv);
       launch_gemm(h, zt, zs, K_ZGEMM, f_z, b_z);
       launch_gemm(h, stt, ss, K_SCHUR, f_s, b_s);
       if (h->debug) {
@@ -1076,6 +1226,10 @@ void factor_impl(lorasp_ctx *h, const double *values) {
     a.r = rc.r;
     a.W = rc.W;
     a.ld = rc.ld;
+    a.zf_off = rc.zf_off;
+    a.zb_off = rc.zb_off;
+    a.lb_off = rc.lb_off;
+    a.sym = (pl.flags & LORASP_SPD) ? 1 : 0;
     a.seg0 = (int)as.size();
     int zc = 0;
     const int K = lv.K;
@@ -1348,7 +1502,6 @@ int lorasp_analyze(int64_t n, const int64_t *row_ptr, const int64_t *col_idx, in
                    int leaf_size, int depth, double eps, unsigned flags, int device, lorasp_handle *out) {
   if (!out) return LORASP_E_ARG;
   *out = nullptr;
-  if (!(flags & LORASP_SPD)) return LORASP_E_ARG;  // only the SPD path in this version
   auto *h = new lorasp_ctx();
   h->device = device;
   std::string err;

@@ -215,7 +215,10 @@ def test_pivot(K, m, r, device=0):
     return A, st
 
 
-def analyze_problem(p, eps=None, flags=LORASP_SPD, device=0, depth=None) -> Handle:
-    """Convenience: analyze a synth.Problem."""
+def analyze_problem(p, eps=None, flags=None, device=0, depth=None) -> Handle:
+    """Convenience: analyze a synth.Problem (SPD path for symmetric problems,
+    the general LU path otherwise, unless flags are given)."""
+    if flags is None:
+        flags = LORASP_SPD if getattr(p, "symmetric", True) else 0
     return Handle(p.n, p.row_ptr, p.col_idx, p.coords, depth=p.depth if depth is None else depth,
                   leaf_size=p.leaf, eps=p.eps if eps is None else eps, flags=flags, device=device)

@@ -73,8 +73,20 @@ def test_analyze_rejects_bad_input(L):
     with pytest.raises(L.LoraspError) as e:
         L.Handle(p.n, p.row_ptr, p.col_idx, p.coords, depth=11, eps=0.1)   # 2^11 > n
     assert e.value.code == -1
-    with pytest.raises(L.LoraspError):
-        L.Handle(p.n, p.row_ptr, p.col_idx, p.coords, depth=6, eps=0.1, flags=0)  # SPD path only
+    with pytest.raises(L.LoraspError) as e:
+        L.Handle(p.n, p.row_ptr, p.col_idx, p.coords, depth=6, eps=1.5)            # eps outside [0, 1]
+    assert e.value.code == -1
+
+
+def test_analyze_general_path_orders_match_spd(L):
+    # the LU path (flags without LORASP_SPD) replays the same symbolic structure
+    p = make_problem("cfg5", dims=(64, 64), depth=7)
+    h1 = L.Handle(p.n, p.row_ptr, p.col_idx, p.coords, depth=7, eps=1e-3, flags=0)
+    h2 = L.Handle(p.n, p.row_ptr, p.col_idx, p.coords, depth=7, eps=1e-3, flags=L.LORASP_SPD)
+    for i in range(1, 8):
+        assert np.array_equal(h1.level_order(i)[0], h2.level_order(i)[0])
+    assert h1.stats()["waves"] == h2.stats()["waves"]
+    h1.close(); h2.close()
 
 
 def test_apply_before_factor_is_state_error(L):

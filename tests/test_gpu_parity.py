@@ -208,3 +208,39 @@ def test_cfg2_full_parity(L):
     ro = O.pcg(mv, lambda v: O.solve(f, v), p.b, tol=1e-10)
     assert rc == 0 and rr <= 1e-10 and abs(it - ro.iters) <= 1
     h.close()
+
+
+# ---------------------------------------------------------------------------
+# General (nonsymmetric) LU path: cfg5 family (first-order upwind convection-
+# diffusion), both block orientations stored, stack [A_k; B_k] (P:l.333-354),
+# no-pivot LU of the fused pivot, GMRES(50).
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dims,depth", [((16, 16), 4), ((24, 16), 4), ((32, 32), 6)])
+def test_lu_eps0_exact(L, dims, depth):
+    p = make_problem("cfg5", dims=dims, depth=depth)
+    h = L.analyze_problem(p, eps=0.0, flags=0)
+    h.factor(torch.tensor(p.values, device="cuda"))
+    x = gpu_apply(h, p.b)
+    A = csr_to_dense(p.n, p.row_ptr, p.col_idx, p.values)
+    assert relerr(x, np.linalg.solve(A, p.b)) <= 1e-10
+    f = oracle_factor(p, 0.0)
+    assert rank_mismatches(h, f, p.depth, 0.0) == []
+    h.close()
+
+
+@pytest.mark.parametrize("dims,depth,eps", [((32, 32), 6, 1e-3), ((64, 64), 7, 1e-2), ((40, 24), 5, 1e-1)])
+def test_lu_ranks_apply_gmres_parity(L, dims, depth, eps):
+    p = make_problem("cfg5", dims=dims, depth=depth)
+    h = L.analyze_problem(p, eps=eps, flags=0)
+    h.factor(torch.tensor(p.values, device="cuda"))
+    f = oracle_factor(p, eps)
+    assert rank_mismatches(h, f, p.depth, eps) == []
+    x = gpu_apply(h, p.b)
+    assert relerr(x, O.solve(f, p.b)) <= 1e-9
+    b = torch.tensor(p.b, device="cuda")
+    xk = torch.empty_like(b)
+    rc, it, rr = h.krylov(b, xk, tol=1e-10, method=L.LORASP_GMRES, restart=50)
+    mv = lambda v: O.spmv(p.row_ptr, p.col_idx, p.values, v)
+    ro = O.gmres(mv, lambda v: O.solve(f, v), p.b, tol=1e-10, restart=50)
+    assert rc == 0 and rr <= 1e-10 and abs(it - ro.iters) <= 1
+    h.close()
