@@ -220,13 +220,18 @@ def main():
         fl, al, kl = h.launch_counts()
         return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), it, rr, rc, fl + kl
 
-    for _ in range(args.warmup):
+    for wi in range(args.warmup):
+        if wi == args.warmup - 1:
+            h.set_timing(True)      # last warm-up step: per-class breakdown (all classes)
         step(False)
+    warm_kernels = h.stats().get("kernels", {})
+    # the timed region times only the dominant class (2 event records per launch of it)
+    dom_cls = max(warm_kernels.values(), key=lambda v: v["ms"])["class"] if warm_kernels else 0
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
-    h.set_timing(True)
+    h.set_timing(1 << dom_cls)
     clk = ClockSampler(local)
     clk.start()
     tfs, tks, its, launches = [], [], [], 0
@@ -278,12 +283,14 @@ def main():
         roof["launches"] = dom["launches"]
         roof["avg_launch_ms"] = per_launch_ms
         roof["share_of_timed"] = dom["ms"] / (sum(tfs) + sum(tks))
+        roof["alg_work_per_launch"] = (dom["alg_bytes"] if roof["bound"] == "hbm" else dom["alg_flops"]) / dom["launches"]
         roof["traffic"] = None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                tr = json.load(f).get(dom_name)
-            if tr is not None:
-                roof["traffic"] = tr
+                trd = json.load(f)
+            if dom_name in trd:
+                roof["traffic"] = trd[dom_name]
+                roof["traffic_note"] = trd.get("_note")
         except Exception:
             pass
 
@@ -301,7 +308,9 @@ def main():
             "tflops_model": tflops, "fp64_peak_tflops": peak_f, "frac_fp64_peak": tflops / peak_f,
             "flops_model": flops, "factor_bytes": stats.get("factor_bytes"), "aux_vars": stats.get("aux_vars"),
             "gpu_launches": launches, "clocks": clocks, "roofline": roof,
-            "kernels": kern}
+            "kernels_warmup_step": warm_kernels,
+            "kernels_note": "per-class breakdown from the last warm-up step (all classes timed); the timed "
+                            "region records CUDA events only around launches of the dominant class"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb, _ = cpu_baseline(p)

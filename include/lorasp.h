@@ -135,9 +135,11 @@ int lorasp_get_sizes(lorasp_handle h, int level, int *sizes, int cap);
  * through *len if len != NULL. */
 int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len);
 
-/* Per-kernel-class CUDA-event timing on the handle's stream: enable != 0
- * resets and starts accumulating (ms, launches, algorithmic flops and bytes
- * per class, reported under "kernels" by lorasp_get_stats); 0 stops. */
+/* Per-kernel-class CUDA-event timing on the handle's stream.  enable is a
+ * bitmask of kernel classes (bit c = the class with "class": c in the stats
+ * JSON; -1 = all); nonzero resets and starts accumulating (ms, launches,
+ * algorithmic flops and bytes per class, reported under "kernels" by
+ * lorasp_get_stats); 0 stops.  Each timed launch costs two event records. */
 int lorasp_set_timing(lorasp_handle h, int enable);
 
 /* Number of kernel launches issued by the last factor / apply / krylov call. */

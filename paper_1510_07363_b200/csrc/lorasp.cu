@@ -166,7 +166,7 @@ enum KClass {
 static const char *KNAME[K_NCLASS] = {"leaf_scatter", "merge_copy", "gram_gemm", "eig_tridiag",
                                       "project_gemm", "assemble_copy", "pivot_chol_inv", "trsm_gemm",
                                       "schur_gemm", "apply_fwd", "apply_bwd", "spmv", "dot", "vec"};
-static const char *KKERNEL[K_NCLASS] = {"k_leaf_scatter", "k_copy", "k_gemm", "k_eig", "k_gemm", "k_copy",
+static const char *KKERNEL[K_NCLASS] = {"k_leaf_scatter", "k_copy", "k_gemm", "k_eig_t", "k_gemm", "k_copy",
                                         "k_pivot", "k_gemm", "k_gemm", "k_apply_fwd", "k_apply_bwd",
                                         "k_spmv", "k_dot_partial+k_dot_final", "k_axpby/k_sub/k_set_rhs/k_get_x"};
 struct KStat {
@@ -224,6 +224,7 @@ struct lorasp_ctx {
   bool debug = getenv("LORASP_DEBUG") != nullptr;
   // kernel timing
   bool timing = false;
+  unsigned timing_mask = 0;
   std::vector<cudaEvent_t> evpool;
   std::vector<TimedEv> pend;
   KStat kst[K_NCLASS];
@@ -237,7 +238,7 @@ inline dim3 grid1(int64_t n, int bs = 256) {
 }
 
 int tbeg(lorasp_ctx *h, int cls) {
-  if (!h->timing) return -1;
+  if (!h->timing || !((h->timing_mask >> cls) & 1u)) return -1;
   size_t need = 2 * (h->pend.size() + 1);
   while (h->evpool.size() < need) {
     cudaEvent_t e;
@@ -1587,6 +1588,7 @@ int lorasp_set_timing(lorasp_handle h, int enable) {
   return guarded(h, [&]() {
     CK(cudaSetDevice(h->device));
     h->timing = enable != 0;
+    h->timing_mask = (unsigned)enable;
     for (auto &k : h->kst) k = KStat();
     h->pend.clear();
     return (int)LORASP_OK;
@@ -1666,7 +1668,8 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
   for (int c = 0; c < K_NCLASS; ++c) {
     const KStat &k = h->kst[c];
     if (k.launches == 0) continue;
-    o << (first ? "" : ",") << "\"" << KNAME[c] << "\":{\"kernel\":\"" << KKERNEL[c] << "\",\"ms\":" << k.ms
+    o << (first ? "" : ",") << "\"" << KNAME[c] << "\":{\"class\":" << c << ",\"kernel\":\"" << KKERNEL[c]
+      << "\",\"ms\":" << k.ms
       << ",\"launches\":" << k.launches << ",\"alg_flops\":" << k.flops << ",\"alg_bytes\":" << k.bytes << "}";
     first = false;
   }

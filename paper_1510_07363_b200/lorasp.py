@@ -146,8 +146,10 @@ class Handle:
     def set_stream(self, stream_ptr: int):
         return self._check(self._lib.lorasp_set_stream(self.h, ctypes.c_void_p(stream_ptr)), "set_stream")
 
-    def set_timing(self, enable: bool):
-        return self._check(self._lib.lorasp_set_timing(self.h, int(bool(enable))), "set_timing")
+    def set_timing(self, mask):
+        """mask: True = all kernel classes, False = off, or an int bitmask of classes."""
+        m = -1 if mask is True else (0 if mask is False else int(mask))
+        return self._check(self._lib.lorasp_set_timing(self.h, m), "set_timing")
 
     def level_order(self, level):
         K = 2 ** (level - 1)
