@@ -1107,6 +1107,163 @@ __global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ ta
     }
 }
 
+// ----------------------------------------------- blocked pivot (one CTA) ----
+// Same result as k_pivot (K = L D L^T, then L^{-1}), for n <= PIVB_MAXN in
+// shared memory, with 16-column blocks so that the number of block barriers is
+// ~5 per block instead of ~5 per column:
+//   factor: warp 0 factors the 16x16 diagonal block and inverts it (warp-
+//   synchronous), every thread solves one row of the panel
+//   L21 = A21 L11^{-T} D1, warps update the trailing lower triangle
+//   A22 -= L21 D1 L21^T;
+//   invert (in place, blocks descending): T = X22 L21 (X22 already inverted)
+//   is parked transposed in the free upper triangle, A21 <- -T L11^{-1},
+//   A11 <- L11^{-1}.
+constexpr int PIVB_NB = 16;
+constexpr int PIVB_MAXN = 160;
+
+__device__ __forceinline__ void pivb_diag_inverse(const double *__restrict__ A, int lda, int j0, int b,
+                                                  double *__restrict__ W, int lane) {
+  // W (16 x 16, ld 16) <- inverse of the lower-triangular diagonal block A[j0.., j0..]
+  // lane c computes column c by forward substitution
+  if (lane < b) {
+    const int c = lane;
+    double x[PIVB_NB];
+#pragma unroll
+    for (int i = 0; i < PIVB_NB; ++i) x[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < PIVB_NB; ++i) {
+      if (i < b && i >= c) {
+        double sacc = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < PIVB_NB; ++k)
+          if (k >= c && k < i) sacc = fma(-A[(j0 + i) + (int64_t)(j0 + k) * lda], x[k], sacc);
+        x[i] = sacc * frcp(A[(j0 + i) + (int64_t)(j0 + i) * lda]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < PIVB_NB; ++i) W[i + c * PIVB_NB] = (i < b) ? x[i] : 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict__ tasks, int *status) {
+  extern __shared__ double sh[];
+  __shared__ double W[PIVB_NB * PIVB_NB];
+  __shared__ int s_fail;
+  const PivTask t = tasks[blockIdx.x];
+  const int n = t.m + t.r;
+  if (n == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int lda = n | 1;   // odd leading dimension: row-wise walks spread over banks
+  double *A = sh;
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i < n; i += 32) A[i + (int64_t)j * lda] = (i >= j) ? t.F[i + (int64_t)j * t.ld] : 0.0;
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  // ---------------- blocked signed Cholesky ----------------
+  for (int j0 = 0; j0 < n; j0 += PIVB_NB) {
+    const int b = min(PIVB_NB, n - j0), j1 = j0 + b;
+    if (warp == 0) {
+      for (int k = 0; k < b; ++k) {           // 16-column diagonal block, lane = row
+        const double d = (j0 + k < t.m) ? 1.0 : -1.0;
+        const double v = A[(j0 + k) + (int64_t)(j0 + k) * lda] * d;
+        if (!(v > 0.0) || !isfinite(v)) {
+          if (lane == 0) {
+            s_fail = 1;
+            if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
+          }
+          break;
+        }
+        const double lkk = sqrt(v), sc = d * frcp(lkk);
+        const int i = j0 + lane;
+        double lik = 0.0;
+        if (lane > k && lane < b) {
+          lik = A[i + (int64_t)(j0 + k) * lda] * sc;
+          A[i + (int64_t)(j0 + k) * lda] = lik;
+        }
+        __syncwarp();
+        if (lane == k) A[i + (int64_t)(j0 + k) * lda] = lkk;
+        if (lane > k && lane < b)
+          for (int jj = k + 1; jj <= lane; ++jj)
+            A[i + (int64_t)(j0 + jj) * lda] =
+                fma(-lik * d, A[(j0 + jj) + (int64_t)(j0 + k) * lda], A[i + (int64_t)(j0 + jj) * lda]);
+        __syncwarp();
+      }
+      if (!s_fail) pivb_diag_inverse(A, lda, j0, b, W, lane);
+    }
+    __syncthreads();
+    if (s_fail) return;
+    // panel: row i of L21 = d .* (Linv11 applied to row i of A21)
+    for (int i = j1 + tid; i < n; i += blockDim.x) {
+      double a[PIVB_NB];
+#pragma unroll
+      for (int k = 0; k < PIVB_NB; ++k) a[k] = (k < b) ? A[i + (int64_t)(j0 + k) * lda] : 0.0;
+#pragma unroll
+      for (int c = 0; c < PIVB_NB; ++c) {
+        if (c < b) {
+          double sacc = 0;
+#pragma unroll
+          for (int k = 0; k <= c; ++k) sacc = fma(W[c + k * PIVB_NB], a[k], sacc);
+          const double dc = (j0 + c < t.m) ? 1.0 : -1.0;
+          A[i + (int64_t)(j0 + c) * lda] = sacc * dc;
+        }
+      }
+    }
+    __syncthreads();
+    // trailing lower triangle: A22 -= L21 D1 L21^T
+    for (int j = j1 + warp; j < n; j += nw) {
+      double lj[PIVB_NB];
+#pragma unroll
+      for (int c = 0; c < PIVB_NB; ++c) {
+        const double dc = (j0 + c < t.m) ? 1.0 : -1.0;
+        lj[c] = (c < b) ? A[j + (int64_t)(j0 + c) * lda] * dc : 0.0;
+      }
+      for (int i = j + lane; i < n; i += 32) {
+        double sacc = A[i + (int64_t)j * lda];
+#pragma unroll
+        for (int c = 0; c < PIVB_NB; ++c)
+          if (c < b) sacc = fma(-A[i + (int64_t)(j0 + c) * lda], lj[c], sacc);
+        A[i + (int64_t)j * lda] = sacc;
+      }
+    }
+    __syncthreads();
+  }
+  // ---------------- blocked in-place inverse of L ----------------
+  const int last = ((n - 1) / PIVB_NB) * PIVB_NB;
+  for (int j0 = last; j0 >= 0; j0 -= PIVB_NB) {
+    const int b = min(PIVB_NB, n - j0), j1 = j0 + b;
+    // (a) T = X22 L21 (rows j1.., cols 0..b), parked transposed in A[j0 + c, j1 + row] (free upper part)
+    if (warp == 0) {
+      pivb_diag_inverse(A, lda, j0, b, W, lane);
+    } else {
+      const int rows = n - j1;
+      for (int q = tid - 32; q < rows * b; q += blockDim.x - 32) {
+        const int ii = q % rows, c = q / rows, i = j1 + ii;
+        double sacc = 0;
+        for (int k = j1; k <= i; ++k) sacc = fma(A[i + (int64_t)k * lda], A[k + (int64_t)(j0 + c) * lda], sacc);
+        A[(j0 + c) + (int64_t)i * lda] = sacc;   // upper part: row j0+c, column i
+      }
+    }
+    __syncthreads();
+    // (b) A21 <- -T L11^{-1};  A11 <- L11^{-1}
+    {
+      const int rows = n - j1;
+      for (int q = tid; q < rows * b; q += blockDim.x) {
+        const int ii = q % rows, c = q / rows, i = j1 + ii;
+        double sacc = 0;
+        for (int k = c; k < b; ++k) sacc = fma(A[(j0 + k) + (int64_t)i * lda], W[k + c * PIVB_NB], sacc);
+        A[i + (int64_t)(j0 + c) * lda] = -sacc;
+      }
+      for (int q = tid; q < b * b; q += blockDim.x) {
+        const int i = q % b, c = q / b;
+        if (i >= c) A[(j0 + i) + (int64_t)(j0 + c) * lda] = W[i + c * PIVB_NB];
+      }
+    }
+    __syncthreads();
+  }
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i < n; i += 32) t.F[i + (int64_t)j * t.ld] = (i >= j) ? A[i + (int64_t)j * lda] : 0.0;
+}
+
 // -------------------------------------------- blocked pivot (large nodes) ----
 // For n = m + r too large for one CTA's shared memory the fused pivot is
 // factored by a right-looking blocked signed Cholesky (64-column panels; panel

@@ -131,26 +131,41 @@ struct Staging {
   void reserve(size_t bytes, cudaStream_t st) {
     size_t need = bytes + 4096;
     if (used + need <= cap) return;
+    flush(st);
     CK(cudaStreamSynchronize(st));
     used = 0;
+    pend = 0;
     if (need > cap) init(std::max(need, cap * 2), st);
   }
-  // copy `bytes` of src into staging and enqueue the H2D copy; returns device ptr
-  void *push(const void *src, size_t bytes, cudaStream_t st) {
+  // copy `bytes` of src into staging; the H2D copy of everything pushed since
+  // the last flush() is one cudaMemcpyAsync (descriptors of a whole wave travel
+  // together).  Returns the device pointer.
+  size_t pend = 0;   // start of the not-yet-copied range
+  void *push_deferred(const void *src, size_t bytes, cudaStream_t st) {
     if (bytes == 0) return d.p;
     size_t need = (bytes + 255) & ~size_t(255);
     if (used + need > cap) {
+      flush(st);
       CK(cudaStreamSynchronize(st));
       used = 0;
+      pend = 0;
       if (need > cap) init(std::max(need, cap * 2), st);
     }
     std::memcpy(h + used, src, bytes);
     void *dp = d.as<char>() + used;
-    CK(cudaMemcpyAsync(dp, h + used, bytes, cudaMemcpyHostToDevice, st));
     used += need;
     return dp;
   }
-  void reset() { used = 0; }  // only after a stream sync
+  void flush(cudaStream_t st) {
+    if (used > pend) CK(cudaMemcpyAsync(d.as<char>() + pend, h + pend, used - pend, cudaMemcpyHostToDevice, st));
+    pend = used;
+  }
+  void *push(const void *src, size_t bytes, cudaStream_t st) {
+    void *dp = push_deferred(src, bytes, st);
+    flush(st);
+    return dp;
+  }
+  void reset() { used = 0; pend = 0; }  // only after a stream sync
   void release() {
     if (h) cudaFreeHost(h);
     h = nullptr;
@@ -222,6 +237,7 @@ struct lorasp_ctx {
   int64_t launches_factor = 0, launches_apply = 0, launches_krylov = 0;
   int64_t f_doubles = 0;
   bool debug = getenv("LORASP_DEBUG") != nullptr;
+  bool pivot_unblocked = getenv("LORASP_PIVOT_UNBLOCKED") != nullptr;   // debug: column-wise k_pivot
   // kernel timing
   bool timing = false;
   unsigned timing_mask = 0;
@@ -299,6 +315,7 @@ void ensure_mem(lorasp_ctx *h) {
   CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_pivot_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
   CK(cudaFuncSetAttribute(k_apply_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   h->mem_ready = true;
@@ -307,6 +324,35 @@ void ensure_mem(lorasp_ctx *h) {
 template <class T>
 T *push(lorasp_ctx *h, const std::vector<T> &v) {
   return reinterpret_cast<T *>(h->stg.push(v.data(), v.size() * sizeof(T), h->stream));
+}
+template <class T>
+T *pushd(lorasp_ctx *h, const std::vector<T> &v) {   // deferred: copied at the next flush
+  return reinterpret_cast<T *>(h->stg.push_deferred(v.data(), v.size() * sizeof(T), h->stream));
+}
+template <class T>
+size_t vbytes(const std::vector<T> &v) {
+  return ((v.size() * sizeof(T) + 255) & ~size_t(255)) + 256;
+}
+
+// launch on descriptors already staged (pushd + flush)
+void launch_gemm_dev(lorasp_ctx *h, const GemmTask *dt, const GemmSeg *ds, size_t ntasks, int cls, double flops,
+                     double bytes) {
+  if (ntasks == 0) return;
+  int ev = cls >= 0 ? tbeg(h, cls) : -1;
+  k_gemm<<<(unsigned)ntasks, 256, 0, h->stream>>>(dt, ds);
+  tend(h, ev, flops, bytes);
+  ++h->launches_factor;
+  CK(cudaGetLastError());
+}
+void launch_copy_dev(lorasp_ctx *h, const CopyTask *dt, const std::vector<CopyTask> &tasks, int cls) {
+  if (tasks.empty()) return;
+  double bytes = 0;
+  for (const CopyTask &t : tasks) bytes += (t.mode == 0 ? 16.0 : 8.0) * t.rows * t.cols;
+  int ev = cls >= 0 ? tbeg(h, cls) : -1;
+  k_copy<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt);
+  tend(h, ev, 0, bytes);
+  ++h->launches_factor;
+  CK(cudaGetLastError());
 }
 
 void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::vector<GemmSeg> &segs,
@@ -407,10 +453,15 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
   int ev = tbeg(h, K_PIVOT);
   if (!small.empty()) {
     PivTask *dp = push(h, small);
-    int64_t want = (int64_t)max_n * max_n + max_n;
-    int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
-    cap = std::max(cap, max_n);
-    k_pivot<<<(unsigned)small.size(), 512, cap * 8, st>>>(dp, cap, h->d_status.as<int>());
+    if (max_n <= PIVB_MAXN && !h->pivot_unblocked) {
+      const size_t sm = (size_t)(max_n | 1) * max_n * 8;
+      k_pivot_blk<<<(unsigned)small.size(), 512, sm, st>>>(dp, h->d_status.as<int>());
+    } else {
+      int64_t want = (int64_t)max_n * max_n + max_n;
+      int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
+      cap = std::max(cap, max_n);
+      k_pivot<<<(unsigned)small.size(), 512, cap * 8, st>>>(dp, cap, h->d_status.as<int>());
+    }
     ++h->launches_factor;
     CK(cudaGetLastError());
   }
@@ -768,9 +819,13 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           e.rank_out = h->d_ranks.as<int>() + q;
           et.push_back(e);
         }
-        launch_gemm(h, gt, gs, K_GRAM, f_gram, b_gram);
-        launch_gemm(h, gt2, gs2, K_GRAM, 0, 0);   // LU: A_k^T A_k half of the Gram
-        EigTask *de = push(h, et);
+        h->stg.reserve(vbytes(gt) + vbytes(gs) + vbytes(gt2) + vbytes(gs2) + 4 * vbytes(et), st);
+        GemmTask *d_gt = pushd(h, gt), *d_gt2 = pushd(h, gt2);
+        GemmSeg *d_gs = pushd(h, gs), *d_gs2 = pushd(h, gs2);
+        EigTask *de = pushd(h, et);
+        h->stg.flush(st);
+        launch_gemm_dev(h, d_gt, d_gs, gt.size(), K_GRAM, f_gram, b_gram);
+        launch_gemm_dev(h, d_gt2, d_gs2, gt2.size(), K_GRAM, 0, 0);   // LU: A_k^T A_k half of the Gram
         int64_t want = (int64_t)max_m * max_m + 6 * (max_m + 8) + std::max(max_m, 512);
         int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
         cap = std::max(cap, 6 * (max_m + 8) + std::max(max_m, 512));
@@ -1157,15 +1212,21 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         b_s += 8.0 * (2.0 * n * W + (double)W * W);
         h->recs.push_back(std::move(rec));
       }
+      // all descriptors of the wave travel in one H2D copy
+      h->stg.reserve(vbytes(pt) + vbytes(ps) + vbytes(ct) + vbytes(zt) + vbytes(zs) + vbytes(stt) + vbytes(ss), st);
+      GemmTask *d_pt = pushd(h, pt), *d_zt = pushd(h, zt), *d_stt = pushd(h, stt);
+      GemmSeg *d_ps = pushd(h, ps), *d_zs = pushd(h, zs), *d_ss = pushd(h, ss);
+      CopyTask *d_ct = pushd(h, ct);
+      h->stg.flush(st);
       h->t_host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
-      launch_gemm(h, pt, ps, K_PROJECT, f_proj, b_proj);
-      launch_copy(h, ct, K_ASSEMBLE);
+      launch_gemm_dev(h, d_pt, d_ps, pt.size(), K_PROJECT, f_proj, b_proj);
+      launch_copy_dev(h, d_ct, ct, K_ASSEMBLE);
       if (sym)
         pivots(h, pv, f_piv, b_piv);
       else
         pivots_lu(h, pv, f_piv, b_piv);
-      launch_gemm(h, zt, zs, K_ZGEMM, f_z, b_z);
-      launch_gemm(h, stt, ss, K_SCHUR, f_s, b_s);
+      launch_gemm_dev(h, d_zt, d_zs, zt.size(), K_ZGEMM, f_z, b_z);
+      launch_gemm_dev(h, d_stt, d_ss, stt.size(), K_SCHUR, f_s, b_s);
       if (h->debug) {
         CK(cudaStreamSynchronize(st));
         CK(cudaMemcpy(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1780,9 +1841,14 @@ int lorasp_test_pivot(int device, double *K, int m, int r) {
     PivTask *dt;
     CK(cudaMalloc(&dt, sizeof(PivTask)));
     CK(cudaMemcpy(dt, &t, sizeof(PivTask), cudaMemcpyHostToDevice));
-    int cap = (int)std::min<int64_t>((int64_t)n * n + n, SMEM_LIMIT / 8);
-    cap = std::max(cap, n);
-    k_pivot<<<1, 512, cap * 8>>>(dt, cap, dst);
+    if (n <= PIVB_MAXN && !getenv("LORASP_PIVOT_UNBLOCKED")) {
+      CK(cudaFuncSetAttribute(k_pivot_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+      k_pivot_blk<<<1, 512, (size_t)(n | 1) * n * 8>>>(dt, dst);
+    } else {
+      int cap = (int)std::min<int64_t>((int64_t)n * n + n, SMEM_LIMIT / 8);
+      cap = std::max(cap, n);
+      k_pivot<<<1, 512, cap * 8>>>(dt, cap, dst);
+    }
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     int st[2];

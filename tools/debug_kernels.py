@@ -33,3 +33,12 @@ for m, rr in [(100, 40), (150, 10)]:
     Li, st = L.test_pivot(K, m, rr)
     Lf = np.linalg.inv(Li); D = np.diag([1]*m+[-1]*rr)
     print("pivot n", n, "st", st, "recon", np.abs(Lf@D@Lf.T - K).max()/np.abs(K).max())
+for m, rr in [(1, 0), (5, 3), (16, 0), (17, 4), (100, 28), (128, 32), (140, 20), (120, 40)]:
+    Sx = rng.standard_normal((m, m)); S = Sx@Sx.T + m*np.eye(m)
+    n = m+rr; K = np.zeros((n,n)); K[:m,:m]=S
+    if rr:
+        Vq,_ = np.linalg.qr(rng.standard_normal((m, rr)))
+        K[m:,:m]=Vq.T; K[:m,m:]=Vq
+    Li, st = L.test_pivot(K, m, rr)
+    Lf = np.linalg.inv(Li); D = np.diag([1]*m+[-1]*rr)
+    print("pivot_blk n", n, "st", st, "recon", np.abs(Lf@D@Lf.T - K).max()/np.abs(K).max(), "upper", np.abs(np.triu(Li,1)).max())
