@@ -89,9 +89,13 @@ struct GemmTask {
   int seg0, nseg;
 };
 
-constexpr int GT = 64, GK = 16;
+constexpr int GT = 64, GK = 32;
 
-__global__ void __launch_bounds__(256) k_gemm(const GemmTask *__restrict__ tasks,
+// 64x64 output tile per CTA (256 threads, 4x4 each, strided so that shared
+// loads are conflict-free); K in chunks of 32 staged through shared memory;
+// the next chunk is loaded into registers while the current one is consumed
+// (one global round trip per chunk is hidden behind 32 rank-1 updates).
+__global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask *__restrict__ tasks,
                                               const GemmSeg *__restrict__ segs) {
   const GemmTask t = tasks[blockIdx.x];
   __shared__ double As[GK][GT + 1];
@@ -111,29 +115,43 @@ __global__ void __launch_bounds__(256) k_gemm(const GemmTask *__restrict__ tasks
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) accs[a][b] = 0.0;
-    for (int k0 = 0; k0 < g.K; k0 += GK) {
+    // per-thread load coordinates (8 elements of A and 8 of B per chunk)
+    double ra[8], rb[8];
+    auto load = [&](int k0) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        int idx = tid + 256 * q;
+      for (int q = 0; q < 8; ++q) {
+        const int idx = tid + 256 * q;   // 0 .. 2047
         int i, kk;
-        if (!t.ta) { i = idx & 63; kk = idx >> 6; } else { kk = idx & 15; i = idx >> 4; }
-        int gi = t.tm + i, gk = k0 + kk;
-        double v = 0.0;
-        if (gi < t.M && gk < g.K)
-          v = t.ta ? g.A[gk + (int64_t)gi * g.lda] : g.A[gi + (int64_t)gk * g.lda];
-        As[kk][i] = v;
+        if (!t.ta) { i = idx & 63; kk = idx >> 6; } else { kk = idx & 31; i = idx >> 5; }
+        const int gi = t.tm + i, gk = k0 + kk;
+        ra[q] = (gi < t.M && gk < g.K) ? (t.ta ? g.A[gk + (int64_t)gi * g.lda] : g.A[gi + (int64_t)gk * g.lda]) : 0.0;
         int j;
-        if (!t.tb) { kk = idx & 15; j = idx >> 4; } else { j = idx & 63; kk = idx >> 6; }
-        int gj = t.tn + j;
-        gk = k0 + kk;
-        v = 0.0;
-        if (gj < t.N && gk < g.K)
-          v = t.tb ? g.B[gj + (int64_t)gk * g.ldb] : g.B[gk + (int64_t)gj * g.ldb];
-        Bs[kk][j] = v;
+        if (!t.tb) { kk = idx & 31; j = idx >> 5; } else { j = idx & 63; kk = idx >> 6; }
+        const int gj = t.tn + j, gk2 = k0 + kk;
+        rb[q] = (gj < t.N && gk2 < g.K) ? (t.tb ? g.B[gj + (int64_t)gk2 * g.ldb] : g.B[gk2 + (int64_t)gj * g.ldb])
+                                         : 0.0;
       }
-      __syncthreads();
+    };
+    auto store = [&]() {
 #pragma unroll
-      for (int kk = 0; kk < GK; ++kk) {
+      for (int q = 0; q < 8; ++q) {
+        const int idx = tid + 256 * q;
+        int i, kk;
+        if (!t.ta) { i = idx & 63; kk = idx >> 6; } else { kk = idx & 31; i = idx >> 5; }
+        As[kk][i] = ra[q];
+        int j;
+        if (!t.tb) { kk = idx & 31; j = idx >> 5; } else { j = idx & 63; kk = idx >> 6; }
+        Bs[kk][j] = rb[q];
+      }
+    };
+    if (g.K > 0) load(0);
+    for (int k0 = 0; k0 < g.K; k0 += GK) {
+      store();
+      __syncthreads();
+      if (k0 + GK < g.K) load(k0 + GK);   // in flight during the rank-1 updates below
+      const int kc = min(GK, g.K - k0);
+#pragma unroll 8
+      for (int kk = 0; kk < kc; ++kk) {
         double av[4], bv[4];
 #pragma unroll
         for (int a = 0; a < 4; ++a) av[a] = As[kk][tx + 16 * a];
