@@ -417,9 +417,546 @@ __device__ __forceinline__ double warp_eig_asc(const double *d, const double *e2
   return 0.5 * (lo + hi);
 }
 
+// Group multisection: EG lanes per eigenvalue (EG - 1 ... split points per
+// round, log2(EG + 1) bits), 32 / EG eigenvalues per warp, all groups of the
+// block at once.  Computes lam[k] (descending index k in [k1, k2)) = the
+// ascending-index (m - 1 - k) eigenvalue of T, scaled by bnorm.  Every lane
+// derives the split points from the same (lo, hi), so no shuffles are needed.
+template <int EG>
+__device__ __forceinline__ void grp_multisect(const double *d, const double *e2, int m, int k1, int k2, double gl,
+                                              double gu, double pivmin, double *lam, double bnorm) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane / EG, gi = lane % EG;
+  constexpr int GPW = 32 / EG;
+  constexpr double STEP = 1.0 / (EG + 1);
+  const int ngroups = (int)(blockDim.x >> 5) * GPW;
+  const int gid = (int)(threadIdx.x >> 5) * GPW + g;
+  for (int base = k1; base < k2; base += ngroups) {
+    const int k = base + gid;
+    const bool act = k < k2;
+    const int j = m - 1 - k;
+    double lo = gl, hi = gu;
+    bool done = !act;
+    for (int round = 0; round < 100 && __any_sync(0xffffffffu, !done); ++round) {
+      // T is scaled to |d|, |e| <= 1: eigenvalues are known to ~u absolutely
+      // (Householder), so an absolute floor of u / 4 loses nothing (|d sigma| <=
+      // 1e-13 sigma_0 at the threshold for eps >= 1e-3).
+      const double tol = 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 5.5e-17 + 2.0 * pivmin;
+      if (hi - lo <= tol) done = true;
+      const double x = fma(hi - lo, (double)(gi + 1) * STEP, lo);
+      const int c = sturm_count(d, e2, m, x, pivmin);
+      const unsigned bal = __ballot_sync(0xffffffffu, c > j);
+      if (!done) {
+        const unsigned gb = (bal >> (g * EG)) & ((1u << EG) - 1u);
+        if (gb == 0) {
+          lo = fma(hi - lo, (double)EG * STEP, lo);
+        } else {
+          const int f = __ffs(gb) - 1;
+          const double xf = fma(hi - lo, (double)(f + 1) * STEP, lo);
+          if (f > 0) lo = fma(hi - lo, (double)f * STEP, lo);
+          hi = xf;
+        }
+      }
+    }
+    if (act && gi == 0) lam[k] = 0.5 * (lo + hi) * bnorm;
+  }
+}
+
+// Inverse iteration for one eigenvalue lam of the tridiagonal (d, e): pivoted
+// LU of T - sft I (dgttrf) then 2 solves from a fixed pseudo-random start,
+// normalised.  Arrays are interleaved with stride S (S vectors side by side,
+// conflict-free when S consecutive threads run S vectors); piv is one byte per
+// row.  The result is written to z (contiguous, length m).
+__device__ __forceinline__ void invit_one(const double *__restrict__ d, const double *__restrict__ e, int m,
+                                          double sft, double pertol, int seed, double *__restrict__ DL,
+                                          double *__restrict__ D, double *__restrict__ DU,
+                                          double *__restrict__ DU2, double *__restrict__ b,
+                                          unsigned char *__restrict__ piv, int S, double *__restrict__ z) {
+  double Di = d[0] - sft, DUi = (m > 1) ? e[0] : 0.0;
+#pragma unroll 2
+  for (int i = 0; i < m - 1; ++i) {
+    const double DLi = e[i];
+    double Dn = d[i + 1] - sft;
+    double DUn = (i < m - 2) ? e[i + 1] : 0.0;
+    if (fabs(Di) >= fabs(DLi)) {
+      if (Di == 0.0) Di = pertol;
+      const double f = DLi * frcp(Di);
+      D[i * S] = Di;
+      DL[i * S] = f;
+      DU[i * S] = DUi;
+      DU2[i * S] = 0.0;
+      piv[i * S] = 0;
+      Dn = fma(-f, DUi, Dn);
+    } else {
+      const double f = Di * frcp(DLi);
+      D[i * S] = DLi;
+      DL[i * S] = f;
+      DU[i * S] = Dn;
+      DU2[i * S] = DUn;
+      piv[i * S] = 1;
+      const double nd = fma(-f, Dn, DUi);
+      DUn = -f * DUn;
+      Dn = nd;
+    }
+    Di = Dn;
+    DUi = DUn;
+  }
+  D[(m - 1) * S] = Di;
+#pragma unroll 4
+  for (int i = 0; i < m; ++i) {  // keep pivots away from 0, store reciprocals
+    double v = D[i * S];
+    if (fabs(v) < pertol) v = copysign(pertol, v == 0.0 ? 1.0 : v);
+    D[i * S] = frcp(v);
+    b[i * S] = 1.0 + 0.5 * (double)((i * 7919u + seed * 104729u + 13u) % 1024u) * (1.0 / 1024.0);
+  }
+  double nrm = 0.0;
+  for (int it = 0; it < 2; ++it) {
+    double bi = b[0];
+#pragma unroll 4
+    for (int i = 0; i < m - 1; ++i) {
+      const double bn = b[(i + 1) * S];
+      const double l = DL[i * S];
+      if (piv[i * S] == 0) {
+        b[i * S] = bi;
+        bi = fma(-l, bi, bn);
+      } else {
+        b[i * S] = bn;
+        bi = fma(-l, bn, bi);
+      }
+    }
+    double x1 = bi * D[(m - 1) * S], x2 = 0.0;
+    b[(m - 1) * S] = x1;
+    nrm = x1 * x1;
+#pragma unroll 4
+    for (int i = m - 2; i >= 0; --i) {
+      const double x0 = (b[i * S] - DU[i * S] * x1 - DU2[i * S] * x2) * D[i * S];
+      b[i * S] = x0;
+      nrm = fma(x0, x0, nrm);
+      x2 = x1;
+      x1 = x0;
+    }
+    nrm = frcp(sqrt(nrm));
+    if (it < 1) {
+#pragma unroll 4
+      for (int i = 0; i < m; ++i) b[i * S] *= nrm;
+    }
+  }
+#pragma unroll 4
+  for (int i = 0; i < m; ++i) z[i] = b[i * S] * nrm;
+}
+
+// Back-transformation V = H_0 ... H_{m-3} Z for r columns of Z, NV columns per
+// warp at once (independent reductions interleaved), Q rows per lane (m <= 32 Q).
+template <int Q, int NV>
+__device__ __forceinline__ void backtr_warp(double *V, const double *A, const double *tau, int m, int r) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k0 = warp; k0 < r; k0 += nw * NV) {
+    double zr[NV][Q];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int k = k0 + v * nw;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int i = lane + 32 * q;
+        zr[v][q] = (k < r && i < m) ? V[(int64_t)k * m + i] : 0.0;
+      }
+    }
+    for (int j = m - 3; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      const double *vj = A + (int64_t)j * m;
+      double vv[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int i = lane + 32 * q;
+        vv[q] = (i > j && i < m) ? vj[i] : 0.0;
+      }
+      double s[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        s[v] = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) s[v] = fma(vv[q], zr[v][q], s[v]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double sv = s[v] * tj;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) zr[v][q] = fma(-sv, vv[q], zr[v][q]);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int k = k0 + v * nw;
+      if (k < r)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int i = lane + 32 * q;
+          if (i < m) V[(int64_t)k * m + i] = zr[v][q];
+        }
+    }
+  }
+}
+
+// Offset of reflector column j in the packed strictly-lower triangle (rows
+// j+1..m-1 stored contiguously; index with the row i > j directly).
+__device__ __forceinline__ int64_t refl_off(int j, int m) {
+  return (int64_t)j * m - (int64_t)j * (j + 1) / 2 - j - 1;
+}
+
+// Modified Gram-Schmidt of the r inverse-iteration vectors followed by the
+// back-transformation V = H_0 ... H_{m-3} Z, with the vectors held in
+// registers: vector k lives in warp k % nw, slot k / nw, rows lane + 32 q.
+// Per MGS step the owner warp normalises z_k and publishes it through a
+// double-buffered shared vector (one block barrier per step); every warp then
+// removes the z_k component from its later vectors (NV reductions interleaved).
+template <int Q, int NV, bool PACKED>
+__device__ __forceinline__ void orth_backtr(double *V, const double *A, const double *tau, int m, int r,
+                                            double *zbuf /* 2 x 32 Q doubles of shared memory */,
+                                            long long *dbg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double z[NV][Q];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int k = warp + v * nw;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = lane + 32 * q;
+      z[v][q] = (k < r && i < m) ? V[(int64_t)k * m + i] : 0.0;
+    }
+  }
+  for (int k = 0; k < r; ++k) {
+    double *zb = zbuf + (k & 1) * 32 * Q;
+    if (warp == k % nw) {
+      const int ov = k / nw;
+      double zk[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        zk[q] = 0.0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          if (v == ov) zk[q] = z[v][q];
+      }
+      double s2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) s2 = fma(zk[q], zk[q], s2);
+      const double inv = frcp(sqrt(warp_sum(s2)));
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        zk[q] *= inv;
+        zb[lane + 32 * q] = zk[q];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          if (v == ov) z[v][q] = zk[q];
+      }
+    }
+    __syncthreads();
+    double zk[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) zk[q] = zb[lane + 32 * q];
+    double s[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      s[v] = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) s[v] = fma(zk[q], z[v][q], s[v]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int kk = warp + v * nw;
+      if (kk > k && kk < r)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) z[v][q] = fma(-s[v], zk[q], z[v][q]);
+    }
+  }
+  if (dbg && threadIdx.x == 0) dbg[9] = clock64();
+  for (int j = m - 3; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    const double *vj = A + (PACKED ? refl_off(j, m) : (int64_t)j * m);
+    double vv[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = lane + 32 * q;
+      vv[q] = (i > j && i < m) ? vj[i] : 0.0;
+    }
+    double s[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      s[v] = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) s[v] = fma(vv[q], z[v][q], s[v]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const double sv = s[v] * tj;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) z[v][q] = fma(-sv, vv[q], z[v][q]);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int k = warp + v * nw;
+    if (k < r)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int i = lane + 32 * q;
+        if (i < m) V[(int64_t)k * m + i] = z[v][q];
+      }
+  }
+}
+
 constexpr int EIG_THREADS = 256;      // generic path
 constexpr int EIG_REG_THREADS = 512;  // register-tile path (m <= 128)
 constexpr int EIG_REG_M = 128;
+// Householder tridiagonalisation Q^T G Q = T of one Gram matrix, m <= 128,
+// with G held in registers (thread (warp w, lane) owns the 4 x 8 tile
+// a[q][u] = G(32 q + lane, 8 w + u): rows strided by 32 so that the per-row
+// shared-memory vectors are conflict-free).  A separate kernel so that the
+// tile has the whole 128-register budget (no spills).  Output, in the task's
+// global scratch at work + 6 m^2: d[128] | e[128] | tau[128] | ||G||_F^2 |
+// (pad) | the packed reflectors (m (m - 1) / 2, refl_off layout), consumed by
+// k_eig_t<true>.
+template <bool PROF>
+__global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTask *__restrict__ tasks, double eps,
+                                                                    long long *prof, int variant = 0) {
+  long long pt[6] = {0, 0, 0, 0, 0, 0}, pc = 0;
+#define TRID_PROF(i)                  \
+  if constexpr (PROF) {               \
+    const long long tn = clock64();   \
+    pt[i] += tn - pc;                 \
+    pc = tn;                          \
+  }
+  __shared__ double s_red[32];
+  __shared__ double d[EIG_REG_M + 8], e[EIG_REG_M + 8], tau[EIG_REG_M + 8];
+  const EigTask t = tasks[blockIdx.x];
+  const int m = t.m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double *out = t.work + 6 * (int64_t)m * m;
+  double *A = out + 4 * EIG_REG_M;   // packed reflectors (global)
+  double a[4][8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = 32 * q + lane, c = 8 * warp + u;
+      a[q][u] = (r < m && c < m) ? t.G[r + (int64_t)c * m] : 0.0;
+    }
+  double fro = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) fro = fma(a[q][u], a[q][u], fro);
+  fro = warp_sum(fro);
+  if (lane == 0) s_red[warp] = fro;
+  __syncthreads();
+  fro = 0;
+  for (int w = 0; w < 16; ++w) fro += s_red[w];
+  __syncthreads();
+  if (tid == 0) out[3 * EIG_REG_M] = fro;
+  if (!(fro > 0.0) || eps == 0.0) return;
+  // ---- 1 (register tile). Householder tridiagonalisation, m <= 128 ----
+  // A lives in registers (4 x 8 per thread, 512 threads); per step k the warp
+  // owning column k forms v (written to shared memory, double-buffered, and
+  // into column k of A_sm for the back-transformation), every thread forms its
+  // 4 partial row sums of A v, rows reduce over the 16 column strips, and the
+  // rank-2 update is register-only.  v and p vanish outside rows/cols > k, so
+  // no predication is needed.  3 barriers per step.
+  __shared__ double vbuf[2][EIG_REG_M];              // v (two buffers, 128 rows each)
+  double *vsm0 = vbuf[0], *vsm1 = vbuf[1];
+  __shared__ double pbuf[2][EIG_REG_M];              // p (two buffers)
+  double *psm0 = pbuf[0], *psm1 = pbuf[1];
+  __shared__ double ps_part[16][EIG_REG_M];
+  __shared__ double colbuf[EIG_REG_M];               // column k+1 before update k
+  // Householder vector of column kk from its (updated) entries col[q] = A(4 lane + q, kk),
+  // run by the owner warp kk >> 3: v into the shared buffer, the packed reflector
+  // store, tau and the off-diagonal beta.
+  auto form_v = [&](int kk, const double *col) {
+    double *vs = (kk & 1) ? vsm1 : vsm0;
+    double s2 = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = 32 * q + lane;
+      if (r >= kk + 2 && r < m) s2 = fma(col[q], col[q], s2);
+    }
+    s2 = warp_sum(s2);
+    const int rx = kk + 1;
+    double x0 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (32 * q + lane == rx) x0 = col[q];
+    x0 = __shfl_sync(0xffffffffu, x0, rx & 31);
+    double beta = x0, scal = 0.0, tk = 0.0;
+    if (s2 != 0.0) {
+      beta = -copysign(sqrt(fma(x0, x0, s2)), x0);
+      tk = (beta - x0) * frcp(beta);
+      scal = frcp(x0 - beta);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = 32 * q + lane;
+      double v = 0.0;
+      if (s2 != 0.0) v = (r == rx) ? 1.0 : ((r > rx && r < m) ? col[q] * scal : 0.0);
+      vs[r] = v;
+      if (r > kk && r < m) A[refl_off(kk, m) + r] = v;   // packed strictly-lower triangle
+    }
+    if (lane == 0) {
+      tau[kk] = tk;
+      e[kk] = beta;
+    }
+  };
+  // Per step k (after the barrier that publishes v_k): partial row sums of
+  // A v over the warp's 8 columns and this tile's share of v^T A v (warp
+  // reduced) -> barrier -> 128 threads finish p = tau A v -> barrier -> the
+  // rank-2 update A -= v w^T + w v^T (w = p + alpha v).  Look-ahead: the warp
+  // owning column k+1 updates that column first and forms v_{k+1} while the
+  // other warps are still updating, so the v barrier costs no extra latency.
+  if (warp == 0 && m > 2) {
+    double col[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) col[q] = a[q][0];
+    form_v(0, col);
+  }
+  __syncthreads();
+  if constexpr (PROF) pc = clock64();
+  for (int k = 0; k < m - 2; ++k) {
+    const double *vs = (k & 1) ? vsm1 : vsm0;
+    double *ps = (k & 1) ? psm1 : psm0;
+    const double tk = tau[k];
+    // Only the trailing block changes: a warp whose 8 columns are all <= k, or
+    // a row group q whose 32 rows are all <= k, multiplies / updates by exact
+    // zeros (v and the masked p vanish there), so it is skipped (bitwise the
+    // same result, ~1/3 of the full-tile FP64 work on average).
+    const bool wact = 8 * warp + 7 > k && variant != 4 && variant != 6;
+    if (warp == ((k + 1) >> 3) && k + 1 < m - 2) {
+      // owner of column k+1 publishes it (as of before update k) for the form warp
+      const int u1 = (k + 1) & 7;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        double c = a[q][0];
+#pragma unroll
+        for (int u = 1; u < 8; ++u) c = (u1 == u) ? a[q][u] : c;
+        colbuf[32 * q + lane] = c;
+      }
+    }
+    if (wact) {
+    double vc[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) vc[u] = vs[8 * warp + u];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (32 * q + 31 <= k) continue;   // rows masked out of p, v_r = 0
+      double s0 = 0, s1 = 0;
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        s0 = fma(a[q][u], vc[u], s0);
+        s1 = fma(a[q][u + 1], vc[u + 1], s1);
+      }
+      ps_part[warp][32 * q + lane] = s0 + s1;
+    }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ps_part[warp][32 * q + lane] = 0.0;
+    }
+
+    TRID_PROF(0)
+    if (variant != 3) __syncthreads();                            // (2) partials visible
+    TRID_PROF(1)
+    if (tid < EIG_REG_M && variant != 2) {
+      double h[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) h[w] = ps_part[w][tid] + ps_part[w + 8][tid];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) h[w] += h[w + 4];
+      const double sacc = (h[0] + h[2]) + (h[1] + h[3]);
+      const double pi = (tid > k && tid < m) ? tk * sacc : 0.0;
+      ps[tid] = pi;
+      // p.v over the 128 rows: 4 warp reductions (shuffles are a shared,
+      // low-throughput resource; 16 warps reducing would cost ~4x more)
+      const double pvw = warp_sum(pi * vs[tid]);
+      if (lane == 0) s_red[warp] = pvw;
+    }
+    TRID_PROF(2)
+    if (variant != 3) __syncthreads();                            // (3) p visible
+    TRID_PROF(3)
+    const double pv = (s_red[0] + s_red[1]) + (s_red[2] + s_red[3]);
+    const double alpha = -0.5 * tk * pv;
+    // (vr, wr, v_c, w_c are re-read from shared memory here: with the 32-double
+    // tile live, keeping them in registers across form_v would spill)
+    const double *psc = ps + 8 * warp, *vsc = vs + 8 * warp;
+    if (8 * warp + 7 > k && variant != 5 && variant != 6) {
+      double vq[4], wq[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        vq[q] = vs[32 * q + lane];
+        wq[q] = fma(alpha, vq[q], ps[32 * q + lane]);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double vcu = vsc[u], wcu = fma(alpha, vcu, psc[u]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (32 * q + 31 > k) a[q][u] = fma(-vq[q], wcu, fma(-wq[q], vcu, a[q][u]));
+      }
+    }
+    const int k1 = k + 1;
+    // v_{k+1} is formed by a warp whose own columns are finished (warp 0 once
+    // k >= 7; warp 15 before), from the published column and the same update
+    // formula the owner applies in registers (bitwise the same column), so it
+    // overlaps the other warps' updates instead of trailing the owner's.
+    if (warp == (k1 >= 8 ? 0 : 15) && k1 < m - 2 && variant != 1 && variant != 6) {
+      const double vcu = vs[k1], wcu = fma(alpha, vcu, ps[k1]);
+      double col[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double vq = vs[32 * q + lane], wq = fma(alpha, vq, ps[32 * q + lane]);
+        col[q] = fma(-vq, wcu, fma(-wq, vcu, colbuf[32 * q + lane]));
+      }
+      form_v(k1, col);
+    }
+    TRID_PROF(4)
+    __syncthreads();                                              // (1) v_{k+1} visible
+    TRID_PROF(5)
+  }
+  if constexpr (PROF) {
+    if (lane == 0)
+      for (int i = 0; i < 6; ++i) prof[warp * 8 + i] = pt[i];
+  }
+#undef TRID_PROF
+  // diagonal and last sub-diagonal from the register tiles
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = 32 * q + lane, c = 8 * warp + u;
+      if (r < m && r == c) d[r] = a[q][u];
+      if (m >= 2 && r == m - 1 && c == m - 2) e[m - 2] = a[q][u];
+    }
+  if (tid == 0) {
+    e[m - 1] = 0.0;
+    if (m >= 2) tau[m - 2] = 0.0;
+    tau[m - 1] = 0.0;
+  }
+  __syncthreads();
+  for (int i = tid; i < m; i += blockDim.x) {
+    out[i] = d[i];
+    out[EIG_REG_M + i] = e[i];
+    out[2 * EIG_REG_M + i] = tau[i];
+  }
+}
+
 template <bool REG>
 __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
     k_eig_t(const EigTask *__restrict__ tasks, double eps, int smem_cap_doubles, int *status) {
@@ -436,17 +973,7 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
   double *A = (REG || (int64_t)m * m + 6 * mp + ml <= smem_cap_doubles) ? lam + ml
                                                                         : t.work + 6 * (int64_t)m * m;
   double *scr = t.work;  // 6 m^2: inverse-iteration scratch
-  // REG: thread (warp w, lane) holds the 4 x 8 tile a[q][u] = G(4 lane + q, 8 w + u)
-  double a[4][8];
-  if constexpr (REG) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int r = 4 * lane + q, c = 8 * warp + u;
-        a[q][u] = (r < m && c < m) ? t.G[r + (int64_t)c * m] : 0.0;
-      }
-  } else {
+  if constexpr (!REG) {
     for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) A[q] = t.G[q];
     __syncthreads();
   }
@@ -463,14 +990,11 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
   };
   double fro = 0;
   if constexpr (REG) {
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int u = 0; u < 8; ++u) fro = fma(a[q][u], a[q][u], fro);
+    fro = t.work[6 * (int64_t)m * m + 3 * EIG_REG_M];   // ||G||_F^2 from k_tridiag_reg
   } else {
     for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) fro += A[q] * A[q];
+    fro = bsum(fro);
   }
-  fro = bsum(fro);
   if (!(fro > 0.0)) {
     if (tid == 0) *t.rank_out = 0;
     for (int q = tid; q < m; q += blockDim.x) t.sig[q] = 0.0;
@@ -483,120 +1007,18 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
     return;
   }
   if constexpr (REG) {
-  // ---- 1 (register tile). Householder tridiagonalisation, m <= 128 ----
-  // A lives in registers (4 x 8 per thread, 512 threads); per step k the warp
-  // owning column k forms v (written to shared memory, double-buffered, and
-  // into column k of A_sm for the back-transformation), every thread forms its
-  // 4 partial row sums of A v, rows reduce over the 16 column strips, and the
-  // rank-2 update is register-only.  v and p vanish outside rows/cols > k, so
-  // no predication is needed.  3 barriers per step.
-  double *vsm0 = vt, *vsm1 = pw;                     // v (two buffers)
-  double *psm0 = lam, *psm1 = lam + 128;             // p (two buffers)
-  double *psum = t.work + 6 * (int64_t)m * m;        // unused (register path uses smem below)
-  (void)psum;
-  __shared__ double ps_part[16][EIG_REG_M + 1];
-  for (int k = 0; k < m - 2; ++k) {
-    double *vs = (k & 1) ? vsm1 : vsm0;
-    double *ps = (k & 1) ? psm1 : psm0;
-    const int wk = k >> 3, uk = k & 7;
-    double tk = 0.0;
-    if (warp == wk) {
-      double col[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        col[q] = 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (u == uk) col[q] = a[q][u];
-      }
-      double s2 = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = 4 * lane + q;
-        if (r >= k + 2 && r < m) s2 = fma(col[q], col[q], s2);
-      }
-      s2 = warp_sum(s2);
-      const int rx = k + 1;
-      double x0 = 0.0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (4 * lane + q == rx) x0 = col[q];
-      x0 = __shfl_sync(0xffffffffu, x0, rx >> 2);
-      double beta = x0, scal = 0.0;
-      if (s2 != 0.0) {
-        beta = -copysign(sqrt(x0 * x0 + s2), x0);
-        tk = (beta - x0) * frcp(beta);
-        scal = frcp(x0 - beta);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = 4 * lane + q;
-        double v = 0.0;
-        if (s2 != 0.0) v = (r == rx) ? 1.0 : ((r > rx && r < m) ? col[q] * scal : 0.0);
-        vs[r] = v;
-        if (r > k && r < m) A[r + (int64_t)k * m] = v;
-      }
-      if (lane == 0) {
-        tau[k] = tk;
-        e[k] = beta;
-      }
+  // ---- 1 (register tile): done by k_tridiag_reg; load T and the reflectors ----
+  {
+    const double *in = t.work + 6 * (int64_t)m * m;
+    for (int i = tid; i < m; i += blockDim.x) {
+      d[i] = in[i];
+      e[i] = in[EIG_REG_M + i];
+      tau[i] = in[2 * EIG_REG_M + i];
     }
-    __syncthreads();                                              // (1) v visible
-    tk = tau[k];
-    // partial row sums over this warp's 8 columns
-    double vc[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) vc[u] = vs[8 * warp + u];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double sacc = 0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) sacc = fma(a[q][u], vc[u], sacc);
-      ps_part[warp][4 * lane + q] = sacc;
-    }
-    __syncthreads();                                              // (2) partials visible
-    double pvp = 0;
-    if (tid < EIG_REG_M) {
-      double sacc = 0;
-#pragma unroll
-      for (int w = 0; w < 16; ++w) sacc += ps_part[w][tid];
-      const double pi = (tid > k && tid < m) ? tk * sacc : 0.0;
-      ps[tid] = pi;
-      pvp = pi * vs[tid];
-    }
-    pvp = warp_sum(pvp);
-    if (lane == 0) s_red[warp] = pvp;
-    __syncthreads();                                              // (3) p, p.v visible
-    double pv = 0;
-#pragma unroll
-    for (int w = 0; w < 16; ++w) pv += s_red[w];
-    const double alpha = -0.5 * tk * pv;
-    double wc[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) wc[u] = fma(alpha, vc[u], ps[8 * warp + u]);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = 4 * lane + q;
-      const double vr = vs[r], wr = fma(alpha, vr, ps[r]);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) a[q][u] -= fma(vr, wc[u], wr * vc[u]);
-    }
+    const int64_t np = (int64_t)m * (m - 1) / 2;
+    for (int64_t q = tid; q < np; q += blockDim.x) A[q] = in[4 * EIG_REG_M + q];
+    __syncthreads();
   }
-  // diagonal and last sub-diagonal from the register tiles
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int r = 4 * lane + q, c = 8 * warp + u;
-      if (r < m && r == c) d[r] = a[q][u];
-      if (m >= 2 && r == m - 1 && c == m - 2) e[m - 2] = a[q][u];
-    }
-  if (tid == 0) {
-    e[m - 1] = 0.0;
-    if (m >= 2) tau[m - 2] = 0.0;
-    tau[m - 1] = 0.0;
-  }
-  __syncthreads();
   } else {
   // ---- 1. Householder tridiagonalisation (thread per row) ----
   // step k: v from column k (its squared norm below x0 comes from the previous
@@ -770,11 +1192,9 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
     }
   }
   __syncthreads();
+  if (t.dbg && tid == 0) t.dbg[10] = clock64();
   const int ncomp = s_int[0];
-  for (int k = 1 + warp; k < ncomp; k += nw) {
-    double lk = warp_eig_asc(d, e2, m, m - 1 - k, gl, gu, pivmin);
-    if (lane == 0) lam[k] = lk * bnorm;
-  }
+  grp_multisect<4>(d, e2, m, 1, ncomp, gl, gu, pivmin, lam, bnorm);
   __syncthreads();
   // restore T (inverse iteration works on the unscaled tridiagonal)
   for (int i = tid; i < m; i += blockDim.x) d[i] *= bnorm;
@@ -790,6 +1210,29 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
   // separated by pertol), then the r vectors are orthonormalised (MGS): mixing
   // kept vectors leaves the kept subspace unchanged.
   const double pertol = 10.0 * 2.2e-16 * bnorm;
+  const bool a_in_smem = REG || (int64_t)m * m + 6 * mp + ml <= smem_cap_doubles;
+  const int64_t used = 6 * (int64_t)mp + ml + (REG ? (int64_t)m * (m - 1) / 2 : (a_in_smem ? (int64_t)m * m : 0));
+  const int64_t per = 5 * (int64_t)m + (m + 7) / 8;   // doubles per vector (5 arrays + piv bytes)
+  const int64_t avail = (int64_t)smem_cap_doubles - used;
+  if (avail >= per) {
+    // batches of nbv vectors with their LU / right-hand side in shared memory
+    const int nbv = (int)min(min(avail / per, (int64_t)r), (int64_t)blockDim.x);
+    double *ws = sh + used;
+    for (int k0 = 0; k0 < r; k0 += nbv) {
+      const int nb = min(nbv, r - k0);
+      const int kk = tid;
+      if (kk < nb) {
+        const int k = k0 + kk;
+        double sft = lam[k];
+        for (int q = 1; q <= k && lam[k - q] - lam[k] < pertol; ++q) sft -= pertol;
+        double *DL = ws + kk, *Dv = DL + (int64_t)m * nb, *DU = Dv + (int64_t)m * nb, *DU2 = DU + (int64_t)m * nb,
+               *bb = DU2 + (int64_t)m * nb;
+        unsigned char *pv = reinterpret_cast<unsigned char *>(ws + 5 * (int64_t)m * nb) + kk;
+        invit_one(d, e, m, sft, pertol, k, DL, Dv, DU, DU2, bb, pv, nb, t.V + (int64_t)k * m);
+      }
+      __syncthreads();
+    }
+  } else
   for (int k = tid; k < r; k += blockDim.x) {
     // interleaved scratch: element i of vector k at [i * r + k] (coalesced across threads)
     const int64_t RR = r;
@@ -875,6 +1318,29 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
     for (int i = 0; i < m; ++i) z[i] = b[(i) * RR];
   }
   __syncthreads();
+  // ---- 4b/5. orthonormalisation + back-transformation V = H_0 ... H_{m-3} Z ----
+  {
+    if (t.dbg && tid == 0) t.dbg[8] = clock64();
+    double *s_zb = lam;   // eigenvalues are no longer needed (2 x 32 Q <= 512 doubles)
+    const int per_w = (r + nw - 1) / nw;
+    if (REG || m <= 64) {
+      // register-resident vectors (REG: m <= 128, 16 warps; generic: m <= 64, 8 warps)
+      if (REG) {
+        if (per_w > 4) orth_backtr<4, 8, true>(t.V, A, tau, m, r, s_zb, t.dbg);
+        else if (per_w > 2) orth_backtr<4, 4, true>(t.V, A, tau, m, r, s_zb, t.dbg);
+        else if (per_w > 1) orth_backtr<4, 2, true>(t.V, A, tau, m, r, s_zb, t.dbg);
+        else orth_backtr<4, 1, true>(t.V, A, tau, m, r, s_zb, t.dbg);
+      } else {
+        if (per_w > 4) orth_backtr<2, 8, false>(t.V, A, tau, m, r, s_zb, t.dbg);
+        else if (per_w > 2) orth_backtr<2, 4, false>(t.V, A, tau, m, r, s_zb, t.dbg);
+        else if (per_w > 1) orth_backtr<2, 2, false>(t.V, A, tau, m, r, s_zb, t.dbg);
+        else orth_backtr<2, 1, false>(t.V, A, tau, m, r, s_zb, t.dbg);
+      }
+      __syncthreads();
+      if (t.dbg && tid == 0) t.dbg[3] = t.dbg[4] = clock64();
+      return;
+    }
+  }
   // modified Gram-Schmidt over the r vectors (warps over later vectors)
   for (int k = 0; k < r; ++k) {
     double *zk = t.V + (int64_t)k * m;
@@ -897,32 +1363,9 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
   if (t.dbg && tid == 0) t.dbg[3] = clock64();
   // ---- 5. back-transformation V = H_0 ... H_{m-3} Z ----
   if (m <= 256) {
-    for (int k = warp; k < r; k += nw) {
-      double *z = t.V + (int64_t)k * m;
-      double zr[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) zr[q] = (lane + 32 * q < m) ? z[lane + 32 * q] : 0.0;
-      for (int j = m - 3; j >= 0; --j) {
-        const double tj = tau[j];
-        if (tj == 0.0) continue;
-        const double *v = A + (int64_t)j * m;  // v_j in rows j+1.. of column j
-        double s2 = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          int i = lane + 32 * q;
-          if (i > j && i < m) s2 = fma(v[i], zr[q], s2);
-        }
-        s2 = warp_sum(s2) * tj;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          int i = lane + 32 * q;
-          if (i > j && i < m) zr[q] -= s2 * v[i];
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (lane + 32 * q < m) z[lane + 32 * q] = zr[q];
-    }
+    const int per_w = (r + nw - 1) / nw;
+    if (per_w >= 2) backtr_warp<8, 2>(t.V, A, tau, m, r);
+    else backtr_warp<8, 1>(t.V, A, tau, m, r);
   } else {
     for (int k = warp; k < r; k += nw) {
       double *z = t.V + (int64_t)k * m;

@@ -49,6 +49,19 @@ struct Err {
 };
 
 static const int SMEM_LIMIT = 226 * 1024;  // dynamic; leaves room for static smem
+static const int EIG_REG_MIN = 65;
+static const size_t EIG_REG_SMEM = 200 * 1024;
+// generic eigen path: shared memory for d/e/tau/..., A when it fits, and an
+// inverse-iteration batch of 16 vectors (5 m doubles + m bytes each)
+static int eig_generic_cap(int m) {
+  const int64_t mp = (m + 8) & ~7;
+  const int64_t base = 6 * mp + std::max(m, 512);
+  const int64_t per = 5 * (int64_t)m + (m + 7) / 8;
+  const int64_t withA = base + (int64_t)m * m + 16 * per;
+  const int64_t lim = SMEM_LIMIT / 8;
+  if (withA <= lim) return (int)withA;
+  return (int)lim;   // A in global scratch; the rest of the 226 KB serves the batches
+}
 
 // growable device buffer; growth synchronises the stream first (no in-flight use)
 struct DevBuf {
@@ -311,7 +324,7 @@ void ensure_mem(lorasp_ctx *h) {
   h->d_dotpart.ensure((DOT_BLOCKS + 64) * sizeof(double), h->stream);
   h->stg.init(size_t(64) << 20, h->stream);
   CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-  CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EIG_REG_SMEM));
   CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
@@ -372,16 +385,18 @@ void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::v
 // eigen tasks: 64 < m <= 128 -> register-tile kernel (512 threads); otherwise
 // the generic shared/global-memory kernel (faster for small m, measured with
 // tools/eig_cmp.py)
-static const int EIG_REG_MIN = 65;
+
 
 void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int max_m, int cap) {
   std::vector<EigTask> small, big;
   for (const EigTask &e : et) ((e.m >= EIG_REG_MIN && e.m <= EIG_REG_M) ? small : big).push_back(e);
   if (!small.empty()) {
     EigTask *ds = big.empty() ? de : push(h, small);
-    int m1 = 0;
-    for (auto &e : small) m1 = std::max(m1, e.m);
-    size_t sm = (size_t)(6 * (m1 + 8) + 512 + (int64_t)m1 * m1) * 8;
+    // register-tile path: the whole 200 KB (A + the inverse-iteration batches)
+    const size_t sm = EIG_REG_SMEM;
+    k_tridiag_reg<false><<<(unsigned)small.size(), EIG_REG_THREADS, 0, h->stream>>>(ds, h->plan.eps, nullptr);
+    ++h->launches_factor;
+    CK(cudaGetLastError());
     k_eig_t<true><<<(unsigned)small.size(), EIG_REG_THREADS, sm, h->stream>>>(ds, h->plan.eps, (int)(sm / 8),
                                                                                h->d_status.as<int>());
     ++h->launches_factor;
@@ -389,12 +404,15 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
   }
   if (!big.empty()) {
     EigTask *db = small.empty() ? de : push(h, big);
-    k_eig_t<false><<<(unsigned)big.size(), EIG_THREADS, cap * 8, h->stream>>>(db, h->plan.eps, cap,
-                                                                             h->d_status.as<int>());
+    int mb = 0;
+    for (auto &e : big) mb = std::max(mb, e.m);
+    k_eig_t<false><<<(unsigned)big.size(), EIG_THREADS, (size_t)eig_generic_cap(mb) * 8, h->stream>>>(
+        db, h->plan.eps, eig_generic_cap(mb), h->d_status.as<int>());
     ++h->launches_factor;
     CK(cudaGetLastError());
   }
   (void)max_m;
+  (void)cap;
 }
 
 void launch_copy(lorasp_ctx *h, const std::vector<CopyTask> &tasks, int cls) {
@@ -1759,7 +1777,7 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
   try {
     CK(cudaSetDevice(device));
     CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-    CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EIG_REG_SMEM));
     CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
     double *dG, *dV, *dS, *dW;
     int *dr, *dst;
@@ -1783,8 +1801,8 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     e.rank_out = dr;
     long long *ddbg = nullptr;
     if (getenv("LORASP_EIG_PROFILE")) {
-      CK(cudaMalloc(&ddbg, 128));
-      CK(cudaMemset(ddbg, 0, 128));
+      CK(cudaMalloc(&ddbg, 4096));
+      CK(cudaMemset(ddbg, 0, 4096));
     }
     e.dbg = ddbg;
     EigTask *de;
@@ -1795,12 +1813,55 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
       cap = std::max(cap, 2 * m);
       k_jacobi<<<1, 512, cap * 8>>>(de, eps, cap, dst);
     } else {
-      int cap = (int)std::min<int64_t>((int64_t)m * m + 6 * (m + 8) + std::max(m, 512), SMEM_LIMIT / 8);
-      cap = std::max(cap, 6 * (m + 8) + std::max(m, 512));
-      if (m >= EIG_REG_MIN && m <= EIG_REG_M && !getenv("LORASP_EIG_GENERIC"))
-        k_eig_t<true><<<1, EIG_REG_THREADS, cap * 8>>>(de, eps, cap, dst);
+      if (m >= EIG_REG_MIN && m <= EIG_REG_M && !getenv("LORASP_EIG_GENERIC")) {
+        if (ddbg) {
+          long long *dprof;
+          CK(cudaMalloc(&dprof, 16 * 8 * 8));
+          k_tridiag_reg<true><<<1, EIG_REG_THREADS>>>(de, eps, dprof);
+          long long hp[128];
+          CK(cudaMemcpy(hp, dprof, sizeof(hp), cudaMemcpyDeviceToHost));
+          const char *nm[6] = {"ph2", "bar2", "ph3", "bar3", "ph4", "bar1"};
+          for (int w = 0; w < 16; ++w) {
+            fprintf(stderr, "  warp %2d:", w);
+            for (int i = 0; i < 6; ++i) fprintf(stderr, " %s %lld", nm[i], hp[w * 8 + i]);
+            fprintf(stderr, "\n");
+          }
+          cudaFree(dprof);
+          k_tridiag_reg<false><<<1, EIG_REG_THREADS>>>(de, eps, nullptr);   // warm-up (timing below)
+          CK(cudaDeviceSynchronize());
+        }
+        if (ddbg) {
+          for (int var = 1; var <= 6; ++var) {
+            cudaEvent_t f0, f1;
+            cudaEventCreate(&f0);
+            cudaEventCreate(&f1);
+            cudaEventRecord(f0);
+            k_tridiag_reg<false><<<1, EIG_REG_THREADS>>>(de, eps, nullptr, var);
+            cudaEventRecord(f1);
+            cudaEventSynchronize(f1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, f0, f1);
+            fprintf(stderr, "[k_tridiag_reg variant %d] %.1f us\n", var, 1e3 * ms);
+          }
+        }
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        k_tridiag_reg<false><<<1, EIG_REG_THREADS>>>(de, eps, nullptr);
+        cudaEventRecord(e1);
+        k_eig_t<true><<<1, EIG_REG_THREADS, EIG_REG_SMEM>>>(de, eps, (int)(EIG_REG_SMEM / 8), dst);
+        if (ddbg) {
+          float ms = 0;
+          cudaEventSynchronize(e1);
+          cudaEventElapsedTime(&ms, e0, e1);
+          fprintf(stderr, "[k_tridiag_reg m=%d] %.1f us\n", m, 1e3 * ms);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+      }
       else
-        k_eig_t<false><<<1, EIG_THREADS, cap * 8>>>(de, eps, cap, dst);
+        k_eig_t<false><<<1, EIG_THREADS, (size_t)eig_generic_cap(m) * 8>>>(de, eps, eig_generic_cap(m), dst);
     }
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
@@ -1810,9 +1871,11 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     CK(cudaMemcpy(sigma, dS, m * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(V, dV, (size_t)m * (*rank) * 8, cudaMemcpyDeviceToHost));
     if (ddbg) {
-      long long tt[10];
+      long long tt[16];
       CK(cudaMemcpy(tt, ddbg, sizeof(tt), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "[tridiag phases] v %lld  matvec %lld  update %lld\n", tt[5], tt[6], tt[7]);
+      fprintf(stderr, "[tridiag phases] v %lld  matvec %lld  update %lld | invit %lld mgs %lld backtr %lld\n", tt[5],
+              tt[6], tt[7], tt[8] - tt[2], tt[9] - tt[8], tt[3] - tt[9]);
+      fprintf(stderr, "[eigvals] lambda0 %lld  rest %lld\n", tt[10] - tt[1], tt[2] - tt[10]);
       fprintf(stderr, "[eig m=%d r=%d] tridiag %lld  eigvals %lld  invit %lld  backtr %lld cycles\n", m, *rank,
               tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3]);
       cudaFree(ddbg);

@@ -1,0 +1,82 @@
+"""GPU unit parity of the compress eigen-solver (k_eig_t) through the C-ABI
+test hook `lorasp_test_eig`, on seeded Gram matrices G = M^T M of every size
+class the sweep launches (generic m < 65, register tile 65..128, generic
+129..256, > 256).
+
+Reference: the SVD of the stack M (numpy/LAPACK), i.e. Eq. lra (P:l.333-355)
+with the rank rule sigma_k >= eps sigma_0 (Eq. cutOff1, P:l.580-584):
+  * rank identical unless sigma_r or sigma_{r+1} lies within 1e-12 sigma_0 of
+    the threshold (north_star window);
+  * sigma_k / sigma_0 within 1e-12 for the kept values (Gram squaring gives
+    |d sigma| <= u sigma_0^2 / (2 sigma), far inside at sigma >= eps sigma_0);
+  * the kept subspace V_r V_r^T within 1e-8 (the spectra below have relative
+    gaps >= 5 % at the threshold, so the subspace is well conditioned);
+  * V_r^T V_r = I within 1e-12.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1510_07363_b200 import build, lorasp
+    build.build()
+    return lorasp
+
+
+def stack(m, rows, decay, seed):
+    rng = np.random.default_rng(seed)
+    Q1, _ = np.linalg.qr(rng.standard_normal((rows, m)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    s = decay ** np.arange(m)
+    return (Q1 * s) @ Q2.T
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 17, 40, 64, 65, 100, 128, 129, 160, 200, 256, 312])
+@pytest.mark.parametrize("eps", [1e-2, 1e-3])
+def test_eig_matches_svd(L, m, eps):
+    M = stack(m, 2 * m + 3, 0.9 if m > 40 else 0.7, seed=m)
+    G = M.T @ M
+    sig, V, r, st = L.test_eig(G, eps)
+    assert st == 0
+    s_ref = np.linalg.svd(M, compute_uv=False)
+    r_ref = int(np.sum(s_ref >= eps * s_ref[0]))
+    near = any(0 <= k < m and abs(s_ref[k] / s_ref[0] - eps) <= 1e-12 for k in (r_ref - 1, r_ref))
+    assert r == r_ref or near, (r, r_ref)
+    assert np.max(np.abs(sig[:r] - s_ref[:r])) <= 1e-12 * s_ref[0]
+    assert np.allclose(V.T @ V, np.eye(r), rtol=0, atol=1e-12)
+    _, _, Vt = np.linalg.svd(M)
+    Pr = Vt[:r].T @ Vt[:r]
+    assert np.max(np.abs(V @ V.T - Pr)) <= 1e-8
+
+
+@pytest.mark.parametrize("m", [50, 128, 200])
+def test_eig_clustered_and_degenerate(L, m):
+    """Repeated singular values (a cluster straddling nothing) and exact zeros:
+    the kept subspace is still the right one, the rank counts ties (>=)."""
+    rng = np.random.default_rng(7)
+    s = np.concatenate([np.full(m // 4, 3.0), np.full(m // 4, 1.0), np.zeros(m - 2 * (m // 4))])
+    Q1, _ = np.linalg.qr(rng.standard_normal((2 * m, m)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    M = (Q1 * s) @ Q2.T
+    sig, V, r, st = L.test_eig(M.T @ M, 0.2)
+    assert st == 0 and r == 2 * (m // 4)
+    _, _, Vt = np.linalg.svd(M)
+    Pr = Vt[:r].T @ Vt[:r]
+    assert np.max(np.abs(V @ V.T - Pr)) <= 1e-10
+    assert np.allclose(sig[:r], s[:r], rtol=1e-12, atol=0)
+
+
+def test_eig_zero_and_eps0(L):
+    sig, V, r, st = L.test_eig(np.zeros((70, 70)), 1e-2)
+    assert st == 0 and r == 0
+    G = stack(90, 200, 0.9, 3)
+    G = G.T @ G
+    sig, V, r, st = L.test_eig(G, 0.0)
+    assert st == 0 and r == 90 and np.array_equal(V, np.eye(90))
