@@ -14,6 +14,7 @@
 //  k_apply_fwd/bwd Alg. 3 / Alg. 4 (P:l.445-500) per colour wave
 //  Krylov helpers  CSR SpMV, deterministic dots, axpys
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -545,10 +546,17 @@ __device__ __forceinline__ void invit_one(const double *__restrict__ d, const do
   for (int i = 0; i < m; ++i) z[i] = b[i * S] * nrm;
 }
 
+// Offset of reflector column j in the packed strictly-lower triangle (rows
+// j+1..m-1 stored contiguously; index with the row i > j directly).
+__device__ __forceinline__ int64_t refl_off(int j, int m) {
+  return (int64_t)j * m - (int64_t)j * (j + 1) / 2 - j - 1;
+}
+
 // Back-transformation V = H_0 ... H_{m-3} Z for r columns of Z, NV columns per
 // warp at once (independent reductions interleaved), Q rows per lane (m <= 32 Q).
 template <int Q, int NV>
-__device__ __forceinline__ void backtr_warp(double *V, const double *A, const double *tau, int m, int r) {
+__device__ __forceinline__ void backtr_warp(double *V, const double *A, const double *tau, int m, int r,
+                                            bool packed) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k0 = warp; k0 < r; k0 += nw * NV) {
     double zr[NV][Q];
@@ -564,7 +572,7 @@ __device__ __forceinline__ void backtr_warp(double *V, const double *A, const do
     for (int j = m - 3; j >= 0; --j) {
       const double tj = tau[j];
       if (tj == 0.0) continue;
-      const double *vj = A + (int64_t)j * m;
+      const double *vj = A + (packed ? refl_off(j, m) : (int64_t)j * m);
       double vv[Q];
 #pragma unroll
       for (int q = 0; q < Q; ++q) {
@@ -602,12 +610,6 @@ __device__ __forceinline__ void backtr_warp(double *V, const double *A, const do
   }
 }
 
-// Offset of reflector column j in the packed strictly-lower triangle (rows
-// j+1..m-1 stored contiguously; index with the row i > j directly).
-__device__ __forceinline__ int64_t refl_off(int j, int m) {
-  return (int64_t)j * m - (int64_t)j * (j + 1) / 2 - j - 1;
-}
-
 // Modified Gram-Schmidt of the r inverse-iteration vectors followed by the
 // back-transformation V = H_0 ... H_{m-3} Z, with the vectors held in
 // registers: vector k lives in warp k % nw, slot k / nw, rows lane + 32 q.
@@ -617,7 +619,7 @@ __device__ __forceinline__ int64_t refl_off(int j, int m) {
 template <int Q, int NV, bool PACKED>
 __device__ __forceinline__ void orth_backtr(double *V, const double *A, const double *tau, int m, int r,
                                             double *zbuf /* 2 x 32 Q doubles of shared memory */,
-                                            long long *dbg) {
+                                            long long *dbg, double *stg = nullptr, int stg_cap = 0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   double z[NV][Q];
 #pragma unroll
@@ -678,10 +680,24 @@ __device__ __forceinline__ void orth_backtr(double *V, const double *A, const do
     }
   }
   if (dbg && threadIdx.x == 0) dbg[9] = clock64();
-  for (int j = m - 3; j >= 0; --j) {
+  // Reflectors in global memory (stg != nullptr): staged into shared memory in
+  // chunks of ch columns (one contiguous packed segment per chunk, copied by
+  // the whole block), so the per-reflector loads are shared-memory hits.
+  const int ch = stg ? max(1, stg_cap / max(m, 1)) : m;
+  for (int jc = m - 3; jc >= 0; jc -= ch) {
+    const int jl = max(0, jc - ch + 1);
+    const double *base = A;
+    if (stg) {
+      const int64_t lo = refl_off(jl, m) + jl + 1, hi = refl_off(jc, m) + m;
+      __syncthreads();
+      for (int64_t q = lo + threadIdx.x; q < hi; q += blockDim.x) stg[q - lo] = A[q];
+      __syncthreads();
+      base = stg - lo;
+    }
+  for (int j = jc; j >= jl; --j) {
     const double tj = tau[j];
     if (tj == 0.0) continue;
-    const double *vj = A + (PACKED ? refl_off(j, m) : (int64_t)j * m);
+    const double *vj = base + (PACKED ? refl_off(j, m) : (int64_t)j * m);
     double vv[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -706,6 +722,7 @@ __device__ __forceinline__ void orth_backtr(double *V, const double *A, const do
       for (int q = 0; q < Q; ++q) z[v][q] = fma(-sv, vv[q], z[v][q]);
     }
   }
+  }
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     const int k = warp + v * nw;
@@ -721,6 +738,9 @@ __device__ __forceinline__ void orth_backtr(double *V, const double *A, const do
 constexpr int EIG_THREADS = 256;      // generic path
 constexpr int EIG_REG_THREADS = 512;  // register-tile path (m <= 128)
 constexpr int EIG_REG_M = 128;
+// tridiagonal record (at work + 6 m^2): d | e | tau | fro, bnorm (pad to 4m) |
+// packed reflectors (m (m-1)/2) | kept eigenvalues lambda_0..lambda_{r-1}
+__host__ __device__ __forceinline__ int64_t rec_lam_off(int m) { return 4 * (int64_t)m + (int64_t)m * (m - 1) / 2; }
 // Householder tridiagonalisation Q^T G Q = T of one Gram matrix, m <= 128,
 // with G held in registers (thread (warp w, lane) owns the 4 x 8 tile
 // a[q][u] = G(32 q + lane, 8 w + u): rows strided by 32 so that the per-row
@@ -745,7 +765,7 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
   const int m = t.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double *out = t.work + 6 * (int64_t)m * m;
-  double *A = out + 4 * EIG_REG_M;   // packed reflectors (global)
+  double *A = out + 4 * (int64_t)m;   // packed reflectors (global)
   double a[4][8];
 #pragma unroll
   for (int q = 0; q < 4; ++q)
@@ -765,7 +785,7 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
   fro = 0;
   for (int w = 0; w < 16; ++w) fro += s_red[w];
   __syncthreads();
-  if (tid == 0) out[3 * EIG_REG_M] = fro;
+  if (tid == 0) out[3 * m] = fro;
   if (!(fro > 0.0) || eps == 0.0) return;
   // ---- 1 (register tile). Householder tridiagonalisation, m <= 128 ----
   // A lives in registers (4 x 8 per thread, 512 threads); per step k the warp
@@ -952,13 +972,292 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
   __syncthreads();
   for (int i = tid; i < m; i += blockDim.x) {
     out[i] = d[i];
-    out[EIG_REG_M + i] = e[i];
-    out[2 * EIG_REG_M + i] = tau[i];
+    out[m + i] = e[i];
+    out[2 * m + i] = tau[i];
   }
 }
 
-template <bool REG>
-__global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
+
+// DSMEM helpers: shared::cluster address of `p` in CTA `rank` of the cluster,
+// and 64-bit loads / stores through it (no generic-address window checks).
+__device__ __forceinline__ uint32_t dsm_addr(const void *p, int rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ double dsm_ld(uint32_t a) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void dsm_st(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+
+// ------------------------------------------- cluster tridiagonalisation ----
+// Householder tridiagonalisation of one Gram matrix with 128 < m <= 32 QR,
+// spread over a thread-block cluster of CL CTAs (distributed shared memory):
+// CTA j holds the column strip [16 UC j, 16 UC (j+1)) in registers (thread
+// (warp w, lane) owns a[q][u] = G(32 q + lane, 16 UC j + UC w + u)).  Per
+// step k:
+//   A  every active warp forms partial row sums of A v_k over its UC columns
+//      (finished tiles, all columns or all 32 rows <= k, are exact zeros and
+//      skipped); the owner warp of column k+1 publishes that column;
+//   B  block barrier, the CTA's partial (A v)_t, t < m (16-term tree);
+//   C  cluster barrier, p_t = tau_k sum_j pcta_j[t] read from every CTA in the
+//      same order (identical on all CTAs), masked to t > k; p.v reduced;
+//   D  rank-2 update of the strip; in the CTA owning column k+1 a warp whose
+//      columns are finished forms v_{k+1} (same update formula on the
+//      published column) and pushes v, tau to every CTA; cluster barrier.
+// Same numerics as k_tridiag_reg; output in the same tridiagonal record.
+// Dynamic shared memory: 21 * 32 QR doubles.
+template <int QR, int UC, int CL>
+__global__ void __launch_bounds__(512, 1) k_tridiag_cl(const EigTask *__restrict__ tasks, double eps,
+                                                       long long *prof = nullptr) {
+  long long pt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pc = 0;
+#define TCL_PROF(i)                                  \
+  if (prof && threadIdx.x == 0 && blockIdx.x == 0) { \
+    const long long tn = clock64();                  \
+    pt[i] += tn - pc;                                \
+    pc = tn;                                         \
+  }
+  constexpr int MMAX = 32 * QR;
+  constexpr int CW = 16 * UC;   // columns per CTA
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  // dynamic shared memory: vbuf[2][MMAX] | ps_part[16][MMAX] | pcta | psm | colbuf
+  extern __shared__ double dsh[];
+  double(*vbuf)[MMAX] = reinterpret_cast<double(*)[MMAX]>(dsh);
+  double(*ps_part)[MMAX] = reinterpret_cast<double(*)[MMAX]>(dsh + 2 * MMAX);
+  double *pcta = dsh + 18 * MMAX, *psm = dsh + 19 * MMAX, *colbuf = dsh + 20 * MMAX;
+  __shared__ double taub[2];
+  __shared__ double s_red[16];
+  __shared__ double s_fro[CL];
+  const EigTask t = tasks[blockIdx.x / CL];
+  const int m = t.m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c0 = rank * CW + warp * UC;   // first column of this warp
+  double *out = t.work + 6 * (int64_t)m * m;
+  double *A = out + 4 * (int64_t)m;        // packed reflectors (global)
+  // Exchanges go through L2 (global scratch at work[0..), free in this path):
+  // DSMEM serves ~1 thread-request per cycle per SM, too slow for the
+  // all-gather of CL partial vectors; coalesced L2 traffic is not.
+  double *xg = t.work;                                  // [2][CL][MMAX] partials of A v
+  double *vg = t.work + 2 * CL * MMAX;                  // [2][MMAX + 8] v and tau
+  double a[QR][UC];
+#pragma unroll
+  for (int q = 0; q < QR; ++q)
+#pragma unroll
+    for (int u = 0; u < UC; ++u) {
+      const int r = 32 * q + lane, c = c0 + u;
+      a[q][u] = (r < m && c < m) ? t.G[r + (int64_t)c * m] : 0.0;
+    }
+  // ||G||_F^2: CTA partial pushed to every CTA, summed in rank order
+  {
+    double f = 0;
+#pragma unroll
+    for (int q = 0; q < QR; ++q)
+#pragma unroll
+      for (int u = 0; u < UC; ++u) f = fma(a[q][u], a[q][u], f);
+    f = warp_sum(f);
+    if (lane == 0) s_red[warp] = f;
+    __syncthreads();
+    if (tid < CL) {
+      double fc = 0;
+      for (int w = 0; w < 16; ++w) fc += s_red[w];
+      *cl.map_shared_rank(&s_fro[rank], tid) = fc;
+    }
+    cl.sync();
+  }
+  double fro = 0;
+  for (int j = 0; j < CL; ++j) fro += s_fro[j];
+  if (rank == 0 && tid == 0) out[3 * m] = fro;
+  if (!(fro > 0.0) || eps == 0.0) return;   // uniform over the cluster
+
+  // v of column kk from its updated entries col[q] (rows 32 q + lane), by one
+  // warp: pushed (with tau) into every CTA of the cluster; e, tau and the
+  // packed reflector to the global record.
+  auto form_v = [&](int kk, const double *col) {
+    double s2 = 0;
+#pragma unroll
+    for (int q = 0; q < QR; ++q) {
+      const int r = 32 * q + lane;
+      if (r >= kk + 2 && r < m) s2 = fma(col[q], col[q], s2);
+    }
+    s2 = warp_sum(s2);
+    const int rx = kk + 1;
+    double x0 = 0.0;
+#pragma unroll
+    for (int q = 0; q < QR; ++q)
+      if (32 * q + lane == rx) x0 = col[q];
+    x0 = __shfl_sync(0xffffffffu, x0, rx & 31);
+    double beta = x0, scal = 0.0, tk = 0.0;
+    if (s2 != 0.0) {
+      beta = -copysign(sqrt(fma(x0, x0, s2)), x0);
+      tk = (beta - x0) * frcp(beta);
+      scal = frcp(x0 - beta);
+    }
+    const int b = kk & 1;
+#pragma unroll
+    for (int q = 0; q < QR; ++q) {
+      const int r = 32 * q + lane;
+      double v = 0.0;
+      if (s2 != 0.0) v = (r == rx) ? 1.0 : ((r > rx && r < m) ? col[q] * scal : 0.0);
+      vg[b * (MMAX + 8) + r] = v;   // every CTA reads it after the cluster barrier
+      if (r > kk && r < m) A[refl_off(kk, m) + r] = v;
+    }
+    if (lane == 0) vg[b * (MMAX + 8) + MMAX] = tk;
+    if (lane == 0) {
+      out[2 * m + kk] = tk;
+      out[m + kk] = beta;
+    }
+  };
+  // v_0: column 0 lives in CTA 0, warp 0, u = 0
+  // every CTA copies v_kk (and tau) from the CTA that formed it (pull: one
+  // remote load per thread instead of QR x CL serial remote stores in one warp)
+  auto pull_v = [&](int kk) {
+    const int b = kk & 1;
+    for (int r = tid; r < MMAX; r += blockDim.x) vbuf[b][r] = __ldcg(vg + b * (MMAX + 8) + r);
+    if (tid == 0) taub[b] = __ldcg(vg + b * (MMAX + 8) + MMAX);
+    __syncthreads();
+  };
+  if (rank == 0 && warp == 0 && m > 2) {
+    double col[QR];
+#pragma unroll
+    for (int q = 0; q < QR; ++q) col[q] = a[q][0];
+    form_v(0, col);
+  }
+  cl.sync();
+  if (m > 2) pull_v(0);
+  if (prof && threadIdx.x == 0 && blockIdx.x == 0) pc = clock64();
+  for (int k = 0; k < m - 2; ++k) {
+    const double *vs = vbuf[k & 1];
+    const double tk = taub[k & 1];
+    const int k1 = k + 1;
+    const bool own1 = k1 < m - 2 && k1 >= rank * CW && k1 < (rank + 1) * CW;   // column k+1 is ours
+    // ---- A ----
+    if (own1 && warp == (k1 - rank * CW) / UC) {
+      const int u1 = (k1 - rank * CW) % UC;
+#pragma unroll
+      for (int q = 0; q < QR; ++q) {
+        double c = a[q][0];
+#pragma unroll
+        for (int u = 1; u < UC; ++u) c = (u1 == u) ? a[q][u] : c;
+        colbuf[32 * q + lane] = c;
+      }
+    }
+    const bool wact = c0 + UC - 1 > k;
+    if (wact) {
+      double vc[UC];
+#pragma unroll
+      for (int u = 0; u < UC; ++u) vc[u] = (c0 + u < MMAX) ? vs[c0 + u] : 0.0;
+#pragma unroll
+      for (int q = 0; q < QR; ++q) {
+        if (32 * q + 31 <= k) continue;
+        double s0 = 0;
+#pragma unroll
+        for (int u = 0; u < UC; ++u) s0 = fma(a[q][u], vc[u], s0);
+        ps_part[warp][32 * q + lane] = s0;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < QR; ++q) ps_part[warp][32 * q + lane] = 0.0;
+    }
+    TCL_PROF(0)
+    __syncthreads();
+    TCL_PROF(1)
+    // ---- B ----
+    for (int r = tid; r < MMAX; r += blockDim.x) {
+      double h[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) h[w] = ps_part[w][r] + ps_part[w + 8][r];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) h[w] += h[w + 4];
+      xg[((k & 1) * CL + rank) * MMAX + r] = (h[0] + h[2]) + (h[1] + h[3]);
+    }
+    TCL_PROF(2)
+    cl.sync();
+    TCL_PROF(3)
+    // ---- C ----
+    if (tid < MMAX) {
+      double pj[CL];
+#pragma unroll
+      for (int j = 0; j < CL; ++j) pj[j] = __ldcg(xg + ((k & 1) * CL + j) * MMAX + tid);
+      double sacc = 0.0;
+#pragma unroll
+      for (int j = 0; j < CL; ++j) sacc += pj[j];
+      const double pi = (tid > k && tid < m) ? tk * sacc : 0.0;
+      psm[tid] = pi;
+      const double pvw = warp_sum(pi * vs[tid]);
+      if (lane == 0) s_red[warp] = pvw;
+    }
+    TCL_PROF(4)
+    __syncthreads();
+    double pv = 0.0;
+#pragma unroll
+    for (int w = 0; w < MMAX / 32; ++w) pv += s_red[w];
+    const double alpha = -0.5 * tk * pv;
+    // ---- D ----
+    if (wact) {
+      double vq[QR], wq[QR];
+#pragma unroll
+      for (int q = 0; q < QR; ++q) {
+        vq[q] = vs[32 * q + lane];
+        wq[q] = fma(alpha, vq[q], psm[32 * q + lane]);
+      }
+#pragma unroll
+      for (int u = 0; u < UC; ++u) {
+        const int c = c0 + u;
+        const double vcu = (c < MMAX) ? vs[c] : 0.0, wcu = fma(alpha, vcu, (c < MMAX) ? psm[c] : 0.0);
+#pragma unroll
+        for (int q = 0; q < QR; ++q)
+          if (32 * q + 31 > k) a[q][u] = fma(-vq[q], wcu, fma(-wq[q], vcu, a[q][u]));
+      }
+    }
+    if (own1) {
+      const int wo = (k1 - rank * CW) / UC;
+      if (warp == (wo >= 1 ? 0 : 15)) {
+        const double vcu = vs[k1], wcu = fma(alpha, vcu, psm[k1]);
+        double col[QR];
+#pragma unroll
+        for (int q = 0; q < QR; ++q) {
+          const double vq = vs[32 * q + lane], wq = fma(alpha, vq, psm[32 * q + lane]);
+          col[q] = fma(-vq, wcu, fma(-wq, vcu, colbuf[32 * q + lane]));
+        }
+        form_v(k1, col);
+      }
+    }
+    TCL_PROF(5)
+    cl.sync();
+    TCL_PROF(6)
+    if (k1 < m - 2) pull_v(k1);
+    TCL_PROF(7)
+  }
+  if (prof && threadIdx.x == 0 && blockIdx.x == 0)
+    for (int q = 0; q < 8; ++q) prof[q] = pt[q];
+#undef TCL_PROF
+  // diagonal and the last sub-diagonal from the register tiles
+#pragma unroll
+  for (int q = 0; q < QR; ++q)
+#pragma unroll
+    for (int u = 0; u < UC; ++u) {
+      const int r = 32 * q + lane, c = c0 + u;
+      if (r < m && r == c) out[r] = a[q][u];
+      if (m >= 2 && r == m - 1 && c == m - 2) out[m + m - 2] = a[q][u];
+    }
+  if (rank == 0 && tid == 0) {
+    out[m + m - 1] = 0.0;
+    if (m >= 2) out[2 * m + m - 2] = 0.0;
+    out[2 * m + m - 1] = 0.0;
+  }
+}
+
+// REG: tridiagonal record from k_tridiag_reg (m <= 128, reflectors copied to
+// shared memory); PRE: record from k_tridiag_cl (128 < m <= 512, reflectors
+// read from the global record); neither: tridiagonalise here (generic path).
+template <bool REG, bool PRE = false>
+__global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
     k_eig_t(const EigTask *__restrict__ tasks, double eps, int smem_cap_doubles, int *status) {
   extern __shared__ double sh[];
   __shared__ double s_red[32];
@@ -970,10 +1269,11 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
   const int ml = m > 512 ? m : 512;  // lam doubles as p-partials scratch during phase 1
   const int mp = (m + 8) & ~7;       // padded length (>= m + 1, multiple of 8)
   double *d = sh, *e = d + mp, *tau = e + mp, *e2 = tau + mp, *vt = e2 + mp, *pw = vt + mp, *lam = pw + mp;
-  double *A = (REG || (int64_t)m * m + 6 * mp + ml <= smem_cap_doubles) ? lam + ml
-                                                                        : t.work + 6 * (int64_t)m * m;
+  double *A = PRE ? t.work + 6 * (int64_t)m * m + 4 * (int64_t)m
+                 : ((REG || (int64_t)m * m + 6 * mp + ml <= smem_cap_doubles) ? lam + ml
+                                                                              : t.work + 6 * (int64_t)m * m);
   double *scr = t.work;  // 6 m^2: inverse-iteration scratch
-  if constexpr (!REG) {
+  if constexpr (!REG && !PRE) {
     for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) A[q] = t.G[q];
     __syncthreads();
   }
@@ -989,8 +1289,8 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
     return r;
   };
   double fro = 0;
-  if constexpr (REG) {
-    fro = t.work[6 * (int64_t)m * m + 3 * EIG_REG_M];   // ||G||_F^2 from k_tridiag_reg
+  if constexpr (REG || PRE) {
+    fro = t.work[6 * (int64_t)m * m + 3 * m];   // ||G||_F^2 from the tridiagonal record
   } else {
     for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) fro += A[q] * A[q];
     fro = bsum(fro);
@@ -1006,17 +1306,19 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
     if (tid == 0) *t.rank_out = m;
     return;
   }
-  if constexpr (REG) {
-  // ---- 1 (register tile): done by k_tridiag_reg; load T and the reflectors ----
+  if constexpr (REG || PRE) {
+  // ---- 1: done by k_tridiag_reg / k_tridiag_cl; load T (and, REG, the reflectors) ----
   {
     const double *in = t.work + 6 * (int64_t)m * m;
     for (int i = tid; i < m; i += blockDim.x) {
       d[i] = in[i];
-      e[i] = in[EIG_REG_M + i];
-      tau[i] = in[2 * EIG_REG_M + i];
+      e[i] = in[m + i];
+      tau[i] = in[2 * m + i];
     }
-    const int64_t np = (int64_t)m * (m - 1) / 2;
-    for (int64_t q = tid; q < np; q += blockDim.x) A[q] = in[4 * EIG_REG_M + q];
+    if constexpr (REG) {
+      const int64_t np = (int64_t)m * (m - 1) / 2;
+      for (int64_t q = tid; q < np; q += blockDim.x) A[q] = in[4 * (int64_t)m + q];
+    }
     __syncthreads();
   }
   } else {
@@ -1204,13 +1506,22 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
   for (int k = 0; k < ncomp; ++k) r += (sqrt(fmax(lam[k], 0.0)) >= eps * sig0);
   for (int k = tid; k < m; k += blockDim.x) t.sig[k] = (k < ncomp) ? sqrt(fmax(lam[k], 0.0)) : 0.0;
   if (tid == 0) *t.rank_out = r;
+  if constexpr (PRE) {
+    // PRE pipeline stage 0 ends here: the kept eigenvalues and ||T|| bound go to
+    // the tridiagonal record for k_invit_multi; MGS + back-transformation follow
+    // in k_orth_pre / k_backtr_multi.
+    double *rec = t.work + 6 * (int64_t)m * m;
+    for (int k = tid; k < r; k += blockDim.x) rec[rec_lam_off(m) + k] = lam[k];
+    if (tid == 0) rec[3 * m + 1] = bnorm;
+    return;
+  }
   if (t.dbg && tid == 0) t.dbg[2] = clock64();
   // ---- 4. inverse iteration, one thread per kept eigenvalue ----
   // Each vector is computed independently (shift lambda_k, equal shifts
   // separated by pertol), then the r vectors are orthonormalised (MGS): mixing
   // kept vectors leaves the kept subspace unchanged.
   const double pertol = 10.0 * 2.2e-16 * bnorm;
-  const bool a_in_smem = REG || (int64_t)m * m + 6 * mp + ml <= smem_cap_doubles;
+  const bool a_in_smem = !PRE && (REG || (int64_t)m * m + 6 * mp + ml <= smem_cap_doubles);
   const int64_t used = 6 * (int64_t)mp + ml + (REG ? (int64_t)m * (m - 1) / 2 : (a_in_smem ? (int64_t)m * m : 0));
   const int64_t per = 5 * (int64_t)m + (m + 7) / 8;   // doubles per vector (5 arrays + piv bytes)
   const int64_t avail = (int64_t)smem_cap_doubles - used;
@@ -1323,7 +1634,31 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
     if (t.dbg && tid == 0) t.dbg[8] = clock64();
     double *s_zb = lam;   // eigenvalues are no longer needed (2 x 32 Q <= 512 doubles)
     const int per_w = (r + nw - 1) / nw;
-    if (REG || m <= 64) {
+    if constexpr (PRE) {
+      // register-resident vectors, 16 warps, packed reflectors in global memory
+      double *zb = sh + 6 * (int64_t)mp + ml;   // inverse-iteration workspace (free now)
+      const int stg_cap = smem_cap_doubles - (6 * mp + ml) - 1024;   // reflector staging
+      bool done = true;
+      if (m <= 256 && per_w <= 4) {
+        if (per_w > 2) orth_backtr<8, 4, true>(t.V, A, tau, m, r, zb, t.dbg, zb + 1024, stg_cap);
+        else if (per_w > 1) orth_backtr<8, 2, true>(t.V, A, tau, m, r, zb, t.dbg, zb + 1024, stg_cap);
+        else orth_backtr<8, 1, true>(t.V, A, tau, m, r, zb, t.dbg, zb + 1024, stg_cap);
+      } else if (m <= 384 && per_w <= 3) {
+        if (per_w > 2) orth_backtr<12, 3, true>(t.V, A, tau, m, r, zb, t.dbg, zb + 1024, stg_cap);
+        else if (per_w > 1) orth_backtr<12, 2, true>(t.V, A, tau, m, r, zb, t.dbg, zb + 1024, stg_cap);
+        else orth_backtr<12, 1, true>(t.V, A, tau, m, r, zb, t.dbg, zb + 1024, stg_cap);
+      } else if (m <= 512 && per_w <= 2) {
+        if (per_w > 1) orth_backtr<16, 2, true>(t.V, A, tau, m, r, zb, t.dbg, zb + 1024, stg_cap);
+        else orth_backtr<16, 1, true>(t.V, A, tau, m, r, zb, t.dbg, zb + 1024, stg_cap);
+      } else {
+        done = false;
+      }
+      if (done) {
+        __syncthreads();
+        if (t.dbg && tid == 0) t.dbg[3] = t.dbg[4] = clock64();
+        return;
+      }
+    } else if (REG || m <= 64) {
       // register-resident vectors (REG: m <= 128, 16 warps; generic: m <= 64, 8 warps)
       if (REG) {
         if (per_w > 4) orth_backtr<4, 8, true>(t.V, A, tau, m, r, s_zb, t.dbg);
@@ -1364,15 +1699,15 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
   // ---- 5. back-transformation V = H_0 ... H_{m-3} Z ----
   if (m <= 256) {
     const int per_w = (r + nw - 1) / nw;
-    if (per_w >= 2) backtr_warp<8, 2>(t.V, A, tau, m, r);
-    else backtr_warp<8, 1>(t.V, A, tau, m, r);
+    if (per_w >= 2) backtr_warp<8, 2>(t.V, A, tau, m, r, PRE);
+    else backtr_warp<8, 1>(t.V, A, tau, m, r, PRE);
   } else {
     for (int k = warp; k < r; k += nw) {
       double *z = t.V + (int64_t)k * m;
       for (int j = m - 3; j >= 0; --j) {
         const double tj = tau[j];
         if (tj == 0.0) continue;
-        const double *v = A + (int64_t)j * m;
+        const double *v = A + (PRE ? refl_off(j, m) : (int64_t)j * m);
         double s2 = 0;
         for (int i = j + 1 + lane; i < m; i += 32) s2 = fma(v[i], z[i], s2);
         s2 = warp_sum(s2) * tj;
@@ -1383,6 +1718,147 @@ __global__ void __launch_bounds__(REG ? EIG_REG_THREADS : EIG_THREADS)
   }
   __syncthreads();
   if (t.dbg && tid == 0) t.dbg[4] = clock64();
+}
+
+// ---------------------------------------- PRE pipeline (128 < m <= 512) ----
+// Inverse iteration for the kept eigenvalues of the tridiagonal record, one
+// CTA per chunk of vectors (chunk c: k in [c nb, (c+1) nb) ∩ [0, r)), each
+// chunk's LU / right-hand sides in shared memory; grid = nodes x nch.
+__global__ void __launch_bounds__(256) k_invit_multi(const EigTask *__restrict__ tasks, int nch, int smem_cap_doubles) {
+  extern __shared__ double sh[];
+  const EigTask t = tasks[blockIdx.x / nch];
+  const int c = blockIdx.x % nch;
+  const int m = t.m;
+  const int r = *t.rank_out;
+  const int64_t per = 5 * (int64_t)m + (m + 7) / 8;
+  const int mp = (m + 8) & ~7;
+  const int nb = (int)min((int64_t)blockDim.x, ((int64_t)smem_cap_doubles - 2 * mp) / per);
+  const int k0 = c * nb;
+  if (k0 >= r || nb <= 0) return;
+  const int nbc = min(nb, r - k0);
+  const double *rec = t.work + 6 * (int64_t)m * m;
+  double *d = sh, *e = sh + mp, *ws = sh + 2 * mp;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    d[i] = rec[i];
+    e[i] = rec[m + i];
+  }
+  __syncthreads();
+  const double *lam = rec + rec_lam_off(m);
+  const double pertol = 10.0 * 2.2e-16 * rec[3 * m + 1];
+  const int kk = threadIdx.x;
+  if (kk < nbc) {
+    const int k = k0 + kk;
+    double sft = lam[k];
+    for (int q = 1; q <= k && lam[k - q] - lam[k] < pertol; ++q) sft -= pertol;
+    double *DL = ws + kk, *Dv = DL + (int64_t)m * nbc, *DU = Dv + (int64_t)m * nbc, *DU2 = DU + (int64_t)m * nbc,
+           *bb = DU2 + (int64_t)m * nbc;
+    unsigned char *pv = reinterpret_cast<unsigned char *>(ws + 5 * (int64_t)m * nbc) + kk;
+    invit_one(d, e, m, sft, pertol, k, DL, Dv, DU, DU2, bb, pv, nbc, t.V + (int64_t)k * m);
+  }
+}
+
+// Modified Gram-Schmidt of the r inverse-iteration vectors in t.V (global,
+// L2-resident), one CTA per node: the owner warp normalises z_k, every warp
+// removes it from its later vectors.
+__global__ void __launch_bounds__(512) k_orth_pre(const EigTask *__restrict__ tasks) {
+  const EigTask t = tasks[blockIdx.x];
+  const int m = t.m, r = *t.rank_out;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = 0; k < r; ++k) {
+    double *zk = t.V + (int64_t)k * m;
+    if (warp == 0) {
+      double s2 = 0;
+      for (int i = lane; i < m; i += 32) s2 = fma(zk[i], zk[i], s2);
+      s2 = frcp(sqrt(warp_sum(s2)));
+      for (int i = lane; i < m; i += 32) zk[i] *= s2;
+    }
+    __syncthreads();
+    for (int j = k + 1 + warp; j < r; j += nw) {
+      double *zj = t.V + (int64_t)j * m;
+      double s2 = 0;
+      for (int i = lane; i < m; i += 32) s2 = fma(zk[i], zj[i], s2);
+      s2 = warp_sum(s2);
+      for (int i = lane; i < m; i += 32) zj[i] -= s2 * zk[i];
+    }
+    __syncthreads();
+  }
+}
+
+// Back-transformation V = H_0 ... H_{m-3} Z for a chunk of 16 NV vectors per
+// CTA (register-resident, reflectors staged through shared memory in
+// contiguous packed segments); grid = nodes x nch.
+template <int Q, int NV>
+__global__ void __launch_bounds__(512) k_backtr_multi(const EigTask *__restrict__ tasks, int nch, int smem_cap_doubles) {
+  extern __shared__ double sh[];
+  const EigTask t = tasks[blockIdx.x / nch];
+  const int c = blockIdx.x % nch;
+  const int m = t.m, r = *t.rank_out;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int k0 = c * nw * NV;
+  if (k0 >= r) return;
+  const double *rec = t.work + 6 * (int64_t)m * m;
+  double *tau = sh;
+  double *stg = sh + ((m + 8) & ~7);
+  const int stg_cap = smem_cap_doubles - ((m + 8) & ~7);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) tau[i] = rec[2 * m + i];
+  const double *A = rec + 4 * (int64_t)m;
+  double z[NV][Q];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int k = k0 + warp + v * nw;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int i = lane + 32 * q;
+      z[v][q] = (k < r && i < m) ? t.V[(int64_t)k * m + i] : 0.0;
+    }
+  }
+  const int ch = max(1, stg_cap / max(m, 1));
+  for (int jc = m - 3; jc >= 0; jc -= ch) {
+    const int jl = max(0, jc - ch + 1);
+    const int64_t lo = refl_off(jl, m) + jl + 1, hi = refl_off(jc, m) + m;
+    __syncthreads();
+    for (int64_t q = lo + threadIdx.x; q < hi; q += blockDim.x) stg[q - lo] = A[q];
+    __syncthreads();
+    const double *base = stg - lo;
+    for (int j = jc; j >= jl; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      const double *vj = base + refl_off(j, m);
+      double vv[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int i = lane + 32 * q;
+        vv[q] = (i > j && i < m) ? vj[i] : 0.0;
+      }
+      double s[NV];
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        s[v] = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) s[v] = fma(vv[q], z[v][q], s[v]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        const double sv = s[v] * tj;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) z[v][q] = fma(-sv, vv[q], z[v][q]);
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int k = k0 + warp + v * nw;
+    if (k < r)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const int i = lane + 32 * q;
+        if (i < m) t.V[(int64_t)k * m + i] = z[v][q];
+      }
+  }
 }
 
 // ----------------------------------------------------------------- pivot ----

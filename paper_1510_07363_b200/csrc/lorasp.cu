@@ -308,6 +308,83 @@ bool is_device_ptr(const void *p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// Cluster eigen path (128 < m <= 512): k_tridiag_cl over a CTA cluster, then
+// k_eig_t<false, true> (eigenvalues, inverse iteration, back-transformation).
+static int eig_cl_class(int m) {
+  if (m > EIG_REG_M && m <= 256) return 1;
+  if (m > 256 && m <= 384) return 2;
+  if (m > 384 && m <= 512) return 3;
+  return 0;
+}
+static const char *eig_cl_disabled = getenv("LORASP_EIG_NO_CLUSTER");   // debug: generic path only
+
+template <int QR, int UC, int CL>
+static void launch_tridiag_cl_t(cudaStream_t st, const EigTask *dt, int n, double eps, long long *prof) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n * CL));
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = (size_t)21 * 32 * QR * 8;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_tridiag_cl<QR, UC, CL>, dt, eps, prof));
+}
+
+static void launch_tridiag_cl(cudaStream_t st, const EigTask *dt, int n, int cls, double eps,
+                              long long *prof = nullptr) {
+  if (cls == 1) launch_tridiag_cl_t<8, 4, 4>(st, dt, n, eps, prof);
+  else if (cls == 2) launch_tridiag_cl_t<12, 3, 8>(st, dt, n, eps, prof);
+  else launch_tridiag_cl_t<16, 2, 16>(st, dt, n, eps, prof);
+}
+
+// After k_tridiag_cl: eigenvalues + rank (k_eig_t<false, true>), chunked
+// inverse iteration, MGS, chunked back-transformation.  Returns the launches.
+static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double eps, int *dstatus) {
+  k_eig_t<false, true><<<(unsigned)n, EIG_REG_THREADS, SMEM_LIMIT, st>>>(dp, eps, SMEM_LIMIT / 8, dstatus);
+  CK(cudaGetLastError());
+  if (eps == 0.0) return 1;   // V = I already written
+  const int cap = SMEM_LIMIT / 8;
+  const int64_t per = 5 * (int64_t)mmax + (mmax + 7) / 8;
+  const int mp = (mmax + 8) & ~7;
+  const int nb = (int)std::min<int64_t>(256, (cap - 2 * mp) / per);
+  const int nch = (mmax + nb - 1) / nb;
+  k_invit_multi<<<(unsigned)(n * nch), 256, SMEM_LIMIT, st>>>(dp, nch, cap);
+  CK(cudaGetLastError());
+  k_orth_pre<<<(unsigned)n, 512, 0, st>>>(dp);
+  CK(cudaGetLastError());
+  if (mmax <= 256) {
+    const int nc = (mmax + 63) / 64;
+    k_backtr_multi<8, 4><<<(unsigned)(n * nc), 512, SMEM_LIMIT, st>>>(dp, nc, cap);
+  } else if (mmax <= 384) {
+    const int nc = (mmax + 47) / 48;
+    k_backtr_multi<12, 3><<<(unsigned)(n * nc), 512, SMEM_LIMIT, st>>>(dp, nc, cap);
+  } else {
+    const int nc = (mmax + 31) / 32;
+    k_backtr_multi<16, 2><<<(unsigned)(n * nc), 512, SMEM_LIMIT, st>>>(dp, nc, cap);
+  }
+  CK(cudaGetLastError());
+  return 4;
+}
+
+static void set_eig_attrs() {
+  CK(cudaFuncSetAttribute(k_invit_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_backtr_multi<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_backtr_multi<12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_backtr_multi<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EIG_REG_SMEM));
+  CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_eig_t<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_tridiag_cl<8, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 8 * 8));
+  CK(cudaFuncSetAttribute(k_tridiag_cl<12, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 12 * 8));
+  CK(cudaFuncSetAttribute(k_tridiag_cl<16, 2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 16 * 8));
+  CK(cudaFuncSetAttribute(k_tridiag_cl<16, 2, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+
 void ensure_mem(lorasp_ctx *h) {
   if (h->mem_ready) return;
   CK(cudaSetDevice(h->device));
@@ -324,8 +401,7 @@ void ensure_mem(lorasp_ctx *h) {
   h->d_dotpart.ensure((DOT_BLOCKS + 64) * sizeof(double), h->stream);
   h->stg.init(size_t(64) << 20, h->stream);
   CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-  CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EIG_REG_SMEM));
-  CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  set_eig_attrs();
   CK(cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
@@ -388,10 +464,16 @@ void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::v
 
 
 void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int max_m, int cap) {
-  std::vector<EigTask> small, big;
-  for (const EigTask &e : et) ((e.m >= EIG_REG_MIN && e.m <= EIG_REG_M) ? small : big).push_back(e);
+  std::vector<EigTask> small, big, clt[4];
+  for (const EigTask &e : et) {
+    const int cls = eig_cl_disabled ? 0 : eig_cl_class(e.m);
+    if (e.m >= EIG_REG_MIN && e.m <= EIG_REG_M) small.push_back(e);
+    else if (cls) clt[cls].push_back(e);
+    else big.push_back(e);
+  }
+  const bool single = (small.size() == et.size()) || (big.size() == et.size());
   if (!small.empty()) {
-    EigTask *ds = big.empty() ? de : push(h, small);
+    EigTask *ds = single ? de : push(h, small);
     // register-tile path: the whole 200 KB (A + the inverse-iteration batches)
     const size_t sm = EIG_REG_SMEM;
     k_tridiag_reg<false><<<(unsigned)small.size(), EIG_REG_THREADS, 0, h->stream>>>(ds, h->plan.eps, nullptr);
@@ -402,8 +484,22 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
     ++h->launches_factor;
     CK(cudaGetLastError());
   }
+  std::vector<EigTask> post;
+  for (int c = 1; c <= 3; ++c) {
+    if (clt[c].empty()) continue;
+    EigTask *dc = push(h, clt[c]);
+    launch_tridiag_cl(h->stream, dc, (int)clt[c].size(), c, h->plan.eps);
+    ++h->launches_factor;
+    post.insert(post.end(), clt[c].begin(), clt[c].end());
+  }
+  if (!post.empty()) {
+    EigTask *dp = push(h, post);
+    int mmax = 0;
+    for (auto &e : post) mmax = std::max(mmax, e.m);
+    h->launches_factor += launch_pre_post(h->stream, dp, (int)post.size(), mmax, h->plan.eps, h->d_status.as<int>());
+  }
   if (!big.empty()) {
-    EigTask *db = small.empty() ? de : push(h, big);
+    EigTask *db = single ? de : push(h, big);
     int mb = 0;
     for (auto &e : big) mb = std::max(mb, e.m);
     k_eig_t<false><<<(unsigned)big.size(), EIG_THREADS, (size_t)eig_generic_cap(mb) * 8, h->stream>>>(
@@ -1777,8 +1873,7 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
   try {
     CK(cudaSetDevice(device));
     CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-    CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EIG_REG_SMEM));
-    CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+    set_eig_attrs();
     double *dG, *dV, *dS, *dW;
     int *dr, *dst;
     size_t mm = (size_t)m * m;
@@ -1859,9 +1954,35 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
         }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-      }
-      else
+      } else if (eig_cl_class(m) && !getenv("LORASP_EIG_GENERIC")) {
+        if (ddbg) {
+          long long *dprof, hp[8];
+          CK(cudaMalloc(&dprof, 64));
+          launch_tridiag_cl(0, de, 1, eig_cl_class(m), eps, dprof);
+          CK(cudaMemcpy(hp, dprof, 64, cudaMemcpyDeviceToHost));
+          cudaFree(dprof);
+          fprintf(stderr, "  [cl phases, cycles/step] A %.0f bar %.0f B %.0f clsync1 %.0f C %.0f (bar+)D %.0f clsync2 %.0f pull %.0f\n",
+                  hp[0] / (m - 2.0), hp[1] / (m - 2.0), hp[2] / (m - 2.0), hp[3] / (m - 2.0), hp[4] / (m - 2.0),
+                  hp[5] / (m - 2.0), hp[6] / (m - 2.0), hp[7] / (m - 2.0));
+        }
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        launch_tridiag_cl(0, de, 1, eig_cl_class(m), eps);
+        cudaEventRecord(e1);
+        launch_pre_post(0, de, 1, m, eps, dst);
+        if (ddbg) {
+          float ms = 0;
+          cudaEventSynchronize(e1);
+          cudaEventElapsedTime(&ms, e0, e1);
+          fprintf(stderr, "[k_tridiag_cl m=%d class %d] %.1f us\n", m, eig_cl_class(m), 1e3 * ms);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+      } else {
         k_eig_t<false><<<1, EIG_THREADS, (size_t)eig_generic_cap(m) * 8>>>(de, eps, eig_generic_cap(m), dst);
+      }
     }
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());

@@ -80,3 +80,24 @@ def test_eig_zero_and_eps0(L):
     G = G.T @ G
     sig, V, r, st = L.test_eig(G, 0.0)
     assert st == 0 and r == 90 and np.array_equal(V, np.eye(90))
+
+
+@pytest.mark.parametrize("m", [150, 300, 450])
+def test_eig_large_rank(L, m):
+    """Ranks ~0.6 m (the 3D upper levels): chunked inverse iteration, MGS and
+    back-transformation of many vectors."""
+    eps = 1e-2
+    decay = eps ** (1.0 / (0.6 * m))
+    M = stack(m, 2 * m + 5, decay, seed=3 * m)
+    sig, V, r, st = L.test_eig(M.T @ M, eps)
+    assert st == 0
+    s_ref = np.linalg.svd(M, compute_uv=False)
+    r_ref = int(np.sum(s_ref >= eps * s_ref[0]))
+    near = any(0 <= k < m and abs(s_ref[k] / s_ref[0] - eps) <= 1e-12 for k in (r_ref - 1, r_ref))
+    assert r == r_ref or near, (r, r_ref)
+    assert r > m // 2
+    assert np.max(np.abs(sig[:r] - s_ref[:r])) <= 1e-12 * s_ref[0]
+    assert np.allclose(V.T @ V, np.eye(r), rtol=0, atol=1e-12)
+    _, _, Vt = np.linalg.svd(M)
+    Pr = Vt[:r].T @ Vt[:r]
+    assert np.max(np.abs(V @ V.T - Pr)) <= 1e-8
