@@ -749,9 +749,11 @@ __host__ __device__ __forceinline__ int64_t rec_lam_off(int m) { return 4 * (int
 // global scratch at work + 6 m^2: d[128] | e[128] | tau[128] | ||G||_F^2 |
 // (pad) | the packed reflectors (m (m - 1) / 2, refl_off layout), consumed by
 // k_eig_t<true>.
-template <bool PROF>
-__global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTask *__restrict__ tasks, double eps,
+template <bool PROF, int QR = 4, int NW = 16, int UW = 8>
+__global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__restrict__ tasks, double eps,
                                                                     long long *prof, int variant = 0) {
+  constexpr int MR = 32 * QR;   // tile rows (= NW * UW columns)
+  static_assert(MR == NW * UW, "square register tile");
   long long pt[6] = {0, 0, 0, 0, 0, 0}, pc = 0;
 #define TRID_PROF(i)                  \
   if constexpr (PROF) {               \
@@ -760,30 +762,30 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
     pc = tn;                          \
   }
   __shared__ double s_red[32];
-  __shared__ double d[EIG_REG_M + 8], e[EIG_REG_M + 8], tau[EIG_REG_M + 8];
+  __shared__ double d[MR + 8], e[MR + 8], tau[MR + 8];
   const EigTask t = tasks[blockIdx.x];
   const int m = t.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double *out = t.work + 6 * (int64_t)m * m;
   double *A = out + 4 * (int64_t)m;   // packed reflectors (global)
-  double a[4][8];
+  double a[QR][UW];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < QR; ++q)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int r = 32 * q + lane, c = 8 * warp + u;
+    for (int u = 0; u < UW; ++u) {
+      const int r = 32 * q + lane, c = UW * warp + u;
       a[q][u] = (r < m && c < m) ? t.G[r + (int64_t)c * m] : 0.0;
     }
   double fro = 0;
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < QR; ++q)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) fro = fma(a[q][u], a[q][u], fro);
+    for (int u = 0; u < UW; ++u) fro = fma(a[q][u], a[q][u], fro);
   fro = warp_sum(fro);
   if (lane == 0) s_red[warp] = fro;
   __syncthreads();
   fro = 0;
-  for (int w = 0; w < 16; ++w) fro += s_red[w];
+  for (int w = 0; w < NW; ++w) fro += s_red[w];
   __syncthreads();
   if (tid == 0) out[3 * m] = fro;
   if (!(fro > 0.0) || eps == 0.0) return;
@@ -794,12 +796,12 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
   // 4 partial row sums of A v, rows reduce over the 16 column strips, and the
   // rank-2 update is register-only.  v and p vanish outside rows/cols > k, so
   // no predication is needed.  3 barriers per step.
-  __shared__ double vbuf[2][EIG_REG_M];              // v (two buffers, 128 rows each)
+  __shared__ double vbuf[2][MR];              // v (two buffers, 128 rows each)
   double *vsm0 = vbuf[0], *vsm1 = vbuf[1];
-  __shared__ double pbuf[2][EIG_REG_M];              // p (two buffers)
+  __shared__ double pbuf[2][MR];              // p (two buffers)
   double *psm0 = pbuf[0], *psm1 = pbuf[1];
-  __shared__ double ps_part[16][EIG_REG_M];
-  __shared__ double colbuf[EIG_REG_M];               // column k+1 before update k
+  __shared__ double ps_part[NW][MR];
+  __shared__ double colbuf[MR];               // column k+1 before update k
   // Householder vector of column kk from its (updated) entries col[q] = A(4 lane + q, kk),
   // run by the owner warp kk >> 3: v into the shared buffer, the packed reflector
   // store, tau and the off-diagonal beta.
@@ -807,7 +809,7 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
     double *vs = (kk & 1) ? vsm1 : vsm0;
     double s2 = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < QR; ++q) {
       const int r = 32 * q + lane;
       if (r >= kk + 2 && r < m) s2 = fma(col[q], col[q], s2);
     }
@@ -815,7 +817,7 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
     const int rx = kk + 1;
     double x0 = 0.0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < QR; ++q)
       if (32 * q + lane == rx) x0 = col[q];
     x0 = __shfl_sync(0xffffffffu, x0, rx & 31);
     double beta = x0, scal = 0.0, tk = 0.0;
@@ -825,7 +827,7 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
       scal = frcp(x0 - beta);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < QR; ++q) {
       const int r = 32 * q + lane;
       double v = 0.0;
       if (s2 != 0.0) v = (r == rx) ? 1.0 : ((r > rx && r < m) ? col[q] * scal : 0.0);
@@ -844,9 +846,9 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
   // owning column k+1 updates that column first and forms v_{k+1} while the
   // other warps are still updating, so the v barrier costs no extra latency.
   if (warp == 0 && m > 2) {
-    double col[4];
+    double col[QR];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) col[q] = a[q][0];
+    for (int q = 0; q < QR; ++q) col[q] = a[q][0];
     form_v(0, col);
   }
   __syncthreads();
@@ -859,28 +861,28 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
     // a row group q whose 32 rows are all <= k, multiplies / updates by exact
     // zeros (v and the masked p vanish there), so it is skipped (bitwise the
     // same result, ~1/3 of the full-tile FP64 work on average).
-    const bool wact = 8 * warp + 7 > k && variant != 4 && variant != 6;
-    if (warp == ((k + 1) >> 3) && k + 1 < m - 2) {
+    const bool wact = UW * warp + UW - 1 > k && variant != 4 && variant != 6;
+    if (warp == ((k + 1) / UW) && k + 1 < m - 2) {
       // owner of column k+1 publishes it (as of before update k) for the form warp
-      const int u1 = (k + 1) & 7;
+      const int u1 = (k + 1) % UW;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < QR; ++q) {
         double c = a[q][0];
 #pragma unroll
-        for (int u = 1; u < 8; ++u) c = (u1 == u) ? a[q][u] : c;
+        for (int u = 1; u < UW; ++u) c = (u1 == u) ? a[q][u] : c;
         colbuf[32 * q + lane] = c;
       }
     }
     if (wact) {
-    double vc[8];
+    double vc[UW];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) vc[u] = vs[8 * warp + u];
+    for (int u = 0; u < UW; ++u) vc[u] = vs[UW * warp + u];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < QR; ++q) {
       if (32 * q + 31 <= k) continue;   // rows masked out of p, v_r = 0
       double s0 = 0, s1 = 0;
 #pragma unroll
-      for (int u = 0; u < 8; u += 2) {
+      for (int u = 0; u < UW; u += 2) {
         s0 = fma(a[q][u], vc[u], s0);
         s1 = fma(a[q][u + 1], vc[u + 1], s1);
       }
@@ -888,19 +890,21 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
     }
     } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) ps_part[warp][32 * q + lane] = 0.0;
+      for (int q = 0; q < QR; ++q) ps_part[warp][32 * q + lane] = 0.0;
     }
 
     TRID_PROF(0)
     if (variant != 3) __syncthreads();                            // (2) partials visible
     TRID_PROF(1)
-    if (tid < EIG_REG_M && variant != 2) {
-      double h[8];
+    if (tid < MR && variant != 2) {
+      double h[NW];
 #pragma unroll
-      for (int w = 0; w < 8; ++w) h[w] = ps_part[w][tid] + ps_part[w + 8][tid];
+      for (int w = 0; w < NW; ++w) h[w] = ps_part[w][tid];
 #pragma unroll
-      for (int w = 0; w < 4; ++w) h[w] += h[w + 4];
-      const double sacc = (h[0] + h[2]) + (h[1] + h[3]);
+      for (int st = NW / 2; st > 0; st /= 2)
+#pragma unroll
+        for (int w = 0; w < st; ++w) h[w] += h[w + st];   // pairwise tree
+      const double sacc = h[0];
       const double pi = (tid > k && tid < m) ? tk * sacc : 0.0;
       ps[tid] = pi;
       // p.v over the 128 rows: 4 warp reductions (shuffles are a shared,
@@ -911,23 +915,24 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
     TRID_PROF(2)
     if (variant != 3) __syncthreads();                            // (3) p visible
     TRID_PROF(3)
-    const double pv = (s_red[0] + s_red[1]) + (s_red[2] + s_red[3]);
+    const double pv = QR == 4 ? (s_red[0] + s_red[1]) + (s_red[2] + s_red[3])
+                              : (QR == 2 ? s_red[0] + s_red[1] : s_red[0]);
     const double alpha = -0.5 * tk * pv;
     // (vr, wr, v_c, w_c are re-read from shared memory here: with the 32-double
     // tile live, keeping them in registers across form_v would spill)
-    const double *psc = ps + 8 * warp, *vsc = vs + 8 * warp;
-    if (8 * warp + 7 > k && variant != 5 && variant != 6) {
-      double vq[4], wq[4];
+    const double *psc = ps + UW * warp, *vsc = vs + UW * warp;
+    if (UW * warp + UW - 1 > k && variant != 5 && variant != 6) {
+      double vq[QR], wq[QR];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < QR; ++q) {
         vq[q] = vs[32 * q + lane];
         wq[q] = fma(alpha, vq[q], ps[32 * q + lane]);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < UW; ++u) {
         const double vcu = vsc[u], wcu = fma(alpha, vcu, psc[u]);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < QR; ++q)
           if (32 * q + 31 > k) a[q][u] = fma(-vq[q], wcu, fma(-wq[q], vcu, a[q][u]));
       }
     }
@@ -936,11 +941,11 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
     // k >= 7; warp 15 before), from the published column and the same update
     // formula the owner applies in registers (bitwise the same column), so it
     // overlaps the other warps' updates instead of trailing the owner's.
-    if (warp == (k1 >= 8 ? 0 : 15) && k1 < m - 2 && variant != 1 && variant != 6) {
+    if (warp == (k1 >= UW ? 0 : NW - 1) && k1 < m - 2 && variant != 1 && variant != 6) {
       const double vcu = vs[k1], wcu = fma(alpha, vcu, ps[k1]);
-      double col[4];
+      double col[QR];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < QR; ++q) {
         const double vq = vs[32 * q + lane], wq = fma(alpha, vq, ps[32 * q + lane]);
         col[q] = fma(-vq, wcu, fma(-wq, vcu, colbuf[32 * q + lane]));
       }
@@ -957,10 +962,10 @@ __global__ void __launch_bounds__(EIG_REG_THREADS, 1) k_tridiag_reg(const EigTas
 #undef TRID_PROF
   // diagonal and last sub-diagonal from the register tiles
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < QR; ++q)
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int r = 32 * q + lane, c = 8 * warp + u;
+    for (int u = 0; u < UW; ++u) {
+      const int r = 32 * q + lane, c = UW * warp + u;
       if (r < m && r == c) d[r] = a[q][u];
       if (m >= 2 && r == m - 1 && c == m - 2) e[m - 2] = a[q][u];
     }

@@ -49,7 +49,7 @@ struct Err {
 };
 
 static const int SMEM_LIMIT = 226 * 1024;  // dynamic; leaves room for static smem
-static const int EIG_REG_MIN = 65;
+static const int EIG_REG_MIN = 3;
 static const size_t EIG_REG_SMEM = 200 * 1024;
 // generic eigen path: shared memory for d/e/tau/..., A when it fits, and an
 // inverse-iteration batch of 16 vectors (5 m doubles + m bytes each)
@@ -342,6 +342,19 @@ static void launch_tridiag_cl(cudaStream_t st, const EigTask *dt, int n, int cls
   else launch_tridiag_cl_t<16, 2, 16>(st, dt, n, eps, prof);
 }
 
+// Register-tile eigen path for m <= 128: tridiagonalisation (tile class c:
+// 32 / 64 / 128 rows) then k_eig_t<true>.
+static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps, int *dstatus) {
+  if (c == 0) k_tridiag_reg<false, 1, 4, 8><<<(unsigned)n, 128, 0, st>>>(ds, eps, nullptr);
+  else if (c == 1) k_tridiag_reg<false, 2, 8, 8><<<(unsigned)n, 256, 0, st>>>(ds, eps, nullptr);
+  else k_tridiag_reg<false><<<(unsigned)n, EIG_REG_THREADS, 0, st>>>(ds, eps, nullptr);
+  CK(cudaGetLastError());
+  k_eig_t<true><<<(unsigned)n, c == 2 ? EIG_REG_THREADS : 256, EIG_REG_SMEM, st>>>(ds, eps, (int)(EIG_REG_SMEM / 8),
+                                                                                   dstatus);
+  CK(cudaGetLastError());
+  return 2;
+}
+
 // After k_tridiag_cl: eigenvalues + rank (k_eig_t<false, true>), chunked
 // inverse iteration, MGS, chunked back-transformation.  Returns the launches.
 static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double eps, int *dstatus) {
@@ -473,16 +486,15 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
   }
   const bool single = (small.size() == et.size()) || (big.size() == et.size());
   if (!small.empty()) {
-    EigTask *ds = single ? de : push(h, small);
-    // register-tile path: the whole 200 KB (A + the inverse-iteration batches)
-    const size_t sm = EIG_REG_SMEM;
-    k_tridiag_reg<false><<<(unsigned)small.size(), EIG_REG_THREADS, 0, h->stream>>>(ds, h->plan.eps, nullptr);
-    ++h->launches_factor;
-    CK(cudaGetLastError());
-    k_eig_t<true><<<(unsigned)small.size(), EIG_REG_THREADS, sm, h->stream>>>(ds, h->plan.eps, (int)(sm / 8),
-                                                                               h->d_status.as<int>());
-    ++h->launches_factor;
-    CK(cudaGetLastError());
+    // register-tile path, by tile class (32 / 64 / 128 rows); the whole 200 KB
+    // of shared memory serves A + the inverse-iteration batches
+    std::vector<EigTask> rc[3];
+    for (auto &e : small) rc[e.m <= 32 ? 0 : (e.m <= 64 ? 1 : 2)].push_back(e);
+    for (int c = 0; c < 3; ++c) {
+      if (rc[c].empty()) continue;
+      EigTask *ds = (single && rc[c].size() == et.size()) ? de : push(h, rc[c]);
+      h->launches_factor += launch_eig_reg(h->stream, ds, (int)rc[c].size(), c, h->plan.eps, h->d_status.as<int>());
+    }
   }
   std::vector<EigTask> post;
   for (int c = 1; c <= 3; ++c) {
@@ -1335,10 +1347,32 @@ void factor_impl(lorasp_ctx *h, const double *values) {
       h->t_host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
       launch_gemm_dev(h, d_pt, d_ps, pt.size(), K_PROJECT, f_proj, b_proj);
       launch_copy_dev(h, d_ct, ct, K_ASSEMBLE);
-      if (sym)
+      if (sym) {
+        cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+        if (h->debug) {
+          cudaEventCreate(&pe0);
+          cudaEventCreate(&pe1);
+          cudaEventRecord(pe0, st);
+        }
         pivots(h, pv, f_piv, b_piv);
-      else
+        if (h->debug) {
+          cudaEventRecord(pe1, st);
+          cudaEventSynchronize(pe1);
+          float ms = 0;
+          cudaEventElapsedTime(&ms, pe0, pe1);
+          int nmin = 1 << 30, nmax = 0;
+          for (auto &t : pv) {
+            nmin = std::min(nmin, t.m + t.r);
+            nmax = std::max(nmax, t.m + t.r);
+          }
+          fprintf(stderr, "[lorasp] level %d wave %zu pivot: %zu tasks n in [%d, %d]: %.3f ms\n", i, w, pv.size(), nmin,
+                  nmax, ms);
+          cudaEventDestroy(pe0);
+          cudaEventDestroy(pe1);
+        }
+      } else {
         pivots_lu(h, pv, f_piv, b_piv);
+      }
       launch_gemm_dev(h, d_zt, d_zs, zt.size(), K_ZGEMM, f_z, b_z);
       launch_gemm_dev(h, d_stt, d_ss, stt.size(), K_SCHUR, f_s, b_s);
       if (h->debug) {
@@ -1943,9 +1977,8 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        k_tridiag_reg<false><<<1, EIG_REG_THREADS>>>(de, eps, nullptr);
+        launch_eig_reg(0, de, 1, m <= 32 ? 0 : (m <= 64 ? 1 : 2), eps, dst);
         cudaEventRecord(e1);
-        k_eig_t<true><<<1, EIG_REG_THREADS, EIG_REG_SMEM>>>(de, eps, (int)(EIG_REG_SMEM / 8), dst);
         if (ddbg) {
           float ms = 0;
           cudaEventSynchronize(e1);
