@@ -191,6 +191,29 @@ def test_identity_and_natural_order(L):
     h.close()
 
 
+@pytest.mark.parametrize("dims,depth", [((32, 32, 32), 9), pytest.param((48, 48, 48), 11, marks=pytest.mark.slow)])
+def test_3d_upper_levels_parity(L, dims, depth):
+    """cfg3 family at sizes whose upper-level super-nodes exceed the register
+    tile (m up to ~230 at 32^3, ~320 at 48^3): the cluster eigen path
+    (k_tridiag_cl + chunked inverse iteration / back-transformation) and the
+    blocked pivots (n = m + r up to ~470) inside the full sweep."""
+    p = make_problem("cfg3", dims=dims, depth=depth)
+    h = L.analyze_problem(p)
+    h.factor(torch.tensor(p.values, device="cuda"))
+    f = oracle_factor(p, p.eps)
+    assert max(max(f.rank.get((i, c), 0) for c in range(2 ** (i - 1))) for i in range(1, depth + 1)) > 64
+    assert rank_mismatches(h, f, p.depth, p.eps) == []
+    x = gpu_apply(h, p.b)
+    assert relerr(x, O.solve(f, p.b)) <= 1e-9
+    b = torch.tensor(p.b, device="cuda")
+    xk = torch.empty_like(b)
+    rc, it, rr = h.krylov(b, xk, tol=1e-10)
+    mv = lambda v: O.spmv(p.row_ptr, p.col_idx, p.values, v)
+    ro = O.pcg(mv, lambda v: O.solve(f, v), p.b, tol=1e-10)
+    assert rc == 0 and rr <= 1e-10 and abs(it - ro.iters) <= 1
+    h.close()
+
+
 @pytest.mark.slow
 def test_cfg2_full_parity(L):
     """BASELINE cfg2 at full size, in the launch configuration bench.py times."""
