@@ -288,7 +288,7 @@ def main():
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
                 trd = json.load(f)
-            if dom_name in trd:
+            if dom_name in trd and trd.get("_config", "cfg2") == args.config:
                 roof["traffic"] = trd[dom_name]
                 roof["traffic_note"] = trd.get("_note")
         except Exception:
