@@ -242,6 +242,11 @@ struct lorasp_ctx {
   std::vector<double> ap_wave_flops, ap_wave_bytes;  // per wave, one pass (fwd or bwd)
   size_t ap_fwd_smem = 0, ap_bwd_smem = 0;
   int ap_chunk = 0;
+  // the forward + backward wave launches of one apply, captured once per
+  // factorization (static after it) and replayed as one graph launch
+  cudaGraphExec_t ap_graph = nullptr;
+  std::vector<int64_t> ap_graph_sig;   // launch parameters the graph was captured with
+  bool no_graph = getenv("LORASP_NO_GRAPH") != nullptr;
   int64_t vec_len = 0;
   bool dest_ready = false;
   std::vector<int64_t> leaf_soff;  // leaf-level slot offsets used for d_dest
@@ -1508,6 +1513,47 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
   const ApNode *nodes = h->d_apnodes.as<ApNode>();
   const ApSeg *segs = h->d_apsegs.as<ApSeg>();
   const int nw = (int)h->ap_wave_begin.size() - 1;
+  const bool timed = h->timing && (((h->timing_mask >> K_APPLY_FWD) & 1u) || ((h->timing_mask >> K_APPLY_BWD) & 1u));
+  if (!timed && !h->no_graph && nw > 0) {
+    // Alg. 3 / Alg. 4 wave launches as one CUDA graph (per-class timing, when
+    // requested for the apply classes, uses the launch-by-launch path below)
+    // the graph stays valid across re-factorizations as long as every launch
+    // parameter is unchanged (the node descriptors live in device memory)
+    std::vector<int64_t> sig(h->ap_wave_begin.begin(), h->ap_wave_begin.end());
+    sig.push_back((int64_t)h->ap_fwd_smem);
+    sig.push_back((int64_t)h->ap_bwd_smem);
+    sig.push_back(h->ap_chunk);
+    sig.push_back((int64_t)(intptr_t)nodes);
+    sig.push_back((int64_t)(intptr_t)segs);
+    sig.push_back((int64_t)(intptr_t)h->d_vec.p);
+    if (h->ap_graph && sig != h->ap_graph_sig) {
+      CK(cudaGraphExecDestroy(h->ap_graph));
+      h->ap_graph = nullptr;
+    }
+    if (!h->ap_graph) {
+      h->ap_graph_sig = sig;
+      // captured on a private stream (the library stream may be the legacy
+      // default stream, which cannot be captured); launched on the library stream
+      cudaStream_t cs;
+      CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+      for (int w = 0; w < nw; ++w) {
+        int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
+        k_apply_fwd<<<b1 - b0, 256, h->ap_fwd_smem, cs>>>(nodes + b0, segs, h->d_vec.as<double>(), h->ap_chunk);
+      }
+      for (int w = nw - 1; w >= 0; --w) {
+        int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
+        k_apply_bwd<<<b1 - b0, 256, h->ap_bwd_smem, cs>>>(nodes + b0, segs, h->d_vec.as<double>(), h->ap_chunk);
+      }
+      const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+      cudaStreamDestroy(cs);
+      CK(ce);
+      CK(cudaGraphInstantiate(&h->ap_graph, g, 0));
+      CK(cudaGraphDestroy(g));
+    }
+    CK(cudaGraphLaunch(h->ap_graph, st));
+  } else {
   for (int w = 0; w < nw; ++w) {
     int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
     ev = tbeg(h, K_APPLY_FWD);
@@ -1519,6 +1565,7 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
     ev = tbeg(h, K_APPLY_BWD);
     k_apply_bwd<<<b1 - b0, 256, h->ap_bwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>(), h->ap_chunk);
     tend(h, ev, h->ap_wave_flops[w], h->ap_wave_bytes[w]);
+  }
   }
   ev = tbeg(h, K_VEC);
   k_get_x<<<grid1(pl.n), 256, 0, st>>>(h->d_vec.as<double>(), h->d_perm.as<int64_t>(), pl.n, x);
@@ -2092,6 +2139,7 @@ void lorasp_destroy(lorasp_handle h) {
                       &h->d_apsegs, &h->d_dotpart};
     for (DevBuf *b : bufs) b->release();
     for (cudaEvent_t e : h->evpool) cudaEventDestroy(e);
+    if (h->ap_graph) cudaGraphExecDestroy(h->ap_graph);
     h->fpool.release();
     h->stg.release();
     if (h->h_ranks) cudaFreeHost(h->h_ranks);
