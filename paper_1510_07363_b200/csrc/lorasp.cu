@@ -245,6 +245,17 @@ struct lorasp_ctx {
   // the forward + backward wave launches of one apply, captured once per
   // factorization (static after it) and replayed as one graph launch
   cudaGraphExec_t ap_graph = nullptr;
+  // split pivot (SPD): chol(S) + L11^{-1} of the wave's super-nodes on a second
+  // stream, overlapped with the compress (whose rank sync follows)
+  cudaStream_t stream2 = nullptr;     // least priority: fills SMs the sweep leaves idle
+  cudaStream_t stream_hi = nullptr;   // greatest priority: the factorization itself
+  cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr, ev_u = nullptr;
+  bool s1_pending = false;
+  DevBuf ws_S, ws_Y, ws_T1, d_sp;
+  void *h_sp = nullptr;     // pinned upload of the part-1 copy + pivot task lists
+  size_t h_sp_cap = 0;
+  bool no_split = getenv("LORASP_NO_SPLIT") != nullptr;
+  int split_min_m = getenv("LORASP_SPLIT_MIN_M") ? atoi(getenv("LORASP_SPLIT_MIN_M")) : 0;
   std::vector<int64_t> ap_graph_sig;   // launch parameters the graph was captured with
   bool no_graph = getenv("LORASP_NO_GRAPH") != nullptr;
   int64_t vec_len = 0;
@@ -420,6 +431,15 @@ void ensure_mem(lorasp_ctx *h) {
   h->stg.init(size_t(64) << 20, h->stream);
   CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   set_eig_attrs();
+  {
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CK(cudaStreamCreateWithPriority(&h->stream2, cudaStreamNonBlocking, least));
+    CK(cudaStreamCreateWithPriority(&h->stream_hi, cudaStreamNonBlocking, greatest));
+  }
+  CK(cudaEventCreateWithFlags(&h->ev_u, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&h->ev_s0, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&h->ev_s1, cudaEventDisableTiming));
   CK(cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
@@ -855,6 +875,11 @@ void factor_impl(lorasp_ctx *h, const double *values) {
     }
 
     // ---- colour waves ---------------------------------------------------------
+    // rank / size ratio seen so far (this level, else the level below): predicts
+    // the fused pivot size n = m + r before the rank sync
+    double rho_pred = 0.0;
+    for (int c = 0; c < (int)h->rnk[i + 1].size() && i < L; ++c)
+      if (h->msz[i + 1][c] > 0) rho_pred = std::max(rho_pred, (double)h->rnk[i + 1][c] / h->msz[i + 1][c]);
     for (size_t w = 0; w + 1 < lv.wave_begin.size(); ++w) {
       std::vector<int> comp, elim;
       for (int t = lv.wave_begin[w]; t < lv.wave_begin[w + 1]; ++t) {
@@ -865,6 +890,76 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         if (nd.aux) comp.push_back(c);
       }
       if (elim.empty()) continue;
+      // --- split pivot, part 1 (SPD): S -> L11^{-1} for the super-nodes of the
+      // wave on stream2, overlapped with the compress below (S is final: only
+      // earlier waves' Schur updates touch it).  K = [[S, V], [V^T, 0]] =
+      // L diag(I, -I) L^T has L11 = chol(S); the V-dependent rest follows the
+      // rank sync (part 2).  Nodes with m > PIVB_MAXN keep the fused pivot.
+      std::vector<int64_t> s_off(K, -1);
+      std::vector<CopyTask> s_ct;
+      std::vector<PivTask> s_pt;
+      int s_max = 0;
+      if (sym && !comp.empty() && !h->no_split) {
+        int64_t stot2 = 0;
+        // A node is split when that pays: in waves wider than the GPU (the S
+        // pivots then fill the sync gaps), or when its fused pivot would likely
+        // exceed PIVB_MAXN (rank predicted from the largest r / m seen so far
+        // at this level or the one below) and so take the launch-heavy blocked
+        // path.  Otherwise the single fused k_pivot_blk is cheaper.
+        const bool wide = elim.size() > 148;
+        for (int c : elim)
+          if (m[c] <= PIVB_MAXN && m[c] >= h->split_min_m &&
+              (wide || h->split_min_m > 0 || m[c] + (int)std::ceil(rho_pred * m[c]) > PIVB_MAXN)) {
+            s_off[c] = stot2;
+            stot2 += (int64_t)m[c] * m[c];
+          }
+        if (stot2 > 0) {
+          h->ws_S.ensure(stot2 * 8 + 256, st);
+          for (int c : elim) {
+            if (s_off[c] < 0) continue;
+            const SymNode &nd = lv.node[c];
+            CopyTask t{};
+            t.src = slot_ptr(nd.self_slot);
+            t.lds = sld[nd.self_slot];
+            t.dst = h->ws_S.as<double>() + s_off[c];
+            t.ldd = m[c];
+            t.rows = m[c];
+            t.cols = m[c];
+            t.mode = 0;
+            t.alpha = 1.0;
+            s_ct.push_back(t);
+            s_pt.push_back(PivTask{h->ws_S.as<double>() + s_off[c], m[c], m[c], 0, c});
+            s_max = std::max(s_max, m[c]);
+          }
+          CK(cudaEventRecord(h->ev_s0, st));   // S is final here; stream2 starts after it
+        }
+      }
+      // part 1 is enqueued on stream2 once the compress kernels are queued
+      auto enqueue_split_part1 = [&]() {
+        if (s_pt.empty()) return;
+        CK(cudaStreamWaitEvent(h->stream2, h->ev_s0, 0));
+        if (h->s1_pending) CK(cudaEventSynchronize(h->ev_s1));   // pinned task buffer reuse
+        const size_t nbytes = s_ct.size() * sizeof(CopyTask) + s_pt.size() * sizeof(PivTask);
+        if (h->h_sp_cap < nbytes) {
+          if (h->h_sp) CK(cudaFreeHost(h->h_sp));
+          h->h_sp_cap = std::max<size_t>(nbytes * 2, 1 << 16);
+          CK(cudaMallocHost(&h->h_sp, h->h_sp_cap));
+        }
+        char *hb = reinterpret_cast<char *>(h->h_sp);
+        std::memcpy(hb, s_ct.data(), s_ct.size() * sizeof(CopyTask));
+        std::memcpy(hb + s_ct.size() * sizeof(CopyTask), s_pt.data(), s_pt.size() * sizeof(PivTask));
+        h->d_sp.ensure(nbytes + 64, st);
+        CK(cudaMemcpyAsync(h->d_sp.p, hb, nbytes, cudaMemcpyHostToDevice, h->stream2));
+        const CopyTask *dct = h->d_sp.as<CopyTask>();
+        const PivTask *dpt = reinterpret_cast<const PivTask *>(h->d_sp.as<char>() + s_ct.size() * sizeof(CopyTask));
+        k_copy<<<(unsigned)s_ct.size(), 256, 0, h->stream2>>>(dct);
+        const size_t smem = (size_t)(s_max | 1) * s_max * 8;
+        k_pivot_blk<<<(unsigned)s_pt.size(), 512, smem, h->stream2>>>(dpt, h->d_status.as<int>());
+        h->launches_factor += 2;
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(h->ev_s1, h->stream2));
+        h->s1_pending = true;
+      };
       // --- Compress: Gram + Jacobi + rank ---
       std::vector<int64_t> goff(K, 0);
       if (!comp.empty()) {
@@ -968,6 +1063,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           cudaEventRecord(dbg_e0, st);
         }
         launch_eig(h, et, de, max_m, cap);
+        enqueue_split_part1();
         if (h->debug) {
           cudaEventRecord(dbg_e1, st);
           cudaEventSynchronize(dbg_e1);
@@ -999,7 +1095,10 @@ void factor_impl(lorasp_ctx *h, const double *values) {
                                         " at level " + std::to_string(i) + " node " +
                                         std::to_string(h->h_status[1]));
         }
-        for (size_t q = 0; q < comp.size(); ++q) r[comp[q]] = h->h_ranks[q];
+        for (size_t q = 0; q < comp.size(); ++q) {
+          r[comp[q]] = h->h_ranks[q];
+          if (m[comp[q]] > 0) rho_pred = std::max(rho_pred, (double)r[comp[q]] / m[comp[q]]);
+        }
       }
       // --- project, assemble, pivot, Z, Schur ---
       auto th0 = std::chrono::steady_clock::now();
@@ -1021,6 +1120,22 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         ctr_tot += ((int64_t)(m[c] + r[c]) * W * (sym ? 1 : 2) + 31) & ~int64_t(31);
       }
       h->ws_ctr.ensure(std::max<int64_t>(ctr_tot, 32) * 8, st);
+      // split-pivot scratch: Y (m x r) and T1 (r x m) per split node
+      std::vector<GemmTask> sy_t, sg_t, sx_t;
+      std::vector<GemmSeg> sy_s, sg_s, sx_s;
+      std::vector<int64_t> split_off(elim.size(), 0);
+      {
+        int64_t yt = 0;
+        for (size_t e = 0; e < elim.size(); ++e) {
+          const int c = elim[e];
+          split_off[e] = yt;
+          if (s_off[c] >= 0) yt += ((int64_t)m[c] * r[c] + 31) & ~int64_t(31);
+        }
+        if (yt > 0) {
+          h->ws_Y.ensure(yt * 8 + 256, st);
+          h->ws_T1.ensure(yt * 8 + 256, st);
+        }
+      }
       int max_n = 0;
       double f_proj = 0, b_proj = 0, f_piv = 0, b_piv = 0, f_z = 0, b_z = 0, f_s = 0, b_s = 0;
       for (size_t e = 0; e < elim.size(); ++e) {
@@ -1098,10 +1213,12 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         rec.zf_off = sym ? offX : offY;   // forward: Z (SPD) / Y^T (LU)
         rec.zb_off = offX;                // backward: Z / X
         rec.lb_off = sym ? 0 : (int64_t)ldF * n;   // backward triangle: L^{-1} / U^{-T}
-        // assemble pivot K = [[S, V], [V^T, 0]] (lower part used)
+        // assemble pivot K = [[S, V], [V^T, 0]] (lower part used); split nodes:
+        // L11^{-1} from part 1 (upper triangle zero) and a zero upper-right block
+        const bool split = s_off[c] >= 0;
         CopyTask t{};
-        t.src = slot_ptr(nd.self_slot);
-        t.lds = sld[nd.self_slot];
+        t.src = split ? h->ws_S.as<double>() + s_off[c] : slot_ptr(nd.self_slot);
+        t.lds = split ? mc : sld[nd.self_slot];
         t.dst = F;
         t.ldd = ldF;
         t.rows = mc;
@@ -1110,7 +1227,17 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         t.trans = 0;
         t.alpha = 1.0;
         ct.push_back(t);
-        if (rc > 0) {
+        if (split && rc > 0) {
+          t = CopyTask{};
+          t.dst = F + (int64_t)mc * ldF;
+          t.ldd = ldF;
+          t.rows = mc;
+          t.cols = rc;
+          t.mode = 1;
+          t.alpha = 0.0;
+          ct.push_back(t);
+        }
+        if (!split && rc > 0) {
           t = CopyTask{};
           t.src = V;
           t.lds = mc;
@@ -1236,7 +1363,57 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           }
         }
         // pivot
-        pv.push_back(PivTask{F, ldF, mc, rc, c});
+        if (!split) {
+          pv.push_back(PivTask{F, ldF, mc, rc, c});
+        } else if (rc > 0) {
+          // part 2: Y = L11^{-1} V, L21 = Y^T, L22 = chol(Y^T Y) (K22 = 0 and
+          // D2 = -I), X21 = -L22^{-1} Y^T L11^{-1}
+          double *Yb = h->ws_Y.as<double>() + split_off[e];
+          double *T1 = h->ws_T1.as<double>() + split_off[e];
+          GemmTask g{};
+          g.C = Yb;
+          g.ldc = mc;
+          g.M = mc;
+          g.N = rc;
+          g.beta = 0;
+          g.seg0 = (int)sy_s.size();
+          g.nseg = 1;
+          sy_s.push_back(GemmSeg{F, V, ldF, mc, mc, 1.0});
+          add_tiles(sy_t, g);
+          g = GemmTask{};
+          g.C = F + mc + (int64_t)mc * ldF;
+          g.ldc = ldF;
+          g.M = rc;
+          g.N = rc;
+          g.ta = 1;
+          g.beta = 0;
+          g.seg0 = (int)sg_s.size();
+          g.nseg = 1;
+          sg_s.push_back(GemmSeg{Yb, Yb, mc, mc, mc, 1.0});
+          add_tiles(sg_t, g);
+          g = GemmTask{};
+          g.C = T1;
+          g.ldc = rc;
+          g.M = rc;
+          g.N = mc;
+          g.ta = 1;
+          g.beta = 0;
+          g.seg0 = (int)sg_s.size();
+          g.nseg = 1;
+          sg_s.push_back(GemmSeg{Yb, F, mc, ldF, mc, 1.0});
+          add_tiles(sg_t, g);
+          pv.push_back(PivTask{F + mc + (int64_t)mc * ldF, ldF, rc, 0, c});
+          g = GemmTask{};
+          g.C = F + mc;
+          g.ldc = ldF;
+          g.M = rc;
+          g.N = mc;
+          g.beta = 0;
+          g.seg0 = (int)sx_s.size();
+          g.nseg = 1;
+          sx_s.push_back(GemmSeg{F + mc + (int64_t)mc * ldF, T1, ldF, rc, rc, -1.0});
+          add_tiles(sx_t, g);
+        }
         // Z = L^{-1} C  (L^{-1} lower triangular: row tile tm needs k < tm + 64)
         if (W > 0) {
           for (int tn = 0; tn < W; tn += GT)
@@ -1351,7 +1528,12 @@ void factor_impl(lorasp_ctx *h, const double *values) {
       h->stg.flush(st);
       h->t_host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
       launch_gemm_dev(h, d_pt, d_ps, pt.size(), K_PROJECT, f_proj, b_proj);
+      if (h->s1_pending) CK(cudaStreamWaitEvent(st, h->ev_s1, 0));   // part 1 done (L11^{-1} in ws_S)
       launch_copy_dev(h, d_ct, ct, K_ASSEMBLE);
+      if (!sy_t.empty()) {
+        launch_gemm(h, sy_t, sy_s, K_PIVOT, 0, 0);
+        launch_gemm(h, sg_t, sg_s, K_PIVOT, 0, 0);
+      }
       if (sym) {
         cudaEvent_t pe0 = nullptr, pe1 = nullptr;
         if (h->debug) {
@@ -1375,6 +1557,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
           cudaEventDestroy(pe0);
           cudaEventDestroy(pe1);
         }
+        if (!sx_t.empty()) launch_gemm(h, sx_t, sx_s, K_PIVOT, 0, 0);
       } else {
         pivots_lu(h, pv, f_piv, b_piv);
       }
@@ -1777,7 +1960,22 @@ int lorasp_factor(lorasp_handle h, const double *values) {
     CK(cudaSetDevice(h->device));
     auto t0 = std::chrono::steady_clock::now();
     h->f_doubles = 0;
-    factor_impl(h, values);
+    // the sweep runs on the library's high-priority stream (ordered after the
+    // caller's stream), so that the low-priority overlap work (split pivots)
+    // only takes SMs the sweep leaves idle; the call returns synchronised
+    ensure_mem(h);
+    cudaStream_t user = h->stream;
+    CK(cudaEventRecord(h->ev_u, user));
+    CK(cudaStreamWaitEvent(h->stream_hi, h->ev_u, 0));
+    h->stream = h->stream_hi;
+    try {
+      factor_impl(h, values);
+    } catch (...) {
+      cudaStreamSynchronize(h->stream_hi);
+      h->stream = user;
+      throw;
+    }
+    h->stream = user;
     h->t_factor_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return (int)LORASP_OK;
   });
@@ -2140,6 +2338,22 @@ void lorasp_destroy(lorasp_handle h) {
     for (DevBuf *b : bufs) b->release();
     for (cudaEvent_t e : h->evpool) cudaEventDestroy(e);
     if (h->ap_graph) cudaGraphExecDestroy(h->ap_graph);
+    if (h->stream2) {
+      cudaStreamSynchronize(h->stream2);
+      cudaStreamDestroy(h->stream2);
+    }
+    if (h->stream_hi) {
+      cudaStreamSynchronize(h->stream_hi);
+      cudaStreamDestroy(h->stream_hi);
+    }
+    if (h->ev_u) cudaEventDestroy(h->ev_u);
+    if (h->ev_s0) cudaEventDestroy(h->ev_s0);
+    if (h->ev_s1) cudaEventDestroy(h->ev_s1);
+    if (h->h_sp) cudaFreeHost(h->h_sp);
+    h->ws_S.release();
+    h->ws_Y.release();
+    h->ws_T1.release();
+    h->d_sp.release();
     h->fpool.release();
     h->stg.release();
     if (h->h_ranks) cudaFreeHost(h->h_ranks);
