@@ -2206,6 +2206,216 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
     for (int i = lane; i < n; i += 32) t.F[i + (int64_t)j * t.ld] = (i >= j) ? A[i + (int64_t)j * lda] : 0.0;
 }
 
+// Blocked no-pivot LU of the fused LU-path pivot, same outputs as k_pivot_lu
+// (region 0 <- L^{-1}, unit lower; region 1 <- U^{-T}), for n <= PIVLU_MAXN in
+// shared memory with 16-column blocks.  LU: per block the diagonal factor by
+// one warp (lane = row), the two 16 x 16 triangular inverses, the panels
+// L21 = A21 U11^{-1} and U12 = L11^{-1} A12, the trailing A22 -= L21 U12.
+// Inverses, last block first: L21 <- -(X22 L21) X11 and U12 <- -Y11 (U12 Y22)
+// with X = L^{-1}, Y = U^{-1} of the already inverted trailing parts (scratch
+// TL, TU: n x 16 each).  Singular if |u_kk| <= 1e-14 max|A| (as k_pivot_lu).
+constexpr int PIVLU_MAXN = 148;
+__device__ __forceinline__ void lu_diag_inverses(const double *__restrict__ A, int lda, int j0, int b,
+                                                 double *__restrict__ WL, double *__restrict__ WU, int lane) {
+  // WL = L11^{-1} (unit lower, column c by lane c); WU = U11^{-1} (upper, row c by lane c)
+  if (lane >= b) return;
+  const int c = lane;
+  double x[PIVB_NB];
+#pragma unroll
+  for (int i = 0; i < PIVB_NB; ++i) {
+    double v = 0.0;
+    if (i == c) {
+      v = 1.0;
+    } else if (i > c && i < b) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int k = 0; k < PIVB_NB; ++k)
+        if (k >= c && k < i) sacc = fma(A[(j0 + i) + (int64_t)(j0 + k) * lda], x[k], sacc);
+      v = -sacc;
+    }
+    x[i] = v;
+  }
+#pragma unroll
+  for (int i = 0; i < PIVB_NB; ++i) WL[i + c * PIVB_NB] = (i < b) ? x[i] : 0.0;
+  // y = e_c^T U11^{-1}:  y_c = 1 / u_cc,  y_j = -(sum_{k=c}^{j-1} y_k u_kj) / u_jj
+#pragma unroll
+  for (int j = 0; j < PIVB_NB; ++j) {
+    double v = 0.0;
+    if (j == c) {
+      v = frcp(A[(j0 + c) + (int64_t)(j0 + c) * lda]);
+    } else if (j > c && j < b) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int k = 0; k < PIVB_NB; ++k)
+        if (k >= c && k < j) sacc = fma(x[k], A[(j0 + k) + (int64_t)(j0 + j) * lda], sacc);
+      v = -sacc * frcp(A[(j0 + j) + (int64_t)(j0 + j) * lda]);
+    }
+    x[j] = v;   // reuse: x now holds row c of U11^{-1}
+  }
+#pragma unroll
+  for (int j = 0; j < PIVB_NB; ++j) WU[c + j * PIVB_NB] = (j < b) ? x[j] : 0.0;
+}
+
+__global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restrict__ tasks, int *status) {
+  extern __shared__ double sh[];
+  __shared__ double WL[PIVB_NB * PIVB_NB], WU[PIVB_NB * PIVB_NB];
+  __shared__ int s_fail;
+  __shared__ double s_amax[16];
+  const PivTask t = tasks[blockIdx.x];
+  const int n = t.m + t.r;
+  if (n == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int lda = n | 1;
+  double *A = sh;
+  double *TL = sh + (int64_t)lda * n;           // (n x 16, ld n): X22 L21
+  double *TU = TL + (int64_t)n * PIVB_NB;       // (n x 16, ld n): (U12 Y22)^T
+  double amax = 0;
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i < n; i += 32) {
+      const double v = t.F[i + (int64_t)j * t.ld];
+      A[i + (int64_t)j * lda] = v;
+      amax = fmax(amax, fabs(v));
+    }
+  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  if (lane == 0) s_amax[warp] = amax;
+  if (tid == 0) s_fail = 0;
+  __syncthreads();
+  amax = 0;
+  for (int w = 0; w < nw; ++w) amax = fmax(amax, s_amax[w]);
+  const double tiny = 1e-14 * amax;
+  // ---------------- blocked LU (no pivoting) ----------------
+  for (int j0 = 0; j0 < n; j0 += PIVB_NB) {
+    const int b = min(PIVB_NB, n - j0), j1 = j0 + b;
+    if (warp == 0) {
+      for (int k = 0; k < b; ++k) {
+        const double piv = A[(j0 + k) + (int64_t)(j0 + k) * lda];
+        if (!(fabs(piv) > tiny) || !isfinite(piv)) {
+          if (lane == 0) {
+            s_fail = 1;
+            if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
+          }
+          break;
+        }
+        const double rp = frcp(piv);
+        double lik = 0.0;
+        if (lane > k && lane < b) {
+          lik = A[(j0 + lane) + (int64_t)(j0 + k) * lda] * rp;
+          A[(j0 + lane) + (int64_t)(j0 + k) * lda] = lik;
+        }
+        __syncwarp();
+        if (lane > k && lane < b)
+          for (int jj = k + 1; jj < b; ++jj)
+            A[(j0 + lane) + (int64_t)(j0 + jj) * lda] =
+                fma(-lik, A[(j0 + k) + (int64_t)(j0 + jj) * lda], A[(j0 + lane) + (int64_t)(j0 + jj) * lda]);
+        __syncwarp();
+      }
+      if (!s_fail) lu_diag_inverses(A, lda, j0, b, WL, WU, lane);
+    }
+    __syncthreads();
+    if (s_fail) return;
+    // panels: rows i >= j1 (L21 = A21 U11^{-1}) and columns j >= j1 (U12 = L11^{-1} A12)
+    const int rest = n - j1;
+    for (int q = tid; q < 2 * rest; q += blockDim.x) {
+      double a[PIVB_NB];
+      if (q < rest) {
+        const int i = j1 + q;
+#pragma unroll
+        for (int k = 0; k < PIVB_NB; ++k) a[k] = (k < b) ? A[i + (int64_t)(j0 + k) * lda] : 0.0;
+#pragma unroll
+        for (int c = 0; c < PIVB_NB; ++c) {
+          if (c < b) {
+            double sacc = 0.0;
+#pragma unroll
+            for (int k = 0; k <= c; ++k) sacc = fma(a[k], WU[k + c * PIVB_NB], sacc);
+            A[i + (int64_t)(j0 + c) * lda] = sacc;
+          }
+        }
+      } else {
+        const int j = j1 + (q - rest);
+#pragma unroll
+        for (int k = 0; k < PIVB_NB; ++k) a[k] = (k < b) ? A[(j0 + k) + (int64_t)j * lda] : 0.0;
+#pragma unroll
+        for (int c = 0; c < PIVB_NB; ++c) {
+          if (c < b) {
+            double sacc = a[c];   // unit diagonal of L11^{-1}
+#pragma unroll
+            for (int k = 0; k < c; ++k) sacc = fma(WL[c + k * PIVB_NB], a[k], sacc);
+            A[(j0 + c) + (int64_t)j * lda] = sacc;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // trailing: A22 -= L21 U12
+    for (int j = j1 + warp; j < n; j += nw) {
+      double uj[PIVB_NB];
+#pragma unroll
+      for (int c = 0; c < PIVB_NB; ++c) uj[c] = (c < b) ? A[(j0 + c) + (int64_t)j * lda] : 0.0;
+      for (int i = j1 + lane; i < n; i += 32) {
+        double sacc = A[i + (int64_t)j * lda];
+#pragma unroll
+        for (int c = 0; c < PIVB_NB; ++c)
+          if (c < b) sacc = fma(-A[i + (int64_t)(j0 + c) * lda], uj[c], sacc);
+        A[i + (int64_t)j * lda] = sacc;
+      }
+    }
+    __syncthreads();
+  }
+  // ---------------- blocked inverses, last block first ----------------
+  const int last = ((n - 1) / PIVB_NB) * PIVB_NB;
+  for (int j0 = last; j0 >= 0; j0 -= PIVB_NB) {
+    const int b = min(PIVB_NB, n - j0), j1 = j0 + b, rest = n - j1;
+    // (a) warp 0: WL = L11^{-1}, WU = U11^{-1}; the others:
+    //     TL[i][c] = sum_{k=j1}^{i} X22[i][k] L21[k][c]   (X22 unit lower, inverted)
+    //     TU[j][c] = sum_{k=j1}^{j} U12[c][k] Y22[k][j]   (Y22 upper, inverted)
+    if (warp == 0) {
+      lu_diag_inverses(A, lda, j0, b, WL, WU, lane);
+    } else {
+      for (int q = tid - 32; q < 2 * rest * b; q += blockDim.x - 32) {
+        if (q < rest * b) {
+          const int ii = q % rest, c = q / rest, i = j1 + ii;
+          double sacc = A[i + (int64_t)(j0 + c) * lda];   // k = i (unit diagonal of X22)
+          for (int k = j1; k < i; ++k) sacc = fma(A[i + (int64_t)k * lda], A[k + (int64_t)(j0 + c) * lda], sacc);
+          TL[ii + (int64_t)c * n] = sacc;
+        } else {
+          const int qq = q - rest * b, jj = qq % rest, c = qq / rest, j = j1 + jj;
+          double sacc = 0.0;
+          for (int k = j1; k <= j; ++k) sacc = fma(A[(j0 + c) + (int64_t)k * lda], A[k + (int64_t)j * lda], sacc);
+          TU[jj + (int64_t)c * n] = sacc;
+        }
+      }
+    }
+    __syncthreads();
+    // (b) L21 <- -TL X11,  U12 <- -Y11 TU^T,  A11 <- (X11 strict lower | Y11 upper)
+    for (int q = tid; q < 2 * rest * b; q += blockDim.x) {
+      if (q < rest * b) {
+        const int ii = q % rest, c = q / rest, i = j1 + ii;
+        double sacc = TL[ii + (int64_t)c * n];   // X11[c][c] = 1
+        for (int k = c + 1; k < b; ++k) sacc = fma(TL[ii + (int64_t)k * n], WL[k + c * PIVB_NB], sacc);
+        A[i + (int64_t)(j0 + c) * lda] = -sacc;
+      } else {
+        const int qq = q - rest * b, jj = qq % rest, c = qq / rest, j = j1 + jj;
+        double sacc = 0.0;
+        for (int k = c; k < b; ++k) sacc = fma(WU[c + k * PIVB_NB], TU[jj + (int64_t)k * n], sacc);
+        A[(j0 + c) + (int64_t)j * lda] = -sacc;
+      }
+    }
+    for (int q = tid; q < b * b; q += blockDim.x) {
+      const int i = q % b, c = q / b;
+      if (i > c) A[(j0 + i) + (int64_t)(j0 + c) * lda] = WL[i + c * PIVB_NB];
+      else A[(j0 + i) + (int64_t)(j0 + c) * lda] = WU[i + c * PIVB_NB];
+    }
+    __syncthreads();
+  }
+  // region 0 <- L^{-1} (unit lower), region 1 <- U^{-T}
+  double *R1 = t.F + (int64_t)t.ld * n;
+  for (int j = warp; j < n; j += nw)
+    for (int i = lane; i < n; i += 32) {
+      t.F[i + (int64_t)j * t.ld] = (i > j) ? A[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
+      R1[i + (int64_t)j * t.ld] = (i >= j) ? A[j + (int64_t)i * lda] : 0.0;
+    }
+}
+
 // -------------------------------------------- blocked pivot (large nodes) ----
 // For n = m + r too large for one CTA's shared memory the fused pivot is
 // factored by a right-looking blocked signed Cholesky (64-column panels; panel

@@ -443,6 +443,7 @@ void ensure_mem(lorasp_ctx *h) {
   CK(cudaFuncSetAttribute(k_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_pivot_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
+  CK(cudaFuncSetAttribute(k_pivot_lu_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024));
   CK(cudaFuncSetAttribute(k_apply_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   h->mem_ready = true;
@@ -767,11 +768,16 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
   int max_n = 0;
   for (const PivTask &t : pv) max_n = std::max(max_n, t.m + t.r);
   PivTask *dp = push(h, pv);
-  int64_t want = (int64_t)max_n * max_n + max_n;
-  int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
-  cap = std::max(cap, max_n);
   int ev = tbeg(h, K_PIVOT);
-  k_pivot_lu<<<(unsigned)pv.size(), 512, cap * 8, h->stream>>>(dp, cap, h->d_status.as<int>());
+  if (max_n <= PIVLU_MAXN && !h->pivot_unblocked) {
+    const size_t sm = ((size_t)(max_n | 1) * max_n + 2 * (size_t)max_n * PIVB_NB) * 8;
+    k_pivot_lu_blk<<<(unsigned)pv.size(), 512, sm, h->stream>>>(dp, h->d_status.as<int>());
+  } else {
+    int64_t want = (int64_t)max_n * max_n + max_n;
+    int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
+    cap = std::max(cap, max_n);
+    k_pivot_lu<<<(unsigned)pv.size(), 512, cap * 8, h->stream>>>(dp, cap, h->d_status.as<int>());
+  }
   tend(h, ev, f_piv, b_piv);
   ++h->launches_factor;
   CK(cudaGetLastError());
@@ -1559,7 +1565,28 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         }
         if (!sx_t.empty()) launch_gemm(h, sx_t, sx_s, K_PIVOT, 0, 0);
       } else {
+        cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+        if (h->debug) {
+          cudaEventCreate(&pe0);
+          cudaEventCreate(&pe1);
+          cudaEventRecord(pe0, st);
+        }
         pivots_lu(h, pv, f_piv, b_piv);
+        if (h->debug) {
+          cudaEventRecord(pe1, st);
+          cudaEventSynchronize(pe1);
+          float ms = 0;
+          cudaEventElapsedTime(&ms, pe0, pe1);
+          int nmin = 1 << 30, nmax = 0;
+          for (auto &t : pv) {
+            nmin = std::min(nmin, t.m + t.r);
+            nmax = std::max(nmax, t.m + t.r);
+          }
+          fprintf(stderr, "[lorasp] level %d wave %zu pivot: %zu tasks n in [%d, %d]: %.3f ms\n", i, w, pv.size(), nmin,
+                  nmax, ms);
+          cudaEventDestroy(pe0);
+          cudaEventDestroy(pe1);
+        }
       }
       launch_gemm_dev(h, d_zt, d_zs, zt.size(), K_ZGEMM, f_z, b_z);
       launch_gemm_dev(h, d_stt, d_ss, stt.size(), K_SCHUR, f_s, b_s);
