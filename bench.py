@@ -302,7 +302,10 @@ def main():
                        "eps": p.eps, "depth": p.depth, "leaf": p.leaf,
                        "parallelism": "replicas" if world > 1 else "single GPU",
                        "l2": "flushed between timed steps (256 MiB write, untimed)",
-                       "value_def": "n * ranks * steps / sum(factor time); PCG time reported as krylov_ms"},
+                       "value_def": "n * ranks * steps / sum(factor time); PCG time reported as krylov_ms",
+                       "schedule": ("rank-predicted: every wave enqueued with the previous factorization's ranks, "
+                                    "device ranks verified after the sweep (a miss re-runs the synchronised sweep)")
+                                   if stats.get("schedule_rank_predicted") else "per-wave rank synchronisation"},
             "factor_ms": tot_f_max / args.steps, "krylov_ms": tot_k_max / args.steps,
             "krylov_iters": its[-1], "relres": rr_last, "krylov_status": rc_last,
             "tflops_model": tflops, "fp64_peak_tflops": peak_f, "frac_fp64_peak": tflops / peak_f,

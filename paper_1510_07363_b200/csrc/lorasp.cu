@@ -255,6 +255,16 @@ struct lorasp_ctx {
   void *h_sp = nullptr;     // pinned upload of the part-1 copy + pivot task lists
   size_t h_sp_cap = 0;
   bool no_split = getenv("LORASP_NO_SPLIT") != nullptr;
+  // rank-predicted schedule: after a factorization, its ranks predict the
+  // next one's (same pattern); the host then builds and enqueues every wave
+  // without the per-wave rank synchronisation, the device ranks are logged
+  // and verified at the end, and a mismatch re-runs the synchronised sweep
+  std::vector<std::vector<int>> rank_cache;
+  bool cache_valid = false, replay_used = false;
+  int replay_hits = 0, replay_misses = 0;
+  bool no_replay = getenv("LORASP_NO_REPLAY") != nullptr;
+  int *h_ranklog = nullptr;
+  size_t ranklog_cap = 0;
   int split_min_m = getenv("LORASP_SPLIT_MIN_M") ? atoi(getenv("LORASP_SPLIT_MIN_M")) : 0;
   std::vector<int64_t> ap_graph_sig;   // launch parameters the graph was captured with
   bool no_graph = getenv("LORASP_NO_GRAPH") != nullptr;
@@ -783,7 +793,9 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
   CK(cudaGetLastError());
 }
 
-void factor_impl(lorasp_ctx *h, const double *values) {
+// Returns false only in replay mode when the predicted ranks were wrong (the
+// caller then re-runs with replay = false).
+bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
   ensure_mem(h);
   const Plan &pl = h->plan;
   cudaStream_t st = h->stream;
@@ -809,6 +821,22 @@ void factor_impl(lorasp_ctx *h, const double *values) {
   std::vector<int> prev_sld;
   h->stg.reset();
   CK(cudaStreamSynchronize(st));
+  struct RankLog {
+    int level;
+    size_t pos;
+    std::vector<int> comp;
+  };
+  std::vector<RankLog> rlog;
+  size_t rlog_pos = 0;
+  if (replay) {
+    size_t need = 0;
+    for (int i = 1; i <= L; ++i) need += (size_t)pl.lev[i].K;
+    if (h->ranklog_cap < need) {
+      if (h->h_ranklog) CK(cudaFreeHost(h->h_ranklog));
+      CK(cudaMallocHost(&h->h_ranklog, std::max<size_t>(need, 64) * sizeof(int)));
+      h->ranklog_cap = std::max<size_t>(need, 64);
+    }
+  }
 
   for (int i = L; i >= 1; --i) {
     const SymLevel &lv = pl.lev[i];
@@ -1088,6 +1116,19 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         tend(h, ev, f_eig, b_eig);
         ++h->launches_factor;
         CK(cudaGetLastError());
+        if (replay) {
+          // predicted ranks; the computed ones are logged (stream order) and
+          // compared after the final synchronisation
+          CK(cudaMemcpyAsync(h->h_ranklog + rlog_pos, h->d_ranks.p, comp.size() * sizeof(int),
+                             cudaMemcpyDeviceToHost, st));
+          rlog.push_back(RankLog{i, rlog_pos, comp});
+          rlog_pos += comp.size();
+          for (size_t q = 0; q < comp.size(); ++q) {
+            const int c = comp[q];
+            r[c] = h->rank_cache[i][c];
+            if (m[c] > 0) rho_pred = std::max(rho_pred, (double)r[c] / m[c]);
+          }
+        } else {
         CK(cudaMemcpyAsync(h->h_ranks, h->d_ranks.p, comp.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
         auto ts0 = std::chrono::steady_clock::now();
@@ -1104,6 +1145,7 @@ void factor_impl(lorasp_ctx *h, const double *values) {
         for (size_t q = 0; q < comp.size(); ++q) {
           r[comp[q]] = h->h_ranks[q];
           if (m[comp[q]] > 0) rho_pred = std::max(rho_pred, (double)r[comp[q]] / m[comp[q]]);
+        }
         }
       }
       // --- project, assemble, pivot, Z, Schur ---
@@ -1606,11 +1648,26 @@ void factor_impl(lorasp_ctx *h, const double *values) {
   CK(cudaStreamSynchronize(st));
   h->stg.reset();
   tflush(h);
+  if (replay) {
+    for (const RankLog &rl : rlog)
+      for (size_t q = 0; q < rl.comp.size(); ++q)
+        if (h->h_ranklog[rl.pos + q] != h->rank_cache[rl.level][rl.comp[q]]) {
+          ++h->replay_misses;
+          return false;
+        }
+    ++h->replay_hits;
+  }
   if (h->h_status[0] != 0)
     throw Err(h->h_status[0], std::string(h->h_status[0] == LORASP_E_EIG_NOCONV
                                               ? "Jacobi eigen-solver did not converge"
                                               : "singular pivot (signed Cholesky failed)") +
                                   " at node " + std::to_string(h->h_status[1]));
+  if (replay) {
+    // same ranks => same record layout (the pool is bump-allocated in the same
+    // order): the apply plan of the previous factorization is still valid
+    h->factored = true;
+    return true;
+  }
 
   // ---- apply plan: vector layout over red nodes of every level --------------
   std::vector<std::vector<int64_t>> voff(L + 1);
@@ -1710,6 +1767,9 @@ void factor_impl(lorasp_ctx *h, const double *values) {
   h->d_b.ensure(pl.n * 8, st);
   h->d_x.ensure(pl.n * 8, st);
   h->factored = true;
+  h->rank_cache = h->rnk;
+  h->cache_valid = true;
+  return true;
 }
 
 // x = Ã b on device buffers
@@ -1996,8 +2056,15 @@ int lorasp_factor(lorasp_handle h, const double *values) {
     CK(cudaStreamWaitEvent(h->stream_hi, h->ev_u, 0));
     h->stream = h->stream_hi;
     try {
-      factor_impl(h, values);
+      bool ok = false;
+      h->replay_used = false;
+      if (h->cache_valid && !h->no_replay) {
+        ok = factor_impl(h, values, true);
+        h->replay_used = ok;
+      }
+      if (!ok) factor_impl(h, values, false);
     } catch (...) {
+      h->cache_valid = false;
       cudaStreamSynchronize(h->stream_hi);
       h->stream = user;
       throw;
@@ -2122,6 +2189,8 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
     o << ",\"flops_model\":" << h->flops_model << ",\"factor_bytes\":" << h->f_doubles * 8
       << ",\"t_factor_host_ms\":" << h->t_factor_ms << ",\"t_task_build_ms\":" << h->t_host_ms
       << ",\"t_rank_sync_wait_ms\":" << h->t_sync_ms << ",\"launches_factor\":" << h->launches_factor
+      << ",\"schedule_rank_predicted\":" << (h->replay_used ? "true" : "false")
+      << ",\"rank_prediction_hits\":" << h->replay_hits << ",\"rank_prediction_misses\":" << h->replay_misses
       << ",\"aux_vars\":";
     int64_t aux = 0;
     for (int i = 1; i <= pl.depth; ++i)
@@ -2377,6 +2446,7 @@ void lorasp_destroy(lorasp_handle h) {
     if (h->ev_s0) cudaEventDestroy(h->ev_s0);
     if (h->ev_s1) cudaEventDestroy(h->ev_s1);
     if (h->h_sp) cudaFreeHost(h->h_sp);
+    if (h->h_ranklog) cudaFreeHost(h->h_ranklog);
     h->ws_S.release();
     h->ws_Y.release();
     h->ws_T1.release();

@@ -159,6 +159,11 @@ def test_refactor_new_values_and_determinism(L):
     h.factor(torch.tensor(p.values, device="cuda"))
     x3 = gpu_apply(h, p.b)
     assert np.array_equal(x2, x3)                        # no FP atomics: bitwise repeatable
+    st = h.stats()
+    # x3 came from the rank-predicted schedule (same values => same ranks), x2
+    # from the synchronised sweep after the miss of the new values
+    assert st["schedule_rank_predicted"] and st["rank_prediction_hits"] >= 1
+    assert st["rank_prediction_misses"] >= 1
     f = oracle_factor(p, 1e-2)
     assert rank_mismatches(h, f, p.depth, 1e-2) == []
     assert relerr(x2, O.solve(f, p.b)) <= 1e-9
