@@ -262,6 +262,7 @@ struct lorasp_ctx {
   std::vector<std::vector<int>> rank_cache;
   bool cache_valid = false, replay_used = false;
   int replay_hits = 0, replay_misses = 0;
+  int64_t split_nodes = 0;   // fused pivots factored by the split path (last factorization)
   bool no_replay = getenv("LORASP_NO_REPLAY") != nullptr;
   int *h_ranklog = nullptr;
   size_t ranklog_cap = 0;
@@ -802,6 +803,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
   const int L = pl.depth;
   const bool sym = (pl.flags & LORASP_SPD) != 0;
   h->launches_factor = 0;
+  h->split_nodes = 0;
   h->flops_model = 0;
   h->t_host_ms = 0;
   h->t_sync_ms = 0;
@@ -963,6 +965,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
             t.alpha = 1.0;
             s_ct.push_back(t);
             s_pt.push_back(PivTask{h->ws_S.as<double>() + s_off[c], m[c], m[c], 0, c});
+            ++h->split_nodes;
             s_max = std::max(s_max, m[c]);
           }
           CK(cudaEventRecord(h->ev_s0, st));   // S is final here; stream2 starts after it
@@ -2191,6 +2194,7 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
       << ",\"t_rank_sync_wait_ms\":" << h->t_sync_ms << ",\"launches_factor\":" << h->launches_factor
       << ",\"schedule_rank_predicted\":" << (h->replay_used ? "true" : "false")
       << ",\"rank_prediction_hits\":" << h->replay_hits << ",\"rank_prediction_misses\":" << h->replay_misses
+      << ",\"split_pivot_nodes\":" << h->split_nodes
       << ",\"aux_vars\":";
     int64_t aux = 0;
     for (int i = 1; i <= pl.depth; ++i)

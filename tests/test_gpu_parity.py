@@ -205,6 +205,7 @@ def test_3d_upper_levels_parity(L, dims, depth):
     p = make_problem("cfg3", dims=dims, depth=depth)
     h = L.analyze_problem(p)
     h.factor(torch.tensor(p.values, device="cuda"))
+    assert h.stats()["split_pivot_nodes"] > 0       # the split pivot path is exercised
     f = oracle_factor(p, p.eps)
     assert max(max(f.rank.get((i, c), 0) for c in range(2 ** (i - 1))) for i in range(1, depth + 1)) > 64
     assert rank_mismatches(h, f, p.depth, p.eps) == []
