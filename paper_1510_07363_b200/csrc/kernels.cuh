@@ -479,28 +479,19 @@ __device__ __forceinline__ void invit_one(const double *__restrict__ d, const do
     const double DLi = e[i];
     double Dn = d[i + 1] - sft;
     double DUn = (i < m - 2) ? e[i + 1] : 0.0;
-    if (fabs(Di) >= fabs(DLi)) {
-      if (Di == 0.0) Di = pertol;
-      const double f = DLi * frcp(Di);
-      D[i * S] = Di;
-      DL[i * S] = f;
-      DU[i * S] = DUi;
-      DU2[i * S] = 0.0;
-      piv[i * S] = 0;
-      Dn = fma(-f, DUi, Dn);
-    } else {
-      const double f = Di * frcp(DLi);
-      D[i * S] = DLi;
-      DL[i * S] = f;
-      DU[i * S] = Dn;
-      DU2[i * S] = DUn;
-      piv[i * S] = 1;
-      const double nd = fma(-f, Dn, DUi);
-      DUn = -f * DUn;
-      Dn = nd;
-    }
-    Di = Dn;
-    DUi = DUn;
+    // partial pivoting by selects (threads run different vectors: no divergence)
+    const bool np = fabs(Di) >= fabs(DLi);
+    if (np && Di == 0.0) Di = pertol;
+    const double den = np ? Di : DLi, num = np ? DLi : Di;
+    const double f = num * frcp(den);
+    D[i * S] = den;
+    DL[i * S] = f;
+    DU[i * S] = np ? DUi : Dn;
+    DU2[i * S] = np ? 0.0 : DUn;
+    piv[i * S] = np ? 0 : 1;
+    const double nd = fma(-f, np ? DUi : Dn, np ? Dn : DUi);
+    DUi = np ? DUn : -f * DUn;
+    Di = nd;
   }
   D[(m - 1) * S] = Di;
 #pragma unroll 4
@@ -517,13 +508,9 @@ __device__ __forceinline__ void invit_one(const double *__restrict__ d, const do
     for (int i = 0; i < m - 1; ++i) {
       const double bn = b[(i + 1) * S];
       const double l = DL[i * S];
-      if (piv[i * S] == 0) {
-        b[i * S] = bi;
-        bi = fma(-l, bi, bn);
-      } else {
-        b[i * S] = bn;
-        bi = fma(-l, bn, bi);
-      }
+      const bool pv = piv[i * S] != 0;
+      b[i * S] = pv ? bn : bi;
+      bi = fma(-l, pv ? bn : bi, pv ? bi : bn);
     }
     double x1 = bi * D[(m - 1) * S], x2 = 0.0;
     b[(m - 1) * S] = x1;
