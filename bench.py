@@ -115,15 +115,35 @@ class ClockSampler:
 
 
 def dist_init():
+    """One process per GPU (torchrun env).  NCCL on the GPU box; the CPU tests of
+    the multi-process plumbing select gloo with LORASP_BENCH_BACKEND=gloo."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = "nccl"
+        backend = os.environ.get("LORASP_BENCH_BACKEND", "nccl")
         dist.init_process_group(backend=backend, rank=rank, world_size=world)
     return world, rank, local
+
+
+def max_over_ranks(values, world, device="cpu"):
+    """Element-wise max over ranks of per-rank device times (the timing rule:
+    the job is as slow as its slowest rank).  Identity for one process."""
+    import torch
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t]
+
+
+def weak_scaling_value(n, world, steps, max_total_ms):
+    """Whole-job throughput: every rank factors its own replica of the n-unknown
+    workload, so the job processes n * world * steps unknowns in the slowest
+    rank's time."""
+    return n * world * steps / (max_total_ms / 1e3)
 
 
 def cpu_baseline(p, sample="factor+krylov"):
@@ -253,12 +273,8 @@ def main():
     stats = h.stats()
     h.set_timing(False)
     tot_f = sum(tfs)
-    tot = torch.tensor([tot_f, sum(tks)], dtype=torch.float64, device=dev)
-    if world > 1:
-        import torch.distributed as dist
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    tot_f_max, tot_k_max = float(tot[0]), float(tot[1])
-    value = p.n * world * args.steps / (tot_f_max / 1e3)
+    tot_f_max, tot_k_max = max_over_ranks([tot_f, sum(tks)], world, dev)
+    value = weak_scaling_value(p.n, world, args.steps, tot_f_max)
     flops = stats["flops_model"]
     peak_f, peak_src = fp64_peak()
     tflops = flops / (tot_f_max / args.steps / 1e3) / 1e12
@@ -337,13 +353,10 @@ def main():
             if s >= args.warmup:
                 tfe.append(t1 - t0)
                 tke.append(t2 - t1)
-        te = torch.tensor([sum(tfe), sum(tke)], dtype=torch.float64, device=dev)
-        if world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        line["e2e"] = {"value": p.n * world * args.steps / float(te[0]), "unit": "unknowns/s",
+        te = max_over_ranks([sum(tfe), sum(tke)], world, dev)
+        line["e2e"] = {"value": weak_scaling_value(p.n, world, args.steps, 1e3 * te[0]), "unit": "unknowns/s",
                        "h2d_bytes_per_step": 8 * (p.nnz + p.n), "d2h_bytes_per_step": 8 * p.n,
-                       "factor_ms": 1e3 * float(te[0]) / args.steps, "krylov_ms": 1e3 * float(te[1]) / args.steps,
+                       "factor_ms": 1e3 * te[0] / args.steps, "krylov_ms": 1e3 * te[1] / args.steps,
                        "how": "host wall clock around the synchronous C-ABI calls, pinned host buffers"}
     if rank == 0:
         print(json.dumps(line))
