@@ -189,6 +189,94 @@ __global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask *__restrict__ ta
 // y_k / ||y_k|| = v_k, without accumulating V.  Cyclic round-robin pairs, one
 // warp per pair.  Rank r = #{sigma_k >= eps sigma_0}; eps = 0 keeps every
 // direction (reading Z3): V = I_m, r = m (r = 0 if G = 0, reading Z4).
+// k_gemm2: same task semantics as k_gemm (C tile 64 x 64 = sum_seg alpha op(A)
+// op(B), beta accumulate, tc = store transposed), 128 threads with 4 x 8
+// accumulators each (32 FMAs per 12 shared loads), cp.async double-buffered
+// 16-deep K chunks (no staging registers), alpha folded into the A fragment
+// (one accumulator set across segments).  Up to 4 CTAs per SM.
+constexpr int G2K = 16;
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem, const void *gbase, bool pred) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 8 : 0;   // 0: zero-fill (the source, a valid global address, is not read)
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(pred ? gmem : gbase), "r"(sz)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(128, 4) k_gemm2(const GemmTask *__restrict__ tasks,
+                                                const GemmSeg *__restrict__ segs) {
+  const GemmTask t = tasks[blockIdx.x];
+  __shared__ __align__(16) double As[2][G2K][GT + 1];
+  __shared__ __align__(16) double Bs[2][G2K][GT + 1];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;   // rows tx + 16 a, columns ty + 8 b
+  double acc[4][8];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+
+  for (int s = 0; s < t.nseg; ++s) {
+    const GemmSeg g = segs[t.seg0 + s];
+    if (g.K <= 0) continue;
+    auto load = [&](int k0, int st) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int idx = tid + 128 * q;   // 0 .. 1023
+        int i, kk;
+        if (!t.ta) { i = idx & 63; kk = idx >> 6; } else { kk = idx & 15; i = idx >> 4; }
+        const int gi = t.tm + i, gk = k0 + kk;
+        const bool pa = gi < t.M && gk < g.K;
+        cp_async8(&As[st][kk][i], t.ta ? g.A + (gk + (int64_t)gi * g.lda) : g.A + (gi + (int64_t)gk * g.lda), g.A, pa);
+        int j;
+        if (!t.tb) { kk = idx & 15; j = idx >> 4; } else { j = idx & 63; kk = idx >> 6; }
+        const int gj = t.tn + j, gk2 = k0 + kk;
+        const bool pb = gj < t.N && gk2 < g.K;
+        cp_async8(&Bs[st][kk][j], t.tb ? g.B + (gj + (int64_t)gk2 * g.ldb) : g.B + (gk2 + (int64_t)gj * g.ldb), g.B, pb);
+      }
+      cp_async_commit();
+    };
+    const double alpha = g.alpha;
+    const int nch = (g.K + G2K - 1) / G2K;
+    load(0, 0);
+    for (int c = 0; c < nch; ++c) {
+      if (c + 1 < nch) {
+        load((c + 1) * G2K, (c + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const int st = c & 1;
+#pragma unroll
+      for (int kk = 0; kk < G2K; ++kk) {
+        double av[4], bv[8];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = alpha * As[st][kk][tx + 16 * a];
+#pragma unroll
+        for (int b = 0; b < 8; ++b) bv[b] = Bs[st][kk][ty + 8 * b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+      }
+      __syncthreads();   // stage st is refilled by the load two chunks ahead
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int i = t.tm + tx + 16 * a, j = t.tn + ty + 8 * b;
+      if (i < t.M && j < t.N) {
+        double *p = t.tc ? &t.C[j + (int64_t)i * t.ldc] : &t.C[i + (int64_t)j * t.ldc];
+        *p = t.beta ? (*p + acc[a][b]) : acc[a][b];
+      }
+    }
+}
+
 struct EigTask {
   const double *G;   // m x m, ld m
   double *V;         // out: m x r (ld m), columns sorted by sigma descending

@@ -255,6 +255,7 @@ struct lorasp_ctx {
   void *h_sp = nullptr;     // pinned upload of the part-1 copy + pivot task lists
   size_t h_sp_cap = 0;
   bool no_split = getenv("LORASP_NO_SPLIT") != nullptr;
+  bool gemm_v1 = getenv("LORASP_GEMM_V1") != nullptr;   // debug: the 256-thread 4 x 4 GEMM
   // rank-predicted schedule: after a factorization, its ranks predict the
   // next one's (same pattern); the host then builds and enqueues every wave
   // without the per-wave rank synchronisation, the device ranks are logged
@@ -478,7 +479,8 @@ void launch_gemm_dev(lorasp_ctx *h, const GemmTask *dt, const GemmSeg *ds, size_
                      double bytes) {
   if (ntasks == 0) return;
   int ev = cls >= 0 ? tbeg(h, cls) : -1;
-  k_gemm<<<(unsigned)ntasks, 256, 0, h->stream>>>(dt, ds);
+  if (h->gemm_v1) k_gemm<<<(unsigned)ntasks, 256, 0, h->stream>>>(dt, ds);
+  else k_gemm2<<<(unsigned)ntasks, 128, 0, h->stream>>>(dt, ds);
   tend(h, ev, flops, bytes);
   ++h->launches_factor;
   CK(cudaGetLastError());
@@ -501,7 +503,8 @@ void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::v
   GemmSeg *ds = push(h, segs);
   GemmTask *dt = push(h, tasks);
   int ev = cls >= 0 ? tbeg(h, cls) : -1;
-  k_gemm<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt, ds);
+  if (h->gemm_v1) k_gemm<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt, ds);
+  else k_gemm2<<<(unsigned)tasks.size(), 128, 0, h->stream>>>(dt, ds);
   tend(h, ev, flops, bytes);
   ++h->launches_factor;
   CK(cudaGetLastError());
