@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <type_traits>
 
 namespace lorasp {
 
@@ -250,18 +251,28 @@ __global__ void __launch_bounds__(128, 4) k_gemm2(const GemmTask *__restrict__ t
       }
       __syncthreads();
       const int st = c & 1;
+      // alpha = +-1 (every segment the sweep issues) rides on the FMA's operand
+      // negation for free; other values scale the A fragment
+      auto chunk = [&](auto sgn) {
 #pragma unroll
-      for (int kk = 0; kk < G2K; ++kk) {
-        double av[4], bv[8];
+        for (int kk = 0; kk < G2K; ++kk) {
+          double av[4], bv[8];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) av[a] = alpha * As[st][kk][tx + 16 * a];
+          for (int a = 0; a < 4; ++a) {
+            const double x = As[st][kk][tx + 16 * a];
+            av[a] = decltype(sgn)::value == 0 ? alpha * x : (decltype(sgn)::value > 0 ? x : -x);
+          }
 #pragma unroll
-        for (int b = 0; b < 8; ++b) bv[b] = Bs[st][kk][ty + 8 * b];
+          for (int b = 0; b < 8; ++b) bv[b] = Bs[st][kk][ty + 8 * b];
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+          for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
-      }
+            for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        }
+      };
+      if (alpha == 1.0) chunk(std::integral_constant<int, 1>{});
+      else if (alpha == -1.0) chunk(std::integral_constant<int, -1>{});
+      else chunk(std::integral_constant<int, 0>{});
       __syncthreads();   // stage st is refilled by the load two chunks ahead
     }
   }
