@@ -89,6 +89,7 @@ struct GemmTask {
   int ta, tb, tc;    // op(A) = A^T, op(B) = B^T, C stored transposed
   int beta;          // 0: overwrite, 1: accumulate
   int seg0, nseg;
+  int tnw;           // k_gemm2 tile width: 32 for narrow products (N <= 32), else 64 (0 = 64)
 };
 
 constexpr int GT = 64, GK = 32;
@@ -206,18 +207,18 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__global__ void __launch_bounds__(128, 4) k_gemm2(const GemmTask *__restrict__ tasks,
-                                                const GemmSeg *__restrict__ segs) {
-  const GemmTask t = tasks[blockIdx.x];
-  __shared__ __align__(16) double As[2][G2K][GT + 1];
-  __shared__ __align__(16) double Bs[2][G2K][GT + 1];
+// One 64 x (8 NB) tile of a k_gemm2 task (NB = 8: 64 columns, NB = 4: 32).
+template <int NB>
+__device__ __forceinline__ void gemm2_tile(const GemmTask &t, const GemmSeg *__restrict__ segs,
+                                           double (*As)[G2K][GT + 1], double (*Bs)[G2K][GT + 1]) {
+  constexpr int TN = 8 * NB;
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;   // rows tx + 16 a, columns ty + 8 b
-  double acc[4][8];
+  double acc[4][NB];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+    for (int b = 0; b < NB; ++b) acc[a][b] = 0.0;
 
   for (int s = 0; s < t.nseg; ++s) {
     const GemmSeg g = segs[t.seg0 + s];
@@ -225,17 +226,21 @@ __global__ void __launch_bounds__(128, 4) k_gemm2(const GemmTask *__restrict__ t
     auto load = [&](int k0, int st) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int idx = tid + 128 * q;   // 0 .. 1023
+        const int idx = tid + 128 * q;   // A: 64 x 16
         int i, kk;
         if (!t.ta) { i = idx & 63; kk = idx >> 6; } else { kk = idx & 15; i = idx >> 4; }
         const int gi = t.tm + i, gk = k0 + kk;
-        const bool pa = gi < t.M && gk < g.K;
-        cp_async8(&As[st][kk][i], t.ta ? g.A + (gk + (int64_t)gi * g.lda) : g.A + (gi + (int64_t)gk * g.lda), g.A, pa);
-        int j;
-        if (!t.tb) { kk = idx & 15; j = idx >> 4; } else { j = idx & 63; kk = idx >> 6; }
-        const int gj = t.tn + j, gk2 = k0 + kk;
-        const bool pb = gj < t.N && gk2 < g.K;
-        cp_async8(&Bs[st][kk][j], t.tb ? g.B + (gj + (int64_t)gk2 * g.ldb) : g.B + (gk2 + (int64_t)gj * g.ldb), g.B, pb);
+        cp_async8(&As[st][kk][i], t.ta ? g.A + (gk + (int64_t)gi * g.lda) : g.A + (gi + (int64_t)gk * g.lda), g.A,
+                  gi < t.M && gk < g.K);
+      }
+#pragma unroll
+      for (int q = 0; q < TN / 8; ++q) {
+        const int idx = tid + 128 * q;   // B: 16 x TN
+        int j, kk;
+        if (!t.tb) { kk = idx & 15; j = idx >> 4; } else { j = idx % TN; kk = idx / TN; }
+        const int gj = t.tn + j, gk = k0 + kk;
+        cp_async8(&Bs[st][kk][j], t.tb ? g.B + (gj + (int64_t)gk * g.ldb) : g.B + (gk + (int64_t)gj * g.ldb), g.B,
+                  gj < t.N && gk < g.K);
       }
       cp_async_commit();
     };
@@ -256,18 +261,18 @@ __global__ void __launch_bounds__(128, 4) k_gemm2(const GemmTask *__restrict__ t
       auto chunk = [&](auto sgn) {
 #pragma unroll
         for (int kk = 0; kk < G2K; ++kk) {
-          double av[4], bv[8];
+          double av[4], bv[NB];
 #pragma unroll
           for (int a = 0; a < 4; ++a) {
             const double x = As[st][kk][tx + 16 * a];
             av[a] = decltype(sgn)::value == 0 ? alpha * x : (decltype(sgn)::value > 0 ? x : -x);
           }
 #pragma unroll
-          for (int b = 0; b < 8; ++b) bv[b] = Bs[st][kk][ty + 8 * b];
+          for (int b = 0; b < NB; ++b) bv[b] = Bs[st][kk][ty + 8 * b];
 #pragma unroll
           for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 8; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+            for (int b = 0; b < NB; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
         }
       };
       if (alpha == 1.0) chunk(std::integral_constant<int, 1>{});
@@ -279,13 +284,22 @@ __global__ void __launch_bounds__(128, 4) k_gemm2(const GemmTask *__restrict__ t
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
+    for (int b = 0; b < NB; ++b) {
       const int i = t.tm + tx + 16 * a, j = t.tn + ty + 8 * b;
       if (i < t.M && j < t.N) {
         double *p = t.tc ? &t.C[j + (int64_t)i * t.ldc] : &t.C[i + (int64_t)j * t.ldc];
         *p = t.beta ? (*p + acc[a][b]) : acc[a][b];
       }
     }
+}
+
+__global__ void __launch_bounds__(128, 4) k_gemm2(const GemmTask *__restrict__ tasks,
+                                                const GemmSeg *__restrict__ segs) {
+  __shared__ __align__(16) double As[2][G2K][GT + 1];
+  __shared__ __align__(16) double Bs[2][G2K][GT + 1];
+  const GemmTask t = tasks[blockIdx.x];
+  if (t.tnw == 32) gemm2_tile<4>(t, segs, As, Bs);
+  else gemm2_tile<8>(t, segs, As, Bs);
 }
 
 struct EigTask {

@@ -576,8 +576,19 @@ void launch_copy(lorasp_ctx *h, const std::vector<CopyTask> &tasks, int cls) {
 }
 
 // tile a logical M x N product into 64x64 tasks
+static bool g_narrow_tiles = getenv("LORASP_GEMM_V1") == nullptr;   // k_gemm2 supports 64 x 32 tiles
 void add_tiles(std::vector<GemmTask> &tasks, GemmTask base, int kmax_by_row = 0) {
   (void)kmax_by_row;
+  if (g_narrow_tiles && base.N <= 32) {   // narrow product (e.g. R_k = A_k^T V with r <= 32)
+    for (int tm = 0; tm < base.M; tm += GT) {
+      GemmTask t = base;
+      t.tm = tm;
+      t.tn = 0;
+      t.tnw = 32;
+      tasks.push_back(t);
+    }
+    return;
+  }
   for (int tn = 0; tn < base.N; tn += GT)
     for (int tm = 0; tm < base.M; tm += GT) {
       GemmTask t = base;
