@@ -835,6 +835,101 @@ __device__ __forceinline__ void orth_backtr(double *V, const double *A, const do
   }
 }
 
+// Eigenvalues of the tridiagonal (d, e) for Compress (P:l.333-359, l.580-584):
+// Gershgorin bounds, scaling to |T| <= 1, lambda_0 by warp multisection, the
+// candidates with lambda >= (eps sigma_0)^2 / 4 by group multisection; writes
+// lam[0..ncomp), t.sig, *t.rank_out; restores d; returns the rank r and the
+// scale bnorm.  Every thread of the block calls it.
+__device__ __forceinline__ int eig_values_phase(const EigTask &t, double eps, int m, int mp, double *d, const double *e,
+                                                double *e2, double *lam, double *s_red, double *s_bc, int *s_int,
+                                                double &bnorm_out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double gl = 1e300, gu = -1e300, emax2 = 0;
+  for (int i = tid; i < m; i += blockDim.x) {
+    double off = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < m - 1 ? fabs(e[i]) : 0.0);
+    gl = fmin(gl, d[i] - off);
+    gu = fmax(gu, d[i] + off);
+    if (i < m - 1) {
+      e2[i] = e[i] * e[i];
+      emax2 = fmax(emax2, e2[i]);
+    }
+  }
+  // block min / max
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+  }
+  __syncthreads();
+  if (lane == 0) {
+    s_red[warp] = gl;
+    s_red[16 + warp] = gu;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 1e300, b = -1e300;
+    for (int w = 0; w < nw; ++w) {
+      a = fmin(a, s_red[w]);
+      b = fmax(b, s_red[16 + w]);
+    }
+    s_bc[0] = a;
+    s_bc[1] = b;
+  }
+  __syncthreads();
+  if (lane == 0) s_red[warp] = emax2;
+  __syncthreads();
+  double em = 0;
+  for (int w = 0; w < nw; ++w) em = fmax(em, s_red[w]);
+  gl = s_bc[0];
+  gu = s_bc[1];
+  const double bnorm = fmax(fabs(gl), fabs(gu));
+  // work on T / bnorm (|d|, |e| <= 1): the division-free Sturm recurrence then
+  // cannot overflow within a few hundred steps; eigenvalues are scaled back.
+  const double isc = 1.0 / bnorm;
+  __syncthreads();
+  for (int i = tid; i < mp; i += blockDim.x) {
+    if (i < m) {
+      d[i] *= isc;
+      if (i < m - 1) e2[i] *= isc * isc;
+      else e2[i] = 0.0;
+    } else {
+      d[i] = 4.0;   // padding: no sign change for x < 4
+      e2[i] = 0.0;
+    }
+  }
+  gl *= isc;
+  gu *= isc;
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, em * isc * isc) * 1e10;
+  gl -= 2.2e-16 * 2 * m + 2 * pivmin;
+  gu += 2.2e-16 * 2 * m + 2 * pivmin;
+  __syncthreads();
+  if (warp == 0) {
+    double l0 = warp_eig_asc(d, e2, m, m - 1, gl, gu, pivmin);
+    if (lane == 0) {
+      lam[0] = l0 * bnorm;
+      double thr = eps * sqrt(fmax(l0, 0.0));
+      thr = thr * thr;
+      int below = sturm_count(d, e2, m, 0.25 * thr, pivmin);
+      s_int[0] = min(m, m - below + 1);  // candidates to compute (superset of kept + 1)
+    }
+  }
+  __syncthreads();
+  if (t.dbg && tid == 0) t.dbg[10] = clock64();
+  const int ncomp = s_int[0];
+  grp_multisect<4>(d, e2, m, 1, ncomp, gl, gu, pivmin, lam, bnorm);
+  __syncthreads();
+  // restore T (inverse iteration works on the unscaled tridiagonal)
+  for (int i = tid; i < m; i += blockDim.x) d[i] *= bnorm;
+  __syncthreads();
+  const double sig0 = sqrt(fmax(lam[0], 0.0));
+  int r = 0;
+  for (int k = 0; k < ncomp; ++k) r += (sqrt(fmax(lam[k], 0.0)) >= eps * sig0);
+  for (int k = tid; k < m; k += blockDim.x) t.sig[k] = (k < ncomp) ? sqrt(fmax(lam[k], 0.0)) : 0.0;
+  if (tid == 0) *t.rank_out = r;
+  bnorm_out = bnorm;
+  return r;
+}
+
 constexpr int EIG_THREADS = 256;      // generic path
 constexpr int EIG_REG_THREADS = 512;  // register-tile path (m <= 128)
 constexpr int EIG_REG_M = 128;
@@ -1529,88 +1624,8 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
   }
   if (t.dbg && tid == 0) t.dbg[1] = clock64();
   // ---- 2. eigenvalues (Sturm multisection) ----
-  double gl = 1e300, gu = -1e300, emax2 = 0;
-  for (int i = tid; i < m; i += blockDim.x) {
-    double off = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < m - 1 ? fabs(e[i]) : 0.0);
-    gl = fmin(gl, d[i] - off);
-    gu = fmax(gu, d[i] + off);
-    if (i < m - 1) {
-      e2[i] = e[i] * e[i];
-      emax2 = fmax(emax2, e2[i]);
-    }
-  }
-  // block min / max
-  for (int o = 16; o > 0; o >>= 1) {
-    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
-    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
-    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
-  }
-  __syncthreads();
-  if (lane == 0) {
-    s_red[warp] = gl;
-    s_red[16 + warp] = gu;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double a = 1e300, b = -1e300;
-    for (int w = 0; w < nw; ++w) {
-      a = fmin(a, s_red[w]);
-      b = fmax(b, s_red[16 + w]);
-    }
-    s_bc[0] = a;
-    s_bc[1] = b;
-  }
-  __syncthreads();
-  if (lane == 0) s_red[warp] = emax2;
-  __syncthreads();
-  double em = 0;
-  for (int w = 0; w < nw; ++w) em = fmax(em, s_red[w]);
-  gl = s_bc[0];
-  gu = s_bc[1];
-  const double bnorm = fmax(fabs(gl), fabs(gu));
-  // work on T / bnorm (|d|, |e| <= 1): the division-free Sturm recurrence then
-  // cannot overflow within a few hundred steps; eigenvalues are scaled back.
-  const double isc = 1.0 / bnorm;
-  __syncthreads();
-  for (int i = tid; i < mp; i += blockDim.x) {
-    if (i < m) {
-      d[i] *= isc;
-      if (i < m - 1) e2[i] *= isc * isc;
-      else e2[i] = 0.0;
-    } else {
-      d[i] = 4.0;   // padding: no sign change for x < 4
-      e2[i] = 0.0;
-    }
-  }
-  gl *= isc;
-  gu *= isc;
-  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, em * isc * isc) * 1e10;
-  gl -= 2.2e-16 * 2 * m + 2 * pivmin;
-  gu += 2.2e-16 * 2 * m + 2 * pivmin;
-  __syncthreads();
-  if (warp == 0) {
-    double l0 = warp_eig_asc(d, e2, m, m - 1, gl, gu, pivmin);
-    if (lane == 0) {
-      lam[0] = l0 * bnorm;
-      double thr = eps * sqrt(fmax(l0, 0.0));
-      thr = thr * thr;
-      int below = sturm_count(d, e2, m, 0.25 * thr, pivmin);
-      s_int[0] = min(m, m - below + 1);  // candidates to compute (superset of kept + 1)
-    }
-  }
-  __syncthreads();
-  if (t.dbg && tid == 0) t.dbg[10] = clock64();
-  const int ncomp = s_int[0];
-  grp_multisect<4>(d, e2, m, 1, ncomp, gl, gu, pivmin, lam, bnorm);
-  __syncthreads();
-  // restore T (inverse iteration works on the unscaled tridiagonal)
-  for (int i = tid; i < m; i += blockDim.x) d[i] *= bnorm;
-  __syncthreads();
-  const double sig0 = sqrt(fmax(lam[0], 0.0));
-  int r = 0;
-  for (int k = 0; k < ncomp; ++k) r += (sqrt(fmax(lam[k], 0.0)) >= eps * sig0);
-  for (int k = tid; k < m; k += blockDim.x) t.sig[k] = (k < ncomp) ? sqrt(fmax(lam[k], 0.0)) : 0.0;
-  if (tid == 0) *t.rank_out = r;
+  double bnorm;
+  const int r = eig_values_phase(t, eps, m, mp, d, e, e2, lam, s_red, s_bc, s_int, bnorm);
   if constexpr (PRE) {
     // PRE pipeline stage 0 ends here: the kept eigenvalues and ||T|| bound go to
     // the tridiagonal record for k_invit_multi; MGS + back-transformation follow
