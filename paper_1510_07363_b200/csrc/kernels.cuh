@@ -946,7 +946,7 @@ __host__ __device__ __forceinline__ int64_t rec_lam_off(int m) { return 4 * (int
 // k_eig_t<true>.
 template <bool PROF, int QR = 4, int NW = 16, int UW = 8>
 __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__restrict__ tasks, double eps,
-                                                                    long long *prof, int variant = 0) {
+                                                                    long long *prof) {
   constexpr int MR = 32 * QR;   // tile rows (= NW * UW columns)
   static_assert(MR == NW * UW, "square register tile");
   long long pt[6] = {0, 0, 0, 0, 0, 0}, pc = 0;
@@ -1056,7 +1056,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
     // a row group q whose 32 rows are all <= k, multiplies / updates by exact
     // zeros (v and the masked p vanish there), so it is skipped (bitwise the
     // same result, ~1/3 of the full-tile FP64 work on average).
-    const bool wact = UW * warp + UW - 1 > k && variant != 4 && variant != 6;
+    const bool wact = UW * warp + UW - 1 > k;
     if (warp == ((k + 1) / UW) && k + 1 < m - 2) {
       // owner of column k+1 publishes it (as of before update k) for the form warp
       const int u1 = (k + 1) % UW;
@@ -1089,9 +1089,9 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
     }
 
     TRID_PROF(0)
-    if (variant != 3) __syncthreads();                            // (2) partials visible
+    __syncthreads();                                              // (2) partials visible
     TRID_PROF(1)
-    if (tid < MR && variant != 2) {
+    if (tid < MR) {
       double h[NW];
 #pragma unroll
       for (int w = 0; w < NW; ++w) h[w] = ps_part[w][tid];
@@ -1108,7 +1108,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
       if (lane == 0) s_red[warp] = pvw;
     }
     TRID_PROF(2)
-    if (variant != 3) __syncthreads();                            // (3) p visible
+    __syncthreads();                                              // (3) p visible
     TRID_PROF(3)
     const double pv = QR == 4 ? (s_red[0] + s_red[1]) + (s_red[2] + s_red[3])
                               : (QR == 2 ? s_red[0] + s_red[1] : s_red[0]);
@@ -1116,7 +1116,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
     // (vr, wr, v_c, w_c are re-read from shared memory here: with the 32-double
     // tile live, keeping them in registers across form_v would spill)
     const double *psc = ps + UW * warp, *vsc = vs + UW * warp;
-    if (UW * warp + UW - 1 > k && variant != 5 && variant != 6) {
+    if (wact) {
       double vq[QR], wq[QR];
 #pragma unroll
       for (int q = 0; q < QR; ++q) {
@@ -1136,7 +1136,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
     // k >= 7; warp 15 before), from the published column and the same update
     // formula the owner applies in registers (bitwise the same column), so it
     // overlaps the other warps' updates instead of trailing the owner's.
-    if (warp == (k1 >= UW ? 0 : NW - 1) && k1 < m - 2 && variant != 1 && variant != 6) {
+    if (warp == (k1 >= UW ? 0 : NW - 1) && k1 < m - 2) {
       const double vcu = vs[k1], wcu = fma(alpha, vcu, ps[k1]);
       double col[QR];
 #pragma unroll

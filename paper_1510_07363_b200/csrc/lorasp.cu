@@ -2318,20 +2318,6 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
           k_tridiag_reg<false><<<1, EIG_REG_THREADS>>>(de, eps, nullptr);   // warm-up (timing below)
           CK(cudaDeviceSynchronize());
         }
-        if (ddbg) {
-          for (int var = 1; var <= 6; ++var) {
-            cudaEvent_t f0, f1;
-            cudaEventCreate(&f0);
-            cudaEventCreate(&f1);
-            cudaEventRecord(f0);
-            k_tridiag_reg<false><<<1, EIG_REG_THREADS>>>(de, eps, nullptr, var);
-            cudaEventRecord(f1);
-            cudaEventSynchronize(f1);
-            float ms = 0;
-            cudaEventElapsedTime(&ms, f0, f1);
-            fprintf(stderr, "[k_tridiag_reg variant %d] %.1f us\n", var, 1e3 * ms);
-          }
-        }
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
