@@ -2623,6 +2623,12 @@ struct ApNode {
   int sym;         // SPD: apply D = diag(I_m, -I_r)
   int m, r, W, ld;
   int seg0, nseg;
+  int nsplit;      // split apply: Z column parts (1 = one CTA streams the whole record)
+  int64_t upart;   // split apply: offset of the nsplit x n partial backward sums
+};
+// one CTA of a split wave: Z columns [c0, c1) of node `node` (part p)
+struct ApPart {
+  int node, c0, c1, p;
 };
 struct ApSeg {
   int64_t voff;   // vector offset of the target's Var/RHS
@@ -2841,6 +2847,155 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
       }
     }
     __syncthreads();
+  }
+}
+
+// ---- split apply (waves with few, large records) --------------------------
+// The fused kernels stream a node's whole record with one CTA; for the upper
+// levels (few nodes per wave, records of MBs) the Z columns are split over
+// CTAs instead.  Forward: k_apply_fwd_y (y = L^{-1}[:, :m] rhs, one CTA per
+// node) then k_apply_fwd_z (zo = Z^T D y for a column slice, scattered into the
+// targets; slices own disjoint target entries).  Backward: k_apply_bwd_z
+// (partial Z x_T per slice into scratch) then k_apply_bwd_l (u = y - sum of
+// the partials in slice order, D u, x_s = L^{-T} u): deterministic.
+__global__ void __launch_bounds__(256) k_apply_fwd_y(const ApNode *__restrict__ nodes, double *__restrict__ vec) {
+  extern __shared__ __align__(16) double sh[];
+  const ApNode nd = nodes[blockIdx.x];
+  const int n = nd.m + nd.r;
+  if (n == 0) return;
+  double *rhs = sh;
+  for (int i = threadIdx.x; i < nd.m; i += blockDim.x) rhs[i] = vec[nd.off_s + i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double s0 = 0, s1 = 0;
+    const int kl = min(nd.m - 1, i);
+    int k = 0;
+    for (; k + 1 <= kl; k += 2) {
+      s0 = fma(nd.F[i + (int64_t)k * nd.ld], rhs[k], s0);
+      s1 = fma(nd.F[i + (int64_t)(k + 1) * nd.ld], rhs[k + 1], s1);
+    }
+    if (k <= kl) s0 = fma(nd.F[i + (int64_t)k * nd.ld], rhs[k], s0);
+    nd.y[i] = s0 + s1;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_apply_fwd_z(const ApNode *__restrict__ nodes, const ApPart *__restrict__ parts,
+                                                     const ApSeg *__restrict__ segs, double *__restrict__ vec,
+                                                     int chunk_doubles) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) uint64_t bars[2];
+  const ApPart P = parts[blockIdx.x];
+  const ApNode nd = nodes[P.node];
+  const int n = nd.m + nd.r, ncol = P.c1 - P.c0;
+  if (n == 0 || ncol <= 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double *stage0 = sh, *stage1 = sh + chunk_doubles, *dy = stage1 + chunk_doubles, *zo = dy + n;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double y = nd.y[i];
+    dy[i] = (i < nd.m || !nd.sym) ? y : -y;
+  }
+  __syncthreads();
+  const int ld = nd.ld;
+  const int cc = max(1, chunk_doubles / ld);
+  ColStream Bz{nd.F + nd.zf_off + (int64_t)P.c0 * ld, ld, ncol, cc, {stage0, stage1}, bars};
+  const int nb = Bz.nchunks();
+  if (tid == 0) Bz.issue(0);
+  for (int c = 0; c < nb; ++c) {
+    if (tid == 0 && c + 1 < nb) Bz.issue(c + 1);
+    mbar_wait(&bars[c & 1], (c >> 1) & 1);
+    const double *buf = (c & 1) ? stage1 : stage0;
+    const int j0 = c * cc, j1 = min(ncol, j0 + cc);
+    for (int j = j0 + warp; j < j1; j += nw) {
+      const double *col = buf + (int64_t)(j - j0) * ld;
+      double sacc = 0;
+      for (int k = lane; k < n; k += 32) sacc = fma(col[k], dy[k], sacc);
+      sacc = warp_sum(sacc);
+      if (lane == 0) zo[j] = sacc;
+    }
+    __syncthreads();
+  }
+  // scatter the slice: Z column P.c0 + j belongs to the segment covering it
+  for (int sg = 0; sg < nd.nseg; ++sg) {
+    const ApSeg S = segs[nd.seg0 + sg];
+    const int a = max(S.zc, P.c0), b = min(S.zc + S.w, P.c1);
+    for (int j = a + tid; j < b; j += blockDim.x) vec[S.voff + (j - S.zc)] -= zo[j - P.c0];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_apply_bwd_z(const ApNode *__restrict__ nodes, const ApPart *__restrict__ parts,
+                                                     const ApSeg *__restrict__ segs, const double *__restrict__ vec,
+                                                     double *__restrict__ upart, int chunk_doubles) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) uint64_t bars[2];
+  const ApPart P = parts[blockIdx.x];
+  const ApNode nd = nodes[P.node];
+  const int n = nd.m + nd.r, ncol = P.c1 - P.c0;
+  if (n == 0) return;
+  const int tid = threadIdx.x;
+  double *stage0 = sh, *stage1 = sh + chunk_doubles, *xt = stage1 + chunk_doubles, *u = xt + ncol;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int sg = 0; sg < nd.nseg; ++sg) {
+    const ApSeg S = segs[nd.seg0 + sg];
+    const int a = max(S.zc, P.c0), b = min(S.zc + S.w, P.c1);
+    for (int j = a + tid; j < b; j += blockDim.x) xt[j - P.c0] = vec[S.voff + (j - S.zc)];
+  }
+  for (int i = tid; i < n; i += blockDim.x) u[i] = 0.0;
+  __syncthreads();
+  const int ld = nd.ld;
+  const int cc = max(1, chunk_doubles / ld);
+  ColStream Bz{nd.F + nd.zb_off + (int64_t)P.c0 * ld, ld, ncol, cc, {stage0, stage1}, bars};
+  const int nb = ncol > 0 ? Bz.nchunks() : 0;
+  if (tid == 0 && nb > 0) Bz.issue(0);
+  for (int c = 0; c < nb; ++c) {
+    if (tid == 0 && c + 1 < nb) Bz.issue(c + 1);
+    mbar_wait(&bars[c & 1], (c >> 1) & 1);
+    const double *buf = (c & 1) ? stage1 : stage0;
+    const int j0 = c * cc, j1 = min(ncol, j0 + cc);
+    for (int i = tid; i < n; i += blockDim.x) {
+      double s0 = 0, s1 = 0;
+      int j = j0;
+      for (; j + 1 < j1; j += 2) {
+        s0 = fma(buf[(int64_t)(j - j0) * ld + i], xt[j], s0);
+        s1 = fma(buf[(int64_t)(j + 1 - j0) * ld + i], xt[j + 1], s1);
+      }
+      if (j < j1) s0 = fma(buf[(int64_t)(j - j0) * ld + i], xt[j], s0);
+      u[i] += s0 + s1;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += blockDim.x) upart[nd.upart + (int64_t)P.p * n + i] = u[i];
+}
+
+__global__ void __launch_bounds__(256) k_apply_bwd_l(const ApNode *__restrict__ nodes, const double *__restrict__ upart,
+                                                     double *__restrict__ vec) {
+  extern __shared__ __align__(16) double sh[];
+  const ApNode nd = nodes[blockIdx.x];
+  const int n = nd.m + nd.r;
+  if (n == 0) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double *u = sh;
+  for (int i = tid; i < n; i += blockDim.x) {
+    double acc = nd.y[i];
+    for (int p = 0; p < nd.nsplit; ++p) acc -= upart[nd.upart + (int64_t)p * n + i];
+    u[i] = (i < nd.m || !nd.sym) ? acc : -acc;   // D u
+  }
+  __syncthreads();
+  const double *Lb = nd.F + nd.lb_off;
+  for (int i = warp; i < nd.m; i += nw) {
+    const double *col = Lb + (int64_t)i * nd.ld;
+    double sacc = 0;
+    for (int k = i + lane; k < n; k += 32) sacc = fma(col[k], u[k], sacc);
+    sacc = warp_sum(sacc);
+    if (lane == 0) vec[nd.off_s + i] = sacc;
   }
 }
 

@@ -240,6 +240,10 @@ struct lorasp_ctx {
   std::vector<NodeRec> recs;
   // apply plan
   std::vector<int> ap_wave_begin;  // in recs order (factor order), per wave
+  std::vector<int> ap_part_begin;  // split apply: parts of wave w in [ap_part_begin[w], ap_part_begin[w+1])
+  std::vector<char> ap_wave_split; // wave uses the split kernels
+  DevBuf d_apparts, d_upart;
+  bool no_split_apply = getenv("LORASP_NO_SPLIT_APPLY") != nullptr;
   std::vector<double> ap_wave_flops, ap_wave_bytes;  // per wave, one pass (fwd or bwd)
   size_t ap_fwd_smem = 0, ap_bwd_smem = 0;
   int ap_chunk = 0;
@@ -463,6 +467,10 @@ void ensure_mem(lorasp_ctx *h) {
   CK(cudaFuncSetAttribute(k_pivot_lu_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 216 * 1024));
   CK(cudaFuncSetAttribute(k_apply_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_apply_fwd_y, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_apply_fwd_z, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_apply_bwd_z, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_apply_bwd_l, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   h->mem_ready = true;
 }
 
@@ -1754,6 +1762,49 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
     max_col = std::max(max_col, (size_t)rc.ld);
   }
   h->ap_wave_begin.push_back((int)h->recs.size());
+  // split apply: waves narrower than the GPU whose records are large get their
+  // Z columns spread over several CTAs (>= ~192 KB of Z per CTA)
+  std::vector<ApPart> parts;
+  h->ap_part_begin.assign(1, 0);
+  h->ap_wave_split.assign(h->ap_wave_begin.size() - 1, 0);
+  int64_t utot = 0;
+  for (size_t w = 0; w + 1 < h->ap_wave_begin.size(); ++w) {
+    const int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1], cnt = b1 - b0;
+    std::vector<int> ns(cnt, 1);
+    bool split = false;
+    if (!h->no_split_apply && cnt <= 64) {
+      double zmax = 0;
+      for (int q = b0; q < b1; ++q) zmax = std::max(zmax, 8.0 * (an[q].m + an[q].r) * an[q].W);
+      if (zmax >= 1024.0 * 1024) {   // a record of >= 1 MB would bound the wave's latency
+        const int cap = std::max(1, std::min(32, 444 / std::max(cnt, 1)));
+        for (int q = b0; q < b1; ++q) {
+          const double zbytes = 8.0 * (an[q].m + an[q].r) * an[q].W;
+          int k = (int)std::ceil(zbytes / (256.0 * 1024));
+          k = std::max(1, std::min({k, cap, std::max(1, an[q].W)}));
+          ns[q - b0] = k;
+          split = split || k > 1;
+        }
+      }
+    }
+    h->ap_wave_split[w] = split;
+    if (split) {
+      for (int q = b0; q < b1; ++q) {
+        const int k = ns[q - b0], n = an[q].m + an[q].r, W = an[q].W;
+        an[q].nsplit = k;
+        an[q].upart = utot;
+        utot += (int64_t)k * n;
+        for (int pp = 0; pp < k; ++pp)
+          parts.push_back(ApPart{q, (int)((int64_t)W * pp / k), (int)((int64_t)W * (pp + 1) / k), pp});
+      }
+    } else {
+      for (int q = b0; q < b1; ++q) an[q].nsplit = 1;
+    }
+    h->ap_part_begin.push_back((int)parts.size());
+  }
+  h->d_apparts.ensure(std::max<size_t>(1, parts.size()) * sizeof(ApPart), st);
+  if (!parts.empty())
+    CK(cudaMemcpy(h->d_apparts.p, parts.data(), parts.size() * sizeof(ApPart), cudaMemcpyHostToDevice));
+  h->d_upart.ensure(std::max<int64_t>(utot, 8) * 8, st);
   h->ap_wave_flops.assign(h->ap_wave_begin.size() - 1, 0.0);
   h->ap_wave_bytes.assign(h->ap_wave_begin.size() - 1, 0.0);
   for (size_t w = 0; w + 1 < h->ap_wave_begin.size(); ++w)
@@ -1794,6 +1845,29 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
   return true;
 }
 
+// One wave of Alg. 3 (fwd) or Alg. 4 (bwd): fused one-CTA-per-node kernel, or
+// the split kernels (y / L part per node + Z column slices over CTAs).
+void apply_wave(lorasp_ctx *h, int w, bool fwd, cudaStream_t s) {
+  const ApNode *nodes = h->d_apnodes.as<ApNode>();
+  const ApSeg *segs = h->d_apsegs.as<ApSeg>();
+  const int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
+  double *vec = h->d_vec.as<double>();
+  if (!h->ap_wave_split[w]) {
+    if (fwd) k_apply_fwd<<<b1 - b0, 256, h->ap_fwd_smem, s>>>(nodes + b0, segs, vec, h->ap_chunk);
+    else k_apply_bwd<<<b1 - b0, 256, h->ap_bwd_smem, s>>>(nodes + b0, segs, vec, h->ap_chunk);
+    return;
+  }
+  const ApPart *parts = h->d_apparts.as<ApPart>() + h->ap_part_begin[w];
+  const int np = h->ap_part_begin[w + 1] - h->ap_part_begin[w];
+  if (fwd) {
+    k_apply_fwd_y<<<b1 - b0, 256, h->ap_fwd_smem, s>>>(nodes + b0, vec);
+    k_apply_fwd_z<<<np, 256, h->ap_fwd_smem, s>>>(nodes, parts, segs, vec, h->ap_chunk);
+  } else {
+    k_apply_bwd_z<<<np, 256, h->ap_bwd_smem, s>>>(nodes, parts, segs, vec, h->d_upart.as<double>(), h->ap_chunk);
+    k_apply_bwd_l<<<b1 - b0, 256, h->ap_bwd_smem, s>>>(nodes + b0, h->d_upart.as<double>(), vec);
+  }
+}
+
 // x = Ã b on device buffers
 void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
   cudaStream_t st = h->stream;
@@ -1817,6 +1891,10 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
     sig.push_back((int64_t)(intptr_t)nodes);
     sig.push_back((int64_t)(intptr_t)segs);
     sig.push_back((int64_t)(intptr_t)h->d_vec.p);
+    sig.insert(sig.end(), h->ap_part_begin.begin(), h->ap_part_begin.end());
+    sig.insert(sig.end(), h->ap_wave_split.begin(), h->ap_wave_split.end());
+    sig.push_back((int64_t)(intptr_t)h->d_apparts.p);
+    sig.push_back((int64_t)(intptr_t)h->d_upart.p);
     if (h->ap_graph && sig != h->ap_graph_sig) {
       CK(cudaGraphExecDestroy(h->ap_graph));
       h->ap_graph = nullptr;
@@ -1829,14 +1907,8 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
       CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       cudaGraph_t g;
       CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      for (int w = 0; w < nw; ++w) {
-        int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
-        k_apply_fwd<<<b1 - b0, 256, h->ap_fwd_smem, cs>>>(nodes + b0, segs, h->d_vec.as<double>(), h->ap_chunk);
-      }
-      for (int w = nw - 1; w >= 0; --w) {
-        int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
-        k_apply_bwd<<<b1 - b0, 256, h->ap_bwd_smem, cs>>>(nodes + b0, segs, h->d_vec.as<double>(), h->ap_chunk);
-      }
+      for (int w = 0; w < nw; ++w) apply_wave(h, w, true, cs);
+      for (int w = nw - 1; w >= 0; --w) apply_wave(h, w, false, cs);
       const cudaError_t ce = cudaStreamEndCapture(cs, &g);
       cudaStreamDestroy(cs);
       CK(ce);
@@ -1860,15 +1932,13 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
     }
   } else {
   for (int w = 0; w < nw; ++w) {
-    int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
     ev = tbeg(h, K_APPLY_FWD);
-    k_apply_fwd<<<b1 - b0, 256, h->ap_fwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>(), h->ap_chunk);
+    apply_wave(h, w, true, st);
     tend(h, ev, h->ap_wave_flops[w], h->ap_wave_bytes[w]);
   }
   for (int w = nw - 1; w >= 0; --w) {
-    int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
     ev = tbeg(h, K_APPLY_BWD);
-    k_apply_bwd<<<b1 - b0, 256, h->ap_bwd_smem, st>>>(nodes + b0, segs, h->d_vec.as<double>(), h->ap_chunk);
+    apply_wave(h, w, false, st);
     tend(h, ev, h->ap_wave_flops[w], h->ap_wave_bytes[w]);
   }
   }
