@@ -82,7 +82,7 @@ def test_eig_zero_and_eps0(L):
     assert st == 0 and r == 90 and np.array_equal(V, np.eye(90))
 
 
-@pytest.mark.parametrize("m", [150, 300, 450])
+@pytest.mark.parametrize("m", [150, 300, 450, 560])   # 560: the generic single-CTA path (m > 512)
 def test_eig_large_rank(L, m):
     """Ranks ~0.6 m (the 3D upper levels): chunked inverse iteration, MGS and
     back-transformation of many vectors."""

@@ -257,7 +257,8 @@ def test_lu_eps0_exact(L, dims, depth):
     h.close()
 
 
-@pytest.mark.parametrize("dims,depth,eps", [((32, 32), 6, 1e-3), ((64, 64), 7, 1e-2), ((40, 24), 5, 1e-1)])
+@pytest.mark.parametrize("dims,depth,eps", [((32, 32), 6, 1e-3), ((64, 64), 7, 1e-2), ((40, 24), 5, 1e-1),
+                                             ((128, 128), 8, 1e-4)])   # fused n up to 151: unblocked LU pivot
 def test_lu_ranks_apply_gmres_parity(L, dims, depth, eps):
     p = make_problem("cfg5", dims=dims, depth=depth)
     h = L.analyze_problem(p, eps=eps, flags=0)
