@@ -85,11 +85,18 @@ int lorasp_analyze(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
  * lorasp_factor — numeric phase: Alg. 1 (P:l.265-289) on the device.
  *   values  nnz float64 in the CSR order given to analyze (host or device).
  *   Per level: MergeRedNodes (P:l.295-313); per distance-2 colour wave:
- *   Compress (P:l.319-394: batched Gram + Jacobi eigen-solver, rank
+ *   Compress (P:l.319-394: batched Gram + symmetric eigen-solver, rank
  *   sigma_k >= eps sigma_0, R_k = A_k V, five edge rules) and the fused
  *   elimination of s and b (P:l.396-399, P:l.101-106).  Re-callable with new
  *   values on the same pattern.  Returns LORASP_E_SINGULAR_PIVOT /
  *   LORASP_E_EIG_NOCONV on numerical failure.
+ *   Scheduling (results identical either way): the sweep runs on a
+ *   high-priority library stream ordered after the handle's stream and the
+ *   call returns synchronised.  The first factorization synchronises once per
+ *   compress wave (the ranks size what follows); later calls enqueue every wave
+ *   with the previous call's ranks, verify the device ranks after the sweep and
+ *   redo the synchronised sweep on a mismatch (stats: schedule_rank_predicted,
+ *   rank_prediction_hits / _misses; LORASP_NO_REPLAY=1 disables).
  */
 int lorasp_factor(lorasp_handle h, const double *values);
 
