@@ -646,6 +646,62 @@ __device__ __forceinline__ void invit_one(const double *__restrict__ d, const do
   for (int i = 0; i < m; ++i) z[i] = b[i * S] * nrm;
 }
 
+// NV simultaneous warp sums, every lane ending with all NV totals.  For NV a
+// power of two: reduce-scatter (each xor stage halves the values a lane keeps)
+// then one broadcast per value -- 2 NV + 4 - log2 NV exchanges instead of 5 NV
+// (shuffles are a shared, low-throughput resource).  Other NV: plain butterflies.
+template <int NV>
+__device__ __forceinline__ void warp_sum_multi(double (&s)[NV]) {
+  constexpr bool POW2 = NV > 1 && (NV & (NV - 1)) == 0 && NV <= 16;
+  if constexpr (!POW2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
+  } else {
+    const int lane = threadIdx.x & 31;
+    double t[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) t[v] = s[v];
+    int vidx = 0;   // index (0..NV-1) of the total this lane ends with
+#pragma unroll
+    for (int o = 16, cnt = NV; o > 0; o >>= 1) {
+      if (cnt > 1) {
+        const int half = cnt / 2;
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < NV / 2; ++i) {
+          if (i < half) {
+            const double send = up ? t[i] : t[i + half];
+            const double keep = up ? t[i + half] : t[i];
+            t[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        if (up) vidx += half;
+        cnt = half;
+      } else {
+        t[0] += __shfl_xor_sync(0xffffffffu, t[0], o);
+      }
+    }
+    // broadcast: total v lives on the lanes whose stage bits spell v
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      int src = 0;
+#pragma unroll
+      for (int o = 16, cnt = NV, rem = v; cnt > 1; o >>= 1) {
+        const int half = cnt / 2;
+        if (rem >= half) {
+          src |= o;
+          rem -= half;
+        }
+        cnt = half;
+      }
+      s[v] = __shfl_sync(0xffffffffu, t[0], src);
+    }
+    (void)vidx;
+  }
+}
+
 // Offset of reflector column j in the packed strictly-lower triangle (rows
 // j+1..m-1 stored contiguously; index with the row i > j directly).
 __device__ __forceinline__ int64_t refl_off(int j, int m) {
@@ -686,10 +742,7 @@ __device__ __forceinline__ void backtr_warp(double *V, const double *A, const do
 #pragma unroll
         for (int q = 0; q < Q; ++q) s[v] = fma(vv[q], zr[v][q], s[v]);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
+      warp_sum_multi<NV>(s);
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const double sv = s[v] * tj;
@@ -767,10 +820,7 @@ __device__ __forceinline__ void orth_backtr(double *V, const double *A, const do
 #pragma unroll
       for (int q = 0; q < Q; ++q) s[v] = fma(zk[q], z[v][q], s[v]);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
+    warp_sum_multi<NV>(s);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const int kk = warp + v * nw;
@@ -811,10 +861,7 @@ __device__ __forceinline__ void orth_backtr(double *V, const double *A, const do
 #pragma unroll
       for (int q = 0; q < Q; ++q) s[v] = fma(vv[q], z[v][q], s[v]);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
+    warp_sum_multi<NV>(s);
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const double sv = s[v] * tj;
@@ -1957,10 +2004,7 @@ __global__ void __launch_bounds__(512) k_backtr_multi(const EigTask *__restrict_
 #pragma unroll
         for (int q = 0; q < Q; ++q) s[v] = fma(vv[q], z[v][q], s[v]);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) s[v] += __shfl_xor_sync(0xffffffffu, s[v], o);
+      warp_sum_multi<NV>(s);
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         const double sv = s[v] * tj;
