@@ -405,7 +405,9 @@ static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double
   const int nch = (mmax + nb - 1) / nb;
   k_invit_multi<<<(unsigned)(n * nch), 256, SMEM_LIMIT, st>>>(dp, nch, cap);
   CK(cudaGetLastError());
-  k_orth_pre<<<(unsigned)n, 512, 0, st>>>(dp);
+  if (mmax <= 256) k_orth_pre<8><<<(unsigned)n, 256, 0, st>>>(dp);
+  else if (mmax <= 384) k_orth_pre<12><<<(unsigned)n, 256, 0, st>>>(dp);
+  else k_orth_pre<16><<<(unsigned)n, 256, 0, st>>>(dp);
   CK(cudaGetLastError());
   if (mmax <= 256) {
     const int nc = (mmax + 63) / 64;
