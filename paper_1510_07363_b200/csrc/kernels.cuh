@@ -1986,6 +1986,58 @@ __global__ void __launch_bounds__(256) k_orth_pre(const EigTask *__restrict__ ta
   }
 }
 
+// MGS of the r inverse-iteration vectors over a thread-block cluster of CL
+// CTAs: CTA c keeps vectors [c rb, (c+1) rb) in shared memory (rb = ceil(r/CL),
+// column stride m | 1).  Step k: the CTA holding z_k normalises it and writes it
+// to a global exchange slot (double-buffered, L2); one cluster barrier; every
+// CTA reads z_k and removes it from its later vectors (warps over vectors).
+// The vectors stay on chip: a single CTA streaming them through L2 each step is
+// bound by that SM's L2 bandwidth.  Dynamic shared memory: rb (m|1) + m doubles.
+template <int CL>
+__global__ void __launch_bounds__(512, 1) k_orth_cl(const EigTask *__restrict__ tasks) {
+  extern __shared__ double sh[];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const EigTask t = tasks[blockIdx.x / CL];
+  const int m = t.m, r = *t.rank_out;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int rb = (r + CL - 1) / CL, j0 = rank * rb, j1 = min(r, j0 + rb);
+  const int ldz = m | 1;
+  double *Z = sh, *zk = sh + (int64_t)rb * ldz;
+  double *xg = t.work;   // exchange: [2][m] (the work scratch is free after inverse iteration)
+  for (int j = j0 + warp; j < j1; j += nw)
+    for (int i = lane; i < m; i += 32) Z[(int64_t)(j - j0) * ldz + i] = t.V[(int64_t)j * m + i];
+  __syncthreads();
+  for (int k = 0; k < r; ++k) {
+    double *slot = xg + (int64_t)(k & 1) * m;
+    if (k >= j0 && k < j1 && warp == 0) {
+      double *zc = Z + (int64_t)(k - j0) * ldz;
+      double s2 = 0;
+      for (int i = lane; i < m; i += 32) s2 = fma(zc[i], zc[i], s2);
+      const double inv = frcp(sqrt(warp_sum(s2)));
+      for (int i = lane; i < m; i += 32) {
+        const double v = zc[i] * inv;
+        zc[i] = v;
+        slot[i] = v;
+      }
+    }
+    cl.sync();
+    for (int i = tid; i < m; i += blockDim.x) zk[i] = __ldcg(slot + i);
+    __syncthreads();
+    for (int j = max(j0, k + 1) + warp; j < j1; j += nw) {
+      double *zj = Z + (int64_t)(j - j0) * ldz;
+      double sacc = 0;
+      for (int i = lane; i < m; i += 32) sacc = fma(zk[i], zj[i], sacc);
+      sacc = warp_sum(sacc);
+      for (int i = lane; i < m; i += 32) zj[i] = fma(-sacc, zk[i], zj[i]);
+    }
+    __syncthreads();
+  }
+  for (int j = j0 + warp; j < j1; j += nw)
+    for (int i = lane; i < m; i += 32) t.V[(int64_t)j * m + i] = Z[(int64_t)(j - j0) * ldz + i];
+}
+
 // Back-transformation V = H_0 ... H_{m-3} Z for a chunk of 16 NV vectors per
 // CTA (register-resident, reflectors staged through shared memory in
 // contiguous packed segments); grid = nodes x nch.

@@ -405,9 +405,27 @@ static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double
   const int nch = (mmax + nb - 1) / nb;
   k_invit_multi<<<(unsigned)(n * nch), 256, SMEM_LIMIT, st>>>(dp, nch, cap);
   CK(cudaGetLastError());
-  if (mmax <= 256) k_orth_pre<8><<<(unsigned)n, 256, 0, st>>>(dp);
-  else if (mmax <= 384) k_orth_pre<12><<<(unsigned)n, 256, 0, st>>>(dp);
-  else k_orth_pre<16><<<(unsigned)n, 256, 0, st>>>(dp);
+  {
+    // vectors on chip over a 4- or 8-CTA cluster (all r <= m fit: (m/CL) (m|1) + m doubles)
+    const int CLn = (mmax <= 320) ? 4 : (mmax <= 448 ? 8 : 16);
+    const int rbmax = (mmax + CLn - 1) / CLn;
+    const size_t smem = ((size_t)rbmax * (mmax | 1) + mmax) * 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(n * CLn));
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CLn;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (CLn == 4) CK(cudaLaunchKernelEx(&cfg, k_orth_cl<4>, (const EigTask *)dp));
+    else if (CLn == 8) CK(cudaLaunchKernelEx(&cfg, k_orth_cl<8>, (const EigTask *)dp));
+    else CK(cudaLaunchKernelEx(&cfg, k_orth_cl<16>, (const EigTask *)dp));
+  }
   CK(cudaGetLastError());
   if (mmax <= 256) {
     const int nc = (mmax + 63) / 64;
@@ -425,6 +443,10 @@ static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double
 
 static void set_eig_attrs() {
   CK(cudaFuncSetAttribute(k_invit_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_orth_cl<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_orth_cl<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_orth_cl<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_orth_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(k_backtr_multi<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_backtr_multi<12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_backtr_multi<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
