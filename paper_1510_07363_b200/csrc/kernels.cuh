@@ -950,20 +950,29 @@ __device__ __forceinline__ int eig_values_phase(const EigTask &t, double eps, in
   gl -= 2.2e-16 * 2 * m + 2 * pivmin;
   gu += 2.2e-16 * 2 * m + 2 * pivmin;
   __syncthreads();
-  if (warp == 0) {
-    double l0 = warp_eig_asc(d, e2, m, m - 1, gl, gu, pivmin);
-    if (lane == 0) {
-      lam[0] = l0 * bnorm;
-      double thr = eps * sqrt(fmax(l0, 0.0));
-      thr = thr * thr;
-      int below = sturm_count(d, e2, m, 0.25 * thr, pivmin);
-      s_int[0] = min(m, m - below + 1);  // candidates to compute (superset of kept + 1)
+  int ncomp;
+  if (m <= 64 && 4 * m <= (int)blockDim.x) {
+    // small m: every eigenvalue at once (4 lanes each), no sequential lambda_0
+    // pass first (for larger m computing all of them costs more than it saves)
+    if (t.dbg && tid == 0) t.dbg[10] = clock64();
+    ncomp = m;
+    grp_multisect<4>(d, e2, m, 0, m, gl, gu, pivmin, lam, bnorm);
+  } else {
+    if (warp == 0) {
+      double l0 = warp_eig_asc(d, e2, m, m - 1, gl, gu, pivmin);
+      if (lane == 0) {
+        lam[0] = l0 * bnorm;
+        double thr = eps * sqrt(fmax(l0, 0.0));
+        thr = thr * thr;
+        int below = sturm_count(d, e2, m, 0.25 * thr, pivmin);
+        s_int[0] = min(m, m - below + 1);  // candidates to compute (superset of kept + 1)
+      }
     }
+    __syncthreads();
+    if (t.dbg && tid == 0) t.dbg[10] = clock64();
+    ncomp = s_int[0];
+    grp_multisect<4>(d, e2, m, 1, ncomp, gl, gu, pivmin, lam, bnorm);
   }
-  __syncthreads();
-  if (t.dbg && tid == 0) t.dbg[10] = clock64();
-  const int ncomp = s_int[0];
-  grp_multisect<4>(d, e2, m, 1, ncomp, gl, gu, pivmin, lam, bnorm);
   __syncthreads();
   // restore T (inverse iteration works on the unscaled tridiagonal)
   for (int i = tid; i < m; i += blockDim.x) d[i] *= bnorm;
