@@ -1,18 +1,28 @@
 // Device kernels of the LoRaSp level sweep (sm_100a, FP64).
 //
-//  k_leaf_scatter  CSR values -> dense leaf super-node blocks       (P:l.231, l.293)
-//  k_copy          block copies / transposes: MergeRedNodes (P:l.298-304)
-//                  and the gather of a node's fused pivot record
-//  k_gemm          batched tiled DGEMM on task lists: Gram of the
-//                  well-separated stack (Eq. lra), R_k = A_k V (P:l.356-359),
-//                  Z = L^{-1} C (elimination panel) and the Schur update
-//                  -Z_a^T D Z_b scattered into the target blocks (P:l.103-106)
-//  k_jacobi        one-sided Jacobi eigen-solver on the Gram matrix, rank by
-//                  sigma_k >= eps sigma_0 (Eq. cutOff1, P:l.580-584)
-//  k_pivot         signed Cholesky K = L D L^T of the fused (s, b) pivot,
-//                  D = diag(I_m, -I_r), and L^{-1}
-//  k_apply_fwd/bwd Alg. 3 / Alg. 4 (P:l.445-500) per colour wave
-//  Krylov helpers  CSR SpMV, deterministic dots, axpys
+//  k_leaf_scatter     CSR values -> dense leaf super-node blocks    (P:l.231, l.293)
+//  k_copy             block copies / transposes: MergeRedNodes (P:l.298-304)
+//                     and the gather of a node's fused pivot record
+//  k_gemm2 (k_gemm)   batched tiled DGEMM on task lists: Gram of the
+//                     well-separated stack (Eq. lra), R_k = A_k V (P:l.356-359),
+//                     Z = L^{-1} C (elimination panel), the Schur update
+//                     -Z_a^T D Z_b scattered into the target blocks (P:l.103-106)
+//  Compress eigen-solver (sigma_k = sqrt(lambda_k(G)), rank sigma_k >= eps sigma_0,
+//  Eq. cutOff1, P:l.580-584):
+//    k_tridiag_reg    Householder tridiagonalisation, m <= 128, G in registers
+//    k_tridiag_cl     the same over a thread-block cluster, 128 < m <= 512
+//    k_eig_t          eigenvalues (Sturm multisection), inverse iteration, MGS,
+//                     back-transformation (generic m or after the kernels above)
+//    k_invit_multi / k_orth_cl / k_backtr_multi   the same steps split over CTAs
+//                     for 128 < m <= 512 (ranks ~0.6 m there)
+//    k_jacobi         one-sided Jacobi variant (test hook only)
+//  Fused (s, b) pivot (P:l.396-399, P:l.101-106):
+//    k_pivot_blk      signed Cholesky K = L diag(I_m, -I_r) L^T + L^{-1}, n <= 160
+//    k_pivdiag        diagonal blocks of the blocked path (n > 160, with k_gemm2)
+//    k_pivot_lu_blk / k_pivot_lu   LU path (no-pivot LU, L^{-1} and U^{-T})
+//  k_apply_fwd/bwd    Alg. 3 / Alg. 4 (P:l.445-500) per colour wave (+ the split
+//                     k_apply_fwd_y/_z, k_apply_bwd_z/_l for few large records)
+//  Krylov helpers     CSR SpMV, deterministic dots, axpys
 #pragma once
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
