@@ -31,6 +31,15 @@
 
 namespace lorasp {
 
+// Programmatic dependent launch (the factor sweep's kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): every such kernel lets
+// its successor be scheduled at once and waits for its predecessor's memory
+// before touching anything.  Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- copies ----
 struct CopyTask {
   const double *src;
@@ -43,6 +52,7 @@ struct CopyTask {
 };
 
 __global__ void __launch_bounds__(256) k_copy(const CopyTask *__restrict__ tasks) {
+  pdl_enter();
   const CopyTask t = tasks[blockIdx.x];
   if (t.rows <= 0 || t.cols <= 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -307,6 +317,7 @@ __global__ void __launch_bounds__(128, 4) k_gemm2(const GemmTask *__restrict__ t
                                                 const GemmSeg *__restrict__ segs) {
   __shared__ __align__(16) double As[2][G2K][GT + 1];
   __shared__ __align__(16) double Bs[2][G2K][GT + 1];
+  pdl_enter();
   const GemmTask t = tasks[blockIdx.x];
   if (t.tnw == 32) gemm2_tile<4>(t, segs, As, Bs);
   else gemm2_tile<8>(t, segs, As, Bs);
@@ -1024,6 +1035,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
   }
   __shared__ double s_red[32];
   __shared__ double d[MR + 8], e[MR + 8], tau[MR + 8];
+  pdl_enter();
   const EigTask t = tasks[blockIdx.x];
   const int m = t.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1529,6 +1541,7 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
   __shared__ double s_red[32];
   __shared__ double s_bc[8];
   __shared__ int s_int[4];
+  pdl_enter();
   const EigTask t = tasks[blockIdx.x];
   const int m = t.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -2356,6 +2369,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
   extern __shared__ double sh[];
   __shared__ double W[PIVB_NB * PIVB_NB];
   __shared__ int s_fail;
+  pdl_enter();
   const PivTask t = tasks[blockIdx.x];
   const int n = t.m + t.r;
   if (n == 0) return;
@@ -2526,6 +2540,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
   __shared__ double WL[PIVB_NB * PIVB_NB], WU[PIVB_NB * PIVB_NB];
   __shared__ int s_fail;
   __shared__ double s_amax[16];
+  pdl_enter();
   const PivTask t = tasks[blockIdx.x];
   const int n = t.m + t.r;
   if (n == 0) return;
@@ -2700,6 +2715,7 @@ __global__ void __launch_bounds__(256) k_pivdiag(const PivDiagTask *__restrict__
   __shared__ double A[64 * 65];
   __shared__ double tmp[64];
   __shared__ int s_fail;
+  pdl_enter();
   const PivDiagTask t = tasks[blockIdx.x];
   const int b = t.b, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int la = 65;

@@ -48,6 +48,27 @@ struct Err {
   Err(int c, std::string m) : code(c), msg(std::move(m)) {}
 };
 
+// Sweep kernels go out with programmatic dependent launch: the next kernel's
+// CTAs are scheduled while the current one drains and block in pdl_enter()
+// until its memory is visible (hides the ~launch gap between the ~400
+// dependent launches of a factorization).  LORASP_NO_PDL: plain launches.
+static const bool g_pdl = getenv("LORASP_NO_PDL") == nullptr;
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 static const int SMEM_LIMIT = 226 * 1024;  // dynamic; leaves room for static smem
 static const int EIG_REG_MIN = 3;
 static const size_t EIG_REG_SMEM = 200 * 1024;
@@ -382,12 +403,12 @@ static void launch_tridiag_cl(cudaStream_t st, const EigTask *dt, int n, int cls
 // Register-tile eigen path for m <= 128: tridiagonalisation (tile class c:
 // 32 / 64 / 128 rows) then k_eig_t<true>.
 static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps, int *dstatus) {
-  if (c == 0) k_tridiag_reg<false, 1, 4, 8><<<(unsigned)n, 128, 0, st>>>(ds, eps, nullptr);
-  else if (c == 1) k_tridiag_reg<false, 2, 8, 8><<<(unsigned)n, 256, 0, st>>>(ds, eps, nullptr);
-  else k_tridiag_reg<false><<<(unsigned)n, EIG_REG_THREADS, 0, st>>>(ds, eps, nullptr);
+  if (c == 0) launch_k(k_tridiag_reg<false, 1, 4, 8>, (unsigned)n, 128, 0, st, ds, eps, (long long *)nullptr);
+  else if (c == 1) launch_k(k_tridiag_reg<false, 2, 8, 8>, (unsigned)n, 256, 0, st, ds, eps, (long long *)nullptr);
+  else launch_k(k_tridiag_reg<false>, (unsigned)n, EIG_REG_THREADS, 0, st, ds, eps, (long long *)nullptr);
   CK(cudaGetLastError());
-  k_eig_t<true><<<(unsigned)n, c == 2 ? EIG_REG_THREADS : 256, EIG_REG_SMEM, st>>>(ds, eps, (int)(EIG_REG_SMEM / 8),
-                                                                                   dstatus);
+  launch_k(k_eig_t<true>, (unsigned)n, c == 2 ? EIG_REG_THREADS : 256, EIG_REG_SMEM, st, ds, eps,
+           (int)(EIG_REG_SMEM / 8), dstatus);
   CK(cudaGetLastError());
   return 2;
 }
@@ -517,7 +538,7 @@ void launch_gemm_dev(lorasp_ctx *h, const GemmTask *dt, const GemmSeg *ds, size_
   if (ntasks == 0) return;
   int ev = cls >= 0 ? tbeg(h, cls) : -1;
   if (h->gemm_v1) k_gemm<<<(unsigned)ntasks, 256, 0, h->stream>>>(dt, ds);
-  else k_gemm2<<<(unsigned)ntasks, 128, 0, h->stream>>>(dt, ds);
+  else launch_k(k_gemm2, (unsigned)ntasks, 128, 0, h->stream, dt, ds);
   tend(h, ev, flops, bytes);
   ++h->launches_factor;
   CK(cudaGetLastError());
@@ -527,7 +548,7 @@ void launch_copy_dev(lorasp_ctx *h, const CopyTask *dt, const std::vector<CopyTa
   double bytes = 0;
   for (const CopyTask &t : tasks) bytes += (t.mode == 0 ? 16.0 : 8.0) * t.rows * t.cols;
   int ev = cls >= 0 ? tbeg(h, cls) : -1;
-  k_copy<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt);
+  launch_k(k_copy, (unsigned)tasks.size(), 256, 0, h->stream, dt);
   tend(h, ev, 0, bytes);
   ++h->launches_factor;
   CK(cudaGetLastError());
@@ -541,7 +562,7 @@ void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::v
   GemmTask *dt = push(h, tasks);
   int ev = cls >= 0 ? tbeg(h, cls) : -1;
   if (h->gemm_v1) k_gemm<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt, ds);
-  else k_gemm2<<<(unsigned)tasks.size(), 128, 0, h->stream>>>(dt, ds);
+  else launch_k(k_gemm2, (unsigned)tasks.size(), 128, 0, h->stream, dt, ds);
   tend(h, ev, flops, bytes);
   ++h->launches_factor;
   CK(cudaGetLastError());
@@ -606,7 +627,7 @@ void launch_copy(lorasp_ctx *h, const std::vector<CopyTask> &tasks, int cls) {
   double bytes = 0;
   for (const CopyTask &t : tasks) bytes += (t.mode == 0 ? 16.0 : 8.0) * t.rows * t.cols;
   int ev = cls >= 0 ? tbeg(h, cls) : -1;
-  k_copy<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt);
+  launch_k(k_copy, (unsigned)tasks.size(), 256, 0, h->stream, dt);
   tend(h, ev, 0, bytes);
   ++h->launches_factor;
   CK(cudaGetLastError());
@@ -669,7 +690,7 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
     PivTask *dp = push(h, small);
     if (max_n <= PIVB_MAXN && !h->pivot_unblocked) {
       const size_t sm = (size_t)(max_n | 1) * max_n * 8;
-      k_pivot_blk<<<(unsigned)small.size(), 512, sm, st>>>(dp, h->d_status.as<int>());
+      launch_k(k_pivot_blk, (unsigned)small.size(), 512, sm, st, dp, h->d_status.as<int>());
     } else {
       int64_t want = (int64_t)max_n * max_n + max_n;
       int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
@@ -758,7 +779,7 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
       }
       if (!dt.empty()) {
         PivDiagTask *dd = push(h, dt);
-        k_pivdiag<<<(unsigned)dt.size(), 256, 0, st>>>(dd, h->d_status.as<int>());
+        launch_k(k_pivdiag, (unsigned)dt.size(), 256, 0, st, dd, h->d_status.as<int>());
         ++h->launches_factor;
         CK(cudaGetLastError());
       }
@@ -833,7 +854,7 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
   int ev = tbeg(h, K_PIVOT);
   if (max_n <= PIVLU_MAXN && !h->pivot_unblocked) {
     const size_t sm = ((size_t)(max_n | 1) * max_n + 2 * (size_t)max_n * PIVB_NB) * 8;
-    k_pivot_lu_blk<<<(unsigned)pv.size(), 512, sm, h->stream>>>(dp, h->d_status.as<int>());
+    launch_k(k_pivot_lu_blk, (unsigned)pv.size(), 512, sm, h->stream, dp, h->d_status.as<int>());
   } else {
     int64_t want = (int64_t)max_n * max_n + max_n;
     int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
@@ -1040,9 +1061,9 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
         CK(cudaMemcpyAsync(h->d_sp.p, hb, nbytes, cudaMemcpyHostToDevice, h->stream2));
         const CopyTask *dct = h->d_sp.as<CopyTask>();
         const PivTask *dpt = reinterpret_cast<const PivTask *>(h->d_sp.as<char>() + s_ct.size() * sizeof(CopyTask));
-        k_copy<<<(unsigned)s_ct.size(), 256, 0, h->stream2>>>(dct);
+        launch_k(k_copy, (unsigned)s_ct.size(), 256, 0, h->stream2, dct);
         const size_t smem = (size_t)(s_max | 1) * s_max * 8;
-        k_pivot_blk<<<(unsigned)s_pt.size(), 512, smem, h->stream2>>>(dpt, h->d_status.as<int>());
+        launch_k(k_pivot_blk, (unsigned)s_pt.size(), 512, smem, h->stream2, dpt, h->d_status.as<int>());
         h->launches_factor += 2;
         CK(cudaGetLastError());
         CK(cudaEventRecord(h->ev_s1, h->stream2));
