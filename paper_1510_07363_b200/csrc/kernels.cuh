@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(256) k_copy(const CopyTask *__restrict__ tasks
 
 __global__ void k_leaf_scatter(const double *__restrict__ vals, const int64_t *__restrict__ dest,
                                int64_t nnz, double *__restrict__ base) {
+  pdl_enter();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
        k += (int64_t)gridDim.x * blockDim.x) {
     int64_t d = dest[k];
@@ -1924,6 +1925,7 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
 // CTA per chunk of vectors (chunk c: k in [c nb, (c+1) nb) ∩ [0, r)), each
 // chunk's LU / right-hand sides in shared memory; grid = nodes x nch.
 __global__ void __launch_bounds__(256) k_invit_multi(const EigTask *__restrict__ tasks, int nch, int smem_cap_doubles) {
+  pdl_enter();
   extern __shared__ double sh[];
   const EigTask t = tasks[blockIdx.x / nch];
   const int c = blockIdx.x % nch;
@@ -2075,6 +2077,7 @@ __global__ void __launch_bounds__(512, 1) k_orth_cl(const EigTask *__restrict__ 
 // contiguous packed segments); grid = nodes x nch.
 template <int Q, int NV>
 __global__ void __launch_bounds__(512) k_backtr_multi(const EigTask *__restrict__ tasks, int nch, int smem_cap_doubles) {
+  pdl_enter();
   extern __shared__ double sh[];
   const EigTask t = tasks[blockIdx.x / nch];
   const int c = blockIdx.x % nch;
@@ -2158,6 +2161,7 @@ struct PivTask {
 
 __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks,
                                                int smem_cap_doubles, int *status) {
+  pdl_enter();
   extern __shared__ double sh[];
   const PivTask t = tasks[blockIdx.x];
   const int n = t.m + t.r;
@@ -2236,6 +2240,7 @@ __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks
 // in region 0 (global).
 __global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ tasks, int smem_cap_doubles,
                                                   int *status) {
+  pdl_enter();
   extern __shared__ double sh[];
   const PivTask t = tasks[blockIdx.x];
   const int n = t.m + t.r;
@@ -2852,6 +2857,7 @@ struct ColStream {
 __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ nodes,
                                                    const ApSeg *__restrict__ segs,
                                                    double *__restrict__ vec, int chunk_doubles) {
+  pdl_enter();
   extern __shared__ __align__(16) double sh[];
   __shared__ __align__(8) uint64_t bars[2];
   const ApNode nd = nodes[blockIdx.x];
@@ -2938,6 +2944,7 @@ __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ no
 __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ nodes,
                                                    const ApSeg *__restrict__ segs,
                                                    double *__restrict__ vec, int chunk_doubles) {
+  pdl_enter();
   extern __shared__ __align__(16) double sh[];
   __shared__ __align__(8) uint64_t bars[2];
   const ApNode nd = nodes[blockIdx.x];
@@ -3025,6 +3032,7 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
 // (partial Z x_T per slice into scratch) then k_apply_bwd_l (u = y - sum of
 // the partials in slice order, D u, x_s = L^{-T} u): deterministic.
 __global__ void __launch_bounds__(256) k_apply_fwd_y(const ApNode *__restrict__ nodes, double *__restrict__ vec) {
+  pdl_enter();
   extern __shared__ __align__(16) double sh[];
   const ApNode nd = nodes[blockIdx.x];
   const int n = nd.m + nd.r;
@@ -3048,6 +3056,7 @@ __global__ void __launch_bounds__(256) k_apply_fwd_y(const ApNode *__restrict__ 
 __global__ void __launch_bounds__(256) k_apply_fwd_z(const ApNode *__restrict__ nodes, const ApPart *__restrict__ parts,
                                                      const ApSeg *__restrict__ segs, double *__restrict__ vec,
                                                      int chunk_doubles) {
+  pdl_enter();
   extern __shared__ __align__(16) double sh[];
   __shared__ __align__(8) uint64_t bars[2];
   const ApPart P = parts[blockIdx.x];
@@ -3096,6 +3105,7 @@ __global__ void __launch_bounds__(256) k_apply_fwd_z(const ApNode *__restrict__ 
 __global__ void __launch_bounds__(256) k_apply_bwd_z(const ApNode *__restrict__ nodes, const ApPart *__restrict__ parts,
                                                      const ApSeg *__restrict__ segs, const double *__restrict__ vec,
                                                      double *__restrict__ upart, int chunk_doubles) {
+  pdl_enter();
   extern __shared__ __align__(16) double sh[];
   __shared__ __align__(8) uint64_t bars[2];
   const ApPart P = parts[blockIdx.x];
@@ -3143,6 +3153,7 @@ __global__ void __launch_bounds__(256) k_apply_bwd_z(const ApNode *__restrict__ 
 
 __global__ void __launch_bounds__(256) k_apply_bwd_l(const ApNode *__restrict__ nodes, const double *__restrict__ upart,
                                                      double *__restrict__ vec) {
+  pdl_enter();
   extern __shared__ __align__(16) double sh[];
   const ApNode nd = nodes[blockIdx.x];
   const int n = nd.m + nd.r;
@@ -3167,12 +3178,14 @@ __global__ void __launch_bounds__(256) k_apply_bwd_l(const ApNode *__restrict__ 
 
 __global__ void k_set_rhs(const double *__restrict__ b, const int64_t *__restrict__ perm, int64_t n,
                           double *__restrict__ vec) {
+  pdl_enter();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x)
     vec[perm[q]] = b[q];
 }
 __global__ void k_get_x(const double *__restrict__ vec, const int64_t *__restrict__ perm, int64_t n,
                         double *__restrict__ x) {
+  pdl_enter();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x)
     x[q] = vec[perm[q]];
@@ -3182,6 +3195,7 @@ __global__ void k_get_x(const double *__restrict__ vec, const int64_t *__restric
 __global__ void k_spmv(int64_t n, const int64_t *__restrict__ rp, const int64_t *__restrict__ ci,
                        const double *__restrict__ va, const double *__restrict__ x,
                        double *__restrict__ y) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0;
@@ -3195,6 +3209,7 @@ constexpr int DOT_BLOCKS = 296;
 __global__ void __launch_bounds__(256) k_dot_partial(int64_t n, const double *__restrict__ a,
                                                      const double *__restrict__ b,
                                                      double *__restrict__ part) {
+  pdl_enter();
   __shared__ double red[8];
   double s = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -3210,6 +3225,7 @@ __global__ void __launch_bounds__(256) k_dot_partial(int64_t n, const double *__
   }
 }
 __global__ void k_dot_final(const double *__restrict__ part, int np, double *__restrict__ out) {
+  pdl_enter();
   __shared__ double red[8];
   double s = 0;
   for (int i = threadIdx.x; i < np; i += blockDim.x) s += part[i];
@@ -3225,6 +3241,7 @@ __global__ void k_dot_final(const double *__restrict__ part, int np, double *__r
 // y = a*x + b*y
 __global__ void k_axpby(int64_t n, double a, const double *__restrict__ x, double b,
                         double *__restrict__ y) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = a * x[i] + b * y[i];
@@ -3232,6 +3249,7 @@ __global__ void k_axpby(int64_t n, double a, const double *__restrict__ x, doubl
 // z = x - y
 __global__ void k_sub(int64_t n, const double *__restrict__ x, const double *__restrict__ y,
                       double *__restrict__ z) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     z[i] = x[i] - y[i];

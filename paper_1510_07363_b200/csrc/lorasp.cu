@@ -54,10 +54,10 @@ struct Err {
 // dependent launches of a factorization).  LORASP_NO_PDL: plain launches.
 static const bool g_pdl = getenv("LORASP_NO_PDL") == nullptr;
 template <typename... KArgs, typename... Args>
-static void launch_k(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+static void launch_k(void (*kern)(KArgs...), dim3 grid, unsigned block, size_t smem, cudaStream_t st,
                      Args... args) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = grid;
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -416,7 +416,7 @@ static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps
 // After k_tridiag_cl: eigenvalues + rank (k_eig_t<false, true>), chunked
 // inverse iteration, MGS, chunked back-transformation.  Returns the launches.
 static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double eps, int *dstatus) {
-  k_eig_t<false, true><<<(unsigned)n, EIG_REG_THREADS, SMEM_LIMIT, st>>>(dp, eps, SMEM_LIMIT / 8, dstatus);
+  launch_k(k_eig_t<false, true>, (unsigned)n, EIG_REG_THREADS, SMEM_LIMIT, st, dp, eps, SMEM_LIMIT / 8, dstatus);
   CK(cudaGetLastError());
   if (eps == 0.0) return 1;   // V = I already written
   const int cap = SMEM_LIMIT / 8;
@@ -424,7 +424,7 @@ static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double
   const int mp = (mmax + 8) & ~7;
   const int nb = (int)std::min<int64_t>(256, (cap - 2 * mp) / per);
   const int nch = (mmax + nb - 1) / nb;
-  k_invit_multi<<<(unsigned)(n * nch), 256, SMEM_LIMIT, st>>>(dp, nch, cap);
+  launch_k(k_invit_multi, (unsigned)(n * nch), 256, SMEM_LIMIT, st, dp, nch, cap);
   CK(cudaGetLastError());
   {
     // vectors on chip over a 4- or 8-CTA cluster (all r <= m fit: (m/CL) (m|1) + m doubles)
@@ -450,13 +450,13 @@ static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double
   CK(cudaGetLastError());
   if (mmax <= 256) {
     const int nc = (mmax + 63) / 64;
-    k_backtr_multi<8, 4><<<(unsigned)(n * nc), 512, SMEM_LIMIT, st>>>(dp, nc, cap);
+    launch_k(k_backtr_multi<8, 4>, (unsigned)(n * nc), 512, SMEM_LIMIT, st, dp, nc, cap);
   } else if (mmax <= 384) {
     const int nc = (mmax + 47) / 48;
-    k_backtr_multi<12, 3><<<(unsigned)(n * nc), 512, SMEM_LIMIT, st>>>(dp, nc, cap);
+    launch_k(k_backtr_multi<12, 3>, (unsigned)(n * nc), 512, SMEM_LIMIT, st, dp, nc, cap);
   } else {
     const int nc = (mmax + 31) / 32;
-    k_backtr_multi<16, 2><<<(unsigned)(n * nc), 512, SMEM_LIMIT, st>>>(dp, nc, cap);
+    launch_k(k_backtr_multi<16, 2>, (unsigned)(n * nc), 512, SMEM_LIMIT, st, dp, nc, cap);
   }
   CK(cudaGetLastError());
   return 4;
@@ -612,7 +612,7 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
     EigTask *db = single ? de : push(h, big);
     int mb = 0;
     for (auto &e : big) mb = std::max(mb, e.m);
-    k_eig_t<false><<<(unsigned)big.size(), EIG_THREADS, (size_t)eig_generic_cap(mb) * 8, h->stream>>>(
+    launch_k(k_eig_t<false>, (unsigned)big.size(), EIG_THREADS, (size_t)eig_generic_cap(mb) * 8, h->stream, 
         db, h->plan.eps, eig_generic_cap(mb), h->d_status.as<int>());
     ++h->launches_factor;
     CK(cudaGetLastError());
@@ -695,7 +695,7 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
       int64_t want = (int64_t)max_n * max_n + max_n;
       int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
       cap = std::max(cap, max_n);
-      k_pivot<<<(unsigned)small.size(), 512, cap * 8, st>>>(dp, cap, h->d_status.as<int>());
+      launch_k(k_pivot, (unsigned)small.size(), 512, cap * 8, st, dp, cap, h->d_status.as<int>());
     }
     ++h->launches_factor;
     CK(cudaGetLastError());
@@ -859,7 +859,7 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
     int64_t want = (int64_t)max_n * max_n + max_n;
     int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
     cap = std::max(cap, max_n);
-    k_pivot_lu<<<(unsigned)pv.size(), 512, cap * 8, h->stream>>>(dp, cap, h->d_status.as<int>());
+    launch_k(k_pivot_lu, (unsigned)pv.size(), 512, cap * 8, h->stream, dp, cap, h->d_status.as<int>());
   }
   tend(h, ev, f_piv, b_piv);
   ++h->launches_factor;
@@ -953,7 +953,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
         h->dest_ready = true;
       }
       int ev = tbeg(h, K_SCATTER);
-      k_leaf_scatter<<<grid1(pl.nnz), 256, 0, st>>>(h->d_values.as<double>(), h->d_dest.as<int64_t>(),
+      launch_k(k_leaf_scatter, grid1(pl.nnz), 256, 0, st, h->d_values.as<double>(), h->d_dest.as<int64_t>(),
                                                     pl.nnz, base);
       tend(h, ev, 0, 24.0 * pl.nnz);
       ++h->launches_factor;
@@ -1898,18 +1898,18 @@ void apply_wave(lorasp_ctx *h, int w, bool fwd, cudaStream_t s) {
   const int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
   double *vec = h->d_vec.as<double>();
   if (!h->ap_wave_split[w]) {
-    if (fwd) k_apply_fwd<<<b1 - b0, 256, h->ap_fwd_smem, s>>>(nodes + b0, segs, vec, h->ap_chunk);
-    else k_apply_bwd<<<b1 - b0, 256, h->ap_bwd_smem, s>>>(nodes + b0, segs, vec, h->ap_chunk);
+    if (fwd) launch_k(k_apply_fwd, b1 - b0, 256, h->ap_fwd_smem, s, nodes + b0, segs, vec, h->ap_chunk);
+    else launch_k(k_apply_bwd, b1 - b0, 256, h->ap_bwd_smem, s, nodes + b0, segs, vec, h->ap_chunk);
     return;
   }
   const ApPart *parts = h->d_apparts.as<ApPart>() + h->ap_part_begin[w];
   const int np = h->ap_part_begin[w + 1] - h->ap_part_begin[w];
   if (fwd) {
-    k_apply_fwd_y<<<b1 - b0, 256, h->ap_fwd_smem, s>>>(nodes + b0, vec);
-    k_apply_fwd_z<<<np, 256, h->ap_fwd_smem, s>>>(nodes, parts, segs, vec, h->ap_chunk);
+    launch_k(k_apply_fwd_y, b1 - b0, 256, h->ap_fwd_smem, s, nodes + b0, vec);
+    launch_k(k_apply_fwd_z, np, 256, h->ap_fwd_smem, s, nodes, parts, segs, vec, h->ap_chunk);
   } else {
-    k_apply_bwd_z<<<np, 256, h->ap_bwd_smem, s>>>(nodes, parts, segs, vec, h->d_upart.as<double>(), h->ap_chunk);
-    k_apply_bwd_l<<<b1 - b0, 256, h->ap_bwd_smem, s>>>(nodes + b0, h->d_upart.as<double>(), vec);
+    launch_k(k_apply_bwd_z, np, 256, h->ap_bwd_smem, s, nodes, parts, segs, vec, h->d_upart.as<double>(), h->ap_chunk);
+    launch_k(k_apply_bwd_l, b1 - b0, 256, h->ap_bwd_smem, s, nodes + b0, h->d_upart.as<double>(), vec);
   }
 }
 
@@ -1919,7 +1919,7 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
   const Plan &pl = h->plan;
   CK(cudaMemsetAsync(h->d_vec.p, 0, h->vec_len * 8, st));
   int ev = tbeg(h, K_VEC);
-  k_set_rhs<<<grid1(pl.n), 256, 0, st>>>(b, h->d_perm.as<int64_t>(), pl.n, h->d_vec.as<double>());
+  launch_k(k_set_rhs, grid1(pl.n), 256, 0, st, b, h->d_perm.as<int64_t>(), pl.n, h->d_vec.as<double>());
   tend(h, ev, 0, 24.0 * pl.n);
   const ApNode *nodes = h->d_apnodes.as<ApNode>();
   const ApSeg *segs = h->d_apsegs.as<ApSeg>();
@@ -1988,7 +1988,7 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
   }
   }
   ev = tbeg(h, K_VEC);
-  k_get_x<<<grid1(pl.n), 256, 0, st>>>(h->d_vec.as<double>(), h->d_perm.as<int64_t>(), pl.n, x);
+  launch_k(k_get_x, grid1(pl.n), 256, 0, st, h->d_vec.as<double>(), h->d_perm.as<int64_t>(), pl.n, x);
   tend(h, ev, 0, 24.0 * pl.n);
   *counter += 2 * nw + 2;
   CK(cudaGetLastError());
@@ -1997,8 +1997,8 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
 double dot_dev(lorasp_ctx *h, const double *a, const double *b) {
   cudaStream_t st = h->stream;
   int ev = tbeg(h, K_DOT);
-  k_dot_partial<<<DOT_BLOCKS, 256, 0, st>>>(h->plan.n, a, b, h->d_dotpart.as<double>());
-  k_dot_final<<<1, 256, 0, st>>>(h->d_dotpart.as<double>(), DOT_BLOCKS,
+  launch_k(k_dot_partial, DOT_BLOCKS, 256, 0, st, h->plan.n, a, b, h->d_dotpart.as<double>());
+  launch_k(k_dot_final, 1, 256, 0, st, h->d_dotpart.as<double>(), DOT_BLOCKS,
                                  h->d_dotpart.as<double>() + DOT_BLOCKS);
   tend(h, ev, 2.0 * h->plan.n, 16.0 * h->plan.n);
   CK(cudaMemcpyAsync(h->h_dot, h->d_dotpart.as<double>() + DOT_BLOCKS, 8, cudaMemcpyDeviceToHost, st));
@@ -2010,7 +2010,7 @@ double dot_dev(lorasp_ctx *h, const double *a, const double *b) {
 void spmv_dev(lorasp_ctx *h, const double *x, double *y) {
   const Plan &pl = h->plan;
   int ev = tbeg(h, K_SPMV);
-  k_spmv<<<grid1(pl.n), 256, 0, h->stream>>>(pl.n, h->d_rowptr.as<int64_t>(), h->d_colidx.as<int64_t>(),
+  launch_k(k_spmv, grid1(pl.n), 256, 0, h->stream, pl.n, h->d_rowptr.as<int64_t>(), h->d_colidx.as<int64_t>(),
                                             h->d_values.as<double>(), x, y);
   tend(h, ev, 2.0 * pl.nnz, 20.0 * pl.nnz + 16.0 * pl.n);
   ++h->launches_krylov;
@@ -2018,7 +2018,7 @@ void spmv_dev(lorasp_ctx *h, const double *x, double *y) {
 
 void axpby(lorasp_ctx *h, double a, const double *x, double b, double *y) {
   int ev = tbeg(h, K_VEC);
-  k_axpby<<<grid1(h->plan.n), 256, 0, h->stream>>>(h->plan.n, a, x, b, y);
+  launch_k(k_axpby, grid1(h->plan.n), 256, 0, h->stream, h->plan.n, a, x, b, y);
   tend(h, ev, 3.0 * h->plan.n, 24.0 * h->plan.n);
   ++h->launches_krylov;
 }
@@ -2065,7 +2065,7 @@ int pcg_dev(lorasp_ctx *h, const double *b, double *x, double tol, int maxit, in
   if (it > maxit) it = maxit;
   // true residual
   spmv_dev(h, x, q);
-  k_sub<<<grid1(n), 256, 0, st>>>(n, b, q, r);
+  launch_k(k_sub, grid1(n), 256, 0, st, n, b, q, r);
   ++h->launches_krylov;
   double rr = std::sqrt(dot_dev(h, r, r)) / nb;
   if (iters) *iters = it;
@@ -2095,7 +2095,7 @@ int gmres_dev(lorasp_ctx *h, const double *b, double *x, double tol, int restart
   std::vector<double> H((restart + 1) * restart), cs(restart), sn(restart), g(restart + 1);
   while (it < maxit && !conv) {
     spmv_dev(h, x, w);
-    k_sub<<<grid1(n), 256, 0, st>>>(n, b, w, r);
+    launch_k(k_sub, grid1(n), 256, 0, st, n, b, w, r);
     ++h->launches_krylov;
     double beta = std::sqrt(dot_dev(h, r, r));
     if (beta / nb <= tol) {
@@ -2149,7 +2149,7 @@ int gmres_dev(lorasp_ctx *h, const double *b, double *x, double tol, int restart
     for (int j = 0; j < k_used; ++j) axpby(h, y[j], Zb + (int64_t)j * n, 1.0, x);
   }
   spmv_dev(h, x, w);
-  k_sub<<<grid1(n), 256, 0, st>>>(n, b, w, r);
+  launch_k(k_sub, grid1(n), 256, 0, st, n, b, w, r);
   ++h->launches_krylov;
   double rr = std::sqrt(dot_dev(h, r, r)) / nb;
   if (iters) *iters = it;
