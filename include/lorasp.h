@@ -126,6 +126,44 @@ int lorasp_krylov_ex(lorasp_handle h, const double *b, double *x, double tol,
 /* Use an existing cudaStream_t (passed as void*) for all device work; NULL = default. */
 int lorasp_set_stream(lorasp_handle h, void *cuda_stream);
 
+/*
+ * Distributed factorization over `world` ranks (one process / handle per GPU),
+ * the subtree partition of SURVEY 8(e) (P:l.55: the tree's subtrees are
+ * independent up to the separator couplings, P:l.843: distributed memory).
+ *   world   power of two with 2^(depth-1) >= world; rank in [0, world).
+ *   Owner of level-i super-node c (and of its black node): c >> (i - 1 - log2
+ *   world) when i - 1 >= log2 world (the subtree of level-(log2 world + 1)
+ *   node g belongs to rank g), else rank 0 (the top levels).
+ *   Every rank runs the same host schedule (identical plan, ranks and record
+ *   layout) and launches only the tasks of the nodes it owns.  Two exchange
+ *   points per colour wave go through `fn`:
+ *     after Compress, the ranks of the wave's nodes (and the status flags):
+ *       LORASP_COLL_MAXINT — elementwise max over ranks of the first nbytes/4
+ *       int32 of the send buffer, in place (non-owned entries are 0);
+ *     after the Schur updates, every block and factor record the rank wrote
+ *     (packed in a fixed order every rank can recompute):
+ *       LORASP_COLL_ALLGATHER — rank q's send[0, nbytes) lands in every rank's
+ *       recv[q * nbytes, (q + 1) * nbytes).
+ *   LORASP_COLL_RESERVE asks for send >= nbytes and recv >= world * nbytes
+ *   bytes of device memory; the callback registers them with
+ *   lorasp_set_dist_buffers before returning.  The engine synchronises its
+ *   stream before every call; the callback returns with the transfer complete
+ *   (0 = OK, anything else aborts the factorization with LORASP_E_CUDA).
+ *   Distance-2 colouring makes the blocks written in one wave disjoint across
+ *   nodes, so every rank ends the factorization with the G = 1 store, bit for
+ *   bit; lorasp_apply / lorasp_krylov_ex then run replicated on every rank.
+ *   Rank-predicted replay and split pivots are off in this mode.
+ *   world = 1 (or fn = NULL) switches back to the single-GPU sweep.
+ */
+typedef enum { LORASP_COLL_ALLGATHER = 0, LORASP_COLL_MAXINT = 1, LORASP_COLL_RESERVE = 2 } lorasp_coll_kind;
+typedef int (*lorasp_coll_fn)(void *user, int kind, int64_t nbytes);
+int lorasp_set_dist(lorasp_handle h, int rank, int world, lorasp_coll_fn fn, void *user);
+/* Device buffers (owned by the caller) for the exchanges; capacity in bytes
+ * (send_cap >= the reserve request, recv_cap >= world times it). */
+int lorasp_set_dist_buffers(lorasp_handle h, void *send, int64_t send_cap, void *recv, int64_t recv_cap);
+/* Owner rank of level-`level` super-node c under the partition above (host only). */
+int lorasp_dist_owner(int level, int c, int world);
+
 /* Structure queries (valid after analyze): depth l and, for level i (1..l),
  * the number of clusters 2^(i-1) and the processing order of those clusters
  * (order[k] = cluster processed k-th) and its colour waves (wave[c]). */

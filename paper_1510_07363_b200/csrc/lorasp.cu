@@ -311,6 +311,15 @@ struct lorasp_ctx {
   std::vector<cudaEvent_t> evpool;
   std::vector<TimedEv> pend;
   KStat kst[K_NCLASS];
+  // distributed factorization (lorasp_set_dist): subtree owner-computes with
+  // per-wave exchanges through the caller's collective callback
+  int dist_rank = 0, dist_world = 1, dist_l0 = 0;
+  lorasp_coll_fn dist_fn = nullptr;
+  void *dist_user = nullptr;
+  void *dist_send = nullptr, *dist_recv = nullptr;
+  int64_t dist_send_cap = 0, dist_recv_cap = 0;
+  int64_t dist_bytes = 0, dist_calls = 0;
+  int piv_maxn_hint = 0;   // batch-independent pivot path choice (max n of the whole wave)
 };
 
 namespace {
@@ -685,6 +694,7 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
       big.push_back(t);
     }
   }
+  if (!small.empty() && h->piv_maxn_hint > max_n) max_n = std::min(h->piv_maxn_hint, PIV_SMALL_N);
   int ev = tbeg(h, K_PIVOT);
   if (!small.empty()) {
     PivTask *dp = push(h, small);
@@ -850,6 +860,7 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
   if (pv.empty()) return;
   int max_n = 0;
   for (const PivTask &t : pv) max_n = std::max(max_n, t.m + t.r);
+  max_n = std::max(max_n, h->piv_maxn_hint);
   PivTask *dp = push(h, pv);
   int ev = tbeg(h, K_PIVOT);
   if (max_n <= PIVLU_MAXN && !h->pivot_unblocked) {
@@ -866,6 +877,108 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
   CK(cudaGetLastError());
 }
 
+// ---- distributed factorization (include/lorasp.h) --------------
+int dist_owner_of(int level, int c, int l0) {
+  const int sh = level - 1 - l0;
+  return sh >= 0 ? (c >> sh) : 0;
+}
+
+void dist_call(lorasp_ctx *h, int kind, int64_t nbytes) {
+  ++h->dist_calls;
+  if (h->dist_fn(h->dist_user, kind, nbytes) != 0)
+    throw Err(LORASP_E_CUDA, "distributed exchange callback failed (kind " + std::to_string(kind) + ")");
+}
+
+void dist_reserve(lorasp_ctx *h, int64_t nbytes) {
+  if (h->dist_send_cap >= nbytes && h->dist_recv_cap >= nbytes * h->dist_world) return;
+  dist_call(h, LORASP_COLL_RESERVE, nbytes);
+  if (h->dist_send_cap < nbytes || h->dist_recv_cap < nbytes * h->dist_world)
+    throw Err(LORASP_E_ARG, "distributed exchange buffers too small after the reserve callback");
+}
+
+// max over ranks of n device ints (non-owned entries are 0) and of the status
+// pair; results to host_out[0..n) and h->h_status[0..2)
+void dist_allmax_ints(lorasp_ctx *h, const int *dev, size_t n, int *host_out) {
+  const int64_t nbytes = (int64_t)(n + 2) * sizeof(int);
+  dist_reserve(h, nbytes);
+  int *sb = static_cast<int *>(h->dist_send);
+  if (n) CK(cudaMemcpyAsync(sb, dev, n * sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaMemcpyAsync(sb + n, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  dist_call(h, LORASP_COLL_MAXINT, nbytes);
+  std::vector<int> tmp(n + 2);
+  CK(cudaMemcpy(tmp.data(), sb, nbytes, cudaMemcpyDeviceToHost));
+  for (size_t q = 0; q < n; ++q) host_out[q] = tmp[q];
+  h->h_status[0] = tmp[n];
+  h->h_status[1] = tmp[n + 1];
+}
+
+// contiguous n-double copy as k_copy tasks of <= 2048 x 16 doubles
+void contig_copies(std::vector<CopyTask> &ct, const double *src, double *dst, int64_t n) {
+  while (n > 0) {
+    CopyTask t{};
+    t.mode = 0;
+    t.alpha = 1.0;
+    t.src = src;
+    t.dst = dst;
+    int64_t take;
+    if (n >= 2048) {
+      t.rows = 2048;
+      t.cols = (int)std::min<int64_t>(16, n / 2048);
+      take = (int64_t)t.rows * t.cols;
+    } else {
+      t.rows = (int)n;
+      t.cols = 1;
+      take = n;
+    }
+    t.lds = t.ldd = t.rows;
+    ct.push_back(t);
+    src += take;
+    dst += take;
+    n -= take;
+  }
+}
+
+using DirtyList = std::vector<std::pair<double *, int64_t>>;
+
+// end of a colour wave: every rank's written regions (lists in the same order
+// on every rank) travel in one all-gather and are copied into the store
+void dist_exchange(lorasp_ctx *h, const std::vector<DirtyList> &dirty) {
+  const int G = h->dist_world, me = h->dist_rank;
+  int64_t mx = 0;
+  for (int g = 0; g < G; ++g) {
+    int64_t t = 0;
+    for (auto &pr : dirty[g]) t += pr.second;
+    mx = std::max(mx, t);
+  }
+  if (mx == 0) return;
+  const int64_t nbytes = mx * 8;
+  dist_reserve(h, nbytes);
+  std::vector<CopyTask> ct;
+  double *send = static_cast<double *>(h->dist_send);
+  int64_t off = 0;
+  for (auto &pr : dirty[me]) {
+    contig_copies(ct, pr.first, send + off, pr.second);
+    off += pr.second;
+  }
+  launch_copy(h, ct, -1);
+  CK(cudaStreamSynchronize(h->stream));
+  dist_call(h, LORASP_COLL_ALLGATHER, nbytes);
+  h->dist_bytes += nbytes;
+  ct.clear();
+  const double *recv = static_cast<const double *>(h->dist_recv);
+  for (int g = 0; g < G; ++g) {
+    if (g == me) continue;
+    off = 0;
+    for (auto &pr : dirty[g]) {
+      contig_copies(ct, recv + (int64_t)g * mx + off, pr.first, pr.second);
+      off += pr.second;
+    }
+  }
+  launch_copy(h, ct, -1);
+}
+
+
 // Returns false only in replay mode when the predicted ranks were wrong (the
 // caller then re-runs with replay = false).
 bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
@@ -874,6 +987,11 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
   cudaStream_t st = h->stream;
   const int L = pl.depth;
   const bool sym = (pl.flags & LORASP_SPD) != 0;
+  const bool dist = h->dist_world > 1 && h->dist_fn;
+  if (dist && replay) return false;
+  h->dist_bytes = 0;
+  h->dist_calls = 0;
+  h->piv_maxn_hint = 0;
   h->launches_factor = 0;
   h->split_nodes = 0;
   h->flops_model = 0;
@@ -925,13 +1043,14 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
     auto bound = [&](int id) { return id < K ? m[id] : (lv.node[id - K].aux ? m[id - K] : 0); };
     auto size = [&](int id) { return id < K ? m[id] : r[id - K]; };
     // slot layout (bound sizes; P-node ranks are not known yet)
-    std::vector<int64_t> soff(lv.slots.size());
+    std::vector<int64_t> soff(lv.slots.size()), slen(lv.slots.size());
     std::vector<int> sld(lv.slots.size());
     int64_t tot = 0;
     for (size_t s = 0; s < lv.slots.size(); ++s) {
       int rows = bound(lv.slots[s].row), cols = bound(lv.slots[s].col);
       sld[s] = std::max(1, rows);
       soff[s] = tot;
+      slen[s] = (int64_t)rows * cols;
       tot += ((int64_t)rows * cols + 31) & ~int64_t(31);
     }
     DevBuf &ar = h->arena[i & 1];
@@ -939,6 +1058,11 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
     CK(cudaMemsetAsync(ar.p, 0, tot * sizeof(double), st));
     double *base = ar.as<double>();
     auto slot_ptr = [&](int s) { return base + soff[s]; };
+    // distributed mode: the owner of each node of this level (include/lorasp.h)
+    if (dist && K != (1 << (i - 1)))
+      throw Err(LORASP_E_ARG, "distributed factorization needs 2^(i-1) clusters at level i");
+    auto owner = [&](int c) { return dist ? dist_owner_of(i, c, h->dist_l0) : 0; };
+    auto own = [&](int c) { return !dist || owner(c) == h->dist_rank; };
 
     // ---- MergeRedNodes ------------------------------------------------------
     if (i == L) {
@@ -1007,7 +1131,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
       std::vector<CopyTask> s_ct;
       std::vector<PivTask> s_pt;
       int s_max = 0;
-      if (sym && !comp.empty() && !h->no_split) {
+      if (sym && !comp.empty() && !h->no_split && !dist) {
         int64_t stot2 = 0;
         // A node is split when that pays: in waves wider than the GPU (the S
         // pivots then fill the sync gaps), or when its fused pivot would likely
@@ -1090,8 +1214,10 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
         int64_t soff_sig = 0, xoff = 0;
         int max_m = 0;
         double f_gram = 0, b_gram = 0, f_eig = 0, b_eig = 0;
+        if (dist) CK(cudaMemsetAsync(h->d_ranks.p, 0, comp.size() * sizeof(int), st));
         for (size_t q = 0; q < comp.size(); ++q) {
           const int c = comp[q];
+          if (!own(c)) continue;   // distributed: the owner compresses (ranks exchanged below)
           const SymNode &nd = lv.node[c];
           const int mc = m[c];
           max_m = std::max(max_m, mc);
@@ -1204,10 +1330,14 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
             if (m[c] > 0) rho_pred = std::max(rho_pred, (double)r[c] / m[c]);
           }
         } else {
-        CK(cudaMemcpyAsync(h->h_ranks, h->d_ranks.p, comp.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
         auto ts0 = std::chrono::steady_clock::now();
-        CK(cudaStreamSynchronize(st));
+        if (dist) {
+          dist_allmax_ints(h, h->d_ranks.as<int>(), comp.size(), h->h_ranks);
+        } else {
+          CK(cudaMemcpyAsync(h->h_ranks, h->d_ranks.p, comp.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+          CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+        }
         h->t_sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts0).count();
         h->stg.reset();
         if (h->h_status[0] != 0) {
@@ -1259,13 +1389,20 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
           h->ws_T1.ensure(yt * 8 + 256, st);
         }
       }
-      int max_n = 0;
+      int max_n = 0, max_n_small = 0;
       double f_proj = 0, b_proj = 0, f_piv = 0, b_piv = 0, f_z = 0, b_z = 0, f_s = 0, b_s = 0;
+      std::vector<DirtyList> dirty(dist ? h->dist_world : 0);
       for (size_t e = 0; e < elim.size(); ++e) {
         const int c = elim[e];
         const SymNode &nd = lv.node[c];
         const int mc = m[c], rc = r[c], n = mc + rc, W = Wn[e];
         max_n = std::max(max_n, n);
+        if (n <= PIV_SMALL_N) max_n_small = std::max(max_n_small, n);
+        // distributed: every rank lays out every node (same records and host
+        // state); the tasks of nodes it does not own are dropped at the end
+        const size_t n_pt = pt.size(), n_ps = ps.size(), n_ct = ct.size(), n_pv = pv.size(), n_zt = zt.size(),
+                     n_zs = zs.size(), n_stt = stt.size(), n_ss = ss.size();
+        std::vector<int> wslots;   // slots this node writes (projection + Schur targets)
         double *V = h->ws_V.as<double>() + goff[c];
         // project: R_k = A_k V  into  P(b) <-> p_k  (edge rules 2/3, P:l.385-386)
         int R = 0;
@@ -1279,6 +1416,8 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
             // LU:  R_k = A_k V (Mat(s->p)) into Mat(P->p);  Q_k = B_k V (Mat(p->s)^T V)
             //      stored transposed into Mat(p->P) = Q_k^T
             int s1 = sym ? nd.pslot_src[k] : nd.pslot_src2[k], s2 = nd.pslot_dst[k];
+            wslots.push_back(s2);
+            if (!sym) wslots.push_back(nd.pslot_dst2[k]);
             GemmTask b{};
             b.C = slot_ptr(s2);
             b.ldc = sld[s2];
@@ -1583,6 +1722,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
                 const int wa = rec.w[a], wb = rec.w[bb];
                 if (wa == 0 || wb == 0) continue;
                 const int sl = nd.tslot[a * T.size() + bb];
+                wslots.push_back(sl);
                 GemmTask b{};
                 b.C = slot_ptr(sl);
                 b.ldc = sld[sl];
@@ -1604,6 +1744,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
               int wa = rec.w[a], wb = rec.w[bb];
               if (wa == 0 || wb == 0) continue;
               int sl = nd.tslot[idx];
+              wslots.push_back(sl);
               GemmTask b{};
               b.C = slot_ptr(sl);
               b.ldc = sld[sl];
@@ -1641,8 +1782,27 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
         b_z += 8.0 * ((double)n * n + 2.0 * n * W);
         f_s += (double)(mc + rc) * W * W;
         b_s += 8.0 * (2.0 * n * W + (double)W * W);
+        if (dist) {
+          DirtyList &dl = dirty[owner(c)];
+          dl.push_back({F, (int64_t)ldF * fcols});
+          std::sort(wslots.begin(), wslots.end());
+          wslots.erase(std::unique(wslots.begin(), wslots.end()), wslots.end());
+          for (int sl : wslots)
+            if (slen[sl] > 0) dl.push_back({slot_ptr(sl), slen[sl]});
+          if (!own(c)) {
+            pt.resize(n_pt);
+            ps.resize(n_ps);
+            ct.resize(n_ct);
+            pv.resize(n_pv);
+            zt.resize(n_zt);
+            zs.resize(n_zs);
+            stt.resize(n_stt);
+            ss.resize(n_ss);
+          }
+        }
         h->recs.push_back(std::move(rec));
       }
+      h->piv_maxn_hint = dist ? (sym ? max_n_small : max_n) : 0;
       // all descriptors of the wave travel in one H2D copy
       h->stg.reserve(vbytes(pt) + vbytes(ps) + vbytes(ct) + vbytes(zt) + vbytes(zs) + vbytes(stt) + vbytes(ss), st);
       GemmTask *d_pt = pushd(h, pt), *d_zt = pushd(h, zt), *d_stt = pushd(h, stt);
@@ -1707,6 +1867,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
       }
       launch_gemm_dev(h, d_zt, d_zs, zt.size(), K_ZGEMM, f_z, b_z);
       launch_gemm_dev(h, d_stt, d_ss, stt.size(), K_SCHUR, f_s, b_s);
+      if (dist) dist_exchange(h, dirty);
       if (h->debug) {
         CK(cudaStreamSynchronize(st));
         CK(cudaMemcpy(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost));
@@ -1719,8 +1880,12 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
     prev_soff.swap(soff);
     prev_sld.swap(sld);
   }
-  CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if (dist) {
+    dist_allmax_ints(h, nullptr, 0, nullptr);
+  } else {
+    CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
   h->stg.reset();
   tflush(h);
   if (replay) {
@@ -2208,7 +2373,7 @@ int lorasp_factor(lorasp_handle h, const double *values) {
     try {
       bool ok = false;
       h->replay_used = false;
-      if (h->cache_valid && !h->no_replay) {
+      if (h->cache_valid && !h->no_replay && h->dist_world == 1) {
         ok = factor_impl(h, values, true);
         h->replay_used = ok;
       }
@@ -2282,6 +2447,37 @@ int lorasp_set_stream(lorasp_handle h, void *s) {
   return LORASP_OK;
 }
 
+int lorasp_set_dist(lorasp_handle h, int rank, int world, lorasp_coll_fn fn, void *user) {
+  if (!h) return LORASP_E_ARG;
+  if (world < 1 || (world & (world - 1)) != 0 || rank < 0 || rank >= world) return LORASP_E_ARG;
+  int l0 = 0;
+  while ((1 << l0) < world) ++l0;
+  if (world > 1 && (!fn || h->plan.depth - 1 < l0)) return LORASP_E_ARG;
+  h->dist_rank = world > 1 ? rank : 0;
+  h->dist_world = world;
+  h->dist_l0 = l0;
+  h->dist_fn = world > 1 ? fn : nullptr;
+  h->dist_user = user;
+  h->cache_valid = false;
+  return LORASP_OK;
+}
+
+int lorasp_set_dist_buffers(lorasp_handle h, void *send, int64_t send_cap, void *recv, int64_t recv_cap) {
+  if (!h || send_cap < 0 || recv_cap < 0) return LORASP_E_ARG;
+  h->dist_send = send;
+  h->dist_send_cap = send ? send_cap : 0;
+  h->dist_recv = recv;
+  h->dist_recv_cap = recv ? recv_cap : 0;
+  return LORASP_OK;
+}
+
+int lorasp_dist_owner(int level, int c, int world) {
+  if (level < 1 || c < 0 || world < 1 || (world & (world - 1)) != 0) return -1;
+  int l0 = 0;
+  while ((1 << l0) < world) ++l0;
+  return dist_owner_of(level, c, l0);
+}
+
 int lorasp_set_timing(lorasp_handle h, int enable) {
   return guarded(h, [&]() {
     CK(cudaSetDevice(h->device));
@@ -2341,7 +2537,9 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
       << ",\"t_rank_sync_wait_ms\":" << h->t_sync_ms << ",\"launches_factor\":" << h->launches_factor
       << ",\"schedule_rank_predicted\":" << (h->replay_used ? "true" : "false")
       << ",\"rank_prediction_hits\":" << h->replay_hits << ",\"rank_prediction_misses\":" << h->replay_misses
-      << ",\"split_pivot_nodes\":" << h->split_nodes
+      << ",\"split_pivot_nodes\":" << h->split_nodes << ",\"dist_world\":" << h->dist_world
+      << ",\"dist_rank\":" << h->dist_rank << ",\"dist_exchange_calls\":" << h->dist_calls
+      << ",\"dist_allgather_bytes\":" << h->dist_bytes
       << ",\"aux_vars\":";
     int64_t aux = 0;
     for (int i = 1; i <= pl.depth; ++i)

@@ -34,7 +34,14 @@ STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "E_ARG", -2: "E_PATTERN", -3: "E_SING
 SYMBOLS = ["lorasp_analyze", "lorasp_factor", "lorasp_apply", "lorasp_gmres", "lorasp_krylov_ex",
            "lorasp_set_stream", "lorasp_set_timing", "lorasp_get_depth", "lorasp_get_level_order", "lorasp_get_ranks",
            "lorasp_get_sizes", "lorasp_get_stats", "lorasp_get_launch_count", "lorasp_test_eig",
-           "lorasp_test_pivot", "lorasp_last_error", "lorasp_destroy"]
+           "lorasp_test_pivot", "lorasp_last_error", "lorasp_destroy", "lorasp_set_dist",
+           "lorasp_set_dist_buffers", "lorasp_dist_owner"]
+
+LORASP_COLL_ALLGATHER = 0
+LORASP_COLL_MAXINT = 1
+LORASP_COLL_RESERVE = 2
+# int (*lorasp_coll_fn)(void *user, int kind, int64_t nbytes)
+COLL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64)
 
 _lib = None
 
@@ -78,6 +85,9 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lorasp_last_error.restype = ctypes.c_char_p
     lib.lorasp_destroy.argtypes = [P]
     lib.lorasp_destroy.restype = None
+    lib.lorasp_set_dist.argtypes = [P, ctypes.c_int, ctypes.c_int, COLL_FN, P]
+    lib.lorasp_set_dist_buffers.argtypes = [P, P, ctypes.c_int64, P, ctypes.c_int64]
+    lib.lorasp_dist_owner.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
     for s in SYMBOLS:
         if s not in ("lorasp_last_error", "lorasp_destroy"):
             getattr(lib, s).restype = ctypes.c_int
@@ -146,6 +156,36 @@ class Handle:
     def set_stream(self, stream_ptr: int):
         return self._check(self._lib.lorasp_set_stream(self.h, ctypes.c_void_p(stream_ptr)), "set_stream")
 
+    def set_dist(self, rank, world, comm=None):
+        """Distributed factorization (include/lorasp.h, lorasp_set_dist): `comm`
+        provides reserve(nbytes) -> (send, recv) device tensors, allgather(nbytes)
+        and allmax_int(nbytes) (paper_1510_07363_b200.dist).  world = 1 resets."""
+        lib = self._lib
+        if world == 1 or comm is None:
+            self._coll = None
+            return self._check(lib.lorasp_set_dist(self.h, 0, 1, COLL_FN(), None), "set_dist")
+
+        def cb(_user, kind, nbytes):
+            try:
+                if kind == LORASP_COLL_RESERVE:
+                    send, recv = comm.reserve(int(nbytes))
+                    lib.lorasp_set_dist_buffers(self.h, _ptr(send), send.numel() * send.element_size(),
+                                                _ptr(recv), recv.numel() * recv.element_size())
+                elif kind == LORASP_COLL_ALLGATHER:
+                    comm.allgather(int(nbytes))
+                elif kind == LORASP_COLL_MAXINT:
+                    comm.allmax_int(int(nbytes))
+                else:
+                    return 1
+                return 0
+            except Exception:   # reported to the engine, which aborts with E_CUDA
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._coll = COLL_FN(cb)   # the handle keeps the callback alive
+        return self._check(lib.lorasp_set_dist(self.h, int(rank), int(world), self._coll, None), "set_dist")
+
     def set_timing(self, mask):
         """mask: True = all kernel classes, False = off, or an int bitmask of classes."""
         m = -1 if mask is True else (0 if mask is False else int(mask))
@@ -192,6 +232,11 @@ class Handle:
             self.close()
         except Exception:
             pass
+
+
+def dist_owner(level, c, world):
+    """Owner rank of level-`level` super-node c (lorasp_dist_owner)."""
+    return load().lorasp_dist_owner(int(level), int(c), int(world))
 
 
 def test_eig(G, eps, device=0):
