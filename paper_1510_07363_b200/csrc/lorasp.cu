@@ -320,6 +320,7 @@ struct lorasp_ctx {
   int64_t dist_send_cap = 0, dist_recv_cap = 0;
   int64_t dist_bytes = 0, dist_calls = 0;
   int piv_maxn_hint = 0;   // batch-independent pivot path choice (max n of the whole wave)
+  int eig_clmax_hint = 0, eig_bigmax_hint = 0;   // the same for the eigen-solver classes
 };
 
 namespace {
@@ -613,13 +614,13 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
   }
   if (!post.empty()) {
     EigTask *dp = push(h, post);
-    int mmax = 0;
+    int mmax = h->eig_clmax_hint;
     for (auto &e : post) mmax = std::max(mmax, e.m);
     h->launches_factor += launch_pre_post(h->stream, dp, (int)post.size(), mmax, h->plan.eps, h->d_status.as<int>());
   }
   if (!big.empty()) {
     EigTask *db = single ? de : push(h, big);
-    int mb = 0;
+    int mb = h->eig_bigmax_hint;
     for (auto &e : big) mb = std::max(mb, e.m);
     launch_k(k_eig_t<false>, (unsigned)big.size(), EIG_THREADS, (size_t)eig_generic_cap(mb) * 8, h->stream, 
         db, h->plan.eps, eig_generic_cap(mb), h->d_status.as<int>());
@@ -1131,7 +1132,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
       std::vector<CopyTask> s_ct;
       std::vector<PivTask> s_pt;
       int s_max = 0;
-      if (sym && !comp.empty() && !h->no_split && !dist) {
+      if (sym && !comp.empty() && !h->no_split) {
         int64_t stot2 = 0;
         // A node is split when that pays: in waves wider than the GPU (the S
         // pivots then fill the sync gaps), or when its fused pivot would likely
@@ -1147,8 +1148,10 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
           }
         if (stot2 > 0) {
           h->ws_S.ensure(stot2 * 8 + 256, st);
+          for (int c : elim)
+            if (s_off[c] >= 0) s_max = std::max(s_max, m[c]);   // launch shape of the whole wave
           for (int c : elim) {
-            if (s_off[c] < 0) continue;
+            if (s_off[c] < 0 || !own(c)) continue;
             const SymNode &nd = lv.node[c];
             CopyTask t{};
             t.src = slot_ptr(nd.self_slot);
@@ -1162,7 +1165,6 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
             s_ct.push_back(t);
             s_pt.push_back(PivTask{h->ws_S.as<double>() + s_off[c], m[c], m[c], 0, c});
             ++h->split_nodes;
-            s_max = std::max(s_max, m[c]);
           }
           CK(cudaEventRecord(h->ev_s0, st));   // S is final here; stream2 starts after it
         }
@@ -1214,7 +1216,18 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
         int64_t soff_sig = 0, xoff = 0;
         int max_m = 0;
         double f_gram = 0, b_gram = 0, f_eig = 0, b_eig = 0;
-        if (dist) CK(cudaMemsetAsync(h->d_ranks.p, 0, comp.size() * sizeof(int), st));
+        h->eig_clmax_hint = h->eig_bigmax_hint = 0;
+        if (dist) {
+          CK(cudaMemsetAsync(h->d_ranks.p, 0, comp.size() * sizeof(int), st));
+          // launch-shape choices from the whole wave, so that every rank runs
+          // the single-GPU kernel variants (bit-identical results)
+          for (int c : comp) {
+            const int mc = m[c];
+            if (mc >= EIG_REG_MIN && mc <= EIG_REG_M) continue;
+            if (!eig_cl_disabled && eig_cl_class(mc)) h->eig_clmax_hint = std::max(h->eig_clmax_hint, mc);
+            else h->eig_bigmax_hint = std::max(h->eig_bigmax_hint, mc);
+          }
+        }
         for (size_t q = 0; q < comp.size(); ++q) {
           const int c = comp[q];
           if (!own(c)) continue;   // distributed: the owner compresses (ranks exchanged below)
@@ -1389,7 +1402,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
           h->ws_T1.ensure(yt * 8 + 256, st);
         }
       }
-      int max_n = 0, max_n_small = 0;
+      int max_n = 0, pv_max_small = 0, pv_max_all = 0;
       double f_proj = 0, b_proj = 0, f_piv = 0, b_piv = 0, f_z = 0, b_z = 0, f_s = 0, b_s = 0;
       std::vector<DirtyList> dirty(dist ? h->dist_world : 0);
       for (size_t e = 0; e < elim.size(); ++e) {
@@ -1397,11 +1410,12 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
         const SymNode &nd = lv.node[c];
         const int mc = m[c], rc = r[c], n = mc + rc, W = Wn[e];
         max_n = std::max(max_n, n);
-        if (n <= PIV_SMALL_N) max_n_small = std::max(max_n_small, n);
         // distributed: every rank lays out every node (same records and host
         // state); the tasks of nodes it does not own are dropped at the end
         const size_t n_pt = pt.size(), n_ps = ps.size(), n_ct = ct.size(), n_pv = pv.size(), n_zt = zt.size(),
-                     n_zs = zs.size(), n_stt = stt.size(), n_ss = ss.size();
+                     n_zs = zs.size(), n_stt = stt.size(), n_ss = ss.size(), n_syt = sy_t.size(),
+                     n_sys = sy_s.size(), n_sgt = sg_t.size(), n_sgs = sg_s.size(), n_sxt = sx_t.size(),
+                     n_sxs = sx_s.size();
         std::vector<int> wslots;   // slots this node writes (projection + Schur targets)
         double *V = h->ws_V.as<double>() + goff[c];
         // project: R_k = A_k V  into  P(b) <-> p_k  (edge rules 2/3, P:l.385-386)
@@ -1783,6 +1797,11 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
         f_s += (double)(mc + rc) * W * W;
         b_s += 8.0 * (2.0 * n * W + (double)W * W);
         if (dist) {
+          for (size_t q = n_pv; q < pv.size(); ++q) {   // the pivot batch as one GPU would see it
+            const int pn = pv[q].m + pv[q].r;
+            pv_max_all = std::max(pv_max_all, pn);
+            if (pn <= PIV_SMALL_N) pv_max_small = std::max(pv_max_small, pn);
+          }
           DirtyList &dl = dirty[owner(c)];
           dl.push_back({F, (int64_t)ldF * fcols});
           std::sort(wslots.begin(), wslots.end());
@@ -1798,11 +1817,17 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
             zs.resize(n_zs);
             stt.resize(n_stt);
             ss.resize(n_ss);
+            sy_t.resize(n_syt);
+            sy_s.resize(n_sys);
+            sg_t.resize(n_sgt);
+            sg_s.resize(n_sgs);
+            sx_t.resize(n_sxt);
+            sx_s.resize(n_sxs);
           }
         }
         h->recs.push_back(std::move(rec));
       }
-      h->piv_maxn_hint = dist ? (sym ? max_n_small : max_n) : 0;
+      h->piv_maxn_hint = dist ? (sym ? pv_max_small : pv_max_all) : 0;
       // all descriptors of the wave travel in one H2D copy
       h->stg.reserve(vbytes(pt) + vbytes(ps) + vbytes(ct) + vbytes(zt) + vbytes(zs) + vbytes(stt) + vbytes(ss), st);
       GemmTask *d_pt = pushd(h, pt), *d_zt = pushd(h, zt), *d_stt = pushd(h, stt);

@@ -41,11 +41,14 @@ def _single(L, p):
     ("cfg1", (64, 64), 4),
     ("cfg2", (128, 128), 8),
     ("cfg5", (64, 64), 4),      # general (LU) path
+    ("cfg3", (32, 32, 32), 4),  # 3D: cluster eigen-solver classes and split pivots
 ])
 def test_virtual_ranks_match_single_gpu(L, name, dims, world):
     from paper_1510_07363_b200.dist import VirtualGroup, factor_virtual
     p = make_problem(name, dims=dims)
     h1, x1, r1 = _single(L, p)
+    if name == "cfg3":
+        assert h1.stats()["split_pivot_nodes"] > 0
     group = VirtualGroup(world)
     hs = [L.analyze_problem(p) for _ in range(world)]
     errs = factor_virtual(hs, p.values, group)
