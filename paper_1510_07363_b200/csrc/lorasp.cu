@@ -320,7 +320,8 @@ struct lorasp_ctx {
   int64_t dist_send_cap = 0, dist_recv_cap = 0;
   int64_t dist_bytes = 0, dist_calls = 0;
   int piv_maxn_hint = 0;   // batch-independent pivot path choice (max n of the whole wave)
-  int eig_clmax_hint = 0, eig_bigmax_hint = 0;   // the same for the eigen-solver classes
+  int eig_clmax_hint = 0, eig_bigmax_hint = 0, eig_regmax_hint = 0;   // the same for the eigen-solver classes
+  bool eig_split_classes = getenv("LORASP_EIG_SPLIT_CLASSES") != nullptr;   // A/B: one launch per tile class
 };
 
 namespace {
@@ -596,8 +597,16 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
   if (!small.empty()) {
     // register-tile path, by tile class (32 / 64 / 128 rows); the whole 200 KB
     // of shared memory serves A + the inverse-iteration batches
+    // one launch pair at the largest tile class of the wave: the classes would
+    // otherwise run one after the other, each a full chain of latency-bound steps
     std::vector<EigTask> rc[3];
-    for (auto &e : small) rc[e.m <= 32 ? 0 : (e.m <= 64 ? 1 : 2)].push_back(e);
+    int cmax = 0;
+    for (auto &e : small) cmax = std::max(cmax, e.m <= 32 ? 0 : (e.m <= 64 ? 1 : 2));
+    if (h->eig_regmax_hint > 0) cmax = std::max(cmax, h->eig_regmax_hint <= 32 ? 0 : (h->eig_regmax_hint <= 64 ? 1 : 2));
+    if (h->eig_split_classes)
+      for (auto &e : small) rc[e.m <= 32 ? 0 : (e.m <= 64 ? 1 : 2)].push_back(e);
+    else
+      rc[cmax] = small;
     for (int c = 0; c < 3; ++c) {
       if (rc[c].empty()) continue;
       EigTask *ds = (single && rc[c].size() == et.size()) ? de : push(h, rc[c]);
@@ -1216,14 +1225,17 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
         int64_t soff_sig = 0, xoff = 0;
         int max_m = 0;
         double f_gram = 0, b_gram = 0, f_eig = 0, b_eig = 0;
-        h->eig_clmax_hint = h->eig_bigmax_hint = 0;
+        h->eig_clmax_hint = h->eig_bigmax_hint = h->eig_regmax_hint = 0;
         if (dist) {
           CK(cudaMemsetAsync(h->d_ranks.p, 0, comp.size() * sizeof(int), st));
           // launch-shape choices from the whole wave, so that every rank runs
           // the single-GPU kernel variants (bit-identical results)
           for (int c : comp) {
             const int mc = m[c];
-            if (mc >= EIG_REG_MIN && mc <= EIG_REG_M) continue;
+            if (mc >= EIG_REG_MIN && mc <= EIG_REG_M) {
+              h->eig_regmax_hint = std::max(h->eig_regmax_hint, mc);
+              continue;
+            }
             if (!eig_cl_disabled && eig_cl_class(mc)) h->eig_clmax_hint = std::max(h->eig_clmax_hint, mc);
             else h->eig_bigmax_hint = std::max(h->eig_bigmax_hint, mc);
           }
