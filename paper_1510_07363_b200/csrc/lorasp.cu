@@ -276,6 +276,10 @@ struct lorasp_ctx {
   cudaStream_t stream2 = nullptr;     // least priority: fills SMs the sweep leaves idle
   cudaStream_t stream_hi = nullptr;   // greatest priority: the factorization itself
   cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr, ev_u = nullptr;
+  cudaStream_t stream_eig = nullptr;   // register-tile eigen path beside the cluster / generic one
+  cudaEvent_t ev_ef = nullptr, ev_ej = nullptr;
+  cudaStream_t stream_cl[2] = {nullptr, nullptr};   // cluster tridiagonalisation classes 2, 3
+  cudaEvent_t ev_cf = nullptr, ev_cj[2] = {nullptr, nullptr};
   bool s1_pending = false;
   DevBuf ws_S, ws_Y, ws_T1, d_sp;
   void *h_sp = nullptr;     // pinned upload of the part-1 copy + pivot task lists
@@ -513,7 +517,13 @@ void ensure_mem(lorasp_ctx *h) {
     CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     CK(cudaStreamCreateWithPriority(&h->stream2, cudaStreamNonBlocking, least));
     CK(cudaStreamCreateWithPriority(&h->stream_hi, cudaStreamNonBlocking, greatest));
+    CK(cudaStreamCreateWithPriority(&h->stream_eig, cudaStreamNonBlocking, greatest));
+    for (auto &cs : h->stream_cl) CK(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, greatest));
   }
+  CK(cudaEventCreateWithFlags(&h->ev_cf, cudaEventDisableTiming));
+  for (auto &e : h->ev_cj) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&h->ev_ef, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&h->ev_ej, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&h->ev_u, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&h->ev_s0, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&h->ev_s1, cudaEventDisableTiming));
@@ -587,6 +597,7 @@ void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::v
 
 void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int max_m, int cap) {
   std::vector<EigTask> small, big, clt[4];
+  bool reg_fork = false;
   for (const EigTask &e : et) {
     const int cls = eig_cl_disabled ? 0 : eig_cl_class(e.m);
     if (e.m >= EIG_REG_MIN && e.m <= EIG_REG_M) small.push_back(e);
@@ -607,19 +618,49 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
       for (auto &e : small) rc[e.m <= 32 ? 0 : (e.m <= 64 ? 1 : 2)].push_back(e);
     else
       rc[cmax] = small;
-    for (int c = 0; c < 3; ++c) {
-      if (rc[c].empty()) continue;
-      EigTask *ds = (single && rc[c].size() == et.size()) ? de : push(h, rc[c]);
-      h->launches_factor += launch_eig_reg(h->stream, ds, (int)rc[c].size(), c, h->plan.eps, h->d_status.as<int>());
+    EigTask *ds[3] = {nullptr, nullptr, nullptr};
+    for (int c = 0; c < 3; ++c)
+      if (!rc[c].empty()) ds[c] = (single && rc[c].size() == et.size()) ? de : push(h, rc[c]);
+    // with cluster / generic tasks in the same wave the register-tile pair runs
+    // on its own stream beside them (few nodes per class: the SMs are idle)
+    reg_fork = !single && !h->eig_split_classes;
+    cudaStream_t rs = h->stream;
+    if (reg_fork) {
+      CK(cudaEventRecord(h->ev_ef, h->stream));
+      CK(cudaStreamWaitEvent(h->stream_eig, h->ev_ef, 0));
+      rs = h->stream_eig;
     }
+    for (int c = 0; c < 3; ++c)
+      if (ds[c]) h->launches_factor += launch_eig_reg(rs, ds[c], (int)rc[c].size(), c, h->plan.eps, h->d_status.as<int>());
+    if (reg_fork) CK(cudaEventRecord(h->ev_ej, h->stream_eig));
   }
   std::vector<EigTask> post;
-  for (int c = 1; c <= 3; ++c) {
-    if (clt[c].empty()) continue;
-    EigTask *dc = push(h, clt[c]);
-    launch_tridiag_cl(h->stream, dc, (int)clt[c].size(), c, h->plan.eps);
-    ++h->launches_factor;
-    post.insert(post.end(), clt[c].begin(), clt[c].end());
+  {
+    // the cluster classes side by side (classes 2 and 3 on their own streams)
+    EigTask *dc[4] = {nullptr, nullptr, nullptr, nullptr};
+    int ncls = 0;
+    for (int c = 1; c <= 3; ++c)
+      if (!clt[c].empty()) {
+        dc[c] = push(h, clt[c]);
+        ++ncls;
+      }
+    const bool fork = ncls > 1 && !h->eig_split_classes;
+    if (fork) CK(cudaEventRecord(h->ev_cf, h->stream));
+    for (int c = 1; c <= 3; ++c) {
+      if (!dc[c]) continue;
+      cudaStream_t cs = h->stream;
+      if (fork && c > 1) {
+        cs = h->stream_cl[c - 2];
+        CK(cudaStreamWaitEvent(cs, h->ev_cf, 0));
+      }
+      launch_tridiag_cl(cs, dc[c], (int)clt[c].size(), c, h->plan.eps);
+      ++h->launches_factor;
+      if (cs != h->stream) {
+        CK(cudaEventRecord(h->ev_cj[c - 2], cs));
+        CK(cudaStreamWaitEvent(h->stream, h->ev_cj[c - 2], 0));
+      }
+      post.insert(post.end(), clt[c].begin(), clt[c].end());
+    }
   }
   if (!post.empty()) {
     EigTask *dp = push(h, post);
@@ -636,6 +677,7 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
     ++h->launches_factor;
     CK(cudaGetLastError());
   }
+  if (reg_fork) CK(cudaStreamWaitEvent(h->stream, h->ev_ej, 0));
   (void)max_m;
   (void)cap;
 }
@@ -2814,6 +2856,20 @@ void lorasp_destroy(lorasp_handle h) {
       cudaStreamSynchronize(h->stream_hi);
       cudaStreamDestroy(h->stream_hi);
     }
+    if (h->stream_eig) {
+      cudaStreamSynchronize(h->stream_eig);
+      cudaStreamDestroy(h->stream_eig);
+    }
+    for (auto &cs : h->stream_cl)
+      if (cs) {
+        cudaStreamSynchronize(cs);
+        cudaStreamDestroy(cs);
+      }
+    if (h->ev_cf) cudaEventDestroy(h->ev_cf);
+    for (auto &e : h->ev_cj)
+      if (e) cudaEventDestroy(e);
+    if (h->ev_ef) cudaEventDestroy(h->ev_ef);
+    if (h->ev_ej) cudaEventDestroy(h->ev_ej);
     if (h->ev_u) cudaEventDestroy(h->ev_u);
     if (h->ev_s0) cudaEventDestroy(h->ev_s0);
     if (h->ev_s1) cudaEventDestroy(h->ev_s1);
