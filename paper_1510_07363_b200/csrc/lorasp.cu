@@ -85,11 +85,22 @@ static int eig_generic_cap(int m) {
 }
 
 // growable device buffer; growth synchronises the stream first (no in-flight use)
+// bumped by every device (re)allocation: a recorded factorization graph holds
+// raw pointers and is only replayed while this is unchanged
+static long long g_alloc_gen = 0;
+struct CaptureAbort {};
+
 struct DevBuf {
   void *p = nullptr;
   size_t cap = 0;
   void ensure(size_t bytes, cudaStream_t st) {
     if (bytes <= cap) return;
+    {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      if (st && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+        throw CaptureAbort{};   // growth inside a graph capture: record later
+    }
+    ++g_alloc_gen;
     if (p) {
       CK(cudaStreamSynchronize(st));
       CK(cudaFree(p));
@@ -127,6 +138,7 @@ struct Pool {
       used = 0;
     }
     if (ci == chunks.size()) {
+      ++g_alloc_gen;
       size_t cap = std::max<size_t>(nd, size_t(32) << 20);  // >= 256 MB
       double *p = nullptr;
       if (cudaMalloc(&p, cap * sizeof(double)) != cudaSuccess) {
@@ -163,6 +175,7 @@ struct Staging {
   }
   // make room for a group of pushes that one launch consumes together
   void reserve(size_t bytes, cudaStream_t st) {
+    if (cap_mode) return;
     size_t need = bytes + 4096;
     if (used + need <= cap) return;
     flush(st);
@@ -175,9 +188,26 @@ struct Staging {
   // the last flush() is one cudaMemcpyAsync (descriptors of a whole wave travel
   // together).  Returns the device pointer.
   size_t pend = 0;   // start of the not-yet-copied range
+  // graph capture: descriptors go to `blob` (host) at their final offsets in the
+  // persistent device buffer `gd`, copied once after the capture
+  bool cap_mode = false, cap_overflow = false;
+  std::vector<char> blob;
+  char *gd = nullptr;
+  size_t gd_cap = 0, total = 0;   // total: bytes pushed by the current factorization
   void *push_deferred(const void *src, size_t bytes, cudaStream_t st) {
-    if (bytes == 0) return d.p;
+    if (bytes == 0) return cap_mode ? (void *)gd : d.p;
     size_t need = (bytes + 255) & ~size_t(255);
+    if (cap_mode) {
+      const size_t off = blob.size();
+      blob.resize(off + need);
+      std::memcpy(blob.data() + off, src, bytes);
+      if (off + need > gd_cap) {
+        cap_overflow = true;
+        return gd;
+      }
+      return gd + off;
+    }
+    total += need;
     if (used + need > cap) {
       flush(st);
       CK(cudaStreamSynchronize(st));
@@ -191,6 +221,7 @@ struct Staging {
     return dp;
   }
   void flush(cudaStream_t st) {
+    if (cap_mode) return;
     if (used > pend) CK(cudaMemcpyAsync(d.as<char>() + pend, h + pend, used - pend, cudaMemcpyHostToDevice, st));
     pend = used;
   }
@@ -199,7 +230,11 @@ struct Staging {
     flush(st);
     return dp;
   }
-  void reset() { used = 0; pend = 0; }  // only after a stream sync
+  void reset() {   // only after a stream sync
+    if (cap_mode) return;
+    used = 0;
+    pend = 0;
+  }
   void release() {
     if (h) cudaFreeHost(h);
     h = nullptr;
@@ -240,6 +275,13 @@ struct NodeRec {  // one eliminated (s, b) pair, for apply + stats
 }  // namespace lorasp
 
 using namespace lorasp;
+
+// ranks a rank-predicted sweep logged (device -> pinned host, stream order)
+struct RankLog {
+  int level;
+  size_t pos;
+  std::vector<int> comp;
+};
 
 struct lorasp_ctx {
   Plan plan;
@@ -324,6 +366,20 @@ struct lorasp_ctx {
   int64_t dist_send_cap = 0, dist_recv_cap = 0;
   int64_t dist_bytes = 0, dist_calls = 0;
   int piv_maxn_hint = 0;   // batch-independent pivot path choice (max n of the whole wave)
+  // recorded factorization: a verified rank-predicted sweep captured once as a
+  // CUDA graph (descriptors resident in fg_desc) and replayed while the ranks,
+  // the allocations and the timing mask stay the same
+  cudaGraphExec_t fgraph = nullptr;
+  DevBuf fg_desc;
+  long long fg_gen = -1;
+  unsigned fg_timing = 0;
+  std::vector<TimedEv> fg_pend;
+  std::vector<RankLog> fg_rlog;
+  int64_t fg_fdoubles = 0;
+  bool no_fgraph = getenv("LORASP_NO_FGRAPH") != nullptr;
+  bool fgraph_used = false;
+  int fg_captures = 0, fg_failures = 0;
+  int64_t fg_launches = 0;
   int eig_clmax_hint = 0, eig_bigmax_hint = 0, eig_regmax_hint = 0;   // the same for the eigen-solver classes
   bool eig_split_classes = getenv("LORASP_EIG_SPLIT_CLASSES") != nullptr;   // A/B: one launch per tile class
 };
@@ -348,13 +404,15 @@ int tbeg_force(lorasp_ctx *h, int cls) {
     h->evpool.push_back(e);
   }
   TimedEv t{cls, h->evpool[need - 2], h->evpool[need - 1], 0, 0, 1};
-  CK(cudaEventRecord(t.a, h->stream));
+  if (h->stg.cap_mode) CK(cudaEventRecordWithFlags(t.a, h->stream, cudaEventRecordExternal));
+  else CK(cudaEventRecord(t.a, h->stream));
   h->pend.push_back(t);
   return (int)h->pend.size() - 1;
 }
 void tend(lorasp_ctx *h, int idx, double flops, double bytes) {
   if (idx < 0) return;
-  CK(cudaEventRecord(h->pend[idx].b, h->stream));
+  if (h->stg.cap_mode) CK(cudaEventRecordWithFlags(h->pend[idx].b, h->stream, cudaEventRecordExternal));
+  else CK(cudaEventRecord(h->pend[idx].b, h->stream));
   h->pend[idx].flops = flops;
   h->pend[idx].bytes = bytes;
 }
@@ -1031,9 +1089,37 @@ void dist_exchange(lorasp_ctx *h, const std::vector<DirtyList> &dirty) {
 }
 
 
+
+void copy_values(lorasp_ctx *h, const double *values) {
+  const size_t nb = h->plan.nnz * sizeof(double);
+  CK(cudaMemcpyAsync(h->d_values.p, values, nb, is_device_ptr(values) ? cudaMemcpyDeviceToDevice
+                                                                       : cudaMemcpyHostToDevice, h->stream));
+}
+
+// after the sweep's final synchronisation: the ranks a rank-predicted sweep
+// logged against the prediction it was built with
+bool replay_check(lorasp_ctx *h, const std::vector<RankLog> &rlog) {
+  for (const RankLog &rl : rlog)
+    for (size_t q = 0; q < rl.comp.size(); ++q)
+      if (h->h_ranklog[rl.pos + q] != h->rank_cache[rl.level][rl.comp[q]]) {
+        ++h->replay_misses;
+        return false;
+      }
+  ++h->replay_hits;
+  return true;
+}
+
+void status_check(lorasp_ctx *h) {
+  if (h->h_status[0] != 0)
+    throw Err(h->h_status[0], std::string(h->h_status[0] == LORASP_E_EIG_NOCONV
+                                              ? "Jacobi eigen-solver did not converge"
+                                              : "singular pivot (signed Cholesky failed)") +
+                                  " at node " + std::to_string(h->h_status[1]));
+}
+
 // Returns false only in replay mode when the predicted ranks were wrong (the
 // caller then re-runs with replay = false).
-bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
+bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture = false) {
   ensure_mem(h);
   const Plan &pl = h->plan;
   cudaStream_t st = h->stream;
@@ -1050,12 +1136,8 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
   h->t_host_ms = 0;
   h->t_sync_ms = 0;
   h->factored = false;
-  // values -> device
-  if (is_device_ptr(values)) {
-    CK(cudaMemcpyAsync(h->d_values.p, values, pl.nnz * sizeof(double), cudaMemcpyDeviceToDevice, st));
-  } else {
-    CK(cudaMemcpyAsync(h->d_values.p, values, pl.nnz * sizeof(double), cudaMemcpyHostToDevice, st));
-  }
+  // values -> device (a capture's caller copies them before the capture)
+  if (!capture) copy_values(h, values);
   CK(cudaMemsetAsync(h->d_status.p, 0, 64, st));
   h->fpool.reset();
   h->recs.clear();
@@ -1063,13 +1145,13 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
   h->rnk.assign(L + 2, {});
   std::vector<int64_t> prev_soff;
   std::vector<int> prev_sld;
-  h->stg.reset();
-  CK(cudaStreamSynchronize(st));
-  struct RankLog {
-    int level;
-    size_t pos;
-    std::vector<int> comp;
-  };
+  if (!capture) {
+    h->stg.reset();
+    h->stg.total = 0;
+    CK(cudaStreamSynchronize(st));
+  } else {
+    h->s1_pending = false;   // the previous sweep's stream2 work is complete (caller synchronised)
+  }
   std::vector<RankLog> rlog;
   size_t rlog_pos = 0;
   if (replay) {
@@ -1224,20 +1306,27 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
       auto enqueue_split_part1 = [&]() {
         if (s_pt.empty()) return;
         CK(cudaStreamWaitEvent(h->stream2, h->ev_s0, 0));
-        if (h->s1_pending) CK(cudaEventSynchronize(h->ev_s1));   // pinned task buffer reuse
-        const size_t nbytes = s_ct.size() * sizeof(CopyTask) + s_pt.size() * sizeof(PivTask);
-        if (h->h_sp_cap < nbytes) {
-          if (h->h_sp) CK(cudaFreeHost(h->h_sp));
-          h->h_sp_cap = std::max<size_t>(nbytes * 2, 1 << 16);
-          CK(cudaMallocHost(&h->h_sp, h->h_sp_cap));
+        const CopyTask *dct;
+        const PivTask *dpt;
+        if (capture) {   // descriptors resident in the graph's buffer
+          dct = static_cast<const CopyTask *>(h->stg.push_deferred(s_ct.data(), s_ct.size() * sizeof(CopyTask), st));
+          dpt = static_cast<const PivTask *>(h->stg.push_deferred(s_pt.data(), s_pt.size() * sizeof(PivTask), st));
+        } else {
+          if (h->s1_pending) CK(cudaEventSynchronize(h->ev_s1));   // pinned task buffer reuse
+          const size_t nbytes = s_ct.size() * sizeof(CopyTask) + s_pt.size() * sizeof(PivTask);
+          if (h->h_sp_cap < nbytes) {
+            if (h->h_sp) CK(cudaFreeHost(h->h_sp));
+            h->h_sp_cap = std::max<size_t>(nbytes * 2, 1 << 16);
+            CK(cudaMallocHost(&h->h_sp, h->h_sp_cap));
+          }
+          char *hb = reinterpret_cast<char *>(h->h_sp);
+          std::memcpy(hb, s_ct.data(), s_ct.size() * sizeof(CopyTask));
+          std::memcpy(hb + s_ct.size() * sizeof(CopyTask), s_pt.data(), s_pt.size() * sizeof(PivTask));
+          h->d_sp.ensure(nbytes + 64, st);
+          CK(cudaMemcpyAsync(h->d_sp.p, hb, nbytes, cudaMemcpyHostToDevice, h->stream2));
+          dct = h->d_sp.as<CopyTask>();
+          dpt = reinterpret_cast<const PivTask *>(h->d_sp.as<char>() + s_ct.size() * sizeof(CopyTask));
         }
-        char *hb = reinterpret_cast<char *>(h->h_sp);
-        std::memcpy(hb, s_ct.data(), s_ct.size() * sizeof(CopyTask));
-        std::memcpy(hb + s_ct.size() * sizeof(CopyTask), s_pt.data(), s_pt.size() * sizeof(PivTask));
-        h->d_sp.ensure(nbytes + 64, st);
-        CK(cudaMemcpyAsync(h->d_sp.p, hb, nbytes, cudaMemcpyHostToDevice, h->stream2));
-        const CopyTask *dct = h->d_sp.as<CopyTask>();
-        const PivTask *dpt = reinterpret_cast<const PivTask *>(h->d_sp.as<char>() + s_ct.size() * sizeof(CopyTask));
         launch_k(k_copy, (unsigned)s_ct.size(), 256, 0, h->stream2, dct);
         const size_t smem = (size_t)(s_max | 1) * s_max * 8;
         launch_k(k_pivot_blk, (unsigned)s_pt.size(), 512, smem, h->stream2, dpt, h->d_status.as<int>());
@@ -1959,6 +2048,11 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
     prev_soff.swap(soff);
     prev_sld.swap(sld);
   }
+  if (capture) {   // the caller ends the capture, launches and verifies
+    CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    h->fg_rlog = std::move(rlog);
+    return true;
+  }
   if (dist) {
     dist_allmax_ints(h, nullptr, 0, nullptr);
   } else {
@@ -1967,20 +2061,8 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay) {
   }
   h->stg.reset();
   tflush(h);
-  if (replay) {
-    for (const RankLog &rl : rlog)
-      for (size_t q = 0; q < rl.comp.size(); ++q)
-        if (h->h_ranklog[rl.pos + q] != h->rank_cache[rl.level][rl.comp[q]]) {
-          ++h->replay_misses;
-          return false;
-        }
-    ++h->replay_hits;
-  }
-  if (h->h_status[0] != 0)
-    throw Err(h->h_status[0], std::string(h->h_status[0] == LORASP_E_EIG_NOCONV
-                                              ? "Jacobi eigen-solver did not converge"
-                                              : "singular pivot (signed Cholesky failed)") +
-                                  " at node " + std::to_string(h->h_status[1]));
+  if (replay && !replay_check(h, rlog)) return false;
+  status_check(h);
   if (replay) {
     // same ranks => same record layout (the pool is bump-allocated in the same
     // order): the apply plan of the previous factorization is still valid
@@ -2401,6 +2483,94 @@ int gmres_dev(lorasp_ctx *h, const double *b, double *x, double tol, int restart
   return (rr <= tol) ? LORASP_OK : LORASP_NOT_CONVERGED;
 }
 
+
+// Rank-predicted re-factorization.  Once a predicted sweep has been verified
+// (replay_hits > 0), the next one is captured into a CUDA graph with its task
+// descriptors resident in fg_desc; later calls copy the values and launch the
+// graph (no host task building, no staging copies, no launch gaps), then
+// verify the logged ranks as usual.  A capture that cannot complete (a buffer
+// would grow, an API refuses capture) falls back to the plain predicted sweep.
+bool graph_launch(lorasp_ctx *h, const double *values) {
+  copy_values(h, values);
+  CK(cudaGraphLaunch(h->fgraph, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  ++h->fg_launches;
+  h->fgraph_used = true;
+  h->f_doubles = h->fg_fdoubles;
+  h->t_host_ms = 0;
+  h->t_sync_ms = 0;
+  h->pend.insert(h->pend.end(), h->fg_pend.begin(), h->fg_pend.end());
+  tflush(h);
+  if (!replay_check(h, h->fg_rlog)) {
+    cudaGraphExecDestroy(h->fgraph);
+    h->fgraph = nullptr;
+    return false;
+  }
+  status_check(h);
+  h->factored = true;
+  return true;
+}
+
+bool factor_replay(lorasp_ctx *h, const double *values) {
+  h->fgraph_used = false;
+  const unsigned tsig = h->timing ? h->timing_mask : 0u;
+  const bool want = !h->no_fgraph && !h->debug && h->replay_hits > 0 && h->fg_failures < 2;
+  if (want && h->fgraph && h->fg_gen == g_alloc_gen && h->fg_timing == tsig) return graph_launch(h, values);
+  if (!want) return factor_impl(h, values, true);
+  if (h->fgraph) {
+    cudaGraphExecDestroy(h->fgraph);
+    h->fgraph = nullptr;
+  }
+  // record
+  CK(cudaStreamSynchronize(h->stream));
+  h->fg_desc.ensure(h->stg.total + h->stg.total / 8 + (size_t(1) << 20), h->stream);
+  h->stg.gd = h->fg_desc.as<char>();
+  h->stg.gd_cap = h->fg_desc.cap;
+  h->stg.blob.clear();
+  h->stg.cap_overflow = false;
+  h->pend.clear();
+  cudaGraph_t g = nullptr;
+  bool ok = false;
+  CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+  h->stg.cap_mode = true;
+  try {
+    ok = factor_impl(h, values, true, true);
+  } catch (const CaptureAbort &) {
+    ok = false;
+  } catch (const Err &) {   // an API that refuses capture: the plain sweep below decides
+    ok = false;
+  } catch (...) {
+    h->stg.cap_mode = false;
+    cudaStreamEndCapture(h->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    h->s1_pending = false;
+    h->pend.clear();
+    throw;
+  }
+  h->stg.cap_mode = false;
+  h->s1_pending = false;   // the capture's events only ordered nodes
+  cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+  if (e == cudaSuccess && ok && !h->stg.cap_overflow && g) e = cudaGraphInstantiate(&h->fgraph, g, 0);
+  else if (e == cudaSuccess) e = cudaErrorUnknown;
+  if (g) cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    h->fgraph = nullptr;
+    ++h->fg_failures;
+    h->pend.clear();
+    return factor_impl(h, values, true);
+  }
+  CK(cudaMemcpy(h->fg_desc.p, h->stg.blob.data(), h->stg.blob.size(), cudaMemcpyHostToDevice));
+  h->fg_gen = g_alloc_gen;
+  h->fg_timing = tsig;
+  h->fg_pend = h->pend;
+  h->pend.clear();
+  ++h->fg_captures;
+  h->fg_fdoubles = h->f_doubles;
+  return graph_launch(h, values);
+}
+
 template <class F>
 int guarded(lorasp_ctx *h, F &&f) {
   if (!h) return LORASP_E_ARG;
@@ -2453,10 +2623,17 @@ int lorasp_factor(lorasp_handle h, const double *values) {
       bool ok = false;
       h->replay_used = false;
       if (h->cache_valid && !h->no_replay && h->dist_world == 1) {
-        ok = factor_impl(h, values, true);
+        ok = factor_replay(h, values);
         h->replay_used = ok;
       }
-      if (!ok) factor_impl(h, values, false);
+      if (!ok) {
+        if (h->fgraph) {   // built for the old ranks
+          cudaGraphExecDestroy(h->fgraph);
+          h->fgraph = nullptr;
+        }
+        h->fgraph_used = false;
+        factor_impl(h, values, false);
+      }
     } catch (...) {
       h->cache_valid = false;
       cudaStreamSynchronize(h->stream_hi);
@@ -2616,7 +2793,9 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
       << ",\"t_rank_sync_wait_ms\":" << h->t_sync_ms << ",\"launches_factor\":" << h->launches_factor
       << ",\"schedule_rank_predicted\":" << (h->replay_used ? "true" : "false")
       << ",\"rank_prediction_hits\":" << h->replay_hits << ",\"rank_prediction_misses\":" << h->replay_misses
-      << ",\"split_pivot_nodes\":" << h->split_nodes << ",\"dist_world\":" << h->dist_world
+      << ",\"split_pivot_nodes\":" << h->split_nodes << ",\"factor_graph\":" << (h->fgraph_used ? "true" : "false")
+      << ",\"factor_graph_captures\":" << h->fg_captures << ",\"factor_graph_launches\":" << h->fg_launches
+      << ",\"factor_graph_failures\":" << h->fg_failures << ",\"dist_world\":" << h->dist_world
       << ",\"dist_rank\":" << h->dist_rank << ",\"dist_exchange_calls\":" << h->dist_calls
       << ",\"dist_allgather_bytes\":" << h->dist_bytes
       << ",\"aux_vars\":";
@@ -2848,6 +3027,8 @@ void lorasp_destroy(lorasp_handle h) {
     for (DevBuf *b : bufs) b->release();
     for (cudaEvent_t e : h->evpool) cudaEventDestroy(e);
     if (h->ap_graph) cudaGraphExecDestroy(h->ap_graph);
+    if (h->fgraph) cudaGraphExecDestroy(h->fgraph);
+    h->fg_desc.release();
     if (h->stream2) {
       cudaStreamSynchronize(h->stream2);
       cudaStreamDestroy(h->stream2);
