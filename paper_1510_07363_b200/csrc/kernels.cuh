@@ -2346,8 +2346,50 @@ __global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ ta
 constexpr int PIVB_NB = 16;
 constexpr int PIVB_MAXN = 160;
 
+// signed Cholesky of the b x b diagonal block at j0 by one warp with the block
+// in registers (lane = row, columns by shuffles): no shared-memory round trip
+// per column step.  rd[j0 + k] <- 1 / l_kk.  Returns false on a non-positive
+// pivot (uniform across the warp).
+__device__ __forceinline__ bool pivb_diag_chol(double *__restrict__ A, int lda, int j0, int b, int m,
+                                               double *__restrict__ rd, int lane) {
+  const int i = lane;
+  double a[PIVB_NB];
+#pragma unroll
+  for (int c = 0; c < PIVB_NB; ++c) a[c] = (i < b && c <= i) ? A[(j0 + i) + (j0 + c) * lda] : 0.0;
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < PIVB_NB; ++k) {
+    if (k < b) {
+      const double d = (j0 + k < m) ? 1.0 : -1.0;
+      const double v = __shfl_sync(0xffffffffu, a[k], k) * d;
+      if (!(v > 0.0) || !isfinite(v)) {
+        ok = false;
+        break;
+      }
+      const double lkk = sqrt(v), rk = frcp(lkk);
+      const double lik = (i > k) ? a[k] * (d * rk) : 0.0;
+      if (i == k) a[k] = lkk;
+      else if (i > k) a[k] = lik;
+      if (lane == 0) rd[j0 + k] = rk;
+      const double f = -d * lik;
+#pragma unroll
+      for (int jj = k + 1; jj < PIVB_NB; ++jj) {
+        const double ljk = __shfl_sync(0xffffffffu, lik, jj);
+        if (jj < b && i >= jj) a[jj] = fma(f, ljk, a[jj]);
+      }
+    }
+  }
+  if (ok) {
+#pragma unroll
+    for (int c = 0; c < PIVB_NB; ++c)
+      if (i < b && c <= i) A[(j0 + i) + (j0 + c) * lda] = a[c];
+  }
+  __syncwarp();
+  return ok;
+}
+
 __device__ __forceinline__ void pivb_diag_inverse(const double *__restrict__ A, int lda, int j0, int b,
-                                                  double *__restrict__ W, int lane) {
+                                                  double *__restrict__ W, int lane, const double *__restrict__ rd) {
   // W (16 x 16, ld 16) <- inverse of the lower-triangular diagonal block A[j0.., j0..]
   // lane c computes column c by forward substitution
   if (lane < b) {
@@ -2358,11 +2400,14 @@ __device__ __forceinline__ void pivb_diag_inverse(const double *__restrict__ A, 
 #pragma unroll
     for (int i = 0; i < PIVB_NB; ++i) {
       if (i < b && i >= c) {
-        double sacc = (i == c) ? 1.0 : 0.0;
+        double s0 = (i == c) ? 1.0 : 0.0, s1 = 0.0;   // two chains
 #pragma unroll
         for (int k = 0; k < PIVB_NB; ++k)
-          if (k >= c && k < i) sacc = fma(-A[(j0 + i) + (int64_t)(j0 + k) * lda], x[k], sacc);
-        x[i] = sacc * frcp(A[(j0 + i) + (int64_t)(j0 + i) * lda]);
+          if (k >= c && k < i) {
+            if (k & 1) s1 = fma(-A[(j0 + i) + (j0 + k) * lda], x[k], s1);
+            else s0 = fma(-A[(j0 + i) + (j0 + k) * lda], x[k], s0);
+          }
+        x[i] = (s0 + s1) * rd[j0 + i];
       }
     }
 #pragma unroll
@@ -2373,6 +2418,7 @@ __device__ __forceinline__ void pivb_diag_inverse(const double *__restrict__ A, 
 __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict__ tasks, int *status) {
   extern __shared__ double sh[];
   __shared__ double W[PIVB_NB * PIVB_NB];
+  __shared__ double rd[PIVB_MAXN + PIVB_NB];   // 1 / l_kk
   __shared__ int s_fail;
   pdl_enter();
   const PivTask t = tasks[blockIdx.x];
@@ -2389,32 +2435,14 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
   for (int j0 = 0; j0 < n; j0 += PIVB_NB) {
     const int b = min(PIVB_NB, n - j0), j1 = j0 + b;
     if (warp == 0) {
-      for (int k = 0; k < b; ++k) {           // 16-column diagonal block, lane = row
-        const double d = (j0 + k < t.m) ? 1.0 : -1.0;
-        const double v = A[(j0 + k) + (int64_t)(j0 + k) * lda] * d;
-        if (!(v > 0.0) || !isfinite(v)) {
-          if (lane == 0) {
-            s_fail = 1;
-            if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
-          }
-          break;
+      if (!pivb_diag_chol(A, lda, j0, b, t.m, rd, lane)) {   // 16-column diagonal block
+        if (lane == 0) {
+          s_fail = 1;
+          if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
         }
-        const double lkk = sqrt(v), sc = d * frcp(lkk);
-        const int i = j0 + lane;
-        double lik = 0.0;
-        if (lane > k && lane < b) {
-          lik = A[i + (int64_t)(j0 + k) * lda] * sc;
-          A[i + (int64_t)(j0 + k) * lda] = lik;
-        }
-        __syncwarp();
-        if (lane == k) A[i + (int64_t)(j0 + k) * lda] = lkk;
-        if (lane > k && lane < b)
-          for (int jj = k + 1; jj <= lane; ++jj)
-            A[i + (int64_t)(j0 + jj) * lda] =
-                fma(-lik * d, A[(j0 + jj) + (int64_t)(j0 + k) * lda], A[i + (int64_t)(j0 + jj) * lda]);
-        __syncwarp();
+      } else {
+        pivb_diag_inverse(A, lda, j0, b, W, lane, rd);
       }
-      if (!s_fail) pivb_diag_inverse(A, lda, j0, b, W, lane);
     }
     __syncthreads();
     if (s_fail) return;
@@ -2459,7 +2487,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
     const int b = min(PIVB_NB, n - j0), j1 = j0 + b;
     // (a) T = X22 L21 (rows j1.., cols 0..b), parked transposed in A[j0 + c, j1 + row] (free upper part)
     if (warp == 0) {
-      pivb_diag_inverse(A, lda, j0, b, W, lane);
+      pivb_diag_inverse(A, lda, j0, b, W, lane, rd);
     } else {
       const int rows = n - j1;
       for (int q = tid - 32; q < rows * b; q += blockDim.x - 32) {
