@@ -2527,8 +2527,47 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
 // with X = L^{-1}, Y = U^{-1} of the already inverted trailing parts (scratch
 // TL, TU: n x 16 each).  Singular if |u_kk| <= 1e-14 max|A| (as k_pivot_lu).
 constexpr int PIVLU_MAXN = 148;
+// no-pivot LU of the b x b diagonal block at j0 by one warp, block in registers
+// (lane = row; the pivot row's entries by shuffles).  rd[j0 + k] <- 1 / u_kk.
+// Returns false when |u_kk| <= tiny (uniform across the warp).
+__device__ __forceinline__ bool lu_diag_factor(double *__restrict__ A, int lda, int j0, int b, double tiny,
+                                               double *__restrict__ rd, int lane) {
+  const int i = lane;
+  double a[PIVB_NB];
+#pragma unroll
+  for (int c = 0; c < PIVB_NB; ++c) a[c] = (i < b && c < b) ? A[(j0 + i) + (j0 + c) * lda] : 0.0;
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < PIVB_NB; ++k) {
+    if (k < b) {
+      const double piv = __shfl_sync(0xffffffffu, a[k], k);
+      if (!(fabs(piv) > tiny) || !isfinite(piv)) {
+        ok = false;
+        break;
+      }
+      const double rp = frcp(piv);
+      if (lane == 0) rd[j0 + k] = rp;
+      const double lik = (i > k) ? a[k] * rp : 0.0;
+      if (i > k) a[k] = lik;
+#pragma unroll
+      for (int jj = k + 1; jj < PIVB_NB; ++jj) {
+        const double ukj = __shfl_sync(0xffffffffu, a[jj], k);
+        if (jj < b && i > k) a[jj] = fma(-lik, ukj, a[jj]);
+      }
+    }
+  }
+  if (ok) {
+#pragma unroll
+    for (int c = 0; c < PIVB_NB; ++c)
+      if (i < b && c < b) A[(j0 + i) + (j0 + c) * lda] = a[c];
+  }
+  __syncwarp();
+  return ok;
+}
+
 __device__ __forceinline__ void lu_diag_inverses(const double *__restrict__ A, int lda, int j0, int b,
-                                                 double *__restrict__ WL, double *__restrict__ WU, int lane) {
+                                                 double *__restrict__ WL, double *__restrict__ WU, int lane,
+                                                 const double *__restrict__ rd) {
   // WL = L11^{-1} (unit lower, column c by lane c); WU = U11^{-1} (upper, row c by lane c)
   if (lane >= b) return;
   const int c = lane;
@@ -2554,13 +2593,13 @@ __device__ __forceinline__ void lu_diag_inverses(const double *__restrict__ A, i
   for (int j = 0; j < PIVB_NB; ++j) {
     double v = 0.0;
     if (j == c) {
-      v = frcp(A[(j0 + c) + (int64_t)(j0 + c) * lda]);
+      v = rd[j0 + c];
     } else if (j > c && j < b) {
       double sacc = 0.0;
 #pragma unroll
       for (int k = 0; k < PIVB_NB; ++k)
         if (k >= c && k < j) sacc = fma(x[k], A[(j0 + k) + (int64_t)(j0 + j) * lda], sacc);
-      v = -sacc * frcp(A[(j0 + j) + (int64_t)(j0 + j) * lda]);
+      v = -sacc * rd[j0 + j];
     }
     x[j] = v;   // reuse: x now holds row c of U11^{-1}
   }
@@ -2571,6 +2610,7 @@ __device__ __forceinline__ void lu_diag_inverses(const double *__restrict__ A, i
 __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restrict__ tasks, int *status) {
   extern __shared__ double sh[];
   __shared__ double WL[PIVB_NB * PIVB_NB], WU[PIVB_NB * PIVB_NB];
+  __shared__ double rd[PIVLU_MAXN + PIVB_NB];   // 1 / u_kk
   __shared__ int s_fail;
   __shared__ double s_amax[16];
   pdl_enter();
@@ -2600,29 +2640,14 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
   for (int j0 = 0; j0 < n; j0 += PIVB_NB) {
     const int b = min(PIVB_NB, n - j0), j1 = j0 + b;
     if (warp == 0) {
-      for (int k = 0; k < b; ++k) {
-        const double piv = A[(j0 + k) + (int64_t)(j0 + k) * lda];
-        if (!(fabs(piv) > tiny) || !isfinite(piv)) {
-          if (lane == 0) {
-            s_fail = 1;
-            if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
-          }
-          break;
+      if (!lu_diag_factor(A, lda, j0, b, tiny, rd, lane)) {
+        if (lane == 0) {
+          s_fail = 1;
+          if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
         }
-        const double rp = frcp(piv);
-        double lik = 0.0;
-        if (lane > k && lane < b) {
-          lik = A[(j0 + lane) + (int64_t)(j0 + k) * lda] * rp;
-          A[(j0 + lane) + (int64_t)(j0 + k) * lda] = lik;
-        }
-        __syncwarp();
-        if (lane > k && lane < b)
-          for (int jj = k + 1; jj < b; ++jj)
-            A[(j0 + lane) + (int64_t)(j0 + jj) * lda] =
-                fma(-lik, A[(j0 + k) + (int64_t)(j0 + jj) * lda], A[(j0 + lane) + (int64_t)(j0 + jj) * lda]);
-        __syncwarp();
+      } else {
+        lu_diag_inverses(A, lda, j0, b, WL, WU, lane, rd);
       }
-      if (!s_fail) lu_diag_inverses(A, lda, j0, b, WL, WU, lane);
     }
     __syncthreads();
     if (s_fail) return;
@@ -2682,7 +2707,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
     //     TL[i][c] = sum_{k=j1}^{i} X22[i][k] L21[k][c]   (X22 unit lower, inverted)
     //     TU[j][c] = sum_{k=j1}^{j} U12[c][k] Y22[k][j]   (Y22 upper, inverted)
     if (warp == 0) {
-      lu_diag_inverses(A, lda, j0, b, WL, WU, lane);
+      lu_diag_inverses(A, lda, j0, b, WL, WU, lane, rd);
     } else {
       for (int q = tid - 32; q < 2 * rest * b; q += blockDim.x - 32) {
         if (q < rest * b) {
