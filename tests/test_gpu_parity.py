@@ -171,6 +171,42 @@ def test_refactor_new_values_and_determinism(L):
     h.close()
 
 
+@pytest.mark.parametrize("name,dims", [("cfg2", (64, 64)), ("cfg3", (32, 32, 32)), ("cfg5", (64, 64))])
+def test_recorded_factorization_graph(L, name, dims):
+    """Re-factorizations replay one recorded CUDA graph of the whole sweep
+    (DESIGN.md 6b): bitwise the result of the synchronised sweep; new values
+    whose ranks differ drop the graph and redo the synchronised sweep."""
+    p = make_problem(name, dims=dims)
+    vals = torch.tensor(p.values, device="cuda")
+    h = L.analyze_problem(p)
+    xs, graph = [], []
+    for _ in range(4):          # sync sweep, predicted sweep, capture + launch, launch
+        h.factor(vals)
+        xs.append(gpu_apply(h, p.b))
+        graph.append(h.stats()["factor_graph"])
+    st = h.stats()
+    assert graph == [False, False, True, True] and st["factor_graph_captures"] == 1
+    assert st["factor_graph_launches"] >= 2 and st["factor_graph_failures"] == 0
+    for x in xs[1:]:
+        assert np.array_equal(x, xs[0])
+    # values scaled by 2: same ranks (scale-invariant rule) -> the graph replays
+    h.factor(2.0 * vals)
+    x2 = gpu_apply(h, p.b)
+    assert h.stats()["factor_graph"] and relerr(2.0 * x2, xs[0]) <= 1e-12
+    # a different operator on the same pattern: ranks change -> synchronised sweep
+    rows = np.repeat(np.arange(p.n), np.diff(p.row_ptr))
+    vq = p.values.copy()
+    vq[rows == p.col_idx] *= 1.5       # stronger diagonal (symmetry kept)
+    h.factor(torch.tensor(vq, device="cuda"))
+    st2 = h.stats()
+    h2 = L.analyze_problem(p)
+    h2.factor(torch.tensor(vq, device="cuda"))
+    assert np.array_equal(gpu_apply(h, p.b), gpu_apply(h2, p.b))
+    assert st2["rank_prediction_misses"] >= 1 or st2["factor_graph"]
+    h.close()
+    h2.close()
+
+
 def test_identity_and_natural_order(L):
     n = 64
     rp = np.arange(n + 1, dtype=np.int64)
