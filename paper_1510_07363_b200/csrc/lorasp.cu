@@ -305,8 +305,13 @@ struct lorasp_ctx {
   std::vector<int> ap_wave_begin;  // in recs order (factor order), per wave
   std::vector<int> ap_part_begin;  // split apply: parts of wave w in [ap_part_begin[w], ap_part_begin[w+1])
   std::vector<char> ap_wave_split; // wave uses the split kernels
+  // per-wave shared-memory footprint of the fused kernels (waves of small
+  // records run many more CTAs per SM than the global worst case allows)
+  std::vector<int> ap_wave_ch;
+  std::vector<size_t> ap_wave_fsm, ap_wave_bsm;
   DevBuf d_apparts, d_upart;
   bool no_split_apply = getenv("LORASP_NO_SPLIT_APPLY") != nullptr;
+  bool no_wave_smem = getenv("LORASP_APPLY_GLOBAL_SMEM") != nullptr;   // A/B: one footprint for all waves
   std::vector<double> ap_wave_flops, ap_wave_bytes;  // per wave, one pass (fwd or bwd)
   size_t ap_fwd_smem = 0, ap_bwd_smem = 0;
   int ap_chunk = 0;
@@ -2198,6 +2203,55 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
     h->ap_chunk = (int)ch;
     h->ap_fwd_smem = fwd * 8 + 2 * ch * 8 + 64;
     h->ap_bwd_smem = bwd * 8 + 2 * ch * 8 + 64;
+    const size_t nwv = h->ap_wave_begin.size() - 1;
+    h->ap_wave_ch.assign(nwv, (int)ch);
+    h->ap_wave_fsm.assign(nwv, h->ap_fwd_smem);
+    h->ap_wave_bsm.assign(nwv, h->ap_bwd_smem);
+    if (!h->no_wave_smem)
+      for (size_t w = 0; w < nwv; ++w) {
+        size_t wf = 0, wb = 0, wc = 2;
+        for (int q = h->ap_wave_begin[w]; q < h->ap_wave_begin[w + 1]; ++q) {
+          const NodeRec &rc = h->recs[q];
+          const size_t n = rc.m + rc.r;
+          wf = std::max(wf, (size_t)(rc.m + n + rc.W + 2));
+          wb = std::max(wb, (size_t)(n + rc.W + 2));
+          // one stage holds a whole part of the record (L^{-1} columns or Z)
+          wc = std::max(wc, std::max<size_t>(2 * (size_t)rc.ld + 2,
+                                             (size_t)rc.ld * std::max<size_t>(n, (size_t)rc.W)));
+        }
+        wc = std::min(wc, ch);
+        // wide waves: smaller stages so that several CTAs share an SM (each
+        // CTA's chain of bulk copies is latency bound; more of them in flight)
+        {
+          const int cnt = h->ap_wave_begin[w + 1] - h->ap_wave_begin[w];
+          const int target = std::min(5, (cnt + 147) / 148);
+          size_t ldmax = 2;
+          for (int q = h->ap_wave_begin[w]; q < h->ap_wave_begin[w + 1]; ++q)
+            ldmax = std::max(ldmax, (size_t)h->recs[q].ld);
+          if (target > 2) {
+            const size_t room = (size_t)SMEM_LIMIT / target;
+            const size_t fix = std::max(wf, wb) * 8 + 256;
+            if (room > fix) wc = std::min(wc, std::max<size_t>((room - fix) / 16, 2 * ldmax + 2));
+          }
+        }
+        wc = (wc + 1) & ~size_t(1);
+        if (h->debug) {
+          double avg = 0;
+          size_t mx = 0;
+          for (int q = h->ap_wave_begin[w]; q < h->ap_wave_begin[w + 1]; ++q) {
+            const NodeRec &rc = h->recs[q];
+            const size_t e = (size_t)rc.ld * (rc.m + rc.r + rc.W);
+            avg += e;
+            mx = std::max(mx, e);
+          }
+          const int cnt = h->ap_wave_begin[w + 1] - h->ap_wave_begin[w];
+          fprintf(stderr, "[lorasp] apply wave %zu: %d nodes, record doubles avg %.0f max %zu, chunk %zu, smem %zu / %zu\n",
+                  w, cnt, avg / cnt, mx, wc, wf * 8 + 2 * wc * 8 + 64, wb * 8 + 2 * wc * 8 + 64);
+        }
+        h->ap_wave_ch[w] = (int)wc;
+        h->ap_wave_fsm[w] = wf * 8 + 2 * wc * 8 + 64;
+        h->ap_wave_bsm[w] = wb * 8 + 2 * wc * 8 + 64;
+      }
   }
   h->d_apnodes.ensure(std::max<size_t>(1, an.size()) * sizeof(ApNode), st);
   h->d_apsegs.ensure(std::max<size_t>(1, as.size()) * sizeof(ApSeg), st);
@@ -2224,8 +2278,8 @@ void apply_wave(lorasp_ctx *h, int w, bool fwd, cudaStream_t s) {
   const int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1];
   double *vec = h->d_vec.as<double>();
   if (!h->ap_wave_split[w]) {
-    if (fwd) launch_k(k_apply_fwd, b1 - b0, 256, h->ap_fwd_smem, s, nodes + b0, segs, vec, h->ap_chunk);
-    else launch_k(k_apply_bwd, b1 - b0, 256, h->ap_bwd_smem, s, nodes + b0, segs, vec, h->ap_chunk);
+    if (fwd) launch_k(k_apply_fwd, b1 - b0, 256, h->ap_wave_fsm[w], s, nodes + b0, segs, vec, h->ap_wave_ch[w]);
+    else launch_k(k_apply_bwd, b1 - b0, 256, h->ap_wave_bsm[w], s, nodes + b0, segs, vec, h->ap_wave_ch[w]);
     return;
   }
   const ApPart *parts = h->d_apparts.as<ApPart>() + h->ap_part_begin[w];
@@ -2264,6 +2318,9 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
     sig.push_back((int64_t)(intptr_t)h->d_vec.p);
     sig.insert(sig.end(), h->ap_part_begin.begin(), h->ap_part_begin.end());
     sig.insert(sig.end(), h->ap_wave_split.begin(), h->ap_wave_split.end());
+    sig.insert(sig.end(), h->ap_wave_ch.begin(), h->ap_wave_ch.end());
+    for (size_t v : h->ap_wave_fsm) sig.push_back((int64_t)v);
+    for (size_t v : h->ap_wave_bsm) sig.push_back((int64_t)v);
     sig.push_back((int64_t)(intptr_t)h->d_apparts.p);
     sig.push_back((int64_t)(intptr_t)h->d_upart.p);
     if (h->ap_graph && sig != h->ap_graph_sig) {
