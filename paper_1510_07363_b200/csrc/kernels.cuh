@@ -2910,50 +2910,59 @@ struct ColStream {
 __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ nodes,
                                                    const ApSeg *__restrict__ segs,
                                                    double *__restrict__ vec, int chunk_doubles) {
-  pdl_enter();
+  // PDL: the record (written by the factorization) is fetched before waiting
+  // for the previous wave; only the vector depends on it
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(16) double sh[];
   __shared__ __align__(8) uint64_t bars[2];
   const ApNode nd = nodes[blockIdx.x];
   const int n = nd.m + nd.r;
-  if (n == 0) return;
+  if (n == 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   double *stage0 = sh, *stage1 = sh + chunk_doubles;
   double *rhs = stage1 + chunk_doubles;  // m
   double *dy = rhs + nd.m;               // n (accumulates y)
   double *zo = dy + n;                   // W: Z^T D y, written back once at the end
+  const int ld = nd.ld;
+  const int cc = max(1, chunk_doubles / ld);
+  const double *Z = nd.F + nd.zf_off;
+  const int na = (nd.m + cc - 1) / cc;   // L^{-1}[:, :m] chunks, then Z chunks
+  const int nb = (nd.W + cc - 1) / cc;
+  const int ntot = na + nb;
+  auto issue = [&](int c) {
+    const double *src;
+    int c0, c1;
+    if (c < na) {
+      c0 = c * cc;
+      c1 = min(nd.m, c0 + cc);
+      src = nd.F + (int64_t)c0 * ld;
+    } else {
+      c0 = (c - na) * cc;
+      c1 = min(nd.W, c0 + cc);
+      src = Z + (int64_t)c0 * ld;
+    }
+    const uint32_t bytes = (uint32_t)((int64_t)(c1 - c0) * ld * 8);
+    fence_proxy_async();
+    mbar_expect_tx(&bars[c & 1], bytes);
+    bulk_g2s((c & 1) ? stage1 : stage0, src, bytes, &bars[c & 1]);
+  };
   if (tid == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (ntot > 0) issue(0);
+    if (ntot > 1) issue(1);
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int i = tid; i < nd.m; i += blockDim.x) rhs[i] = vec[nd.off_s + i];
   for (int i = tid; i < n; i += blockDim.x) dy[i] = 0.0;
   __syncthreads();
-  const int ld = nd.ld;
-  int cc = max(1, chunk_doubles / ld);
-  // ---- y = L^{-1}[:, :m] rhs ----
-  ColStream A{nd.F, ld, nd.m, cc, {stage0, stage1}, bars};
-  const int na = A.nchunks();
-  const double *Z = nd.F + nd.zf_off;
-  ColStream B{Z, ld, nd.W, cc, {stage0, stage1}, bars};
-  const int nb = B.nchunks();
-  const int ntot = na + nb;
-  if (tid == 0) {
-    if (ntot > 0) (0 < na ? A : B).issue(0 < na ? 0 : 0);
-  }
+  // ---- y = L^{-1}[:, :m] rhs, then Z^T D y ----
   for (int c = 0; c < ntot; ++c) {
-    if (tid == 0 && c + 1 < ntot) {
-      if (c + 1 < na) A.issue(c + 1);
-      else {
-        // B chunk index (c+1-na) must land in stage (c+1)&1: reuse issue with a shifted parity
-        const int cb = c + 1 - na;
-        const int c0 = cb * cc, c1 = min(nd.W, c0 + cc);
-        uint32_t bytes = (uint32_t)((int64_t)(c1 - c0) * ld * 8);
-        fence_proxy_async();
-        mbar_expect_tx(&bars[(c + 1) & 1], bytes);
-        bulk_g2s(((c + 1) & 1) ? stage1 : stage0, Z + (int64_t)c0 * ld, bytes, &bars[(c + 1) & 1]);
-      }
-    }
+    if (tid == 0 && c >= 1 && c + 1 < ntot) issue(c + 1);   // stage (c+1)&1 freed at the end of c-1
     mbar_wait(&bars[c & 1], (c >> 1) & 1);
     const double *buf = (c & 1) ? stage1 : stage0;
     if (c < na) {
@@ -2997,27 +3006,19 @@ __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ no
 __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ nodes,
                                                    const ApSeg *__restrict__ segs,
                                                    double *__restrict__ vec, int chunk_doubles) {
-  pdl_enter();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // PDL: record fetched before the wait
   extern __shared__ __align__(16) double sh[];
   __shared__ __align__(8) uint64_t bars[2];
   const ApNode nd = nodes[blockIdx.x];
   const int n = nd.m + nd.r;
-  if (n == 0) return;
+  if (n == 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    return;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   double *stage0 = sh, *stage1 = sh + chunk_doubles;
   double *u = stage1 + chunk_doubles;  // n
   double *xt = u + n;                  // W
-  if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int sg = 0; sg < nd.nseg; ++sg) {
-    const ApSeg S = segs[nd.seg0 + sg];
-    for (int j = tid; j < S.w; j += blockDim.x) xt[S.zc + j] = vec[S.voff + j];
-  }
-  for (int i = tid; i < n; i += blockDim.x) u[i] = nd.y[i];
-  __syncthreads();
   const int ld = nd.ld;
   int cc = max(1, chunk_doubles / ld);
   const double *Z = nd.F + nd.zb_off;
@@ -3042,9 +3043,22 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
     mbar_expect_tx(&bars[c & 1], bytes);
     bulk_g2s((c & 1) ? stage1 : stage0, src, bytes, &bars[c & 1]);
   };
-  if (tid == 0 && ntot > 0) issue(0);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (ntot > 0) issue(0);
+    if (ntot > 1) issue(1);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int sg = 0; sg < nd.nseg; ++sg) {
+    const ApSeg S = segs[nd.seg0 + sg];
+    for (int j = tid; j < S.w; j += blockDim.x) xt[S.zc + j] = vec[S.voff + j];
+  }
+  for (int i = tid; i < n; i += blockDim.x) u[i] = nd.y[i];
+  __syncthreads();
   for (int c = 0; c < ntot; ++c) {
-    if (tid == 0 && c + 1 < ntot) issue(c + 1);
+    if (tid == 0 && c >= 1 && c + 1 < ntot) issue(c + 1);   // stage (c+1)&1 freed at the end of c-1
     mbar_wait(&bars[c & 1], (c >> 1) & 1);
     const double *buf = (c & 1) ? stage1 : stage0;
     if (c < nb) {
