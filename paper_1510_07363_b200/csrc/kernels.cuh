@@ -35,9 +35,11 @@ namespace lorasp {
 // cudaLaunchAttributeProgrammaticStreamSerialization): every such kernel lets
 // its successor be scheduled at once and waits for its predecessor's memory
 // before touching anything.  Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_trigger();
+  pdl_wait();
 }
 
 // ---------------------------------------------------------------- copies ----
@@ -52,8 +54,9 @@ struct CopyTask {
 };
 
 __global__ void __launch_bounds__(256) k_copy(const CopyTask *__restrict__ tasks) {
-  pdl_enter();
+  pdl_trigger();
   const CopyTask t = tasks[blockIdx.x];
+  pdl_wait();   // task descriptors are static: read before the wait
   if (t.rows <= 0 || t.cols <= 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (t.mode != 0) {
@@ -318,8 +321,9 @@ __global__ void __launch_bounds__(128, 4) k_gemm2(const GemmTask *__restrict__ t
                                                 const GemmSeg *__restrict__ segs) {
   __shared__ __align__(16) double As[2][G2K][GT + 1];
   __shared__ __align__(16) double Bs[2][G2K][GT + 1];
-  pdl_enter();
+  pdl_trigger();
   const GemmTask t = tasks[blockIdx.x];
+  pdl_wait();   // task descriptors are static: read before the wait
   if (t.tnw == 32) gemm2_tile<4>(t, segs, As, Bs);
   else gemm2_tile<8>(t, segs, As, Bs);
 }
@@ -1036,8 +1040,9 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
   }
   __shared__ double s_red[32];
   __shared__ double d[MR + 8], e[MR + 8], tau[MR + 8];
-  pdl_enter();
+  pdl_trigger();
   const EigTask t = tasks[blockIdx.x];
+  pdl_wait();   // task descriptors are static: read before the wait
   const int m = t.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double *out = t.work + 6 * (int64_t)m * m;
@@ -1542,8 +1547,9 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
   __shared__ double s_red[32];
   __shared__ double s_bc[8];
   __shared__ int s_int[4];
-  pdl_enter();
+  pdl_trigger();
   const EigTask t = tasks[blockIdx.x];
+  pdl_wait();   // task descriptors are static: read before the wait
   const int m = t.m;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int ml = m > 512 ? m : 512;  // lam doubles as p-partials scratch during phase 1
@@ -1925,9 +1931,10 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
 // CTA per chunk of vectors (chunk c: k in [c nb, (c+1) nb) ∩ [0, r)), each
 // chunk's LU / right-hand sides in shared memory; grid = nodes x nch.
 __global__ void __launch_bounds__(256) k_invit_multi(const EigTask *__restrict__ tasks, int nch, int smem_cap_doubles) {
-  pdl_enter();
+  pdl_trigger();
   extern __shared__ double sh[];
   const EigTask t = tasks[blockIdx.x / nch];
+  pdl_wait();   // task descriptors are static: read before the wait
   const int c = blockIdx.x % nch;
   const int m = t.m;
   const int r = *t.rank_out;
@@ -2077,9 +2084,10 @@ __global__ void __launch_bounds__(512, 1) k_orth_cl(const EigTask *__restrict__ 
 // contiguous packed segments); grid = nodes x nch.
 template <int Q, int NV>
 __global__ void __launch_bounds__(512) k_backtr_multi(const EigTask *__restrict__ tasks, int nch, int smem_cap_doubles) {
-  pdl_enter();
+  pdl_trigger();
   extern __shared__ double sh[];
   const EigTask t = tasks[blockIdx.x / nch];
+  pdl_wait();   // task descriptors are static: read before the wait
   const int c = blockIdx.x % nch;
   const int m = t.m, r = *t.rank_out;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -2161,9 +2169,10 @@ struct PivTask {
 
 __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks,
                                                int smem_cap_doubles, int *status) {
-  pdl_enter();
+  pdl_trigger();
   extern __shared__ double sh[];
   const PivTask t = tasks[blockIdx.x];
+  pdl_wait();   // task descriptors are static: read before the wait
   const int n = t.m + t.r;
   if (n == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -2240,9 +2249,10 @@ __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks
 // in region 0 (global).
 __global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ tasks, int smem_cap_doubles,
                                                   int *status) {
-  pdl_enter();
+  pdl_trigger();
   extern __shared__ double sh[];
   const PivTask t = tasks[blockIdx.x];
+  pdl_wait();   // task descriptors are static: read before the wait
   const int n = t.m + t.r;
   if (n == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -2420,8 +2430,9 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
   __shared__ double W[PIVB_NB * PIVB_NB];
   __shared__ double rd[PIVB_MAXN + PIVB_NB];   // 1 / l_kk
   __shared__ int s_fail;
-  pdl_enter();
+  pdl_trigger();
   const PivTask t = tasks[blockIdx.x];
+  pdl_wait();   // task descriptors are static: read before the wait
   const int n = t.m + t.r;
   if (n == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -2613,8 +2624,9 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
   __shared__ double rd[PIVLU_MAXN + PIVB_NB];   // 1 / u_kk
   __shared__ int s_fail;
   __shared__ double s_amax[16];
-  pdl_enter();
+  pdl_trigger();
   const PivTask t = tasks[blockIdx.x];
+  pdl_wait();   // task descriptors are static: read before the wait
   const int n = t.m + t.r;
   if (n == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -2773,8 +2785,9 @@ __global__ void __launch_bounds__(256) k_pivdiag(const PivDiagTask *__restrict__
   __shared__ double A[64 * 65];
   __shared__ double tmp[64];
   __shared__ int s_fail;
-  pdl_enter();
+  pdl_trigger();
   const PivDiagTask t = tasks[blockIdx.x];
+  pdl_wait();   // task descriptors are static: read before the wait
   const int b = t.b, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int la = 65;
   double *K = t.F + t.j0 + (int64_t)t.j0 * t.ld;
