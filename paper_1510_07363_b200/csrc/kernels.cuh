@@ -1867,6 +1867,10 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
     } else if (REG || m <= 64) {
       // register-resident vectors (REG: m <= 128, 16 warps; generic: m <= 64, 8 warps)
       if (REG) {
+        if (per_w > 8) {   // 8-warp launch with r > 64 (only from a wrong rank prediction)
+          if (tid == 0 && atomicCAS(&status[0], 0, -4) == 0) status[1] = t.node;
+          return;
+        }
         if (per_w > 4) orth_backtr<4, 8, true>(t.V, A, tau, m, r, s_zb, t.dbg);
         else if (per_w > 2) orth_backtr<4, 4, true>(t.V, A, tau, m, r, s_zb, t.dbg);
         else if (per_w > 1) orth_backtr<4, 2, true>(t.V, A, tau, m, r, s_zb, t.dbg);

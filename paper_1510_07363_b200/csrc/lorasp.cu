@@ -386,6 +386,7 @@ struct lorasp_ctx {
   int fg_captures = 0, fg_failures = 0;
   int64_t fg_launches = 0;
   int eig_clmax_hint = 0, eig_bigmax_hint = 0, eig_regmax_hint = 0;   // the same for the eigen-solver classes
+  int eig_rank_hint = -1;   // largest predicted rank of the wave (rank-predicted sweep), -1 unknown
   bool eig_split_classes = getenv("LORASP_EIG_SPLIT_CLASSES") != nullptr;   // A/B: one launch per tile class
 };
 
@@ -480,13 +481,25 @@ static void launch_tridiag_cl(cudaStream_t st, const EigTask *dt, int n, int cls
 
 // Register-tile eigen path for m <= 128: tridiagonalisation (tile class c:
 // 32 / 64 / 128 rows) then k_eig_t<true>.
-static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps, int *dstatus) {
+static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps, int *dstatus,
+                          int rank_hint = -1) {
   if (c == 0) launch_k(k_tridiag_reg<false, 1, 4, 8>, (unsigned)n, 128, 0, st, ds, eps, (long long *)nullptr);
   else if (c == 1) launch_k(k_tridiag_reg<false, 2, 8, 8>, (unsigned)n, 256, 0, st, ds, eps, (long long *)nullptr);
   else launch_k(k_tridiag_reg<false>, (unsigned)n, EIG_REG_THREADS, 0, st, ds, eps, (long long *)nullptr);
   CK(cudaGetLastError());
-  launch_k(k_eig_t<true>, (unsigned)n, c == 2 ? EIG_REG_THREADS : 256, EIG_REG_SMEM, st, ds, eps,
-           (int)(EIG_REG_SMEM / 8), dstatus);
+  // waves wider than the GPU are throughput bound: for m <= 64 half the shared
+  // memory (still room for ~30 inverse-iteration vectors per batch) lets two
+  // CTAs share an SM
+  static const bool narrow_off = getenv("LORASP_EIG_WIDE_FULL_SMEM") != nullptr;
+  static const bool narrow_force = getenv("LORASP_EIG_FORCE_NARROW") != nullptr;   // test hook
+  // (m <= 128 keeps 16 warps: r may exceed 64 = 8 vectors per warp x 8 warps;
+  // the 8-warp form would need the rank before the launch, which only the
+  // rank-predicted sweep has, and the two schedules must agree bit for bit)
+  (void)rank_hint;
+  const bool narrow = !narrow_off && (n > 148 || narrow_force) && c <= 1;
+  const size_t esm = narrow ? (c <= 1 ? EIG_REG_SMEM / 2 : (size_t)110 * 1024) : EIG_REG_SMEM;
+  const int eth = (c == 2 && !narrow) ? EIG_REG_THREADS : 256;
+  launch_k(k_eig_t<true>, (unsigned)n, eth, esm, st, ds, eps, (int)(esm / 8), dstatus);
   CK(cudaGetLastError());
   return 2;
 }
@@ -694,7 +707,9 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
       rs = h->stream_eig;
     }
     for (int c = 0; c < 3; ++c)
-      if (ds[c]) h->launches_factor += launch_eig_reg(rs, ds[c], (int)rc[c].size(), c, h->plan.eps, h->d_status.as<int>());
+      if (ds[c])
+        h->launches_factor += launch_eig_reg(rs, ds[c], (int)rc[c].size(), c, h->plan.eps, h->d_status.as<int>(),
+                                             h->eig_rank_hint);
     if (reg_fork) CK(cudaEventRecord(h->ev_ej, h->stream_eig));
   }
   std::vector<EigTask> post;
@@ -1457,6 +1472,13 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           cudaEventCreate(&dbg_e0);
           cudaEventCreate(&dbg_e1);
           cudaEventRecord(dbg_e0, st);
+        }
+        h->eig_rank_hint = -1;
+        if (replay) {
+          int mx = 0;
+          for (int c : comp)
+            if (own(c)) mx = std::max(mx, h->rank_cache[i][c]);
+          h->eig_rank_hint = mx;
         }
         launch_eig(h, et, de, max_m, cap);
         enqueue_split_part1();
