@@ -386,7 +386,7 @@ struct lorasp_ctx {
   int fg_captures = 0, fg_failures = 0;
   int64_t fg_launches = 0;
   int eig_clmax_hint = 0, eig_bigmax_hint = 0, eig_regmax_hint = 0;   // the same for the eigen-solver classes
-  int eig_rank_hint = -1;   // largest predicted rank of the wave (rank-predicted sweep), -1 unknown
+  int eig_reg_wave_n = 0;   // distributed: register-tile eigen tasks of the whole wave
   bool eig_split_classes = getenv("LORASP_EIG_SPLIT_CLASSES") != nullptr;   // A/B: one launch per tile class
 };
 
@@ -481,8 +481,9 @@ static void launch_tridiag_cl(cudaStream_t st, const EigTask *dt, int n, int cls
 
 // Register-tile eigen path for m <= 128: tridiagonalisation (tile class c:
 // 32 / 64 / 128 rows) then k_eig_t<true>.
-static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps, int *dstatus,
-                          int rank_hint = -1) {
+// wave_n: register-tile tasks in the whole wave (all ranks), which decides the
+// launch shape so that a distributed sweep runs the single-GPU kernels
+static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps, int *dstatus, int wave_n) {
   if (c == 0) launch_k(k_tridiag_reg<false, 1, 4, 8>, (unsigned)n, 128, 0, st, ds, eps, (long long *)nullptr);
   else if (c == 1) launch_k(k_tridiag_reg<false, 2, 8, 8>, (unsigned)n, 256, 0, st, ds, eps, (long long *)nullptr);
   else launch_k(k_tridiag_reg<false>, (unsigned)n, EIG_REG_THREADS, 0, st, ds, eps, (long long *)nullptr);
@@ -495,8 +496,7 @@ static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps
   // (m <= 128 keeps 16 warps: r may exceed 64 = 8 vectors per warp x 8 warps;
   // the 8-warp form would need the rank before the launch, which only the
   // rank-predicted sweep has, and the two schedules must agree bit for bit)
-  (void)rank_hint;
-  const bool narrow = !narrow_off && (n > 148 || narrow_force) && c <= 1;
+  const bool narrow = !narrow_off && (wave_n > 148 || narrow_force) && c <= 1;
   const size_t esm = narrow ? (c <= 1 ? EIG_REG_SMEM / 2 : (size_t)110 * 1024) : EIG_REG_SMEM;
   const int eth = (c == 2 && !narrow) ? EIG_REG_THREADS : 256;
   launch_k(k_eig_t<true>, (unsigned)n, eth, esm, st, ds, eps, (int)(esm / 8), dstatus);
@@ -709,7 +709,7 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
     for (int c = 0; c < 3; ++c)
       if (ds[c])
         h->launches_factor += launch_eig_reg(rs, ds[c], (int)rc[c].size(), c, h->plan.eps, h->d_status.as<int>(),
-                                             h->eig_rank_hint);
+                                             h->eig_reg_wave_n > 0 ? h->eig_reg_wave_n : (int)small.size());
     if (reg_fork) CK(cudaEventRecord(h->ev_ej, h->stream_eig));
   }
   std::vector<EigTask> post;
@@ -1376,7 +1376,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         int64_t soff_sig = 0, xoff = 0;
         int max_m = 0;
         double f_gram = 0, b_gram = 0, f_eig = 0, b_eig = 0;
-        h->eig_clmax_hint = h->eig_bigmax_hint = h->eig_regmax_hint = 0;
+        h->eig_clmax_hint = h->eig_bigmax_hint = h->eig_regmax_hint = h->eig_reg_wave_n = 0;
         if (dist) {
           CK(cudaMemsetAsync(h->d_ranks.p, 0, comp.size() * sizeof(int), st));
           // launch-shape choices from the whole wave, so that every rank runs
@@ -1385,6 +1385,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
             const int mc = m[c];
             if (mc >= EIG_REG_MIN && mc <= EIG_REG_M) {
               h->eig_regmax_hint = std::max(h->eig_regmax_hint, mc);
+              ++h->eig_reg_wave_n;
               continue;
             }
             if (!eig_cl_disabled && eig_cl_class(mc)) h->eig_clmax_hint = std::max(h->eig_clmax_hint, mc);
@@ -1472,13 +1473,6 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           cudaEventCreate(&dbg_e0);
           cudaEventCreate(&dbg_e1);
           cudaEventRecord(dbg_e0, st);
-        }
-        h->eig_rank_hint = -1;
-        if (replay) {
-          int mx = 0;
-          for (int c : comp)
-            if (own(c)) mx = std::max(mx, h->rank_cache[i][c]);
-          h->eig_rank_hint = mx;
         }
         launch_eig(h, et, de, max_m, cap);
         enqueue_split_part1();
@@ -2990,7 +2984,7 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        launch_eig_reg(0, de, 1, m <= 32 ? 0 : (m <= 64 ? 1 : 2), eps, dst);
+        launch_eig_reg(0, de, 1, m <= 32 ? 0 : (m <= 64 ? 1 : 2), eps, dst, 1);
         cudaEventRecord(e1);
         if (ddbg) {
           float ms = 0;

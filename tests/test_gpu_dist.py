@@ -42,6 +42,7 @@ def _single(L, p):
     ("cfg2", (128, 128), 8),
     ("cfg5", (64, 64), 4),      # general (LU) path
     ("cfg3", (32, 32, 32), 4),  # 3D: cluster eigen-solver classes and split pivots
+    ("cfg2", (512, 512), 2),    # waves wider than the GPU (launch shapes of the whole wave)
 ])
 def test_virtual_ranks_match_single_gpu(L, name, dims, world):
     from paper_1510_07363_b200.dist import VirtualGroup, factor_virtual
