@@ -208,10 +208,13 @@ def _cluster_level(u: Node) -> Tuple[int, int]:
 
 class _Factorizer:
     def __init__(self, n, row_ptr, col_idx, values, coords, depth, eps,
-                 order="coloured", symmetric_stack=False, trace=False):
+                 order="coloured", symmetric_stack=False, trace=False, compressor="svd"):
         self.n = n
         self.l = depth
         self.eps = float(eps)
+        if compressor not in ("svd", "rrqr"):
+            raise ValueError(compressor)
+        self.compressor = compressor
         self.symmetric_stack = symmetric_stack
         self.want_trace = trace
         coords = np.asarray(coords, dtype=np.float64).reshape(n, -1)
@@ -342,15 +345,19 @@ class _Factorizer:
         A = [self.M.get((s, p), np.zeros((self.size[p], m))) for p in partners]
         B = [self.M.get((p, s), np.zeros((m, self.size[p]))).T for p in partners]
         stack = np.vstack(A if self.symmetric_stack else A + B)
-        # thin SVD when the stack has >= m rows (V is m x m either way)
-        _, sig, Vt = np.linalg.svd(stack, full_matrices=stack.shape[0] < m)
-        sig0 = float(sig[0]) if sig.size else 0.0
-        if sig0 == 0.0:
-            r = 0                                   # reading Z4
-        elif self.eps == 0.0:
-            r = m                                   # reading Z3: nothing is truncated
+        if self.compressor == "rrqr":
+            r, sig, V = self._rrqr(stack, m)
         else:
-            r = int(np.count_nonzero(sig >= self.eps * sig0))   # Eq. cutOff1, ties kept (Z5)
+            # thin SVD when the stack has >= m rows (V is m x m either way)
+            _, sig, Vt = np.linalg.svd(stack, full_matrices=stack.shape[0] < m)
+            sig0 = float(sig[0]) if sig.size else 0.0
+            if sig0 == 0.0:
+                r = 0                                   # reading Z4
+            elif self.eps == 0.0:
+                r = m                                   # reading Z3: nothing is truncated
+            else:
+                r = int(np.count_nonzero(sig >= self.eps * sig0))   # Eq. cutOff1, ties kept (Z5)
+            V = Vt[:r].T                                # m x r
         self.rank[(i, c)] = r
         self.sigma[(i, c)] = sig
         if self.want_trace:
@@ -362,7 +369,6 @@ class _Factorizer:
         self.size[b] = self.size[P] = r
         if r == 0:
             return
-        V = Vt[:r].T                                # m x r
         for p, Ak, Bk in zip(partners, A, B):
             Rk = Ak @ V                             # A_k ~= R_k V^T
             Qk = Bk @ V                             # B_k ~= Q_k V^T
@@ -374,6 +380,35 @@ class _Factorizer:
         self._set(b, P, -I)                         # rule 5: b <-> P(b) with -I_r
         self._set(P, b, -I.copy())
         # RHS(b) = RHS(P(b)) = 0 (Eq. rhszero) -- applied in SetRHS
+
+    def _rrqr(self, stack: np.ndarray, m: int):
+        """SURVEY 8(f) f1, the paper's proposed cheaper compressor (P:l.616,
+        P:l.840): column-pivoted (Businger-Golub) QR  stack P = Q R,  truncated
+        at the first k with |R_kk| < eps |R_00| (reading F1: the
+        rank-revealing analogue of Eq. cutOff1); the kept row space is that of
+        R[:r, :] P^T, returned as an orthonormal basis V (m x r).  Any basis of
+        that span gives the same preconditioner (the black-node coordinates
+        only change by an r x r rotation)."""
+        Rq, piv = sla.qr(stack, mode="r", pivoting=True)
+        d = np.abs(np.diag(Rq))
+        sig = np.zeros(m)
+        sig[:d.size] = d
+        if d.size == 0 or d[0] == 0.0:
+            return 0, sig, np.zeros((m, 0))          # reading Z4
+        if self.eps == 0.0:
+            r = m                                    # reading Z3
+        else:
+            small = np.nonzero(d < self.eps * d[0])[0]
+            r = int(small[0]) if small.size else d.size
+        if r == 0:
+            return 0, sig, np.zeros((m, 0))
+        W = np.zeros((m, r))
+        if r <= d.size:
+            W[piv, :] = Rq[:r, :].T                  # rows of R P^T, transposed
+        if r > d.size:                               # eps = 0 with fewer rows than columns
+            W = np.eye(m)[:, :r]
+        V, _ = np.linalg.qr(W)
+        return r, sig, V
 
     # -- Eliminate  (P:l.101-106, l.396-399) ------------------------------------
     def eliminate(self, p: Node):
@@ -428,16 +463,19 @@ class _Factorizer:
 
 
 def factorize(n, row_ptr, col_idx, values, coords, depth, eps, order="coloured",
-              symmetric_stack=False, trace=False) -> Factorization:
-    """Alg. 1 on the CSR matrix A (row_ptr, col_idx, values) with point coordinates."""
+              symmetric_stack=False, trace=False, compressor="svd") -> Factorization:
+    """Alg. 1 on the CSR matrix A (row_ptr, col_idx, values) with point coordinates.
+    compressor: "svd" (Eq. lra + Eq. cutOff1) or "rrqr" (f1, column-pivoted QR)."""
     with threadpool_limits(ORACLE_THREADS):
-        return _factorize(n, row_ptr, col_idx, values, coords, depth, eps, order, symmetric_stack, trace)
+        return _factorize(n, row_ptr, col_idx, values, coords, depth, eps, order, symmetric_stack, trace,
+                          compressor)
 
 
-def _factorize(n, row_ptr, col_idx, values, coords, depth, eps, order, symmetric_stack, trace):
+def _factorize(n, row_ptr, col_idx, values, coords, depth, eps, order, symmetric_stack, trace,
+               compressor="svd"):
     return _Factorizer(n, np.asarray(row_ptr, np.int64), np.asarray(col_idx, np.int64),
                        np.asarray(values, np.float64), coords, depth, eps, order=order,
-                       symmetric_stack=symmetric_stack, trace=trace).run()
+                       symmetric_stack=symmetric_stack, trace=trace, compressor=compressor).run()
 
 
 # ---------------------------------------------------------------------------
