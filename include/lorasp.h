@@ -46,6 +46,10 @@ typedef enum {
 #define LORASP_SPD            0x1u  /* symmetric input: symmetric block store, SPD path  */
 #define LORASP_ORDER_NATURAL  0x2u  /* ascending cluster order, one node per wave (debug:
                                        the paper's literal Alg. 1 loop, P:l.281)         */
+#define LORASP_RRQR           0x4u  /* Compress with rank-revealing (column-pivoted) QR
+                                       instead of the SVD (P:l.616, P:l.840; SURVEY 8(f)
+                                       f1): keep the leading k with |R_kk| >= eps |R_00|;
+                                       nodes with m <= 512 (LORASP_E_ARG beyond)          */
 
 /* Krylov methods for lorasp_krylov_ex */
 #define LORASP_CG     0
@@ -71,8 +75,8 @@ typedef enum {
  *   depth     H-tree depth l; <= 0 means round(log2(n / leaf_size))
  *   eps       truncation threshold of Eq. cutOff1 (P:l.580-584): keep
  *             sigma_k >= eps * sigma_0; eps = 0 keeps everything (exact)
- *   flags     LORASP_SPD (required in this version: the SPD path) |
- *             LORASP_ORDER_NATURAL
+ *   flags     LORASP_SPD (symmetric input; else the general LU path) |
+ *             LORASP_ORDER_NATURAL | LORASP_RRQR
  *   device    CUDA device ordinal the handle will use
  *   out       receives the handle
  *   The pattern and coordinates are copied; the caller keeps ownership.

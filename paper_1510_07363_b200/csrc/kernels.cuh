@@ -2159,6 +2159,150 @@ __global__ void __launch_bounds__(512) k_backtr_multi(const EigTask *__restrict_
   }
 }
 
+// ---- f1: rank-revealing QR compressor (P:l.616, P:l.840) ----
+// Column-pivoted (Businger-Golub) QR of the stack M, M P = Q R, computed as
+// the diagonal-pivoted Cholesky of the Gram G = M^T M = P R^T R P^T (the pivot
+// "largest remaining column norm of M" is "largest remaining diagonal of the
+// Schur complement of G").  Truncated at the first k with R_kk < eps R_00
+// (reading F1); V = an orthonormal basis of span(R[:r, :] P^T)^T = span(L),
+// L = the m x r Cholesky columns in the original index order, by classical
+// Gram-Schmidt with reorthogonalisation (CGS2).  One CTA (512 threads) per
+// node, thread j owns row j (m <= 512); left-looking: column k of L is
+// G[:, p] - L[:, :k] L[p, :k]^T, read from the L2-resident output V.
+// Writes V (m x r, ld m), sig (R_kk for k < r, the first dropped R_kk at r,
+// zeros after), *rank_out.  G = 0 -> r = 0 (Z4); eps = 0 -> V = I, r = m (Z3).
+constexpr int RRQR_MAXM = 512;
+__global__ void __launch_bounds__(512, 1) k_rrqr(const EigTask *__restrict__ tasks, double eps, int *status) {
+  __shared__ double s_v[16];
+  __shared__ int s_i[16];
+  __shared__ double Lp[RRQR_MAXM];     // row p of L (pivoted row) / CGS coefficients
+  __shared__ double s_bc[2];
+  __shared__ int s_p;
+  pdl_trigger();
+  const EigTask t = tasks[blockIdx.x];
+  pdl_wait();
+  const int m = t.m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int j = tid;
+  const bool row = j < m;
+  double dj = row ? t.G[j + (int64_t)j * m] : 0.0;   // remaining diagonal
+  bool done = !row;
+  // block argmax of the remaining diagonal (ties -> smallest index)
+  auto argmax = [&](double v, int idx) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (v2 > v || (v2 == v && i2 < idx)) {
+        v = v2;
+        idx = i2;
+      }
+    }
+    if (lane == 0) {
+      s_v[warp] = v;
+      s_i[warp] = idx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double bv = s_v[0];
+      int bi = s_i[0];
+      for (int w = 1; w < nw; ++w)
+        if (s_v[w] > bv || (s_v[w] == bv && s_i[w] < bi)) {
+          bv = s_v[w];
+          bi = s_i[w];
+        }
+      s_bc[0] = bv;
+      s_p = bi;
+    }
+    __syncthreads();
+  };
+  if (eps == 0.0) {
+    argmax(row ? dj : -1.0, row ? j : 1 << 30);
+    const bool zero = !(s_bc[0] > 0.0);
+    for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) t.V[q] = ((q % m) == (q / m)) ? 1.0 : 0.0;
+    for (int q = tid; q < m; q += blockDim.x) t.sig[q] = 0.0;
+    if (tid == 0) *t.rank_out = zero ? 0 : m;
+    return;
+  }
+  double r00 = 0.0;
+  int r = 0;
+  for (int k = 0; k < m; ++k) {
+    argmax(done ? -1.0 : dj, done ? (1 << 30) : j);
+    const double dmax = s_bc[0];
+    const int p = s_p;
+    const double rkk = sqrt(fmax(dmax, 0.0));
+    if (k == 0) r00 = rkk;
+    if (!(rkk > 0.0) || rkk < eps * r00) {   // truncation (uniform)
+      if (tid == 0 && k < m) t.sig[k] = rkk;
+      break;
+    }
+    if (tid == 0) t.sig[k] = rkk;
+    for (int i = tid; i < k; i += blockDim.x) Lp[i] = t.V[p + (int64_t)i * m];
+    __syncthreads();
+    double l = 0.0;
+    if (row && !done) {
+      if (j == p) {
+        l = rkk;
+        done = true;
+      } else {
+        double s0 = t.G[j + (int64_t)p * m], s1 = 0.0;
+        int i = 0;
+        for (; i + 1 < k; i += 2) {
+          s0 = fma(-t.V[j + (int64_t)i * m], Lp[i], s0);
+          s1 = fma(-t.V[j + (int64_t)(i + 1) * m], Lp[i + 1], s1);
+        }
+        if (i < k) s0 = fma(-t.V[j + (int64_t)i * m], Lp[i], s0);
+        l = (s0 + s1) * frcp(rkk);
+        dj -= l * l;
+      }
+    }
+    if (row) t.V[j + (int64_t)k * m] = l;
+    r = k + 1;
+    __syncthreads();   // column k visible before the next step reads row p of L
+  }
+  for (int q = r + 1 + tid; q < m; q += blockDim.x) t.sig[q] = 0.0;
+  if (tid == 0) *t.rank_out = r;
+  if (r == 0) return;
+  // ---- V = orth(L): CGS2 (two projections per column), column k by the block ----
+  for (int k = 0; k < r; ++k) {
+    double *vk = t.V + (int64_t)k * m;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = warp; i < k; i += nw) {   // coefficients against the finished columns
+        const double *vi = t.V + (int64_t)i * m;
+        double sacc = 0.0;
+        for (int q = lane; q < m; q += 32) sacc = fma(vi[q], vk[q], sacc);
+        sacc = warp_sum(sacc);
+        if (lane == 0) Lp[i] = sacc;
+      }
+      __syncthreads();
+      if (row && k > 0) {
+        double s0 = 0.0, s1 = 0.0;
+        int i = 0;
+        for (; i + 1 < k; i += 2) {
+          s0 = fma(t.V[j + (int64_t)i * m], Lp[i], s0);
+          s1 = fma(t.V[j + (int64_t)(i + 1) * m], Lp[i + 1], s1);
+        }
+        if (i < k) s0 = fma(t.V[j + (int64_t)i * m], Lp[i], s0);
+        vk[j] -= s0 + s1;
+      }
+      __syncthreads();
+    }
+    // normalise
+    double ss = row ? vk[j] * vk[j] : 0.0;
+    ss = warp_sum(ss);
+    if (lane == 0) s_v[warp] = ss;
+    __syncthreads();
+    if (tid == 0) {
+      double a = 0.0;
+      for (int w = 0; w < nw; ++w) a += s_v[w];
+      s_bc[1] = a > 0.0 ? 1.0 / sqrt(a) : 0.0;
+    }
+    __syncthreads();
+    if (row) vk[j] *= s_bc[1];
+    __syncthreads();
+  }
+  (void)status;
+}
+
 // ----------------------------------------------------------------- pivot ----
 // (k_eig_t<true> for m <= 128, k_eig_t<false> otherwise)
 

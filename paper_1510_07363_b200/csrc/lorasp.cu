@@ -672,6 +672,15 @@ void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::v
 
 
 void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int max_m, int cap) {
+  if (h->plan.flags & LORASP_RRQR) {   // f1: pivoted QR compressor, one launch for the wave
+    if (et.empty()) return;
+    for (const EigTask &e : et)
+      if (e.m > RRQR_MAXM) throw Err(LORASP_E_ARG, "LORASP_RRQR: node of size " + std::to_string(e.m) + " > 512");
+    launch_k(k_rrqr, (unsigned)et.size(), 512, 0, h->stream, (const EigTask *)de, h->plan.eps, h->d_status.as<int>());
+    ++h->launches_factor;
+    CK(cudaGetLastError());
+    return;
+  }
   std::vector<EigTask> small, big, clt[4];
   bool reg_fork = false;
   for (const EigTask &e : et) {
