@@ -150,11 +150,11 @@ def weak_scaling_value(n, world, steps, max_total_ms):
     return n * world * steps / (max_total_ms / 1e3)
 
 
-def cpu_baseline(p, sample="factor+krylov"):
+def cpu_baseline(p, sample="factor+krylov", compressor="svd"):
     """The oracle as it stands, on the host cores, on one bounded sample."""
     from oracle import lorasp_oracle as O
     t0 = time.perf_counter()
-    f = O.factorize(p.n, p.row_ptr, p.col_idx, p.values, p.coords, p.depth, p.eps)
+    f = O.factorize(p.n, p.row_ptr, p.col_idx, p.values, p.coords, p.depth, p.eps, compressor=compressor)
     tf = time.perf_counter() - t0
     out = {"value": p.n / tf, "unit": "unknowns/s", "cores": O.ORACLE_THREADS, "kind": "oracle",
            "factor_s": tf, "host_cpus": os.cpu_count()}
@@ -212,6 +212,8 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--compressor", default="svd", choices=["svd", "rrqr"],
+                    help="Compress: SVD rule (Eq. cutOff1, the metric's workload) or pivoted QR (f1)")
     ap.add_argument("--mode", default="partition", choices=["partition", "replicas"],
                     help="N > 1: subtree partition of one problem (strong) or independent replicas (weak)")
     args = ap.parse_args()
@@ -228,7 +230,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     p = make_problem(args.config)
-    h = L.analyze_problem(p, device=local)
+    flags = (L.LORASP_SPD if p.symmetric else 0) | (L.LORASP_RRQR if args.compressor == "rrqr" else 0)
+    h = L.analyze_problem(p, device=local, flags=flags)
     part = world > 1 and args.mode == "partition"
     if part:
         from paper_1510_07363_b200.dist import TorchComm
@@ -330,7 +333,7 @@ def main():
             "higher_is_better": True, "scaling": "strong" if part else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOADS.get(args.config, '')}", "n": p.n, "nnz": p.nnz,
-                       "eps": p.eps, "depth": p.depth, "leaf": p.leaf,
+                       "eps": p.eps, "depth": p.depth, "leaf": p.leaf, "compressor": args.compressor,
                        "parallelism": (f"subtree partition over {world} GPUs, per-wave NCCL exchange "
                                        f"({stats.get('dist_exchange_calls')} collectives, "
                                        f"{stats.get('dist_allgather_bytes')} B all-gathered per factorization)")
@@ -350,7 +353,7 @@ def main():
                             "region records CUDA events only around launches of the dominant class"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb, _ = cpu_baseline(p)
+        cb, _ = cpu_baseline(p, compressor=args.compressor)
         line["cpu_baseline"] = cb
 
     if not args.no_e2e:
