@@ -2172,9 +2172,13 @@ __global__ void __launch_bounds__(512) k_backtr_multi(const EigTask *__restrict_
 // Writes V (m x r, ld m), sig (R_kk for k < r, the first dropped R_kk at r,
 // zeros after), *rank_out.  G = 0 -> r = 0 (Z4); eps = 0 -> V = I, r = m (Z3).
 constexpr int RRQR_MAXM = 512;
-__global__ void __launch_bounds__(512, 1) k_rrqr(const EigTask *__restrict__ tasks, double eps, int *status) {
-  __shared__ double s_v[16];
-  __shared__ int s_i[16];
+// NT threads, thread j owns row j (m <= NT).  G and L stay in global memory
+// (L2-resident; measured faster than staging them in shared memory, which
+// costs occupancy on the many-node waves).
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_rrqr(const EigTask *__restrict__ tasks, double eps, int *status) {
+  __shared__ double s_v[NT / 32];
+  __shared__ int s_i[NT / 32];
   __shared__ double Lp[RRQR_MAXM];     // row p of L (pivoted row) / CGS coefficients
   __shared__ double s_bc[2];
   __shared__ int s_p;
@@ -2182,10 +2186,13 @@ __global__ void __launch_bounds__(512, 1) k_rrqr(const EigTask *__restrict__ tas
   const EigTask t = tasks[blockIdx.x];
   pdl_wait();
   const int m = t.m;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = NT / 32;
   const int j = tid;
   const bool row = j < m;
-  double dj = row ? t.G[j + (int64_t)j * m] : 0.0;   // remaining diagonal
+  const double *G = t.G;
+  double *Vw = t.V;                    // L, then V (column-major, ld m)
+  double dj = row ? G[j + (int64_t)j * m] : 0.0;   // remaining diagonal
   bool done = !row;
   // block argmax of the remaining diagonal (ties -> smallest index)
   auto argmax = [&](double v, int idx) {
@@ -2218,8 +2225,8 @@ __global__ void __launch_bounds__(512, 1) k_rrqr(const EigTask *__restrict__ tas
   if (eps == 0.0) {
     argmax(row ? dj : -1.0, row ? j : 1 << 30);
     const bool zero = !(s_bc[0] > 0.0);
-    for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) t.V[q] = ((q % m) == (q / m)) ? 1.0 : 0.0;
-    for (int q = tid; q < m; q += blockDim.x) t.sig[q] = 0.0;
+    for (int64_t q = tid; q < (int64_t)m * m; q += NT) t.V[q] = ((q % m) == (q / m)) ? 1.0 : 0.0;
+    for (int q = tid; q < m; q += NT) t.sig[q] = 0.0;
     if (tid == 0) *t.rank_out = zero ? 0 : m;
     return;
   }
@@ -2232,11 +2239,11 @@ __global__ void __launch_bounds__(512, 1) k_rrqr(const EigTask *__restrict__ tas
     const double rkk = sqrt(fmax(dmax, 0.0));
     if (k == 0) r00 = rkk;
     if (!(rkk > 0.0) || rkk < eps * r00) {   // truncation (uniform)
-      if (tid == 0 && k < m) t.sig[k] = rkk;
+      if (tid == 0) t.sig[k] = rkk;
       break;
     }
     if (tid == 0) t.sig[k] = rkk;
-    for (int i = tid; i < k; i += blockDim.x) Lp[i] = t.V[p + (int64_t)i * m];
+    for (int i = tid; i < k; i += NT) Lp[i] = Vw[p + (int64_t)i * m];
     __syncthreads();
     double l = 0.0;
     if (row && !done) {
@@ -2244,30 +2251,30 @@ __global__ void __launch_bounds__(512, 1) k_rrqr(const EigTask *__restrict__ tas
         l = rkk;
         done = true;
       } else {
-        double s0 = t.G[j + (int64_t)p * m], s1 = 0.0;
+        double s0 = G[j + (int64_t)p * m], s1 = 0.0;
         int i = 0;
         for (; i + 1 < k; i += 2) {
-          s0 = fma(-t.V[j + (int64_t)i * m], Lp[i], s0);
-          s1 = fma(-t.V[j + (int64_t)(i + 1) * m], Lp[i + 1], s1);
+          s0 = fma(-Vw[j + (int64_t)i * m], Lp[i], s0);
+          s1 = fma(-Vw[j + (int64_t)(i + 1) * m], Lp[i + 1], s1);
         }
-        if (i < k) s0 = fma(-t.V[j + (int64_t)i * m], Lp[i], s0);
+        if (i < k) s0 = fma(-Vw[j + (int64_t)i * m], Lp[i], s0);
         l = (s0 + s1) * frcp(rkk);
         dj -= l * l;
       }
     }
-    if (row) t.V[j + (int64_t)k * m] = l;
+    if (row) Vw[j + (int64_t)k * m] = l;
     r = k + 1;
     __syncthreads();   // column k visible before the next step reads row p of L
   }
-  for (int q = r + 1 + tid; q < m; q += blockDim.x) t.sig[q] = 0.0;
+  for (int q = r + 1 + tid; q < m; q += NT) t.sig[q] = 0.0;
   if (tid == 0) *t.rank_out = r;
   if (r == 0) return;
   // ---- V = orth(L): CGS2 (two projections per column), column k by the block ----
   for (int k = 0; k < r; ++k) {
-    double *vk = t.V + (int64_t)k * m;
+    double *vk = Vw + (int64_t)k * m;
     for (int pass = 0; pass < 2; ++pass) {
       for (int i = warp; i < k; i += nw) {   // coefficients against the finished columns
-        const double *vi = t.V + (int64_t)i * m;
+        const double *vi = Vw + (int64_t)i * m;
         double sacc = 0.0;
         for (int q = lane; q < m; q += 32) sacc = fma(vi[q], vk[q], sacc);
         sacc = warp_sum(sacc);
@@ -2278,10 +2285,10 @@ __global__ void __launch_bounds__(512, 1) k_rrqr(const EigTask *__restrict__ tas
         double s0 = 0.0, s1 = 0.0;
         int i = 0;
         for (; i + 1 < k; i += 2) {
-          s0 = fma(t.V[j + (int64_t)i * m], Lp[i], s0);
-          s1 = fma(t.V[j + (int64_t)(i + 1) * m], Lp[i + 1], s1);
+          s0 = fma(Vw[j + (int64_t)i * m], Lp[i], s0);
+          s1 = fma(Vw[j + (int64_t)(i + 1) * m], Lp[i + 1], s1);
         }
-        if (i < k) s0 = fma(t.V[j + (int64_t)i * m], Lp[i], s0);
+        if (i < k) s0 = fma(Vw[j + (int64_t)i * m], Lp[i], s0);
         vk[j] -= s0 + s1;
       }
       __syncthreads();

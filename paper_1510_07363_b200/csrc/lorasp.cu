@@ -676,7 +676,17 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
     if (et.empty()) return;
     for (const EigTask &e : et)
       if (e.m > RRQR_MAXM) throw Err(LORASP_E_ARG, "LORASP_RRQR: node of size " + std::to_string(e.m) + " > 512");
-    launch_k(k_rrqr, (unsigned)et.size(), 512, 0, h->stream, (const EigTask *)de, h->plan.eps, h->d_status.as<int>());
+    // one launch for the wave (classes would run back to back): 128 threads
+    // when every node has m <= 64 (cheaper barriers), else 512 (16 warps share
+    // the Gram-Schmidt coefficients of larger ranks)
+    int mm = 0;
+    for (const EigTask &e : et) mm = std::max(mm, e.m);
+    if (mm <= 64)
+      launch_k(k_rrqr<128>, (unsigned)et.size(), 128, 0, h->stream, (const EigTask *)de, h->plan.eps,
+               h->d_status.as<int>());
+    else
+      launch_k(k_rrqr<512>, (unsigned)et.size(), 512, 0, h->stream, (const EigTask *)de, h->plan.eps,
+               h->d_status.as<int>());
     ++h->launches_factor;
     CK(cudaGetLastError());
     return;
