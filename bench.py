@@ -45,6 +45,8 @@ WORKLOADS = {
             "64-dof leaves, depth 15, eps=1e-2, PCG 1e-10",
     "cfg5": "2D first-order upwind convection-diffusion beta=(50,30) 1024^2 (n=1048576), 64-dof leaves, "
             "depth 14, eps=1e-3, GMRES(50) 1e-10 (LU path)",
+    "adv32": "3D central-difference advection-diffusion sigma T + R grad T - Lap T (P:l.803-823) 32^3 "
+             "(n=32768), sigma=1, depth 9, eps=1e-1, GMRES(50) 1e-10 (LU path; second workload, f3)",
 }
 L2_FLUSH_BYTES = 256 << 20
 
@@ -175,7 +177,7 @@ def run_reference(args, world, rank):
         return 0
     from synth import make_problem
     from oracle import lorasp_oracle as O
-    p = make_problem(args.config)
+    p = make_problem(args.config, R=args.adv_R) if args.config == "adv32" else make_problem(args.config)
     times = []
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -212,6 +214,7 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--adv-R", type=float, default=1.0, help="adv32: the advection number R")
     ap.add_argument("--compressor", default="svd", choices=["svd", "rrqr"],
                     help="Compress: SVD rule (Eq. cutOff1, the metric's workload) or pivoted QR (f1)")
     ap.add_argument("--mode", default="partition", choices=["partition", "replicas"],
@@ -229,7 +232,7 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    p = make_problem(args.config)
+    p = make_problem(args.config, R=args.adv_R) if args.config == "adv32" else make_problem(args.config)
     flags = (L.LORASP_SPD if p.symmetric else 0) | (L.LORASP_RRQR if args.compressor == "rrqr" else 0)
     h = L.analyze_problem(p, device=local, flags=flags)
     part = world > 1 and args.mode == "partition"
@@ -334,6 +337,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOADS.get(args.config, '')}", "n": p.n, "nnz": p.nnz,
                        "eps": p.eps, "depth": p.depth, "leaf": p.leaf, "compressor": args.compressor,
+                       **({"R": args.adv_R, "sigma": 1.0} if args.config == "adv32" else {}),
                        "parallelism": (f"subtree partition over {world} GPUs, per-wave NCCL exchange "
                                        f"({stats.get('dist_exchange_calls')} collectives, "
                                        f"{stats.get('dist_allgather_bytes')} B all-gathered per factorization)")

@@ -159,6 +159,23 @@ def grid_upwind(dims: Sequence[int], beta: Sequence[float] = (50.0, 30.0)):
     return _assemble(n, rows, cols, vals)
 
 
+def grid_advdiff(dims: Sequence[int], sigma: float = 1.0, R: float = 1.0):
+    """The paper's advection-diffusion benchmark (P:l.803-815, Eq. advdiff):
+    sigma T + R (1,...,1).grad T - Lap T = g on the unit cube, Dirichlet,
+    central differences on the N^d interior grid, h = 1/(N+1), scaled by h^2:
+    A_qq = 2d + sigma h^2; the +a / -a neighbours -1 + R h / 2 / -1 - R h / 2
+    (symmetric diffusion + skew-symmetric advection, P:l.817)."""
+    n = int(np.prod(dims)); d = len(dims)
+    h = 1.0 / (max(dims) + 1)
+    rows = [np.arange(n, dtype=np.int64)]; cols = [np.arange(n, dtype=np.int64)]
+    vals = [np.full(n, 2.0 * d + sigma * h * h)]
+    for _, lo, hi in _neighbour_pairs(dims):
+        # row lo: its +a neighbour is hi; row hi: its -a neighbour is lo
+        rows += [lo, hi]; cols += [hi, lo]
+        vals += [np.full(lo.size, -1.0 + 0.5 * R * h), np.full(lo.size, -1.0 - 0.5 * R * h)]
+    return _assemble(n, rows, cols, vals)
+
+
 def _depth_for(n: int, leaf: int) -> int:
     return max(1, int(round(math.log2(n / leaf))))
 
@@ -170,13 +187,16 @@ CONFIGS = {
     "cfg3": dict(kind="poisson", dims=(64, 64, 64), leaf=64, depth=12, eps=1e-2, solver="cg"),
     "cfg4": dict(kind="varcoef", dims=(128, 128, 128), leaf=64, depth=15, eps=1e-2, solver="cg"),
     "cfg5": dict(kind="upwind", dims=(1024, 1024), leaf=64, depth=14, eps=1e-3, solver="gmres"),
+    # second LU-path workload: the paper's 3D advection-diffusion,
+    # 32^3, sigma = 1, eps = 1e-1 (P:l.821-823); R via make_problem(..., R=...)
+    "adv32": dict(kind="advdiff", dims=(32, 32, 32), leaf=64, depth=9, eps=1e-1, solver="gmres"),
 }
 
 
 def make_problem(name: str = "cfg1", dims: Optional[Sequence[int]] = None,
                  kind: Optional[str] = None, leaf: Optional[int] = None,
                  depth: Optional[int] = None, eps: Optional[float] = None,
-                 rhs_seed: int = RHS_SEED) -> Problem:
+                 rhs_seed: int = RHS_SEED, sigma: float = 1.0, R: float = 1.0) -> Problem:
     """Build a config by name, optionally overriding grid dims / kind / leaf / depth / eps."""
     base = dict(CONFIGS.get(name, CONFIGS["cfg1"]))
     if dims is not None:
@@ -199,6 +219,8 @@ def make_problem(name: str = "cfg1", dims: Optional[Sequence[int]] = None,
         rp, ci, va = grid_varcoef(dims); sym = True
     elif k == "upwind":
         rp, ci, va = grid_upwind(dims); sym = False
+    elif k == "advdiff":
+        rp, ci, va = grid_advdiff(dims, sigma, R); sym = False
     else:
         raise ValueError(f"unknown problem kind {k}")
     dep = base["depth"] if base.get("depth") else _depth_for(n, base["leaf"])

@@ -120,3 +120,24 @@ def test_waves_conflict_free_footprints():
             ball = {c} | N1[c]
             assert not (ball & seen)
             seen |= ball
+
+
+def test_synth_advdiff_structure():
+    """Eq. advdiff discretisation (P:l.811-817): symmetric part = the 7-point
+    Laplacian + sigma h^2 I, skew part = R h/2 on each +axis neighbour."""
+    from synth import csr_to_dense, make_problem
+    from synth.problems import grid_poisson
+    dims = (5, 4, 3)
+    for sigma, R in ((0.0, 1.0), (1.0, 300.0)):
+        p = make_problem("adv32", dims=dims, sigma=sigma, R=R)
+        A = csr_to_dense(p.n, p.row_ptr, p.col_idx, p.values)
+        h = 1.0 / (max(dims) + 1)
+        Lp = csr_to_dense(p.n, *grid_poisson(dims))
+        assert np.allclose((A + A.T) / 2, Lp + sigma * h * h * np.eye(p.n), rtol=0, atol=1e-14)
+        K = (A - A.T) / 2
+        # +x neighbour of dof 0 is dof 1 (x fastest): K[0, 1] = R h / 2
+        assert K[0, 1] == pytest.approx(0.5 * R * h) and K[1, 0] == pytest.approx(-0.5 * R * h)
+        assert K[0, dims[0]] == pytest.approx(0.5 * R * h)           # +y
+        assert K[0, dims[0] * dims[1]] == pytest.approx(0.5 * R * h)  # +z
+        assert np.count_nonzero(np.abs(K) > 1e-15) == 2 * sum(
+            (dims[a] - 1) * int(np.prod(dims)) // dims[a] for a in range(3))
