@@ -3473,6 +3473,30 @@ __global__ void k_dot_final(const double *__restrict__ part, int np, double *__r
     *out = t;
   }
 }
+// PCG with device-resident scalars (one host round trip per iteration):
+// x += a p, r -= a q with a = rz / pq; a breakdown (pq <= 0 or rz <= 0,
+// reading Z24) leaves x, r unchanged and raises *flag
+__global__ void k_pcg_update(int64_t n, const double *__restrict__ s_rz, const double *__restrict__ s_pq,
+                             const double *__restrict__ p, const double *__restrict__ q, double *__restrict__ x,
+                             double *__restrict__ r, double *__restrict__ flag) {
+  pdl_enter();
+  const double rz = *s_rz, pq = *s_pq;
+  const bool ok = (pq > 0) && (rz > 0);
+  const double a = ok ? rz / pq : 0.0;
+  if (!ok && blockIdx.x == 0 && threadIdx.x == 0) *flag = 1.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    x[i] = a * p[i] + x[i];
+    r[i] = -a * q[i] + r[i];
+  }
+}
+// p = z + (rz_new / rz_old) p
+__global__ void k_pcg_dir(int64_t n, const double *__restrict__ s_new, const double *__restrict__ s_old,
+                          const double *__restrict__ z, double *__restrict__ p) {
+  pdl_enter();
+  const double beta = *s_new / *s_old;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
 // y = a*x + b*y
 __global__ void k_axpby(int64_t n, double a, const double *__restrict__ x, double b,
                         double *__restrict__ y) {

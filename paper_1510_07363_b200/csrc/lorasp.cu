@@ -2425,6 +2425,16 @@ double dot_dev(lorasp_ctx *h, const double *a, const double *b) {
   return h->h_dot[0];
 }
 
+// dot product into a device scalar (no host round trip)
+void dot_dev_to(lorasp_ctx *h, const double *a, const double *b, double *out) {
+  cudaStream_t st = h->stream;
+  int ev = tbeg(h, K_DOT);
+  launch_k(k_dot_partial, DOT_BLOCKS, 256, 0, st, h->plan.n, a, b, h->d_dotpart.as<double>());
+  launch_k(k_dot_final, 1, 256, 0, st, h->d_dotpart.as<double>(), DOT_BLOCKS, out);
+  tend(h, ev, 2.0 * h->plan.n, 16.0 * h->plan.n);
+  h->launches_krylov += 2;
+}
+
 void spmv_dev(lorasp_ctx *h, const double *x, double *y) {
   const Plan &pl = h->plan;
   int ev = tbeg(h, K_SPMV);
@@ -2457,28 +2467,41 @@ int pcg_dev(lorasp_ctx *h, const double *b, double *x, double tol, int maxit, in
   }
   apply_dev(h, r, z, &h->launches_krylov);
   CK(cudaMemcpyAsync(p, z, n * 8, cudaMemcpyDeviceToDevice, st));
-  double rz = dot_dev(h, r, z);
+  // device scalars: rz (two slots, alternating), pq, rr, breakdown flag
+  double *sc = h->d_dotpart.as<double>() + DOT_BLOCKS + 8;
+  double *rz_cur = sc, *rz_nxt = sc + 1, *d_pq = sc + 2, *d_rr = sc + 3, *d_flag = sc + 4;
+  CK(cudaMemsetAsync(d_flag, 0, 8, st));
+  dot_dev_to(h, r, z, rz_cur);
   int it = 0;
   bool conv = false;
   for (it = 1; it <= maxit; ++it) {
     spmv_dev(h, p, q);
-    double pq = dot_dev(h, p, q);
-    if (!(pq > 0) || !(rz > 0)) {
+    dot_dev_to(h, p, q, d_pq);
+    int ev = tbeg(h, K_VEC);
+    launch_k(k_pcg_update, grid1(n), 256, 0, st, n, (const double *)rz_cur, (const double *)d_pq,
+             (const double *)p, (const double *)q, x, r, d_flag);
+    tend(h, ev, 4.0 * n, 48.0 * n);
+    ++h->launches_krylov;
+    dot_dev_to(h, r, r, d_rr);
+    CK(cudaMemcpyAsync(h->h_dot, d_pq, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));   // pq, rr, flag
+    CK(cudaStreamSynchronize(st));
+    if (h->h_dot[2] != 0.0) {
       it -= 1;
-      break;  // breakdown (reading Z24)
+      break;  // breakdown (reading Z24): x, r were left unchanged
     }
-    double alpha = rz / pq;
-    axpby(h, alpha, p, 1.0, x);
-    axpby(h, -alpha, q, 1.0, r);
-    double rel = std::sqrt(dot_dev(h, r, r)) / nb;
+    const double rel = std::sqrt(h->h_dot[1]) / nb;
     if (rel <= tol) {
       conv = true;
       break;
     }
     apply_dev(h, r, z, &h->launches_krylov);
-    double rz2 = dot_dev(h, r, z);
-    axpby(h, 1.0, z, rz2 / rz, p);
-    rz = rz2;
+    dot_dev_to(h, r, z, rz_nxt);
+    ev = tbeg(h, K_VEC);
+    launch_k(k_pcg_dir, grid1(n), 256, 0, st, n, (const double *)rz_nxt, (const double *)rz_cur,
+             (const double *)z, p);
+    tend(h, ev, 2.0 * n, 24.0 * n);
+    ++h->launches_krylov;
+    std::swap(rz_cur, rz_nxt);
   }
   if (it > maxit) it = maxit;
   // true residual
