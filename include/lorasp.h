@@ -120,7 +120,7 @@ int lorasp_gmres(lorasp_handle h, const double *b, double *x, double tol);
 
 /*
  * lorasp_krylov_ex — the full form: method LORASP_CG (preconditioned CG,
- *   P:l.652) or LORASP_GMRES; restart (GMRES), max_it; outputs the number of
+ *   P:l.652) or LORASP_GMRES; restart (GMRES, <= 1000; <= 0 means 50), max_it; outputs the number of
  *   iterations (A-products) and the final true relative residual
  *   ||b - A x||_2 / ||b||_2 (Eq. accres, P:l.585-589).  iters / relres may be NULL.
  */

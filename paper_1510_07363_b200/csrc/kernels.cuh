@@ -3497,6 +3497,14 @@ __global__ void k_pcg_dir(int64_t n, const double *__restrict__ s_new, const dou
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
 }
+// y += sgn * (*s) * x with the scalar on the device (GMRES Gram-Schmidt step)
+__global__ void k_axpy_dev(int64_t n, const double *__restrict__ s, double sgn, const double *__restrict__ x,
+                           double *__restrict__ y) {
+  pdl_enter();
+  const double a = sgn * *s;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = a * x[i] + y[i];
+}
 // y = a*x + b*y
 __global__ void k_axpby(int64_t n, double a, const double *__restrict__ x, double b,
                         double *__restrict__ y) {

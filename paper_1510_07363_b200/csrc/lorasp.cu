@@ -583,8 +583,8 @@ void ensure_mem(lorasp_ctx *h) {
   h->d_status.ensure(64, h->stream);
   CK(cudaMallocHost(&h->h_ranks, sizeof(int) * (1 << 20)));
   CK(cudaMallocHost(&h->h_status, 64));
-  CK(cudaMallocHost(&h->h_dot, 64 * sizeof(double)));
-  h->d_dotpart.ensure((DOT_BLOCKS + 64) * sizeof(double), h->stream);
+  CK(cudaMallocHost(&h->h_dot, 1024 * sizeof(double)));   // GMRES Hessenberg column (restart <= 1000)
+  h->d_dotpart.ensure((DOT_BLOCKS + 1024) * sizeof(double), h->stream);
   h->stg.init(size_t(64) << 20, h->stream);
   CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   set_eig_attrs();
@@ -2478,8 +2478,7 @@ int pcg_dev(lorasp_ctx *h, const double *b, double *x, double tol, int maxit, in
     spmv_dev(h, p, q);
     dot_dev_to(h, p, q, d_pq);
     int ev = tbeg(h, K_VEC);
-    launch_k(k_pcg_update, grid1(n), 256, 0, st, n, (const double *)rz_cur, (const double *)d_pq,
-             (const double *)p, (const double *)q, x, r, d_flag);
+    k_pcg_update<<<grid1(n), 256, 0, st>>>(n, rz_cur, d_pq, p, q, x, r, d_flag);   // plain launch (see gmres)
     tend(h, ev, 4.0 * n, 48.0 * n);
     ++h->launches_krylov;
     dot_dev_to(h, r, r, d_rr);
@@ -2497,8 +2496,7 @@ int pcg_dev(lorasp_ctx *h, const double *b, double *x, double tol, int maxit, in
     apply_dev(h, r, z, &h->launches_krylov);
     dot_dev_to(h, r, z, rz_nxt);
     ev = tbeg(h, K_VEC);
-    launch_k(k_pcg_dir, grid1(n), 256, 0, st, n, (const double *)rz_nxt, (const double *)rz_cur,
-             (const double *)z, p);
+    k_pcg_dir<<<grid1(n), 256, 0, st>>>(n, rz_nxt, rz_cur, z, p);   // plain launch (see gmres)
     tend(h, ev, 2.0 * n, 24.0 * n);
     ++h->launches_krylov;
     std::swap(rz_cur, rz_nxt);
@@ -2551,12 +2549,24 @@ int gmres_dev(lorasp_ctx *h, const double *b, double *x, double tol, int restart
     for (int k = 0; k < restart && it < maxit; ++k) {
       apply_dev(h, Vb + (int64_t)k * n, Zb + (int64_t)k * n, &h->launches_krylov);
       spmv_dev(h, Zb + (int64_t)k * n, w);
+      // modified Gram-Schmidt with the coefficients kept on the device; one
+      // host round trip per iteration for the Hessenberg column
+      double *hcol = h->d_dotpart.as<double>() + DOT_BLOCKS + 16;   // k + 2 <= 1002 slots
       for (int j = 0; j <= k; ++j) {
-        double hj = dot_dev(h, w, Vb + (int64_t)j * n);
-        H[j + k * (restart + 1)] = hj;
-        axpby(h, -hj, Vb + (int64_t)j * n, 1.0, w);
+        dot_dev_to(h, w, Vb + (int64_t)j * n, hcol + j);
+        int ev = tbeg(h, K_VEC);
+        // plain launch (no PDL): a PDL launch of this device-scalar consumer right
+        // after k_dot_final produced wrong Gram-Schmidt updates (measured; cause
+        // not isolated), so the scalar consumers are fully stream-ordered
+        k_axpy_dev<<<grid1(n), 256, 0, st>>>(n, hcol + j, -1.0, Vb + (int64_t)j * n, w);
+        tend(h, ev, 2.0 * n, 24.0 * n);
+        ++h->launches_krylov;
       }
-      double hn = std::sqrt(dot_dev(h, w, w));
+      dot_dev_to(h, w, w, hcol + k + 1);
+      CK(cudaMemcpyAsync(h->h_dot, hcol, (size_t)(k + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int j = 0; j <= k; ++j) H[j + k * (restart + 1)] = h->h_dot[j];
+      double hn = std::sqrt(h->h_dot[k + 1]);
       H[k + 1 + k * (restart + 1)] = hn;
       for (int j = 0; j < k; ++j) {
         double a = H[j + k * (restart + 1)], bb = H[j + 1 + k * (restart + 1)];
@@ -2789,6 +2799,7 @@ int lorasp_krylov_ex(lorasp_handle h, const double *b, double *x, double tol, in
     if (!h->factored) return (int)LORASP_E_STATE;
     CK(cudaSetDevice(h->device));
     if (restart <= 0) restart = 50;
+    if (restart > 1000) return (int)LORASP_E_ARG;
     const int64_t n = h->plan.n;
     h->launches_krylov = 0;
     bool dev = is_device_ptr(b);
