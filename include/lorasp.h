@@ -50,6 +50,9 @@ typedef enum {
                                        instead of the SVD (P:l.616, P:l.840; SURVEY 8(f)
                                        f1): keep the leading k with |R_kk| >= eps |R_00|;
                                        nodes with m <= 512 (LORASP_E_ARG beyond)          */
+#define LORASP_ALGEBRAIC      0x10u /* nested partitionings from the graph of A alone (BFS
+                                       level-structure bisection; coords
+                                       may be NULL and dim is ignored)                    */
 
 /* Krylov methods for lorasp_krylov_ex */
 #define LORASP_CG     0
@@ -76,7 +79,7 @@ typedef enum {
  *   eps       truncation threshold of Eq. cutOff1 (P:l.580-584): keep
  *             sigma_k >= eps * sigma_0; eps = 0 keeps everything (exact)
  *   flags     LORASP_SPD (symmetric input; else the general LU path) |
- *             LORASP_ORDER_NATURAL | LORASP_RRQR
+ *             LORASP_ORDER_NATURAL | LORASP_RRQR | LORASP_ALGEBRAIC
  *   device    CUDA device ordinal the handle will use
  *   out       receives the handle
  *   The pattern and coordinates are copied; the caller keeps ownership.

@@ -104,6 +104,58 @@ def bisection_tree(coords: np.ndarray, depth: int) -> Tree:
     return Tree(depth=depth, clusters=clusters, axis=axes, leaf_of=leaf_of)
 
 
+def bisection_tree_algebraic(row_ptr, col_idx, depth: int) -> Tree:
+    """nested partitionings from the graph of A alone (no
+    coordinates; the paper used SCOTCH, P:l.560, P:l.838).  Split rule (reading
+    F4): breadth-first level structure of the cluster's induced subgraph from a
+    pseudo-peripheral vertex — BFS from the smallest member, take the smallest
+    vertex of the last level, BFS again — members ordered by (level, index),
+    vertices unreachable from it last (by index); the first floor(|C|/2) form
+    child 2c.  The split axis is recorded as 0 (the colouring's lattice rule then
+    sees one axis and usually falls back to the greedy rule)."""
+    row_ptr = np.asarray(row_ptr, np.int64)
+    col_idx = np.asarray(col_idx, np.int64)
+    n = row_ptr.size - 1
+    INF = 1 << 60
+
+    def levels_from(src, inset):
+        lev = {src: 0}
+        frontier = [src]
+        while frontier:
+            nxt = []
+            for v in frontier:
+                for j in col_idx[row_ptr[v]:row_ptr[v + 1]]:
+                    j = int(j)
+                    if j != v and j in inset and j not in lev:
+                        lev[j] = lev[v] + 1
+                        nxt.append(j)
+            frontier = nxt
+        return lev
+
+    clusters = [[np.arange(n, dtype=np.int64)]]
+    axes = []
+    for k in range(depth):
+        nxt = []
+        for mem in clusters[k]:
+            if mem.size == 0:
+                nxt += [mem, mem]
+                continue
+            inset = set(int(v) for v in mem)
+            l1 = levels_from(int(mem[0]), inset)
+            far = max(l1.values())
+            p = min(v for v, l in l1.items() if l == far)
+            l2 = levels_from(p, inset)
+            order = sorted((int(v) for v in mem), key=lambda v: (l2.get(v, INF), v))
+            h = mem.size // 2
+            nxt += [np.array(sorted(order[:h]), dtype=np.int64), np.array(sorted(order[h:]), dtype=np.int64)]
+        axes.append(np.zeros(2 ** k, dtype=np.int64))
+        clusters.append(nxt)
+    leaf_of = np.empty(n, dtype=np.int64)
+    for c, mem in enumerate(clusters[depth]):
+        leaf_of[mem] = c
+    return Tree(depth=depth, clusters=clusters, axis=axes, leaf_of=leaf_of)
+
+
 # ---------------------------------------------------------------------------
 # Quotient graphs and distances                    (P:l.73-76, l.247-249, l.506-512)
 # ---------------------------------------------------------------------------
@@ -208,7 +260,8 @@ def _cluster_level(u: Node) -> Tuple[int, int]:
 
 class _Factorizer:
     def __init__(self, n, row_ptr, col_idx, values, coords, depth, eps,
-                 order="coloured", symmetric_stack=False, trace=False, compressor="svd"):
+                 order="coloured", symmetric_stack=False, trace=False, compressor="svd",
+                 partition="coordinates"):
         self.n = n
         self.l = depth
         self.eps = float(eps)
@@ -219,7 +272,11 @@ class _Factorizer:
         self.want_trace = trace
         coords = np.asarray(coords, dtype=np.float64).reshape(n, -1)
         self.dim = coords.shape[1]
-        self.tree = bisection_tree(coords, depth)
+        if partition == "algebraic":
+            self.dim = 1
+            self.tree = bisection_tree_algebraic(row_ptr, col_idx, depth)
+        else:
+            self.tree = bisection_tree(coords, depth)
         self.N1, self.N2 = {}, {}
         for k in range(depth + 1):
             cl_of = self.tree.leaf_of >> (depth - k)
@@ -463,19 +520,20 @@ class _Factorizer:
 
 
 def factorize(n, row_ptr, col_idx, values, coords, depth, eps, order="coloured",
-              symmetric_stack=False, trace=False, compressor="svd") -> Factorization:
+              symmetric_stack=False, trace=False, compressor="svd", partition="coordinates") -> Factorization:
     """Alg. 1 on the CSR matrix A (row_ptr, col_idx, values) with point coordinates.
     compressor: "svd" (Eq. lra + Eq. cutOff1) or "rrqr" (f1, column-pivoted QR)."""
     with threadpool_limits(ORACLE_THREADS):
         return _factorize(n, row_ptr, col_idx, values, coords, depth, eps, order, symmetric_stack, trace,
-                          compressor)
+                          compressor, partition)
 
 
 def _factorize(n, row_ptr, col_idx, values, coords, depth, eps, order, symmetric_stack, trace,
-               compressor="svd"):
+               compressor="svd", partition="coordinates"):
     return _Factorizer(n, np.asarray(row_ptr, np.int64), np.asarray(col_idx, np.int64),
                        np.asarray(values, np.float64), coords, depth, eps, order=order,
-                       symmetric_stack=symmetric_stack, trace=trace, compressor=compressor).run()
+                       symmetric_stack=symmetric_stack, trace=trace, compressor=compressor,
+                       partition=partition).run()
 
 
 # ---------------------------------------------------------------------------

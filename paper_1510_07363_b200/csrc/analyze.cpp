@@ -76,7 +76,9 @@ void sorted_erase(std::vector<int> &v, int x) {
 int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int dim,
                const double *coords, int leaf_size, int depth, double eps, unsigned flags,
                std::string &err) {
-  if (n <= 0 || !row_ptr || !col_idx || !coords || dim < 1 || dim > 3 || eps < 0 || eps > 1) {
+  const bool algebraic = (flags & LORASP_ALGEBRAIC) != 0;
+  if (algebraic) dim = 1;   // coordinates unused; one pseudo-axis for the colouring
+  if (n <= 0 || !row_ptr || !col_idx || (!coords && !algebraic) || dim < 1 || dim > 3 || eps < 0 || eps > 1) {
     err = "analyze: bad argument";
     return -1;
   }
@@ -127,12 +129,57 @@ int build_plan(Plan &pl, int64_t n, const int64_t *row_ptr, const int64_t *col_i
   cur[0].resize(n);
   std::iota(cur[0].begin(), cur[0].end(), 0);
   std::vector<std::vector<int>> axis(depth);
+  // algebraic partitioning (reading F4): breadth-first level
+  // structure of the cluster's induced subgraph from a pseudo-peripheral vertex
+  std::vector<int> owner(algebraic ? n : 0, -1), lev(algebraic ? n : 0, -1);
+  auto bfs = [&](int src, int cl, std::vector<int> &touched) {
+    touched.clear();
+    lev[src] = 0;
+    touched.push_back(src);
+    for (size_t h = 0; h < touched.size(); ++h) {
+      const int v = touched[h];
+      for (int64_t q = row_ptr[v]; q < row_ptr[v + 1]; ++q) {
+        const int j = (int)col_idx[q];
+        if (j != v && owner[j] == cl && lev[j] < 0) {
+          lev[j] = lev[v] + 1;
+          touched.push_back(j);
+        }
+      }
+    }
+  };
   for (int k = 0; k < depth; ++k) {
     std::vector<std::vector<int>> nxt(2 * cur.size());
     axis[k].assign(cur.size(), 0);
+    if (algebraic)
+      for (size_t c = 0; c < cur.size(); ++c)
+        for (int v : cur[c]) owner[v] = (int)c;
     for (size_t c = 0; c < cur.size(); ++c) {
       std::vector<int> &mem = cur[c];
       if (mem.empty()) continue;
+      if (algebraic) {
+        std::vector<int> touched;
+        bfs(mem[0], (int)c, touched);   // mem is ascending: mem[0] is the smallest member
+        int far = 0, p = touched[0];
+        for (int v : touched) far = std::max(far, lev[v]);
+        p = n;
+        for (int v : touched)
+          if (lev[v] == far) p = std::min(p, v);
+        for (int v : touched) lev[v] = -1;
+        bfs(p, (int)c, touched);
+        const int INF = 1 << 30;
+        std::vector<std::pair<int, int>> key(mem.size());
+        for (size_t t = 0; t < mem.size(); ++t) key[t] = {lev[mem[t]] < 0 ? INF : lev[mem[t]], mem[t]};
+        for (int v : touched) lev[v] = -1;
+        std::sort(key.begin(), key.end());
+        const size_t h = mem.size() / 2;
+        std::vector<int> lo, hi;
+        for (size_t t = 0; t < key.size(); ++t) (t < h ? lo : hi).push_back(key[t].second);
+        std::sort(lo.begin(), lo.end());
+        std::sort(hi.begin(), hi.end());
+        nxt[2 * c] = std::move(lo);
+        nxt[2 * c + 1] = std::move(hi);
+        continue;
+      }
       double ext[3], mx = 0;
       for (int a = 0; a < dim; ++a) {
         double lo = coords[(int64_t)mem[0] * dim + a], hi = lo;

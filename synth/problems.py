@@ -176,6 +176,30 @@ def grid_advdiff(dims: Sequence[int], sigma: float = 1.0, R: float = 1.0):
     return _assemble(n, rows, cols, vals)
 
 
+def random_knn_laplacian(n: int, k: int = 6, seed: int = COEF_SEED, shift: float = 0.5):
+    """An unstructured SPD test matrix for the algebraic partitioner (f4): points
+    from the seeded splitmix64 stream in the unit square, each joined to its k
+    nearest neighbours (symmetrised), graph Laplacian with unit weights plus
+    shift * I.  The coordinates are NOT passed to the solver."""
+    u = splitmix64_uniform(seed, 2 * n).reshape(n, 2)
+    d2 = ((u[:, None, :] - u[None, :, :]) ** 2).sum(-1)
+    np.fill_diagonal(d2, np.inf)
+    nb = np.argsort(d2, axis=1, kind="stable")[:, :k]
+    pairs = set()
+    for i in range(n):
+        for j in nb[i]:
+            a, b = (i, int(j)) if i < j else (int(j), i)
+            pairs.add((a, b))
+    pairs = sorted(pairs)
+    lo = np.array([a for a, _ in pairs], dtype=np.int64)
+    hi = np.array([b for _, b in pairs], dtype=np.int64)
+    deg = np.bincount(lo, minlength=n) + np.bincount(hi, minlength=n)
+    rows = [np.arange(n, dtype=np.int64), lo, hi]
+    cols = [np.arange(n, dtype=np.int64), hi, lo]
+    vals = [deg.astype(np.float64) + shift, -np.ones(lo.size), -np.ones(lo.size)]
+    return _assemble(n, rows, cols, vals)
+
+
 def _depth_for(n: int, leaf: int) -> int:
     return max(1, int(round(math.log2(n / leaf))))
 

@@ -96,3 +96,33 @@ def test_apply_before_factor_is_state_error(L):
         h.apply(p.b, np.zeros(p.n))
     assert e.value.code == -8
     h.close()
+
+
+def _alg_problems():
+    from synth.problems import random_knn_laplacian
+    out = []
+    for name, dims in (("cfg1", (32, 32)), ("cfg3", (8, 8, 8))):
+        p = make_problem(name, dims=dims)
+        out.append((p.n, p.row_ptr, p.col_idx, p.depth))
+    rp, ci, _ = random_knn_laplacian(1500)
+    out.append((1500, rp, ci, 5))
+    return out
+
+
+@pytest.mark.parametrize("case", range(3))
+def test_analyze_order_matches_oracle_algebraic(L, case):
+    """LORASP_ALGEBRAIC (f4): the C++ BFS bisection + colouring equal the oracle's."""
+    n, rp, ci, depth = _alg_problems()[case]
+    h = L.Handle(n, rp, ci, np.zeros((n, 1)), depth=depth, eps=1e-2,
+                 flags=L.LORASP_SPD | L.LORASP_ALGEBRAIC)
+    t = O.bisection_tree_algebraic(rp, ci, depth)
+    for i in range(1, depth + 1):
+        order, wave = h.level_order(i)
+        k = i - 1
+        cl = t.leaf_of >> (depth - k)
+        N1, N2 = O.distance_sets(O.quotient_graph(rp, ci, cl, 2 ** k))
+        col = O.colour_level(t, k, 1, N1, N2)
+        assert list(order) == sorted(range(2 ** k), key=lambda c: (col[c], c))
+    st = h.stats()
+    assert st["max_edge_distance"] <= 2
+    h.close()

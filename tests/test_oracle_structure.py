@@ -141,3 +141,30 @@ def test_synth_advdiff_structure():
         assert K[0, dims[0] * dims[1]] == pytest.approx(0.5 * R * h)  # +z
         assert np.count_nonzero(np.abs(K) > 1e-15) == 2 * sum(
             (dims[a] - 1) * int(np.prod(dims)) // dims[a] for a in range(3))
+
+
+def test_algebraic_bisection_pins():
+    """Reading F4 on graphs whose BFS level structure is known: a path splits into
+    its two contiguous halves; on a grid every child of a connected cluster is
+    connected (a BFS prefix is) and the sizes are floor / ceil halves."""
+    n = 37
+    rows = np.arange(n - 1)
+    A = sp.coo_matrix((np.ones(2 * (n - 1)), (np.r_[rows, rows + 1], np.r_[rows + 1, rows])), shape=(n, n))
+    A = (A + sp.eye(n)).tocsr()
+    A.sort_indices()
+    t = O.bisection_tree_algebraic(A.indptr, A.indices, 2)
+    # BFS from vertex 0 reaches n-1 last; BFS from n-1 orders n-1, n-2, ..., 0
+    assert list(t.clusters[1][0]) == list(range(19, 37)) and list(t.clusters[1][1]) == list(range(0, 19))
+    p = make_problem("cfg1", dims=(12, 10))
+    t = O.bisection_tree_algebraic(p.row_ptr, p.col_idx, 4)
+    G = sp.csr_matrix((np.ones(p.col_idx.size), p.col_idx, p.row_ptr))
+    for k in range(1, 5):
+        for c, mem in enumerate(t.clusters[k]):
+            par = t.clusters[k - 1][c // 2]
+            assert mem.size in (par.size // 2, par.size - par.size // 2)
+            sub = G[mem][:, mem]
+            ncomp, _ = sp.csgraph.connected_components(sub, directed=False)
+            parent_conn = sp.csgraph.connected_components(G[par][:, par], directed=False)[0] == 1
+            if parent_conn and c % 2 == 0:
+                assert ncomp == 1
+    assert sorted(np.concatenate(t.clusters[4]).tolist()) == list(range(p.n))
