@@ -176,6 +176,30 @@ def grid_advdiff(dims: Sequence[int], sigma: float = 1.0, R: float = 1.0):
     return _assemble(n, rows, cols, vals)
 
 
+def grid_vcp(dims: Sequence[int], case: int = 1, seed: int = COEF_SEED):
+    """The paper's variable-coefficient Poisson benchmark -div(phi grad T) (Eq. VCP,
+    P:l.685-694) with per-point phi: case 1 unif(0,1), case 2 1/unif(0,1), case 3
+    unif(-1,1) (indefinite).  Readings (F3): Dirichlet instead of the
+    paper's periodic boundary (which leaves a constant null space for cases 1-2),
+    face coefficient = arithmetic mean of the two cell values (a harmonic mean is
+    undefined across a sign change), boundary faces phi_p."""
+    n = int(np.prod(dims)); d = len(dims)
+    u = splitmix64_uniform(seed + 100 * case, n)
+    phi = {1: u, 2: 1.0 / np.maximum(u, 1e-300), 3: 2.0 * u - 1.0}[case]
+    diag = np.zeros(n)
+    rows = []; cols = []; vals = []
+    nface = np.zeros(n)
+    for _, lo, hi in _neighbour_pairs(dims):
+        a = 0.5 * (phi[lo] + phi[hi])
+        np.add.at(diag, lo, a); np.add.at(diag, hi, a)
+        np.add.at(nface, lo, 1.0); np.add.at(nface, hi, 1.0)
+        rows += [lo, hi]; cols += [hi, lo]; vals += [-a, -a]
+    diag += (2.0 * d - nface) * phi
+    rows.append(np.arange(n, dtype=np.int64)); cols.append(np.arange(n, dtype=np.int64))
+    vals.append(diag)
+    return _assemble(n, rows, cols, vals)
+
+
 def random_knn_laplacian(n: int, k: int = 6, seed: int = COEF_SEED, shift: float = 0.5):
     """An unstructured SPD test matrix for the algebraic partitioner (f4): points
     from the seeded splitmix64 stream in the unit square, each joined to its k
