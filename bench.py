@@ -324,8 +324,8 @@ def main():
         roof["traffic"] = None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                trd = json.load(f)
-            if dom_name in trd and trd.get("_config", "cfg2") == args.config:
+                trd = json.load(f).get(args.config, {})   # per-config ncu measurements
+            if dom_name in trd:
                 roof["traffic"] = trd[dom_name]
                 roof["traffic_note"] = trd.get("_note")
         except Exception:
