@@ -1715,7 +1715,7 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
   if constexpr (PRE) {
     // PRE pipeline stage 0 ends here: the kept eigenvalues and ||T|| bound go to
     // the tridiagonal record for k_invit_multi; MGS + back-transformation follow
-    // in k_orth_pre / k_backtr_multi.
+    // in k_orth_cl / k_backtr_multi.
     double *rec = t.work + 6 * (int64_t)m * m;
     for (int k = tid; k < r; k += blockDim.x) rec[rec_lam_off(m) + k] = lam[k];
     if (tid == 0) rec[3 * m + 1] = bnorm;
@@ -1966,68 +1966,6 @@ __global__ void __launch_bounds__(256) k_invit_multi(const EigTask *__restrict__
            *bb = DU2 + (int64_t)m * nbc;
     unsigned char *pv = reinterpret_cast<unsigned char *>(ws + 5 * (int64_t)m * nbc) + kk;
     invit_one(d, e, m, sft, pertol, k, DL, Dv, DU, DU2, bb, pv, nbc, t.V + (int64_t)k * m);
-  }
-}
-
-// Modified Gram-Schmidt of the r inverse-iteration vectors in t.V (global,
-// L2-resident), one CTA per node: the owner warp normalises z_k into shared
-// memory; every warp then removes it from 4 later vectors at a time (their
-// loads in flight together, 4 dots reduced at once).  Q = rows per lane.
-template <int Q>
-__global__ void __launch_bounds__(256) k_orth_pre(const EigTask *__restrict__ tasks) {
-  __shared__ double zk[32 * Q];
-  const EigTask t = tasks[blockIdx.x];
-  const int m = t.m, r = *t.rank_out;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int k = 0; k < r; ++k) {
-    double *zkg = t.V + (int64_t)k * m;
-    if (warp == 0) {
-      double v[Q], s2 = 0;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const int i = lane + 32 * q;
-        v[q] = i < m ? zkg[i] : 0.0;
-        s2 = fma(v[q], v[q], s2);
-      }
-      s2 = frcp(sqrt(warp_sum(s2)));
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const int i = lane + 32 * q;
-        zk[i] = v[q] * s2;
-        if (i < m) zkg[i] = v[q] * s2;
-      }
-    }
-    __syncthreads();
-    for (int j0 = k + 1 + 4 * warp; j0 < r; j0 += 4 * nw) {
-      double zz[4][Q], sd[4];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int j = j0 + v;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const int i = lane + 32 * q;
-          zz[v][q] = (j < r && i < m) ? t.V[(int64_t)j * m + i] : 0.0;
-        }
-      }
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        sd[v] = 0.0;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) sd[v] = fma(zk[lane + 32 * q], zz[v][q], sd[v]);
-      }
-      warp_sum_multi<4>(sd);
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int j = j0 + v;
-        if (j < r)
-#pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            const int i = lane + 32 * q;
-            if (i < m) t.V[(int64_t)j * m + i] = fma(-sd[v], zk[i], zz[v][q]);
-          }
-      }
-    }
-    __syncthreads();
   }
 }
 

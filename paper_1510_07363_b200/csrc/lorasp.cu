@@ -8,12 +8,15 @@
 //   per colour wave (distance-2 colouring => all nodes of a wave touch
 //   disjoint blocks, so the wave is one batch):
 //     Compress (P:l.319-394): Gram of the stacked well-separated blocks
-//       (k_gemm) -> Jacobi eigen-solver + rank (k_jacobi) -> host reads the
-//       ranks -> R_k = A_k V written to the new P(b) <-> p_k blocks (k_gemm);
+//       (k_gemm2) -> symmetric eigen-solver + rank (k_tridiag_reg / k_tridiag_cl
+//       + k_eig_t ..., or k_rrqr with LORASP_RRQR) -> ranks (read by the host
+//       in the first sweep; predicted and verified afterwards, recorded graph)
+//       -> R_k = A_k V written to the new P(b) <-> p_k blocks (k_gemm2);
 //     Eliminate s then b (P:l.101-106, l.396-399), fused: gather the pivot
 //       K = [[S, V], [V^T, 0]] and coupling C into the node's record F
-//       (k_copy), K = L D L^T and L^{-1} (k_pivot), Z = L^{-1} C (k_gemm),
-//       Schur update T_ab -= Z_a^T D Z_b into the target blocks (k_gemm).
+//       (k_copy), K = L D L^T and L^{-1} (k_pivot_blk / LU: k_pivot_lu_blk),
+//       Z = L^{-1} C (k_gemm2), Schur update T_ab -= Z_a^T D Z_b into the target
+//       blocks (k_gemm2).
 //   The frozen records F = [L^{-1} | Z] are the factor used by apply().
 #include <cuda_runtime.h>
 
