@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -90,7 +91,7 @@ static int eig_generic_cap(int m) {
 // growable device buffer; growth synchronises the stream first (no in-flight use)
 // bumped by every device (re)allocation: a recorded factorization graph holds
 // raw pointers and is only replayed while this is unchanged
-static long long g_alloc_gen = 0;
+static std::atomic<long long> g_alloc_gen{0};   // handles may allocate from several threads
 struct CaptureAbort {};
 
 struct DevBuf {
@@ -2643,7 +2644,7 @@ bool factor_replay(lorasp_ctx *h, const double *values) {
   h->fgraph_used = false;
   const unsigned tsig = h->timing ? h->timing_mask : 0u;
   const bool want = !h->no_fgraph && !h->debug && h->replay_hits > 0 && h->fg_failures < 2;
-  if (want && h->fgraph && h->fg_gen == g_alloc_gen && h->fg_timing == tsig) return graph_launch(h, values);
+  if (want && h->fgraph && h->fg_gen == g_alloc_gen.load() && h->fg_timing == tsig) return graph_launch(h, values);
   if (!want) return factor_impl(h, values, true);
   if (h->fgraph) {
     cudaGraphExecDestroy(h->fgraph);
@@ -2690,7 +2691,7 @@ bool factor_replay(lorasp_ctx *h, const double *values) {
     return factor_impl(h, values, true);
   }
   CK(cudaMemcpy(h->fg_desc.p, h->stg.blob.data(), h->stg.blob.size(), cudaMemcpyHostToDevice));
-  h->fg_gen = g_alloc_gen;
+  h->fg_gen = g_alloc_gen.load();
   h->fg_timing = tsig;
   h->fg_pend = h->pend;
   h->pend.clear();
