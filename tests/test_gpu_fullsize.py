@@ -1,4 +1,5 @@
-"""GPU checks at BASELINE.json's full sizes (cfg3 64^3, cfg4 128^3, cfg5 1024^2),
+"""GPU checks at BASELINE.json's full sizes (cfg3 64^3, cfg4 128^3, cfg5 1024^2;
+cfg4 / cfg5 also with the RRQR compressor),
 in the launch configuration bench.py times (device buffers, re-factorization
 through the rank-predicted sweep and the recorded graph).  The oracle cannot
 factor these sizes, so the checks are properties that hold at any size
@@ -42,11 +43,13 @@ def _apply(h, v):
     return x.cpu().numpy()
 
 
-@pytest.mark.parametrize("name", ["cfg3", "cfg4", "cfg5"])
-def test_full_size_properties(L, name):
+@pytest.mark.parametrize("name,rrqr", [("cfg3", False), ("cfg4", False), ("cfg5", False), ("cfg4", True),
+                                       ("cfg5", True)])
+def test_full_size_properties(L, name, rrqr):
     p = make_problem(name)
     A = _csr(p)
-    h = L.analyze_problem(p)
+    flags = (L.LORASP_SPD if p.symmetric else 0) | (L.LORASP_RRQR if rrqr else 0)
+    h = L.analyze_problem(p, flags=flags)
     vals = torch.tensor(p.values, device="cuda")
     h.factor(vals)
     # structure of the level sweep
