@@ -2258,6 +2258,7 @@ __global__ void __launch_bounds__(NT, 1) k_rrqr(const EigTask *__restrict__ task
 struct PivTask {
   double *F;  // n x n at ld
   int ld, m, r, node;
+  double *F2;  // LU path: where U^{-T} goes (nullptr: F + ld * n, the record's region 1)
 };
 
 __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks,
@@ -2413,7 +2414,7 @@ __global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ ta
     __syncthreads();
   }
   // region 1 <- U^{-T} (lower): (U^{-T})(i, j) = U^{-1}(j, i) for i >= j
-  double *R1 = t.F + (int64_t)t.ld * n;
+  double *R1 = t.F2 ? t.F2 : t.F + (int64_t)t.ld * n;
   for (int j = warp; j < n; j += nw)
     for (int i = lane; i < n; i += 32) R1[i + (int64_t)j * t.ld] = (i >= j) ? A[j + (int64_t)i * lda] : 0.0;
   __syncthreads();
@@ -2851,7 +2852,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
     __syncthreads();
   }
   // region 0 <- L^{-1} (unit lower), region 1 <- U^{-T}
-  double *R1 = t.F + (int64_t)t.ld * n;
+  double *R1 = t.F2 ? t.F2 : t.F + (int64_t)t.ld * n;
   for (int j = warp; j < n; j += nw)
     for (int i = lane; i < n; i += 32) {
       t.F[i + (int64_t)j * t.ld] = (i > j) ? A[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);

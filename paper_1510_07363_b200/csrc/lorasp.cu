@@ -337,6 +337,7 @@ struct lorasp_ctx {
   size_t h_sp_cap = 0;
   bool no_split = getenv("LORASP_NO_SPLIT") != nullptr;
   bool gemm_v1 = getenv("LORASP_GEMM_V1") != nullptr;   // debug: the 256-thread 4 x 4 GEMM
+  bool no_split_lu = getenv("LORASP_NO_SPLIT_LU") != nullptr;   // A/B: fused LU pivots only
   // rank-predicted schedule: after a factorization, its ranks predict the
   // next one's (same pattern); the host then builds and enqueues every wave
   // without the per-wave rank synchronisation, the device ranks are logged
@@ -1308,7 +1309,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       std::vector<CopyTask> s_ct;
       std::vector<PivTask> s_pt;
       int s_max = 0;
-      if (sym && !comp.empty() && !h->no_split) {
+      if (!comp.empty() && !h->no_split && (sym || !h->no_split_lu)) {
         int64_t stot2 = 0;
         // A node is split when that pays: in waves wider than the GPU (the S
         // pivots then fill the sync gaps), or when its fused pivot would likely
@@ -1316,11 +1317,12 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         // at this level or the one below) and so take the launch-heavy blocked
         // path.  Otherwise the single fused k_pivot_blk is cheaper.
         const bool wide = elim.size() > 148;
+        const int pmax = sym ? PIVB_MAXN : PIVLU_MAXN;
         for (int c : elim)
-          if (m[c] <= PIVB_MAXN && m[c] >= h->split_min_m &&
-              (wide || h->split_min_m > 0 || m[c] + (int)std::ceil(rho_pred * m[c]) > PIVB_MAXN)) {
+          if (m[c] <= pmax && m[c] >= h->split_min_m &&
+              (wide || h->split_min_m > 0 || m[c] + (int)std::ceil(rho_pred * m[c]) > pmax)) {
             s_off[c] = stot2;
-            stot2 += (int64_t)m[c] * m[c];
+            stot2 += (sym ? 1 : 2) * (int64_t)m[c] * m[c];   // LU: L11^{-1} and U11^{-T}
           }
         if (stot2 > 0) {
           h->ws_S.ensure(stot2 * 8 + 256, st);
@@ -1371,8 +1373,13 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           dpt = reinterpret_cast<const PivTask *>(h->d_sp.as<char>() + s_ct.size() * sizeof(CopyTask));
         }
         launch_k(k_copy, (unsigned)s_ct.size(), 256, 0, h->stream2, dct);
-        const size_t smem = (size_t)(s_max | 1) * s_max * 8;
-        launch_k(k_pivot_blk, (unsigned)s_pt.size(), 512, smem, h->stream2, dpt, h->d_status.as<int>());
+        if (sym) {
+          const size_t smem = (size_t)(s_max | 1) * s_max * 8;
+          launch_k(k_pivot_blk, (unsigned)s_pt.size(), 512, smem, h->stream2, dpt, h->d_status.as<int>());
+        } else {   // no-pivot LU of S: L11^{-1} and U11^{-T} side by side in ws_S
+          const size_t smem = ((size_t)(s_max | 1) * s_max + 2 * (size_t)s_max * PIVB_NB) * 8;
+          launch_k(k_pivot_lu_blk, (unsigned)s_pt.size(), 512, smem, h->stream2, dpt, h->d_status.as<int>());
+        }
         h->launches_factor += 2;
         CK(cudaGetLastError());
         CK(cudaEventRecord(h->ev_s1, h->stream2));
@@ -1582,7 +1589,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         for (size_t e = 0; e < elim.size(); ++e) {
           const int c = elim[e];
           split_off[e] = yt;
-          if (s_off[c] >= 0) yt += ((int64_t)m[c] * r[c] + 31) & ~int64_t(31);
+          if (s_off[c] >= 0) yt += (sym ? 1 : 2) * (((int64_t)m[c] * r[c] + 31) & ~int64_t(31));
         }
         if (yt > 0) {
           h->ws_Y.ensure(yt * 8 + 256, st);
@@ -1699,6 +1706,29 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           t.mode = 1;
           t.alpha = 0.0;
           ct.push_back(t);
+        }
+        if (split && !sym) {   // LU: region 1 (1,1) = U11^{-T} from part 1, (1,2) = 0
+          double *R1 = F + (int64_t)ldF * n;
+          t = CopyTask{};
+          t.src = h->ws_S.as<double>() + s_off[c] + (int64_t)mc * mc;
+          t.lds = mc;
+          t.dst = R1;
+          t.ldd = ldF;
+          t.rows = mc;
+          t.cols = mc;
+          t.mode = 0;
+          t.alpha = 1.0;
+          ct.push_back(t);
+          if (rc > 0) {
+            t = CopyTask{};
+            t.dst = R1 + (int64_t)mc * ldF;
+            t.ldd = ldF;
+            t.rows = mc;
+            t.cols = rc;
+            t.mode = 1;
+            t.alpha = 0.0;
+            ct.push_back(t);
+          }
         }
         if (!split && rc > 0) {
           t = CopyTask{};
@@ -1828,6 +1858,37 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         // pivot
         if (!split) {
           pv.push_back(PivTask{F, ldF, mc, rc, c});
+        } else if (rc > 0 && !sym) {
+          // LU part 2 (K = [[S, V], [V^T, 0]] = L U, S = L11 U11 from part 1):
+          // Y = L11^{-1} V (= U12), Zt = U11^{-T} V (= L21^T), L22 U22 = -Zt^T Y;
+          // (L^{-1})21 = -L22^{-1} (Zt^T L11^{-1}), (U^{-T})21 = -U22^{-T} (Y^T U11^{-T})
+          double *R1 = F + (int64_t)ldF * n;
+          double *Yb = h->ws_Y.as<double>() + split_off[e];
+          double *Zt = Yb + (((int64_t)mc * rc + 31) & ~int64_t(31));
+          double *T1 = h->ws_T1.as<double>() + split_off[e];
+          double *T2 = T1 + (((int64_t)mc * rc + 31) & ~int64_t(31));
+          auto gt = [&](std::vector<GemmTask> &tl, std::vector<GemmSeg> &sl, double *C, int ldc, int M, int N, int ta,
+                        GemmSeg g) {
+            GemmTask q{};
+            q.C = C;
+            q.ldc = ldc;
+            q.M = M;
+            q.N = N;
+            q.ta = ta;
+            q.beta = 0;
+            q.seg0 = (int)sl.size();
+            q.nseg = 1;
+            sl.push_back(g);
+            add_tiles(tl, q);
+          };
+          gt(sy_t, sy_s, Yb, mc, mc, rc, 0, GemmSeg{F, V, ldF, mc, mc, 1.0});
+          gt(sy_t, sy_s, Zt, mc, mc, rc, 0, GemmSeg{R1, V, ldF, mc, mc, 1.0});
+          gt(sg_t, sg_s, F + mc + (int64_t)mc * ldF, ldF, rc, rc, 1, GemmSeg{Zt, Yb, mc, mc, mc, -1.0});
+          gt(sg_t, sg_s, T1, rc, rc, mc, 1, GemmSeg{Zt, F, mc, ldF, mc, 1.0});
+          gt(sg_t, sg_s, T2, rc, rc, mc, 1, GemmSeg{Yb, R1, mc, ldF, mc, 1.0});
+          pv.push_back(PivTask{F + mc + (int64_t)mc * ldF, ldF, rc, 0, c, R1 + mc + (int64_t)mc * ldF});
+          gt(sx_t, sx_s, F + mc, ldF, rc, mc, 0, GemmSeg{F + mc + (int64_t)mc * ldF, T1, ldF, rc, rc, -1.0});
+          gt(sx_t, sx_s, R1 + mc, ldF, rc, mc, 0, GemmSeg{R1 + mc + (int64_t)mc * ldF, T2, ldF, rc, rc, -1.0});
         } else if (rc > 0) {
           // part 2: Y = L11^{-1} V, L21 = Y^T, L22 = chol(Y^T Y) (K22 = 0 and
           // D2 = -I), X21 = -L22^{-1} Y^T L11^{-1}
@@ -2061,6 +2122,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           cudaEventRecord(pe0, st);
         }
         pivots_lu(h, pv, f_piv, b_piv);
+        if (!sx_t.empty()) launch_gemm(h, sx_t, sx_s, K_PIVOT, 0, 0);
         if (h->debug) {
           cudaEventRecord(pe1, st);
           cudaEventSynchronize(pe1);
