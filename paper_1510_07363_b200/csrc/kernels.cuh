@@ -3450,7 +3450,7 @@ __global__ void k_axpby(int64_t n, double a, const double *__restrict__ x, doubl
   pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = a * x[i] + b * y[i];
+    y[i] = (b == 0.0) ? a * x[i] : a * x[i] + b * y[i];   // b = 0: y is output only (may be uninitialised)
 }
 // z = x - y
 __global__ void k_sub(int64_t n, const double *__restrict__ x, const double *__restrict__ y,

@@ -97,6 +97,7 @@ struct CaptureAbort {};
 struct DevBuf {
   void *p = nullptr;
   size_t cap = 0;
+  const char *tag = "";   // debug name (LORASP_POISON=<tag>|all NaN-fills new allocations)
   void ensure(size_t bytes, cudaStream_t st) {
     if (bytes <= cap) return;
     {
@@ -115,6 +116,11 @@ struct DevBuf {
     if (cudaMalloc(&p, nb) != cudaSuccess) {
       cudaGetLastError();
       throw Err(LORASP_E_OOM, "device allocation of " + std::to_string(nb) + " bytes failed");
+    }
+    static const char *poison = getenv("LORASP_POISON");   // debug: NaN-fill new buffers
+    if (poison && (!strcmp(poison, "all") || (tag[0] && strstr(poison, tag)))) {
+      cudaMemset(p, 0xFF, nb);   // legacy stream: completes before any later work on the library's streams
+      cudaDeviceSynchronize();
     }
     cap = nb;
   }
@@ -148,6 +154,11 @@ struct Pool {
       if (cudaMalloc(&p, cap * sizeof(double)) != cudaSuccess) {
         cudaGetLastError();
         throw Err(LORASP_E_OOM, "factor pool allocation failed");
+      }
+      if (getenv("LORASP_POISON") && (!strcmp(getenv("LORASP_POISON"), "all") || strstr(getenv("LORASP_POISON"), "pool")))
+      {
+        cudaMemset(p, 0xFF, cap * sizeof(double));   // debug: NaN-fill
+        cudaDeviceSynchronize();
       }
       chunks.push_back({p, cap});
       used = 0;
@@ -577,6 +588,16 @@ static void set_eig_attrs() {
 }
 
 void ensure_mem(lorasp_ctx *h) {
+  {
+    struct {
+      DevBuf *b;
+      const char *t;
+    } tg[] = {{&h->arena[0], "arena"}, {&h->arena[1], "arena"}, {&h->ws_G, "ws_G"}, {&h->ws_V, "ws_V"},
+              {&h->ws_sig, "ws_sig"}, {&h->ws_X, "ws_X"}, {&h->ws_ctr, "ws_ctr"}, {&h->ws_piv, "ws_piv"},
+              {&h->ws_S, "ws_S"}, {&h->ws_Y, "ws_Y"}, {&h->ws_T1, "ws_T1"}, {&h->d_ranks, "d_ranks"},
+              {&h->d_vec, "d_vec"}, {&h->d_y, "d_y"}, {&h->d_kry, "d_kry"}, {&h->fg_desc, "fg_desc"}};
+    for (auto &x : tg) x.b->tag = x.t;
+  }
   if (h->mem_ready) return;
   CK(cudaSetDevice(h->device));
   const Plan &pl = h->plan;
@@ -1234,6 +1255,8 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
     DevBuf &ar = h->arena[i & 1];
     ar.ensure(std::max<int64_t>(tot, 32) * sizeof(double), st);
     CK(cudaMemsetAsync(ar.p, 0, tot * sizeof(double), st));
+    if (getenv("LORASP_POISON_TAIL") && ar.cap > (size_t)tot * 8)   // debug: NaN beyond the level's slots
+      CK(cudaMemsetAsync(ar.as<char>() + tot * 8, 0xFF, ar.cap - (size_t)tot * 8, st));
     double *base = ar.as<double>();
     auto slot_ptr = [&](int s) { return base + soff[s]; };
     // distributed mode: the owner of each node of this level (include/lorasp.h)
