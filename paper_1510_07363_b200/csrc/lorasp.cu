@@ -2100,9 +2100,13 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       }
       h->piv_maxn_hint = dist ? (sym ? pv_max_small : pv_max_all) : 0;
       // all descriptors of the wave travel in one H2D copy
-      h->stg.reserve(vbytes(pt) + vbytes(ps) + vbytes(ct) + vbytes(zt) + vbytes(zs) + vbytes(stt) + vbytes(ss), st);
-      GemmTask *d_pt = pushd(h, pt), *d_zt = pushd(h, zt), *d_stt = pushd(h, stt);
-      GemmSeg *d_ps = pushd(h, ps), *d_zs = pushd(h, zs), *d_ss = pushd(h, ss);
+      // descriptors in two groups: the pivot section below pushes its own task
+      // lists, and a staging-ring wrap there (which reuses the ring after
+      // synchronising) would overwrite descriptors pushed earlier but consumed
+      // later — so Z / Schur descriptors are pushed after the pivots
+      h->stg.reserve(vbytes(pt) + vbytes(ps) + vbytes(ct), st);
+      GemmTask *d_pt = pushd(h, pt);
+      GemmSeg *d_ps = pushd(h, ps);
       CopyTask *d_ct = pushd(h, ct);
       h->stg.flush(st);
       h->t_host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
@@ -2162,6 +2166,10 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           cudaEventDestroy(pe1);
         }
       }
+      h->stg.reserve(vbytes(zt) + vbytes(zs) + vbytes(stt) + vbytes(ss), st);
+      GemmTask *d_zt = pushd(h, zt), *d_stt = pushd(h, stt);
+      GemmSeg *d_zs = pushd(h, zs), *d_ss = pushd(h, ss);
+      h->stg.flush(st);
       launch_gemm_dev(h, d_zt, d_zs, zt.size(), K_ZGEMM, f_z, b_z);
       launch_gemm_dev(h, d_stt, d_ss, stt.size(), K_SCHUR, f_s, b_s);
       if (dist) dist_exchange(h, dirty);
