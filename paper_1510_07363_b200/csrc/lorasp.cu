@@ -744,7 +744,8 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
       if (!rc[c].empty()) ds[c] = (single && rc[c].size() == et.size()) ? de : push(h, rc[c]);
     // with cluster / generic tasks in the same wave the register-tile pair runs
     // on its own stream beside them (few nodes per class: the SMs are idle)
-    reg_fork = !single && !h->eig_split_classes;
+    static const bool no_fork = getenv("LORASP_EIG_NO_FORK") != nullptr;   // A/B: one stream
+    reg_fork = !single && !h->eig_split_classes && !no_fork;
     cudaStream_t rs = h->stream;
     if (reg_fork) {
       CK(cudaEventRecord(h->ev_ef, h->stream));
@@ -767,7 +768,7 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
         dc[c] = push(h, clt[c]);
         ++ncls;
       }
-    const bool fork = ncls > 1 && !h->eig_split_classes;
+    const bool fork = ncls > 1 && !h->eig_split_classes && !getenv("LORASP_EIG_NO_FORK");
     if (fork) CK(cudaEventRecord(h->ev_cf, h->stream));
     for (int c = 1; c <= 3; ++c) {
       if (!dc[c]) continue;
