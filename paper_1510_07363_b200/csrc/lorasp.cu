@@ -195,9 +195,19 @@ struct Staging {
     if (used + need <= cap) return;
     flush(st);
     CK(cudaStreamSynchronize(st));
+    sync_side();
     used = 0;
     pend = 0;
     if (need > cap) init(std::max(need, cap * 2), st);
+  }
+  // Kernels on the side streams (split pivots on stream2, eigen-solver classes)
+  // read descriptors from the device ring too: a wrap or reset must wait for
+  // them as well as for `st`, else the next H2D copy on `st` overwrites
+  // descriptors a pending side-stream kernel has yet to read.
+  std::vector<cudaStream_t> side;
+  void sync_side() {
+    for (cudaStream_t s : side)
+      if (s) CK(cudaStreamSynchronize(s));
   }
   // copy `bytes` of src into staging; the H2D copy of everything pushed since
   // the last flush() is one cudaMemcpyAsync (descriptors of a whole wave travel
@@ -226,6 +236,7 @@ struct Staging {
     if (used + need > cap) {
       flush(st);
       CK(cudaStreamSynchronize(st));
+      sync_side();
       used = 0;
       pend = 0;
       if (need > cap) init(std::max(need, cap * 2), st);
@@ -245,8 +256,9 @@ struct Staging {
     flush(st);
     return dp;
   }
-  void reset() {   // only after a stream sync
+  void reset() {   // only after a sync of `st`
     if (cap_mode) return;
+    sync_side();
     used = 0;
     pend = 0;
   }
@@ -621,6 +633,7 @@ void ensure_mem(lorasp_ctx *h) {
     CK(cudaStreamCreateWithPriority(&h->stream_hi, cudaStreamNonBlocking, greatest));
     CK(cudaStreamCreateWithPriority(&h->stream_eig, cudaStreamNonBlocking, greatest));
     for (auto &cs : h->stream_cl) CK(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, greatest));
+    h->stg.side = {h->stream2, h->stream_hi, h->stream_eig, h->stream_cl[0], h->stream_cl[1]};
   }
   CK(cudaEventCreateWithFlags(&h->ev_cf, cudaEventDisableTiming));
   for (auto &e : h->ev_cj) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -3284,6 +3297,8 @@ void lorasp_destroy(lorasp_handle h) {
     h->ws_Y.release();
     h->ws_T1.release();
     h->d_sp.release();
+    h->d_apparts.release();
+    h->d_upart.release();
     h->fpool.release();
     h->stg.release();
     if (h->h_ranks) cudaFreeHost(h->h_ranks);
