@@ -107,7 +107,9 @@ struct DevBuf {
     }
     ++g_alloc_gen;
     if (p) {
-      CK(cudaStreamSynchronize(st));
+      // side streams (split pivots, eigen classes) may read any workspace: growth
+      // is rare, so wait for the whole device rather than only `st`
+      CK(cudaDeviceSynchronize());
       CK(cudaFree(p));
       p = nullptr;
       cap = 0;
@@ -132,6 +134,16 @@ struct DevBuf {
     cap = 0;
   }
 };
+
+// Host -> device upload of a pageable host buffer, ordered on `st` and complete on
+// return.  A plain cudaMemcpy from pageable memory goes on the legacy stream and may
+// return before its DMA lands; kernels on the library's non-blocking streams are not
+// ordered after it (a fresh handle could then read recycled memory).
+static void h2d_sync(void *dst, const void *src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+}
 
 // bump pool of device chunks for the frozen factor records
 struct Pool {
@@ -256,9 +268,11 @@ struct Staging {
     flush(st);
     return dp;
   }
-  void reset() {   // only after a sync of `st`
+  // Only after a sync of `st`.  Side-stream readers of the ring (eigen classes,
+  // split-pivot part 2) are joined into `st` by events before that sync; wraps
+  // inside a wave (push_deferred / reserve) still wait for the side streams.
+  void reset() {
     if (cap_mode) return;
-    sync_side();
     used = 0;
     pend = 0;
   }
@@ -615,8 +629,8 @@ void ensure_mem(lorasp_ctx *h) {
   const Plan &pl = h->plan;
   h->d_rowptr.ensure((pl.n + 1) * sizeof(int64_t), h->stream);
   h->d_colidx.ensure(std::max<int64_t>(1, pl.nnz) * sizeof(int64_t), h->stream);
-  CK(cudaMemcpy(h->d_rowptr.p, pl.row_ptr.data(), (pl.n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(h->d_colidx.p, pl.col_idx.data(), pl.nnz * sizeof(int64_t), cudaMemcpyHostToDevice));
+  h2d_sync(h->d_rowptr.p, pl.row_ptr.data(), (pl.n + 1) * sizeof(int64_t), h->stream);
+  h2d_sync(h->d_colidx.p, pl.col_idx.data(), pl.nnz * sizeof(int64_t), h->stream);
   h->d_values.ensure(std::max<int64_t>(1, pl.nnz) * sizeof(double), h->stream);
   h->d_status.ensure(64, h->stream);
   CK(cudaMallocHost(&h->h_ranks, sizeof(int) * (1 << 20)));
@@ -1287,7 +1301,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           if (pl.nnz_slot[k] >= 0)
             dest[k] = soff[pl.nnz_slot[k]] + pl.nnz_r[k] + (int64_t)pl.nnz_c[k] * sld[pl.nnz_slot[k]];
         h->d_dest.ensure(std::max<int64_t>(1, pl.nnz) * sizeof(int64_t), st);
-        CK(cudaMemcpy(h->d_dest.p, dest.data(), pl.nnz * sizeof(int64_t), cudaMemcpyHostToDevice));
+        h2d_sync(h->d_dest.p, dest.data(), pl.nnz * sizeof(int64_t), st);
         h->leaf_soff = soff;
         h->dest_ready = true;
       }
@@ -2325,7 +2339,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
   }
   h->d_apparts.ensure(std::max<size_t>(1, parts.size()) * sizeof(ApPart), st);
   if (!parts.empty())
-    CK(cudaMemcpy(h->d_apparts.p, parts.data(), parts.size() * sizeof(ApPart), cudaMemcpyHostToDevice));
+    h2d_sync(h->d_apparts.p, parts.data(), parts.size() * sizeof(ApPart), st);
   h->d_upart.ensure(std::max<int64_t>(utot, 8) * 8, st);
   h->ap_wave_flops.assign(h->ap_wave_begin.size() - 1, 0.0);
   h->ap_wave_bytes.assign(h->ap_wave_begin.size() - 1, 0.0);
@@ -2401,12 +2415,12 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
   }
   h->d_apnodes.ensure(std::max<size_t>(1, an.size()) * sizeof(ApNode), st);
   h->d_apsegs.ensure(std::max<size_t>(1, as.size()) * sizeof(ApSeg), st);
-  CK(cudaMemcpy(h->d_apnodes.p, an.data(), an.size() * sizeof(ApNode), cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(h->d_apsegs.p, as.data(), as.size() * sizeof(ApSeg), cudaMemcpyHostToDevice));
+  h2d_sync(h->d_apnodes.p, an.data(), an.size() * sizeof(ApNode), st);
+  h2d_sync(h->d_apsegs.p, as.data(), as.size() * sizeof(ApSeg), st);
   std::vector<int64_t> perm(pl.n);
   for (int64_t q = 0; q < pl.n; ++q) perm[q] = voff[L][pl.leaf_of[q]] + pl.leaf_pos[q];
   h->d_perm.ensure(pl.n * sizeof(int64_t), st);
-  CK(cudaMemcpy(h->d_perm.p, perm.data(), pl.n * sizeof(int64_t), cudaMemcpyHostToDevice));
+  h2d_sync(h->d_perm.p, perm.data(), pl.n * sizeof(int64_t), st);
   h->d_vec.ensure(std::max<int64_t>(tot, 8) * 8, st);
   h->d_b.ensure(pl.n * 8, st);
   h->d_x.ensure(pl.n * 8, st);
@@ -2797,7 +2811,7 @@ bool factor_replay(lorasp_ctx *h, const double *values) {
     h->pend.clear();
     return factor_impl(h, values, true);
   }
-  CK(cudaMemcpy(h->fg_desc.p, h->stg.blob.data(), h->stg.blob.size(), cudaMemcpyHostToDevice));
+  h2d_sync(h->fg_desc.p, h->stg.blob.data(), h->stg.blob.size(), h->stream);
   h->fg_gen = g_alloc_gen.load();
   h->fg_timing = tsig;
   h->fg_pend = h->pend;
@@ -3255,7 +3269,11 @@ void lorasp_destroy(lorasp_handle h) {
   if (!h) return;
   if (h->mem_ready) {
     cudaSetDevice(h->device);
+    // every library stream drains before any buffer is released (a factorization
+    // that threw may have left split-pivot / eigen work in flight)
     cudaStreamSynchronize(h->stream);
+    for (cudaStream_t s : {h->stream2, h->stream_hi, h->stream_eig, h->stream_cl[0], h->stream_cl[1]})
+      if (s) cudaStreamSynchronize(s);
     DevBuf *bufs[] = {&h->d_values, &h->d_rowptr, &h->d_colidx, &h->d_dest, &h->arena[0], &h->arena[1],
                       &h->ws_G, &h->ws_V, &h->ws_sig, &h->ws_X, &h->ws_ctr, &h->ws_piv, &h->d_ranks,
                       &h->d_status,
