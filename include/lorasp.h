@@ -130,6 +130,15 @@ int lorasp_gmres(lorasp_handle h, const double *b, double *x, double tol);
 int lorasp_krylov_ex(lorasp_handle h, const double *b, double *x, double tol,
                      int method, int restart, int max_it, int *iters, double *relres);
 
+/*
+ * lorasp_paper_residual — the paper's preconditioned residual, Eq. GMRES_residual
+ *   (P:l.665-669): *out = ||Ã b - Ã A x||_2 / ||Ã b||_2, computed on the device
+ *   (SpMV with the values of the last lorasp_factor, two applications of Ã).
+ *   b, x: n float64, host or device (both of the same kind); out: host double.
+ *   LORASP_E_STATE before a successful factorization.
+ */
+int lorasp_paper_residual(lorasp_handle h, const double *b, const double *x, double *out);
+
 /* Use an existing cudaStream_t (passed as void*) for all device work; NULL = default. */
 int lorasp_set_stream(lorasp_handle h, void *cuda_stream);
 

@@ -2944,6 +2944,36 @@ int lorasp_krylov_ex(lorasp_handle h, const double *b, double *x, double tol, in
   });
 }
 
+// Eq. GMRES_residual (P:l.665-669): ||Ã b - Ã A x||_2 / ||Ã b||_2, all on the device
+// (SpMV, two preconditioner applications, dot products in the library's kernels)
+int lorasp_paper_residual(lorasp_handle h, const double *b, const double *x, double *out) {
+  return guarded(h, [&]() {
+    if (!b || !x || !out) return (int)LORASP_E_ARG;
+    if (!h->factored) return (int)LORASP_E_STATE;
+    CK(cudaSetDevice(h->device));
+    const int64_t n = h->plan.n;
+    h->d_kry.ensure(6 * n * 8, h->stream);
+    double *w = h->d_kry.as<double>(), *ab = w + n, *aax = ab + n, *bd = aax + n, *xd = bd + n, *ax = xd + n;
+    cudaStream_t st = h->stream;
+    const bool dev = is_device_ptr(b) && is_device_ptr(x);
+    if (!dev) {
+      CK(cudaMemcpyAsync(bd, b, n * 8, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(xd, x, n * 8, cudaMemcpyHostToDevice, st));
+      b = bd;
+      x = xd;
+    }
+    h->launches_krylov = 0;
+    apply_dev(h, b, ab, &h->launches_krylov);            // Ã b
+    spmv_dev(h, x, ax);                                  // A x
+    apply_dev(h, ax, aax, &h->launches_krylov);          // Ã A x
+    launch_k(k_sub, grid1(n), 256, 0, st, n, ab, aax, w);
+    const double num = dot_dev(h, w, w), den = dot_dev(h, ab, ab);
+    *out = den > 0.0 ? std::sqrt(num / den) : 0.0;
+    tflush(h);
+    return (int)LORASP_OK;
+  });
+}
+
 int lorasp_gmres(lorasp_handle h, const double *b, double *x, double tol) {
   return lorasp_krylov_ex(h, b, x, tol, LORASP_GMRES, 50, 500, nullptr, nullptr);
 }

@@ -37,7 +37,7 @@ SYMBOLS = ["lorasp_analyze", "lorasp_factor", "lorasp_apply", "lorasp_gmres", "l
            "lorasp_set_stream", "lorasp_set_timing", "lorasp_get_depth", "lorasp_get_level_order", "lorasp_get_ranks",
            "lorasp_get_sizes", "lorasp_get_stats", "lorasp_get_launch_count", "lorasp_test_eig",
            "lorasp_test_pivot", "lorasp_last_error", "lorasp_destroy", "lorasp_set_dist",
-           "lorasp_set_dist_buffers", "lorasp_dist_owner"]
+           "lorasp_set_dist_buffers", "lorasp_dist_owner", "lorasp_paper_residual"]
 
 LORASP_COLL_ALLGATHER = 0
 LORASP_COLL_MAXINT = 1
@@ -72,6 +72,7 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lorasp_gmres.argtypes = [P, P, P, ctypes.c_double]
     lib.lorasp_krylov_ex.argtypes = [P, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+    lib.lorasp_paper_residual.argtypes = [P, P, P, ctypes.POINTER(ctypes.c_double)]
     lib.lorasp_set_stream.argtypes = [P, P]
     lib.lorasp_set_timing.argtypes = [P, ctypes.c_int]
     lib.lorasp_get_depth.argtypes = [P, ctypes.POINTER(ctypes.c_int)]
@@ -154,6 +155,13 @@ class Handle:
                                                     int(restart), int(max_it), ctypes.byref(it),
                                                     ctypes.byref(rr)), "lorasp_krylov_ex")
         return rc, it.value, rr.value
+
+    def paper_residual(self, b, x) -> float:
+        """Eq. GMRES_residual (P:l.665-669): ||Ã b - Ã A x|| / ||Ã b|| (on the device)."""
+        out = ctypes.c_double()
+        self._check(self._lib.lorasp_paper_residual(self.h, _ptr(b), _ptr(x), ctypes.byref(out)),
+                    "lorasp_paper_residual")
+        return out.value
 
     def set_stream(self, stream_ptr: int):
         return self._check(self._lib.lorasp_set_stream(self.h, ctypes.c_void_p(stream_ptr)), "set_stream")

@@ -310,3 +310,23 @@ def test_lu_ranks_apply_gmres_parity(L, dims, depth, eps):
     ro = O.gmres(mv, lambda v: O.solve(f, v), p.b, tol=1e-10, restart=50)
     assert rc == 0 and rr <= 1e-10 and abs(it - ro.iters) <= 1
     h.close()
+
+
+@pytest.mark.parametrize("kind,dims,depth,eps", [("poisson", (32, 32), 6, 1e-2), ("upwind", (32, 32), 6, 1e-3)])
+def test_paper_preconditioned_residual_parity(L, kind, dims, depth, eps):
+    """Eq. GMRES_residual (P:l.665-669) computed on the device through the C ABI
+    (lorasp_paper_residual) vs the C++ oracle on the same x; at eps = 0 it is the
+    relative error of x (Ã = A^{-1})."""
+    from oracle import cpp_oracle as CO
+    p = make_problem("cfg1", dims=dims, kind=kind, depth=depth)
+    x = np.linalg.solve(csr_to_dense(p.n, p.row_ptr, p.col_idx, p.values), p.b)
+    x = x + 1e-4 * np.random.default_rng(9).standard_normal(p.n)
+    for e in (0.0, eps):
+        h = L.analyze_problem(p, eps=e)
+        h.factor(torch.tensor(p.values, device="cuda"))
+        g = h.paper_residual(torch.tensor(p.b, device="cuda"), torch.tensor(x, device="cuda"))
+        gh = h.paper_residual(np.ascontiguousarray(p.b), np.ascontiguousarray(x))   # host buffers
+        f = CO.factorize(p.n, p.row_ptr, p.col_idx, p.values, p.coords, depth, e)
+        o = CO.paper_preconditioned_residual(f, p.row_ptr, p.col_idx, p.values, p.b, x)
+        assert abs(g - o) <= 1e-8 * o and g == gh
+        h.close()
