@@ -17,8 +17,17 @@ solve then runs replicated); strong scaling: value = n * K / max-over-ranks
 factor time.  --mode replicas: every rank factors its own replica (weak
 scaling, no data-path collective).  Barrier + max-over-ranks timing.
 
---impl reference times the CPU oracle (oracle/, plain numpy, sequential) on
-the same workload (rank 0 only).
+--impl reference times the CPU oracle (oracle/cpp, C++17 plain loops, OpenMP
+across the nodes of a colour wave, all host cores) on the same workload (rank 0
+only).  `--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N processes; a mismatching WORLD_SIZE is an error.
+
+Besides the timed re-factorizations the line reports: the first factorization
+of a fresh handle (allocation + per-wave rank synchronisation) and the host
+analyze time; a re-factorization with CHANGED values whose ranks differ (the
+rank prediction misses and the synchronised sweep runs); the paper's
+preconditioned residual Eq. GMRES_residual (P:l.665-669) at the final iterate;
+and (default for cfg2) the same measurement on cfg4, the largest 1-GPU config.
 """
 from __future__ import annotations
 
@@ -152,42 +161,63 @@ def weak_scaling_value(n, world, steps, max_total_ms):
     return n * world * steps / (max_total_ms / 1e3)
 
 
-def cpu_baseline(p, sample="factor+krylov", compressor="svd"):
-    """The oracle as it stands, on the host cores, on one bounded sample."""
-    from oracle import lorasp_oracle as O
-    t0 = time.perf_counter()
-    f = O.factorize(p.n, p.row_ptr, p.col_idx, p.values, p.coords, p.depth, p.eps, compressor=compressor)
-    tf = time.perf_counter() - t0
-    out = {"value": p.n / tf, "unit": "unknowns/s", "cores": O.ORACLE_THREADS, "kind": "oracle",
-           "factor_s": tf, "host_cpus": os.cpu_count()}
-    if sample == "factor+krylov":
-        mv = lambda v: O.spmv(p.row_ptr, p.col_idx, p.values, v)
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(p, compressor="svd"):
+    """The oracle as it stands (C++17, oracle/cpp) on the host cores, on one bounded
+    sample: one full factorization + the Krylov solve of this workload, with all
+    host threads and with 1 thread."""
+    from oracle import cpp_oracle as CO
+    out = {"unit": "unknowns/s", "kind": "oracle", "host_cpus": os.cpu_count(), "cpu_model": _cpu_model()}
+    for th in (CO.default_threads(), 1):
         t0 = time.perf_counter()
-        kry = O.pcg if p.solver == "cg" else O.gmres
-        r = kry(mv, lambda v: O.solve(f, v), p.b, tol=1e-10)
-        out["krylov_s"] = time.perf_counter() - t0
-        out["krylov_iters"] = r.iters
-        out["sample"] = (f"1 full {p.name} factorization (n={p.n}) + {p.solver.upper()} to 1e-10 "
-                         f"({r.iters} iters), numpy oracle, 1 BLAS thread")
-    return out, f
+        f = CO.factorize(p.n, p.row_ptr, p.col_idx, p.values, p.coords, p.depth, p.eps, compressor=compressor,
+                         threads=th)
+        tf = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        r = CO.krylov(f, p.row_ptr, p.col_idx, p.values, p.b, method=p.solver, tol=1e-10, restart=50)
+        tk = time.perf_counter() - t0
+        f.close()
+        rec = {"value": p.n / tf, "cores": th, "factor_s": tf, "krylov_s": tk, "krylov_iters": r.iters}
+        if th == 1:
+            out["single_thread"] = rec
+        else:
+            out.update(rec)
+        if th == 1 or CO.default_threads() == 1:
+            break
+    out["sample"] = (f"1 full {p.name} factorization (n={p.n}) + {p.solver.upper()} to 1e-10 "
+                     f"({out['krylov_iters']} iters), C++ oracle (oracle/cpp), {out['cores']} threads; "
+                     f"single_thread = the same with 1 thread")
+    return out
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return 0
     from synth import make_problem
-    from oracle import lorasp_oracle as O
+    from oracle import cpp_oracle as CO
     p = make_problem(args.config, R=args.adv_R) if args.config == "adv32" else make_problem(args.config)
+    th = CO.default_threads()
     times = []
+    f = None
     for s in range(args.warmup + args.steps):
+        if f is not None:
+            f.close()
         t0 = time.perf_counter()
-        f = O.factorize(p.n, p.row_ptr, p.col_idx, p.values, p.coords, p.depth, p.eps)
+        f = CO.factorize(p.n, p.row_ptr, p.col_idx, p.values, p.coords, p.depth, p.eps, threads=th)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
-    mv = lambda v: O.spmv(p.row_ptr, p.col_idx, p.values, v)
     t0 = time.perf_counter()
-    kr = (O.pcg if p.solver == "cg" else O.gmres)(mv, lambda v: O.solve(f, v), p.b, tol=1e-10)
+    kr = CO.krylov(f, p.row_ptr, p.col_idx, p.values, p.b, method=p.solver, tol=1e-10, restart=50)
     tk = time.perf_counter() - t0
     tf = sum(times) / len(times)
     val = p.n / tf
@@ -195,14 +225,66 @@ def run_reference(args, world, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tf, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.config}: {WORKLOADS.get(args.config, '')}", "n": p.n,
-                       "eps": p.eps, "depth": p.depth, "parallelism": "rank 0 only (host CPU)"},
+                       "eps": p.eps, "depth": p.depth, "parallelism": f"rank 0 only (host CPU, {th} threads)"},
             "krylov_ms": 1e3 * tk, "krylov_iters": kr.iters, "relres": kr.relres,
-            "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": O.ORACLE_THREADS, "kind": "oracle",
-                             "sample": f"each step = 1 full {args.config} factorization (n={p.n}), numpy "
-                                       "oracle, 1 BLAS thread; PCG timed once after the steps"},
+            "cpu_baseline": {"value": val, "unit": "unknowns/s", "cores": th, "kind": "oracle",
+                             "cpu_model": _cpu_model(),
+                             "sample": f"each step = 1 full {args.config} factorization (n={p.n}), C++ oracle "
+                                       f"(oracle/cpp), {th} threads; the Krylov solve timed once after the steps"},
             "e2e": {"value": val, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
+
+
+def relaunch_under_torchrun(n):
+    """`bench.py --gpus N` outside torchrun: one process per GPU via torch.distributed.run."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def measure_config(L, name, dev, steps=3, warmup=3):
+    """Compact measurement of another config in the same run (cfg4 beside cfg2):
+    fresh handle, first factorization, warm-ups, `steps` timed re-factorizations
+    + Krylov (CUDA events, L2 flushed before each)."""
+    import torch
+    from synth import make_problem
+    p = make_problem(name)
+    t0 = time.perf_counter()
+    h = L.analyze_problem(p, device=dev.index or 0)
+    t_an = time.perf_counter() - t0
+    vals = torch.tensor(p.values, device=dev)
+    b = torch.tensor(p.b, device=dev)
+    x = torch.empty_like(b)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    method = L.LORASP_CG if p.solver == "cg" else L.LORASP_GMRES
+    res = []
+    for s in range(warmup + steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        h.factor(vals)
+        ev[1].record()
+        rc, it, rr = h.krylov(b, x, tol=1e-10, method=method, restart=50)
+        ev[2].record()
+        torch.cuda.synchronize()
+        res.append((ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), it, rr, rc))
+    st = h.stats()
+    tf = sum(r[0] for r in res[warmup:]) / steps
+    tk = sum(r[1] for r in res[warmup:]) / steps
+    out = {"workload": f"{name}: {WORKLOADS[name]}", "n": p.n, "value": p.n / (tf / 1e3), "unit": "unknowns/s",
+           "factor_ms": tf, "krylov_ms": tk, "krylov_iters": res[-1][2], "relres": res[-1][3],
+           "krylov_status": res[-1][4], "first_factor_ms": res[0][0], "analyze_s": t_an,
+           "tflops_model": st["flops_model"] / (tf / 1e3) / 1e12, "flops_model": st["flops_model"],
+           "factor_graph": st.get("factor_graph"), "steps": steps, "warmup": warmup,
+           "paper_residual": h.paper_residual(b, x)}
+    h.close()
+    return out
 
 
 def main():
@@ -219,9 +301,16 @@ def main():
                     help="Compress: SVD rule (Eq. cutOff1, the metric's workload) or pivoted QR (f1)")
     ap.add_argument("--mode", default="partition", choices=["partition", "replicas"],
                     help="N > 1: subtree partition of one problem (strong) or independent replicas (weak)")
+    ap.add_argument("--extra", default="auto",
+                    help="other config measured in the same run (auto: cfg4 when --config cfg2; none: off)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3     # timing rule: >= 3 warm-up steps
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch_under_torchrun(args.gpus)
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}\n")
+        return 2
     world, rank, local = dist_init()
     if args.impl == "reference":
         return run_reference(args, world, rank)
@@ -234,7 +323,9 @@ def main():
     dev = torch.device("cuda", local)
     p = make_problem(args.config, R=args.adv_R) if args.config == "adv32" else make_problem(args.config)
     flags = (L.LORASP_SPD if p.symmetric else 0) | (L.LORASP_RRQR if args.compressor == "rrqr" else 0)
+    t_an0 = time.perf_counter()
     h = L.analyze_problem(p, device=local, flags=flags)
+    t_analyze = time.perf_counter() - t_an0
     part = world > 1 and args.mode == "partition"
     if part:
         from paper_1510_07363_b200.dist import TorchComm
@@ -259,10 +350,13 @@ def main():
         fl, al, kl = h.launch_counts()
         return ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), it, rr, rc, fl + kl
 
+    first = None
     for wi in range(args.warmup):
         if wi == args.warmup - 1:
             h.set_timing(True)      # last warm-up step: per-class breakdown (all classes)
-        step(False)
+        r = step(False)
+        if first is None:
+            first = r               # a fresh handle's first factorization (allocation, rank syncs)
     warm_kernels = h.stats().get("kernels", {})
     # the timed region times only the dominant class (2 event records per launch of it)
     dom_cls = max(warm_kernels.values(), key=lambda v: v["ms"])["class"] if warm_kernels else 0
@@ -293,6 +387,31 @@ def main():
         dist.barrier()
     stats = h.stats()
     h.set_timing(False)
+    paper_res = h.paper_residual(b, x)      # Eq. GMRES_residual at the last timed iterate
+    # re-factorization with CHANGED values (diagonal shift +0.5: faster decay, so
+    # the ranks change): the rank prediction misses and the synchronised sweep runs
+    diag = torch.tensor(np.repeat(np.arange(p.n), np.diff(p.row_ptr)) == p.col_idx, device=dev)
+    vals2 = vals + 0.5 * diag.to(torch.float64)
+    ranks_before = [h.ranks(i).copy() for i in range(1, h.depth + 1)]
+    miss0 = stats.get("rank_prediction_misses", 0)
+    newv = []
+    for k in range(2):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h.factor(vals2)
+        e1.record()
+        torch.cuda.synchronize()
+        newv.append(e0.elapsed_time(e1))
+    st2 = h.stats()
+    changed = any(not np.array_equal(a_, h.ranks(i + 1)) for i, a_ in enumerate(ranks_before))
+    refactor_new = {"ms_first": newv[0], "ms_second": newv[1], "ranks_changed": bool(changed),
+                    "prediction_misses": st2.get("rank_prediction_misses", 0) - miss0,
+                    "values": "A + 0.5 I (same pattern)",
+                    "note": "first call: predicted sweep, rank miss, synchronised re-run; second: rank-predicted "
+                            "replay with the new ranks"}
+    h.factor(vals)                          # back to the workload's values
     tot_f = sum(tfs)
     tot_f_max, tot_k_max = max_over_ranks([tot_f, sum(tks)], world, dev)
     value = units(tot_f_max, args.steps)
@@ -352,13 +471,15 @@ def main():
             "tflops_model": tflops, "fp64_peak_tflops": peak_f, "frac_fp64_peak": tflops / peak_f,
             "flops_model": flops, "factor_bytes": stats.get("factor_bytes"), "aux_vars": stats.get("aux_vars"),
             "gpu_launches": launches, "clocks": clocks, "roofline": roof,
+            "first_factor_ms": first[0] if first else None, "analyze_s": t_analyze,
+            "refactor_new_values": refactor_new, "paper_residual": paper_res,
+            "paper_residual_def": "Eq. GMRES_residual (P:l.665-669) ||A~ b - A~ A x|| / ||A~ b||, device, last iterate",
             "kernels_warmup_step": warm_kernels,
             "kernels_note": "per-class breakdown from the last warm-up step (all classes timed); the timed "
                             "region records CUDA events only around launches of the dominant class"}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb, _ = cpu_baseline(p, compressor=args.compressor)
-        line["cpu_baseline"] = cb
+        line["cpu_baseline"] = cpu_baseline(p, compressor=args.compressor)
 
     if not args.no_e2e:
         # e2e: the same metric through the C ABI with pinned HOST buffers; every step
@@ -383,6 +504,9 @@ def main():
                        "h2d_bytes_per_step": 8 * (p.nnz + p.n), "d2h_bytes_per_step": 8 * p.n,
                        "factor_ms": 1e3 * te[0] / args.steps, "krylov_ms": 1e3 * te[1] / args.steps,
                        "how": "host wall clock around the synchronous C-ABI calls, pinned host buffers"}
+    extra = ("cfg4" if args.config == "cfg2" else "none") if args.extra == "auto" else args.extra
+    if extra != "none" and world == 1:
+        line["other_configs"] = {extra: measure_config(L, extra, dev)}
     if rank == 0:
         print(json.dumps(line))
     h.close()

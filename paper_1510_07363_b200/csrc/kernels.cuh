@@ -2259,7 +2259,37 @@ struct PivTask {
   double *F;  // n x n at ld
   int ld, m, r, node;
   double *F2;  // LU path: where U^{-T} goes (nullptr: F + ld * n, the record's region 1)
+  int pivot;   // LU path (k_pivot_lu): partial pivoting (see there); 0 = none
 };
+
+// LU path without pivoting: a multiplier |l_ij| above this (partial pivoting
+// keeps |l_ij| <= 1), or a vanishing pivot, reports LORASP_NEED_PIVOT; the host
+// then re-runs the sweep with partial pivoting (k_pivot_lu, pivot = 1).
+constexpr double LU_GROWTH_MAX = 64.0;
+constexpr int LORASP_NEED_PIVOT = -10;   // internal status, never returned by the C ABI
+
+// block-wide max of v (all threads get it); red: >= 16 doubles of shared scratch
+__device__ __forceinline__ double block_max(double v, double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  v = 0;
+  for (int w = 0; w < nw; ++w) v = fmax(v, red[w]);
+  return v;
+}
+// growth of the multipliers max |l_ij| (strict lower of A, n x n at lda); every
+// thread returns it; the largest seen is kept in status[2..3] (a double)
+__device__ __forceinline__ double lu_growth(const double *A, int lda, int n, double *red, int *status) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double g = 0;
+  for (int j = warp; j < n; j += nw)
+    for (int i = j + 1 + lane; i < n; i += 32) g = fmax(g, fabs(A[i + (int64_t)j * lda]));
+  g = block_max(g, red);
+  if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long *>(status + 2), (unsigned long long)__double_as_longlong(g));
+  return g;
+}
 
 __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks,
                                                int smem_cap_doubles, int *status) {
@@ -2336,11 +2366,18 @@ __global__ void __launch_bounds__(512) k_pivot(const PivTask *__restrict__ tasks
 
 // --------------------------------------------------------- LU pivot (general) ----
 // LU path: the fused pivot K = [[S, V], [V^T, 0]] (n = m + r, full, ld) is
-// factored without pivoting, K = L U (S is an M-matrix-like block whose Schur
-// complements stay positive real, so no zero pivots arise; a vanishing pivot
-// reports LORASP_E_SINGULAR_PIVOT), then region 0 <- L^{-1} (unit lower) and
-// region 1 <- U^{-T} (lower).  Shared memory when n^2 + n fits, else in place
-// in region 0 (global).
+// factored P K = L U, then region 0 <- L^{-1} P and region 1 <- U^{-T} (lower),
+// so that K^{-1} = U^{-1} (L^{-1} P): the Z GEMM X = (L^{-1} P) C and the apply's
+// forward step y = (L^{-1} P)[:, :m] rhs use region 0 as a general matrix.
+// pivot = 0: no pivoting (P = I; region 0 unit lower); a vanishing pivot or a
+//   multiplier above LU_GROWTH_MAX reports LORASP_NEED_PIVOT.
+// pivot = 1: partial pivoting restricted to the two diagonal blocks -- rows of
+//   [0, m) for the columns of S, rows of [m, n) for the Schur block -- i.e.
+//   P = diag(P1, P2): exactly the oracle's Eliminate(s) then Eliminate(b), each
+//   with a partial-pivot LU (P:l.101-106, P:l.396-399; reading Z11).  A vanishing
+//   pivot then is LORASP_E_SINGULAR_PIVOT.
+// Shared memory when n^2 + 2n fits (A, tmp, the permutation), else in place in
+// region 0 (global), with per-warp row strips for the final column permutation.
 __global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ tasks, int smem_cap_doubles,
                                                   int *status) {
   pdl_trigger();
@@ -2350,13 +2387,15 @@ __global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ ta
   const int n = t.m + t.r;
   if (n == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  __shared__ int s_fail;
-  const bool in_smem = (int64_t)n * n + n <= smem_cap_doubles;
+  __shared__ int s_fail, s_p;
+  __shared__ double s_red[16];
+  const bool in_smem = (int64_t)n * n + 2 * (int64_t)n <= smem_cap_doubles;
   double *tmp = sh;
+  int *perm = reinterpret_cast<int *>(sh + n);   // n ints
   double *A;
   int lda;
   if (in_smem) {
-    A = sh + n;
+    A = sh + 2 * n;
     lda = n;
     for (int j = warp; j < n; j += nw)
       for (int i = lane; i < n; i += 32) A[i + (int64_t)j * n] = t.F[i + (int64_t)j * t.ld];
@@ -2364,24 +2403,60 @@ __global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ ta
     A = t.F;
     lda = t.ld;
   }
+  for (int i = tid; i < n; i += blockDim.x) perm[i] = i;
   if (tid == 0) s_fail = 0;
   __syncthreads();
   double amax = 0;   // scale for the singularity test
   for (int j = warp; j < n; j += nw)
     for (int i = lane; i < n; i += 32) amax = fmax(amax, fabs(A[i + (int64_t)j * lda]));
-  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-  __shared__ double s_amax[16];
-  if (lane == 0) s_amax[warp] = amax;
-  __syncthreads();
-  amax = 0;
-  for (int w = 0; w < nw; ++w) amax = fmax(amax, s_amax[w]);
-  // right-looking LU without pivoting
+  amax = block_max(amax, s_red);
+  const int fail_code = t.pivot ? -3 : LORASP_NEED_PIVOT;
+  // right-looking LU
   for (int k = 0; k < n; ++k) {
+    if (t.pivot) {
+      const int e = (k < t.m) ? t.m : n;   // candidate rows [k, e)
+      if (warp == 0) {
+        double best = -1.0;
+        int bi = k;
+        for (int i = k + lane; i < e; i += 32) {
+          const double v = fabs(A[i + (int64_t)k * lda]);
+          if (v > best) {
+            best = v;
+            bi = i;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {   // max |a|, ties -> smaller row
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+          }
+        }
+        if (lane == 0) {
+          s_p = bi;
+          if (bi != k) {
+            const int q = perm[k];
+            perm[k] = perm[bi];
+            perm[bi] = q;
+          }
+        }
+      }
+      __syncthreads();
+      const int p = s_p;
+      if (p != k)
+        for (int j = tid; j < n; j += blockDim.x) {   // whole rows (L part included)
+          const double a = A[k + (int64_t)j * lda];
+          A[k + (int64_t)j * lda] = A[p + (int64_t)j * lda];
+          A[p + (int64_t)j * lda] = a;
+        }
+      __syncthreads();
+    }
     const double piv = A[k + (int64_t)k * lda];
     if (!(fabs(piv) > 1e-14 * amax) || !isfinite(piv)) {
       if (tid == 0) {
         s_fail = 1;
-        if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
+        if (atomicCAS(&status[0], 0, fail_code) == 0) status[1] = t.node;
       }
       break;
     }
@@ -2398,6 +2473,10 @@ __global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ ta
     __syncthreads();
   }
   if (s_fail) return;
+  if (!t.pivot && lu_growth(A, lda, n, s_red, status) > LU_GROWTH_MAX) {
+    if (tid == 0 && atomicCAS(&status[0], 0, LORASP_NEED_PIVOT) == 0) status[1] = t.node;
+    return;
+  }
   // U^{-1} in place (upper incl. diagonal), columns ascending:
   // u_jj <- 1/u_jj; A[0:j, j] <- -u_jj^{-1} * Uinv[0:j, 0:j] A[0:j, j]
   for (int j = 0; j < n; ++j) {
@@ -2429,11 +2508,22 @@ __global__ void __launch_bounds__(512) k_pivot_lu(const PivTask *__restrict__ ta
     }
     __syncthreads();
   }
-  for (int j = warp; j < n; j += nw)
-    for (int i = lane; i < n; i += 32) {
-      const double v = (i > j) ? A[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
-      t.F[i + (int64_t)j * t.ld] = v;
+  // region 0 <- L^{-1} P: column perm[k] of L^{-1} P is column k of L^{-1}
+  if (in_smem || !t.pivot) {
+    for (int j = warp; j < n; j += nw)
+      for (int i = lane; i < n; i += 32) {
+        const double v = (i > j) ? A[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
+        t.F[i + (int64_t)perm[j] * t.ld] = v;
+      }
+  } else {   // in place: each warp permutes whole rows through its strip of n doubles
+    double *strip = sh + 2 * n + (int64_t)warp * n;
+    for (int i = warp; i < n; i += nw) {
+      for (int k = lane; k < n; k += 32) strip[k] = (i > k) ? A[i + (int64_t)k * lda] : (i == k ? 1.0 : 0.0);
+      __syncwarp();
+      for (int k = lane; k < n; k += 32) t.F[i + (int64_t)perm[k] * t.ld] = strip[k];
+      __syncwarp();
     }
+  }
 }
 
 // ----------------------------------------------- blocked pivot (one CTA) ----
@@ -2749,7 +2839,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
       if (!lu_diag_factor(A, lda, j0, b, tiny, rd, lane)) {
         if (lane == 0) {
           s_fail = 1;
-          if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
+          if (atomicCAS(&status[0], 0, LORASP_NEED_PIVOT) == 0) status[1] = t.node;
         }
       } else {
         lu_diag_inverses(A, lda, j0, b, WL, WU, lane, rd);
@@ -2804,6 +2894,10 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
       }
     }
     __syncthreads();
+  }
+  if (lu_growth(A, lda, n, s_amax, status) > LU_GROWTH_MAX) {   // no pivoting: check the multipliers
+    if (tid == 0 && atomicCAS(&status[0], 0, LORASP_NEED_PIVOT) == 0) status[1] = t.node;
+    return;
   }
   // ---------------- blocked inverses, last block first ----------------
   const int last = ((n - 1) / PIVB_NB) * PIVB_NB;
@@ -2956,6 +3050,7 @@ struct ApNode {
   int seg0, nseg;
   int nsplit;      // split apply: Z column parts (1 = one CTA streams the whole record)
   int64_t upart;   // split apply: offset of the nsplit x n partial backward sums
+  int full;        // LU with partial pivoting: region 0 = L^{-1} P is not lower triangular
 };
 // one CTA of a split wave: Z columns [c0, c1) of node `node` (part p)
 struct ApPart {
@@ -3076,7 +3171,7 @@ __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ no
       const int k0 = c * cc, k1 = min(nd.m, k0 + cc);
       for (int i = tid; i < n; i += blockDim.x) {
         double sacc = 0;
-        const int kl = min(k1 - 1, i);
+        const int kl = nd.full ? k1 - 1 : min(k1 - 1, i);
         for (int k = k0; k <= kl; ++k) sacc = fma(buf[(int64_t)(k - k0) * ld + i], rhs[k], sacc);
         dy[i] += sacc;
       }
@@ -3216,7 +3311,7 @@ __global__ void __launch_bounds__(256) k_apply_fwd_y(const ApNode *__restrict__ 
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double s0 = 0, s1 = 0;
-    const int kl = min(nd.m - 1, i);
+    const int kl = nd.full ? nd.m - 1 : min(nd.m - 1, i);
     int k = 0;
     for (; k + 1 <= kl; k += 2) {
       s0 = fma(nd.F[i + (int64_t)k * nd.ld], rhs[k], s0);

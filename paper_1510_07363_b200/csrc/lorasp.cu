@@ -398,6 +398,15 @@ struct lorasp_ctx {
   int64_t f_doubles = 0;
   bool debug = getenv("LORASP_DEBUG") != nullptr;
   bool pivot_unblocked = getenv("LORASP_PIVOT_UNBLOCKED") != nullptr;   // debug: column-wise k_pivot
+  // LU path: partial pivoting inside the fused pivots (k_pivot_lu, pivot = 1),
+  // switched on (for the rest of the handle's life) when the no-pivot kernels
+  // report LORASP_NEED_PIVOT; SPD path: a failed signed Cholesky re-plans the
+  // handle on the general LU path (reading Z12)
+  bool lu_pivot = false;
+  int lu_pivot_switches = 0, spd_fallbacks = 0;
+  std::string spd_fallback_node;
+  std::vector<double> an_coords;   // analyze inputs kept for a re-plan
+  int an_dim = 0, an_leaf = 0;
   // kernel timing
   bool timing = false;
   unsigned timing_mask = 0;
@@ -1064,15 +1073,22 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
   int max_n = 0;
   for (const PivTask &t : pv) max_n = std::max(max_n, t.m + t.r);
   max_n = std::max(max_n, h->piv_maxn_hint);
-  PivTask *dp = push(h, pv);
+  std::vector<PivTask> pvp;
+  if (h->lu_pivot) {   // partial pivoting (k_pivot_lu only)
+    pvp = pv;
+    for (PivTask &t : pvp) t.pivot = 1;
+  }
+  PivTask *dp = push(h, h->lu_pivot ? pvp : pv);
   int ev = tbeg(h, K_PIVOT);
-  if (max_n <= PIVLU_MAXN && !h->pivot_unblocked) {
+  if (max_n <= PIVLU_MAXN && !h->pivot_unblocked && !h->lu_pivot) {
     const size_t sm = ((size_t)(max_n | 1) * max_n + 2 * (size_t)max_n * PIVB_NB) * 8;
     launch_k(k_pivot_lu_blk, (unsigned)pv.size(), 512, sm, h->stream, dp, h->d_status.as<int>());
   } else {
-    int64_t want = (int64_t)max_n * max_n + max_n;
+    int64_t want = (int64_t)max_n * max_n + 2 * max_n;
     int cap = (int)std::min<int64_t>(want, SMEM_LIMIT / 8);
-    cap = std::max(cap, max_n);
+    cap = std::max(cap, 2 * max_n);
+    if (h->lu_pivot && want > cap && 18 * (int64_t)max_n > cap)
+      throw Err(LORASP_E_ARG, "pivot block of order " + std::to_string(max_n) + " too large for partial pivoting");
     launch_k(k_pivot_lu, (unsigned)pv.size(), 512, cap * 8, h->stream, dp, cap, h->d_status.as<int>());
   }
   tend(h, ev, f_piv, b_piv);
@@ -1203,6 +1219,8 @@ bool replay_check(lorasp_ctx *h, const std::vector<RankLog> &rlog) {
 }
 
 void status_check(lorasp_ctx *h) {
+  if (h->h_status[0] == LORASP_NEED_PIVOT)
+    throw Err(LORASP_NEED_PIVOT, "LU without pivoting unstable at node " + std::to_string(h->h_status[1]));
   if (h->h_status[0] != 0)
     throw Err(h->h_status[0], std::string(h->h_status[0] == LORASP_E_EIG_NOCONV
                                               ? "Jacobi eigen-solver did not converge"
@@ -1360,7 +1378,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       std::vector<CopyTask> s_ct;
       std::vector<PivTask> s_pt;
       int s_max = 0;
-      if (!comp.empty() && !h->no_split && (sym || !h->no_split_lu)) {
+      if (!comp.empty() && !h->no_split && (sym || (!h->no_split_lu && !h->lu_pivot))) {
         int64_t stot2 = 0;
         // A node is split when that pays: in waves wider than the GPU (the S
         // pivots then fill the sync gaps), or when its fused pivot would likely
@@ -1593,7 +1611,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           dist_allmax_ints(h, h->d_ranks.as<int>(), comp.size(), h->h_ranks);
         } else {
           CK(cudaMemcpyAsync(h->h_ranks, h->d_ranks.p, comp.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
-          CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+          CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
           CK(cudaStreamSynchronize(st));
         }
         h->t_sync_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts0).count();
@@ -2008,7 +2026,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
               g.lda = ldF;
               g.B = ctr;
               g.ldb = n;
-              g.K = std::min(n, tm + GT);
+              g.K = (!sym && h->lu_pivot) ? n : std::min(n, tm + GT);   // L^{-1} P is not triangular
               g.alpha = 1.0;
               zs.push_back(g);
               zt.push_back(b);
@@ -2203,7 +2221,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       if (dist) dist_exchange(h, dirty);
       if (h->debug) {
         CK(cudaStreamSynchronize(st));
-        CK(cudaMemcpy(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(h->h_status, h->d_status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost));
         fprintf(stderr, "[lorasp] level %d wave %zu: %zu nodes, %zu compressed, status %d (node %d); ranks:",
                 i, w, elim.size(), comp.size(), h->h_status[0], h->h_status[1]);
         for (int c : elim) fprintf(stderr, " %d:%d/%d", c, r[c], m[c]);
@@ -2214,14 +2232,14 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
     prev_sld.swap(sld);
   }
   if (capture) {   // the caller ends the capture, launches and verifies
-    CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     h->fg_rlog = std::move(rlog);
     return true;
   }
   if (dist) {
     dist_allmax_ints(h, nullptr, 0, nullptr);
   } else {
-    CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h->h_status, h->d_status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
   }
   h->stg.reset();
@@ -2278,6 +2296,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
     a.zb_off = rc.zb_off;
     a.lb_off = rc.lb_off;
     a.sym = (pl.flags & LORASP_SPD) ? 1 : 0;
+    a.full = (!a.sym && h->lu_pivot) ? 1 : 0;
     a.seg0 = (int)as.size();
     int zc = 0;
     const int K = lv.K;
@@ -2839,6 +2858,50 @@ int guarded(lorasp_ctx *h, F &&f) {
 
 extern "C" {
 
+// forget everything a previous sweep cached for the current plan / pivot mode
+void reset_sweep_state(lorasp_ctx *h) {
+  CK(cudaDeviceSynchronize());
+  h->cache_valid = false;
+  h->factored = false;
+  if (h->fgraph) {
+    cudaGraphExecDestroy(h->fgraph);
+    h->fgraph = nullptr;
+  }
+  if (h->ap_graph) {
+    cudaGraphExecDestroy(h->ap_graph);
+    h->ap_graph = nullptr;
+  }
+  h->ap_graph_sig.clear();
+  h->s1_pending = false;
+  h->pend.clear();
+  h->stg.reset();
+  CK(cudaMemsetAsync(h->d_status.p, 0, 64, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+}
+
+// reading Z12: the SPD path's signed Cholesky met a non-positive pivot (the
+// approximation broke definiteness).  The handle is re-planned on the general
+// path (both block orientations, stacks [A; B]) with partial pivoting, and the
+// sweep re-runs there; counted in the stats (spd_fallbacks).
+void replan_general(lorasp_ctx *h, const char *why) {
+  const Plan &old = h->plan;
+  Plan np;
+  std::string err;
+  const int rc = build_plan(np, old.n, old.row_ptr.data(), old.col_idx.data(), h->an_dim,
+                            h->an_coords.empty() ? nullptr : h->an_coords.data(), h->an_leaf, old.depth, old.eps,
+                            old.flags & ~(unsigned)LORASP_SPD, err);
+  if (rc != 0) throw Err(LORASP_E_PATTERN, "re-plan for the LU fallback failed: " + err);
+  h->plan = std::move(np);
+  h->dest_ready = false;
+  h->leaf_soff.clear();
+  h->piv_maxn_hint = 0;
+  h->eig_clmax_hint = h->eig_bigmax_hint = h->eig_regmax_hint = 0;
+  h->rank_cache.clear();
+  h->lu_pivot = true;
+  ++h->spd_fallbacks;
+  h->spd_fallback_node = why;
+}
+
 int lorasp_analyze(int64_t n, const int64_t *row_ptr, const int64_t *col_idx, int dim, const double *coords,
                    int leaf_size, int depth, double eps, unsigned flags, int device, lorasp_handle *out) {
   if (!out) return LORASP_E_ARG;
@@ -2851,6 +2914,9 @@ int lorasp_analyze(int64_t n, const int64_t *row_ptr, const int64_t *col_idx, in
     delete h;
     return rc == -1 ? LORASP_E_ARG : LORASP_E_PATTERN;
   }
+  if (coords && dim > 0) h->an_coords.assign(coords, coords + n * dim);
+  h->an_dim = dim;
+  h->an_leaf = leaf_size;
   *out = h;
   return LORASP_OK;
 }
@@ -2870,19 +2936,36 @@ int lorasp_factor(lorasp_handle h, const double *values) {
     CK(cudaStreamWaitEvent(h->stream_hi, h->ev_u, 0));
     h->stream = h->stream_hi;
     try {
-      bool ok = false;
-      h->replay_used = false;
-      if (h->cache_valid && !h->no_replay && h->dist_world == 1) {
-        ok = factor_replay(h, values);
-        h->replay_used = ok;
-      }
-      if (!ok) {
-        if (h->fgraph) {   // built for the old ranks
-          cudaGraphExecDestroy(h->fgraph);
-          h->fgraph = nullptr;
+      for (int attempt = 0;; ++attempt) {
+        try {
+          bool ok = false;
+          h->replay_used = false;
+          if (h->cache_valid && !h->no_replay && h->dist_world == 1) {
+            ok = factor_replay(h, values);
+            h->replay_used = ok;
+          }
+          if (!ok) {
+            if (h->fgraph) {   // built for the old ranks
+              cudaGraphExecDestroy(h->fgraph);
+              h->fgraph = nullptr;
+            }
+            h->fgraph_used = false;
+            factor_impl(h, values, false);
+          }
+          break;
+        } catch (const Err &e) {
+          if (attempt >= 2) throw;
+          const bool lu = !(h->plan.flags & LORASP_SPD);
+          if (e.code == LORASP_NEED_PIVOT && lu && !h->lu_pivot) {
+            h->lu_pivot = true;   // re-run the sweep with partial pivoting
+            ++h->lu_pivot_switches;
+          } else if (e.code == LORASP_E_SINGULAR_PIVOT && !lu && h->dist_world == 1) {
+            replan_general(h, e.msg.c_str());   // Z12: signed Cholesky failed -> LU path
+          } else {
+            throw;
+          }
+          reset_sweep_state(h);
         }
-        h->fgraph_used = false;
-        factor_impl(h, values, false);
       }
     } catch (...) {
       h->cache_valid = false;
@@ -3079,7 +3162,15 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
       << ",\"factor_graph_failures\":" << h->fg_failures << ",\"dist_world\":" << h->dist_world
       << ",\"dist_rank\":" << h->dist_rank << ",\"dist_exchange_calls\":" << h->dist_calls
       << ",\"dist_allgather_bytes\":" << h->dist_bytes
-      << ",\"aux_vars\":";
+      << ",\"lu_partial_pivoting\":" << (h->lu_pivot ? "true" : "false")
+      << ",\"lu_pivot_switches\":" << h->lu_pivot_switches << ",\"spd_fallbacks\":" << h->spd_fallbacks
+      << ",\"path\":\"" << ((pl.flags & LORASP_SPD) ? "spd" : "lu") << "\"";
+    {
+      double g = 0;
+      std::memcpy(&g, h->h_status + 2, sizeof(double));
+      o << ",\"lu_max_multiplier\":" << g;
+    }
+    o << ",\"aux_vars\":";
     int64_t aux = 0;
     for (int i = 1; i <= pl.depth; ++i)
       for (int r : h->rnk[i]) aux += 2 * r;

@@ -74,3 +74,21 @@ def test_reference_arm_under_torchrun_gloo():
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_gpus_flag_relaunches_or_rejects():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 processes
+    (here: the reference arm, gloo); a WORLD_SIZE that disagrees with --gpus is
+    rejected instead of silently measuring one process."""
+    env = dict(os.environ, LORASP_BENCH_BACKEND="gloo", PYTHONPATH=ROOT)
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "cfg1", "--gpus", "2",
+           "--steps", "1", "--warmup", "3"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["n_gpus"] == 2
+    bad = subprocess.run(cmd[:-6] + ["--gpus", "4", "--steps", "1", "--warmup", "3"],
+                         env=dict(env, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0"), capture_output=True, text=True,
+                         timeout=120, cwd=ROOT)
+    assert bad.returncode == 2
