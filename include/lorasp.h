@@ -53,6 +53,12 @@ typedef enum {
 #define LORASP_ALGEBRAIC      0x10u /* nested partitionings from the graph of A alone (BFS
                                        level-structure bisection; coords
                                        may be NULL and dim is ignored)                    */
+#define LORASP_FROBENIUS      0x20u /* truncation by the Frobenius rule Eq. curOff6
+                                       (P:l.756-761): keep the smallest k
+                                       with ||B - U_k S_k V_k^T||_F < eps ||all levels
+                                       below||_F, the denominator = every super-node block
+                                       of this and the deeper levels right after
+                                       MergeRedNodes (reading F2); SVD only    */
 
 /* Krylov methods for lorasp_krylov_ex */
 #define LORASP_CG     0

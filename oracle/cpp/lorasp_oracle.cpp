@@ -810,6 +810,7 @@ struct Factorizer {
     return r;
   }
   double frob_D2 = 0.0;
+  std::map<int, double> frob_level;   // D^2 in force while level i is processed
 
   // -- Compress edits: edge rules (P:l.383-389) --------------------------------
   void compress_apply(int i, int64_t c, CompressOut &co) {
@@ -964,6 +965,7 @@ struct Factorizer {
           if (kind_of(kv.first.first) == KS && lev_of(kv.first.first) == i && kind_of(kv.first.second) == KS &&
               lev_of(kv.first.second) == i)
             for (double v : kv.second->a) frob_D2 += v * v;
+      frob_level[i] = frob_D2;
       const int k = i - 1;
       const int64_t ncl = (int64_t)1 << k;
       std::vector<int64_t> seq(ncl);
@@ -1484,6 +1486,12 @@ int orc_info(OrcHandle *h, int64_t *info) {
   for (auto &kv : h->F.pivots) d += (int64_t)kv.second.a.size();
   info[4] = d;
   return 0;
+}
+
+// Frobenius rule (F2): ||all levels below||_F^2 in force at level i (0 if unused)
+double orc_frob_d2(OrcHandle *h, int level) {
+  auto it = h->F.frob_level.find(level);
+  return it == h->F.frob_level.end() ? 0.0 : it->second;
 }
 
 // size of node (kind 0 = s, 1 = b, 2 = r; level; cluster)

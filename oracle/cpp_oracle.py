@@ -70,6 +70,8 @@ def _load():
             lib.orc_trace.restype = C.c_int64
             lib.orc_info.argtypes = [P, i64p]
             lib.orc_size.argtypes = [P, C.c_int, C.c_int, C.c_int64]
+            lib.orc_frob_d2.argtypes = [P, C.c_int]
+            lib.orc_frob_d2.restype = C.c_double
             lib.orc_spmv.argtypes = [C.c_int64, i64p, i64p, dp, dp, dp]
             lib.orc_krylov.argtypes = [P, C.c_int64, i64p, i64p, dp, dp, dp, C.c_double, C.c_int, C.c_int, C.c_int,
                                        C.c_int, ip, ip, ip, dp]
@@ -199,6 +201,10 @@ class CFactorization:
         _load().orc_info(self._h, _p(a, C.c_int64))
         return {"max_edge_distance": int(a[0]), "waves_parallel": int(a[1]), "waves_total": int(a[2]),
                 "blocks": int(a[3]), "doubles": int(a[4])}
+
+    def frob_d2(self, level: int) -> float:
+        """Frobenius rule (F2): ||all levels below||_F^2 used at `level`."""
+        return float(_load().orc_frob_d2(self._h, level))
 
     @property
     def max_edge_distance(self) -> int:

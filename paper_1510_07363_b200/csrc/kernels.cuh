@@ -337,6 +337,12 @@ struct EigTask {
   int node;          // cluster id (for status)
   int *rank_out;
   long long *dbg;    // optional phase timestamps (test hook), may be null
+  // Frobenius rule (f2, Eq. curOff6 P:l.756-761, reading F2): device scalar
+  // D^2 = ||all levels below||_F^2; nullptr = the relative-sigma rule Eq. cutOff1.
+  // frob_w: energy of the oracle's stack [A; B] per unit of this stack's (SPD path
+  // stacks only A: 2; LU path: 1)
+  const double *frob;
+  double frob_w;
 };
 
 // FP64 division is a long software sequence on sm_100a (~430 cycles of latency
@@ -917,6 +923,21 @@ __device__ __forceinline__ int eig_values_phase(const EigTask &t, double eps, in
                                                 double *e2, double *lam, double *s_red, double *s_bc, int *s_int,
                                                 double &bnorm_out) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // Frobenius rule: budget B = eps^2 D^2 / w on this stack's energy; tail(k) =
+  // sum_{t >= k} lambda_t = trace(G) - sum_{t < k} lambda_t (the tridiagonal keeps
+  // the trace); every k >= #{lambda >= B / m} has tail(k) < B, so only those
+  // eigenvalues are computed
+  double trace = 0.0, fbud = 0.0;
+  if (t.frob) {
+    double tr = 0.0;
+    for (int i = tid; i < m; i += blockDim.x) tr += d[i];
+    for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    __syncthreads();
+    if (lane == 0) s_red[warp] = tr;
+    __syncthreads();
+    for (int w = 0; w < nw; ++w) trace += s_red[w];
+    fbud = eps * eps * (*t.frob) / t.frob_w;
+  }
   double gl = 1e300, gu = -1e300, emax2 = 0;
   for (int i = tid; i < m; i += blockDim.x) {
     double off = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < m - 1 ? fabs(e[i]) : 0.0);
@@ -989,8 +1010,9 @@ __device__ __forceinline__ int eig_values_phase(const EigTask &t, double eps, in
       if (lane == 0) {
         lam[0] = l0 * bnorm;
         double thr = eps * sqrt(fmax(l0, 0.0));
-        thr = thr * thr;
-        int below = sturm_count(d, e2, m, 0.25 * thr, pivmin);
+        thr = 0.25 * thr * thr;
+        if (t.frob) thr = fbud / m * isc;   // (scaled) candidate bound of the Frobenius rule
+        int below = sturm_count(d, e2, m, thr, pivmin);
         s_int[0] = min(m, m - below + 1);  // candidates to compute (superset of kept + 1)
       }
     }
@@ -1005,11 +1027,64 @@ __device__ __forceinline__ int eig_values_phase(const EigTask &t, double eps, in
   __syncthreads();
   const double sig0 = sqrt(fmax(lam[0], 0.0));
   int r = 0;
-  for (int k = 0; k < ncomp; ++k) r += (sqrt(fmax(lam[k], 0.0)) >= eps * sig0);
+  if (t.frob) {   // smallest k with tail(k) < B (Eq. curOff6)
+    if (tid == 0) {
+      double pre = 0.0;
+      int k = 0;
+      while (k < ncomp && !(trace - pre < fbud)) pre += fmax(lam[k++], 0.0);
+      s_int[1] = k;
+    }
+    __syncthreads();
+    r = s_int[1];
+  } else {
+    for (int k = 0; k < ncomp; ++k) r += (sqrt(fmax(lam[k], 0.0)) >= eps * sig0);
+  }
   for (int k = tid; k < m; k += blockDim.x) t.sig[k] = (k < ncomp) ? sqrt(fmax(lam[k], 0.0)) : 0.0;
   if (tid == 0) *t.rank_out = r;
   bnorm_out = bnorm;
   return r;
+}
+
+// f2: squared Frobenius norm of one stored block, weighted (reading F2):
+// mode 0 full block, 2 = twice the full block (SPD off-diagonal slot: both
+// orientations), 1 = symmetric block from its lower triangle (SPD self slot).
+struct FrobTask {
+  const double *A;
+  int ld, rows, cols, mode;
+};
+__global__ void __launch_bounds__(256) k_frob_part(const FrobTask *__restrict__ tasks, double *__restrict__ part) {
+  pdl_enter();
+  __shared__ double red[8];
+  const FrobTask t = tasks[blockIdx.x];
+  double s = 0.0;
+  for (int64_t q = threadIdx.x; q < (int64_t)t.rows * t.cols; q += blockDim.x) {
+    const int i = (int)(q % t.rows), j = (int)(q / t.rows);
+    const double a = t.A[i + (int64_t)j * t.ld];
+    if (t.mode == 1) s += (i > j) ? 2.0 * a * a : (i == j ? a * a : 0.0);
+    else s += a * a;
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    part[blockIdx.x] = (t.mode == 2) ? 2.0 * tot : tot;
+  }
+}
+// *d2 += sum of part[0..n) in a fixed order (deterministic)
+__global__ void __launch_bounds__(256) k_frob_final(const double *__restrict__ part, int n, double *__restrict__ d2) {
+  pdl_enter();
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int q = threadIdx.x; q < n; q += blockDim.x) s += part[q];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *d2 += red[0];
 }
 
 constexpr int EIG_THREADS = 256;      // generic path

@@ -370,6 +370,7 @@ struct lorasp_ctx {
   cudaEvent_t ev_cf = nullptr, ev_cj[2] = {nullptr, nullptr};
   bool s1_pending = false;
   DevBuf ws_S, ws_Y, ws_T1, d_sp;
+  DevBuf d_frob, d_frobpart;   // f2: ||all levels below||_F^2 (device scalar) and per-slot partial sums
   void *h_sp = nullptr;     // pinned upload of the part-1 copy + pivot task lists
   size_t h_sp_cap = 0;
   bool no_split = getenv("LORASP_NO_SPLIT") != nullptr;
@@ -1250,6 +1251,10 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
   // values -> device (a capture's caller copies them before the capture)
   if (!capture) copy_values(h, values);
   CK(cudaMemsetAsync(h->d_status.p, 0, 64, st));
+  if (pl.flags & LORASP_FROBENIUS) {
+    h->d_frob.ensure(64, st);
+    CK(cudaMemsetAsync(h->d_frob.p, 0, 8, st));
+  }
   h->fpool.reset();
   h->recs.clear();
   h->msz.assign(L + 2, {});
@@ -1351,6 +1356,26 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         ct.push_back(t);
       }
       launch_copy(h, ct, K_MERGE);
+    }
+    // ---- f2: ||all levels below||_F^2 += every super-node block of this level right
+    // after MergeRedNodes (reading F2; the other slots are still zero here).  SPD
+    // path: an off-diagonal slot stands for both orientations, a self slot's lower
+    // triangle for the symmetric block.
+    if (pl.flags & LORASP_FROBENIUS) {
+      std::vector<FrobTask> ft;
+      for (size_t q = 0; q < lv.slots.size(); ++q) {
+        const int rows = bound(lv.slots[q].row), cols = bound(lv.slots[q].col);
+        if (rows == 0 || cols == 0) continue;
+        const bool self = lv.slots[q].row == lv.slots[q].col;
+        ft.push_back(FrobTask{slot_ptr((int)q), sld[q], rows, cols, sym ? (self ? 1 : 2) : 0});
+      }
+      if (!ft.empty()) {
+        h->d_frobpart.ensure(ft.size() * sizeof(double), st);
+        FrobTask *dft = push(h, ft);
+        launch_k(k_frob_part, (unsigned)ft.size(), 256, 0, st, dft, h->d_frobpart.as<double>());
+        launch_k(k_frob_final, 1, 256, 0, st, h->d_frobpart.as<double>(), (int)ft.size(), h->d_frob.as<double>());
+        h->launches_factor += 2;
+      }
     }
 
     // ---- colour waves ---------------------------------------------------------
@@ -1554,6 +1579,10 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           e.m = mc;
           e.node = c;
           e.rank_out = h->d_ranks.as<int>() + q;
+          if (pl.flags & LORASP_FROBENIUS) {   // f2: Eq. curOff6 against ||all levels below||_F
+            e.frob = h->d_frob.as<double>();
+            e.frob_w = sym ? 2.0 : 1.0;
+          }
           et.push_back(e);
         }
         h->stg.reserve(vbytes(gt) + vbytes(gs) + vbytes(gt2) + vbytes(gs2) + 4 * vbytes(et), st);
@@ -2906,6 +2935,7 @@ int lorasp_analyze(int64_t n, const int64_t *row_ptr, const int64_t *col_idx, in
                    int leaf_size, int depth, double eps, unsigned flags, int device, lorasp_handle *out) {
   if (!out) return LORASP_E_ARG;
   *out = nullptr;
+  if ((flags & LORASP_FROBENIUS) && (flags & LORASP_RRQR)) return LORASP_E_ARG;   // f2 is an SVD rule
   auto *h = new lorasp_ctx();
   h->device = device;
   std::string err;

@@ -26,6 +26,7 @@ LORASP_SPD = 0x1
 LORASP_ORDER_NATURAL = 0x2
 LORASP_RRQR = 0x4          # f1: column-pivoted QR compressor (include/lorasp.h)
 LORASP_ALGEBRAIC = 0x10    # f4: partition from the graph of A (include/lorasp.h)
+LORASP_FROBENIUS = 0x20    # f2: Frobenius truncation rule Eq. curOff6 (include/lorasp.h)
 LORASP_CG = 0
 LORASP_GMRES = 1
 
