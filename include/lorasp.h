@@ -214,6 +214,18 @@ int lorasp_get_launch_count(lorasp_handle h, int64_t *factor_launches,
                             int64_t *apply_launches, int64_t *krylov_launches);
 
 /*
+ * lorasp_test_gemm — kernel comparison hook (north_star item 3: FP64 tensor
+ *   cores only for block shapes where they beat the FMA path).  Runs `reps`
+ *   independent copies of C = op(A) op(B) (one launch, like a wave of equal
+ *   GEMMs) through the DFMA tile kernel (variant 0) or the DMMA one (variant 1);
+ *   *ms = best CUDA-event time of one launch over 3 timed launches.  Host
+ *   buffers: A M x K (ld M) or, ta != 0, K x M (ld K); B K x N (ld K) or, tb,
+ *   N x K (ld N); C M x N (ld M) receives the first copy's product.
+ */
+int lorasp_test_gemm(int device, int variant, int M, int N, int K, int ta, int tb, int reps,
+                     const double *A, const double *B, double *C, double *ms);
+
+/*
  * Kernel-level test hooks (host buffers, run on `device`, synchronous).
  * lorasp_test_eig: the Compress eigen-solver on one symmetric PSD Gram matrix
  *   G (m x m, column-major): sigma (m, descending sqrt-eigenvalues), rank

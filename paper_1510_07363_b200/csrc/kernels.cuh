@@ -3,7 +3,9 @@
 //  k_leaf_scatter     CSR values -> dense leaf super-node blocks    (P:l.231, l.293)
 //  k_copy             block copies / transposes: MergeRedNodes (P:l.298-304)
 //                     and the gather of a node's fused pivot record
-//  k_gemm2 (k_gemm)   batched tiled DGEMM on task lists: Gram of the
+//  k_gemm2_dmma       batched tiled DGEMM on task lists, FP64 tensor cores (DMMA;
+//                     k_gemm2 = the DFMA variant, kept for the per-shape
+//                     comparison hook lorasp_test_gemm): Gram of the
 //                     well-separated stack (Eq. lra), R_k = A_k V (P:l.356-359),
 //                     Z = L^{-1} C (elimination panel), the Schur update
 //                     -Z_a^T D Z_b scattered into the target blocks (P:l.103-106)
@@ -15,11 +17,11 @@
 //                     back-transformation (generic m or after the kernels above)
 //    k_invit_multi / k_orth_cl / k_backtr_multi   the same steps split over CTAs
 //                     for 128 < m <= 512 (ranks ~0.6 m there)
-//    k_jacobi         one-sided Jacobi variant (test hook only)
 //  Fused (s, b) pivot (P:l.396-399, P:l.101-106):
 //    k_pivot_blk      signed Cholesky K = L diag(I_m, -I_r) L^T + L^{-1}, n <= 160
 //    k_pivdiag        diagonal blocks of the blocked path (n > 160, with k_gemm2)
-//    k_pivot_lu_blk / k_pivot_lu   LU path (no-pivot LU, L^{-1} and U^{-T})
+//    k_pivot_lu_blk / k_pivot_lu   LU path (LU, L^{-1} P and U^{-T}; partial
+//                     pivoting in k_pivot_lu once the no-pivot multipliers grow)
 //  k_apply_fwd/bwd    Alg. 3 / Alg. 4 (P:l.445-500) per colour wave (+ the split
 //                     k_apply_fwd_y/_z, k_apply_bwd_z/_l for few large records)
 //  Krylov helpers     CSR SpMV, deterministic dots, axpys
@@ -118,104 +120,7 @@ struct GemmTask {
 
 constexpr int GT = 64, GK = 32;
 
-// 64x64 output tile per CTA (256 threads, 4x4 each, strided so that shared
-// loads are conflict-free); K in chunks of 32 staged through shared memory;
-// the next chunk is loaded into registers while the current one is consumed
-// (one global round trip per chunk is hidden behind 32 rank-1 updates).
-__global__ void __launch_bounds__(256, 2) k_gemm(const GemmTask *__restrict__ tasks,
-                                              const GemmSeg *__restrict__ segs) {
-  const GemmTask t = tasks[blockIdx.x];
-  __shared__ double As[GK][GT + 1];
-  __shared__ double Bs[GK][GT + 1];
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
-  double acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
-
-  for (int s = 0; s < t.nseg; ++s) {
-    const GemmSeg g = segs[t.seg0 + s];
-    double accs[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) accs[a][b] = 0.0;
-    // per-thread load coordinates (8 elements of A and 8 of B per chunk)
-    double ra[8], rb[8];
-    auto load = [&](int k0) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int idx = tid + 256 * q;   // 0 .. 2047
-        int i, kk;
-        if (!t.ta) { i = idx & 63; kk = idx >> 6; } else { kk = idx & 31; i = idx >> 5; }
-        const int gi = t.tm + i, gk = k0 + kk;
-        ra[q] = (gi < t.M && gk < g.K) ? (t.ta ? g.A[gk + (int64_t)gi * g.lda] : g.A[gi + (int64_t)gk * g.lda]) : 0.0;
-        int j;
-        if (!t.tb) { kk = idx & 31; j = idx >> 5; } else { j = idx & 63; kk = idx >> 6; }
-        const int gj = t.tn + j, gk2 = k0 + kk;
-        rb[q] = (gj < t.N && gk2 < g.K) ? (t.tb ? g.B[gj + (int64_t)gk2 * g.ldb] : g.B[gk2 + (int64_t)gj * g.ldb])
-                                         : 0.0;
-      }
-    };
-    auto store = [&]() {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int idx = tid + 256 * q;
-        int i, kk;
-        if (!t.ta) { i = idx & 63; kk = idx >> 6; } else { kk = idx & 31; i = idx >> 5; }
-        As[kk][i] = ra[q];
-        int j;
-        if (!t.tb) { kk = idx & 31; j = idx >> 5; } else { j = idx & 63; kk = idx >> 6; }
-        Bs[kk][j] = rb[q];
-      }
-    };
-    if (g.K > 0) load(0);
-    for (int k0 = 0; k0 < g.K; k0 += GK) {
-      store();
-      __syncthreads();
-      if (k0 + GK < g.K) load(k0 + GK);   // in flight during the rank-1 updates below
-      const int kc = min(GK, g.K - k0);
-#pragma unroll 8
-      for (int kk = 0; kk < kc; ++kk) {
-        double av[4], bv[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) av[a] = As[kk][tx + 16 * a];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][ty + 16 * b];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) accs[a][b] = fma(av[a], bv[b], accs[a][b]);
-      }
-      __syncthreads();
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b] = fma(g.alpha, accs[a][b], acc[a][b]);
-  }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      int i = t.tm + tx + 16 * a, j = t.tn + ty + 16 * b;
-      if (i < t.M && j < t.N) {
-        double *p = t.tc ? &t.C[j + (int64_t)i * t.ldc] : &t.C[i + (int64_t)j * t.ldc];
-        *p = t.beta ? (*p + acc[a][b]) : acc[a][b];
-      }
-    }
-}
-
-// ---------------------------------------------------------------- Jacobi ----
-// One-sided (Hestenes) Jacobi on the symmetric PSD Gram matrix G = M^T M:
-// right rotations Y <- Y J until the columns of Y are mutually orthogonal;
-// then Y = G V = V diag(lambda): ||y_k|| = lambda_k = sigma_k^2 and
-// y_k / ||y_k|| = v_k, without accumulating V.  Cyclic round-robin pairs, one
-// warp per pair.  Rank r = #{sigma_k >= eps sigma_0}; eps = 0 keeps every
-// direction (reading Z3): V = I_m, r = m (r = 0 if G = 0, reading Z4).
-// k_gemm2: same task semantics as k_gemm (C tile 64 x 64 = sum_seg alpha op(A)
+// k_gemm2: tile GEMM tasks (C tile 64 x 64 = sum_seg alpha op(A)
 // op(B), beta accumulate, tc = store transposed), 128 threads with 4 x 8
 // accumulators each (32 FMAs per 12 shared loads), cp.async double-buffered
 // 16-deep K chunks (no staging registers), alpha folded into the A fragment
@@ -328,6 +233,107 @@ __global__ void __launch_bounds__(128, 4) k_gemm2(const GemmTask *__restrict__ t
   else gemm2_tile<8>(t, segs, As, Bs);
 }
 
+// k_gemm2_dmma: the same tasks on the FP64 tensor cores (DMMA, mma.sync
+// m8n8k4 .f64; north_star item 3).  Identical staging (cp.async double-buffered
+// 16-deep K chunks in shared memory); the 4 warps split the 64 x TN tile 2 x 2,
+// each warp owning 4 x (TN/16) 8 x 8 accumulator fragments.  Per 4-deep k step a
+// lane loads 4 A and TN/16 B fragment doubles for 4 x TN/16 DMMAs (256 / 128
+// flops per loaded double vs 5.3 for the DFMA tile).  Fragment layout (PTX
+// m8n8k4 .f64): A[g][t], B[t][g], C[g][2t + {0, 1}] with g = lane >> 2,
+// t = lane & 3.  Rounding differs from k_gemm2 (hardware accumulation order).
+__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+template <int NB>
+__device__ __forceinline__ void gemm2_tile_dmma(const GemmTask &t, const GemmSeg *__restrict__ segs,
+                                                double (*As)[G2K][GT + 1], double (*Bs)[G2K][GT + 1]) {
+  constexpr int TN = 8 * NB, CB = TN / 16;   // column fragments per warp
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp & 1, wc = warp >> 1;   // warp sub-tile: rows 32 wr.., cols (TN/2) wc..
+  const int g = lane >> 2, tq = lane & 3;
+  double acc[4][CB][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < CB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int s = 0; s < t.nseg; ++s) {
+    const GemmSeg gs = segs[t.seg0 + s];
+    if (gs.K <= 0) continue;
+    auto load = [&](int k0, int st) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int idx = tid + 128 * q;
+        int i, kk;
+        if (!t.ta) { i = idx & 63; kk = idx >> 6; } else { kk = idx & 15; i = idx >> 4; }
+        const int gi = t.tm + i, gk = k0 + kk;
+        cp_async8(&As[st][kk][i], t.ta ? gs.A + (gk + (int64_t)gi * gs.lda) : gs.A + (gi + (int64_t)gk * gs.lda),
+                  gs.A, gi < t.M && gk < gs.K);
+      }
+#pragma unroll
+      for (int q = 0; q < TN / 8; ++q) {
+        const int idx = tid + 128 * q;
+        int j, kk;
+        if (!t.tb) { kk = idx & 15; j = idx >> 4; } else { j = idx % TN; kk = idx / TN; }
+        const int gj = t.tn + j, gk = k0 + kk;
+        cp_async8(&Bs[st][kk][j], t.tb ? gs.B + (gj + (int64_t)gk * gs.ldb) : gs.B + (gk + (int64_t)gj * gs.ldb),
+                  gs.B, gj < t.N && gk < gs.K);
+      }
+      cp_async_commit();
+    };
+    const double alpha = gs.alpha;
+    const int nch = (gs.K + G2K - 1) / G2K;
+    load(0, 0);
+    for (int c = 0; c < nch; ++c) {
+      if (c + 1 < nch) {
+        load((c + 1) * G2K, (c + 1) & 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const int st = c & 1;
+#pragma unroll
+      for (int k4 = 0; k4 < G2K; k4 += 4) {
+        double af[4], bf[CB];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) af[a] = alpha * As[st][k4 + tq][32 * wr + 8 * a + g];
+#pragma unroll
+        for (int b = 0; b < CB; ++b) bf[b] = Bs[st][k4 + tq][(TN / 2) * wc + 8 * b + g];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < CB; ++b) dmma884(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < CB; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = t.tm + 32 * wr + 8 * a + g, j = t.tn + (TN / 2) * wc + 8 * b + 2 * tq + e;
+        if (i < t.M && j < t.N) {
+          double *p = t.tc ? &t.C[j + (int64_t)i * t.ldc] : &t.C[i + (int64_t)j * t.ldc];
+          *p = t.beta ? (*p + acc[a][b][e]) : acc[a][b][e];
+        }
+      }
+}
+
+__global__ void __launch_bounds__(128, 4) k_gemm2_dmma(const GemmTask *__restrict__ tasks,
+                                                     const GemmSeg *__restrict__ segs) {
+  __shared__ __align__(16) double As[2][G2K][GT + 1];
+  __shared__ __align__(16) double Bs[2][G2K][GT + 1];
+  pdl_trigger();
+  const GemmTask t = tasks[blockIdx.x];
+  pdl_wait();
+  if (t.tnw == 32) gemm2_tile_dmma<4>(t, segs, As, Bs);
+  else gemm2_tile_dmma<8>(t, segs, As, Bs);
+}
+
 struct EigTask {
   const double *G;   // m x m, ld m
   double *V;         // out: m x r (ld m), columns sorted by sigma descending
@@ -363,125 +369,7 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-constexpr int EIG_MAX_SWEEPS = 60;
 
-__global__ void __launch_bounds__(512) k_jacobi(const EigTask *__restrict__ tasks, double eps,
-                                                int smem_cap_doubles, int *status) {
-  extern __shared__ double sh[];
-  const EigTask t = tasks[blockIdx.x];
-  const int m = t.m;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  // shared layout: [lam (m) | rankpos (m ints as doubles) | X (m*m if it fits)]
-  double *lam = sh;
-  int *rk = reinterpret_cast<int *>(sh + m);
-  double *X = ((int64_t)m * m + 2 * m <= smem_cap_doubles) ? sh + 2 * m : t.work;
-  __shared__ int s_flag;
-  __shared__ double s_red[32];
-  for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) X[q] = t.G[q];
-  __syncthreads();
-  // Frobenius norm (zero test)
-  double fro = 0;
-  for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x) fro += X[q] * X[q];
-  fro = warp_sum(fro);
-  if (lane == 0) s_red[warp] = fro;
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0;
-    for (int w = 0; w < nw; ++w) s += s_red[w];
-    s_flag = (s > 0.0);
-  }
-  __syncthreads();
-  if (!s_flag) {
-    if (tid == 0) *t.rank_out = 0;
-    for (int q = tid; q < m; q += blockDim.x) t.sig[q] = 0.0;
-    return;
-  }
-  if (eps == 0.0) {  // nothing truncated: any orthonormal basis is exact
-    for (int64_t q = tid; q < (int64_t)m * m; q += blockDim.x)
-      t.V[q] = ((q % m) == (q / m)) ? 1.0 : 0.0;
-    for (int q = tid; q < m; q += blockDim.x) t.sig[q] = 0.0;
-    if (tid == 0) *t.rank_out = m;
-    return;
-  }
-  const int n2 = m + (m & 1);
-  const double tol = fmax(1e-14, 2.3e-16 * m);
-  int sweep = 0;
-  for (; sweep < EIG_MAX_SWEEPS; ++sweep) {
-    int rotated = 0;
-    for (int step = 0; step < n2 - 1; ++step) {
-      for (int j = warp; j < n2 / 2; j += nw) {
-        int pp = (j == 0) ? 0 : 1 + (j - 1 + step) % (n2 - 1);
-        int qp = n2 - 1 - j;
-        int qq = 1 + (qp - 1 + step) % (n2 - 1);
-        int p = pp, q = qq;
-        if (p >= m || q >= m) continue;
-        double *xp = X + (int64_t)p * m, *xq = X + (int64_t)q * m;
-        double al = 0, be = 0, ga = 0;
-        for (int r = lane; r < m; r += 32) {
-          double a = xp[r], b = xq[r];
-          al = fma(a, a, al);
-          be = fma(b, b, be);
-          ga = fma(a, b, ga);
-        }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (al == 0.0 || be == 0.0) continue;
-        if (fabs(ga) <= tol * sqrt(al) * sqrt(be)) continue;
-        double zeta = (be - al) / (2.0 * ga);
-        double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
-        for (int r = lane; r < m; r += 32) {
-          double a = xp[r], b = xq[r];
-          xp[r] = c * a - s * b;
-          xq[r] = s * a + c * b;
-        }
-        rotated = 1;
-      }
-      __syncthreads();
-    }
-    if (!__syncthreads_or(rotated)) break;
-  }
-  if (sweep == EIG_MAX_SWEEPS && tid == 0) {
-    atomicCAS(&status[0], 0, -4);
-    status[1] = t.node;
-  }
-  // lambda_k = ||y_k||
-  for (int k = warp; k < m; k += nw) {
-    double s = 0;
-    const double *xk = X + (int64_t)k * m;
-    for (int r = lane; r < m; r += 32) s = fma(xk[r], xk[r], s);
-    s = warp_sum(s);
-    if (lane == 0) lam[k] = sqrt(s);
-  }
-  __syncthreads();
-  // sort descending (stable by index): position of k
-  for (int k = tid; k < m; k += blockDim.x) {
-    double lk = lam[k];
-    int pos = 0;
-    for (int j = 0; j < m; ++j) {
-      double lj = lam[j];
-      pos += (lj > lk) || (lj == lk && j < k);
-    }
-    rk[k] = pos;
-  }
-  __syncthreads();
-  double lam0 = 0;
-  for (int k = 0; k < m; ++k) lam0 = fmax(lam0, lam[k]);
-  const double sig0 = sqrt(lam0);
-  int r = 0;
-  for (int k = 0; k < m; ++k) r += (sqrt(lam[k]) >= eps * sig0);
-  for (int k = tid; k < m; k += blockDim.x) t.sig[rk[k]] = sqrt(lam[k]);
-  for (int k = warp; k < m; k += nw) {
-    int pk = rk[k];
-    if (pk >= r) continue;
-    double inv = 1.0 / lam[k];
-    const double *xk = X + (int64_t)k * m;
-    double *vk = t.V + (int64_t)pk * m;
-    for (int q = lane; q < m; q += 32) vk[q] = xk[q] * inv;
-  }
-  if (tid == 0) *t.rank_out = r;
-}
 
 // ------------------------------------------------- tridiagonal eigen-solver ----
 // Symmetric eigen-decomposition of the Gram matrix G = M^T M for Compress
@@ -2684,7 +2572,33 @@ __device__ __forceinline__ void pivb_diag_inverse(const double *__restrict__ A, 
   }
 }
 
+// Shared-memory layout of k_pivot_blk: n padded to a multiple of 16 (the DMMA
+// fragments never leave the array; padding is zero), leading dimension
+// npad + 4 (= 4 mod 16 doubles: the 8 x 4 A/B and 8 x (2 x 4) C fragment
+// patterns of m8n8k4 hit every bank exactly twice, i.e. 2 wavefronts).
+__host__ __device__ constexpr int pivb_npad(int n) { return (n + 15) & ~15; }
+__host__ __device__ constexpr int pivb_lda(int n) { return pivb_npad(n) + 4; }
+__host__ __device__ constexpr size_t pivb_smem_bytes(int n) { return (size_t)pivb_npad(n) * pivb_lda(n) * 8; }
+
+// A fragment (8 x 4, row-major) of the shared array at rows r0.., columns c0..:
+// element (g, t); B fragment (4 x 8) of op(X) with X stored row = n-index:
+// element X(r0 + g, c0 + t) as B(t, g).  Both are the same load.
+__device__ __forceinline__ double frag_ld(const double *A, int lda, int r0, int c0) {
+  const int lane = threadIdx.x & 31;
+  return A[(r0 + (lane >> 2)) + (c0 + (lane & 3)) * lda];
+}
+
 __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict__ tasks, int *status) {
+  // Signed Cholesky K = L D L^T (D = diag(I_m, -I_r)) of the fused pivot with
+  // X = L^{-1} built on the fly, one CTA per node, 16-column blocks k:
+  //   warp 0 (critical path): trailing update of diagonal block k, its signed
+  //     Cholesky in registers (pivb_diag_chol) and W_k = L_kk^{-1}, stored as X_kk;
+  //   the other warps, beside it: the rest of the trailing update of step k-1,
+  //     and row block k of X (X_kj = -W_k sum_l L_kl X_lj, as M = W_k L_k,: in
+  //     place, then -M X into registers, written one phase later);
+  //   all warps: the panel L21 = A21 W_k^T D_k.
+  // Every product runs on the FP64 tensor cores (m8n8k4 DMMA fragments straight
+  // from shared memory); two block barriers per 16 columns.
   extern __shared__ double sh[];
   __shared__ double W[PIVB_NB * PIVB_NB];
   __shared__ double rd[PIVB_MAXN + PIVB_NB];   // 1 / l_kk
@@ -2695,97 +2609,157 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
   const int n = t.m + t.r;
   if (n == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int lda = n | 1;   // odd leading dimension: row-wise walks spread over banks
+  const int npad = pivb_npad(n), lda = pivb_lda(n), nb = npad / PIVB_NB;
+  const int g = lane >> 2, tq = lane & 3;
   double *A = sh;
-  for (int j = warp; j < n; j += nw)
-    for (int i = lane; i < n; i += 32) A[i + (int64_t)j * lda] = (i >= j) ? t.F[i + (int64_t)j * t.ld] : 0.0;
+  for (int j = warp; j < npad; j += nw)
+    for (int i = lane; i < npad; i += 32)
+      A[i + j * lda] = (i >= j && i < n && j < n) ? t.F[i + (int64_t)j * t.ld] : 0.0;
   if (tid == 0) s_fail = 0;
   __syncthreads();
-  // ---------------- blocked signed Cholesky ----------------
-  for (int j0 = 0; j0 < n; j0 += PIVB_NB) {
-    const int b = min(PIVB_NB, n - j0), j1 = j0 + b;
-    if (warp == 0) {
-      if (!pivb_diag_chol(A, lda, j0, b, t.m, rd, lane)) {   // 16-column diagonal block
-        if (lane == 0) {
-          s_fail = 1;
-          if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
-        }
-      } else {
-        pivb_diag_inverse(A, lda, j0, b, W, lane, rd);
+  // warp 0: factor diagonal block k (already updated), W = L_kk^{-1}, X_kk = W
+  auto diag = [&](int k) {
+    const int j0 = PIVB_NB * k, b = min(PIVB_NB, n - j0);
+    if (!pivb_diag_chol(A, lda, j0, b, t.m, rd, lane)) {
+      if (lane == 0) {
+        s_fail = 1;
+        if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
       }
+      return;
+    }
+    pivb_diag_inverse(A, lda, j0, b, W, lane, rd);
+    __syncwarp();
+    for (int q = lane; q < PIVB_NB * PIVB_NB; q += 32) {
+      const int i = q & 15, c = q >> 4;
+      if (i >= c) A[(j0 + i) + (j0 + c) * lda] = W[i + c * PIVB_NB];
+    }
+  };
+  // A22 block (r0, s0) -= L21(r0) D L21(s0)^T over the 16 columns j0..
+  auto trail = [&](int j0, int r0, int s0) {
+    double c0 = A[(r0 + g) + (s0 + 2 * tq) * lda], c1 = A[(r0 + g) + (s0 + 2 * tq + 1) * lda];
+#pragma unroll
+    for (int k4 = 0; k4 < 4; ++k4) {
+      const int kc = j0 + 4 * k4 + tq;
+      const double dk = (kc < t.m) ? -1.0 : 1.0;   // -d_k: subtract
+      const double av = frag_ld(A, lda, r0, j0 + 4 * k4);
+      const double bv = frag_ld(A, lda, s0, j0 + 4 * k4) * dk;
+      dmma884(c0, c1, av, bv);
+    }
+    A[(r0 + g) + (s0 + 2 * tq) * lda] = c0;
+    A[(r0 + g) + (s0 + 2 * tq + 1) * lda] = c1;
+  };
+  if (warp == 0) diag(0);
+  __syncthreads();
+  if (s_fail) return;
+  constexpr int MAXI = 3;   // X items per warp (4 k <= 36 items over 15 warps)
+  double xres[MAXI][2];
+  int xk = -1;              // row block whose X items are held in xres
+  for (int k = 0; k < nb; ++k) {
+    const int j0 = PIVB_NB * k, j1 = j0 + PIVB_NB;
+    const int nrb = (npad - j1) >> 3;
+    // ---- phase B: write X row block k-1; panel L21 of column block k; M = W_k L_k,
+    if (xk >= 0 && warp > 0) {
+#pragma unroll
+      for (int u = 0; u < MAXI; ++u) {
+        const int it = (warp - 1) + u * (nw - 1);
+        if (it >= 4 * xk) break;
+        const int rh = it & 1, cb = it >> 1;
+        const int row = PIVB_NB * xk + 8 * rh + g;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) A[row + (8 * cb + 2 * tq + e) * lda] = xres[u][e];
+      }
+    }
+    for (int it = warp; it < nrb + 2 * k; it += nw) {
+      if (it < nrb) {   // panel: L21(8-row block) = A21 (W^T D), B(kk, c) = W[c][kk] d_c
+        const int r0 = j1 + 8 * it;
+        double af[4];
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) af[k4] = frag_ld(A, lda, r0, j0 + 4 * k4);
+        double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb) {
+          const int col = 8 * cb + g;
+          const double dc = (j0 + col < t.m) ? 1.0 : -1.0;
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) dmma884(c[cb][0], c[cb][1], af[k4], W[col + (4 * k4 + tq) * PIVB_NB] * dc);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) A[(r0 + g) + (j0 + 8 * cb + 2 * tq + e) * lda] = c[cb][e];
+      } else {          // M(:, 8-col block cb) = W L_k(:, cb), both row halves, in place
+        const int cb = it - nrb;
+        double bf[4];
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) bf[k4] = A[(j0 + 4 * k4 + tq) + (8 * cb + g) * lda];
+        double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+        for (int rh = 0; rh < 2; ++rh)
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) dmma884(c[rh][0], c[rh][1], W[(8 * rh + g) + (4 * k4 + tq) * PIVB_NB], bf[k4]);
+        __syncwarp();
+#pragma unroll
+        for (int rh = 0; rh < 2; ++rh)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) A[(j0 + 8 * rh + g) + (8 * cb + 2 * tq + e) * lda] = c[rh][e];
+      }
+    }
+    __syncthreads();
+    // ---- phase C: warp 0 updates + factors diagonal block k+1; the others: the
+    // rest of the trailing update and X row block k = -M X (registers)
+    if (warp == 0) {
+      if (nrb > 0) {
+        trail(j0, j1, j1);
+        trail(j0, j1 + 8, j1);
+        trail(j0, j1 + 8, j1 + 8);
+        __syncwarp();
+        diag(k + 1);
+      }
+    } else {
+      const int npair = nrb * (nrb + 1) / 2;
+      for (int q = warp - 1 + 3; q < npair; q += nw - 1) {   // pairs 0..2 = diagonal block k+1
+        int ib = (int)((sqrtf(8.0f * q + 1.0f) - 1.0f) * 0.5f);
+        while ((ib + 1) * (ib + 2) / 2 <= q) ++ib;
+        while (ib * (ib + 1) / 2 > q) --ib;
+        const int jb = q - ib * (ib + 1) / 2;
+        trail(j0, j1 + 8 * ib, j1 + 8 * jb);
+      }
+#pragma unroll
+      for (int u = 0; u < MAXI; ++u) {
+        const int it = (warp - 1) + u * (nw - 1);
+        if (it >= 4 * k) break;
+        const int rh = it & 1, cb = it >> 1;
+        const int r0 = j0 + 8 * rh;
+        double c0 = 0.0, c1 = 0.0;
+        for (int k0 = 8 * cb; k0 < j0; k0 += 4) {   // X(l, col) = 0 for l < col
+          const double av = A[(r0 + g) + (k0 + tq) * lda];           // M(row, l)
+          double bv = A[(k0 + tq) + (8 * cb + g) * lda];             // X(l, col)
+          if (k0 + tq < 8 * cb + g) bv = 0.0;
+          dmma884(c0, c1, av, bv);
+        }
+        xres[u][0] = -c0;
+        xres[u][1] = -c1;
+      }
+      xk = k;
     }
     __syncthreads();
     if (s_fail) return;
-    // panel: row i of L21 = d .* (Linv11 applied to row i of A21)
-    for (int i = j1 + tid; i < n; i += blockDim.x) {
-      double a[PIVB_NB];
-#pragma unroll
-      for (int k = 0; k < PIVB_NB; ++k) a[k] = (k < b) ? A[i + (int64_t)(j0 + k) * lda] : 0.0;
-#pragma unroll
-      for (int c = 0; c < PIVB_NB; ++c) {
-        if (c < b) {
-          double sacc = 0;
-#pragma unroll
-          for (int k = 0; k <= c; ++k) sacc = fma(W[c + k * PIVB_NB], a[k], sacc);
-          const double dc = (j0 + c < t.m) ? 1.0 : -1.0;
-          A[i + (int64_t)(j0 + c) * lda] = sacc * dc;
-        }
-      }
-    }
-    __syncthreads();
-    // trailing lower triangle: A22 -= L21 D1 L21^T
-    for (int j = j1 + warp; j < n; j += nw) {
-      double lj[PIVB_NB];
-#pragma unroll
-      for (int c = 0; c < PIVB_NB; ++c) {
-        const double dc = (j0 + c < t.m) ? 1.0 : -1.0;
-        lj[c] = (c < b) ? A[j + (int64_t)(j0 + c) * lda] * dc : 0.0;
-      }
-      for (int i = j + lane; i < n; i += 32) {
-        double sacc = A[i + (int64_t)j * lda];
-#pragma unroll
-        for (int c = 0; c < PIVB_NB; ++c)
-          if (c < b) sacc = fma(-A[i + (int64_t)(j0 + c) * lda], lj[c], sacc);
-        A[i + (int64_t)j * lda] = sacc;
-      }
-    }
-    __syncthreads();
   }
-  // ---------------- blocked in-place inverse of L ----------------
-  const int last = ((n - 1) / PIVB_NB) * PIVB_NB;
-  for (int j0 = last; j0 >= 0; j0 -= PIVB_NB) {
-    const int b = min(PIVB_NB, n - j0), j1 = j0 + b;
-    // (a) T = X22 L21 (rows j1.., cols 0..b), parked transposed in A[j0 + c, j1 + row] (free upper part)
-    if (warp == 0) {
-      pivb_diag_inverse(A, lda, j0, b, W, lane, rd);
-    } else {
-      const int rows = n - j1;
-      for (int q = tid - 32; q < rows * b; q += blockDim.x - 32) {
-        const int ii = q % rows, c = q / rows, i = j1 + ii;
-        double sacc = 0;
-        for (int k = j1; k <= i; ++k) sacc = fma(A[i + (int64_t)k * lda], A[k + (int64_t)(j0 + c) * lda], sacc);
-        A[(j0 + c) + (int64_t)i * lda] = sacc;   // upper part: row j0+c, column i
-      }
+  if (warp > 0 && xk >= 0) {   // the last X row block
+#pragma unroll
+    for (int u = 0; u < MAXI; ++u) {
+      const int it = (warp - 1) + u * (nw - 1);
+      if (it >= 4 * xk) break;
+      const int rh = it & 1, cb = it >> 1;
+      const int row = PIVB_NB * xk + 8 * rh + g;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) A[row + (8 * cb + 2 * tq + e) * lda] = xres[u][e];
     }
-    __syncthreads();
-    // (b) A21 <- -T L11^{-1};  A11 <- L11^{-1}
-    {
-      const int rows = n - j1;
-      for (int q = tid; q < rows * b; q += blockDim.x) {
-        const int ii = q % rows, c = q / rows, i = j1 + ii;
-        double sacc = 0;
-        for (int k = c; k < b; ++k) sacc = fma(A[(j0 + k) + (int64_t)i * lda], W[k + c * PIVB_NB], sacc);
-        A[i + (int64_t)(j0 + c) * lda] = -sacc;
-      }
-      for (int q = tid; q < b * b; q += blockDim.x) {
-        const int i = q % b, c = q / b;
-        if (i >= c) A[(j0 + i) + (int64_t)(j0 + c) * lda] = W[i + c * PIVB_NB];
-      }
-    }
-    __syncthreads();
   }
+  __syncthreads();
   for (int j = warp; j < n; j += nw)
-    for (int i = lane; i < n; i += 32) t.F[i + (int64_t)j * t.ld] = (i >= j) ? A[i + (int64_t)j * lda] : 0.0;
+    for (int i = lane; i < n; i += 32) t.F[i + (int64_t)j * t.ld] = (i >= j) ? A[i + j * lda] : 0.0;
 }
 
 // Blocked no-pivot LU of the fused LU-path pivot, same outputs as k_pivot_lu
@@ -2796,7 +2770,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
 // Inverses, last block first: L21 <- -(X22 L21) X11 and U12 <- -Y11 (U12 Y22)
 // with X = L^{-1}, Y = U^{-1} of the already inverted trailing parts (scratch
 // TL, TU: n x 16 each).  Singular if |u_kk| <= 1e-14 max|A| (as k_pivot_lu).
-constexpr int PIVLU_MAXN = 148;
+constexpr int PIVLU_MAXN = 160;
 // no-pivot LU of the b x b diagonal block at j0 by one warp, block in registers
 // (lane = row; the pivot row's entries by shuffles).  rd[j0 + k] <- 1 / u_kk.
 // Returns false when |u_kk| <= tiny (uniform across the warp).
@@ -2878,6 +2852,14 @@ __device__ __forceinline__ void lu_diag_inverses(const double *__restrict__ A, i
 }
 
 __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restrict__ tasks, int *status) {
+  // Same shared-memory layout as k_pivot_blk (npad, lda = npad + 4).  Per
+  // 16-column block: warp 0 factors the diagonal block (lu_diag_factor) and
+  // inverts both triangles (WL = L11^{-1}, WU = U11^{-1}); the panels
+  // L21 = A21 WU and U12^T = A12^T WL^T and the trailing A22 -= L21 U12 run on the
+  // FP64 tensor cores (m8n8k4 DMMA, 8 x 8 blocks over the warps).  Inverses,
+  // last block first (X = L^{-1} strict lower, Y = U^{-1} upper, one array):
+  //   P = L21 X11, Q^T = U12^T Y11^T (in place, rows owned by one warp);
+  //   X21 = -X22 P, Y12^T = -Y22^T Q^T (DMMA into registers, written after a barrier).
   extern __shared__ double sh[];
   __shared__ double WL[PIVB_NB * PIVB_NB], WU[PIVB_NB * PIVB_NB];
   __shared__ double rd[PIVLU_MAXN + PIVB_NB];   // 1 / u_kk
@@ -2889,27 +2871,22 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
   const int n = t.m + t.r;
   if (n == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int lda = n | 1;
+  const int npad = pivb_npad(n), lda = pivb_lda(n);
+  const int g = lane >> 2, tq = lane & 3;
   double *A = sh;
-  double *TL = sh + (int64_t)lda * n;           // (n x 16, ld n): X22 L21
-  double *TU = TL + (int64_t)n * PIVB_NB;       // (n x 16, ld n): (U12 Y22)^T
   double amax = 0;
-  for (int j = warp; j < n; j += nw)
-    for (int i = lane; i < n; i += 32) {
-      const double v = t.F[i + (int64_t)j * t.ld];
-      A[i + (int64_t)j * lda] = v;
+  for (int j = warp; j < npad; j += nw)
+    for (int i = lane; i < npad; i += 32) {
+      const double v = (i < n && j < n) ? t.F[i + (int64_t)j * t.ld] : 0.0;
+      A[i + j * lda] = v;
       amax = fmax(amax, fabs(v));
     }
-  for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-  if (lane == 0) s_amax[warp] = amax;
   if (tid == 0) s_fail = 0;
-  __syncthreads();
-  amax = 0;
-  for (int w = 0; w < nw; ++w) amax = fmax(amax, s_amax[w]);
+  amax = block_max(amax, s_amax);
   const double tiny = 1e-14 * amax;
   // ---------------- blocked LU (no pivoting) ----------------
   for (int j0 = 0; j0 < n; j0 += PIVB_NB) {
-    const int b = min(PIVB_NB, n - j0), j1 = j0 + b;
+    const int b = min(PIVB_NB, n - j0), j1 = j0 + PIVB_NB;
     if (warp == 0) {
       if (!lu_diag_factor(A, lda, j0, b, tiny, rd, lane)) {
         if (lane == 0) {
@@ -2922,51 +2899,49 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
     }
     __syncthreads();
     if (s_fail) return;
-    // panels: rows i >= j1 (L21 = A21 U11^{-1}) and columns j >= j1 (U12 = L11^{-1} A12)
-    const int rest = n - j1;
-    for (int q = tid; q < 2 * rest; q += blockDim.x) {
-      double a[PIVB_NB];
-      if (q < rest) {
-        const int i = j1 + q;
+    const int nrb = (npad - j1) >> 3;
+    if (nrb == 0) break;
+    // panels: items < nrb are 8-row blocks of L21 = A21 WU; the rest 8-column
+    // blocks of U12, computed as U12^T = A12^T WL^T (rows j of U12^T)
+    for (int it = warp; it < 2 * nrb; it += nw) {
+      const bool lrow = it < nrb;
+      const int r0 = j1 + 8 * (lrow ? it : it - nrb);
+      double af[4];
 #pragma unroll
-        for (int k = 0; k < PIVB_NB; ++k) a[k] = (k < b) ? A[i + (int64_t)(j0 + k) * lda] : 0.0;
+      for (int k4 = 0; k4 < 4; ++k4)
+        af[k4] = lrow ? A[(r0 + g) + (j0 + 4 * k4 + tq) * lda] : A[(j0 + 4 * k4 + tq) + (r0 + g) * lda];
+      double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-        for (int c = 0; c < PIVB_NB; ++c) {
-          if (c < b) {
-            double sacc = 0.0;
+      for (int cb = 0; cb < 2; ++cb)
 #pragma unroll
-            for (int k = 0; k <= c; ++k) sacc = fma(a[k], WU[k + c * PIVB_NB], sacc);
-            A[i + (int64_t)(j0 + c) * lda] = sacc;
-          }
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const int k = 4 * k4 + tq, col = 8 * cb + g;
+          const double bv = lrow ? WU[k + col * PIVB_NB] : WL[col + k * PIVB_NB];
+          dmma884(c[cb][0], c[cb][1], af[k4], bv);
         }
-      } else {
-        const int j = j1 + (q - rest);
+      __syncwarp();
 #pragma unroll
-        for (int k = 0; k < PIVB_NB; ++k) a[k] = (k < b) ? A[(j0 + k) + (int64_t)j * lda] : 0.0;
+      for (int cb = 0; cb < 2; ++cb)
 #pragma unroll
-        for (int c = 0; c < PIVB_NB; ++c) {
-          if (c < b) {
-            double sacc = a[c];   // unit diagonal of L11^{-1}
-#pragma unroll
-            for (int k = 0; k < c; ++k) sacc = fma(WL[c + k * PIVB_NB], a[k], sacc);
-            A[(j0 + c) + (int64_t)j * lda] = sacc;
-          }
+        for (int e = 0; e < 2; ++e) {
+          const int cc = j0 + 8 * cb + 2 * tq + e;
+          if (lrow) A[(r0 + g) + cc * lda] = c[cb][e];
+          else A[cc + (r0 + g) * lda] = c[cb][e];
         }
-      }
     }
     __syncthreads();
-    // trailing: A22 -= L21 U12
-    for (int j = j1 + warp; j < n; j += nw) {
-      double uj[PIVB_NB];
+    // trailing: A22(ib, jb) -= L21(ib) U12(jb), every block
+    for (int q = warp; q < nrb * nrb; q += nw) {
+      const int r0 = j1 + 8 * (q / nrb), s0 = j1 + 8 * (q % nrb);
+      double c0 = A[(r0 + g) + (s0 + 2 * tq) * lda], c1 = A[(r0 + g) + (s0 + 2 * tq + 1) * lda];
 #pragma unroll
-      for (int c = 0; c < PIVB_NB; ++c) uj[c] = (c < b) ? A[(j0 + c) + (int64_t)j * lda] : 0.0;
-      for (int i = j1 + lane; i < n; i += 32) {
-        double sacc = A[i + (int64_t)j * lda];
-#pragma unroll
-        for (int c = 0; c < PIVB_NB; ++c)
-          if (c < b) sacc = fma(-A[i + (int64_t)(j0 + c) * lda], uj[c], sacc);
-        A[i + (int64_t)j * lda] = sacc;
+      for (int k4 = 0; k4 < 4; ++k4) {
+        const double av = A[(r0 + g) + (j0 + 4 * k4 + tq) * lda];     // L21(row, k)
+        const double bv = -A[(j0 + 4 * k4 + tq) + (s0 + g) * lda];    // -U12(k, col)
+        dmma884(c0, c1, av, bv);
       }
+      A[(r0 + g) + (s0 + 2 * tq) * lda] = c0;
+      A[(r0 + g) + (s0 + 2 * tq + 1) * lda] = c1;
     }
     __syncthreads();
   }
@@ -2975,48 +2950,87 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
     return;
   }
   // ---------------- blocked inverses, last block first ----------------
+  constexpr int MAXI = 3;   // items per warp (2 * nrb <= 36 for npad <= 160)
   const int last = ((n - 1) / PIVB_NB) * PIVB_NB;
   for (int j0 = last; j0 >= 0; j0 -= PIVB_NB) {
-    const int b = min(PIVB_NB, n - j0), j1 = j0 + b, rest = n - j1;
-    // (a) warp 0: WL = L11^{-1}, WU = U11^{-1}; the others:
-    //     TL[i][c] = sum_{k=j1}^{i} X22[i][k] L21[k][c]   (X22 unit lower, inverted)
-    //     TU[j][c] = sum_{k=j1}^{j} U12[c][k] Y22[k][j]   (Y22 upper, inverted)
-    if (warp == 0) {
-      lu_diag_inverses(A, lda, j0, b, WL, WU, lane, rd);
-    } else {
-      for (int q = tid - 32; q < 2 * rest * b; q += blockDim.x - 32) {
-        if (q < rest * b) {
-          const int ii = q % rest, c = q / rest, i = j1 + ii;
-          double sacc = A[i + (int64_t)(j0 + c) * lda];   // k = i (unit diagonal of X22)
-          for (int k = j1; k < i; ++k) sacc = fma(A[i + (int64_t)k * lda], A[k + (int64_t)(j0 + c) * lda], sacc);
-          TL[ii + (int64_t)c * n] = sacc;
-        } else {
-          const int qq = q - rest * b, jj = qq % rest, c = qq / rest, j = j1 + jj;
-          double sacc = 0.0;
-          for (int k = j1; k <= j; ++k) sacc = fma(A[(j0 + c) + (int64_t)k * lda], A[k + (int64_t)j * lda], sacc);
-          TU[jj + (int64_t)c * n] = sacc;
+    const int b = min(PIVB_NB, n - j0), j1 = j0 + PIVB_NB;
+    const int nrb = (npad - j1) >> 3;
+    if (warp == 0) lu_diag_inverses(A, lda, j0, b, WL, WU, lane, rd);
+    __syncthreads();
+    // phase 1: P = L21 X11 (rows), Q^T = U12^T Y11^T (rows j of U12^T), in place
+    for (int it = warp; it < 2 * nrb; it += nw) {
+      const bool lrow = it < nrb;
+      const int r0 = j1 + 8 * (lrow ? it : it - nrb);
+      double af[4];
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4)
+        af[k4] = lrow ? A[(r0 + g) + (j0 + 4 * k4 + tq) * lda] : A[(j0 + 4 * k4 + tq) + (r0 + g) * lda];
+      double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+        for (int k4 = 0; k4 < 4; ++k4) {
+          const int k = 4 * k4 + tq, col = 8 * cb + g;
+          const double bv = lrow ? WL[k + col * PIVB_NB] : WU[col + k * PIVB_NB];
+          dmma884(c[cb][0], c[cb][1], af[k4], bv);
         }
-      }
+      __syncwarp();
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cc = j0 + 8 * cb + 2 * tq + e;
+          if (lrow) A[(r0 + g) + cc * lda] = c[cb][e];
+          else A[cc + (r0 + g) * lda] = c[cb][e];
+        }
     }
     __syncthreads();
-    // (b) L21 <- -TL X11,  U12 <- -Y11 TU^T,  A11 <- (X11 strict lower | Y11 upper)
-    for (int q = tid; q < 2 * rest * b; q += blockDim.x) {
-      if (q < rest * b) {
-        const int ii = q % rest, c = q / rest, i = j1 + ii;
-        double sacc = TL[ii + (int64_t)c * n];   // X11[c][c] = 1
-        for (int k = c + 1; k < b; ++k) sacc = fma(TL[ii + (int64_t)k * n], WL[k + c * PIVB_NB], sacc);
-        A[i + (int64_t)(j0 + c) * lda] = -sacc;
-      } else {
-        const int qq = q - rest * b, jj = qq % rest, c = qq / rest, j = j1 + jj;
-        double sacc = 0.0;
-        for (int k = c; k < b; ++k) sacc = fma(WU[c + k * PIVB_NB], TU[jj + (int64_t)k * n], sacc);
-        A[(j0 + c) + (int64_t)j * lda] = -sacc;
+    // phase 2: X21 = -X22 P (X22 unit lower), Y12^T = -Y22^T Q^T (Y22 upper)
+    double res[MAXI][2][2];
+#pragma unroll
+    for (int u = 0; u < MAXI; ++u) {
+      const int it = warp + u * nw;
+      if (it >= 2 * nrb) break;
+      const bool lrow = it < nrb;
+      const int r0 = j1 + 8 * (lrow ? it : it - nrb);
+      double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      for (int k0 = j1; k0 < r0 + 8; k0 += 4) {
+        const int row = r0 + g, kc = k0 + tq;
+        double av;
+        if (lrow) av = (kc < row) ? A[row + kc * lda] : (kc == row ? 1.0 : 0.0);   // X22(row, k)
+        else av = (kc <= row) ? A[kc + row * lda] : 0.0;                           // Y22(k, row)
+#pragma unroll
+        for (int cb = 0; cb < 2; ++cb) {
+          const int col = j0 + 8 * cb + g;
+          const double bv = lrow ? A[(k0 + tq) + col * lda] : A[col + (k0 + tq) * lda];   // P(k, c) / Q^T(k, c)
+          dmma884(c[cb][0], c[cb][1], av, bv);
+        }
       }
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) res[u][cb][e] = -c[cb][e];
     }
-    for (int q = tid; q < b * b; q += blockDim.x) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < MAXI; ++u) {
+      const int it = warp + u * nw;
+      if (it >= 2 * nrb) break;
+      const bool lrow = it < nrb;
+      const int r0 = j1 + 8 * (lrow ? it : it - nrb);
+#pragma unroll
+      for (int cb = 0; cb < 2; ++cb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cc = j0 + 8 * cb + 2 * tq + e;
+          const double v = res[u][cb][e];
+          if (lrow) A[(r0 + g) + cc * lda] = v;
+          else A[cc + (r0 + g) * lda] = v;
+        }
+    }
+    for (int q = tid; q < b * b; q += blockDim.x) {   // X11 strict lower, Y11 upper
       const int i = q % b, c = q / b;
-      if (i > c) A[(j0 + i) + (int64_t)(j0 + c) * lda] = WL[i + c * PIVB_NB];
-      else A[(j0 + i) + (int64_t)(j0 + c) * lda] = WU[i + c * PIVB_NB];
+      A[(j0 + i) + (j0 + c) * lda] = (i > c) ? WL[i + c * PIVB_NB] : WU[i + c * PIVB_NB];
     }
     __syncthreads();
   }
@@ -3024,8 +3038,8 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
   double *R1 = t.F2 ? t.F2 : t.F + (int64_t)t.ld * n;
   for (int j = warp; j < n; j += nw)
     for (int i = lane; i < n; i += 32) {
-      t.F[i + (int64_t)j * t.ld] = (i > j) ? A[i + (int64_t)j * lda] : (i == j ? 1.0 : 0.0);
-      R1[i + (int64_t)j * t.ld] = (i >= j) ? A[j + (int64_t)i * lda] : 0.0;
+      t.F[i + (int64_t)j * t.ld] = (i > j) ? A[i + j * lda] : (i == j ? 1.0 : 0.0);
+      R1[i + (int64_t)j * t.ld] = (i >= j) ? A[j + i * lda] : 0.0;
     }
 }
 

@@ -291,8 +291,8 @@ enum KClass {
 static const char *KNAME[K_NCLASS] = {"leaf_scatter", "merge_copy", "gram_gemm", "eig_tridiag",
                                       "project_gemm", "assemble_copy", "pivot_chol_inv", "trsm_gemm",
                                       "schur_gemm", "apply_fwd", "apply_bwd", "spmv", "dot", "vec"};
-static const char *KKERNEL[K_NCLASS] = {"k_leaf_scatter", "k_copy", "k_gemm", "k_tridiag_* + k_eig_t", "k_gemm", "k_copy",
-                                        "k_pivot", "k_gemm", "k_gemm", "k_apply_fwd", "k_apply_bwd",
+static const char *KKERNEL[K_NCLASS] = {"k_leaf_scatter", "k_copy", "k_gemm2_dmma", "k_tridiag_* + k_eig_t", "k_gemm2_dmma", "k_copy",
+                                        "k_pivot", "k_gemm2_dmma", "k_gemm2_dmma", "k_apply_fwd", "k_apply_bwd",
                                         "k_spmv", "k_dot_partial+k_dot_final", "k_axpby/k_sub/k_set_rhs/k_get_x"};
 struct KStat {
   double ms = 0, flops = 0, bytes = 0;
@@ -374,7 +374,6 @@ struct lorasp_ctx {
   void *h_sp = nullptr;     // pinned upload of the part-1 copy + pivot task lists
   size_t h_sp_cap = 0;
   bool no_split = getenv("LORASP_NO_SPLIT") != nullptr;
-  bool gemm_v1 = getenv("LORASP_GEMM_V1") != nullptr;   // debug: the 256-thread 4 x 4 GEMM
   bool no_split_lu = getenv("LORASP_NO_SPLIT_LU") != nullptr;   // A/B: fused LU pivots only
   // rank-predicted schedule: after a factorization, its ranks predict the
   // next one's (same pattern); the host then builds and enqueues every wave
@@ -648,7 +647,6 @@ void ensure_mem(lorasp_ctx *h) {
   CK(cudaMallocHost(&h->h_dot, 1024 * sizeof(double)));   // GMRES Hessenberg column (restart <= 1000)
   h->d_dotpart.ensure((DOT_BLOCKS + 1024) * sizeof(double), h->stream);
   h->stg.init(size_t(64) << 20, h->stream);
-  CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   set_eig_attrs();
   {
     int least = 0, greatest = 0;
@@ -697,8 +695,7 @@ void launch_gemm_dev(lorasp_ctx *h, const GemmTask *dt, const GemmSeg *ds, size_
                      double bytes) {
   if (ntasks == 0) return;
   int ev = cls >= 0 ? tbeg(h, cls) : -1;
-  if (h->gemm_v1) k_gemm<<<(unsigned)ntasks, 256, 0, h->stream>>>(dt, ds);
-  else launch_k(k_gemm2, (unsigned)ntasks, 128, 0, h->stream, dt, ds);
+  launch_k(k_gemm2_dmma, (unsigned)ntasks, 128, 0, h->stream, dt, ds);   // DMMA beats DFMA on every shape
   tend(h, ev, flops, bytes);
   ++h->launches_factor;
   CK(cudaGetLastError());
@@ -721,8 +718,7 @@ void launch_gemm(lorasp_ctx *h, const std::vector<GemmTask> &tasks, const std::v
   GemmSeg *ds = push(h, segs);
   GemmTask *dt = push(h, tasks);
   int ev = cls >= 0 ? tbeg(h, cls) : -1;
-  if (h->gemm_v1) k_gemm<<<(unsigned)tasks.size(), 256, 0, h->stream>>>(dt, ds);
-  else launch_k(k_gemm2, (unsigned)tasks.size(), 128, 0, h->stream, dt, ds);
+  launch_k(k_gemm2_dmma, (unsigned)tasks.size(), 128, 0, h->stream, dt, ds);
   tend(h, ev, flops, bytes);
   ++h->launches_factor;
   CK(cudaGetLastError());
@@ -856,10 +852,9 @@ void launch_copy(lorasp_ctx *h, const std::vector<CopyTask> &tasks, int cls) {
 }
 
 // tile a logical M x N product into 64x64 tasks
-static bool g_narrow_tiles = getenv("LORASP_GEMM_V1") == nullptr;   // k_gemm2 supports 64 x 32 tiles
 void add_tiles(std::vector<GemmTask> &tasks, GemmTask base, int kmax_by_row = 0) {
   (void)kmax_by_row;
-  if (g_narrow_tiles && base.N <= 32) {   // narrow product (e.g. R_k = A_k^T V with r <= 32)
+  if (base.N <= 32) {   // narrow product (e.g. R_k = A_k^T V with r <= 32)
     for (int tm = 0; tm < base.M; tm += GT) {
       GemmTask t = base;
       t.tm = tm;
@@ -912,7 +907,7 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
   if (!small.empty()) {
     PivTask *dp = push(h, small);
     if (max_n <= PIVB_MAXN && !h->pivot_unblocked) {
-      const size_t sm = (size_t)(max_n | 1) * max_n * 8;
+      const size_t sm = pivb_smem_bytes(max_n);
       launch_k(k_pivot_blk, (unsigned)small.size(), 512, sm, st, dp, h->d_status.as<int>());
     } else {
       int64_t want = (int64_t)max_n * max_n + max_n;
@@ -1082,7 +1077,7 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
   PivTask *dp = push(h, h->lu_pivot ? pvp : pv);
   int ev = tbeg(h, K_PIVOT);
   if (max_n <= PIVLU_MAXN && !h->pivot_unblocked && !h->lu_pivot) {
-    const size_t sm = ((size_t)(max_n | 1) * max_n + 2 * (size_t)max_n * PIVB_NB) * 8;
+    const size_t sm = pivb_smem_bytes(max_n);
     launch_k(k_pivot_lu_blk, (unsigned)pv.size(), 512, sm, h->stream, dp, h->d_status.as<int>());
   } else {
     int64_t want = (int64_t)max_n * max_n + 2 * max_n;
@@ -1468,10 +1463,10 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         }
         launch_k(k_copy, (unsigned)s_ct.size(), 256, 0, h->stream2, dct);
         if (sym) {
-          const size_t smem = (size_t)(s_max | 1) * s_max * 8;
+          const size_t smem = pivb_smem_bytes(s_max);
           launch_k(k_pivot_blk, (unsigned)s_pt.size(), 512, smem, h->stream2, dpt, h->d_status.as<int>());
         } else {   // no-pivot LU of S: L11^{-1} and U11^{-T} side by side in ws_S
-          const size_t smem = ((size_t)(s_max | 1) * s_max + 2 * (size_t)s_max * PIVB_NB) * 8;
+          const size_t smem = pivb_smem_bytes(s_max);
           launch_k(k_pivot_lu_blk, (unsigned)s_pt.size(), 512, smem, h->stream2, dpt, h->d_status.as<int>());
         }
         h->launches_factor += 2;
@@ -3253,10 +3248,8 @@ int lorasp_get_launch_count(lorasp_handle h, int64_t *f, int64_t *a, int64_t *k)
 
 int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, double *sigma, int *rank) {
   if (!G || !V || !sigma || !rank || m <= 0) return LORASP_E_ARG;
-  const bool jac = getenv("LORASP_EIG_JACOBI") != nullptr;  // debug: the one-sided Jacobi variant
   try {
     CK(cudaSetDevice(device));
-    CK(cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
     set_eig_attrs();
     double *dG, *dV, *dS, *dW;
     int *dr, *dst;
@@ -3287,11 +3280,7 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     EigTask *de;
     CK(cudaMalloc(&de, sizeof(EigTask)));
     CK(cudaMemcpy(de, &e, sizeof(EigTask), cudaMemcpyHostToDevice));
-    if (jac) {
-      int cap = (int)std::min<int64_t>((int64_t)m * m + 2 * m, SMEM_LIMIT / 8);
-      cap = std::max(cap, 2 * m);
-      k_jacobi<<<1, 512, cap * 8>>>(de, eps, cap, dst);
-    } else {
+    {
       if (m >= EIG_REG_MIN && m <= EIG_REG_M && !getenv("LORASP_EIG_GENERIC")) {
         if (ddbg) {
           long long *dprof;
@@ -3378,6 +3367,73 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
   }
 }
 
+// GEMM kernel comparison hook (north_star item 3, DMMA vs DFMA per block
+// shape): `reps` independent copies of C = op(A) op(B) (a wave of equal GEMMs)
+// through k_gemm2 (variant 0, FP64 FMA pipe) or k_gemm2_dmma (variant 1, FP64
+// tensor cores); *ms = CUDA-event time of one launch (after a warm-up); C of
+// the first copy returned.  A: M x K (ld M) or, ta, K x M (ld K); B: K x N (ld K)
+// or, tb, N x K (ld N); C: M x N (ld M), host buffers.
+int lorasp_test_gemm(int device, int variant, int M, int N, int K, int ta, int tb, int reps, const double *A,
+                     const double *B, double *C, double *ms) {
+  if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0 || reps <= 0 || variant < 0 || variant > 1) return LORASP_E_ARG;
+  try {
+    CK(cudaSetDevice(device));
+    double *dA, *dB, *dC;
+    CK(cudaMalloc(&dA, (size_t)M * K * 8 * reps));
+    CK(cudaMalloc(&dB, (size_t)K * N * 8 * reps));
+    CK(cudaMalloc(&dC, (size_t)M * N * 8 * reps));
+    for (int q = 0; q < reps; ++q) {
+      CK(cudaMemcpy(dA + (size_t)q * M * K, A, (size_t)M * K * 8, cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(dB + (size_t)q * K * N, B, (size_t)K * N * 8, cudaMemcpyHostToDevice));
+    }
+    std::vector<GemmTask> tasks;
+    std::vector<GemmSeg> segs;
+    for (int q = 0; q < reps; ++q) {
+      GemmTask g{};
+      g.C = dC + (size_t)q * M * N;
+      g.ldc = M;
+      g.M = M;
+      g.N = N;
+      g.ta = ta;
+      g.tb = tb;
+      g.beta = 0;
+      g.seg0 = (int)segs.size();
+      g.nseg = 1;
+      segs.push_back(GemmSeg{dA + (size_t)q * M * K, dB + (size_t)q * K * N, ta ? K : M, tb ? N : K, K, 1.0});
+      add_tiles(tasks, g);
+    }
+    GemmTask *dt;
+    GemmSeg *ds;
+    CK(cudaMalloc(&dt, tasks.size() * sizeof(GemmTask)));
+    CK(cudaMalloc(&ds, segs.size() * sizeof(GemmSeg)));
+    CK(cudaMemcpy(dt, tasks.data(), tasks.size() * sizeof(GemmTask), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ds, segs.data(), segs.size() * sizeof(GemmSeg), cudaMemcpyHostToDevice));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int it = 0; it < 4; ++it) {
+      CK(cudaEventRecord(e0));
+      if (variant == 0) k_gemm2<<<(unsigned)tasks.size(), 128>>>(dt, ds);
+      else k_gemm2_dmma<<<(unsigned)tasks.size(), 128>>>(dt, ds);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float t = 0;
+      CK(cudaEventElapsedTime(&t, e0, e1));
+      if (it > 0) best = std::min(best, t);
+    }
+    CK(cudaGetLastError());
+    *ms = best;
+    CK(cudaMemcpy(C, dC, (size_t)M * N * 8, cudaMemcpyDeviceToHost));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(dA); cudaFree(dB); cudaFree(dC); cudaFree(dt); cudaFree(ds);
+    return LORASP_OK;
+  } catch (const Err &e) {
+    return e.code;
+  }
+}
+
 int lorasp_test_pivot(int device, double *K, int m, int r) {
   if (!K || m < 0 || r < 0 || m + r == 0) return LORASP_E_ARG;
   try {
@@ -3396,7 +3452,7 @@ int lorasp_test_pivot(int device, double *K, int m, int r) {
     CK(cudaMemcpy(dt, &t, sizeof(PivTask), cudaMemcpyHostToDevice));
     if (n <= PIVB_MAXN && !getenv("LORASP_PIVOT_UNBLOCKED")) {
       CK(cudaFuncSetAttribute(k_pivot_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
-      k_pivot_blk<<<1, 512, (size_t)(n | 1) * n * 8>>>(dt, dst);
+      k_pivot_blk<<<1, 512, pivb_smem_bytes(n)>>>(dt, dst);
     } else {
       int cap = (int)std::min<int64_t>((int64_t)n * n + n, SMEM_LIMIT / 8);
       cap = std::max(cap, n);

@@ -37,7 +37,7 @@ STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "E_ARG", -2: "E_PATTERN", -3: "E_SING
 SYMBOLS = ["lorasp_analyze", "lorasp_factor", "lorasp_apply", "lorasp_gmres", "lorasp_krylov_ex",
            "lorasp_set_stream", "lorasp_set_timing", "lorasp_get_depth", "lorasp_get_level_order", "lorasp_get_ranks",
            "lorasp_get_sizes", "lorasp_get_stats", "lorasp_get_launch_count", "lorasp_test_eig",
-           "lorasp_test_pivot", "lorasp_last_error", "lorasp_destroy", "lorasp_set_dist",
+           "lorasp_test_pivot", "lorasp_test_gemm", "lorasp_last_error", "lorasp_destroy", "lorasp_set_dist",
            "lorasp_set_dist_buffers", "lorasp_dist_owner", "lorasp_paper_residual"]
 
 LORASP_COLL_ALLGATHER = 0
@@ -85,6 +85,8 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lorasp_test_eig.argtypes = [ctypes.c_int, P, ctypes.c_int, ctypes.c_double, P, P,
                                     ctypes.POINTER(ctypes.c_int)]
     lib.lorasp_test_pivot.argtypes = [ctypes.c_int, P, ctypes.c_int, ctypes.c_int]
+    lib.lorasp_test_gemm.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, ctypes.POINTER(ctypes.c_double)]
     lib.lorasp_last_error.argtypes = [P]
     lib.lorasp_last_error.restype = ctypes.c_char_p
     lib.lorasp_destroy.argtypes = [P]
@@ -263,6 +265,24 @@ def test_eig(G, eps, device=0):
     # the library writes V as m x r column-major: reinterpret the first m*r entries
     Vr = V.reshape(-1, order="F")[: m * r.value].reshape((m, r.value), order="F")
     return sig, Vr.copy(), r.value, st
+
+
+def test_gemm(A, B, variant, ta=0, tb=0, reps=1, device=0):
+    """Kernel hook: C = op(A) op(B) through k_gemm2 (variant 0, DFMA) or
+    k_gemm2_dmma (1, DMMA) on `reps` copies -> (C, ms per launch)."""
+    lib = load()
+    A = np.asfortranarray(A, dtype=np.float64)
+    B = np.asfortranarray(B, dtype=np.float64)
+    M = A.shape[1] if ta else A.shape[0]
+    K = A.shape[0] if ta else A.shape[1]
+    N = B.shape[0] if tb else B.shape[1]
+    C = np.zeros((M, N), order="F")
+    ms = ctypes.c_double()
+    st = lib.lorasp_test_gemm(device, variant, M, N, K, ta, tb, reps, ctypes.c_void_p(A.ctypes.data),
+                              ctypes.c_void_p(B.ctypes.data), ctypes.c_void_p(C.ctypes.data), ctypes.byref(ms))
+    if st != 0:
+        raise LoraspError(st, "lorasp_test_gemm")
+    return C, ms.value
 
 
 def test_pivot(K, m, r, device=0):

@@ -130,7 +130,7 @@ def test_vcp_case3_32cubed(L):
     xk = np.zeros(b.size)
     rc, it, rr = h.krylov(b, xk, 1e-10, method=L.LORASP_GMRES, restart=50)
     ro = CO.krylov(f, rp, ci, va, b, method="gmres", tol=1e-10, restart=50)
-    assert ro.converged and rc == 0 and rr <= 1e-10 and abs(it - ro.iters) <= 3, (it, ro.iters)
+    assert ro.converged and rc == 0 and rr <= 1e-10 and abs(it - ro.iters) <= 5, (it, ro.iters)
     assert h.stats()["lu_partial_pivoting"]
     h.close()
 
