@@ -11,10 +11,11 @@ preconditioner).  `value` = factorization unknowns/s = n * (ranks) * K /
 sum of the factor times (max over ranks); the PCG time is reported beside it.
 
 Multi-GPU (torchrun, one process per GPU), --mode partition (default): the
-subtree partition of SURVEY 8(e) — rank g factors the nodes of its subtree and
-the ranks exchange per colour wave over NCCL (lorasp_set_dist; the Krylov
-solve then runs replicated); strong scaling: value = n * K / max-over-ranks
-factor time.  --mode replicas: every rank factors its own replica (weak
+subtree partition of SURVEY 8(e) — rank g factors the nodes of its subtree, the
+ranks exchange the blocks written in each colour wave through the library's own
+NCCL communicator (lorasp_set_dist_nccl), the factor records stay on their owner
+and the apply runs distributed (per-wave vector exchange; Krylov vectors
+replicated); strong scaling: value = n * K / max-over-ranks factor time.  --mode replicas: every rank factors its own replica (weak
 scaling, no data-path collective).  Barrier + max-over-ranks timing.
 
 --impl reference times the CPU oracle (oracle/cpp, C++17 plain loops, OpenMP
@@ -328,9 +329,12 @@ def main():
     t_analyze = time.perf_counter() - t_an0
     part = world > 1 and args.mode == "partition"
     if part:
-        from paper_1510_07363_b200.dist import TorchComm
-        comm = TorchComm(device=dev)
-        h.set_dist(rank, world, comm)
+        # library-owned NCCL communicator (include/lorasp.h lorasp_set_dist_nccl);
+        # the 128-byte unique id travels once over the process group
+        import torch.distributed as tdist
+        uid = [L.nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(uid, src=0)
+        h.set_dist_nccl(rank, world, uid[0])
     units = (lambda ms, steps: p.n * steps / (ms / 1e3)) if part else \
         (lambda ms, steps: weak_scaling_value(p.n, world, steps, ms))
     vals = torch.tensor(p.values, device=dev)
@@ -457,9 +461,12 @@ def main():
             "config": {"workload": f"{args.config}: {WORKLOADS.get(args.config, '')}", "n": p.n, "nnz": p.nnz,
                        "eps": p.eps, "depth": p.depth, "leaf": p.leaf, "compressor": args.compressor,
                        **({"R": args.adv_R, "sigma": 1.0} if args.config == "adv32" else {}),
-                       "parallelism": (f"subtree partition over {world} GPUs, per-wave NCCL exchange "
+                       "parallelism": (f"subtree partition over {world} GPUs, library-owned NCCL communicator: "
+                                       f"per-wave exchange of the written blocks "
                                        f"({stats.get('dist_exchange_calls')} collectives, "
-                                       f"{stats.get('dist_allgather_bytes')} B all-gathered per factorization)")
+                                       f"{stats.get('dist_allgather_bytes')} B per factorization; records stay "
+                                       f"local), distributed apply ({stats.get('dist_apply_bytes')} B of vector "
+                                       f"segments)")
                                       if part else ("replicas" if world > 1 else "single GPU"),
                        "l2": "flushed between timed steps (256 MiB write, untimed)",
                        "value_def": "n * ranks * steps / sum(factor time); PCG time reported as krylov_ms",

@@ -157,13 +157,21 @@ int lorasp_set_stream(lorasp_handle h, void *cuda_stream);
  *   world) when i - 1 >= log2 world (the subtree of level-(log2 world + 1)
  *   node g belongs to rank g), else rank 0 (the top levels).
  *   Every rank runs the same host schedule (identical plan, ranks and record
- *   layout) and launches only the tasks of the nodes it owns.  Two exchange
- *   points per colour wave go through `fn`:
+ *   layout) and launches only the tasks of the nodes it owns.  Exchange points
+ *   go through `fn`:
  *     after Compress, the ranks of the wave's nodes (and the status flags):
  *       LORASP_COLL_MAXINT — elementwise max over ranks of the first nbytes/4
  *       int32 of the send buffer, in place (non-owned entries are 0);
- *     after the Schur updates, every block and factor record the rank wrote
- *     (packed in a fixed order every rank can recompute):
+ *     after the Schur updates (neighbour push): every block a rank wrote goes
+ *       only to the ranks that read or update it later (the owners of the
+ *       nodes whose plan references it, and the readers of the next level's
+ *       block it is merged into); factor records never leave their owner:
+ *       LORASP_COLL_ALLTOALLV — rank q's send holds, back to back for p = 0..
+ *       world-1, counts[q][p] bytes for rank p; rank p's recv receives, back to
+ *       back for q = 0.., counts[q][p] bytes from rank q (lorasp_dist_counts
+ *       gives the world x world byte matrix, [q * world + p]);
+ *     in the distributed apply, after every colour wave, the vector segments
+ *       written there (tiny):
  *       LORASP_COLL_ALLGATHER — rank q's send[0, nbytes) lands in every rank's
  *       recv[q * nbytes, (q + 1) * nbytes).
  *   LORASP_COLL_RESERVE asks for send >= nbytes and recv >= world * nbytes
@@ -172,14 +180,38 @@ int lorasp_set_stream(lorasp_handle h, void *cuda_stream);
  *   stream before every call; the callback returns with the transfer complete
  *   (0 = OK, anything else aborts the factorization with LORASP_E_CUDA).
  *   Distance-2 colouring makes the blocks written in one wave disjoint across
- *   nodes, so every rank ends the factorization with the G = 1 store, bit for
- *   bit; lorasp_apply / lorasp_krylov_ex then run replicated on every rank.
- *   Rank-predicted replay and split pivots are off in this mode.
+ *   nodes, so every rank's blocks and its own records equal the G = 1 ones bit
+ *   for bit.  lorasp_apply / lorasp_krylov_ex are collective in this mode (every
+ *   rank calls them): each rank applies its own nodes (see lorasp_set_dist_nccl).
+ *   Rank-predicted replay and split pivots are off in this mode.  world <= 32.
  *   world = 1 (or fn = NULL) switches back to the single-GPU sweep.
  */
-typedef enum { LORASP_COLL_ALLGATHER = 0, LORASP_COLL_MAXINT = 1, LORASP_COLL_RESERVE = 2 } lorasp_coll_kind;
+typedef enum {
+  LORASP_COLL_ALLGATHER = 0, LORASP_COLL_MAXINT = 1, LORASP_COLL_RESERVE = 2, LORASP_COLL_ALLTOALLV = 3
+} lorasp_coll_kind;
 typedef int (*lorasp_coll_fn)(void *user, int kind, int64_t nbytes);
 int lorasp_set_dist(lorasp_handle h, int rank, int world, lorasp_coll_fn fn, void *user);
+/* byte matrix of the current LORASP_COLL_ALLTOALLV ([src * world + dst]); returns world^2 */
+int lorasp_dist_counts(lorasp_handle h, int64_t *counts, int cap);
+
+/*
+ * Library-owned communicator (SURVEY 8(b) `comm`): the same distributed mode
+ * with the per-wave collectives issued by the library itself through NCCL on
+ * its stream (ncclAllGather / ncclAllReduce(max) over library-owned device
+ * buffers), no callback.  lorasp_nccl_unique_id fills 128 bytes on one rank;
+ * the caller distributes them (any channel); every rank then calls
+ * lorasp_set_dist_nccl with its rank, the world size (a power of two) and the
+ * same id.  NCCL is resolved at run time (the libnccl.so.2 already loaded, else
+ * the system one); LORASP_E_NCCL when unavailable or on an NCCL error.
+ * In distributed mode the factor records stay on their owner and lorasp_apply /
+ * lorasp_krylov_ex run the apply distributed: each rank applies its own nodes,
+ * and after every colour wave the vector segments written there are exchanged
+ * (every rank must call them; the Krylov vectors are replicated).
+ */
+int lorasp_nccl_unique_id(void *id_out);
+int lorasp_set_dist_nccl(lorasp_handle h, int rank, int world, const void *unique_id);
+/* NCCL plumbing check on one device (1-rank communicator, all-gather + max-reduce of n ints). */
+int lorasp_test_nccl(int device, int n);
 /* Device buffers (owned by the caller) for the exchanges; capacity in bytes
  * (send_cap >= the reserve request, recv_cap >= world times it). */
 int lorasp_set_dist_buffers(lorasp_handle h, void *send, int64_t send_cap, void *recv, int64_t recv_cap);

@@ -31,7 +31,7 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp"] + SOURCES + ["-lcudart"]
+    cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp"] + SOURCES + ["-lcudart", "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

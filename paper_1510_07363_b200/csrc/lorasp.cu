@@ -22,12 +22,15 @@
 
 #include <algorithm>
 #include <atomic>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -421,6 +424,23 @@ struct lorasp_ctx {
   void *dist_send = nullptr, *dist_recv = nullptr;
   int64_t dist_send_cap = 0, dist_recv_cap = 0;
   int64_t dist_bytes = 0, dist_calls = 0;
+  int64_t dist_apply_bytes = 0, dist_apply_calls = 0;   // vector exchanges of the distributed apply
+  // distributed apply (records stay on their owner): per wave, the number of
+  // owned nodes (ordered first in the wave's ApNode range) and, per rank, the
+  // vector segments its nodes write: forward = the target RHS segments,
+  // backward = the nodes' own Var segments (offsets into d_vec, lengths)
+  std::vector<int> ap_wave_nown;
+  std::vector<std::vector<std::vector<std::pair<int64_t, int64_t>>>> ap_dirty_f, ap_dirty_b;
+  // library-owned NCCL communicator (lorasp_set_dist_nccl): the transport of the
+  // per-wave collectives instead of the caller's callback
+  ncclComm_t nccl = nullptr;
+  DevBuf nccl_send, nccl_recv;
+  // neighbour push: per level, per slot, the ranks that read or update it later
+  // (owners of the nodes whose plan references it, and -- through MergeRedNodes --
+  // every reader of the next level's slot it lands in); bytes moved per (src, dst)
+  // pair of the current all-to-all-v exchange
+  std::vector<std::vector<uint32_t>> slot_readers;
+  std::vector<int64_t> a2a_counts;   // world x world, bytes, [src * world + dst]
   int piv_maxn_hint = 0;   // batch-independent pivot path choice (max n of the whole wave)
   // recorded factorization: a verified rank-predicted sweep captured once as a
   // CUDA graph (descriptors resident in fg_desc) and replayed while the ranks,
@@ -1098,8 +1118,96 @@ int dist_owner_of(int level, int c, int l0) {
   return sh >= 0 ? (c >> sh) : 0;
 }
 
+// NCCL entry points, resolved at run time: the libnccl.so.2 already in the
+// process (e.g. torch's) when there is one, else the system's.  Link-time
+// binding would risk two different libnccl builds in one process.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+};
+static const NcclApi *nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (tried) return api.CommInitRank ? &api : nullptr;
+  tried = true;
+  void *lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) lib = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!lib) return nullptr;
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(lib, "ncclCommInitRank");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(lib, "ncclCommDestroy");
+  api.AllGather = (decltype(api.AllGather))dlsym(lib, "ncclAllGather");
+  api.AllReduce = (decltype(api.AllReduce))dlsym(lib, "ncclAllReduce");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(lib, "ncclGetErrorString");
+  api.Send = (decltype(api.Send))dlsym(lib, "ncclSend");
+  api.Recv = (decltype(api.Recv))dlsym(lib, "ncclRecv");
+  api.GroupStart = (decltype(api.GroupStart))dlsym(lib, "ncclGroupStart");
+  api.GroupEnd = (decltype(api.GroupEnd))dlsym(lib, "ncclGroupEnd");
+  if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllGather || !api.AllReduce || !api.Send ||
+      !api.Recv || !api.GroupStart || !api.GroupEnd) {
+    api.CommInitRank = nullptr;
+    return nullptr;
+  }
+  return &api;
+}
+#define NCK(x)                                                                                    \
+  do {                                                                                            \
+    ncclResult_t r_ = (x);                                                                        \
+    if (r_ != ncclSuccess)                                                                        \
+      throw Err(LORASP_E_NCCL, std::string("NCCL: ") +                                            \
+                                   (nccl_api() && nccl_api()->GetErrorString ? nccl_api()->GetErrorString(r_) \
+                                                                             : "error"));       \
+  } while (0)
+
 void dist_call(lorasp_ctx *h, int kind, int64_t nbytes) {
   ++h->dist_calls;
+  if (h->nccl) {   // library-owned communicator, on the library stream
+    const NcclApi *api = nccl_api();
+    if (kind == LORASP_COLL_RESERVE) {
+      h->nccl_send.ensure(nbytes, h->stream);
+      h->nccl_recv.ensure(nbytes * h->dist_world, h->stream);
+      h->dist_send = h->nccl_send.p;
+      h->dist_recv = h->nccl_recv.p;
+      h->dist_send_cap = (int64_t)h->nccl_send.cap;
+      h->dist_recv_cap = (int64_t)h->nccl_recv.cap;
+    } else if (kind == LORASP_COLL_ALLGATHER) {
+      NCK(api->AllGather(h->dist_send, h->dist_recv, (size_t)nbytes, ncclUint8, h->nccl, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    } else if (kind == LORASP_COLL_ALLTOALLV) {   // grouped point-to-point: only the neighbours' blocks
+      const int G = h->dist_world, me = h->dist_rank;
+      const int64_t *cn = h->a2a_counts.data();
+      int64_t so = 0, ro = 0;
+      NCK(api->GroupStart());
+      for (int p = 0; p < G; ++p) {
+        if (cn[me * G + p] > 0 && p != me)
+          NCK(api->Send(static_cast<char *>(h->dist_send) + so, (size_t)cn[me * G + p], ncclUint8, p, h->nccl,
+                        h->stream));
+        if (cn[p * G + me] > 0 && p != me)
+          NCK(api->Recv(static_cast<char *>(h->dist_recv) + ro, (size_t)cn[p * G + me], ncclUint8, p, h->nccl,
+                        h->stream));
+        so += cn[me * G + p];
+        ro += cn[p * G + me];
+      }
+      NCK(api->GroupEnd());
+      CK(cudaStreamSynchronize(h->stream));
+    } else {
+      NCK(api->AllReduce(h->dist_send, h->dist_send, (size_t)nbytes / 4, ncclInt32, ncclMax, h->nccl, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+    }
+    return;
+  }
   if (h->dist_fn(h->dist_user, kind, nbytes) != 0)
     throw Err(LORASP_E_CUDA, "distributed exchange callback failed (kind " + std::to_string(kind) + ")");
 }
@@ -1120,11 +1228,18 @@ void dist_allmax_ints(lorasp_ctx *h, const int *dev, size_t n, int *host_out) {
   if (n) CK(cudaMemcpyAsync(sb, dev, n * sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
   CK(cudaMemcpyAsync(sb + n, h->d_status.p, 2 * sizeof(int), cudaMemcpyDeviceToDevice, h->stream));
   CK(cudaStreamSynchronize(h->stream));
+  // status codes are negative: the max over ranks of -code keeps any failure
+  {
+    int stv[2];
+    CK(cudaMemcpy(stv, sb + n, 2 * sizeof(int), cudaMemcpyDeviceToHost));
+    stv[0] = -stv[0];
+    CK(cudaMemcpy(sb + n, stv, 2 * sizeof(int), cudaMemcpyHostToDevice));
+  }
   dist_call(h, LORASP_COLL_MAXINT, nbytes);
   std::vector<int> tmp(n + 2);
   CK(cudaMemcpy(tmp.data(), sb, nbytes, cudaMemcpyDeviceToHost));
   for (size_t q = 0; q < n; ++q) host_out[q] = tmp[q];
-  h->h_status[0] = tmp[n];
+  h->h_status[0] = -tmp[n];
   h->h_status[1] = tmp[n + 1];
 }
 
@@ -1195,6 +1310,88 @@ void dist_exchange(lorasp_ctx *h, const std::vector<DirtyList> &dirty) {
 
 
 
+// per level, per slot: bit mask of the ranks that reference the slot later (see
+// lorasp_ctx::slot_readers), from the top level down (a slot merged into the
+// next level inherits that slot's readers)
+void build_slot_readers(lorasp_ctx *h) {
+  const Plan &pl = h->plan;
+  h->slot_readers.assign(pl.depth + 1, {});
+  for (int i = 1; i <= pl.depth; ++i) {
+    const SymLevel &lv = pl.lev[i];
+    std::vector<uint32_t> &mk = h->slot_readers[i];
+    mk.assign(lv.slots.size(), 0u);
+    for (int c = 0; c < lv.K; ++c) {
+      const SymNode &nd = lv.node[c];
+      if (!nd.exists) continue;
+      const uint32_t bit = 1u << dist_owner_of(i, c, h->dist_l0);
+      auto add = [&](const std::vector<int> &v) {
+        for (int sl : v)
+          if (sl >= 0) mk[sl] |= bit;
+      };
+      if (nd.self_slot >= 0) mk[nd.self_slot] |= bit;
+      add(nd.n1_slot);
+      add(nd.n1_slot2);
+      add(nd.pslot_src);
+      add(nd.pslot_src2);
+      add(nd.pslot_dst);
+      add(nd.pslot_dst2);
+      add(nd.tslot);
+    }
+    if (i > 1)   // MergeRedNodes into level i-1 (lev[i-1].merge: sources are level-i slots)
+      for (const MergeSrc &ms : pl.lev[i - 1].merge) mk[ms.src_slot] |= h->slot_readers[i - 1][ms.dst_slot];
+  }
+}
+
+// end of a colour wave (neighbour push): block k written by rank q goes only to
+// the ranks in its reader mask; one all-to-all-v (grouped NCCL send / recv)
+void dist_push(lorasp_ctx *h, const std::vector<std::vector<std::pair<double *, int64_t>>> &wr,
+               const std::vector<uint32_t> &masks, const std::vector<int> &writer) {
+  const int G = h->dist_world, me = h->dist_rank;
+  // lists[q][p]: blocks q sends to p, in one order every rank derives
+  std::vector<std::vector<DirtyList>> lists(G, std::vector<DirtyList>(G));
+  for (size_t k = 0; k < wr.size(); ++k) {
+    const int q = writer[k];
+    for (int p = 0; p < G; ++p)
+      if (p != q && ((masks[k] >> p) & 1u))
+        for (auto &pr : wr[k]) lists[q][p].push_back(pr);
+  }
+  h->a2a_counts.assign((size_t)G * G, 0);
+  int64_t out = 0, in = 0;
+  for (int q = 0; q < G; ++q)
+    for (int p = 0; p < G; ++p) {
+      int64_t t = 0;
+      for (auto &pr : lists[q][p]) t += pr.second;
+      h->a2a_counts[(size_t)q * G + p] = 8 * t;
+      if (q == me) out += 8 * t;
+      if (p == me) in += 8 * t;
+    }
+  int64_t any = 0;
+  for (int64_t c : h->a2a_counts) any += c;
+  if (!any) return;
+  dist_reserve(h, std::max(out, in));
+  std::vector<CopyTask> ct;
+  double *send = static_cast<double *>(h->dist_send);
+  int64_t off = 0;
+  for (int p = 0; p < G; ++p)
+    for (auto &pr : lists[me][p]) {
+      contig_copies(ct, pr.first, send + off, pr.second);
+      off += pr.second;
+    }
+  launch_copy(h, ct, -1);
+  CK(cudaStreamSynchronize(h->stream));
+  dist_call(h, LORASP_COLL_ALLTOALLV, std::max(out, in));
+  h->dist_bytes += out;
+  ct.clear();
+  const double *recv = static_cast<const double *>(h->dist_recv);
+  off = 0;
+  for (int q = 0; q < G; ++q)
+    for (auto &pr : lists[q][me]) {
+      contig_copies(ct, recv + off, pr.first, pr.second);
+      off += pr.second;
+    }
+  launch_copy(h, ct, -1);
+}
+
 void copy_values(lorasp_ctx *h, const double *values) {
   const size_t nb = h->plan.nnz * sizeof(double);
   CK(cudaMemcpyAsync(h->d_values.p, values, nb, is_device_ptr(values) ? cudaMemcpyDeviceToDevice
@@ -1232,7 +1429,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
   cudaStream_t st = h->stream;
   const int L = pl.depth;
   const bool sym = (pl.flags & LORASP_SPD) != 0;
-  const bool dist = h->dist_world > 1 && h->dist_fn;
+  const bool dist = h->dist_world > 1 && (h->dist_fn || h->nccl);
   if (dist && replay) return false;
   h->dist_bytes = 0;
   h->dist_calls = 0;
@@ -1246,6 +1443,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
   // values -> device (a capture's caller copies them before the capture)
   if (!capture) copy_values(h, values);
   CK(cudaMemsetAsync(h->d_status.p, 0, 64, st));
+  if (dist && h->slot_readers.size() != (size_t)L + 1) build_slot_readers(h);
   if (pl.flags & LORASP_FROBENIUS) {
     h->d_frob.ensure(64, st);
     CK(cudaMemsetAsync(h->d_frob.p, 0, 8, st));
@@ -1691,7 +1889,10 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       }
       int max_n = 0, pv_max_small = 0, pv_max_all = 0;
       double f_proj = 0, b_proj = 0, f_piv = 0, b_piv = 0, f_z = 0, b_z = 0, f_s = 0, b_s = 0;
-      std::vector<DirtyList> dirty(dist ? h->dist_world : 0);
+      // neighbour push (dist): the blocks each node writes, their reader masks, the writer
+      std::vector<DirtyList> wr_blocks;
+      std::vector<uint32_t> wr_masks;
+      std::vector<int> wr_writer;
       for (size_t e = 0; e < elim.size(); ++e) {
         const int c = elim[e];
         const SymNode &nd = lv.node[c];
@@ -2143,12 +2344,16 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
             pv_max_all = std::max(pv_max_all, pn);
             if (pn <= PIV_SMALL_N) pv_max_small = std::max(pv_max_small, pn);
           }
-          DirtyList &dl = dirty[owner(c)];
-          dl.push_back({F, (int64_t)ldF * fcols});
+          // the record F stays on its owner (distributed apply); each written
+          // block goes to the ranks that read or update it later
           std::sort(wslots.begin(), wslots.end());
           wslots.erase(std::unique(wslots.begin(), wslots.end()), wslots.end());
           for (int sl : wslots)
-            if (slen[sl] > 0) dl.push_back({slot_ptr(sl), slen[sl]});
+            if (slen[sl] > 0) {
+              wr_blocks.push_back(DirtyList{{slot_ptr(sl), slen[sl]}});
+              wr_masks.push_back(h->slot_readers[i][sl]);
+              wr_writer.push_back(owner(c));
+            }
           if (!own(c)) {
             pt.resize(n_pt);
             ps.resize(n_ps);
@@ -2242,7 +2447,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       h->stg.flush(st);
       launch_gemm_dev(h, d_zt, d_zs, zt.size(), K_ZGEMM, f_z, b_z);
       launch_gemm_dev(h, d_stt, d_ss, stt.size(), K_SCHUR, f_s, b_s);
-      if (dist) dist_exchange(h, dirty);
+      if (dist) dist_push(h, wr_blocks, wr_masks, wr_writer);
       if (h->debug) {
         CK(cudaStreamSynchronize(st));
         CK(cudaMemcpy(h->h_status, h->d_status.p, 4 * sizeof(int), cudaMemcpyDeviceToHost));
@@ -2300,12 +2505,38 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
   h->d_y.ensure(std::max<int64_t>(ytot, 8) * 8, st);
   h->ap_wave_begin.clear();
   size_t fwd = 0, bwd = 0, max_col = 0;
+  // waves in recs order; distributed: a wave's owned nodes first (the apply
+  // launches only those), every rank's written vector segments recorded
+  std::vector<size_t> order;
+  {
+    std::vector<size_t> wb;
+    int pl_ = -1, pw_ = -1;
+    for (size_t q = 0; q < h->recs.size(); ++q) {
+      const int wv = pl.lev[h->recs[q].level].node[h->recs[q].c].wave;
+      if (h->recs[q].level != pl_ || wv != pw_) wb.push_back(q);
+      pl_ = h->recs[q].level;
+      pw_ = wv;
+    }
+    wb.push_back(h->recs.size());
+    h->ap_wave_nown.assign(wb.size() - 1, 0);
+    h->ap_dirty_f.assign(dist ? wb.size() - 1 : 0, std::vector<std::vector<std::pair<int64_t, int64_t>>>(h->dist_world));
+    h->ap_dirty_b.assign(dist ? wb.size() - 1 : 0, std::vector<std::vector<std::pair<int64_t, int64_t>>>(h->dist_world));
+    for (size_t w = 0; w + 1 < wb.size(); ++w) {
+      for (int pass = 0; pass < 2; ++pass)
+        for (size_t q = wb[w]; q < wb[w + 1]; ++q) {
+          const bool mine = !dist || dist_owner_of(h->recs[q].level, h->recs[q].c, h->dist_l0) == h->dist_rank;
+          if (mine == (pass == 0)) order.push_back(q);
+          if (mine && pass == 0) ++h->ap_wave_nown[w];
+        }
+    }
+  }
   int prev_level = -1, prev_wave = -1;
-  for (size_t q = 0; q < h->recs.size(); ++q) {
+  for (size_t qq = 0; qq < order.size(); ++qq) {
+    const size_t q = order[qq];
     const NodeRec &rc = h->recs[q];
     const SymLevel &lv = pl.lev[rc.level];
     int wv = lv.node[rc.c].wave;
-    if (rc.level != prev_level || wv != prev_wave) h->ap_wave_begin.push_back((int)q);
+    if (rc.level != prev_level || wv != prev_wave) h->ap_wave_begin.push_back((int)qq);
     prev_level = rc.level;
     prev_wave = wv;
     ApNode a{};
@@ -2334,6 +2565,12 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       if (sgm.w > 0) as.push_back(sgm);
     }
     a.nseg = (int)as.size() - a.seg0;
+    if (dist) {
+      const int wi = (int)h->ap_wave_begin.size() - 1;
+      const int g = dist_owner_of(rc.level, rc.c, h->dist_l0);
+      for (int k = a.seg0; k < a.seg0 + a.nseg; ++k) h->ap_dirty_f[wi][g].push_back({as[k].voff, (int64_t)as[k].w});
+      h->ap_dirty_b[wi][g].push_back({a.off_s, (int64_t)rc.m});
+    }
     an.push_back(a);
     int n = rc.m + rc.r;
     fwd = std::max(fwd, (size_t)(rc.m + n + rc.W + 2));   // rhs, y, Z^T D y
@@ -2351,7 +2588,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
     const int b0 = h->ap_wave_begin[w], b1 = h->ap_wave_begin[w + 1], cnt = b1 - b0;
     std::vector<int> ns(cnt, 1);
     bool split = false;
-    if (!h->no_split_apply && cnt <= 64) {
+    if (!h->no_split_apply && !dist && cnt <= 64) {
       double zmax = 0;
       for (int q = b0; q < b1; ++q) zmax = std::max(zmax, 8.0 * (an[q].m + an[q].r) * an[q].W);
       if (zmax >= 1024.0 * 1024) {   // a record of >= 1 MB would bound the wave's latency
@@ -2507,7 +2744,43 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
   const ApNode *nodes = h->d_apnodes.as<ApNode>();
   const ApSeg *segs = h->d_apsegs.as<ApSeg>();
   const int nw = (int)h->ap_wave_begin.size() - 1;
-  if (!h->no_graph && nw > 0) {
+  if (h->dist_world > 1) {
+    // distributed apply: each rank runs the nodes it owns (their
+    // records never left it); after every wave the vector segments written
+    // there travel to every rank (distance-2 colouring: one writer per segment
+    // per wave), so each rank enters the next wave with the full vector
+    double *vec = h->d_vec.as<double>();
+    auto exch = [&](const std::vector<std::vector<std::pair<int64_t, int64_t>>> &dl) {
+      std::vector<DirtyList> dirty(h->dist_world);
+      int64_t any = 0;
+      for (int g = 0; g < h->dist_world; ++g)
+        for (auto &pr : dl[g]) {
+          dirty[g].push_back({vec + pr.first, pr.second});
+          any += pr.second;
+        }
+      if (!any) return;
+      const int64_t b0 = h->dist_bytes, c0 = h->dist_calls;
+      dist_exchange(h, dirty);
+      h->dist_apply_bytes += h->dist_bytes - b0;
+      h->dist_apply_calls += h->dist_calls - c0;
+      h->dist_bytes = b0;
+      h->dist_calls = c0;
+    };
+    for (int w = 0; w < nw; ++w) {
+      const int b0 = h->ap_wave_begin[w], no = h->ap_wave_nown[w];
+      ev = tbeg(h, K_APPLY_FWD);
+      if (no > 0) launch_k(k_apply_fwd, no, 256, h->ap_wave_fsm[w], st, nodes + b0, segs, vec, h->ap_wave_ch[w]);
+      tend(h, ev, h->ap_wave_flops[w], h->ap_wave_bytes[w]);
+      exch(h->ap_dirty_f[w]);
+    }
+    for (int w = nw - 1; w >= 0; --w) {
+      const int b0 = h->ap_wave_begin[w], no = h->ap_wave_nown[w];
+      ev = tbeg(h, K_APPLY_BWD);
+      if (no > 0) launch_k(k_apply_bwd, no, 256, h->ap_wave_bsm[w], st, nodes + b0, segs, vec, h->ap_wave_ch[w]);
+      tend(h, ev, h->ap_wave_flops[w], h->ap_wave_bytes[w]);
+      exch(h->ap_dirty_b[w]);
+    }
+  } else if (!h->no_graph && nw > 0) {
     // Alg. 3 / Alg. 4 wave launches as one CUDA graph (per-class timing, when
     // requested for the apply classes, uses the launch-by-launch path below)
     // the graph stays valid across re-factorizations as long as every launch
@@ -3094,7 +3367,7 @@ int lorasp_set_stream(lorasp_handle h, void *s) {
 
 int lorasp_set_dist(lorasp_handle h, int rank, int world, lorasp_coll_fn fn, void *user) {
   if (!h) return LORASP_E_ARG;
-  if (world < 1 || (world & (world - 1)) != 0 || rank < 0 || rank >= world) return LORASP_E_ARG;
+  if (world < 1 || world > 32 || (world & (world - 1)) != 0 || rank < 0 || rank >= world) return LORASP_E_ARG;
   int l0 = 0;
   while ((1 << l0) < world) ++l0;
   if (world > 1 && (!fn || h->plan.depth - 1 < l0)) return LORASP_E_ARG;
@@ -3104,7 +3377,94 @@ int lorasp_set_dist(lorasp_handle h, int rank, int world, lorasp_coll_fn fn, voi
   h->dist_fn = world > 1 ? fn : nullptr;
   h->dist_user = user;
   h->cache_valid = false;
+  h->slot_readers.clear();
+  if (h->nccl) {
+    if (const NcclApi *api = nccl_api()) api->CommDestroy(h->nccl);
+    h->nccl = nullptr;
+  }
   return LORASP_OK;
+}
+
+int lorasp_nccl_unique_id(void *id_out) {
+  if (!id_out) return LORASP_E_ARG;
+  const NcclApi *api = nccl_api();
+  if (!api) return LORASP_E_NCCL;
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != ncclSuccess) return LORASP_E_NCCL;
+  std::memcpy(id_out, &id, sizeof(id));
+  return LORASP_OK;
+}
+
+int lorasp_set_dist_nccl(lorasp_handle h, int rank, int world, const void *unique_id) {
+  return guarded(h, [&]() {
+    if (world < 1 || world > 32 || (world & (world - 1)) != 0 || rank < 0 || rank >= world || !unique_id)
+      return (int)LORASP_E_ARG;
+    int l0 = 0;
+    while ((1 << l0) < world) ++l0;
+    if (world > 1 && h->plan.depth - 1 < l0) return (int)LORASP_E_ARG;
+    const NcclApi *api = nccl_api();
+    if (!api) return (int)LORASP_E_NCCL;
+    CK(cudaSetDevice(h->device));
+    if (h->nccl) {
+      api->CommDestroy(h->nccl);
+      h->nccl = nullptr;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    NCK(api->CommInitRank(&comm, world, id, rank));
+    h->nccl = comm;
+    h->dist_rank = world > 1 ? rank : 0;
+    h->dist_world = world;
+    h->dist_l0 = l0;
+    h->dist_fn = nullptr;
+    h->dist_user = nullptr;
+    h->dist_send = h->dist_recv = nullptr;
+    h->dist_send_cap = h->dist_recv_cap = 0;
+    h->cache_valid = false;
+    h->slot_readers.clear();
+    return (int)LORASP_OK;
+  });
+}
+
+// NCCL plumbing check on one device: a 1-rank communicator from a fresh unique
+// id, all-gather and int32 max-reduce of `n` values through the library's
+// transport calls; returns LORASP_OK when the results are the inputs.
+int lorasp_test_nccl(int device, int n) {
+  try {
+    const NcclApi *api = nccl_api();
+    if (!api || n <= 0) return LORASP_E_NCCL;
+    CK(cudaSetDevice(device));
+    ncclUniqueId id;
+    NCK(api->GetUniqueId(&id));
+    ncclComm_t comm;
+    NCK(api->CommInitRank(&comm, 1, id, 0));
+    int *d;
+    CK(cudaMalloc(&d, 3 * (size_t)n * sizeof(int)));
+    std::vector<int> hv(n);
+    for (int i = 0; i < n; ++i) hv[i] = 3 * i - 7;
+    CK(cudaMemcpy(d, hv.data(), n * sizeof(int), cudaMemcpyHostToDevice));
+    NCK(api->AllGather(d, d + n, (size_t)n * sizeof(int), ncclUint8, comm, 0));
+    NCK(api->AllReduce(d, d + 2 * n, (size_t)n, ncclInt32, ncclMax, comm, 0));
+    CK(cudaDeviceSynchronize());
+    std::vector<int> out(3 * (size_t)n);
+    CK(cudaMemcpy(out.data(), d, 3 * (size_t)n * sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    api->CommDestroy(comm);
+    for (int i = 0; i < n; ++i)
+      if (out[n + i] != hv[i] || out[2 * n + i] != hv[i]) return LORASP_E_NCCL;
+    return LORASP_OK;
+  } catch (const Err &e) {
+    return e.code;
+  }
+}
+
+int lorasp_dist_counts(lorasp_handle h, int64_t *counts, int cap) {
+  if (!h || !counts) return LORASP_E_ARG;
+  const int n = (int)h->a2a_counts.size();
+  if (cap < n) return LORASP_E_ARG;
+  std::copy(h->a2a_counts.begin(), h->a2a_counts.end(), counts);
+  return n;
 }
 
 int lorasp_set_dist_buffers(lorasp_handle h, void *send, int64_t send_cap, void *recv, int64_t recv_cap) {
@@ -3186,7 +3546,9 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
       << ",\"factor_graph_captures\":" << h->fg_captures << ",\"factor_graph_launches\":" << h->fg_launches
       << ",\"factor_graph_failures\":" << h->fg_failures << ",\"dist_world\":" << h->dist_world
       << ",\"dist_rank\":" << h->dist_rank << ",\"dist_exchange_calls\":" << h->dist_calls
-      << ",\"dist_allgather_bytes\":" << h->dist_bytes
+      << ",\"dist_allgather_bytes\":" << h->dist_bytes << ",\"dist_apply_bytes\":" << h->dist_apply_bytes
+      << ",\"dist_apply_calls\":" << h->dist_apply_calls << ",\"dist_transport\":\""
+      << (h->nccl ? "nccl" : (h->dist_world > 1 ? "callback" : "none")) << "\""
       << ",\"lu_partial_pivoting\":" << (h->lu_pivot ? "true" : "false")
       << ",\"lu_pivot_switches\":" << h->lu_pivot_switches << ",\"spd_fallbacks\":" << h->spd_fallbacks
       << ",\"path\":\"" << ((pl.flags & LORASP_SPD) ? "spd" : "lu") << "\"";
@@ -3489,6 +3851,12 @@ void lorasp_destroy(lorasp_handle h) {
     for (DevBuf *b : bufs) b->release();
     for (cudaEvent_t e : h->evpool) cudaEventDestroy(e);
     if (h->ap_graph) cudaGraphExecDestroy(h->ap_graph);
+    if (h->nccl) {
+      if (const NcclApi *api = nccl_api()) api->CommDestroy(h->nccl);
+      h->nccl = nullptr;
+    }
+    h->nccl_send.release();
+    h->nccl_recv.release();
     if (h->fgraph) cudaGraphExecDestroy(h->fgraph);
     h->fg_desc.release();
     if (h->stream2) {

@@ -2,9 +2,12 @@
 lorasp_set_dist; subtree per GPU, per-wave exchange).
 
 The engine packs what a rank wrote during a colour wave into a device send
-buffer and asks for two collectives: an all-gather of those buffers and an
-elementwise int32 max (the ranks of the wave's nodes).  These classes provide
-them over
+buffer and asks for three collectives: an all-to-all-v of the written blocks
+(each block only to the ranks that read it later: the neighbour push), an
+elementwise int32 max (the ranks of the wave's nodes), and, in the distributed
+apply, an all-gather of the vector segments written in a wave.  (Production
+multi-GPU runs use the library's own NCCL communicator instead, see
+Handle.set_dist_nccl.)  These classes provide them over
 
   * `TorchComm`   — torch.distributed (NCCL between GPUs; one process per GPU);
   * `VirtualGroup` — G virtual ranks as G threads of one process on one GPU,
@@ -57,6 +60,16 @@ class TorchComm:
         if self.device.type == "cuda":
             torch.cuda.synchronize(self.device)
 
+    def alltoallv(self, counts):
+        """counts[q][p] bytes from rank q to rank p (send / recv back to back)."""
+        me = self.rank
+        ins = [int(counts[me][p]) for p in range(self.world)]
+        outs = [int(counts[q][me]) for q in range(self.world)]
+        dist.all_to_all_single(self.recv[: sum(outs)], self.send[: sum(ins)], output_split_sizes=outs,
+                               input_split_sizes=ins, group=self.group)
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
+
 
 class VirtualGroup:
     """G virtual ranks in one process (threads), buffers on one device."""
@@ -90,6 +103,20 @@ class VirtualComm:
         self._sync()
         g.barrier.wait()                       # nobody overwrites a send buffer early
 
+    def alltoallv(self, counts):
+        g = self.g
+        me = self.rank
+        g.barrier.wait()                       # every rank's send buffer is complete
+        ro = 0
+        for q, peer in enumerate(g.members):
+            so = int(sum(counts[q][:me]))
+            k = int(counts[q][me])
+            if k:
+                self.recv[ro:ro + k].copy_(peer.send[so:so + k])
+            ro += k
+        self._sync()
+        g.barrier.wait()                       # nobody overwrites a send buffer early
+
     def allmax_int(self, nbytes):
         g = self.g
         g.barrier.wait()
@@ -98,6 +125,34 @@ class VirtualComm:
         g.barrier.wait()                       # all reads done before the in-place write
         self.send[:nbytes].view(torch.int32).copy_(acc)
         self._sync()
+
+
+def run_virtual(handles, fn):
+    """Run fn(rank, handle) on every virtual rank concurrently (the distributed
+    factor / apply / Krylov calls each rendezvous at every exchange); returns
+    (results, exceptions) per rank."""
+    errs = [None] * len(handles)
+    res = [None] * len(handles)
+    barrier = None
+    for h in handles:
+        comm = getattr(h, "_vcomm", None)
+        if comm is not None:
+            barrier = comm.g.barrier
+
+    def run(r):
+        try:
+            res[r] = fn(r, handles[r])
+        except BaseException as e:  # noqa: BLE001 - reported to the caller
+            errs[r] = e
+            if barrier is not None:
+                barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(len(handles))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    return res, errs
 
 
 def factor_virtual(handles, values, group: VirtualGroup):
@@ -114,6 +169,7 @@ def factor_virtual(handles, values, group: VirtualGroup):
 
     for r, h in enumerate(handles):
         h.set_dist(r, group.world, group.members[r])
+        h._vcomm = group.members[r]
     th = [threading.Thread(target=run, args=(r,)) for r in range(len(handles))]
     for t in th:
         t.start()

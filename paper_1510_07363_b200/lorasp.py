@@ -38,11 +38,13 @@ SYMBOLS = ["lorasp_analyze", "lorasp_factor", "lorasp_apply", "lorasp_gmres", "l
            "lorasp_set_stream", "lorasp_set_timing", "lorasp_get_depth", "lorasp_get_level_order", "lorasp_get_ranks",
            "lorasp_get_sizes", "lorasp_get_stats", "lorasp_get_launch_count", "lorasp_test_eig",
            "lorasp_test_pivot", "lorasp_test_gemm", "lorasp_last_error", "lorasp_destroy", "lorasp_set_dist",
-           "lorasp_set_dist_buffers", "lorasp_dist_owner", "lorasp_paper_residual"]
+           "lorasp_set_dist_buffers", "lorasp_dist_owner", "lorasp_paper_residual", "lorasp_nccl_unique_id",
+           "lorasp_set_dist_nccl", "lorasp_test_nccl", "lorasp_dist_counts"]
 
 LORASP_COLL_ALLGATHER = 0
 LORASP_COLL_MAXINT = 1
 LORASP_COLL_RESERVE = 2
+LORASP_COLL_ALLTOALLV = 3
 # int (*lorasp_coll_fn)(void *user, int kind, int64_t nbytes)
 COLL_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64)
 
@@ -94,6 +96,10 @@ def load(path: Optional[str] = None) -> ctypes.CDLL:
     lib.lorasp_set_dist.argtypes = [P, ctypes.c_int, ctypes.c_int, COLL_FN, P]
     lib.lorasp_set_dist_buffers.argtypes = [P, P, ctypes.c_int64, P, ctypes.c_int64]
     lib.lorasp_dist_owner.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    lib.lorasp_nccl_unique_id.argtypes = [P]
+    lib.lorasp_set_dist_nccl.argtypes = [P, ctypes.c_int, ctypes.c_int, P]
+    lib.lorasp_test_nccl.argtypes = [ctypes.c_int, ctypes.c_int]
+    lib.lorasp_dist_counts.argtypes = [P, P, ctypes.c_int]
     for s in SYMBOLS:
         if s not in ("lorasp_last_error", "lorasp_destroy"):
             getattr(lib, s).restype = ctypes.c_int
@@ -188,6 +194,10 @@ class Handle:
                     comm.allgather(int(nbytes))
                 elif kind == LORASP_COLL_MAXINT:
                     comm.allmax_int(int(nbytes))
+                elif kind == LORASP_COLL_ALLTOALLV:
+                    cnt = np.zeros(world * world, dtype=np.int64)
+                    lib.lorasp_dist_counts(self.h, ctypes.c_void_p(cnt.ctypes.data), cnt.size)
+                    comm.alltoallv(cnt.reshape(world, world))
                 else:
                     return 1
                 return 0
@@ -198,6 +208,11 @@ class Handle:
 
         self._coll = COLL_FN(cb)   # the handle keeps the callback alive
         return self._check(lib.lorasp_set_dist(self.h, int(rank), int(world), self._coll, None), "set_dist")
+
+    def set_dist_nccl(self, rank, world, unique_id: bytes):
+        """Distributed mode over a library-owned NCCL communicator (include/lorasp.h)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        return self._check(self._lib.lorasp_set_dist_nccl(self.h, int(rank), int(world), buf), "set_dist_nccl")
 
     def set_timing(self, mask):
         """mask: True = all kernel classes, False = off, or an int bitmask of classes."""
@@ -245,6 +260,20 @@ class Handle:
             self.close()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for lorasp_set_dist_nccl (call on one rank, share it)."""
+    buf = ctypes.create_string_buffer(128)
+    rc = load().lorasp_nccl_unique_id(buf)
+    if rc != LORASP_OK:
+        raise LoraspError(rc, "lorasp_nccl_unique_id")
+    return buf.raw
+
+
+def test_nccl(n=1000, device=0):
+    """NCCL plumbing hook (1-rank communicator): status code."""
+    return load().lorasp_test_nccl(int(device), int(n))
 
 
 def dist_owner(level, c, world):

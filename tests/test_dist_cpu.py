@@ -68,7 +68,16 @@ def _worker(rank, world, port, out):
     iv.copy_(torch.tensor([rank, 0, 5 - rank, -1], dtype=torch.int32))
     c.allmax_int(16)
     mx = send[:16].view(torch.int32).clone().numpy()
-    out.put((rank, got, mx))
+    # all-to-all-v (neighbour push): rank q sends (q + 1) * (p + 1) bytes valued
+    # 10 q + p to rank p
+    counts = np.array([[(q + 1) * (p + 1) for p in range(world)] for q in range(world)])
+    c.reserve(64)
+    chunks = [torch.full(((rank + 1) * (p + 1),), 10 * rank + p, dtype=torch.uint8) for p in range(world)]
+    flat = torch.cat(chunks)
+    c.send[:flat.numel()] = flat
+    c.alltoallv(counts)
+    a2a = c.recv[:int(counts[:, rank].sum())].clone().numpy()
+    out.put((rank, got, mx, a2a))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -86,9 +95,11 @@ def test_torch_comm_gloo_world2():
         p.join(timeout=120)
         assert p.exitcode == 0
     want = np.concatenate([np.arange(24, dtype=np.uint8) + 100 * r for r in range(world)])
-    for r, got, mx in res:
+    for r, got, mx, a2a in res:
         assert np.array_equal(got, want)
         assert list(mx) == [1, 0, 5, -1]
+        exp = np.concatenate([np.full((q + 1) * (r + 1), 10 * q + r, dtype=np.uint8) for q in range(world)])
+        assert np.array_equal(a2a, exp)
 
 
 def test_virtual_group_semantics():
@@ -105,7 +116,13 @@ def test_virtual_group_semantics():
         iv = send[:8].view(torch.int32)
         iv.copy_(torch.tensor([r, 3 * (r % 2)], dtype=torch.int32))
         c.allmax_int(8)
-        out[r] = (c.recv[:world * 8].clone(), send[:8].view(torch.int32).clone())
+        res = (c.recv[:world * 8].clone(), send[:8].view(torch.int32).clone())
+        counts = np.array([[q + 2 * p for p in range(world)] for q in range(world)])
+        flat = torch.cat([torch.full((q,), 0, dtype=torch.uint8) for q in []] +
+                         [torch.full((int(counts[r][p]),), 16 * r + p, dtype=torch.uint8) for p in range(world)])
+        c.send[:flat.numel()] = flat
+        c.alltoallv(counts)
+        out[r] = res + (c.recv[:int(counts[:, r].sum())].clone(), counts)
 
     th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
     for t in th:
@@ -116,3 +133,6 @@ def test_virtual_group_semantics():
     for r in range(world):
         assert torch.equal(out[r][0], want)
         assert out[r][1].tolist() == [world - 1, 3]
+        counts = out[r][3]
+        exp = torch.cat([torch.full((int(counts[q][r]),), 16 * q + r, dtype=torch.uint8) for q in range(world)])
+        assert torch.equal(out[r][2], exp)

@@ -1,13 +1,16 @@
-"""GPU: the distributed factorization (include/lorasp.h lorasp_set_dist,
+"""GPU: the distributed factorization and apply (include/lorasp.h lorasp_set_dist,
 SURVEY 8(e)) emulated with G virtual ranks on the one GPU (threads, one
 handle and store each; exchanges are host rendezvous + device copies, no
 kernel ever waits on another).
 
 Every rank computes only the nodes of its subtree (owner = c >> (i-1-log2 G),
-top levels on rank 0) and receives the rest through the per-wave exchanges, so
-each rank must end with exactly the single-GPU factorization: identical ranks
-at every level, and Ã b equal bit for bit (distance-2 colouring makes the
-blocks written in a wave disjoint, so no sum is reordered)."""
+top levels on rank 0) and receives through the per-wave exchanges only the
+blocks the sweep writes -- its factor records never leave it.  The apply runs
+distributed: each rank applies its own nodes and the vector segments written
+in a colour wave are exchanged after it.  So every rank must reproduce the
+single-GPU result exactly: identical ranks at every level, Ã b equal bit for bit
+(distance-2 colouring makes the regions written in a wave disjoint, so no sum
+is reordered), the same Krylov iterations and solution."""
 import numpy as np
 import pytest
 
@@ -28,7 +31,14 @@ def L():
 
 
 def _single(L, p):
-    h = L.analyze_problem(p)
+    # the distributed apply runs the fused one-CTA-per-node apply kernels; the
+    # single-GPU reference does the same (no split apply) so that x is bitwise comparable
+    import os
+    os.environ["LORASP_NO_SPLIT_APPLY"] = "1"
+    try:
+        h = L.analyze_problem(p)
+    finally:
+        del os.environ["LORASP_NO_SPLIT_APPLY"]
     h.factor(p.values)
     x = np.zeros(p.n)
     h.apply(p.b, x)
@@ -45,7 +55,7 @@ def _single(L, p):
     ("cfg2", (512, 512), 2),    # waves wider than the GPU (launch shapes of the whole wave)
 ])
 def test_virtual_ranks_match_single_gpu(L, name, dims, world):
-    from paper_1510_07363_b200.dist import VirtualGroup, factor_virtual
+    from paper_1510_07363_b200.dist import VirtualGroup, factor_virtual, run_virtual
     p = make_problem(name, dims=dims)
     h1, x1, r1 = _single(L, p)
     if name == "cfg3":
@@ -54,24 +64,63 @@ def test_virtual_ranks_match_single_gpu(L, name, dims, world):
     hs = [L.analyze_problem(p) for _ in range(world)]
     errs = factor_virtual(hs, p.values, group)
     assert errs == [None] * world, errs
+    fbytes = h1.stats()["factor_bytes"]
+
+    def apply(r, h):
+        x = np.zeros(p.n)
+        h.apply(p.b, x)
+        return x
+
+    xs, errs = run_virtual(hs, apply)
+    assert errs == [None] * world, errs
     for r, h in enumerate(hs):
         st = h.stats()
         assert st["dist_world"] == world and st["dist_rank"] == r
         assert st["dist_exchange_calls"] > 0 and st["dist_allgather_bytes"] > 0
+        # records stay local and each written block goes only to its readers
+        # (neighbour push): a rank sends less than the single-GPU factor bytes
+        assert st["dist_allgather_bytes"] < fbytes, (st["dist_allgather_bytes"], fbytes)
+        assert st["dist_apply_calls"] > 0
         for i in range(1, h.depth + 1):
             assert np.array_equal(h.ranks(i), r1[i - 1]), (r, i)
-        x = np.zeros(p.n)
-        h.apply(p.b, x)
-        assert np.array_equal(x, x1), (r, float(np.max(np.abs(x - x1))))
-    # the Krylov solve runs replicated on a rank's store: same iterations
-    xk = np.zeros(p.n)
-    rc, it, rr = hs[-1].krylov(p.b, xk, 1e-10, method=L.LORASP_CG if p.symmetric else L.LORASP_GMRES)
+        assert np.array_equal(xs[r], x1), (r, float(np.max(np.abs(xs[r] - x1))))
+    # Krylov with the distributed apply (vectors replicated): same iterations, same x
+    meth = L.LORASP_CG if p.symmetric else L.LORASP_GMRES
+
+    def kry(r, h):
+        xk = np.zeros(p.n)
+        rc, it, rr = h.krylov(p.b, xk, 1e-10, method=meth)
+        return rc, it, xk
+
+    out, errs = run_virtual(hs, kry)
+    assert errs == [None] * world, errs
     x1k = np.zeros(p.n)
-    rc1, it1, rr1 = h1.krylov(p.b, x1k, 1e-10, method=L.LORASP_CG if p.symmetric else L.LORASP_GMRES)
-    assert rc == rc1 == 0 and it == it1 and np.array_equal(xk, x1k)
-    # back to single-GPU mode on the same handle
+    rc1, it1, rr1 = h1.krylov(p.b, x1k, 1e-10, method=meth)
+    for rc, it, xk in out:
+        assert rc == rc1 == 0 and it == it1 and np.array_equal(xk, x1k)
+    # back to single-GPU mode on the same handle (default apply kernels)
+    hd = L.analyze_problem(p)
+    hd.factor(p.values)
+    xd = np.zeros(p.n)
+    hd.apply(p.b, xd)
     hs[0].set_dist(0, 1)
     hs[0].factor(p.values)
     x = np.zeros(p.n)
     hs[0].apply(p.b, x)
+    assert np.array_equal(x, xd)
+
+
+def test_nccl_transport_plumbing(L):
+    """The library-owned NCCL transport: run-time resolved libnccl, a 1-rank
+    communicator, all-gather and int32 max-reduce through the same calls the
+    distributed sweep issues; and a handle in NCCL mode with world 1."""
+    assert L.test_nccl(4096) == L.LORASP_OK
+    p = make_problem("cfg1")
+    h = L.analyze_problem(p)
+    h.set_dist_nccl(0, 1, L.nccl_unique_id())
+    h.factor(p.values)
+    x = np.zeros(p.n)
+    h.apply(p.b, x)
+    assert h.stats()["dist_transport"] == "nccl"
+    h1, x1, _ = _single(L, p)
     assert np.array_equal(x, x1)
