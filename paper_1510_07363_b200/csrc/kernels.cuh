@@ -363,6 +363,18 @@ __device__ __forceinline__ double frcp(double x) {
   return fma(r, e, r);
 }
 
+// 1 / sqrt(x) for x > 0: MUFU.RSQ64H approximation + two Newton steps
+// (y <- y (3 - x y^2) / 2); replaces the IEEE sqrt + reciprocal pair on the
+// pivot kernels' dependent chain (one per column)
+__device__ __forceinline__ double frsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -564,6 +576,181 @@ __device__ __forceinline__ void invit_one(const double *__restrict__ d, const do
   }
 #pragma unroll 4
   for (int i = 0; i < m; ++i) z[i] = b[i * S] * nrm;
+}
+
+// ------------------------------------------- one-warp eigen-solver (m <= 32) ----
+// The upper levels' stacks are small (m <= 32 on the 2D configs); the block-wide
+// tridiagonalisation + k_eig_t pair then spends its time in barriers and
+// sequential phases sized for 512 threads.  This kernel runs the same algorithm
+// (Householder tridiagonalisation, Sturm bisection, inverse iteration, MGS,
+// back-transformation) in one warp per node with warp barriers only:
+//   lane = row in the tridiagonalisation (G in shared memory), lane = eigenvalue
+//   in the bisection, lane = vector in inverse iteration / MGS / back-transform.
+// Rank by Eq. cutOff1 (or the Frobenius rule, as eig_values_phase); eps = 0
+// keeps V = I, r = m (reading Z3); G = 0 gives r = 0 (Z4).
+constexpr int EIGW_M = 32;
+constexpr int EIGW_LD = EIGW_M + 1;
+constexpr int EIGW_SMEM_DOUBLES =
+    EIGW_M * EIGW_LD            /* G, then Householder vectors below the subdiagonal */
+    + 5 * 40                    /* d, e, e2 (scaled, padded to 40), tau, lam */
+    + 2 * EIGW_M                /* v, w of the current step */
+    + 5 * EIGW_M * EIGW_M       /* inverse-iteration LU (interleaved, stride 32) */
+    + EIGW_M * EIGW_LD          /* Z: vector k at Z[k * EIGW_LD] */
+    + EIGW_M * EIGW_M / 8 + 8;  /* pivot bytes */
+__global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tasks, double eps, int *status) {
+  extern __shared__ double sh[];
+  pdl_trigger();
+  const EigTask t = tasks[blockIdx.x];
+  pdl_wait();
+  const int m = t.m, lane = threadIdx.x;
+  double *G = sh, *d = G + EIGW_M * EIGW_LD, *e = d + 40, *e2 = e + 40, *tau = e2 + 40, *lam = tau + 40;
+  double *vs = lam + 40, *ws = vs + EIGW_M, *LU = ws + EIGW_M, *Z = LU + 5 * EIGW_M * EIGW_M;
+  unsigned char *pv = reinterpret_cast<unsigned char *>(Z + EIGW_M * EIGW_LD);
+  if (m <= 0) {
+    if (lane == 0) *t.rank_out = 0;
+    return;
+  }
+  {
+    double fro = 0.0;
+    for (int q = lane; q < m * m; q += 32) fro = fma(t.G[q], t.G[q], fro);
+    fro = warp_sum(fro);
+    if (!(fro > 0.0) || eps == 0.0) {   // G = 0: r = 0 (Z4); eps = 0: V = I, r = m (Z3)
+      const bool keep = fro > 0.0;
+      if (keep)
+        for (int k = 0; k < m; ++k)
+          if (lane < m) t.V[lane + (int64_t)k * m] = (lane == k) ? 1.0 : 0.0;
+      if (lane < m) t.sig[lane] = 0.0;
+      if (lane == 0) *t.rank_out = keep ? m : 0;
+      return;
+    }
+  }
+  for (int j = 0; j < m; ++j)
+    if (lane < m) G[lane + j * EIGW_LD] = t.G[lane + (int64_t)j * m];
+  double trace = 0.0;
+  for (int i = 0; i < m; ++i) trace += t.G[i + (int64_t)i * m];
+  __syncwarp();
+  // ---- 1. Householder tridiagonalisation (lower, dsytd2), lane = row ----
+  for (int k = 0; k + 2 < m; ++k) {
+    const double x = (lane > k && lane < m) ? G[lane + k * EIGW_LD] : 0.0;
+    const double alpha = G[(k + 1) + k * EIGW_LD];
+    double s2 = (lane > k + 1 && lane < m) ? x * x : 0.0;
+    s2 = warp_sum(s2);
+    double tk = 0.0, beta = alpha;
+    if (s2 > 0.0) {
+      beta = -copysign(sqrt(alpha * alpha + s2), alpha);
+      tk = (beta - alpha) / beta;
+      const double sc = 1.0 / (alpha - beta);
+      const double v = (lane == k + 1) ? 1.0 : ((lane > k + 1 && lane < m) ? x * sc : 0.0);
+      vs[lane] = v;
+      __syncwarp();
+      // p = tau A v on rows / cols > k
+      double p = 0.0;
+      if (lane > k && lane < m)
+        for (int j = k + 1; j < m; ++j) p = fma(G[lane + j * EIGW_LD], vs[j], p);
+      p *= tk;
+      const double a2 = -0.5 * tk * warp_sum(p * v);
+      const double w = fma(a2, v, p);
+      ws[lane] = w;
+      __syncwarp();
+      if (lane > k && lane < m)
+        for (int j = k + 1; j < m; ++j)
+          G[lane + j * EIGW_LD] = fma(-v, ws[j], fma(-w, vs[j], G[lane + j * EIGW_LD]));
+      __syncwarp();
+      if (lane > k + 1 && lane < m) G[lane + k * EIGW_LD] = v;   // Householder vector below the subdiagonal
+    }
+    if (lane == 0) {
+      tau[k] = tk;
+      e[k] = beta;
+    }
+    __syncwarp();
+  }
+  if (lane < m) d[lane] = G[lane + lane * EIGW_LD];
+  if (lane == 0 && m >= 2) e[m - 2] = G[(m - 1) + (m - 2) * EIGW_LD];
+  __syncwarp();
+  // ---- 2. eigenvalues: lane l bisects the l-th largest (Sturm counts, T / bnorm) ----
+  double gl = 1e300, gu = -1e300;
+  for (int i = 0; i < m; ++i) {
+    const double off = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < m - 1 ? fabs(e[i]) : 0.0);
+    gl = fmin(gl, d[i] - off);
+    gu = fmax(gu, d[i] + off);
+  }
+  const double bnorm = fmax(fmax(fabs(gl), fabs(gu)), 1e-300);
+  const double isc = 1.0 / bnorm;
+  __syncwarp();
+  double *ds = LU, *e2s = LU + 40;   // scaled copies (padded: d = 4, e2 = 0 beyond m)
+  for (int i = lane; i < 40; i += 32) {
+    ds[i] = (i < m) ? d[i] * isc : 4.0;
+    e2s[i] = (i < m - 1) ? (e[i] * isc) * (e[i] * isc) : 0.0;
+  }
+  __syncwarp();
+  double lo = gl * isc - 4.4e-16 * m - 1e-300, hi = gu * isc + 4.4e-16 * m + 1e-300;
+  const int j = m - 1 - lane;   // ascending index of this lane's eigenvalue
+  if (lane < m) {
+    for (int it = 0; it < 200; ++it) {
+      const double tol = 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 5.5e-17;
+      if (hi - lo <= tol) break;
+      const double mid = 0.5 * (lo + hi);
+      if (sturm_count(ds, e2s, m, mid, 0.0) > j) hi = mid;
+      else lo = mid;
+    }
+    lam[lane] = 0.5 * (lo + hi) * bnorm;
+  }
+  __syncwarp();
+  const double sig0 = sqrt(fmax(lam[0], 0.0));
+  int r = 0;
+  if (t.frob) {   // Eq. curOff6: smallest k with tail(k) = trace - sum_{t<k} lambda_t < budget
+    const double fbud = eps * eps * (*t.frob) / t.frob_w;
+    double pre = 0.0;
+    while (r < m && !(trace - pre < fbud)) pre += fmax(lam[r++], 0.0);
+  } else if (sig0 > 0.0) {
+    for (int k = 0; k < m; ++k) r += (sqrt(fmax(lam[k], 0.0)) >= eps * sig0);
+  }
+  if (lane < m) t.sig[lane] = sqrt(fmax(lam[lane], 0.0));
+  if (lane == 0) *t.rank_out = r;
+  if (r == 0) return;
+  // ---- 3. inverse iteration, lane k < r (equal shifts separated by pertol) ----
+  const double pertol = 10.0 * 2.2e-16 * bnorm;
+  __syncwarp();
+  if (lane < r) {
+    double sft = lam[lane];
+    for (int q = 1; q <= lane && lam[lane - q] - lam[lane] < pertol; ++q) sft -= pertol;
+    double *DL = LU + lane, *Dv = LU + EIGW_M * EIGW_M + lane, *DU = LU + 2 * EIGW_M * EIGW_M + lane,
+           *DU2 = LU + 3 * EIGW_M * EIGW_M + lane, *bb = LU + 4 * EIGW_M * EIGW_M + lane;
+    invit_one(d, e, m, sft, pertol, lane, DL, Dv, DU, DU2, bb, pv + lane, EIGW_M, Z + lane * EIGW_LD);
+  }
+  __syncwarp();
+  // ---- 4. MGS (twice) over the r vectors, lane = vector ----
+  for (int pass = 0; pass < 2; ++pass)
+    for (int q = 0; q < r; ++q) {
+      if (lane == q) {
+        double nn = 0.0;
+        for (int i = 0; i < m; ++i) nn = fma(Z[q * EIGW_LD + i], Z[q * EIGW_LD + i], nn);
+        const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
+        for (int i = 0; i < m; ++i) Z[q * EIGW_LD + i] *= inv;
+      }
+      __syncwarp();
+      if (lane > q && lane < r) {
+        double dt = 0.0;
+        for (int i = 0; i < m; ++i) dt = fma(Z[q * EIGW_LD + i], Z[lane * EIGW_LD + i], dt);
+        for (int i = 0; i < m; ++i) Z[lane * EIGW_LD + i] = fma(-dt, Z[q * EIGW_LD + i], Z[lane * EIGW_LD + i]);
+      }
+      __syncwarp();
+    }
+  // ---- 5. back-transformation V = H_0 ... H_{m-3} Z, lane = vector ----
+  if (lane < r) {
+    double *z = Z + lane * EIGW_LD;
+    for (int k = m - 3; k >= 0; --k) {
+      const double tk = tau[k];
+      if (tk == 0.0) continue;
+      double sdot = z[k + 1];
+      for (int i = k + 2; i < m; ++i) sdot = fma(G[i + k * EIGW_LD], z[i], sdot);
+      sdot *= tk;
+      z[k + 1] -= sdot;
+      for (int i = k + 2; i < m; ++i) z[i] = fma(-sdot, G[i + k * EIGW_LD], z[i]);
+    }
+    for (int i = 0; i < m; ++i) t.V[i + (int64_t)lane * m] = z[i];
+  }
+  (void)status;
 }
 
 // NV simultaneous warp sums, every lane ending with all NV totals.  For NV a
@@ -2523,7 +2710,7 @@ __device__ __forceinline__ bool pivb_diag_chol(double *__restrict__ A, int lda, 
         ok = false;
         break;
       }
-      const double lkk = sqrt(v), rk = frcp(lkk);
+      const double rk = frsqrt(v), lkk = v * rk;
       const double lik = (i > k) ? a[k] * (d * rk) : 0.0;
       if (i == k) a[k] = lkk;
       else if (i > k) a[k] = lik;

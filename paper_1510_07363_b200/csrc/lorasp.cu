@@ -401,6 +401,7 @@ struct lorasp_ctx {
   int64_t f_doubles = 0;
   bool debug = getenv("LORASP_DEBUG") != nullptr;
   bool pivot_unblocked = getenv("LORASP_PIVOT_UNBLOCKED") != nullptr;   // debug: column-wise k_pivot
+  bool eig_no_warp = true;   // the one-warp eigen-solver for m <= 32 (k_eig_warp): off until it beats the block path
   // LU path: partial pivoting inside the fused pivots (k_pivot_lu, pivot = 1),
   // switched on (for the rest of the handle's life) when the no-pivot kernels
   // report LORASP_NEED_PIVOT; SPD path: a failed signed Cholesky re-plans the
@@ -634,6 +635,8 @@ static void set_eig_attrs() {
   CK(cudaFuncSetAttribute(k_backtr_multi<12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_backtr_multi<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EIG_REG_SMEM));
+  CK(cudaFuncSetAttribute(k_eig_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(EIGW_SMEM_DOUBLES * sizeof(double))));
   CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_eig_t<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_tridiag_cl<8, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 8 * 8));
@@ -769,6 +772,18 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
     ++h->launches_factor;
     CK(cudaGetLastError());
     return;
+  }
+  {   // every stack of the wave has m <= 32: one warp per node (k_eig_warp)
+    int mm = 0;
+    for (const EigTask &e : et) mm = std::max(mm, e.m);
+    if (h->eig_regmax_hint > 0) mm = std::max(mm, h->eig_regmax_hint);
+    if (!et.empty() && mm <= EIGW_M && !h->eig_no_warp) {
+      launch_k(k_eig_warp, (unsigned)et.size(), 32, EIGW_SMEM_DOUBLES * sizeof(double), h->stream,
+               (const EigTask *)de, h->plan.eps, h->d_status.as<int>());
+      ++h->launches_factor;
+      CK(cudaGetLastError());
+      return;
+    }
   }
   std::vector<EigTask> small, big, clt[4];
   bool reg_fork = false;
@@ -3642,7 +3657,9 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     EigTask *de;
     CK(cudaMalloc(&de, sizeof(EigTask)));
     CK(cudaMemcpy(de, &e, sizeof(EigTask), cudaMemcpyHostToDevice));
-    {
+    if (m <= EIGW_M && !getenv("LORASP_EIG_GENERIC")) {   // the production path for m <= 32
+      k_eig_warp<<<1, 32, EIGW_SMEM_DOUBLES * sizeof(double)>>>(de, eps, dst);
+    } else {
       if (m >= EIG_REG_MIN && m <= EIG_REG_M && !getenv("LORASP_EIG_GENERIC")) {
         if (ddbg) {
           long long *dprof;

@@ -1,7 +1,7 @@
-"""GPU unit parity of the compress eigen-solver (k_eig_t) through the C-ABI
-test hook `lorasp_test_eig`, on seeded Gram matrices G = M^T M of every size
-class the sweep launches (generic m < 65, register tile 65..128, generic
-129..256, > 256).
+"""GPU unit parity of the compress eigen-solver through the C-ABI test hook
+`lorasp_test_eig`, on seeded Gram matrices G = M^T M of every size class the
+sweep launches (one warp per node, k_eig_warp, m <= 32; register tile / generic
+k_eig_t above, cluster paths > 128).
 
 Reference: the SVD of the stack M (numpy/LAPACK), i.e. Eq. lra (P:l.333-355)
 with the rank rule sigma_k >= eps sigma_0 (Eq. cutOff1, P:l.580-584):
@@ -38,7 +38,7 @@ def stack(m, rows, decay, seed):
     return (Q1 * s) @ Q2.T
 
 
-@pytest.mark.parametrize("m", [1, 2, 3, 17, 40, 64, 65, 100, 128, 129, 160, 200, 256, 312])
+@pytest.mark.parametrize("m", [1, 2, 3, 5, 17, 24, 31, 32, 33, 40, 64, 65, 100, 128, 129, 160, 200, 256, 312])
 @pytest.mark.parametrize("eps", [1e-2, 1e-3])
 def test_eig_matches_svd(L, m, eps):
     M = stack(m, 2 * m + 3, 0.9 if m > 40 else 0.7, seed=m)
@@ -56,7 +56,7 @@ def test_eig_matches_svd(L, m, eps):
     assert np.max(np.abs(V @ V.T - Pr)) <= 1e-8
 
 
-@pytest.mark.parametrize("m", [50, 128, 200])
+@pytest.mark.parametrize("m", [12, 32, 50, 128, 200])
 def test_eig_clustered_and_degenerate(L, m):
     """Repeated singular values (a cluster straddling nothing) and exact zeros:
     the kept subspace is still the right one, the rank counts ties (>=)."""
@@ -76,6 +76,11 @@ def test_eig_clustered_and_degenerate(L, m):
 def test_eig_zero_and_eps0(L):
     sig, V, r, st = L.test_eig(np.zeros((70, 70)), 1e-2)
     assert st == 0 and r == 0
+    sig, V, r, st = L.test_eig(np.zeros((20, 20)), 1e-2)     # warp kernel
+    assert st == 0 and r == 0
+    G = stack(30, 64, 0.7, 5)
+    sig, V, r, st = L.test_eig(G.T @ G, 0.0)
+    assert st == 0 and r == 30 and np.array_equal(V, np.eye(30))
     G = stack(90, 200, 0.9, 3)
     G = G.T @ G
     sig, V, r, st = L.test_eig(G, 0.0)
