@@ -591,82 +591,146 @@ __device__ __forceinline__ void invit_one(const double *__restrict__ d, const do
 constexpr int EIGW_M = 32;
 constexpr int EIGW_LD = EIGW_M + 1;
 constexpr int EIGW_SMEM_DOUBLES =
-    EIGW_M * EIGW_LD            /* G, then Householder vectors below the subdiagonal */
+    EIGW_M * EIGW_LD            /* Householder vectors (row k: v_k, v_k[k+1] = 1) */
     + 5 * 40                    /* d, e, e2 (scaled, padded to 40), tau, lam */
     + 2 * EIGW_M                /* v, w of the current step */
     + 5 * EIGW_M * EIGW_M       /* inverse-iteration LU (interleaved, stride 32) */
     + EIGW_M * EIGW_LD          /* Z: vector k at Z[k * EIGW_LD] */
     + EIGW_M * EIGW_M / 8 + 8;  /* pivot bytes */
+// P Sturm counts at once (P independent recurrences interleaved: one lane's
+// single count is a chain of dependent DFMAs); same arithmetic per point as
+// sturm_count, a point meeting an exact zero minor is recounted by it.
+template <int P>
+__device__ __forceinline__ void sturm_count_multi(const double *__restrict__ d, const double *__restrict__ e2, int m,
+                                                  const double (&x)[P], int (&c)[P]) {
+  const double *e2m = e2 - 1;
+  double p0[P], p1[P];
+  bool zero[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    p0[q] = p1[q] = 1.0;
+    c[q] = 0;
+    zero[q] = false;
+  }
+  for (int i0 = 0; i0 < m; i0 += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u;
+      const double ee = (i == 0) ? 0.0 : e2m[i];
+      const double di = d[i];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        const double p2 = fma(di - x[q], p1[q], -ee * p0[q]);
+        const long long b2 = __double_as_longlong(p2), b1 = __double_as_longlong(p1[q]);
+        zero[q] |= (b2 << 1) == 0;
+        c[q] += (int)((unsigned long long)(b2 ^ b1) >> 63);
+        p0[q] = p1[q];
+        p1[q] = p2;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const double a = fmax(fabs(p0[q]), fabs(p1[q]));
+      const long long ex = ((__double_as_longlong(a) >> 52) & 0x7ff) - 1023;
+      const double sc = __longlong_as_double((long long)(1023 - ex) << 52);
+      p0[q] *= sc;
+      p1[q] *= sc;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+    if (zero[q]) c[q] = sturm_count(d, e2, m, x[q], 0.0);
+}
+
 __global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tasks, double eps, int *status) {
   extern __shared__ double sh[];
   pdl_trigger();
   const EigTask t = tasks[blockIdx.x];
   pdl_wait();
   const int m = t.m, lane = threadIdx.x;
-  double *G = sh, *d = G + EIGW_M * EIGW_LD, *e = d + 40, *e2 = e + 40, *tau = e2 + 40, *lam = tau + 40;
+  double *Hv = sh, *d = Hv + EIGW_M * EIGW_LD, *e = d + 40, *e2 = e + 40, *tau = e2 + 40, *lam = tau + 40;
   double *vs = lam + 40, *ws = vs + EIGW_M, *LU = ws + EIGW_M, *Z = LU + 5 * EIGW_M * EIGW_M;
   unsigned char *pv = reinterpret_cast<unsigned char *>(Z + EIGW_M * EIGW_LD);
   if (m <= 0) {
     if (lane == 0) *t.rank_out = 0;
     return;
   }
+  // row `lane` of G in registers (G symmetric: row = column); zero padding
+  double g[EIGW_M];
+#pragma unroll
+  for (int jj = 0; jj < EIGW_M; ++jj) g[jj] = (lane < m && jj < m) ? t.G[lane + (int64_t)jj * m] : 0.0;
+  double fro = 0.0, trace = 0.0;
+#pragma unroll
+  for (int jj = 0; jj < EIGW_M; ++jj) {
+    fro = fma(g[jj], g[jj], fro);
+    if (jj == lane) trace = g[jj];
+  }
+  fro = warp_sum(fro);
+  trace = warp_sum(trace);
+  if (!(fro > 0.0) || eps == 0.0) {   // G = 0: r = 0 (Z4); eps = 0: V = I, r = m (Z3)
+    const bool keep = fro > 0.0;
+    if (keep)
+      for (int k = 0; k < m; ++k)
+        if (lane < m) t.V[lane + (int64_t)k * m] = (lane == k) ? 1.0 : 0.0;
+    if (lane < m) t.sig[lane] = 0.0;
+    if (lane == 0) *t.rank_out = keep ? m : 0;
+    return;
+  }
+  if (t.dbg && lane == 0) t.dbg[0] = clock64();
+  // ---- 1. Householder tridiagonalisation (lower, dsytd2), lane = row; the step
+  // loop is unrolled so that every register index is static; reciprocals by
+  // frcp (an IEEE FP64 division is ~430 cycles of latency on this chain) ----
+#pragma unroll
+  for (int k = 0; k < EIGW_M - 2; ++k) {
+    if (k + 2 < m) {
+      const double x = (lane > k) ? g[k] : 0.0;
+      const double alpha = __shfl_sync(0xffffffffu, g[k], k + 1);
+      const double s2 = warp_sum((lane > k + 1) ? x * x : 0.0);
+      double tk = 0.0, beta = alpha;
+      if (s2 > 0.0) {
+        const double nrm2 = fma(alpha, alpha, s2), rn = frsqrt(nrm2);
+        beta = -copysign(nrm2 * rn, alpha);
+        tk = (beta - alpha) * frcp(beta);
+        const double sc = frcp(alpha - beta);
+        const double v = (lane == k + 1) ? 1.0 : ((lane > k + 1) ? x * sc : 0.0);
+        vs[lane] = v;
+        Hv[k * EIGW_LD + lane] = v;
+        __syncwarp();
+        double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+        for (int jj = k + 1; jj < EIGW_M; ++jj) {
+          if (jj & 1) p1 = fma(g[jj], vs[jj], p1);
+          else p0 = fma(g[jj], vs[jj], p0);
+        }
+        const double p = (lane > k) ? tk * (p0 + p1) : 0.0;
+        const double a2 = -0.5 * tk * warp_sum(p * v);
+        const double w = fma(a2, v, p);
+        ws[lane] = w;
+        __syncwarp();
+        if (lane > k) {
+#pragma unroll
+          for (int jj = k + 1; jj < EIGW_M; ++jj) g[jj] = fma(-v, ws[jj], fma(-w, vs[jj], g[jj]));
+        }
+        __syncwarp();
+      }
+      if (lane == 0) {
+        tau[k] = tk;
+        e[k] = beta;
+      }
+    }
+  }
   {
-    double fro = 0.0;
-    for (int q = lane; q < m * m; q += 32) fro = fma(t.G[q], t.G[q], fro);
-    fro = warp_sum(fro);
-    if (!(fro > 0.0) || eps == 0.0) {   // G = 0: r = 0 (Z4); eps = 0: V = I, r = m (Z3)
-      const bool keep = fro > 0.0;
-      if (keep)
-        for (int k = 0; k < m; ++k)
-          if (lane < m) t.V[lane + (int64_t)k * m] = (lane == k) ? 1.0 : 0.0;
-      if (lane < m) t.sig[lane] = 0.0;
-      if (lane == 0) *t.rank_out = keep ? m : 0;
-      return;
+    double dl = 0.0, el = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < EIGW_M; ++jj) {
+      if (jj == lane) dl = g[jj];
+      if (jj + 1 == lane) el = g[jj];
     }
+    if (lane < m) d[lane] = dl;
+    if (m >= 2 && lane == m - 1) e[m - 2] = el;
   }
-  for (int j = 0; j < m; ++j)
-    if (lane < m) G[lane + j * EIGW_LD] = t.G[lane + (int64_t)j * m];
-  double trace = 0.0;
-  for (int i = 0; i < m; ++i) trace += t.G[i + (int64_t)i * m];
   __syncwarp();
-  // ---- 1. Householder tridiagonalisation (lower, dsytd2), lane = row ----
-  for (int k = 0; k + 2 < m; ++k) {
-    const double x = (lane > k && lane < m) ? G[lane + k * EIGW_LD] : 0.0;
-    const double alpha = G[(k + 1) + k * EIGW_LD];
-    double s2 = (lane > k + 1 && lane < m) ? x * x : 0.0;
-    s2 = warp_sum(s2);
-    double tk = 0.0, beta = alpha;
-    if (s2 > 0.0) {
-      beta = -copysign(sqrt(alpha * alpha + s2), alpha);
-      tk = (beta - alpha) / beta;
-      const double sc = 1.0 / (alpha - beta);
-      const double v = (lane == k + 1) ? 1.0 : ((lane > k + 1 && lane < m) ? x * sc : 0.0);
-      vs[lane] = v;
-      __syncwarp();
-      // p = tau A v on rows / cols > k
-      double p = 0.0;
-      if (lane > k && lane < m)
-        for (int j = k + 1; j < m; ++j) p = fma(G[lane + j * EIGW_LD], vs[j], p);
-      p *= tk;
-      const double a2 = -0.5 * tk * warp_sum(p * v);
-      const double w = fma(a2, v, p);
-      ws[lane] = w;
-      __syncwarp();
-      if (lane > k && lane < m)
-        for (int j = k + 1; j < m; ++j)
-          G[lane + j * EIGW_LD] = fma(-v, ws[j], fma(-w, vs[j], G[lane + j * EIGW_LD]));
-      __syncwarp();
-      if (lane > k + 1 && lane < m) G[lane + k * EIGW_LD] = v;   // Householder vector below the subdiagonal
-    }
-    if (lane == 0) {
-      tau[k] = tk;
-      e[k] = beta;
-    }
-    __syncwarp();
-  }
-  if (lane < m) d[lane] = G[lane + lane * EIGW_LD];
-  if (lane == 0 && m >= 2) e[m - 2] = G[(m - 1) + (m - 2) * EIGW_LD];
-  __syncwarp();
+  if (t.dbg && lane == 0) t.dbg[1] = clock64();
   // ---- 2. eigenvalues: lane l bisects the l-th largest (Sturm counts, T / bnorm) ----
   double gl = 1e300, gu = -1e300;
   for (int i = 0; i < m; ++i) {
@@ -675,8 +739,7 @@ __global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tas
     gu = fmax(gu, d[i] + off);
   }
   const double bnorm = fmax(fmax(fabs(gl), fabs(gu)), 1e-300);
-  const double isc = 1.0 / bnorm;
-  __syncwarp();
+  const double isc = frcp(bnorm);
   double *ds = LU, *e2s = LU + 40;   // scaled copies (padded: d = 4, e2 = 0 beyond m)
   for (int i = lane; i < 40; i += 32) {
     ds[i] = (i < m) ? d[i] * isc : 4.0;
@@ -685,6 +748,16 @@ __global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tas
   __syncwarp();
   double lo = gl * isc - 4.4e-16 * m - 1e-300, hi = gu * isc + 4.4e-16 * m + 1e-300;
   const int j = m - 1 - lane;   // ascending index of this lane's eigenvalue
+  {   // common bracketing: the counts at 32 points (one per lane), 33 sub-intervals
+    const double h = (hi - lo) * (1.0 / 33.0);
+    const int cp = sturm_count(ds, e2s, m, fma(h, (double)(lane + 1), lo), 0.0);
+    int f = 32;
+    for (int q = 31; q >= 0; --q)
+      if (__shfl_sync(0xffffffffu, cp, q) > j) f = q;
+    const double l0 = lo;
+    if (f < 32) hi = fma(h, (double)(f + 1), l0);
+    if (f > 0) lo = fma(h, (double)f, l0);
+  }
   if (lane < m) {
     for (int it = 0; it < 200; ++it) {
       const double tol = 2.2e-16 * fmax(fabs(lo), fabs(hi)) + 5.5e-17;
@@ -707,6 +780,7 @@ __global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tas
   }
   if (lane < m) t.sig[lane] = sqrt(fmax(lam[lane], 0.0));
   if (lane == 0) *t.rank_out = r;
+  if (t.dbg && lane == 0) t.dbg[2] = clock64();
   if (r == 0) return;
   // ---- 3. inverse iteration, lane k < r (equal shifts separated by pertol) ----
   const double pertol = 10.0 * 2.2e-16 * bnorm;
@@ -719,37 +793,58 @@ __global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tas
     invit_one(d, e, m, sft, pertol, lane, DL, Dv, DU, DU2, bb, pv + lane, EIGW_M, Z + lane * EIGW_LD);
   }
   __syncwarp();
-  // ---- 4. MGS (twice) over the r vectors, lane = vector ----
-  for (int pass = 0; pass < 2; ++pass)
-    for (int q = 0; q < r; ++q) {
-      if (lane == q) {
-        double nn = 0.0;
-        for (int i = 0; i < m; ++i) nn = fma(Z[q * EIGW_LD + i], Z[q * EIGW_LD + i], nn);
-        const double inv = nn > 0.0 ? 1.0 / sqrt(nn) : 0.0;
-        for (int i = 0; i < m; ++i) Z[q * EIGW_LD + i] *= inv;
-      }
-      __syncwarp();
-      if (lane > q && lane < r) {
-        double dt = 0.0;
-        for (int i = 0; i < m; ++i) dt = fma(Z[q * EIGW_LD + i], Z[lane * EIGW_LD + i], dt);
-        for (int i = 0; i < m; ++i) Z[lane * EIGW_LD + i] = fma(-dt, Z[q * EIGW_LD + i], Z[lane * EIGW_LD + i]);
-      }
-      __syncwarp();
+  if (t.dbg && lane == 0) t.dbg[8] = clock64();
+  // ---- 4. MGS over the r vectors (lane = vector, its elements in registers;
+  // the pivot vector reaches the other lanes by shuffles) ----
+  double z[EIGW_M];
+#pragma unroll
+  for (int i = 0; i < EIGW_M; ++i) z[i] = (lane < r && i < m) ? Z[lane * EIGW_LD + i] : 0.0;
+  for (int q = 0; q < r; ++q) {
+    if (lane == q) {
+      double nn = 0.0;
+#pragma unroll
+      for (int i = 0; i < EIGW_M; ++i) nn = fma(z[i], z[i], nn);
+      const double inv = nn > 0.0 ? frsqrt(nn) : 0.0;
+#pragma unroll
+      for (int i = 0; i < EIGW_M; ++i) z[i] *= inv;
     }
-  // ---- 5. back-transformation V = H_0 ... H_{m-3} Z, lane = vector ----
-  if (lane < r) {
-    double *z = Z + lane * EIGW_LD;
-    for (int k = m - 3; k >= 0; --k) {
-      const double tk = tau[k];
-      if (tk == 0.0) continue;
-      double sdot = z[k + 1];
-      for (int i = k + 2; i < m; ++i) sdot = fma(G[i + k * EIGW_LD], z[i], sdot);
-      sdot *= tk;
-      z[k + 1] -= sdot;
-      for (int i = k + 2; i < m; ++i) z[i] = fma(-sdot, G[i + k * EIGW_LD], z[i]);
+    __syncwarp();
+    double zq[EIGW_M], s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < EIGW_M; ++i) {
+      zq[i] = __shfl_sync(0xffffffffu, z[i], q);
+      if (i & 1) s1 = fma(zq[i], z[i], s1);
+      else s0 = fma(zq[i], z[i], s0);
     }
-    for (int i = 0; i < m; ++i) t.V[i + (int64_t)lane * m] = z[i];
+    if (lane > q && lane < r) {
+      const double dt = s0 + s1;
+#pragma unroll
+      for (int i = 0; i < EIGW_M; ++i) z[i] = fma(-dt, zq[i], z[i]);
+    }
   }
+  if (t.dbg && lane == 0) t.dbg[9] = clock64();
+  // ---- 5. back-transformation V = H_0 ... H_{m-3} Z (lane = vector) ----
+  for (int kk = m - 3; kk >= 0; --kk) {
+    const double tk = tau[kk];
+    if (tk == 0.0) continue;
+    const double *hv = Hv + kk * EIGW_LD;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < EIGW_M; ++i) {
+      if (i & 1) s1 = fma(hv[i], z[i], s1);
+      else s0 = fma(hv[i], z[i], s0);
+    }
+    const double sd = tk * (s0 + s1);
+#pragma unroll
+    for (int i = 0; i < EIGW_M; ++i) z[i] = fma(-sd, hv[i], z[i]);
+  }
+  if (lane < r) {
+#pragma unroll
+    for (int i = 0; i < EIGW_M; ++i)
+      if (i < m) t.V[i + (int64_t)lane * m] = z[i];
+  }
+  __syncwarp();
+  if (t.dbg && lane == 0) t.dbg[3] = t.dbg[4] = clock64();
   (void)status;
 }
 

@@ -401,7 +401,6 @@ struct lorasp_ctx {
   int64_t f_doubles = 0;
   bool debug = getenv("LORASP_DEBUG") != nullptr;
   bool pivot_unblocked = getenv("LORASP_PIVOT_UNBLOCKED") != nullptr;   // debug: column-wise k_pivot
-  bool eig_no_warp = true;   // the one-warp eigen-solver for m <= 32 (k_eig_warp): off until it beats the block path
   // LU path: partial pivoting inside the fused pivots (k_pivot_lu, pivot = 1),
   // switched on (for the rest of the handle's life) when the no-pivot kernels
   // report LORASP_NEED_PIVOT; SPD path: a failed signed Cholesky re-plans the
@@ -777,7 +776,7 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
     int mm = 0;
     for (const EigTask &e : et) mm = std::max(mm, e.m);
     if (h->eig_regmax_hint > 0) mm = std::max(mm, h->eig_regmax_hint);
-    if (!et.empty() && mm <= EIGW_M && !h->eig_no_warp) {
+    if (!et.empty() && mm <= EIGW_M) {
       launch_k(k_eig_warp, (unsigned)et.size(), 32, EIGW_SMEM_DOUBLES * sizeof(double), h->stream,
                (const EigTask *)de, h->plan.eps, h->d_status.as<int>());
       ++h->launches_factor;
