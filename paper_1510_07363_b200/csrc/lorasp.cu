@@ -294,7 +294,7 @@ enum KClass {
 static const char *KNAME[K_NCLASS] = {"leaf_scatter", "merge_copy", "gram_gemm", "eig_tridiag",
                                       "project_gemm", "assemble_copy", "pivot_chol_inv", "trsm_gemm",
                                       "schur_gemm", "apply_fwd", "apply_bwd", "spmv", "dot", "vec"};
-static const char *KKERNEL[K_NCLASS] = {"k_leaf_scatter", "k_copy", "k_gemm2_dmma", "k_tridiag_* + k_eig_t", "k_gemm2_dmma", "k_copy",
+static const char *KKERNEL[K_NCLASS] = {"k_leaf_scatter", "k_copy", "k_gemm2_dmma", "k_eig_warp | k_tridiag_* + k_eig_t", "k_gemm2_dmma", "k_copy",
                                         "k_pivot", "k_gemm2_dmma", "k_gemm2_dmma", "k_apply_fwd", "k_apply_bwd",
                                         "k_spmv", "k_dot_partial+k_dot_final", "k_axpby/k_sub/k_set_rhs/k_get_x"};
 struct KStat {
