@@ -355,7 +355,6 @@ struct lorasp_ctx {
   std::vector<size_t> ap_wave_fsm, ap_wave_bsm;
   DevBuf d_apparts, d_upart;
   bool no_split_apply = getenv("LORASP_NO_SPLIT_APPLY") != nullptr;
-  bool no_wave_smem = getenv("LORASP_APPLY_GLOBAL_SMEM") != nullptr;   // A/B: one footprint for all waves
   std::vector<double> ap_wave_flops, ap_wave_bytes;  // per wave, one pass (fwd or bwd)
   size_t ap_fwd_smem = 0, ap_bwd_smem = 0;
   int ap_chunk = 0;
@@ -377,7 +376,6 @@ struct lorasp_ctx {
   void *h_sp = nullptr;     // pinned upload of the part-1 copy + pivot task lists
   size_t h_sp_cap = 0;
   bool no_split = getenv("LORASP_NO_SPLIT") != nullptr;
-  bool no_split_lu = getenv("LORASP_NO_SPLIT_LU") != nullptr;   // A/B: fused LU pivots only
   // rank-predicted schedule: after a factorization, its ranks predict the
   // next one's (same pattern); the host then builds and enqueues every wave
   // without the per-wave rank synchronisation, the device ranks are logged
@@ -389,7 +387,6 @@ struct lorasp_ctx {
   bool no_replay = getenv("LORASP_NO_REPLAY") != nullptr;
   int *h_ranklog = nullptr;
   size_t ranklog_cap = 0;
-  int split_min_m = getenv("LORASP_SPLIT_MIN_M") ? atoi(getenv("LORASP_SPLIT_MIN_M")) : 0;
   std::vector<int64_t> ap_graph_sig;   // launch parameters the graph was captured with
   bool no_graph = getenv("LORASP_NO_GRAPH") != nullptr;
   int64_t vec_len = 0;
@@ -400,7 +397,6 @@ struct lorasp_ctx {
   int64_t launches_factor = 0, launches_apply = 0, launches_krylov = 0;
   int64_t f_doubles = 0;
   bool debug = getenv("LORASP_DEBUG") != nullptr;
-  bool pivot_unblocked = getenv("LORASP_PIVOT_UNBLOCKED") != nullptr;   // debug: column-wise k_pivot
   // LU path: partial pivoting inside the fused pivots (k_pivot_lu, pivot = 1),
   // switched on (for the rest of the handle's life) when the no-pivot kernels
   // report LORASP_NEED_PIVOT; SPD path: a failed signed Cholesky re-plans the
@@ -458,7 +454,6 @@ struct lorasp_ctx {
   int64_t fg_launches = 0;
   int eig_clmax_hint = 0, eig_bigmax_hint = 0, eig_regmax_hint = 0;   // the same for the eigen-solver classes
   int eig_reg_wave_n = 0;   // distributed: register-tile eigen tasks of the whole wave
-  bool eig_split_classes = getenv("LORASP_EIG_SPLIT_CLASSES") != nullptr;   // A/B: one launch per tile class
 };
 
 namespace {
@@ -524,7 +519,6 @@ static int eig_cl_class(int m) {
   if (m > 384 && m <= 512) return 3;
   return 0;
 }
-static const char *eig_cl_disabled = getenv("LORASP_EIG_NO_CLUSTER");   // debug: generic path only
 
 template <int QR, int UC, int CL>
 static void launch_tridiag_cl_t(cudaStream_t st, const EigTask *dt, int n, double eps, long long *prof) {
@@ -562,12 +556,10 @@ static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps
   // waves wider than the GPU are throughput bound: for m <= 64 half the shared
   // memory (still room for ~30 inverse-iteration vectors per batch) lets two
   // CTAs share an SM
-  static const bool narrow_off = getenv("LORASP_EIG_WIDE_FULL_SMEM") != nullptr;
-  static const bool narrow_force = getenv("LORASP_EIG_FORCE_NARROW") != nullptr;   // test hook
   // (m <= 128 keeps 16 warps: r may exceed 64 = 8 vectors per warp x 8 warps;
   // the 8-warp form would need the rank before the launch, which only the
   // rank-predicted sweep has, and the two schedules must agree bit for bit)
-  const bool narrow = !narrow_off && (wave_n > 148 || narrow_force) && c <= 1;
+  const bool narrow = wave_n > 148 && c <= 1;
   const size_t esm = narrow ? (c <= 1 ? EIG_REG_SMEM / 2 : (size_t)110 * 1024) : EIG_REG_SMEM;
   const int eth = (c == 2 && !narrow) ? EIG_REG_THREADS : 256;
   launch_k(k_eig_t<true>, (unsigned)n, eth, esm, st, ds, eps, (int)(esm / 8), dstatus);
@@ -787,7 +779,7 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
   std::vector<EigTask> small, big, clt[4];
   bool reg_fork = false;
   for (const EigTask &e : et) {
-    const int cls = eig_cl_disabled ? 0 : eig_cl_class(e.m);
+    const int cls = eig_cl_class(e.m);
     if (e.m >= EIG_REG_MIN && e.m <= EIG_REG_M) small.push_back(e);
     else if (cls) clt[cls].push_back(e);
     else big.push_back(e);
@@ -802,17 +794,13 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
     int cmax = 0;
     for (auto &e : small) cmax = std::max(cmax, e.m <= 32 ? 0 : (e.m <= 64 ? 1 : 2));
     if (h->eig_regmax_hint > 0) cmax = std::max(cmax, h->eig_regmax_hint <= 32 ? 0 : (h->eig_regmax_hint <= 64 ? 1 : 2));
-    if (h->eig_split_classes)
-      for (auto &e : small) rc[e.m <= 32 ? 0 : (e.m <= 64 ? 1 : 2)].push_back(e);
-    else
-      rc[cmax] = small;
+    rc[cmax] = small;
     EigTask *ds[3] = {nullptr, nullptr, nullptr};
     for (int c = 0; c < 3; ++c)
       if (!rc[c].empty()) ds[c] = (single && rc[c].size() == et.size()) ? de : push(h, rc[c]);
     // with cluster / generic tasks in the same wave the register-tile pair runs
     // on its own stream beside them (few nodes per class: the SMs are idle)
-    static const bool no_fork = getenv("LORASP_EIG_NO_FORK") != nullptr;   // A/B: one stream
-    reg_fork = !single && !h->eig_split_classes && !no_fork;
+    reg_fork = !single;
     cudaStream_t rs = h->stream;
     if (reg_fork) {
       CK(cudaEventRecord(h->ev_ef, h->stream));
@@ -835,7 +823,7 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
         dc[c] = push(h, clt[c]);
         ++ncls;
       }
-    const bool fork = ncls > 1 && !h->eig_split_classes && !getenv("LORASP_EIG_NO_FORK");
+    const bool fork = ncls > 1;
     if (fork) CK(cudaEventRecord(h->ev_cf, h->stream));
     for (int c = 1; c <= 3; ++c) {
       if (!dc[c]) continue;
@@ -940,7 +928,7 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
   int ev = tbeg(h, K_PIVOT);
   if (!small.empty()) {
     PivTask *dp = push(h, small);
-    if (max_n <= PIVB_MAXN && !h->pivot_unblocked) {
+    if (max_n <= PIVB_MAXN) {
       const size_t sm = pivb_smem_bytes(max_n);
       launch_k(k_pivot_blk, (unsigned)small.size(), 512, sm, st, dp, h->d_status.as<int>());
     } else {
@@ -1110,7 +1098,7 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
   }
   PivTask *dp = push(h, h->lu_pivot ? pvp : pv);
   int ev = tbeg(h, K_PIVOT);
-  if (max_n <= PIVLU_MAXN && !h->pivot_unblocked && !h->lu_pivot) {
+  if (max_n <= PIVLU_MAXN && !h->lu_pivot) {
     const size_t sm = pivb_smem_bytes(max_n);
     launch_k(k_pivot_lu_blk, (unsigned)pv.size(), 512, sm, h->stream, dp, h->d_status.as<int>());
   } else {
@@ -1513,8 +1501,6 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
     DevBuf &ar = h->arena[i & 1];
     ar.ensure(std::max<int64_t>(tot, 32) * sizeof(double), st);
     CK(cudaMemsetAsync(ar.p, 0, tot * sizeof(double), st));
-    if (getenv("LORASP_POISON_TAIL") && ar.cap > (size_t)tot * 8)   // debug: NaN beyond the level's slots
-      CK(cudaMemsetAsync(ar.as<char>() + tot * 8, 0xFF, ar.cap - (size_t)tot * 8, st));
     double *base = ar.as<double>();
     auto slot_ptr = [&](int s) { return base + soff[s]; };
     // distributed mode: the owner of each node of this level (include/lorasp.h)
@@ -1610,7 +1596,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       std::vector<CopyTask> s_ct;
       std::vector<PivTask> s_pt;
       int s_max = 0;
-      if (!comp.empty() && !h->no_split && (sym || (!h->no_split_lu && !h->lu_pivot))) {
+      if (!comp.empty() && !h->no_split && (sym || !h->lu_pivot)) {
         int64_t stot2 = 0;
         // A node is split when that pays: in waves wider than the GPU (the S
         // pivots then fill the sync gaps), or when its fused pivot would likely
@@ -1620,8 +1606,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         const bool wide = elim.size() > 148;
         const int pmax = sym ? PIVB_MAXN : PIVLU_MAXN;
         for (int c : elim)
-          if (m[c] <= pmax && m[c] >= h->split_min_m &&
-              (wide || h->split_min_m > 0 || m[c] + (int)std::ceil(rho_pred * m[c]) > pmax)) {
+          if (m[c] <= pmax && (wide || m[c] + (int)std::ceil(rho_pred * m[c]) > pmax)) {
             s_off[c] = stot2;
             stot2 += (sym ? 1 : 2) * (int64_t)m[c] * m[c];   // LU: L11^{-1} and U11^{-T}
           }
@@ -1719,7 +1704,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
               ++h->eig_reg_wave_n;
               continue;
             }
-            if (!eig_cl_disabled && eig_cl_class(mc)) h->eig_clmax_hint = std::max(h->eig_clmax_hint, mc);
+            if (eig_cl_class(mc)) h->eig_clmax_hint = std::max(h->eig_clmax_hint, mc);
             else h->eig_bigmax_hint = std::max(h->eig_bigmax_hint, mc);
           }
         }
@@ -2661,8 +2646,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
     h->ap_wave_ch.assign(nwv, (int)ch);
     h->ap_wave_fsm.assign(nwv, h->ap_fwd_smem);
     h->ap_wave_bsm.assign(nwv, h->ap_bwd_smem);
-    if (!h->no_wave_smem)
-      for (size_t w = 0; w < nwv; ++w) {
+    for (size_t w = 0; w < nwv; ++w) {
         size_t wf = 0, wb = 0, wc = 2;
         for (int q = h->ap_wave_begin[w]; q < h->ap_wave_begin[w + 1]; ++q) {
           const NodeRec &rc = h->recs[q];
@@ -3828,7 +3812,7 @@ int lorasp_test_pivot(int device, double *K, int m, int r) {
     PivTask *dt;
     CK(cudaMalloc(&dt, sizeof(PivTask)));
     CK(cudaMemcpy(dt, &t, sizeof(PivTask), cudaMemcpyHostToDevice));
-    if (n <= PIVB_MAXN && !getenv("LORASP_PIVOT_UNBLOCKED")) {
+    if (n <= PIVB_MAXN) {
       CK(cudaFuncSetAttribute(k_pivot_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
       k_pivot_blk<<<1, 512, pivb_smem_bytes(n)>>>(dt, dst);
     } else {
