@@ -2790,7 +2790,11 @@ constexpr int PIVB_MAXN = 160;
 // per column step.  rd[j0 + k] <- 1 / l_kk.  Returns false on a non-positive
 // pivot (uniform across the warp).
 __device__ __forceinline__ bool pivb_diag_chol(double *__restrict__ A, int lda, int j0, int b, int m,
-                                               double *__restrict__ rd, int lane) {
+                                               double *__restrict__ rd, int lane, double *lcol) {
+  // Branch-free (selects only, so no reconvergence points on the chain): column
+  // k's multipliers reach the other rows through shared memory (lcol, >= 33
+  // doubles; every lane writes its slot) instead of 15 shuffles; a failure is
+  // accumulated rather than breaking out of the unrolled loop.
   const int i = lane;
   double a[PIVB_NB];
 #pragma unroll
@@ -2801,21 +2805,20 @@ __device__ __forceinline__ bool pivb_diag_chol(double *__restrict__ A, int lda, 
     if (k < b) {
       const double d = (j0 + k < m) ? 1.0 : -1.0;
       const double v = __shfl_sync(0xffffffffu, a[k], k) * d;
-      if (!(v > 0.0) || !isfinite(v)) {
-        ok = false;
-        break;
-      }
-      const double rk = frsqrt(v), lkk = v * rk;
+      ok = ok && (v > 0.0) && isfinite(v);
+      const double rk = frsqrt(fmax(v, 1e-300));
       const double lik = (i > k) ? a[k] * (d * rk) : 0.0;
-      if (i == k) a[k] = lkk;
-      else if (i > k) a[k] = lik;
-      if (lane == 0) rd[j0 + k] = rk;
+      a[k] = (i == k) ? v * rk : ((i > k) ? lik : a[k]);
+      rd[j0 + k] = rk;   // every lane stores the same value
+      lcol[i] = lik;
+      __syncwarp();
       const double f = -d * lik;
 #pragma unroll
       for (int jj = k + 1; jj < PIVB_NB; ++jj) {
-        const double ljk = __shfl_sync(0xffffffffu, lik, jj);
-        if (jj < b && i >= jj) a[jj] = fma(f, ljk, a[jj]);
+        const double u = fma(f, lcol[jj], a[jj]);
+        a[jj] = (jj < b && i >= jj) ? u : a[jj];
       }
+      __syncwarp();
     }
   }
   if (ok) {
@@ -2829,28 +2832,25 @@ __device__ __forceinline__ bool pivb_diag_chol(double *__restrict__ A, int lda, 
 
 __device__ __forceinline__ void pivb_diag_inverse(const double *__restrict__ A, int lda, int j0, int b,
                                                   double *__restrict__ W, int lane, const double *__restrict__ rd) {
-  // W (16 x 16, ld 16) <- inverse of the lower-triangular diagonal block A[j0.., j0..]
-  // lane c computes column c by forward substitution
+  // W (16 x 16, ld 16) <- inverse of the lower-triangular diagonal block A[j0.., j0..];
+  // lane c computes column c by column-oriented forward substitution: the
+  // dependent chain is one multiply + one FMA per step
   if (lane < b) {
     const int c = lane;
     double x[PIVB_NB];
 #pragma unroll
-    for (int i = 0; i < PIVB_NB; ++i) x[i] = 0.0;
+    for (int i = 0; i < PIVB_NB; ++i) x[i] = (i == c) ? 1.0 : 0.0;
 #pragma unroll
-    for (int i = 0; i < PIVB_NB; ++i) {
-      if (i < b && i >= c) {
-        double s0 = (i == c) ? 1.0 : 0.0, s1 = 0.0;   // two chains
+    for (int k = 0; k < PIVB_NB; ++k) {
+      if (k < b) {
+        x[k] *= rd[j0 + k];
 #pragma unroll
-        for (int k = 0; k < PIVB_NB; ++k)
-          if (k >= c && k < i) {
-            if (k & 1) s1 = fma(-A[(j0 + i) + (j0 + k) * lda], x[k], s1);
-            else s0 = fma(-A[(j0 + i) + (j0 + k) * lda], x[k], s0);
-          }
-        x[i] = (s0 + s1) * rd[j0 + i];
+        for (int i = k + 1; i < PIVB_NB; ++i)
+          if (i < b) x[i] = fma(-A[(j0 + i) + (j0 + k) * lda], x[k], x[i]);
       }
     }
 #pragma unroll
-    for (int i = 0; i < PIVB_NB; ++i) W[i + c * PIVB_NB] = (i < b) ? x[i] : 0.0;
+    for (int i = 0; i < PIVB_NB; ++i) W[i + c * PIVB_NB] = (i < b && i >= c) ? x[i] : 0.0;
   }
 }
 
@@ -2884,6 +2884,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
   extern __shared__ double sh[];
   __shared__ double W[PIVB_NB * PIVB_NB];
   __shared__ double rd[PIVB_MAXN + PIVB_NB];   // 1 / l_kk
+  __shared__ double lcol[32];
   __shared__ int s_fail;
   pdl_trigger();
   const PivTask t = tasks[blockIdx.x];
@@ -2902,7 +2903,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
   // warp 0: factor diagonal block k (already updated), W = L_kk^{-1}, X_kk = W
   auto diag = [&](int k) {
     const int j0 = PIVB_NB * k, b = min(PIVB_NB, n - j0);
-    if (!pivb_diag_chol(A, lda, j0, b, t.m, rd, lane)) {
+    if (!pivb_diag_chol(A, lda, j0, b, t.m, rd, lane, lcol)) {
       if (lane == 0) {
         s_fail = 1;
         if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
@@ -3057,7 +3058,10 @@ constexpr int PIVLU_MAXN = 160;
 // (lane = row; the pivot row's entries by shuffles).  rd[j0 + k] <- 1 / u_kk.
 // Returns false when |u_kk| <= tiny (uniform across the warp).
 __device__ __forceinline__ bool lu_diag_factor(double *__restrict__ A, int lda, int j0, int b, double tiny,
-                                               double *__restrict__ rd, int lane) {
+                                               double *__restrict__ rd, int lane, double *urow) {
+  // Branch-free (selects only): the pivot row reaches the other lanes through
+  // shared memory (urow, >= 16 doubles) instead of one shuffle per column entry;
+  // a vanishing pivot is accumulated in the result, not a break.
   const int i = lane;
   double a[PIVB_NB];
 #pragma unroll
@@ -3066,20 +3070,23 @@ __device__ __forceinline__ bool lu_diag_factor(double *__restrict__ A, int lda, 
 #pragma unroll
   for (int k = 0; k < PIVB_NB; ++k) {
     if (k < b) {
-      const double piv = __shfl_sync(0xffffffffu, a[k], k);
-      if (!(fabs(piv) > tiny) || !isfinite(piv)) {
-        ok = false;
-        break;
+      if (i == k) {
+#pragma unroll
+        for (int jj = k; jj < PIVB_NB; ++jj) urow[jj] = a[jj];
       }
+      __syncwarp();
+      const double piv = urow[k];
+      ok = ok && (fabs(piv) > tiny) && isfinite(piv);
       const double rp = frcp(piv);
-      if (lane == 0) rd[j0 + k] = rp;
-      const double lik = (i > k) ? a[k] * rp : 0.0;
-      if (i > k) a[k] = lik;
+      rd[j0 + k] = rp;   // every lane stores the same value
+      const double lik = a[k] * rp;
+      a[k] = (i > k) ? lik : a[k];
 #pragma unroll
       for (int jj = k + 1; jj < PIVB_NB; ++jj) {
-        const double ukj = __shfl_sync(0xffffffffu, a[jj], k);
-        if (jj < b && i > k) a[jj] = fma(-lik, ukj, a[jj]);
+        const double u = fma(-lik, urow[jj], a[jj]);
+        a[jj] = (jj < b && i > k) ? u : a[jj];
       }
+      __syncwarp();
     }
   }
   if (ok) {
@@ -3094,43 +3101,35 @@ __device__ __forceinline__ bool lu_diag_factor(double *__restrict__ A, int lda, 
 __device__ __forceinline__ void lu_diag_inverses(const double *__restrict__ A, int lda, int j0, int b,
                                                  double *__restrict__ WL, double *__restrict__ WU, int lane,
                                                  const double *__restrict__ rd) {
-  // WL = L11^{-1} (unit lower, column c by lane c); WU = U11^{-1} (upper, row c by lane c)
+  // WL = L11^{-1} (unit lower, column c by lane c); WU = U11^{-1} (upper, row c by
+  // lane c); both by column-oriented substitution (one FMA on the chain per step)
   if (lane >= b) return;
   const int c = lane;
   double x[PIVB_NB];
 #pragma unroll
-  for (int i = 0; i < PIVB_NB; ++i) {
-    double v = 0.0;
-    if (i == c) {
-      v = 1.0;
-    } else if (i > c && i < b) {
-      double sacc = 0.0;
+  for (int i = 0; i < PIVB_NB; ++i) x[i] = (i == c) ? 1.0 : 0.0;
 #pragma unroll
-      for (int k = 0; k < PIVB_NB; ++k)
-        if (k >= c && k < i) sacc = fma(A[(j0 + i) + (int64_t)(j0 + k) * lda], x[k], sacc);
-      v = -sacc;
+  for (int k = 0; k < PIVB_NB; ++k)
+    if (k < b) {
+#pragma unroll
+      for (int i = k + 1; i < PIVB_NB; ++i)
+        if (i < b) x[i] = fma(-A[(j0 + i) + (j0 + k) * lda], x[k], x[i]);
     }
-    x[i] = v;
-  }
 #pragma unroll
-  for (int i = 0; i < PIVB_NB; ++i) WL[i + c * PIVB_NB] = (i < b) ? x[i] : 0.0;
-  // y = e_c^T U11^{-1}:  y_c = 1 / u_cc,  y_j = -(sum_{k=c}^{j-1} y_k u_kj) / u_jj
+  for (int i = 0; i < PIVB_NB; ++i) WL[i + c * PIVB_NB] = (i < b && i >= c) ? x[i] : 0.0;
+  // y = e_c^T U11^{-1}: y_j = (delta_cj - sum_{k<j} y_k u_kj) / u_jj
 #pragma unroll
-  for (int j = 0; j < PIVB_NB; ++j) {
-    double v = 0.0;
-    if (j == c) {
-      v = rd[j0 + c];
-    } else if (j > c && j < b) {
-      double sacc = 0.0;
+  for (int j = 0; j < PIVB_NB; ++j) x[j] = (j == c) ? 1.0 : 0.0;
 #pragma unroll
-      for (int k = 0; k < PIVB_NB; ++k)
-        if (k >= c && k < j) sacc = fma(x[k], A[(j0 + k) + (int64_t)(j0 + j) * lda], sacc);
-      v = -sacc * rd[j0 + j];
+  for (int j = 0; j < PIVB_NB; ++j)
+    if (j < b) {
+      x[j] *= rd[j0 + j];
+#pragma unroll
+      for (int jj = j + 1; jj < PIVB_NB; ++jj)
+        if (jj < b) x[jj] = fma(-x[j], A[(j0 + j) + (j0 + jj) * lda], x[jj]);
     }
-    x[j] = v;   // reuse: x now holds row c of U11^{-1}
-  }
 #pragma unroll
-  for (int j = 0; j < PIVB_NB; ++j) WU[c + j * PIVB_NB] = (j < b) ? x[j] : 0.0;
+  for (int j = 0; j < PIVB_NB; ++j) WU[c + j * PIVB_NB] = (j < b && j >= c) ? x[j] : 0.0;
 }
 
 __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restrict__ tasks, int *status) {
@@ -3145,6 +3144,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
   extern __shared__ double sh[];
   __shared__ double WL[PIVB_NB * PIVB_NB], WU[PIVB_NB * PIVB_NB];
   __shared__ double rd[PIVLU_MAXN + PIVB_NB];   // 1 / u_kk
+  __shared__ double urow[PIVB_NB];
   __shared__ int s_fail;
   __shared__ double s_amax[16];
   pdl_trigger();
@@ -3170,7 +3170,7 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
   for (int j0 = 0; j0 < n; j0 += PIVB_NB) {
     const int b = min(PIVB_NB, n - j0), j1 = j0 + PIVB_NB;
     if (warp == 0) {
-      if (!lu_diag_factor(A, lda, j0, b, tiny, rd, lane)) {
+      if (!lu_diag_factor(A, lda, j0, b, tiny, rd, lane, urow)) {
         if (lane == 0) {
           s_fail = 1;
           if (atomicCAS(&status[0], 0, LORASP_NEED_PIVOT) == 0) status[1] = t.node;
