@@ -478,6 +478,10 @@ def main():
             "krylov_iters": its[-1], "relres": rr_last, "krylov_status": rc_last,
             "tflops_model": tflops, "fp64_peak_tflops": peak_f, "frac_fp64_peak": tflops / peak_f,
             "flops_model": flops, "factor_bytes": stats.get("factor_bytes"), "aux_vars": stats.get("aux_vars"),
+            "factor_stats": {"kappa1": stats.get("kappa1"), "kappa2": stats.get("kappa2"),
+                             "alpha_hat": stats.get("alpha_hat"),
+                             "levels": [{k: e[k] for k in ("level", "d_max", "rank_avg", "compression_ratio")}
+                                        for e in stats.get("levels", [])]},
             "gpu_launches": launches, "clocks": clocks, "roofline": roof,
             "first_factor_ms": first[0] if first else None, "analyze_s": t_analyze,
             "refactor_new_values": refactor_new, "paper_residual": paper_res,

@@ -223,9 +223,21 @@ int lorasp_dist_owner(int level, int c, int world);
  * (order[k] = cluster processed k-th) and its colour waves (wave[c]). */
 int lorasp_get_depth(lorasp_handle h, int *depth);
 int lorasp_get_level_order(lorasp_handle h, int level, int *order, int *wave, int cap);
+/* Per-node edge counts of the symbolic Alg. 1 replay (valid after analyze, host
+ * only): partners[c] = number of well-separated super-nodes s_c is compressed
+ * against (distance 2, the kappa_2 of Lemma sparse / Theorem, P:l.527-542) and
+ * n1[c] = number of uneliminated neighbours at its elimination (distance 1, the
+ * kappa_1 edges), counting its own redundant node b when s_c was compressed.  Either pointer may be NULL; cap >= 2^(level-1). */
+int lorasp_get_node_counts(lorasp_handle h, int level, int *partners, int *n1, int cap);
 
 /* Numeric queries (valid after factor): per-node retained rank r of s_c^[i]
- * (c = 0..2^(i-1)-1), and per-level super-node sizes m_c. */
+ * (c = 0..2^(i-1)-1), and per-level super-node sizes m_c.  lorasp_get_stats'
+ * "levels" entries summarise them as the paper's FactorStats (P:l.527-558,
+ * P:l.729-733): d_max (= d_i) and d_avg, rank_avg, compression_ratio =
+ * <rank>_l / <super-node size>_l over the compressed super-nodes, kappa1 /
+ * kappa2 (max of the counts above); top level: alpha_hat = max over i < l of
+ * (d_i / d_l)^(1/(l-i)) (the growth condition d_i <= alpha^(l-i) d_l checked
+ * post hoc, a diagnostic). */
 int lorasp_get_ranks(lorasp_handle h, int level, int *ranks, int cap);
 int lorasp_get_sizes(lorasp_handle h, int level, int *sizes, int cap);
 

@@ -3509,6 +3509,17 @@ int lorasp_get_level_order(lorasp_handle h, int level, int *order, int *wave, in
   return LORASP_OK;
 }
 
+int lorasp_get_node_counts(lorasp_handle h, int level, int *partners, int *n1, int cap) {
+  if (!h || level < 1 || level > h->plan.depth) return LORASP_E_ARG;
+  const SymLevel &lv = h->plan.lev[level];
+  if (cap < lv.K) return LORASP_E_ARG;
+  for (int c = 0; c < lv.K; ++c) {
+    if (partners) partners[c] = (int)lv.node[c].partners.size();
+    if (n1) n1[c] = (int)lv.node[c].n1.size() + (lv.node[c].aux ? 1 : 0);   // + b
+  }
+  return LORASP_OK;
+}
+
 int lorasp_get_ranks(lorasp_handle h, int level, int *ranks, int cap) {
   if (!h || !ranks || level < 1 || level > h->plan.depth) return LORASP_E_ARG;
   if (!h->factored) return LORASP_E_STATE;
@@ -3530,6 +3541,7 @@ int lorasp_get_sizes(lorasp_handle h, int level, int *sizes, int cap) {
 int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
   if (!h) return LORASP_E_ARG;
   std::ostringstream o;
+  o.precision(17);
   const Plan &pl = h->plan;
   o << "{\"n\":" << pl.n << ",\"nnz\":" << pl.nnz << ",\"depth\":" << pl.depth << ",\"eps\":" << pl.eps
     << ",\"waves\":" << pl.total_waves << ",\"max_edge_distance\":" << pl.max_edge_distance
@@ -3560,22 +3572,42 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
     for (int i = 1; i <= pl.depth; ++i)
       for (int r : h->rnk[i]) aux += 2 * r;
     o << aux << ",\"levels\":[";
+    // FactorStats (P:l.527-558, P:l.729-733): d_i, <rank>, compression ratio,
+    // kappa1 / kappa2; alpha_hat = max_{i<l} (d_i / d_l)^(1/(l-i))
+    int kap1 = 0, kap2 = 0;
+    double alpha_hat = 0;
+    const int dl = *std::max_element(h->msz[pl.depth].begin(), h->msz[pl.depth].end());
     for (int i = pl.depth; i >= 1; --i) {
-      int64_t rs = 0, ms = 0;
-      int rmax = 0, mmax = 0, nr = 0;
+      int64_t rs = 0, ms = 0, rs_c = 0, ms_c = 0;
+      int rmax = 0, mmax = 0, nr = 0, k1 = 0, k2 = 0;
       for (size_t c = 0; c < h->rnk[i].size(); ++c) {
+        const SymNode &nd = pl.lev[i].node[c];
         rs += h->rnk[i][c];
         rmax = std::max(rmax, h->rnk[i][c]);
         ms += h->msz[i][c];
         mmax = std::max(mmax, h->msz[i][c]);
-        nr += pl.lev[i].node[c].aux;
+        nr += nd.aux;
+        if (nd.aux) {
+          rs_c += h->rnk[i][c];
+          ms_c += h->msz[i][c];
+        }
+        k1 = std::max(k1, (int)nd.n1.size() + (nd.aux ? 1 : 0));
+        k2 = std::max(k2, (int)nd.partners.size());
       }
+      kap1 = std::max(kap1, k1);
+      kap2 = std::max(kap2, k2);
+      if (i < pl.depth && dl > 0 && mmax > 0)
+        alpha_hat = std::max(alpha_hat, std::pow((double)mmax / dl, 1.0 / (pl.depth - i)));
       o << "{\"level\":" << i << ",\"supers\":" << h->rnk[i].size() << ",\"compressed\":" << nr
         << ",\"rank_sum\":" << rs << ",\"rank_max\":" << rmax << ",\"size_sum\":" << ms
-        << ",\"size_max\":" << mmax << ",\"waves\":" << pl.lev[i].wave_begin.size() - 1
+        << ",\"size_max\":" << mmax << ",\"d_max\":" << mmax
+        << ",\"d_avg\":" << (double)ms / std::max<size_t>(1, h->msz[i].size())
+        << ",\"rank_avg\":" << (nr ? (double)rs_c / nr : 0.0)
+        << ",\"compression_ratio\":" << (ms_c ? (double)rs_c / ms_c : 0.0) << ",\"kappa1\":" << k1
+        << ",\"kappa2\":" << k2 << ",\"waves\":" << pl.lev[i].wave_begin.size() - 1
         << ",\"lattice\":" << (pl.lev[i].lattice ? "true" : "false") << "}" << (i > 1 ? "," : "");
     }
-    o << "]";
+    o << "],\"kappa1\":" << kap1 << ",\"kappa2\":" << kap2 << ",\"alpha_hat\":" << alpha_hat;
   }
   o << ",\"kernels\":{";
   bool first = true;

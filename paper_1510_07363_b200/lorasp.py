@@ -35,7 +35,8 @@ STATUS = {0: "OK", 1: "NOT_CONVERGED", -1: "E_ARG", -2: "E_PATTERN", -3: "E_SING
 
 # every symbol include/lorasp.h declares
 SYMBOLS = ["lorasp_analyze", "lorasp_factor", "lorasp_apply", "lorasp_gmres", "lorasp_krylov_ex",
-           "lorasp_set_stream", "lorasp_set_timing", "lorasp_get_depth", "lorasp_get_level_order", "lorasp_get_ranks",
+           "lorasp_set_stream", "lorasp_set_timing", "lorasp_get_depth", "lorasp_get_level_order", "lorasp_get_node_counts",
+           "lorasp_get_ranks",
            "lorasp_get_sizes", "lorasp_get_stats", "lorasp_get_launch_count", "lorasp_test_eig",
            "lorasp_test_pivot", "lorasp_test_gemm", "lorasp_last_error", "lorasp_destroy", "lorasp_set_dist",
            "lorasp_set_dist_buffers", "lorasp_dist_owner", "lorasp_paper_residual", "lorasp_nccl_unique_id",
@@ -231,6 +232,15 @@ class Handle:
         out = np.zeros(K, dtype=np.int32)
         self._check(self._lib.lorasp_get_ranks(self.h, level, _ptr(out), K), "ranks")
         return out
+
+    def node_counts(self, level):
+        """(partners, n1) per level-`level` super-node: the kappa_2 / kappa_1 edges
+        of the symbolic Alg. 1 replay (lorasp_get_node_counts)."""
+        K = 2 ** (level - 1)
+        a = np.zeros(K, dtype=np.int32)
+        b = np.zeros(K, dtype=np.int32)
+        self._check(self._lib.lorasp_get_node_counts(self.h, level, _ptr(a), _ptr(b), K), "node_counts")
+        return a, b
 
     def sizes(self, level):
         K = 2 ** (level - 1)
