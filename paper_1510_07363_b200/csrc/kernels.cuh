@@ -19,7 +19,6 @@
 //                     for 128 < m <= 512 (ranks ~0.6 m there)
 //  Fused (s, b) pivot (P:l.396-399, P:l.101-106):
 //    k_pivot_blk      signed Cholesky K = L diag(I_m, -I_r) L^T + L^{-1}, n <= 160
-//    k_pivdiag        diagonal blocks of the blocked path (n > 160, with k_gemm2)
 //    k_pivot_lu_blk / k_pivot_lu   LU path (LU, L^{-1} P and U^{-T}; partial
 //                     pivoting in k_pivot_lu once the no-pivot multipliers grow)
 //  k_apply_fwd/bwd    Alg. 3 / Alg. 4 (P:l.445-500) per colour wave (+ the split
@@ -2505,6 +2504,11 @@ struct PivTask {
   int ld, m, r, node;
   double *F2;  // LU path: where U^{-T} goes (nullptr: F + ld * n, the record's region 1)
   int pivot;   // LU path (k_pivot_lu): partial pivoting (see there); 0 = none
+  // k_pivot_blk as the diagonal-block step of the blocked large pivot: when Xo
+  // is set, L^{-1} goes to Xo (ld ldxo, upper triangle zeroed) and
+  // Wt = L^{-T} D (64 x 64, ld 64) instead of back into F
+  double *Xo, *Wt;
+  int ldxo;
 };
 
 // LU path without pivoting: a multiplier |l_ij| above this (partial pivoting
@@ -3041,6 +3045,15 @@ __global__ void __launch_bounds__(512, 1) k_pivot_blk(const PivTask *__restrict_
     }
   }
   __syncthreads();
+  if (t.Xo) {
+    for (int j = warp; j < n; j += nw)
+      for (int i = lane; i < n; i += 32) {
+        t.Xo[i + (int64_t)j * t.ldxo] = (i >= j) ? A[i + j * lda] : 0.0;
+        // Wt(k = i, c = j) = L^{-1}(c, k) d_c (upper triangular)
+        t.Wt[i + j * 64] = (i <= j) ? A[j + i * lda] * ((j < t.m) ? 1.0 : -1.0) : 0.0;
+      }
+    return;
+  }
   for (int j = warp; j < n; j += nw)
     for (int i = lane; i < n; i += 32) t.F[i + (int64_t)j * t.ld] = (i >= j) ? A[i + j * lda] : 0.0;
 }
@@ -3328,80 +3341,10 @@ __global__ void __launch_bounds__(512, 1) k_pivot_lu_blk(const PivTask *__restri
 // -------------------------------------------- blocked pivot (large nodes) ----
 // For n = m + r too large for one CTA's shared memory the fused pivot is
 // factored by a right-looking blocked signed Cholesky (64-column panels; panel
-// and trailing updates are k_gemm launches over all large nodes of the wave)
-// and inverted by blocked forward substitution into a scratch X.  This kernel
-// does one diagonal block: K11 = L11 D1 L11^T (d_k = +1 for global column < m,
-// -1 after), writes L11 back, X11 = L11^{-1}, and Wt = L11^{-T} D1 (for the
-// panel update L21 = K21 Wt).
-struct PivDiagTask {
-  double *F;    // pivot area base (ld)
-  double *X;    // n x n scratch for L^{-1} (ldx), zero-initialised
-  double *Wt;   // 64 x 64 scratch (ld 64)
-  int ld, ldx, j0, b, m, node;
-};
-
-__global__ void __launch_bounds__(256) k_pivdiag(const PivDiagTask *__restrict__ tasks, int *status) {
-  __shared__ double A[64 * 65];
-  __shared__ double tmp[64];
-  __shared__ int s_fail;
-  pdl_trigger();
-  const PivDiagTask t = tasks[blockIdx.x];
-  pdl_wait();   // task descriptors are static: read before the wait
-  const int b = t.b, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int la = 65;
-  double *K = t.F + t.j0 + (int64_t)t.j0 * t.ld;
-  for (int j = warp; j < b; j += nw)
-    for (int i = lane; i < b; i += 32) A[i + j * la] = (i >= j) ? K[i + (int64_t)j * t.ld] : 0.0;
-  if (tid == 0) s_fail = 0;
-  __syncthreads();
-  for (int k = 0; k < b; ++k) {
-    const double d = (t.j0 + k < t.m) ? 1.0 : -1.0;
-    const double v = A[k + k * la] * d;
-    if (!(v > 0.0) || !isfinite(v)) {
-      if (tid == 0) {
-        s_fail = 1;
-        if (atomicCAS(&status[0], 0, -3) == 0) status[1] = t.node;
-      }
-      break;
-    }
-    const double lkk = sqrt(v);
-    const double sc = d * frcp(lkk);
-    __syncthreads();
-    for (int i = k + 1 + tid; i < b; i += blockDim.x) A[i + k * la] *= sc;
-    __syncthreads();
-    if (tid == 0) A[k + k * la] = lkk;
-    for (int j = k + 1 + warp; j < b; j += nw) {
-      const double ljk = A[j + k * la] * d;
-      for (int i = j + lane; i < b; i += 32) A[i + j * la] = fma(-A[i + k * la], ljk, A[i + j * la]);
-    }
-    __syncthreads();
-  }
-  if (s_fail) return;
-  for (int j = warp; j < b; j += nw)
-    for (int i = j + lane; i < b; i += 32) K[i + (int64_t)j * t.ld] = A[i + j * la];
-  __syncthreads();
-  for (int j = b - 1; j >= 0; --j) {   // in-place inverse (as in k_pivot)
-    for (int i = j + 1 + tid; i < b; i += blockDim.x) tmp[i] = A[i + j * la];
-    __syncthreads();
-    const double ajj = frcp(A[j + j * la]);
-    for (int i = j + 1 + tid; i < b; i += blockDim.x) {
-      double s = 0;
-      for (int k = j + 1; k <= i; ++k) s = fma(A[i + k * la], tmp[k], s);
-      A[i + j * la] = -ajj * s;
-    }
-    __syncthreads();
-    if (tid == 0) A[j + j * la] = ajj;
-    __syncthreads();
-  }
-  double *X = t.X + t.j0 + (int64_t)t.j0 * t.ldx;
-  for (int j = warp; j < b; j += nw)
-    for (int i = lane; i < b; i += 32) {
-      X[i + (int64_t)j * t.ldx] = (i >= j) ? A[i + j * la] : 0.0;
-      // Wt(k = i, c = j) = L11^{-1}(c, k) d_c  (upper triangular)
-      const double dc = (t.j0 + j < t.m) ? 1.0 : -1.0;
-      t.Wt[i + j * 64] = (i <= j) ? A[j + i * la] * dc : 0.0;
-    }
-}
+// and trailing updates are k_gemm2_dmma launches over all large nodes of the
+// wave) and inverted by blocked forward substitution into a scratch X.  Each
+// diagonal block K11 = L11 D1 L11^T is one k_pivot_blk task (PivTask::Xo):
+// X11 = L11^{-1} into the scratch, Wt = L11^{-T} D1 for the panel L21 = K21 Wt.
 
 // ----------------------------------------------------------------- apply ----
 // Forward (Alg. 3) and backward (Alg. 4) over the fused records

@@ -861,8 +861,44 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
   (void)cap;
 }
 
-void launch_copy(lorasp_ctx *h, const std::vector<CopyTask> &tasks, int cls) {
+// One k_copy CTA moves one task; a large block (a whole n x n pivot inverse,
+// a big super-node block) as one task ran on a single SM at a few GB/s.  Tasks
+// above COPY_CTA_ELEMS elements are cut into rectangles of at most that many
+// (whole-column runs; rows split only for very tall columns).  Tasks never
+// overlap in their writes, so the pieces may run in any order.  The diagonal
+// fill (mode 2) is cut into column runs with their own diagonal rows.
+static const int64_t COPY_CTA_ELEMS = 16384;
+void split_copies(std::vector<CopyTask> &tasks) {
+  bool any = false;
+  for (const CopyTask &t : tasks)
+    if ((int64_t)t.rows * t.cols > COPY_CTA_ELEMS) any = true;
+  if (!any) return;
+  std::vector<CopyTask> out;
+  out.reserve(tasks.size() * 2);
+  for (const CopyTask &t : tasks) {
+    if ((int64_t)t.rows * t.cols <= COPY_CTA_ELEMS || t.rows <= 0 || t.cols <= 0 || t.mode == 2) {
+      out.push_back(t);
+      continue;
+    }
+    const int rb = (int)std::min<int64_t>(t.rows, 4096);
+    const int cb = (int)std::max<int64_t>(1, COPY_CTA_ELEMS / rb);
+    for (int c0 = 0; c0 < t.cols; c0 += cb)
+      for (int r0 = 0; r0 < t.rows; r0 += rb) {
+        CopyTask p = t;
+        p.rows = std::min(rb, t.rows - r0);
+        p.cols = std::min(cb, t.cols - c0);
+        p.dst = t.dst + r0 + (int64_t)c0 * t.ldd;
+        if (t.mode == 0)   // trans: dst(i, j) = src(j, i)
+          p.src = t.trans ? t.src + c0 + (int64_t)r0 * t.lds : t.src + r0 + (int64_t)c0 * t.lds;
+        out.push_back(p);
+      }
+  }
+  tasks.swap(out);
+}
+
+void launch_copy(lorasp_ctx *h, std::vector<CopyTask> tasks, int cls) {
   if (tasks.empty()) return;
+  split_copies(tasks);
   CopyTask *dt = push(h, tasks);
   double bytes = 0;
   for (const CopyTask &t : tasks) bytes += (t.mode == 0 ? 16.0 : 8.0) * t.rows * t.cols;
@@ -908,7 +944,8 @@ double node_flops(int m, int r, int R, int W, bool sym) {
 }
 
 // Fused pivots of one wave: nodes whose pivot fits one CTA's shared memory go
-// through k_pivot; larger ones through the blocked path (k_pivdiag + k_gemm).
+// through k_pivot_blk; larger ones through the blocked path (k_pivot_blk on the
+// 64 x 64 diagonal blocks + k_gemm2_dmma).
 static const int PIV_SMALL_N = 160;
 
 void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double b_piv) {
@@ -962,7 +999,7 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
       return wb + off[q] + (int64_t)n * n + (int64_t)n * 64 + (int64_t)((n + 63) / 64) * 4096;
     };
     for (int p = 0; p < np_max; ++p) {
-      std::vector<PivDiagTask> dt;
+      std::vector<PivTask> dt;
       std::vector<CopyTask> ct;
       std::vector<GemmTask> g1, g2;
       std::vector<GemmSeg> s1, s2;
@@ -971,7 +1008,14 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
         const int n = t.m + t.r, j0 = 64 * p;
         if (j0 >= n) continue;
         const int b = std::min(64, n - j0), j1 = j0 + b, rest = n - j1;
-        dt.push_back(PivDiagTask{t.F, Xp(q), Wp(q), t.ld, n, j0, b, t.m, t.node});
+        {   // diagonal block: k_pivot_blk on the b x b block (local signs: m - j0 plus)
+          const int ml = std::max(0, std::min(b, t.m - j0));
+          PivTask d{t.F + j0 + (int64_t)j0 * t.ld, t.ld, ml, b - ml, t.node};
+          d.Xo = Xp(q) + j0 + (int64_t)j0 * n;
+          d.ldxo = n;
+          d.Wt = Wp(q);
+          dt.push_back(d);
+        }
         if (rest == 0) continue;
         CopyTask c{};
         c.src = t.F + j1 + (int64_t)j0 * t.ld;
@@ -1018,8 +1062,8 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
           }
       }
       if (!dt.empty()) {
-        PivDiagTask *dd = push(h, dt);
-        launch_k(k_pivdiag, (unsigned)dt.size(), 256, 0, st, dd, h->d_status.as<int>());
+        PivTask *dd = push(h, dt);
+        launch_k(k_pivot_blk, (unsigned)dt.size(), 512, pivb_smem_bytes(64), st, dd, h->d_status.as<int>());
         ++h->launches_factor;
         CK(cudaGetLastError());
       }
@@ -1633,6 +1677,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           CK(cudaEventRecord(h->ev_s0, st));   // S is final here; stream2 starts after it
         }
       }
+      split_copies(s_ct);
       // part 1 is enqueued on stream2 once the compress kernels are queued
       auto enqueue_split_part1 = [&]() {
         if (s_pt.empty()) return;
@@ -2378,6 +2423,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       // lists, and a staging-ring wrap there (which reuses the ring after
       // synchronising) would overwrite descriptors pushed earlier but consumed
       // later — so Z / Schur descriptors are pushed after the pivots
+      split_copies(ct);
       h->stg.reserve(vbytes(pt) + vbytes(ps) + vbytes(ct), st);
       GemmTask *d_pt = pushd(h, pt);
       GemmSeg *d_ps = pushd(h, ps);
