@@ -37,6 +37,7 @@
 
 #include "internal.h"
 #include "kernels.cuh"
+#include "eig_small.cuh"
 #include "lorasp.h"
 
 namespace lorasp {
@@ -371,7 +372,7 @@ struct lorasp_ctx {
   cudaStream_t stream_cl[2] = {nullptr, nullptr};   // cluster tridiagonalisation classes 2, 3
   cudaEvent_t ev_cf = nullptr, ev_cj[2] = {nullptr, nullptr};
   bool s1_pending = false;
-  DevBuf ws_S, ws_Y, ws_T1, d_sp;
+  DevBuf ws_S, ws_Y, ws_T1, d_sp, ws_piv2;   // ws_piv2: blocked split-pivot part 1 (stream2)
   DevBuf d_frob, d_frobpart;   // f2: ||all levels below||_F^2 (device scalar) and per-slot partial sums
   void *h_sp = nullptr;     // pinned upload of the part-1 copy + pivot task lists
   size_t h_sp_cap = 0;
@@ -569,7 +570,8 @@ static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps
 
 // After k_tridiag_cl: eigenvalues + rank (k_eig_t<false, true>), chunked
 // inverse iteration, MGS, chunked back-transformation.  Returns the launches.
-static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double eps, int *dstatus) {
+static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double eps, int *dstatus,
+                           cudaEvent_t *pev = nullptr) {
   launch_k(k_eig_t<false, true>, (unsigned)n, EIG_REG_THREADS, SMEM_LIMIT, st, dp, eps, SMEM_LIMIT / 8, dstatus);
   CK(cudaGetLastError());
   if (eps == 0.0) return 1;   // V = I already written
@@ -578,8 +580,10 @@ static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double
   const int mp = (mmax + 8) & ~7;
   const int nb = (int)std::min<int64_t>(256, (cap - 2 * mp) / per);
   const int nch = (mmax + nb - 1) / nb;
+  if (pev) cudaEventRecord(pev[0], st);
   launch_k(k_invit_multi, (unsigned)(n * nch), 256, SMEM_LIMIT, st, dp, nch, cap);
   CK(cudaGetLastError());
+  if (pev) cudaEventRecord(pev[1], st);
   {
     // vectors on chip over a 4- or 8-CTA cluster (all r <= m fit: (m/CL) (m|1) + m doubles)
     const int CLn = (mmax <= 320) ? 4 : (mmax <= 448 ? 8 : 16);
@@ -602,6 +606,7 @@ static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double
     else CK(cudaLaunchKernelEx(&cfg, k_orth_cl<16>, (const EigTask *)dp));
   }
   CK(cudaGetLastError());
+  if (pev) cudaEventRecord(pev[2], st);
   if (mmax <= 256) {
     const int nc = (mmax + 63) / 64;
     launch_k(k_backtr_multi<8, 4>, (unsigned)(n * nc), 512, SMEM_LIMIT, st, dp, nc, cap);
@@ -629,6 +634,8 @@ static void set_eig_attrs() {
   CK(cudaFuncSetAttribute(k_eig_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(EIGW_SMEM_DOUBLES * sizeof(double))));
   CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_eig_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_small_smem_bytes(1)));
+  CK(cudaFuncSetAttribute(k_eig_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_small_smem_bytes(2)));
   CK(cudaFuncSetAttribute(k_eig_t<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_tridiag_cl<8, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 8 * 8));
   CK(cudaFuncSetAttribute(k_tridiag_cl<12, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 12 * 8));
@@ -643,7 +650,7 @@ void ensure_mem(lorasp_ctx *h) {
       const char *t;
     } tg[] = {{&h->arena[0], "arena"}, {&h->arena[1], "arena"}, {&h->ws_G, "ws_G"}, {&h->ws_V, "ws_V"},
               {&h->ws_sig, "ws_sig"}, {&h->ws_X, "ws_X"}, {&h->ws_ctr, "ws_ctr"}, {&h->ws_piv, "ws_piv"},
-              {&h->ws_S, "ws_S"}, {&h->ws_Y, "ws_Y"}, {&h->ws_T1, "ws_T1"}, {&h->d_ranks, "d_ranks"},
+              {&h->ws_S, "ws_S"}, {&h->ws_Y, "ws_Y"}, {&h->ws_T1, "ws_T1"}, {&h->ws_piv2, "ws_piv2"}, {&h->d_ranks, "d_ranks"},
               {&h->d_vec, "d_vec"}, {&h->d_y, "d_y"}, {&h->d_kry, "d_kry"}, {&h->fg_desc, "fg_desc"}};
     for (auto &x : tg) x.b->tag = x.t;
   }
@@ -943,6 +950,206 @@ double node_flops(int m, int r, int R, int W, bool sym) {
   return f;
 }
 
+// Blocked path for fused SPD pivots with n = m + r > PIV_SMALL_N (right-looking
+// signed Cholesky in 64-column panels, then blocked forward substitution for
+// L^{-1} in a scratch X, copied back over the pivot).  The whole launch
+// sequence is planned on the host first, with every descriptor in one blob, so
+// that it can run on the main stream (descriptors through the staging ring) or
+// on stream2 beside the compress (split pivot, part 1; its own upload).
+// Scratch per node: X (n x n) | S (n x 64) | T (np x 64 x 64) | Wt (64 x 64).
+struct BlockedPlan {
+  struct Step {
+    int kind;            // 0: k_pivot_blk on 64 x 64 diagonal blocks, 1: k_copy, 2: k_gemm2_dmma
+    size_t off, n;       // descriptors (PivTask / CopyTask / GemmTask) in the blob
+    size_t soff;         // GemmSeg array (kind 2)
+  };
+  std::vector<char> blob;
+  std::vector<Step> steps;
+  int64_t ws_doubles = 0;
+  template <class T>
+  size_t add(const std::vector<T> &v) {
+    const size_t off = blob.size();
+    blob.resize(off + ((v.size() * sizeof(T) + 255) & ~size_t(255)));
+    if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  }
+};
+
+static int64_t blocked_ws_doubles_one(int n) {
+  return (int64_t)n * n + (int64_t)n * 64 + (int64_t)((n + 63) / 64) * 4096 + 4096;
+}
+static size_t blocked_ws_bytes(const std::vector<PivTask> &big) {
+  int64_t tot = 0;
+  for (const PivTask &t : big) tot += blocked_ws_doubles_one(t.m + t.r);
+  return (size_t)tot * 8 + 256;
+}
+
+void build_blocked_plan(const std::vector<PivTask> &big, double *wb, BlockedPlan &plan) {
+  std::vector<int64_t> off(big.size());
+  int64_t tot = 0;
+  int np_max = 0;
+  for (size_t q = 0; q < big.size(); ++q) {
+    const int n = big[q].m + big[q].r;
+    off[q] = tot;
+    tot += blocked_ws_doubles_one(n);
+    np_max = std::max(np_max, (n + 63) / 64);
+  }
+  plan.ws_doubles = tot;
+  auto Xp = [&](size_t q) { return wb + off[q]; };
+  auto Sp = [&](size_t q) { const int n = big[q].m + big[q].r; return wb + off[q] + (int64_t)n * n; };
+  auto Tp = [&](size_t q) { const int n = big[q].m + big[q].r; return wb + off[q] + (int64_t)n * n + (int64_t)n * 64; };
+  auto Wp = [&](size_t q) {
+    const int n = big[q].m + big[q].r;
+    return wb + off[q] + (int64_t)n * n + (int64_t)n * 64 + (int64_t)((n + 63) / 64) * 4096;
+  };
+  auto step_copy = [&](std::vector<CopyTask> &ct) {
+    split_copies(ct);
+    if (!ct.empty()) plan.steps.push_back({1, plan.add(ct), ct.size(), 0});
+  };
+  auto step_gemm = [&](const std::vector<GemmTask> &g, const std::vector<GemmSeg> &sg) {
+    if (g.empty()) return;
+    const size_t so = plan.add(sg);
+    plan.steps.push_back({2, plan.add(g), g.size(), so});
+  };
+  for (int p = 0; p < np_max; ++p) {
+    std::vector<PivTask> dt;
+    std::vector<CopyTask> ct;
+    std::vector<GemmTask> g1, g2;
+    std::vector<GemmSeg> s1, s2;
+    for (size_t q = 0; q < big.size(); ++q) {
+      const PivTask &t = big[q];
+      const int n = t.m + t.r, j0 = 64 * p;
+      if (j0 >= n) continue;
+      const int b = std::min(64, n - j0), j1 = j0 + b, rest = n - j1;
+      {   // diagonal block: k_pivot_blk on the b x b block (local signs: m - j0 plus)
+        const int ml = std::max(0, std::min(b, t.m - j0));
+        PivTask d{t.F + j0 + (int64_t)j0 * t.ld, t.ld, ml, b - ml, t.node};
+        d.Xo = Xp(q) + j0 + (int64_t)j0 * n;
+        d.ldxo = n;
+        d.Wt = Wp(q);
+        dt.push_back(d);
+      }
+      if (rest == 0) continue;
+      CopyTask c{};
+      c.src = t.F + j1 + (int64_t)j0 * t.ld;
+      c.lds = t.ld;
+      c.dst = Sp(q);
+      c.ldd = n;
+      c.rows = rest;
+      c.cols = b;
+      c.mode = 0;
+      c.alpha = 1.0;
+      ct.push_back(c);
+      // L21 = S Wt
+      GemmTask g{};
+      g.C = t.F + j1 + (int64_t)j0 * t.ld;
+      g.ldc = t.ld;
+      g.M = rest;
+      g.N = b;
+      g.beta = 0;
+      g.seg0 = (int)s1.size();
+      g.nseg = 1;
+      s1.push_back(GemmSeg{Sp(q), Wp(q), n, 64, b, 1.0});
+      add_tiles(g1, g);
+      // K22 -= L21 D1 L21^T (lower tiles)
+      const int spos = std::max(0, std::min(b, t.m - j0));
+      const double *L21 = t.F + j1 + (int64_t)j0 * t.ld;
+      GemmTask u{};
+      u.C = t.F + j1 + (int64_t)j1 * t.ld;
+      u.ldc = t.ld;
+      u.M = rest;
+      u.N = rest;
+      u.tb = 1;
+      u.beta = 1;
+      u.seg0 = (int)s2.size();
+      if (spos > 0) s2.push_back(GemmSeg{L21, L21, t.ld, t.ld, spos, -1.0});
+      if (spos < b) s2.push_back(GemmSeg{L21 + (int64_t)spos * t.ld, L21 + (int64_t)spos * t.ld, t.ld, t.ld,
+                                         b - spos, 1.0});
+      u.nseg = (int)s2.size() - u.seg0;
+      for (int tn = 0; tn < rest; tn += GT)
+        for (int tm = tn; tm < rest; tm += GT) {
+          GemmTask x = u;
+          x.tm = tm;
+          x.tn = tn;
+          g2.push_back(x);
+        }
+    }
+    if (!dt.empty()) plan.steps.push_back({0, plan.add(dt), dt.size(), 0});
+    step_copy(ct);
+    step_gemm(g1, s1);
+    step_gemm(g2, s2);
+  }
+  // blocked inversion: X_ip = -X_ii * sum_{k=p}^{i-1} L_ik X_kp
+  for (int i = 1; i < np_max; ++i) {
+    std::vector<GemmTask> g1, g2;
+    std::vector<GemmSeg> s1, s2;
+    for (size_t q = 0; q < big.size(); ++q) {
+      const PivTask &t = big[q];
+      const int n = t.m + t.r, i0 = 64 * i;
+      if (i0 >= n) continue;
+      const int bi = std::min(64, n - i0);
+      for (int p = 0; p < i; ++p) {
+        const int p0 = 64 * p, bp = 64;
+        GemmTask g{};
+        g.C = Tp(q) + (int64_t)p * 4096;   // T_ip: bi x 64, ld 64, slot p
+        g.ldc = 64;
+        g.M = bi;
+        g.N = bp;
+        g.beta = 0;
+        g.seg0 = (int)s1.size();
+        g.nseg = 1;
+        s1.push_back(GemmSeg{t.F + i0 + (int64_t)p0 * t.ld, Xp(q) + p0 + (int64_t)p0 * n, t.ld, n, i0 - p0, 1.0});
+        add_tiles(g1, g);
+        GemmTask x{};
+        x.C = Xp(q) + i0 + (int64_t)p0 * n;
+        x.ldc = n;
+        x.M = bi;
+        x.N = bp;
+        x.beta = 0;
+        x.seg0 = (int)s2.size();
+        x.nseg = 1;
+        s2.push_back(GemmSeg{Xp(q) + i0 + (int64_t)i0 * n, Tp(q) + (int64_t)p * 4096, n, 64, bi, -1.0});
+        add_tiles(g2, x);
+      }
+    }
+    step_gemm(g1, s1);
+    step_gemm(g2, s2);
+  }
+  std::vector<CopyTask> ct;
+  for (size_t q = 0; q < big.size(); ++q) {
+    const PivTask &t = big[q];
+    const int n = t.m + t.r;
+    CopyTask c{};
+    c.src = Xp(q);
+    c.lds = n;
+    c.dst = t.F;
+    c.ldd = t.ld;
+    c.rows = n;
+    c.cols = n;
+    c.mode = 0;
+    c.alpha = 1.0;
+    ct.push_back(c);
+  }
+  step_copy(ct);
+}
+
+// The plan's scratch is zeroed first (the upper blocks of X stay zero).
+void run_blocked_plan(lorasp_ctx *h, const BlockedPlan &plan, const char *dbase, double *ws, cudaStream_t st) {
+  CK(cudaMemsetAsync(ws, 0, plan.ws_doubles * 8, st));
+  for (const BlockedPlan::Step &s : plan.steps) {
+    if (s.kind == 0)
+      launch_k(k_pivot_blk, (unsigned)s.n, 512, pivb_smem_bytes(64), st, (const PivTask *)(dbase + s.off),
+               h->d_status.as<int>());
+    else if (s.kind == 1)
+      launch_k(k_copy, (unsigned)s.n, 256, 0, st, (const CopyTask *)(dbase + s.off));
+    else
+      launch_k(k_gemm2_dmma, (unsigned)s.n, 128, 0, st, (const GemmTask *)(dbase + s.off),
+               (const GemmSeg *)(dbase + s.soff));
+    ++h->launches_factor;
+    CK(cudaGetLastError());
+  }
+}
+
 // Fused pivots of one wave: nodes whose pivot fits one CTA's shared memory go
 // through k_pivot_blk; larger ones through the blocked path (k_pivot_blk on the
 // 64 x 64 diagonal blocks + k_gemm2_dmma).
@@ -978,151 +1185,12 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
     CK(cudaGetLastError());
   }
   if (!big.empty()) {
-    // scratch per node: X (n x n) | S (n x 64) | T (n x 64) | Wt (64 x 64)
-    std::vector<int64_t> off(big.size());
-    int64_t tot = 0;
-    int np_max = 0;
-    for (size_t q = 0; q < big.size(); ++q) {
-      const int n = big[q].m + big[q].r;
-      off[q] = tot;
-      tot += (int64_t)n * n + (int64_t)n * 64 + (int64_t)((n + 63) / 64) * 4096 + 4096;
-      np_max = std::max(np_max, (n + 63) / 64);
-    }
-    h->ws_piv.ensure(tot * 8 + 256, st);
-    CK(cudaMemsetAsync(h->ws_piv.p, 0, tot * 8, st));
-    double *wb = h->ws_piv.as<double>();
-    auto Xp = [&](size_t q) { return wb + off[q]; };
-    auto Sp = [&](size_t q) { const int n = big[q].m + big[q].r; return wb + off[q] + (int64_t)n * n; };
-    auto Tp = [&](size_t q) { const int n = big[q].m + big[q].r; return wb + off[q] + (int64_t)n * n + (int64_t)n * 64; };
-    auto Wp = [&](size_t q) {
-      const int n = big[q].m + big[q].r;
-      return wb + off[q] + (int64_t)n * n + (int64_t)n * 64 + (int64_t)((n + 63) / 64) * 4096;
-    };
-    for (int p = 0; p < np_max; ++p) {
-      std::vector<PivTask> dt;
-      std::vector<CopyTask> ct;
-      std::vector<GemmTask> g1, g2;
-      std::vector<GemmSeg> s1, s2;
-      for (size_t q = 0; q < big.size(); ++q) {
-        const PivTask &t = big[q];
-        const int n = t.m + t.r, j0 = 64 * p;
-        if (j0 >= n) continue;
-        const int b = std::min(64, n - j0), j1 = j0 + b, rest = n - j1;
-        {   // diagonal block: k_pivot_blk on the b x b block (local signs: m - j0 plus)
-          const int ml = std::max(0, std::min(b, t.m - j0));
-          PivTask d{t.F + j0 + (int64_t)j0 * t.ld, t.ld, ml, b - ml, t.node};
-          d.Xo = Xp(q) + j0 + (int64_t)j0 * n;
-          d.ldxo = n;
-          d.Wt = Wp(q);
-          dt.push_back(d);
-        }
-        if (rest == 0) continue;
-        CopyTask c{};
-        c.src = t.F + j1 + (int64_t)j0 * t.ld;
-        c.lds = t.ld;
-        c.dst = Sp(q);
-        c.ldd = n;
-        c.rows = rest;
-        c.cols = b;
-        c.mode = 0;
-        c.alpha = 1.0;
-        ct.push_back(c);
-        // L21 = S Wt
-        GemmTask g{};
-        g.C = t.F + j1 + (int64_t)j0 * t.ld;
-        g.ldc = t.ld;
-        g.M = rest;
-        g.N = b;
-        g.beta = 0;
-        g.seg0 = (int)s1.size();
-        g.nseg = 1;
-        s1.push_back(GemmSeg{Sp(q), Wp(q), n, 64, b, 1.0});
-        add_tiles(g1, g);
-        // K22 -= L21 D1 L21^T (lower tiles)
-        const int spos = std::max(0, std::min(b, t.m - j0));
-        const double *L21 = t.F + j1 + (int64_t)j0 * t.ld;
-        GemmTask u{};
-        u.C = t.F + j1 + (int64_t)j1 * t.ld;
-        u.ldc = t.ld;
-        u.M = rest;
-        u.N = rest;
-        u.tb = 1;
-        u.beta = 1;
-        u.seg0 = (int)s2.size();
-        if (spos > 0) s2.push_back(GemmSeg{L21, L21, t.ld, t.ld, spos, -1.0});
-        if (spos < b) s2.push_back(GemmSeg{L21 + (int64_t)spos * t.ld, L21 + (int64_t)spos * t.ld, t.ld, t.ld,
-                                           b - spos, 1.0});
-        u.nseg = (int)s2.size() - u.seg0;
-        for (int tn = 0; tn < rest; tn += GT)
-          for (int tm = tn; tm < rest; tm += GT) {
-            GemmTask x = u;
-            x.tm = tm;
-            x.tn = tn;
-            g2.push_back(x);
-          }
-      }
-      if (!dt.empty()) {
-        PivTask *dd = push(h, dt);
-        launch_k(k_pivot_blk, (unsigned)dt.size(), 512, pivb_smem_bytes(64), st, dd, h->d_status.as<int>());
-        ++h->launches_factor;
-        CK(cudaGetLastError());
-      }
-      launch_copy(h, ct, -1);
-      launch_gemm(h, g1, s1, -1, 0, 0);
-      launch_gemm(h, g2, s2, -1, 0, 0);
-    }
-    // blocked inversion: X_ip = -X_ii * sum_{k=p}^{i-1} L_ik X_kp
-    for (int i = 1; i < np_max; ++i) {
-      std::vector<GemmTask> g1, g2;
-      std::vector<GemmSeg> s1, s2;
-      for (size_t q = 0; q < big.size(); ++q) {
-        const PivTask &t = big[q];
-        const int n = t.m + t.r, i0 = 64 * i;
-        if (i0 >= n) continue;
-        const int bi = std::min(64, n - i0);
-        for (int p = 0; p < i; ++p) {
-          const int p0 = 64 * p, bp = 64;
-          GemmTask g{};
-          g.C = Tp(q) + (int64_t)p * 4096;   // T_ip: bi x 64, ld 64, slot p
-          g.ldc = 64;
-          g.M = bi;
-          g.N = bp;
-          g.beta = 0;
-          g.seg0 = (int)s1.size();
-          g.nseg = 1;
-          s1.push_back(GemmSeg{t.F + i0 + (int64_t)p0 * t.ld, Xp(q) + p0 + (int64_t)p0 * n, t.ld, n, i0 - p0, 1.0});
-          add_tiles(g1, g);
-          GemmTask x{};
-          x.C = Xp(q) + i0 + (int64_t)p0 * n;
-          x.ldc = n;
-          x.M = bi;
-          x.N = bp;
-          x.beta = 0;
-          x.seg0 = (int)s2.size();
-          x.nseg = 1;
-          s2.push_back(GemmSeg{Xp(q) + i0 + (int64_t)i0 * n, Tp(q) + (int64_t)p * 4096, n, 64, bi, -1.0});
-          add_tiles(g2, x);
-        }
-      }
-      launch_gemm(h, g1, s1, -1, 0, 0);
-      launch_gemm(h, g2, s2, -1, 0, 0);
-    }
-    std::vector<CopyTask> ct;
-    for (size_t q = 0; q < big.size(); ++q) {
-      const PivTask &t = big[q];
-      const int n = t.m + t.r;
-      CopyTask c{};
-      c.src = Xp(q);
-      c.lds = n;
-      c.dst = t.F;
-      c.ldd = t.ld;
-      c.rows = n;
-      c.cols = n;
-      c.mode = 0;
-      c.alpha = 1.0;
-      ct.push_back(c);
-    }
-    launch_copy(h, ct, -1);
+    h->ws_piv.ensure(blocked_ws_bytes(big), st);
+    BlockedPlan plan;
+    build_blocked_plan(big, h->ws_piv.as<double>(), plan);
+    h->stg.reserve(plan.blob.size() + 256, st);
+    const char *dbase = static_cast<const char *>(h->stg.push(plan.blob.data(), plan.blob.size(), st));
+    run_blocked_plan(h, plan, dbase, h->ws_piv.as<double>(), st);
   }
   tend(h, ev, f_piv, b_piv);
 }
@@ -1638,7 +1706,8 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       // rank sync (part 2).  Nodes with m > PIVB_MAXN keep the fused pivot.
       std::vector<int64_t> s_off(K, -1);
       std::vector<CopyTask> s_ct;
-      std::vector<PivTask> s_pt;
+      std::vector<PivTask> s_pt, s_big;
+      BlockedPlan s_plan;
       int s_max = 0;
       if (!comp.empty() && !h->no_split && (sym || !h->lu_pivot)) {
         int64_t stot2 = 0;
@@ -1649,15 +1718,17 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         // path.  Otherwise the single fused k_pivot_blk is cheaper.
         const bool wide = elim.size() > 148;
         const int pmax = sym ? PIVB_MAXN : PIVLU_MAXN;
+        // SPD nodes with m > PIVB_MAXN: part 1 is the blocked path on S (stream2,
+        // hidden behind the compress), part 2 the rank-sized rest
         for (int c : elim)
-          if (m[c] <= pmax && (wide || m[c] + (int)std::ceil(rho_pred * m[c]) > pmax)) {
+          if ((m[c] <= pmax && (wide || m[c] + (int)std::ceil(rho_pred * m[c]) > pmax)) || (sym && m[c] > pmax)) {
             s_off[c] = stot2;
             stot2 += (sym ? 1 : 2) * (int64_t)m[c] * m[c];   // LU: L11^{-1} and U11^{-T}
           }
         if (stot2 > 0) {
           h->ws_S.ensure(stot2 * 8 + 256, st);
           for (int c : elim)
-            if (s_off[c] >= 0) s_max = std::max(s_max, m[c]);   // launch shape of the whole wave
+            if (s_off[c] >= 0 && m[c] <= pmax) s_max = std::max(s_max, m[c]);   // launch shape of the whole wave
           for (int c : elim) {
             if (s_off[c] < 0 || !own(c)) continue;
             const SymNode &nd = lv.node[c];
@@ -1671,8 +1742,13 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
             t.mode = 0;
             t.alpha = 1.0;
             s_ct.push_back(t);
-            s_pt.push_back(PivTask{h->ws_S.as<double>() + s_off[c], m[c], m[c], 0, c});
+            if (m[c] <= pmax) s_pt.push_back(PivTask{h->ws_S.as<double>() + s_off[c], m[c], m[c], 0, c});
+            else s_big.push_back(PivTask{h->ws_S.as<double>() + s_off[c], m[c], m[c], 0, c});
             ++h->split_nodes;
+          }
+          if (!s_big.empty()) {
+            h->ws_piv2.ensure(blocked_ws_bytes(s_big), st);
+            build_blocked_plan(s_big, h->ws_piv2.as<double>(), s_plan);
           }
           CK(cudaEventRecord(h->ev_s0, st));   // S is final here; stream2 starts after it
         }
@@ -1680,16 +1756,21 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       split_copies(s_ct);
       // part 1 is enqueued on stream2 once the compress kernels are queued
       auto enqueue_split_part1 = [&]() {
-        if (s_pt.empty()) return;
+        if (s_pt.empty() && s_big.empty()) return;
         CK(cudaStreamWaitEvent(h->stream2, h->ev_s0, 0));
         const CopyTask *dct;
         const PivTask *dpt;
+        const char *dplan = nullptr;
         if (capture) {   // descriptors resident in the graph's buffer
           dct = static_cast<const CopyTask *>(h->stg.push_deferred(s_ct.data(), s_ct.size() * sizeof(CopyTask), st));
           dpt = static_cast<const PivTask *>(h->stg.push_deferred(s_pt.data(), s_pt.size() * sizeof(PivTask), st));
+          if (!s_big.empty())
+            dplan = static_cast<const char *>(h->stg.push_deferred(s_plan.blob.data(), s_plan.blob.size(), st));
         } else {
           if (h->s1_pending) CK(cudaEventSynchronize(h->ev_s1));   // pinned task buffer reuse
-          const size_t nbytes = s_ct.size() * sizeof(CopyTask) + s_pt.size() * sizeof(PivTask);
+          const size_t n0 = s_ct.size() * sizeof(CopyTask) + s_pt.size() * sizeof(PivTask);
+          const size_t poff = (n0 + 255) & ~size_t(255);
+          const size_t nbytes = poff + s_plan.blob.size();
           if (h->h_sp_cap < nbytes) {
             if (h->h_sp) CK(cudaFreeHost(h->h_sp));
             h->h_sp_cap = std::max<size_t>(nbytes * 2, 1 << 16);
@@ -1698,13 +1779,17 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           char *hb = reinterpret_cast<char *>(h->h_sp);
           std::memcpy(hb, s_ct.data(), s_ct.size() * sizeof(CopyTask));
           std::memcpy(hb + s_ct.size() * sizeof(CopyTask), s_pt.data(), s_pt.size() * sizeof(PivTask));
+          if (!s_plan.blob.empty()) std::memcpy(hb + poff, s_plan.blob.data(), s_plan.blob.size());
           h->d_sp.ensure(nbytes + 64, st);
           CK(cudaMemcpyAsync(h->d_sp.p, hb, nbytes, cudaMemcpyHostToDevice, h->stream2));
           dct = h->d_sp.as<CopyTask>();
           dpt = reinterpret_cast<const PivTask *>(h->d_sp.as<char>() + s_ct.size() * sizeof(CopyTask));
+          dplan = h->d_sp.as<char>() + poff;
         }
         launch_k(k_copy, (unsigned)s_ct.size(), 256, 0, h->stream2, dct);
-        if (sym) {
+        if (!s_big.empty()) run_blocked_plan(h, s_plan, dplan, h->ws_piv2.as<double>(), h->stream2);
+        if (s_pt.empty()) {
+        } else if (sym) {
           const size_t smem = pivb_smem_bytes(s_max);
           launch_k(k_pivot_blk, (unsigned)s_pt.size(), 512, smem, h->stream2, dpt, h->d_status.as<int>());
         } else {   // no-pivot LU of S: L11^{-1} and U11^{-T} side by side in ws_S
@@ -3718,6 +3803,29 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     EigTask *de;
     CK(cudaMalloc(&de, sizeof(EigTask)));
     CK(cudaMemcpy(de, &e, sizeof(EigTask), cudaMemcpyHostToDevice));
+    if (m <= 64 && getenv("LORASP_EIG_SMALL")) {
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0);
+      if (m <= 32) k_eig_small<1><<<1, 128, eig_small_smem_bytes(1)>>>(de, eps, dst);
+      else k_eig_small<2><<<1, 256, eig_small_smem_bytes(2)>>>(de, eps, dst);
+      cudaEventRecord(e1);
+      if (ddbg) {
+        float ms = 0;
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        fprintf(stderr, "[k_eig_small m=%d] %.1f us\n", m, 1e3 * ms);
+        long long hp[16 + 64];
+        CK(cudaMemcpy(hp, ddbg, sizeof(hp), cudaMemcpyDeviceToHost));
+        for (int w = 0; w < (m <= 32 ? 4 : 8); ++w)
+          fprintf(stderr, "   [es] warp %d per step: matvec %.0f bar1 %.0f p+pv %.0f update %.0f formv %.0f bar2 %.0f\n", w,
+                  hp[16 + w * 8] / (m - 2.0), hp[17 + w * 8] / (m - 2.0), hp[18 + w * 8] / (m - 2.0),
+                  hp[19 + w * 8] / (m - 2.0), hp[20 + w * 8] / (m - 2.0), hp[21 + w * 8] / (m - 2.0));
+      }
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    } else
     if (m <= EIGW_M && !getenv("LORASP_EIG_GENERIC")) {   // the production path for m <= 32
       k_eig_warp<<<1, 32, EIGW_SMEM_DOUBLES * sizeof(double)>>>(de, eps, dst);
     } else {
@@ -3769,13 +3877,22 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
         cudaEventRecord(e0);
         launch_tridiag_cl(0, de, 1, eig_cl_class(m), eps);
         cudaEventRecord(e1);
-        launch_pre_post(0, de, 1, m, eps, dst);
+        cudaEvent_t pev[4];
+        for (auto &x : pev) cudaEventCreate(&x);
+        launch_pre_post(0, de, 1, m, eps, dst, ddbg ? pev : nullptr);
+        cudaEventRecord(pev[3]);
         if (ddbg) {
-          float ms = 0;
-          cudaEventSynchronize(e1);
+          float ms = 0, a = 0, b = 0, c = 0, d = 0;
+          cudaEventSynchronize(pev[3]);
           cudaEventElapsedTime(&ms, e0, e1);
-          fprintf(stderr, "[k_tridiag_cl m=%d class %d] %.1f us\n", m, eig_cl_class(m), 1e3 * ms);
+          cudaEventElapsedTime(&a, e1, pev[0]);
+          cudaEventElapsedTime(&b, pev[0], pev[1]);
+          cudaEventElapsedTime(&c, pev[1], pev[2]);
+          cudaEventElapsedTime(&d, pev[2], pev[3]);
+          fprintf(stderr, "[k_tridiag_cl m=%d class %d] %.1f us | eigvals %.1f invit %.1f orth %.1f backtr %.1f us\n", m,
+                  eig_cl_class(m), 1e3 * ms, 1e3 * a, 1e3 * b, 1e3 * c, 1e3 * d);
         }
+        for (auto &x : pev) cudaEventDestroy(x);
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
       } else {
@@ -3967,6 +4084,7 @@ void lorasp_destroy(lorasp_handle h) {
     h->ws_S.release();
     h->ws_Y.release();
     h->ws_T1.release();
+    h->ws_piv2.release();
     h->d_sp.release();
     h->d_apparts.release();
     h->d_upart.release();

@@ -197,7 +197,7 @@ int main() {
   cudaMalloc(&c, 8);
   cudaMemcpy(dd, hd, 1024, cudaMemcpyHostToDevice);
   cudaMemcpy(de, he, 1024, cudaMemcpyHostToDevice);
-  for (int v = 0; v < 6; ++v) {
+  for (int v = 0; v < 8; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       if (v == 0) k<0><<<1, 256>>>(dd, de, m, rounds, o, c);
       if (v == 1) k<1><<<1, 256>>>(dd, de, m, rounds, o, c);
@@ -205,6 +205,8 @@ int main() {
       if (v == 3) k<3><<<1, 256>>>(dd, de, m, rounds, o, c);
       if (v == 4) k<4><<<1, 256>>>(dd, de, m, rounds, o, c);
       if (v == 5) k<0><<<1, 128>>>(dd, de, m, rounds, o, c);
+      if (v == 6) k<0><<<1, 32>>>(dd, de, m, rounds, o, c);
+      if (v == 7) k<1><<<1, 32>>>(dd, de, m, rounds, o, c);
     }
     cudaDeviceSynchronize();
     cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);
