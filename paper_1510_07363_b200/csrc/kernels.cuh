@@ -403,36 +403,69 @@ __device__ __forceinline__ int sturm_count(const double *__restrict__ d, const d
   // Number of eigenvalues of T below x: sign changes of the leading principal
   // minors p_i = (d_i - x) p_{i-1} - e_{i-1}^2 p_{i-2}, i.e. negative pivots
   // q_i = p_i / p_{i-1} of the LDL^T count, evaluated without divisions.  T is
-  // pre-scaled to |d|, |e| <= 1, so |p| grows at most 3x per step; the pair
-  // (p0, p1) is renormalised by a power of two every 8 steps.  d / e2 are
+  // pre-scaled to |d|, |e| <= 1, so |p| grows at most 3x per step.  The
+  // sequence is renormalised by a power of two once per 8 steps, the factor
+  // taken from the minors two steps before the block end and folded into the
+  // next block's first two coefficients: the dependent chain is one DFMA per
+  // step (an isolated zero minor counts correctly as it stands).  d / e2 are
   // padded to a multiple of 8 with d = 4, e2 = 0 (no sign change for x < 4).
-  // An exact zero minor (x an eigenvalue of a leading block) is detected off
-  // the dependency chain and the count is redone at the next double above x.
+  // Two consecutive zero minors (a split of T with x an eigenvalue of the
+  // leading block) would stop the count: then it is redone at the next double.
+  // Warps issue in order, so nothing that reads p_i may sit between its DFMA
+  // and the next step's: the sign change of the pair (p_{i-2}, p_{i-1}) is
+  // counted while p_i is in flight, and the next block's d / e2 are loaded
+  // during the current block (measured 17 vs 36 cycles per step on one warp,
+  // tools/micro/sturm_chain.cu).
   (void)pivmin;
-  const double *e2m = e2 - 1;
   for (int attempt = 0; attempt < 4; ++attempt) {
-    double p0 = 1.0, p1 = 1.0;
+    double pa = 1.0, pb = 1.0, s = 1.0;   // p_{i-2}, p_{i-1}, scale of this block
     int c = 0;
-    bool zero = false;
+    bool dead = false;
+    double nd[8], ne[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      nd[u] = d[u];
+      ne[u] = (u == 0) ? 0.0 : e2[u - 1];
+    }
     for (int i0 = 0; i0 < m; i0 += 8) {
+      double dx[8], ee[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int i = i0 + u;
-        const double ee = (i == 0) ? 0.0 : e2m[i];
-        const double p2 = fma(d[i] - x, p1, -ee * p0);
-        const long long b2 = __double_as_longlong(p2), b1 = __double_as_longlong(p1);
-        zero |= (b2 << 1) == 0;                 // +-0
-        c += (int)((unsigned long long)(b2 ^ b1) >> 63);   // sign change
-        p0 = p1;
-        p1 = p2;
+        dx[u] = nd[u] - x;
+        ee[u] = ne[u];
       }
-      const double a = fmax(fabs(p0), fabs(p1));
-      const long long ex = ((__double_as_longlong(a) >> 52) & 0x7ff) - 1023;
-      const double sc = __longlong_as_double((long long)(1023 - ex) << 52);
-      p0 *= sc;
-      p1 *= sc;
+      {   // unconditional (no control flow around the loop-carried registers):
+          // past the last block, block 0 is reloaded and not used
+        const int base = (i0 + 8 < m) ? i0 + 8 : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int ie = base + u - 1;
+          nd[u] = d[base + u];
+          const double t = e2[ie < 0 ? 0 : ie];
+          ne[u] = (ie < 0) ? 0.0 : t;
+        }
+      }
+      dx[0] *= s;
+      ee[0] *= s;
+      ee[1] *= s;
+      double sn = 1.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double p = fma(dx[u], pb, -ee[u] * pa);
+        c += (int)(((unsigned)__double2hiint(pa) ^ (unsigned)__double2hiint(pb)) >> 31);
+        pa = pb;
+        pb = p;
+        if (u == 5) {   // 2^(-exponent of max(|p_{i0+4}|, |p_{i0+5}|)) for the next block
+          const double amax = fmax(fabs(pa), fabs(pb));
+          const int ex = (__double2hiint(amax) >> 20) & 0x7ff;
+          sn = __hiloint2double((2046 - ex) << 20, 0);
+        }
+      }
+      dead |= (pa == 0.0) && (pb == 0.0);
+      s = sn;
     }
-    if (!zero) return c;
+    c += (int)(((unsigned)__double2hiint(pa) ^ (unsigned)__double2hiint(pb)) >> 31);
+    if (!dead) return c;
     x = nextafter(x, 1e300);
   }
   return 0;
@@ -492,7 +525,7 @@ __device__ __forceinline__ void grp_multisect(const double *d, const double *e2,
       const int c = sturm_count(d, e2, m, x, pivmin);
       const unsigned bal = __ballot_sync(0xffffffffu, c > j);
       if (!done) {
-        const unsigned gb = (bal >> (g * EG)) & ((1u << EG) - 1u);
+        const unsigned gb = (EG == 32) ? bal : ((bal >> (g * EG)) & ((1u << (EG & 31)) - 1u));
         if (gb == 0) {
           lo = fma(hi - lo, (double)EG * STEP, lo);
         } else {

@@ -37,7 +37,6 @@
 
 #include "internal.h"
 #include "kernels.cuh"
-#include "eig_small.cuh"
 #include "lorasp.h"
 
 namespace lorasp {
@@ -634,8 +633,6 @@ static void set_eig_attrs() {
   CK(cudaFuncSetAttribute(k_eig_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(EIGW_SMEM_DOUBLES * sizeof(double))));
   CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-  CK(cudaFuncSetAttribute(k_eig_small<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_small_smem_bytes(1)));
-  CK(cudaFuncSetAttribute(k_eig_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)eig_small_smem_bytes(2)));
   CK(cudaFuncSetAttribute(k_eig_t<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_tridiag_cl<8, 4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 8 * 8));
   CK(cudaFuncSetAttribute(k_tridiag_cl<12, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 12 * 8));
@@ -3803,29 +3800,6 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     EigTask *de;
     CK(cudaMalloc(&de, sizeof(EigTask)));
     CK(cudaMemcpy(de, &e, sizeof(EigTask), cudaMemcpyHostToDevice));
-    if (m <= 64 && getenv("LORASP_EIG_SMALL")) {
-      cudaEvent_t e0, e1;
-      cudaEventCreate(&e0);
-      cudaEventCreate(&e1);
-      cudaEventRecord(e0);
-      if (m <= 32) k_eig_small<1><<<1, 128, eig_small_smem_bytes(1)>>>(de, eps, dst);
-      else k_eig_small<2><<<1, 256, eig_small_smem_bytes(2)>>>(de, eps, dst);
-      cudaEventRecord(e1);
-      if (ddbg) {
-        float ms = 0;
-        cudaEventSynchronize(e1);
-        cudaEventElapsedTime(&ms, e0, e1);
-        fprintf(stderr, "[k_eig_small m=%d] %.1f us\n", m, 1e3 * ms);
-        long long hp[16 + 64];
-        CK(cudaMemcpy(hp, ddbg, sizeof(hp), cudaMemcpyDeviceToHost));
-        for (int w = 0; w < (m <= 32 ? 4 : 8); ++w)
-          fprintf(stderr, "   [es] warp %d per step: matvec %.0f bar1 %.0f p+pv %.0f update %.0f formv %.0f bar2 %.0f\n", w,
-                  hp[16 + w * 8] / (m - 2.0), hp[17 + w * 8] / (m - 2.0), hp[18 + w * 8] / (m - 2.0),
-                  hp[19 + w * 8] / (m - 2.0), hp[20 + w * 8] / (m - 2.0), hp[21 + w * 8] / (m - 2.0));
-      }
-      cudaEventDestroy(e0);
-      cudaEventDestroy(e1);
-    } else
     if (m <= EIGW_M && !getenv("LORASP_EIG_GENERIC")) {   // the production path for m <= 32
       k_eig_warp<<<1, 32, EIGW_SMEM_DOUBLES * sizeof(double)>>>(de, eps, dst);
     } else {
