@@ -1171,8 +1171,9 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
   if (!small.empty()) {
     PivTask *dp = push(h, small);
     if (max_n <= PIVW_MAXN) {   // one warp per node
-      launch_k(k_pivot_warp, (unsigned)((small.size() + PIVW_WARPS - 1) / PIVW_WARPS), 32 * PIVW_WARPS, 0, st, (const PivTask *)dp, (int)small.size(),
-               h->d_status.as<int>());
+      constexpr int W = PivW<1>::WARPS;
+      launch_k(k_pivot_warp<1>, (unsigned)((small.size() + W - 1) / W), 32 * W, PivW<1>::SMEM, st, (const PivTask *)dp,
+               (int)small.size(), h->d_status.as<int>());
     } else if (max_n <= PIVB_MAXN) {
       const size_t sm = pivb_smem_bytes(max_n);
       launch_k(k_pivot_blk, (unsigned)small.size(), 512, sm, st, dp, h->d_status.as<int>());
@@ -1212,8 +1213,9 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
   PivTask *dp = push(h, h->lu_pivot ? pvp : pv);
   int ev = tbeg(h, K_PIVOT);
   if (max_n <= PIVW_MAXN && !h->lu_pivot) {   // one warp per node
-    launch_k(k_pivot_lu_warp, (unsigned)((pv.size() + PIVW_WARPS - 1) / PIVW_WARPS), 32 * PIVW_WARPS, 0, h->stream, (const PivTask *)dp, (int)pv.size(),
-             h->d_status.as<int>());
+    constexpr int W = PivW<1>::WARPS;
+    launch_k(k_pivot_lu_warp<1>, (unsigned)((pv.size() + W - 1) / W), 32 * W, PivW<1>::SMEM, h->stream,
+             (const PivTask *)dp, (int)pv.size(), h->d_status.as<int>());
   } else if (max_n <= PIVLU_MAXN && !h->lu_pivot) {
     const size_t sm = pivb_smem_bytes(max_n);
     launch_k(k_pivot_lu_blk, (unsigned)pv.size(), 512, sm, h->stream, dp, h->d_status.as<int>());
@@ -3989,7 +3991,7 @@ int lorasp_test_pivot(int device, double *K, int m, int r) {
     CK(cudaMalloc(&dt, sizeof(PivTask)));
     CK(cudaMemcpy(dt, &t, sizeof(PivTask), cudaMemcpyHostToDevice));
     if (n <= PIVW_MAXN) {   // the production kernel for n <= 32
-      k_pivot_warp<<<1, 32 * PIVW_WARPS>>>(dt, 1, dst);
+      k_pivot_warp<1><<<1, 32 * PivW<1>::WARPS, PivW<1>::SMEM>>>(dt, 1, dst);
     } else if (n <= PIVB_MAXN) {
       CK(cudaFuncSetAttribute(k_pivot_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024));
       k_pivot_blk<<<1, 512, pivb_smem_bytes(n)>>>(dt, dst);
