@@ -1691,6 +1691,13 @@ __global__ void __launch_bounds__(512, 1) k_tridiag_cl(const EigTask *__restrict
   }
   cl.sync();
   if (m > 2) pull_v(0);
+  // column k+1 as of A_k, published by its owner warp with the partials: every
+  // CTA then applies update k to it and forms v_{k+1} itself (the same
+  // arithmetic on the same data in every CTA, so bitwise the same v), which
+  // leaves one cluster barrier per step instead of two plus a pull of v
+  double *colg = vg + 2 * (MMAX + 8);    // [2][MMAX] published column
+  double *colp = pcta;                   // updated column k+1 (shared)
+  __shared__ double s_red2[16];
   if (prof && threadIdx.x == 0 && blockIdx.x == 0) pc = clock64();
   for (int k = 0; k < m - 2; ++k) {
     const double *vs = vbuf[k & 1];
@@ -1705,7 +1712,7 @@ __global__ void __launch_bounds__(512, 1) k_tridiag_cl(const EigTask *__restrict
         double c = a[q][0];
 #pragma unroll
         for (int u = 1; u < UC; ++u) c = (u1 == u) ? a[q][u] : c;
-        colbuf[32 * q + lane] = c;
+        colg[(k & 1) * MMAX + 32 * q + lane] = c;
       }
     }
     const bool wact = c0 + UC - 1 > k;
@@ -1741,10 +1748,12 @@ __global__ void __launch_bounds__(512, 1) k_tridiag_cl(const EigTask *__restrict
     cl.sync();
     TCL_PROF(3)
     // ---- C ----
+    double colr = 0.0;   // column k+1 (as of A_k), row tid
     if (tid < MMAX) {
       double pj[CL];
 #pragma unroll
       for (int j = 0; j < CL; ++j) pj[j] = __ldcg(xg + ((k & 1) * CL + j) * MMAX + tid);
+      if (k1 < m - 2) colr = __ldcg(colg + (k & 1) * MMAX + tid);
       double sacc = 0.0;
 #pragma unroll
       for (int j = 0; j < CL; ++j) sacc += pj[j];
@@ -1776,24 +1785,49 @@ __global__ void __launch_bounds__(512, 1) k_tridiag_cl(const EigTask *__restrict
           if (32 * q + 31 > k) a[q][u] = fma(-vq[q], wcu, fma(-wq[q], vcu, a[q][u]));
       }
     }
-    if (own1) {
-      const int wo = (k1 - rank * CW) / UC;
-      if (warp == (wo >= 1 ? 0 : 15)) {
-        const double vcu = vs[k1], wcu = fma(alpha, vcu, psm[k1]);
-        double col[QR];
-#pragma unroll
-        for (int q = 0; q < QR; ++q) {
-          const double vq = vs[32 * q + lane], wq = fma(alpha, vq, psm[32 * q + lane]);
-          col[q] = fma(-vq, wcu, fma(-wq, vcu, colbuf[32 * q + lane]));
-        }
-        form_v(k1, col);
-      }
-    }
     TCL_PROF(5)
-    cl.sync();
+    // ---- E: v_{k+1} in every CTA ----
+    if (k1 < m - 2) {
+      const double vcu = vs[k1], wcu = fma(alpha, vcu, psm[k1]);
+      double s2p = 0.0;
+      if (tid < MMAX) {
+        const double vq = vs[tid], wq = fma(alpha, vq, psm[tid]);
+        const double cu = fma(-vq, wcu, fma(-wq, vcu, colr));
+        colp[tid] = cu;
+        if (tid >= k1 + 2 && tid < m) s2p = cu * cu;
+      }
+      s2p = warp_sum(s2p);
+      if (lane == 0) s_red2[warp] = s2p;
+      __syncthreads();
+      double s2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < MMAX / 32; ++w) s2 += s_red2[w];
+      const int rx = k1 + 1;
+      const double x0 = colp[rx];
+      double beta = x0, scal = 0.0, tk1 = 0.0;
+      if (s2 != 0.0) {
+        beta = -copysign(sqrt(fma(x0, x0, s2)), x0);
+        tk1 = (beta - x0) * frcp(beta);
+        scal = frcp(x0 - beta);
+      }
+      const int b = k1 & 1;
+      if (tid < MMAX) {
+        const int r = tid;
+        double v = 0.0;
+        if (s2 != 0.0) v = (r == rx) ? 1.0 : ((r > rx && r < m) ? colp[r] * scal : 0.0);
+        vbuf[b][r] = v;
+        if (rank == 0 && r > k1 && r < m) A[refl_off(k1, m) + r] = v;
+      }
+      if (tid == 0) {
+        taub[b] = tk1;
+        if (rank == 0) {
+          out[2 * m + k1] = tk1;
+          out[m + k1] = beta;
+        }
+      }
+      __syncthreads();
+    }
     TCL_PROF(6)
-    if (k1 < m - 2) pull_v(k1);
-    TCL_PROF(7)
   }
   if (prof && threadIdx.x == 0 && blockIdx.x == 0)
     for (int q = 0; q < 8; ++q) prof[q] = pt[q];
