@@ -15,7 +15,7 @@
 //    k_tridiag_cl     the same over a thread-block cluster, 128 < m <= 512
 //    k_eig_t          eigenvalues (Sturm multisection), inverse iteration, MGS,
 //                     back-transformation (generic m or after the kernels above)
-//    k_invit_multi / k_orth_cl / k_backtr_multi   the same steps split over CTAs
+//    k_invit_multi / k_orth_bgs / k_backtr_multi   the same steps split over CTAs
 //                     for 128 < m <= 512 (ranks ~0.6 m there)
 //  Fused (s, b) pivot (P:l.396-399, P:l.101-106):
 //    k_pivot_blk      signed Cholesky K = L diag(I_m, -I_r) L^T + L^{-1}, n <= 160
@@ -1561,16 +1561,18 @@ __device__ __forceinline__ void dsm_st(uint32_t a, double v) {
 // CTA j holds the column strip [16 UC j, 16 UC (j+1)) in registers (thread
 // (warp w, lane) owns a[q][u] = G(32 q + lane, 16 UC j + UC w + u)).  Per
 // step k:
-//   A  every active warp forms partial row sums of A v_k over its UC columns
-//      (finished tiles, all columns or all 32 rows <= k, are exact zeros and
-//      skipped); the owner warp of column k+1 publishes that column;
-//   B  block barrier, the CTA's partial (A v)_t, t < m (16-term tree);
-//   C  cluster barrier, p_t = tau_k sum_j pcta_j[t] read from every CTA in the
-//      same order (identical on all CTAs), masked to t > k; p.v reduced;
-//   D  rank-2 update of the strip; in the CTA owning column k+1 a warp whose
-//      columns are finished forms v_{k+1} (same update formula on the
-//      published column) and pushes v, tau to every CTA; cluster barrier.
-// Same numerics as k_tridiag_reg; output in the same tridiagonal record.
+//   A  every active warp forms p_c = (A v_k)_c for its UC columns as column
+//      dots (A symmetric), rows over the lanes, finished 32-row tiles skipped,
+//      and writes them to the L2 exchange (the strips partition the columns,
+//      so p is gathered, not summed); the owner warp of column k+1 publishes
+//      that column;
+//   C  cluster barrier; p_t = tau_k (A v)_t read by every CTA, masked to t > k;
+//      p.v reduced in the same order everywhere;
+//   D  rank-2 update of the strip;
+//   E  every CTA applies update k to the published column k+1 and forms
+//      v_{k+1} and tau_{k+1} itself (the same arithmetic on the same data in
+//      every CTA, so bitwise the same); one cluster barrier per step.
+// Output in the same tridiagonal record as k_tridiag_reg.
 // Dynamic shared memory: 21 * 32 QR doubles.
 template <int QR, int UC, int CL>
 __global__ void __launch_bounds__(512, 1) k_tridiag_cl(const EigTask *__restrict__ tasks, double eps,
@@ -1587,10 +1589,9 @@ __global__ void __launch_bounds__(512, 1) k_tridiag_cl(const EigTask *__restrict
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
-  // dynamic shared memory: vbuf[2][MMAX] | ps_part[16][MMAX] | pcta | psm | colbuf
+  // dynamic shared memory: vbuf[2][MMAX] | (unused 16 MMAX) | pcta | psm | colbuf
   extern __shared__ double dsh[];
   double(*vbuf)[MMAX] = reinterpret_cast<double(*)[MMAX]>(dsh);
-  double(*ps_part)[MMAX] = reinterpret_cast<double(*)[MMAX]>(dsh + 2 * MMAX);
   double *pcta = dsh + 18 * MMAX, *psm = dsh + 19 * MMAX, *colbuf = dsh + 20 * MMAX;
   __shared__ double taub[2];
   __shared__ double s_red[16];
@@ -1604,7 +1605,7 @@ __global__ void __launch_bounds__(512, 1) k_tridiag_cl(const EigTask *__restrict
   // Exchanges go through L2 (global scratch at work[0..), free in this path):
   // DSMEM serves ~1 thread-request per cycle per SM, too slow for the
   // all-gather of CL partial vectors; coalesced L2 traffic is not.
-  double *xg = t.work;                                  // [2][CL][MMAX] partials of A v
+  double *xg = t.work;                                  // [2][MMAX] p = A v (all-gather)
   double *vg = t.work + 2 * CL * MMAX;                  // [2][MMAX + 8] v and tau
   double a[QR][UC];
 #pragma unroll
@@ -1717,46 +1718,35 @@ __global__ void __launch_bounds__(512, 1) k_tridiag_cl(const EigTask *__restrict
     }
     const bool wact = c0 + UC - 1 > k;
     if (wact) {
-      double vc[UC];
+      // (A v)_c for the warp's columns c as column dots (A symmetric: column c
+      // = row c), rows over the lanes: no cross-warp partials to combine, the
+      // cluster exchanges the MMAX entries of p once (all-gather through L2)
+      double s[UC];
 #pragma unroll
-      for (int u = 0; u < UC; ++u) vc[u] = (c0 + u < MMAX) ? vs[c0 + u] : 0.0;
+      for (int u = 0; u < UC; ++u) s[u] = 0.0;
 #pragma unroll
       for (int q = 0; q < QR; ++q) {
         if (32 * q + 31 <= k) continue;
-        double s0 = 0;
+        const double vr = vs[32 * q + lane];
 #pragma unroll
-        for (int u = 0; u < UC; ++u) s0 = fma(a[q][u], vc[u], s0);
-        ps_part[warp][32 * q + lane] = s0;
+        for (int u = 0; u < UC; ++u) s[u] = fma(a[q][u], vr, s[u]);
       }
-    } else {
+      warp_sum_multi<UC>(s);
+      double pl = s[0];
 #pragma unroll
-      for (int q = 0; q < QR; ++q) ps_part[warp][32 * q + lane] = 0.0;
+      for (int u = 1; u < UC; ++u) pl = (lane == u) ? s[u] : pl;
+      if (lane < UC) xg[(k & 1) * MMAX + c0 + lane] = pl;
     }
     TCL_PROF(0)
-    __syncthreads();
     TCL_PROF(1)
-    // ---- B ----
-    for (int r = tid; r < MMAX; r += blockDim.x) {
-      double h[8];
-#pragma unroll
-      for (int w = 0; w < 8; ++w) h[w] = ps_part[w][r] + ps_part[w + 8][r];
-#pragma unroll
-      for (int w = 0; w < 4; ++w) h[w] += h[w + 4];
-      xg[((k & 1) * CL + rank) * MMAX + r] = (h[0] + h[2]) + (h[1] + h[3]);
-    }
     TCL_PROF(2)
     cl.sync();
     TCL_PROF(3)
     // ---- C ----
     double colr = 0.0;   // column k+1 (as of A_k), row tid
     if (tid < MMAX) {
-      double pj[CL];
-#pragma unroll
-      for (int j = 0; j < CL; ++j) pj[j] = __ldcg(xg + ((k & 1) * CL + j) * MMAX + tid);
+      const double sacc = __ldcg(xg + (k & 1) * MMAX + tid);
       if (k1 < m - 2) colr = __ldcg(colg + (k & 1) * MMAX + tid);
-      double sacc = 0.0;
-#pragma unroll
-      for (int j = 0; j < CL; ++j) sacc += pj[j];
       const double pi = (tid > k && tid < m) ? tk * sacc : 0.0;
       psm[tid] = pi;
       const double pvw = warp_sum(pi * vs[tid]);
@@ -1806,7 +1796,8 @@ __global__ void __launch_bounds__(512, 1) k_tridiag_cl(const EigTask *__restrict
       const double x0 = colp[rx];
       double beta = x0, scal = 0.0, tk1 = 0.0;
       if (s2 != 0.0) {
-        beta = -copysign(sqrt(fma(x0, x0, s2)), x0);
+        const double nrm2 = fma(x0, x0, s2);
+        beta = -copysign(nrm2 * frsqrt(nrm2), x0);
         tk1 = (beta - x0) * frcp(beta);
         scal = frcp(x0 - beta);
       }
@@ -2026,7 +2017,7 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
   if constexpr (PRE) {
     // PRE pipeline stage 0 ends here: the kept eigenvalues and ||T|| bound go to
     // the tridiagonal record for k_invit_multi; MGS + back-transformation follow
-    // in k_orth_cl / k_backtr_multi.
+    // in k_orth_bgs / k_backtr_multi.
     double *rec = t.work + 6 * (int64_t)m * m;
     for (int k = tid; k < r; k += blockDim.x) rec[rec_lam_off(m) + k] = lam[k];
     if (tid == 0) rec[3 * m + 1] = bnorm;
@@ -2280,56 +2271,256 @@ __global__ void __launch_bounds__(256) k_invit_multi(const EigTask *__restrict__
   }
 }
 
-// MGS of the r inverse-iteration vectors over a thread-block cluster of CL
-// CTAs: CTA c keeps vectors [c rb, (c+1) rb) in shared memory (rb = ceil(r/CL),
-// column stride m | 1).  Step k: the CTA holding z_k normalises it and writes it
-// to a global exchange slot (double-buffered, L2); one cluster barrier; every
-// CTA reads z_k and removes it from its later vectors (warps over vectors).
-// The vectors stay on chip: a single CTA streaming them through L2 each step is
-// bound by that SM's L2 bandwidth.  Dynamic shared memory: rb (m|1) + m doubles.
-template <int CL>
-__global__ void __launch_bounds__(512, 1) k_orth_cl(const EigTask *__restrict__ tasks) {
+// Block Gram-Schmidt of the r inverse-iteration vectors over a cluster of CL
+// CTAs (round 1: MGS with one cluster barrier per vector): CTA c
+// owns the panel of vectors [c rb, (c+1) rb) (rb = ceil(r / CL) <= 32), two
+// per warp, in registers (lane's rows 32 q + lane).  For c = 0 .. CL-1:
+//   CTA c orthonormalises its panel by MGS inside the CTA (pivot vector l in
+//   warp l mod 16, broadcast through shared memory: two block barriers per
+//   vector), writing the final vectors to V; one cluster barrier; every later
+//   CTA stages panel c from L2 and removes it from its own vectors (block
+//   classical Gram-Schmidt, 8 columns per warp reduction).
+// Selective reorthogonalisation (Kahan-Parlett): a pivot whose norm fell below
+// 1/sqrt(2) of its norm as produced by inverse iteration is projected once more
+// against every earlier final vector (all 16 warps, partial corrections
+// summed in shared memory) before it is normalised; so clusters of close
+// eigenvalues, whose inverse-iteration vectors are nearly parallel, still come
+// out orthonormal to working precision (single-pass MGS lost up to 1e-7 there).
+// Dynamic shared memory: 32 (m|1) staging + 2 x 512 pivot + 512 + 16 x 512
+// partial corrections (doubles) at the QM class's maximum m.
+template <int QM>
+constexpr int orth_bgs_smem_doubles() {
+  return 32 * (32 * QM + 1) + 2 * 32 * QM + 32 * QM + 16 * 32 * QM;
+}
+template <int QM, int CL>
+__global__ void __launch_bounds__(512, 1) k_orth_bgs(const EigTask *__restrict__ tasks) {
   extern __shared__ double sh[];
+  __shared__ int s_flag[2];
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
+  constexpr int MX = 32 * QM;
   const int rank = (int)cl.block_rank();
   const EigTask t = tasks[blockIdx.x / CL];
   const int m = t.m, r = *t.rank_out;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int rb = (r + CL - 1) / CL, j0 = rank * rb, j1 = min(r, j0 + rb);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (r <= 0) return;   // uniform over the cluster
+  const int rb = (r + CL - 1) / CL, j0 = rank * rb, nown = max(0, min(r, j0 + rb) - j0);
   const int ldz = m | 1;
-  double *Z = sh, *zk = sh + (int64_t)rb * ldz;
-  double *xg = t.work;   // exchange: [2][m] (the work scratch is free after inverse iteration)
-  for (int j = j0 + warp; j < j1; j += nw)
-    for (int i = lane; i < m; i += 32) Z[(int64_t)(j - j0) * ldz + i] = t.V[(int64_t)j * m + i];
-  __syncthreads();
-  for (int k = 0; k < r; ++k) {
-    double *slot = xg + (int64_t)(k & 1) * m;
-    if (k >= j0 && k < j1 && warp == 0) {
-      double *zc = Z + (int64_t)(k - j0) * ldz;
-      double s2 = 0;
-      for (int i = lane; i < m; i += 32) s2 = fma(zc[i], zc[i], s2);
-      const double inv = frcp(sqrt(warp_sum(s2)));
-      for (int i = lane; i < m; i += 32) {
-        const double v = zc[i] * inv;
-        zc[i] = v;
-        slot[i] = v;
+  double *stage = sh, *pbuf = sh + 32 * (MX + 1), *zks = pbuf + 2 * MX, *red = zks + MX;
+  double *V = t.V;
+  double z[2][QM], n0[2];
+#pragma unroll
+  for (int v = 0; v < 2; ++v) {
+    const int l = warp + 16 * v;
+    double a = 0.0;
+#pragma unroll
+    for (int q = 0; q < QM; ++q) {
+      const int i = 32 * q + lane;
+      z[v][q] = (l < nown && i < m) ? V[(int64_t)(j0 + l) * m + i] : 0.0;
+      a = fma(z[v][q], z[v][q], a);
+    }
+    n0[v] = warp_sum(a);
+  }
+  const bool prof = t.dbg && rank == 1 && threadIdx.x == 0;
+  long long pa[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pc = prof ? clock64() : 0;
+#define OBGS_PROF(i) if (prof) { const long long tn = clock64(); pa[i] += tn - pc; pc = tn; }
+  for (int c = 0; c < CL && c * rb < r; ++c) {
+    if (rank == c) {
+      // n2: the pivot's squared norm, carried from the previous step's update
+      // (||z - s q||^2 = z.z - s^2 from the same warp reduction as s; exact
+      // to ~2u relative while no reorthogonalisation is due, i.e. while
+      // ||z'||^2 >= ||z_0||^2 / 2), so each vector costs one block barrier
+      double n2 = 0.0;
+      if (nown > 0 && warp == 0) {
+        double a = 0.0;
+#pragma unroll
+        for (int q = 0; q < QM; ++q) a = fma(z[0][q], z[0][q], a);
+        n2 = warp_sum(a);
+      }
+      for (int l = 0; l < nown; ++l) {
+        const int pw = l & 15, k = j0 + l;
+        const bool sel = (l >> 4) != 0;
+        double *pb = pbuf + (l & 1) * MX;
+        auto finish = [&]() {   // pivot warp: normalise, publish to the CTA and to V
+          const double inv = n2 > 0.0 ? frsqrt(n2) : 0.0;
+#pragma unroll
+          for (int q = 0; q < QM; ++q) {
+            const int row = 32 * q + lane;
+            double x;
+            if (sel) x = (z[1][q] *= inv);
+            else x = (z[0][q] *= inv);
+            pb[row] = x;
+            if (row < m) V[(int64_t)k * m + row] = x;
+          }
+        };
+        if (warp == pw) {
+          const bool need = n2 < 0.5 * (sel ? n0[1] : n0[0]) && k > 0;
+          if (need) {
+#pragma unroll
+            for (int q = 0; q < QM; ++q) zks[32 * q + lane] = sel ? z[1][q] : z[0][q];
+          } else {
+            finish();
+          }
+          if (lane == 0) s_flag[l & 1] = need;
+        }
+        OBGS_PROF(4)
+        __syncthreads();
+        if (s_flag[l & 1]) {   // uniform: reproject the pivot on every earlier final vector
+          double *corr = red + warp * MX + lane;   // this warp's partial correction
+#pragma unroll
+          for (int q = 0; q < QM; ++q) corr[32 * q] = 0.0;
+          for (int i = warp; i < k; i += 16) {
+            double qv[QM], d = 0.0;
+#pragma unroll
+            for (int q = 0; q < QM; ++q) {
+              const int row = 32 * q + lane;
+              qv[q] = row < m ? __ldcg(V + (int64_t)i * m + row) : 0.0;
+              d = fma(qv[q], zks[row], d);
+            }
+            d = warp_sum(d);
+#pragma unroll
+            for (int q = 0; q < QM; ++q) corr[32 * q] = fma(d, qv[q], corr[32 * q]);
+          }
+          __syncthreads();
+          if (warp == pw) {
+            double a = 0.0;
+#pragma unroll
+            for (int q = 0; q < QM; ++q) {
+              double sacc = 0.0;
+              for (int w = 0; w < 16; ++w) sacc += red[w * MX + 32 * q + lane];
+              if (sel) {
+                z[1][q] -= sacc;
+                a = fma(z[1][q], z[1][q], a);
+              } else {
+                z[0][q] -= sacc;
+                a = fma(z[0][q], z[0][q], a);
+              }
+            }
+            n2 = warp_sum(a);
+            finish();
+          }
+          __syncthreads();
+        }
+        OBGS_PROF(5)
+        // remove the pivot from this CTA's later vectors (only warps holding
+        // one: shuffles are a shared, low-throughput resource); the warp of the
+        // next pivot also forms that vector's new squared norm
+        const int ln = l + 1;
+        const bool nxt = ln < nown && warp == (ln & 15), nsel = (ln >> 4) != 0;
+        const bool u0 = warp > l && warp < nown, u1 = warp + 16 > l && warp + 16 < nown;
+        if (u0 || u1) {
+          double pq[QM], s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int q = 0; q < QM; ++q) {
+            pq[q] = pb[32 * q + lane];
+            s4[0] = fma(pq[q], z[0][q], s4[0]);
+            s4[1] = fma(pq[q], z[1][q], s4[1]);
+          }
+          if (nxt) {
+            double a = 0.0;
+#pragma unroll
+            for (int q = 0; q < QM; ++q) a = fma(nsel ? z[1][q] : z[0][q], nsel ? z[1][q] : z[0][q], a);
+            s4[2] = a;
+          }
+          if (u1) {
+            warp_sum_multi<4>(s4);
+          } else if (nxt) {
+            double s2[2] = {s4[0], s4[2]};
+            warp_sum_multi<2>(s2);
+            s4[0] = s2[0];
+            s4[2] = s2[1];
+          } else {
+            s4[0] = warp_sum(s4[0]);
+          }
+#pragma unroll
+          for (int q = 0; q < QM; ++q) {
+            if (u0) z[0][q] = fma(-s4[0], pq[q], z[0][q]);
+            if (u1) z[1][q] = fma(-s4[1], pq[q], z[1][q]);
+          }
+          if (nxt) {
+            const double sn = nsel ? s4[1] : s4[0];
+            n2 = fma(-sn, sn, s4[2]);
+          }
+        }
+        OBGS_PROF(6)
       }
     }
-    cl.sync();
-    for (int i = tid; i < m; i += blockDim.x) zk[i] = __ldcg(slot + i);
-    __syncthreads();
-    for (int j = max(j0, k + 1) + warp; j < j1; j += nw) {
-      double *zj = Z + (int64_t)(j - j0) * ldz;
-      double sacc = 0;
-      for (int i = lane; i < m; i += 32) sacc = fma(zk[i], zj[i], sacc);
-      sacc = warp_sum(sacc);
-      for (int i = lane; i < m; i += 32) zj[i] = fma(-sacc, zk[i], zj[i]);
+    OBGS_PROF(0)
+    cl.sync();   // panel c final in V, visible to the cluster
+    OBGS_PROF(1)
+    if (rank > c) {
+      const int c0 = c * rb, nc = min(r, c0 + rb) - c0;
+      for (int e = threadIdx.x; e < nc * m; e += blockDim.x) {
+        const int i = e / m, row = e - i * m;
+        stage[i * ldz + row] = __ldcg(V + (int64_t)(c0 + i) * m + row);
+      }
+      __syncthreads();
+      OBGS_PROF(2)
+      const bool has0 = warp < nown, has1 = warp + 16 < nown;
+      if (has0 && !has1) {   // one vector in this warp: 8 columns per reduction
+        for (int i0 = 0; i0 < nc; i0 += 8) {
+          double s8[8];
+#pragma unroll
+          for (int ii = 0; ii < 8; ++ii) {
+            const int i = i0 + ii;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int q = 0; q < QM; ++q) {
+              const int row = 32 * q + lane;
+              const double qv = (i < nc && row < m) ? stage[i * ldz + row] : 0.0;
+              if (q & 1) a1 = fma(qv, z[0][q], a1);
+              else a0 = fma(qv, z[0][q], a0);
+            }
+            s8[ii] = a0 + a1;
+          }
+          warp_sum_multi<8>(s8);
+#pragma unroll
+          for (int ii = 0; ii < 8; ++ii) {
+            const int i = i0 + ii;
+#pragma unroll
+            for (int q = 0; q < QM; ++q) {
+              const int row = 32 * q + lane;
+              const double qv = (i < nc && row < m) ? stage[i * ldz + row] : 0.0;
+              z[0][q] = fma(-s8[ii], qv, z[0][q]);
+            }
+          }
+        }
+      } else if (has1)
+      for (int i0 = 0; i0 < nc; i0 += 8) {
+        double s16[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) s16[u] = 0.0;
+#pragma unroll
+        for (int ii = 0; ii < 8; ++ii) {
+          const int i = i0 + ii;
+#pragma unroll
+          for (int q = 0; q < QM; ++q) {
+            const int row = 32 * q + lane;
+            const double qv = (i < nc && row < m) ? stage[i * ldz + row] : 0.0;
+            s16[ii] = fma(qv, z[0][q], s16[ii]);
+            s16[8 + ii] = fma(qv, z[1][q], s16[8 + ii]);
+          }
+        }
+        warp_sum_multi<16>(s16);
+#pragma unroll
+        for (int ii = 0; ii < 8; ++ii) {
+          const int i = i0 + ii;
+#pragma unroll
+          for (int q = 0; q < QM; ++q) {
+            const int row = 32 * q + lane;
+            const double qv = (i < nc && row < m) ? stage[i * ldz + row] : 0.0;
+            z[0][q] = fma(-s16[ii], qv, z[0][q]);
+            z[1][q] = fma(-s16[8 + ii], qv, z[1][q]);
+          }
+        }
+      }
+      __syncthreads();   // the staging buffer is refilled next round
+      OBGS_PROF(3)
     }
-    __syncthreads();
   }
-  for (int j = j0 + warp; j < j1; j += nw)
-    for (int i = lane; i < m; i += 32) t.V[(int64_t)j * m + i] = Z[(int64_t)(j - j0) * ldz + i];
+  if (prof)
+    for (int q = 0; q < 8; ++q) t.dbg[20 + q] = pa[q];
+#undef OBGS_PROF
 }
 
 // Back-transformation V = H_0 ... H_{m-3} Z for a chunk of 16 NV vectors per

@@ -585,29 +585,43 @@ static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double
   CK(cudaGetLastError());
   if (pev) cudaEventRecord(pev[1], st);
   {
-    // vectors on chip over a 4- or 8-CTA cluster (all r <= m fit: (m/CL) (m|1) + m doubles)
-    const int CLn = (mmax <= 320) ? 4 : (mmax <= 448 ? 8 : 16);
-    const int rbmax = (mmax + CLn - 1) / CLn;
-    const size_t smem = ((size_t)rbmax * (mmax | 1) + mmax) * 8;
+    // block Gram-Schmidt over a cluster: CTA c owns <= 32 vectors (two per warp)
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(n * CLn));
     cfg.blockDim = dim3(512);
-    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = CLn;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (CLn == 4) CK(cudaLaunchKernelEx(&cfg, k_orth_cl<4>, (const EigTask *)dp));
-    else if (CLn == 8) CK(cudaLaunchKernelEx(&cfg, k_orth_cl<8>, (const EigTask *)dp));
-    else CK(cudaLaunchKernelEx(&cfg, k_orth_cl<16>, (const EigTask *)dp));
+    if (mmax <= 256) {
+      cfg.gridDim = dim3((unsigned)(n * 8));
+      at[0].val.clusterDim.x = 8;
+      cfg.dynamicSmemBytes = (size_t)orth_bgs_smem_doubles<8>() * 8;
+      CK(cudaLaunchKernelEx(&cfg, k_orth_bgs<8, 8>, (const EigTask *)dp));
+    } else if (mmax <= 384) {
+      cfg.gridDim = dim3((unsigned)(n * 16));
+      at[0].val.clusterDim.x = 16;
+      cfg.dynamicSmemBytes = (size_t)orth_bgs_smem_doubles<12>() * 8;
+      CK(cudaLaunchKernelEx(&cfg, k_orth_bgs<12, 16>, (const EigTask *)dp));
+    } else {
+      cfg.gridDim = dim3((unsigned)(n * 16));
+      at[0].val.clusterDim.x = 16;
+      cfg.dynamicSmemBytes = (size_t)orth_bgs_smem_doubles<16>() * 8;
+      CK(cudaLaunchKernelEx(&cfg, k_orth_bgs<16, 16>, (const EigTask *)dp));
+    }
   }
   CK(cudaGetLastError());
   if (pev) cudaEventRecord(pev[2], st);
-  if (mmax <= 256) {
+  // few nodes (the upper levels): 16 vectors per CTA, the reflector chain is
+  // latency-bound and the SMs are idle; many nodes: more vectors per CTA
+  if (n * ((mmax + 15) / 16) <= 2 * 148) {
+    const int nc = (mmax + 15) / 16;
+    if (mmax <= 256) launch_k(k_backtr_multi<8, 1>, (unsigned)(n * nc), 512, SMEM_LIMIT, st, dp, nc, cap);
+    else if (mmax <= 384) launch_k(k_backtr_multi<12, 1>, (unsigned)(n * nc), 512, SMEM_LIMIT, st, dp, nc, cap);
+    else launch_k(k_backtr_multi<16, 1>, (unsigned)(n * nc), 512, SMEM_LIMIT, st, dp, nc, cap);
+  } else if (mmax <= 256) {
     const int nc = (mmax + 63) / 64;
     launch_k(k_backtr_multi<8, 4>, (unsigned)(n * nc), 512, SMEM_LIMIT, st, dp, nc, cap);
   } else if (mmax <= 384) {
@@ -623,11 +637,15 @@ static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double
 
 static void set_eig_attrs() {
   CK(cudaFuncSetAttribute(k_invit_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-  CK(cudaFuncSetAttribute(k_orth_cl<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-  CK(cudaFuncSetAttribute(k_orth_cl<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-  CK(cudaFuncSetAttribute(k_orth_cl<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
-  CK(cudaFuncSetAttribute(k_orth_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(k_orth_bgs<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, orth_bgs_smem_doubles<8>() * 8));
+  CK(cudaFuncSetAttribute(k_orth_bgs<12, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, orth_bgs_smem_doubles<12>() * 8));
+  CK(cudaFuncSetAttribute(k_orth_bgs<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, orth_bgs_smem_doubles<16>() * 8));
+  CK(cudaFuncSetAttribute(k_orth_bgs<12, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(k_orth_bgs<16, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   CK(cudaFuncSetAttribute(k_backtr_multi<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_backtr_multi<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_backtr_multi<12, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_backtr_multi<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_backtr_multi<12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_backtr_multi<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EIG_REG_SMEM));
@@ -3874,6 +3892,10 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
           cudaEventElapsedTime(&d, pev[2], pev[3]);
           fprintf(stderr, "[k_tridiag_cl m=%d class %d] %.1f us | eigvals %.1f invit %.1f orth %.1f backtr %.1f us\n", m,
                   eig_cl_class(m), 1e3 * ms, 1e3 * a, 1e3 * b, 1e3 * c, 1e3 * d);
+          long long ob[8];
+          CK(cudaMemcpy(ob, ddbg + 20, sizeof(ob), cudaMemcpyDeviceToHost));
+          fprintf(stderr, "  [orth CTA 1 cycles] intra-tail %lld cluster-sync %lld stage %lld project %lld | norm+barA %lld "
+                  "normalise+barD %lld update %lld\n", ob[0], ob[1], ob[2], ob[3], ob[4], ob[5], ob[6]);
         }
         for (auto &x : pev) cudaEventDestroy(x);
         cudaEventDestroy(e0);
