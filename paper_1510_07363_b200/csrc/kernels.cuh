@@ -540,6 +540,22 @@ __device__ __forceinline__ void grp_multisect(const double *d, const double *e2,
   }
 }
 
+// Inverse-iteration start vector entry (row i of vector `seed`): zero-mean,
+// from a 32-bit integer hash of (row, vector).  Starts of different vectors
+// must be independent, or the vectors of a cluster of (nearly) equal
+// eigenvalues come out nearly parallel and their orthogonalisation amplifies
+// rounding (a linear congruence whose vectors were shifted copies of one
+// sequence cost up to 1e-7 of subspace accuracy on degenerate spectra).
+__device__ __forceinline__ double invit_start(int i, int seed) {
+  unsigned h = (unsigned)i * 0x9E3779B9u ^ ((unsigned)seed * 0x85EBCA6Bu + 0x165667B1u);
+  h ^= h >> 16;
+  h *= 0x7FEB352Du;
+  h ^= h >> 15;
+  h *= 0x846CA68Bu;
+  h ^= h >> 16;
+  return (double)(h >> 8) * (2.0 / 16777216.0) - 1.0;
+}
+
 // Inverse iteration for one eigenvalue lam of the tridiagonal (d, e): pivoted
 // LU of T - sft I (dgttrf) then 2 solves from a fixed pseudo-random start,
 // normalised.  Arrays are interleaved with stride S (S vectors side by side,
@@ -576,7 +592,7 @@ __device__ __forceinline__ void invit_one(const double *__restrict__ d, const do
     double v = D[i * S];
     if (fabs(v) < pertol) v = copysign(pertol, v == 0.0 ? 1.0 : v);
     D[i * S] = frcp(v);
-    b[i * S] = 1.0 + 0.5 * (double)((i * 7919u + seed * 104729u + 13u) % 1024u) * (1.0 / 1024.0);
+    b[i * S] = invit_start(i, seed);
   }
   double nrm = 0.0;
   for (int it = 0; it < 2; ++it) {
@@ -2095,7 +2111,7 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
       if (fabs(v) < pertol) v = copysign(pertol, v == 0.0 ? 1.0 : v);
       D[(i) * RR] = frcp(v);
     }
-    for (int i = 0; i < m; ++i) b[(i) * RR] = 1.0 + 0.5 * (double)((i * 7919u + k * 104729u + 13u) % 1024u) * (1.0 / 1024.0);
+    for (int i = 0; i < m; ++i) b[(i) * RR] = invit_start(i, k);
     for (int it = 0; it < 3; ++it) {
       // forward (row interchanges + unit lower)
       double bi = b[(0) * RR];
@@ -2233,24 +2249,177 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
 }
 
 // ---------------------------------------- PRE pipeline (128 < m <= 512) ----
-// Inverse iteration for the kept eigenvalues of the tridiagonal record, one
-// CTA per chunk of vectors (chunk c: k in [c nb, (c+1) nb) ∩ [0, r)), each
-// chunk's LU / right-hand sides in shared memory; grid = nodes x nch.
-__global__ void __launch_bounds__(256) k_invit_multi(const EigTask *__restrict__ tasks, int nch, int smem_cap_doubles) {
+// Stage 0: eigenvalues of the tridiagonal record over nch CTAs per node.  Every
+// CTA scales T, finds lambda_0 (one warp, 32-point multisection) and the
+// candidate count (Sturm count at the candidate bound) -- the same arithmetic
+// on the same data, so bitwise the same in every CTA -- then multisects its
+// slice of the candidates [1, ncomp) with EG lanes per eigenvalue (the more
+// CTAs, the more lanes per eigenvalue and the fewer rounds).  Writes lam[k]
+// (unscaled) to the record; CTA 0 also lam[0], ||T|| bound, ncomp and the trace.
+// The rank (Eq. cutOff1 / curOff6) is decided by k_invit_multi from these.
+constexpr int REC_NCOMP = 2, REC_TRACE = 3;   // record slots rec[3 m + .]
+__global__ void __launch_bounds__(512, 1) k_eigvals_cl(const EigTask *__restrict__ tasks, double eps, int nch) {
+  extern __shared__ double sh[];
+  __shared__ double s_red[32], s_bc[8];
+  __shared__ int s_int[4];
+  pdl_trigger();
+  const EigTask t = tasks[blockIdx.x / nch];
+  pdl_wait();
+  const int c = blockIdx.x % nch;
+  const int m = t.m, mp = (m + 8) & ~7;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double *rec = t.work + 6 * (int64_t)m * m;
+  if (!(rec[3 * m] > 0.0)) return;   // G = 0: k_invit_multi writes r = 0 (Z4)
+  double *d = sh, *e = sh + mp, *e2 = sh + 2 * mp;
+  for (int i = tid; i < m; i += blockDim.x) {
+    d[i] = rec[i];
+    e[i] = rec[m + i];
+  }
+  __syncthreads();
+  double trace = 0.0, fbud = 0.0;
+  if (t.frob) {
+    double tr = 0.0;
+    for (int i = tid; i < m; i += blockDim.x) tr += d[i];
+    tr = warp_sum(tr);
+    if (lane == 0) s_red[warp] = tr;
+    __syncthreads();
+    for (int w = 0; w < nw; ++w) trace += s_red[w];
+    fbud = eps * eps * (*t.frob) / t.frob_w;
+    __syncthreads();
+  }
+  double gl = 1e300, gu = -1e300, emax2 = 0;
+  for (int i = tid; i < m; i += blockDim.x) {
+    const double off = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < m - 1 ? fabs(e[i]) : 0.0);
+    gl = fmin(gl, d[i] - off);
+    gu = fmax(gu, d[i] + off);
+    if (i < m - 1) {
+      e2[i] = e[i] * e[i];
+      emax2 = fmax(emax2, e2[i]);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+    gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+    emax2 = fmax(emax2, __shfl_xor_sync(0xffffffffu, emax2, o));
+  }
+  if (lane == 0) {
+    s_red[warp] = gl;
+    s_red[16 + warp] = gu;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 1e300, b = -1e300;
+    for (int w = 0; w < nw; ++w) {
+      a = fmin(a, s_red[w]);
+      b = fmax(b, s_red[16 + w]);
+    }
+    s_bc[0] = a;
+    s_bc[1] = b;
+  }
+  __syncthreads();
+  if (lane == 0) s_red[warp] = emax2;
+  __syncthreads();
+  double em = 0;
+  for (int w = 0; w < nw; ++w) em = fmax(em, s_red[w]);
+  gl = s_bc[0];
+  gu = s_bc[1];
+  const double bnorm = fmax(fabs(gl), fabs(gu));
+  const double isc = 1.0 / bnorm;
+  __syncthreads();
+  for (int i = tid; i < mp; i += blockDim.x) {
+    if (i < m) {
+      d[i] *= isc;
+      if (i < m - 1) e2[i] *= isc * isc;
+      else e2[i] = 0.0;
+    } else {
+      d[i] = 4.0;   // padding: no sign change for x < 4
+      e2[i] = 0.0;
+    }
+  }
+  gl *= isc;
+  gu *= isc;
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, em * isc * isc) * 1e10;
+  gl -= 2.2e-16 * 2 * m + 2 * pivmin;
+  gu += 2.2e-16 * 2 * m + 2 * pivmin;
+  __syncthreads();
+  if (warp == 0) {
+    const double l0 = warp_eig_asc(d, e2, m, m - 1, gl, gu, pivmin);
+    if (lane == 0) {
+      double thr = eps * sqrt(fmax(l0, 0.0));
+      thr = 0.25 * thr * thr;
+      if (t.frob) thr = fbud / m * isc;   // (scaled) candidate bound of the Frobenius rule
+      const int below = sturm_count(d, e2, m, thr, pivmin);
+      s_int[0] = min(m, m - below + 1);   // candidates to compute (superset of kept + 1)
+      s_bc[2] = l0;
+    }
+  }
+  __syncthreads();
+  const int ncomp = s_int[0];
+  double *lam = rec + rec_lam_off(m);
+  if (c == 0 && tid == 0) {
+    lam[0] = s_bc[2] * bnorm;
+    rec[3 * m + 1] = bnorm;
+    rec[3 * m + REC_NCOMP] = (double)ncomp;
+    rec[3 * m + REC_TRACE] = trace;
+  }
+  const int per = (ncomp - 1 + nch - 1) / nch, k1 = 1 + c * per, k2 = min(ncomp, k1 + per);
+  if (k1 >= k2) return;
+  const int cnt = k2 - k1;
+  if (cnt <= 16) grp_multisect<32>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm);
+  else if (cnt <= 32) grp_multisect<16>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm);
+  else if (cnt <= 64) grp_multisect<8>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm);
+  else grp_multisect<4>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm);
+}
+
+// Stage 1: the rank from the eigenvalues (Eq. cutOff1, or Eq. curOff6 with the
+// trace), then inverse iteration for the kept eigenvalues of the tridiagonal
+// record, one CTA per chunk of vectors (chunk c: k in [c nb, (c+1) nb) ∩ [0, r)),
+// each chunk's LU / right-hand sides in shared memory; grid = nodes x nch.
+// CTA 0 of each node writes sigma and the rank.
+__global__ void __launch_bounds__(256) k_invit_multi(const EigTask *__restrict__ tasks, int nch, int smem_cap_doubles,
+                                                     double eps) {
   pdl_trigger();
   extern __shared__ double sh[];
   const EigTask t = tasks[blockIdx.x / nch];
   pdl_wait();   // task descriptors are static: read before the wait
   const int c = blockIdx.x % nch;
   const int m = t.m;
-  const int r = *t.rank_out;
+  const double *rec = t.work + 6 * (int64_t)m * m;
+  int r = 0, ncomp = 0;
+  {
+    __shared__ int s_cnt;
+    const double *lg = rec + rec_lam_off(m);
+    const bool live = rec[3 * m] > 0.0;
+    ncomp = live ? (int)rec[3 * m + REC_NCOMP] : 0;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    if (t.frob) {   // smallest k with tail(k) = trace - sum_{t<k} lambda_t < budget
+      if (threadIdx.x == 0 && live) {
+        const double trace = rec[3 * m + REC_TRACE], fbud = eps * eps * (*t.frob) / t.frob_w;
+        double pre = 0.0;
+        int k = 0;
+        while (k < ncomp && !(trace - pre < fbud)) pre += fmax(lg[k++], 0.0);
+        s_cnt = k;
+      }
+    } else if (live) {
+      const double sig0 = sqrt(fmax(lg[0], 0.0));
+      int cn = 0;
+      for (int k = threadIdx.x; k < ncomp; k += blockDim.x) cn += (sqrt(fmax(lg[k], 0.0)) >= eps * sig0);
+      if (cn) atomicAdd(&s_cnt, cn);
+    }
+    __syncthreads();
+    r = s_cnt;
+    if (c == 0) {
+      for (int k = threadIdx.x; k < m; k += blockDim.x) t.sig[k] = (k < ncomp) ? sqrt(fmax(lg[k], 0.0)) : 0.0;
+      if (threadIdx.x == 0) *t.rank_out = r;
+    }
+  }
   const int64_t per = 5 * (int64_t)m + (m + 7) / 8;
   const int mp = (m + 8) & ~7;
   const int nb = (int)min((int64_t)blockDim.x, ((int64_t)smem_cap_doubles - 2 * mp) / per);
   const int k0 = c * nb;
   if (k0 >= r || nb <= 0) return;
   const int nbc = min(nb, r - k0);
-  const double *rec = t.work + 6 * (int64_t)m * m;
   double *d = sh, *e = sh + mp, *ws = sh + 2 * mp;
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     d[i] = rec[i];
@@ -2276,7 +2445,7 @@ __global__ void __launch_bounds__(256) k_invit_multi(const EigTask *__restrict__
 // owns the panel of vectors [c rb, (c+1) rb) (rb = ceil(r / CL) <= 32), two
 // per warp, in registers (lane's rows 32 q + lane).  For c = 0 .. CL-1:
 //   CTA c orthonormalises its panel by MGS inside the CTA (pivot vector l in
-//   warp l mod 16, broadcast through shared memory: two block barriers per
+//   warp l mod 16, broadcast through shared memory: one block barrier per
 //   vector), writing the final vectors to V; one cluster barrier; every later
 //   CTA stages panel c from L2 and removes it from its own vectors (block
 //   classical Gram-Schmidt, 8 columns per warp reduction).

@@ -572,16 +572,23 @@ static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps
 // inverse iteration, MGS, chunked back-transformation.  Returns the launches.
 static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double eps, int *dstatus,
                            cudaEvent_t *pev = nullptr) {
-  launch_k(k_eig_t<false, true>, (unsigned)n, EIG_REG_THREADS, SMEM_LIMIT, st, dp, eps, SMEM_LIMIT / 8, dstatus);
+  if (eps == 0.0) {   // V = I, r = m (reading Z3)
+    launch_k(k_eig_t<false, true>, (unsigned)n, EIG_REG_THREADS, SMEM_LIMIT, st, dp, eps, SMEM_LIMIT / 8, dstatus);
+    CK(cudaGetLastError());
+    return 1;
+  }
+  // eigenvalues over several CTAs per node (about 40 candidates each)
+  const int nev = std::max(1, std::min(16, (mmax + 39) / 40));
+  launch_k(k_eigvals_cl, (unsigned)(n * nev), 512, (size_t)3 * ((mmax + 8) & ~7) * 8, st, (const EigTask *)dp, eps,
+           nev);
   CK(cudaGetLastError());
-  if (eps == 0.0) return 1;   // V = I already written
   const int cap = SMEM_LIMIT / 8;
   const int64_t per = 5 * (int64_t)mmax + (mmax + 7) / 8;
   const int mp = (mmax + 8) & ~7;
   const int nb = (int)std::min<int64_t>(256, (cap - 2 * mp) / per);
   const int nch = (mmax + nb - 1) / nb;
   if (pev) cudaEventRecord(pev[0], st);
-  launch_k(k_invit_multi, (unsigned)(n * nch), 256, SMEM_LIMIT, st, dp, nch, cap);
+  launch_k(k_invit_multi, (unsigned)(n * nch), 256, SMEM_LIMIT, st, dp, nch, cap, eps);
   CK(cudaGetLastError());
   if (pev) cudaEventRecord(pev[1], st);
   {
