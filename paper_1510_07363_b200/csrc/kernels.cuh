@@ -1372,7 +1372,11 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
   double *vsm0 = vbuf[0], *vsm1 = vbuf[1];
   __shared__ double pbuf[2][MR];              // p (two buffers)
   double *psm0 = pbuf[0], *psm1 = pbuf[1];
-  __shared__ double ps_part[NW][MR];
+  // row partials of A v: static shared memory, or dynamic past 40 KB (m <= 160)
+  constexpr bool DYN = NW * MR * 8 > 32 * 1024;
+  __shared__ double ps_part_s[DYN ? 1 : NW][DYN ? 1 : MR];
+  extern __shared__ double tr_dyn[];
+  double(*ps_part)[MR] = DYN ? reinterpret_cast<double(*)[MR]>(tr_dyn) : reinterpret_cast<double(*)[MR]>(&ps_part_s[0][0]);
   __shared__ double colbuf[MR];               // column k+1 before update k
   // Householder vector of column kk from its (updated) entries col[q] = A(4 lane + q, kk),
   // run by the owner warp kk >> 3: v into the shared buffer, the packed reflector
@@ -1456,7 +1460,7 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
 #pragma unroll
       for (int u = 0; u < UW; u += 2) {
         s0 = fma(a[q][u], vc[u], s0);
-        s1 = fma(a[q][u + 1], vc[u + 1], s1);
+        if (u + 1 < UW) s1 = fma(a[q][u + 1], vc[u + 1], s1);
       }
       ps_part[warp][32 * q + lane] = s0 + s1;
     }
@@ -1469,14 +1473,25 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
     __syncthreads();                                              // (2) partials visible
     TRID_PROF(1)
     if (tid < MR) {
+      double sacc;
+      if constexpr (QR >= 5) {   // larger tile: four running sums (fewer live registers)
+        double h4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int w = 0; w < NW; ++w) h4[w & 3] += ps_part[w][tid];
+        sacc = (h4[0] + h4[1]) + (h4[2] + h4[3]);
+      } else {
       double h[NW];
 #pragma unroll
       for (int w = 0; w < NW; ++w) h[w] = ps_part[w][tid];
+      constexpr int P2 = (NW >= 32) ? 32 : (NW >= 16) ? 16 : (NW >= 8) ? 8 : (NW >= 4) ? 4 : (NW >= 2) ? 2 : 1;
 #pragma unroll
-      for (int st = NW / 2; st > 0; st /= 2)
+      for (int w = P2; w < NW; ++w) h[w - P2] += h[w];      // NW not a power of two
+#pragma unroll
+      for (int st = P2 / 2; st > 0; st /= 2)
 #pragma unroll
         for (int w = 0; w < st; ++w) h[w] += h[w + st];   // pairwise tree
-      const double sacc = h[0];
+      sacc = h[0];
+      }
       const double pi = (tid > k && tid < m) ? tk * sacc : 0.0;
       ps[tid] = pi;
       // p.v over the 128 rows: 4 warp reductions (shuffles are a shared,
@@ -1487,13 +1502,20 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
     TRID_PROF(2)
     __syncthreads();                                              // (3) p visible
     TRID_PROF(3)
-    const double pv = QR == 4 ? (s_red[0] + s_red[1]) + (s_red[2] + s_red[3])
-                              : (QR == 2 ? s_red[0] + s_red[1] : s_red[0]);
+    double pv;
+    if constexpr (QR == 4) pv = (s_red[0] + s_red[1]) + (s_red[2] + s_red[3]);
+    else if constexpr (QR == 2) pv = s_red[0] + s_red[1];
+    else if constexpr (QR == 1) pv = s_red[0];
+    else {
+      pv = s_red[0];
+#pragma unroll
+      for (int w = 1; w < QR; ++w) pv += s_red[w];
+    }
     const double alpha = -0.5 * tk * pv;
     // (vr, wr, v_c, w_c are re-read from shared memory here: with the 32-double
     // tile live, keeping them in registers across form_v would spill)
     const double *psc = ps + UW * warp, *vsc = vs + UW * warp;
-    if (wact) {
+    if (wact && QR <= 4) {
       double vq[QR], wq[QR];
 #pragma unroll
       for (int q = 0; q < QR; ++q) {
@@ -1506,6 +1528,17 @@ __global__ void __launch_bounds__(32 * NW, 1) k_tridiag_reg(const EigTask *__res
 #pragma unroll
         for (int q = 0; q < QR; ++q)
           if (32 * q + 31 > k) a[q][u] = fma(-vq[q], wcu, fma(-wq[q], vcu, a[q][u]));
+      }
+    } else if (wact) {   // larger tile: row-outer, the column values re-read (fewer live registers)
+#pragma unroll
+      for (int q = 0; q < QR; ++q) {
+        if (32 * q + 31 <= k) continue;
+        const double vq = vs[32 * q + lane], wq = fma(alpha, vq, ps[32 * q + lane]);
+#pragma unroll
+        for (int u = 0; u < UW; ++u) {
+          const double vcu = vsc[u], wcu = fma(alpha, vcu, psc[u]);
+          a[q][u] = fma(-vq, wcu, fma(-wq, vcu, a[q][u]));
+        }
       }
     }
     const int k1 = k + 1;

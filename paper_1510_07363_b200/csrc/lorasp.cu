@@ -369,8 +369,8 @@ struct lorasp_ctx {
   cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr, ev_u = nullptr;
   cudaStream_t stream_eig = nullptr;   // register-tile eigen path beside the cluster / generic one
   cudaEvent_t ev_ef = nullptr, ev_ej = nullptr;
-  cudaStream_t stream_cl[2] = {nullptr, nullptr};   // cluster tridiagonalisation classes 2, 3
-  cudaEvent_t ev_cf = nullptr, ev_cj[2] = {nullptr, nullptr};
+  cudaStream_t stream_cl[3] = {nullptr, nullptr, nullptr};   // tridiagonalisation classes 2, 3, 4
+  cudaEvent_t ev_cf = nullptr, ev_cj[3] = {nullptr, nullptr, nullptr};
   bool s1_pending = false;
   DevBuf ws_S, ws_Y, ws_T1, d_sp, ws_piv2;   // ws_piv2: blocked split-pivot part 1 (stream2)
   DevBuf d_frob, d_frobpart;   // f2: ||all levels below||_F^2 (device scalar) and per-slot partial sums
@@ -515,6 +515,7 @@ bool is_device_ptr(const void *p) {
 // Cluster eigen path (128 < m <= 512): k_tridiag_cl over a CTA cluster, then
 // k_eig_t<false, true> (eigenvalues, inverse iteration, back-transformation).
 static int eig_cl_class(int m) {
+  if (m > EIG_REG_M && m <= 160) return 4;   // one CTA: k_tridiag_reg<5, 16, 10> (5 x 10 tile per thread)
   if (m > EIG_REG_M && m <= 256) return 1;
   if (m > 256 && m <= 384) return 2;
   if (m > 384 && m <= 512) return 3;
@@ -540,6 +541,10 @@ static void launch_tridiag_cl_t(cudaStream_t st, const EigTask *dt, int n, doubl
 
 static void launch_tridiag_cl(cudaStream_t st, const EigTask *dt, int n, int cls, double eps,
                               long long *prof = nullptr) {
+  if (cls == 4) {   // 128 < m <= 160: the register-tile tridiagonalisation in one CTA (the record format is shared)
+    launch_k(k_tridiag_reg<false, 5, 16, 10>, (unsigned)n, 512, 0, st, dt, eps, (long long *)nullptr);
+    return;
+  }
   if (cls == 1) launch_tridiag_cl_t<8, 4, 4>(st, dt, n, eps, prof);
   else if (cls == 2) launch_tridiag_cl_t<12, 3, 8>(st, dt, n, eps, prof);
   else launch_tridiag_cl_t<16, 2, 16>(st, dt, n, eps, prof);
@@ -699,7 +704,7 @@ void ensure_mem(lorasp_ctx *h) {
     CK(cudaStreamCreateWithPriority(&h->stream_hi, cudaStreamNonBlocking, greatest));
     CK(cudaStreamCreateWithPriority(&h->stream_eig, cudaStreamNonBlocking, greatest));
     for (auto &cs : h->stream_cl) CK(cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, greatest));
-    h->stg.side = {h->stream2, h->stream_hi, h->stream_eig, h->stream_cl[0], h->stream_cl[1]};
+    h->stg.side = {h->stream2, h->stream_hi, h->stream_eig, h->stream_cl[0], h->stream_cl[1], h->stream_cl[2]};
   }
   CK(cudaEventCreateWithFlags(&h->ev_cf, cudaEventDisableTiming));
   for (auto &e : h->ev_cj) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -806,7 +811,7 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
       return;
     }
   }
-  std::vector<EigTask> small, big, clt[4];
+  std::vector<EigTask> small, big, clt[5];
   bool reg_fork = false;
   for (const EigTask &e : et) {
     const int cls = eig_cl_class(e.m);
@@ -845,17 +850,17 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
   }
   std::vector<EigTask> post;
   {
-    // the cluster classes side by side (classes 2 and 3 on their own streams)
-    EigTask *dc[4] = {nullptr, nullptr, nullptr, nullptr};
+    // the tridiagonalisation classes side by side (classes 2, 3, 4 on their own streams)
+    EigTask *dc[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     int ncls = 0;
-    for (int c = 1; c <= 3; ++c)
+    for (int c = 1; c <= 4; ++c)
       if (!clt[c].empty()) {
         dc[c] = push(h, clt[c]);
         ++ncls;
       }
     const bool fork = ncls > 1;
     if (fork) CK(cudaEventRecord(h->ev_cf, h->stream));
-    for (int c = 1; c <= 3; ++c) {
+    for (int c = 1; c <= 4; ++c) {
       if (!dc[c]) continue;
       cudaStream_t cs = h->stream;
       if (fork && c > 1) {
@@ -4050,7 +4055,7 @@ void lorasp_destroy(lorasp_handle h) {
     // every library stream drains before any buffer is released (a factorization
     // that threw may have left split-pivot / eigen work in flight)
     cudaStreamSynchronize(h->stream);
-    for (cudaStream_t s : {h->stream2, h->stream_hi, h->stream_eig, h->stream_cl[0], h->stream_cl[1]})
+    for (cudaStream_t s : {h->stream2, h->stream_hi, h->stream_eig, h->stream_cl[0], h->stream_cl[1], h->stream_cl[2]})
       if (s) cudaStreamSynchronize(s);
     DevBuf *bufs[] = {&h->d_values, &h->d_rowptr, &h->d_colidx, &h->d_dest, &h->arena[0], &h->arena[1],
                       &h->ws_G, &h->ws_V, &h->ws_sig, &h->ws_X, &h->ws_ctr, &h->ws_piv, &h->d_ranks,
