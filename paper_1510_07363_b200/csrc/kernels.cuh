@@ -3883,6 +3883,77 @@ struct ColStream {
 
 // One CTA per node: the node's record streams through shared memory once per
 // pass (forward reads L^{-1}[:, :m] and Z, backward reads Z and L^{-1}[:, :m]).
+// Column dots out[j] = sum_{k >= (TRI ? j : 0), k < n} col_j[k] x[k] for the
+// columns j in [j0, j1) of a staged chunk (column j at buf + (j - j0) ld), with
+// G lanes per column (32 / G columns per warp): short columns (the upper
+// levels' small n) waste neither lanes nor shuffles on a whole-warp reduction.
+template <int G, bool TRI>
+__device__ __forceinline__ void ap_col_dots(const double *__restrict__ buf, int ld, int j0, int j1, int n,
+                                            const double *__restrict__ x, double *__restrict__ out, int obase) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  constexpr int CPW = 32 / G;
+  const int sub = lane / G, sl = lane % G;
+  for (int jb = j0 + warp * CPW; jb < j1; jb += nw * CPW) {
+    const int j = jb + sub;
+    double sacc = 0.0;
+    if (j < j1) {
+      const double *col = buf + (int64_t)(j - j0) * ld;
+      for (int k = (TRI ? j : 0) + sl; k < n; k += G) sacc = fma(col[k], x[k], sacc);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (sl == 0 && j < j1) out[j - obase] = sacc;
+  }
+}
+template <bool TRI>
+__device__ __forceinline__ void ap_col_dots_n(const double *__restrict__ buf, int ld, int j0, int j1, int n,
+                                              const double *__restrict__ x, double *__restrict__ out, int obase) {
+  if (n <= 64) ap_col_dots<8, TRI>(buf, ld, j0, j1, n, x, out, obase);
+  else if (n <= 128) ap_col_dots<16, TRI>(buf, ld, j0, j1, n, x, out, obase);
+  else ap_col_dots<32, TRI>(buf, ld, j0, j1, n, x, out, obase);
+}
+// Row sums acc[i] (+)= sum_{k in [k0, k1), k <= kmax(i)} buf[(k - k0) ld + i] x[k]
+// for the rows i < n of a staged chunk: G = 256 / rows-per-group thread groups
+// interleave the columns (rows up to 64: 4 groups, up to 128: 2), partial sums
+// combined in a fixed order through `part` (>= 256 doubles); SUB: subtract.
+// kmax(i) = TRIL ? i : k1 - 1.  Ends with a block barrier.
+template <bool SUB>
+__device__ __forceinline__ void ap_row_sums(const double *__restrict__ buf, int ld, int k0, int k1, int n, bool tril,
+                                            const double *__restrict__ x, double *__restrict__ acc,
+                                            double *__restrict__ part) {
+  const int tid = threadIdx.x;
+  const int G = (n <= 64) ? 4 : (n <= 128 ? 2 : 1);
+  if (G == 1) {
+    for (int i = tid; i < n; i += blockDim.x) {
+      double s0 = 0, s1 = 0;
+      const int kl = tril ? min(k1 - 1, i) : k1 - 1;
+      int k = k0;
+      for (; k + 1 <= kl; k += 2) {
+        s0 = fma(buf[(int64_t)(k - k0) * ld + i], x[k], s0);
+        s1 = fma(buf[(int64_t)(k + 1 - k0) * ld + i], x[k + 1], s1);
+      }
+      if (k <= kl) s0 = fma(buf[(int64_t)(k - k0) * ld + i], x[k], s0);
+      acc[i] = SUB ? acc[i] - (s0 + s1) : acc[i] + (s0 + s1);
+    }
+    __syncthreads();
+    return;
+  }
+  const int rpg = blockDim.x / G, g = tid / rpg, i = tid % rpg;
+  double s = 0;
+  if (i < n) {
+    const int kl = tril ? min(k1 - 1, i) : k1 - 1;
+    for (int k = k0 + g; k <= kl; k += G) s = fma(buf[(int64_t)(k - k0) * ld + i], x[k], s);
+  }
+  part[tid] = s;
+  __syncthreads();
+  if (g == 0 && i < n) {
+    double t = part[i];
+    for (int q = 1; q < G; ++q) t += part[q * rpg + i];
+    acc[i] = SUB ? acc[i] - t : acc[i] + t;
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ nodes,
                                                    const ApSeg *__restrict__ segs,
                                                    double *__restrict__ vec, int chunk_doubles) {
@@ -3902,6 +3973,8 @@ __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ no
   double *rhs = stage1 + chunk_doubles;  // m
   double *dy = rhs + nd.m;               // n (accumulates y)
   double *zo = dy + n;                   // W: Z^T D y, written back once at the end
+  double *tv = zo + nd.W;                // W: the targets' RHS entries (prefetched)
+  double *part = tv + nd.W;              // 256: row-sum partials
   const int ld = nd.ld;
   const int cc = max(1, chunk_doubles / ld);
   const double *Z = nd.F + nd.zf_off;
@@ -3935,6 +4008,10 @@ __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ no
   asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int i = tid; i < nd.m; i += blockDim.x) rhs[i] = vec[nd.off_s + i];
   for (int i = tid; i < n; i += blockDim.x) dy[i] = 0.0;
+  for (int sg = 0; sg < nd.nseg; ++sg) {   // the scatter's reads, issued early
+    const ApSeg S = segs[nd.seg0 + sg];
+    for (int j = tid; j < S.w; j += blockDim.x) tv[S.zc + j] = vec[S.voff + j];
+  }
   __syncthreads();
   // ---- y = L^{-1}[:, :m] rhs, then Z^T D y ----
   for (int c = 0; c < ntot; ++c) {
@@ -3943,14 +4020,8 @@ __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ no
     const double *buf = (c & 1) ? stage1 : stage0;
     if (c < na) {
       const int k0 = c * cc, k1 = min(nd.m, k0 + cc);
-      for (int i = tid; i < n; i += blockDim.x) {
-        double sacc = 0;
-        const int kl = nd.full ? k1 - 1 : min(k1 - 1, i);
-        for (int k = k0; k <= kl; ++k) sacc = fma(buf[(int64_t)(k - k0) * ld + i], rhs[k], sacc);
-        dy[i] += sacc;
-      }
+      ap_row_sums<false>(buf, ld, k0, k1, n, !nd.full, rhs, dy, part);
       if (c == na - 1) {
-        __syncthreads();
         for (int i = tid; i < n; i += blockDim.x) {
           const double y = dy[i];
           nd.y[i] = y;
@@ -3959,20 +4030,14 @@ __global__ void __launch_bounds__(256) k_apply_fwd(const ApNode *__restrict__ no
       }
     } else {
       const int j0 = (c - na) * cc, j1 = min(nd.W, j0 + cc);
-      for (int j = j0 + warp; j < j1; j += nw) {
-        const double *col = buf + (int64_t)(j - j0) * ld;
-        double sacc = 0;
-        for (int k = lane; k < n; k += 32) sacc = fma(col[k], dy[k], sacc);
-        sacc = warp_sum(sacc);
-        if (lane == 0) zo[j] = sacc;
-      }
+      ap_col_dots_n<false>(buf, ld, j0, j1, n, dy, zo, 0);
     }
     __syncthreads();   // stage (c & 1) is free for chunk c + 2
   }
-  // rhs_q -= Z_q^T D y for every target segment (coalesced read-modify-write)
+  // rhs_q -= Z_q^T D y for every target segment (coalesced; read at the start)
   for (int sg = 0; sg < nd.nseg; ++sg) {
     const ApSeg S = segs[nd.seg0 + sg];
-    for (int j = tid; j < S.w; j += blockDim.x) vec[S.voff + j] -= zo[S.zc + j];
+    for (int j = tid; j < S.w; j += blockDim.x) vec[S.voff + j] = tv[S.zc + j] - zo[S.zc + j];
   }
   if (na == 0) {  // m == 0 cannot happen for a recorded node; keep y defined
     for (int i = tid; i < n; i += blockDim.x) nd.y[i] = 0.0;
@@ -3995,6 +4060,7 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
   double *stage0 = sh, *stage1 = sh + chunk_doubles;
   double *u = stage1 + chunk_doubles;  // n
   double *xt = u + n;                  // W
+  double *part = xt + nd.W;            // 256: row-sum partials
   const int ld = nd.ld;
   int cc = max(1, chunk_doubles / ld);
   const double *Z = nd.F + nd.zb_off;
@@ -4039,13 +4105,8 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
     const double *buf = (c & 1) ? stage1 : stage0;
     if (c < nb) {
       const int j0 = c * cc, j1 = min(nd.W, j0 + cc);
-      for (int i = tid; i < n; i += blockDim.x) {
-        double sacc = 0;
-        for (int j = j0; j < j1; ++j) sacc = fma(buf[(int64_t)(j - j0) * ld + i], xt[j], sacc);
-        u[i] -= sacc;
-      }
+      ap_row_sums<true>(buf, ld, j0, j1, n, false, xt, u, part);
       if (c == nb - 1 && nd.sym) {
-        __syncthreads();
         for (int i = nd.m + tid; i < n; i += blockDim.x) u[i] = -u[i];   // D u
       }
     } else {
@@ -4054,13 +4115,7 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
         __syncthreads();
       }
       const int i0 = (c - nb) * cc, i1 = min(nd.m, i0 + cc);
-      for (int i = i0 + warp; i < i1; i += nw) {
-        const double *col = buf + (int64_t)(i - i0) * ld;
-        double sacc = 0;
-        for (int k = i + lane; k < n; k += 32) sacc = fma(col[k], u[k], sacc);
-        sacc = warp_sum(sacc);
-        if (lane == 0) vec[nd.off_s + i] = sacc;
-      }
+      ap_col_dots_n<true>(buf, ld, i0, i1, n, u, vec + nd.off_s, 0);
     }
     __syncthreads();
   }
@@ -4074,26 +4129,35 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
 // targets; slices own disjoint target entries).  Backward: k_apply_bwd_z
 // (partial Z x_T per slice into scratch) then k_apply_bwd_l (u = y - sum of
 // the partials in slice order, D u, x_s = L^{-T} u): deterministic.
-__global__ void __launch_bounds__(256) k_apply_fwd_y(const ApNode *__restrict__ nodes, double *__restrict__ vec) {
+// Split wave, forward: rows [P.c0, P.c1) (<= 64) of y = L^{-1}[:, :m] rhs for node
+// P.node, one CTA per row slab: 64 rows x 4 interleaved column groups (reads
+// coalesced down each column), the four partial sums combined in shared memory.
+__global__ void __launch_bounds__(256) k_apply_fwd_y(const ApNode *__restrict__ nodes, const ApPart *__restrict__ parts,
+                                                     double *__restrict__ vec) {
   pdl_enter();
   extern __shared__ __align__(16) double sh[];
-  const ApNode nd = nodes[blockIdx.x];
+  const ApPart P = parts[blockIdx.x];
+  const ApNode nd = nodes[P.node];
   const int n = nd.m + nd.r;
   if (n == 0) return;
-  double *rhs = sh;
+  double *rhs = sh, *red = sh + nd.m;   // m | 4 x 64 partial sums
   for (int i = threadIdx.x; i < nd.m; i += blockDim.x) rhs[i] = vec[nd.off_s + i];
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double s0 = 0, s1 = 0;
+  const int row = threadIdx.x & 63, grp = threadIdx.x >> 6, i = P.c0 + row;
+  double s0 = 0, s1 = 0;
+  if (i < P.c1) {
     const int kl = nd.full ? nd.m - 1 : min(nd.m - 1, i);
-    int k = 0;
-    for (; k + 1 <= kl; k += 2) {
-      s0 = fma(nd.F[i + (int64_t)k * nd.ld], rhs[k], s0);
-      s1 = fma(nd.F[i + (int64_t)(k + 1) * nd.ld], rhs[k + 1], s1);
+    const double *Fi = nd.F + i;
+    int k = grp;
+    for (; k + 4 <= kl; k += 8) {
+      s0 = fma(Fi[(int64_t)k * nd.ld], rhs[k], s0);
+      s1 = fma(Fi[(int64_t)(k + 4) * nd.ld], rhs[k + 4], s1);
     }
-    if (k <= kl) s0 = fma(nd.F[i + (int64_t)k * nd.ld], rhs[k], s0);
-    nd.y[i] = s0 + s1;
+    for (; k <= kl; k += 4) s0 = fma(Fi[(int64_t)k * nd.ld], rhs[k], s0);
   }
+  red[grp * 64 + row] = s0 + s1;
+  __syncthreads();
+  if (grp == 0 && i < P.c1) nd.y[i] = (red[row] + red[64 + row]) + (red[128 + row] + red[192 + row]);
 }
 
 __global__ void __launch_bounds__(256) k_apply_fwd_z(const ApNode *__restrict__ nodes, const ApPart *__restrict__ parts,
@@ -4194,23 +4258,27 @@ __global__ void __launch_bounds__(256) k_apply_bwd_z(const ApNode *__restrict__ 
   for (int i = tid; i < n; i += blockDim.x) upart[nd.upart + (int64_t)P.p * n + i] = u[i];
 }
 
-__global__ void __launch_bounds__(256) k_apply_bwd_l(const ApNode *__restrict__ nodes, const double *__restrict__ upart,
-                                                     double *__restrict__ vec) {
+// Split wave, backward: x_i = (L^{-1})^T D u for the columns i in [P.c0, P.c1)
+// of node P.node (u = y - the Z-part sums), one CTA per column slab, a warp
+// per column (each CTA forms u itself: n x nsplit loads).
+__global__ void __launch_bounds__(256) k_apply_bwd_l(const ApNode *__restrict__ nodes, const ApPart *__restrict__ parts,
+                                                     const double *__restrict__ upart, double *__restrict__ vec) {
   pdl_enter();
   extern __shared__ __align__(16) double sh[];
-  const ApNode nd = nodes[blockIdx.x];
+  const ApPart P = parts[blockIdx.x];
+  const ApNode nd = nodes[P.node];
   const int n = nd.m + nd.r;
   if (n == 0) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   double *u = sh;
-  for (int i = tid; i < n; i += blockDim.x) {
+  for (int i = tid + P.c0; i < n; i += blockDim.x) {   // rows >= c0 are all the columns read
     double acc = nd.y[i];
     for (int p = 0; p < nd.nsplit; ++p) acc -= upart[nd.upart + (int64_t)p * n + i];
     u[i] = (i < nd.m || !nd.sym) ? acc : -acc;   // D u
   }
   __syncthreads();
   const double *Lb = nd.F + nd.lb_off;
-  for (int i = warp; i < nd.m; i += nw) {
+  for (int i = P.c0 + warp; i < P.c1; i += nw) {
     const double *col = Lb + (int64_t)i * nd.ld;
     double sacc = 0;
     for (int k = i + lane; k < n; k += 32) sacc = fma(col[k], u[k], sacc);

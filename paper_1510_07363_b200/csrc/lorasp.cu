@@ -348,7 +348,8 @@ struct lorasp_ctx {
   std::vector<NodeRec> recs;
   // apply plan
   std::vector<int> ap_wave_begin;  // in recs order (factor order), per wave
-  std::vector<int> ap_part_begin;  // split apply: parts of wave w in [ap_part_begin[w], ap_part_begin[w+1])
+  std::vector<int> ap_part_begin;  // split apply: Z parts of wave w in [ap_part_begin[w], ap_ypart_begin[w])
+  std::vector<int> ap_ypart_begin, ap_lpart_begin, ap_part_end;   // then y row slabs, then L column slabs
   std::vector<char> ap_wave_split; // wave uses the split kernels
   // per-wave shared-memory footprint of the fused kernels (waves of small
   // records run many more CTAs per SM than the global worst case allows)
@@ -357,7 +358,7 @@ struct lorasp_ctx {
   DevBuf d_apparts, d_upart;
   bool no_split_apply = getenv("LORASP_NO_SPLIT_APPLY") != nullptr;
   std::vector<double> ap_wave_flops, ap_wave_bytes;  // per wave, one pass (fwd or bwd)
-  size_t ap_fwd_smem = 0, ap_bwd_smem = 0;
+  size_t ap_fwd_smem = 0, ap_bwd_smem = 0, ap_y_smem = 0;
   int ap_chunk = 0;
   // the forward + backward wave launches of one apply, captured once per
   // factorization (static after it) and replayed as one graph launch
@@ -2739,15 +2740,20 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
     }
     an.push_back(a);
     int n = rc.m + rc.r;
-    fwd = std::max(fwd, (size_t)(rc.m + n + rc.W + 2));   // rhs, y, Z^T D y
-    bwd = std::max(bwd, (size_t)(n + rc.W + 2));
+    fwd = std::max(fwd, (size_t)(rc.m + n + 2 * rc.W + 258));   // rhs, y, Z^T D y, target prefetch, partials
+    bwd = std::max(bwd, (size_t)(n + rc.W + 258));               // u, x_T, partials
     max_col = std::max(max_col, (size_t)rc.ld);
   }
   h->ap_wave_begin.push_back((int)h->recs.size());
-  // split apply: waves narrower than the GPU whose records are large get their
-  // Z columns spread over several CTAs (>= ~192 KB of Z per CTA)
+  // split apply: waves of few nodes (the upper levels) are latency-bound when one
+  // CTA streams a whole record; their Z columns are spread over CTAs (~64 KB of
+  // Z each), y = L^{-1} rhs over 64-row slabs and x = L^{-T} u over 32-column
+  // slabs
   std::vector<ApPart> parts;
-  h->ap_part_begin.assign(1, 0);
+  h->ap_part_begin.clear();
+  h->ap_ypart_begin.clear();
+  h->ap_lpart_begin.clear();
+  h->ap_part_end.clear();
   h->ap_wave_split.assign(h->ap_wave_begin.size() - 1, 0);
   int64_t utot = 0;
   for (size_t w = 0; w + 1 < h->ap_wave_begin.size(); ++w) {
@@ -2757,11 +2763,11 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
     if (!h->no_split_apply && !dist && cnt <= 64) {
       double zmax = 0;
       for (int q = b0; q < b1; ++q) zmax = std::max(zmax, 8.0 * (an[q].m + an[q].r) * an[q].W);
-      if (zmax >= 1024.0 * 1024) {   // a record of >= 1 MB would bound the wave's latency
+      if (zmax >= 64.0 * 1024) {
         const int cap = std::max(1, std::min(32, 444 / std::max(cnt, 1)));
         for (int q = b0; q < b1; ++q) {
           const double zbytes = 8.0 * (an[q].m + an[q].r) * an[q].W;
-          int k = (int)std::ceil(zbytes / (256.0 * 1024));
+          int k = (int)std::ceil(zbytes / (64.0 * 1024));
           k = std::max(1, std::min({k, cap, std::max(1, an[q].W)}));
           ns[q - b0] = k;
           split = split || k > 1;
@@ -2769,6 +2775,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       }
     }
     h->ap_wave_split[w] = split;
+    h->ap_part_begin.push_back((int)parts.size());
     if (split) {
       for (int q = b0; q < b1; ++q) {
         const int k = ns[q - b0], n = an[q].m + an[q].r, W = an[q].W;
@@ -2778,10 +2785,19 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         for (int pp = 0; pp < k; ++pp)
           parts.push_back(ApPart{q, (int)((int64_t)W * pp / k), (int)((int64_t)W * (pp + 1) / k), pp});
       }
+      h->ap_ypart_begin.push_back((int)parts.size());
+      for (int q = b0; q < b1; ++q)
+        for (int i0 = 0; i0 < an[q].m + an[q].r; i0 += 64)
+          parts.push_back(ApPart{q, i0, std::min(an[q].m + an[q].r, i0 + 64), 0});
+      h->ap_lpart_begin.push_back((int)parts.size());
+      for (int q = b0; q < b1; ++q)
+        for (int i0 = 0; i0 < an[q].m; i0 += 32) parts.push_back(ApPart{q, i0, std::min(an[q].m, i0 + 32), 0});
     } else {
       for (int q = b0; q < b1; ++q) an[q].nsplit = 1;
+      h->ap_ypart_begin.push_back((int)parts.size());
+      h->ap_lpart_begin.push_back((int)parts.size());
     }
-    h->ap_part_begin.push_back((int)parts.size());
+    h->ap_part_end.push_back((int)parts.size());
   }
   h->d_apparts.ensure(std::max<size_t>(1, parts.size()) * sizeof(ApPart), st);
   if (!parts.empty())
@@ -2808,6 +2824,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       throw Err(LORASP_E_ARG, "apply: node record too large for the shared-memory apply kernel");
     h->ap_chunk = (int)ch;
     h->ap_fwd_smem = fwd * 8 + 2 * ch * 8 + 64;
+    h->ap_y_smem = (fwd + 256) * 8;
     h->ap_bwd_smem = bwd * 8 + 2 * ch * 8 + 64;
     const size_t nwv = h->ap_wave_begin.size() - 1;
     h->ap_wave_ch.assign(nwv, (int)ch);
@@ -2818,8 +2835,8 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         for (int q = h->ap_wave_begin[w]; q < h->ap_wave_begin[w + 1]; ++q) {
           const NodeRec &rc = h->recs[q];
           const size_t n = rc.m + rc.r;
-          wf = std::max(wf, (size_t)(rc.m + n + rc.W + 2));
-          wb = std::max(wb, (size_t)(n + rc.W + 2));
+          wf = std::max(wf, (size_t)(rc.m + n + 2 * rc.W + 258));
+          wb = std::max(wb, (size_t)(n + rc.W + 258));
           // one stage holds a whole part of the record (L^{-1} columns or Z)
           wc = std::max(wc, std::max<size_t>(2 * (size_t)rc.ld + 2,
                                              (size_t)rc.ld * std::max<size_t>(n, (size_t)rc.W)));
@@ -2887,14 +2904,17 @@ void apply_wave(lorasp_ctx *h, int w, bool fwd, cudaStream_t s) {
     else launch_k(k_apply_bwd, b1 - b0, 256, h->ap_wave_bsm[w], s, nodes + b0, segs, vec, h->ap_wave_ch[w]);
     return;
   }
-  const ApPart *parts = h->d_apparts.as<ApPart>() + h->ap_part_begin[w];
-  const int np = h->ap_part_begin[w + 1] - h->ap_part_begin[w];
+  const ApPart *pall = h->d_apparts.as<ApPart>();
+  const ApPart *parts = pall + h->ap_part_begin[w], *yparts = pall + h->ap_ypart_begin[w],
+               *lparts = pall + h->ap_lpart_begin[w];
+  const int np = h->ap_ypart_begin[w] - h->ap_part_begin[w], ny = h->ap_lpart_begin[w] - h->ap_ypart_begin[w],
+            nl = h->ap_part_end[w] - h->ap_lpart_begin[w];
   if (fwd) {
-    launch_k(k_apply_fwd_y, b1 - b0, 256, h->ap_fwd_smem, s, nodes + b0, vec);
+    launch_k(k_apply_fwd_y, ny, 256, h->ap_y_smem, s, nodes, yparts, vec);
     launch_k(k_apply_fwd_z, np, 256, h->ap_fwd_smem, s, nodes, parts, segs, vec, h->ap_chunk);
   } else {
     launch_k(k_apply_bwd_z, np, 256, h->ap_bwd_smem, s, nodes, parts, segs, vec, h->d_upart.as<double>(), h->ap_chunk);
-    launch_k(k_apply_bwd_l, b1 - b0, 256, h->ap_bwd_smem, s, nodes + b0, h->d_upart.as<double>(), vec);
+    launch_k(k_apply_bwd_l, nl, 256, h->ap_bwd_smem, s, nodes, lparts, h->d_upart.as<double>(), vec);
   }
 }
 
@@ -2958,6 +2978,9 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
     sig.push_back((int64_t)(intptr_t)segs);
     sig.push_back((int64_t)(intptr_t)h->d_vec.p);
     sig.insert(sig.end(), h->ap_part_begin.begin(), h->ap_part_begin.end());
+    sig.insert(sig.end(), h->ap_ypart_begin.begin(), h->ap_ypart_begin.end());
+    sig.insert(sig.end(), h->ap_lpart_begin.begin(), h->ap_lpart_begin.end());
+    sig.insert(sig.end(), h->ap_part_end.begin(), h->ap_part_end.end());
     sig.insert(sig.end(), h->ap_wave_split.begin(), h->ap_wave_split.end());
     sig.insert(sig.end(), h->ap_wave_ch.begin(), h->ap_wave_ch.end());
     for (size_t v : h->ap_wave_fsm) sig.push_back((int64_t)v);
