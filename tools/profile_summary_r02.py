@@ -41,7 +41,7 @@ for c in r2:
     a, b = r1[c], r2[c]
     out.append(f"| {c} | {b['config']['n']:,} | {a['factor_ms']:.1f} -> {b['factor_ms']:.1f} | {b['value']/1e6:.2f} M | "
                f"{b['tflops_model']:.2f} | {b['krylov_ms']:.1f} ({b['krylov_iters']}) | {b['first_factor_ms']:.0f} | "
-               f"{b['roofline']['kernel']}, {b['roofline']['frac']:.3f} |")
+               f"{b['roofline']['kernel'].replace(' | ', ' or ')}, {b['roofline']['frac']:.3f} |")
 o4 = d.get("other_configs", {}).get("cfg4")
 if o4:
     out.append(f"\ncfg4 measured inside the default cfg2 run (`other_configs`): factor {o4['factor_ms']:.1f} ms "
@@ -53,7 +53,7 @@ k1 = r1["cfg2"]["kernels_warmup_step"]
 for k, v in sorted(d["kernels_warmup_step"].items(), key=lambda kv: -kv[1]["ms"]):
     tf = v["alg_flops"] / (v["ms"] / 1e3) / 1e12 if v["ms"] > 0 else 0
     old = k1.get(k, {}).get("ms", 0.0)
-    out.append(f"| {k} | {v['kernel']} | {old:.3f} -> {v['ms']:.3f} | {v['launches']} | {v['alg_flops']/1e9:.2f} | {tf:.2f} |")
+    out.append(f"| {k} | {v['kernel'].replace(' | ', ' or ')} | {old:.3f} -> {v['ms']:.3f} | {v['launches']} | {v['alg_flops']/1e9:.2f} | {tf:.2f} |")
 rows = list(csv.reader(open(P + "r02_launches_bench.csv")))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
 h = rows[hi]
