@@ -245,9 +245,23 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
-template <int NB>
+// Shared tiles of the DMMA kernel.  An operand whose rows are contiguous in
+// memory (A not transposed, B transposed) is staged k-major [16][GLD] (row
+// stride 72 doubles); one whose K is contiguous (A transposed, B not -- the
+// Gram, Schur and most products) is staged row-major [64][GLK] (row stride 20
+// doubles).  Both strides keep 16-byte aligned pairs for the 16-byte async
+// copies and put the fragment reads of lanes (g, tq) on 2 wavefronts, the
+// minimum for 32 doubles.
+constexpr int GLD = 72, GLK = 20, GSTAGE = 64 * GLK;   // 1280 >= 16 x 72
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, const void *gbase, int bytes) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(bytes ? gmem : gbase), "r"(bytes)
+               : "memory");
+}
+// AK: op(A) tile stored [i][k] (t.ta); BK: op(B) tile stored [j][k] (!t.tb)
+template <int NB, bool AK, bool BK>
 __device__ __forceinline__ void gemm2_tile_dmma(const GemmTask &t, const GemmSeg *__restrict__ segs,
-                                                double (*As)[G2K][GT + 1], double (*Bs)[G2K][GT + 1]) {
+                                                double (*As)[GSTAGE], double (*Bs)[GSTAGE]) {
   constexpr int TN = 8 * NB, CB = TN / 16;   // column fragments per warp
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp & 1, wc = warp >> 1;   // warp sub-tile: rows 32 wr.., cols (TN/2) wc..
@@ -260,28 +274,94 @@ __device__ __forceinline__ void gemm2_tile_dmma(const GemmTask &t, const GemmSeg
   for (int s = 0; s < t.nseg; ++s) {
     const GemmSeg gs = segs[t.seg0 + s];
     if (gs.K <= 0) continue;
+    // 16-byte copies when the contiguous pairs are 16-byte aligned
+    const bool a16 = (gs.lda & 1) == 0 && ((uintptr_t)gs.A & 15) == 0;
+    const bool b16 = (gs.ldb & 1) == 0 && ((uintptr_t)gs.B & 15) == 0;
     auto load = [&](int k0, int st) {
+      if constexpr (AK) {   // A(gk, gi) at A + gk + gi lda
+        if (a16) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int idx = tid + 128 * q;
-        int i, kk;
-        if (!t.ta) { i = idx & 63; kk = idx >> 6; } else { kk = idx & 15; i = idx >> 4; }
-        const int gi = t.tm + i, gk = k0 + kk;
-        cp_async8(&As[st][kk][i], t.ta ? gs.A + (gk + (int64_t)gi * gs.lda) : gs.A + (gi + (int64_t)gk * gs.lda),
-                  gs.A, gi < t.M && gk < gs.K);
+          for (int q = 0; q < 4; ++q) {
+            const int idx = tid + 128 * q, i = idx >> 3, kk = 2 * (idx & 7);
+            const int gi = t.tm + i, gk = k0 + kk;
+            const int nb = (gi < t.M) ? (gk + 1 < gs.K ? 16 : (gk < gs.K ? 8 : 0)) : 0;
+            cp_async16(&As[st][i * GLK + kk], gs.A + (gk + (int64_t)gi * gs.lda), gs.A, nb);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int idx = tid + 128 * q, kk = idx & 15, i = idx >> 4;
+            const int gi = t.tm + i, gk = k0 + kk;
+            cp_async8(&As[st][i * GLK + kk], gs.A + (gk + (int64_t)gi * gs.lda), gs.A, gi < t.M && gk < gs.K);
+          }
+        }
+      } else {   // A(gi, gk) at A + gi + gk lda
+        if (a16) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int idx = tid + 128 * q, i = 2 * (idx & 31), kk = idx >> 5;
+            const int gi = t.tm + i, gk = k0 + kk;
+            const int nb = (gk < gs.K) ? (gi + 1 < t.M ? 16 : (gi < t.M ? 8 : 0)) : 0;
+            cp_async16(&As[st][kk * GLD + i], gs.A + (gi + (int64_t)gk * gs.lda), gs.A, nb);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int idx = tid + 128 * q, i = idx & 63, kk = idx >> 6;
+            const int gi = t.tm + i, gk = k0 + kk;
+            cp_async8(&As[st][kk * GLD + i], gs.A + (gi + (int64_t)gk * gs.lda), gs.A, gi < t.M && gk < gs.K);
+          }
+        }
       }
+      if constexpr (BK) {   // B(gk, gj) at B + gk + gj ldb
+        if (b16) {
 #pragma unroll
-      for (int q = 0; q < TN / 8; ++q) {
-        const int idx = tid + 128 * q;
-        int j, kk;
-        if (!t.tb) { kk = idx & 15; j = idx >> 4; } else { j = idx % TN; kk = idx / TN; }
-        const int gj = t.tn + j, gk = k0 + kk;
-        cp_async8(&Bs[st][kk][j], t.tb ? gs.B + (gj + (int64_t)gk * gs.ldb) : gs.B + (gk + (int64_t)gj * gs.ldb),
-                  gs.B, gj < t.N && gk < gs.K);
+          for (int q = 0; q < TN / 16; ++q) {
+            const int idx = tid + 128 * q, j = idx >> 3, kk = 2 * (idx & 7);
+            const int gj = t.tn + j, gk = k0 + kk;
+            const int nb = (gj < t.N) ? (gk + 1 < gs.K ? 16 : (gk < gs.K ? 8 : 0)) : 0;
+            cp_async16(&Bs[st][j * GLK + kk], gs.B + (gk + (int64_t)gj * gs.ldb), gs.B, nb);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < TN / 8; ++q) {
+            const int idx = tid + 128 * q, kk = idx & 15, j = idx >> 4;
+            const int gj = t.tn + j, gk = k0 + kk;
+            cp_async8(&Bs[st][j * GLK + kk], gs.B + (gk + (int64_t)gj * gs.ldb), gs.B, gj < t.N && gk < gs.K);
+          }
+        }
+      } else {   // B(gj, gk) at B + gj + gk ldb
+        if (b16) {
+#pragma unroll
+          for (int q = 0; q < TN / 16; ++q) {
+            const int idx = tid + 128 * q, j = 2 * (idx % (TN / 2)), kk = idx / (TN / 2);
+            const int gj = t.tn + j, gk = k0 + kk;
+            const int nb = (gk < gs.K) ? (gj + 1 < t.N ? 16 : (gj < t.N ? 8 : 0)) : 0;
+            cp_async16(&Bs[st][kk * GLD + j], gs.B + (gj + (int64_t)gk * gs.ldb), gs.B, nb);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < TN / 8; ++q) {
+            const int idx = tid + 128 * q, j = idx % TN, kk = idx / TN;
+            const int gj = t.tn + j, gk = k0 + kk;
+            cp_async8(&Bs[st][kk * GLD + j], gs.B + (gj + (int64_t)gk * gs.ldb), gs.B, gj < t.N && gk < gs.K);
+          }
+        }
       }
       cp_async_commit();
     };
+    // alpha = +-1 (every product of the sweep): the sign goes on the
+    // accumulators around the segment (exact), no multiply per fragment
     const double alpha = gs.alpha;
+    const bool neg = alpha == -1.0, unit = neg || alpha == 1.0;
+    if (neg)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < CB; ++b) {
+          acc[a][b][0] = -acc[a][b][0];
+          acc[a][b][1] = -acc[a][b][1];
+        }
     const int nch = (gs.K + G2K - 1) / G2K;
     load(0, 0);
     for (int c = 0; c < nch; ++c) {
@@ -292,14 +372,21 @@ __device__ __forceinline__ void gemm2_tile_dmma(const GemmTask &t, const GemmSeg
         cp_async_wait<0>();
       }
       __syncthreads();
-      const int st = c & 1;
+      const double *Ast = As[c & 1], *Bst = Bs[c & 1];
 #pragma unroll
       for (int k4 = 0; k4 < G2K; k4 += 4) {
         double af[4], bf[CB];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) af[a] = alpha * As[st][k4 + tq][32 * wr + 8 * a + g];
+        for (int a = 0; a < 4; ++a) {
+          const int i = 32 * wr + 8 * a + g, k = k4 + tq;
+          const double v = AK ? Ast[i * GLK + k] : Ast[k * GLD + i];
+          af[a] = unit ? v : alpha * v;
+        }
 #pragma unroll
-        for (int b = 0; b < CB; ++b) bf[b] = Bs[st][k4 + tq][(TN / 2) * wc + 8 * b + g];
+        for (int b = 0; b < CB; ++b) {
+          const int j = (TN / 2) * wc + 8 * b + g, k = k4 + tq;
+          bf[b] = BK ? Bst[j * GLK + k] : Bst[k * GLD + j];
+        }
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -307,6 +394,14 @@ __device__ __forceinline__ void gemm2_tile_dmma(const GemmTask &t, const GemmSeg
       }
       __syncthreads();
     }
+    if (neg)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < CB; ++b) {
+          acc[a][b][0] = -acc[a][b][0];
+          acc[a][b][1] = -acc[a][b][1];
+        }
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -324,13 +419,22 @@ __device__ __forceinline__ void gemm2_tile_dmma(const GemmTask &t, const GemmSeg
 
 __global__ void __launch_bounds__(128, 4) k_gemm2_dmma(const GemmTask *__restrict__ tasks,
                                                      const GemmSeg *__restrict__ segs) {
-  __shared__ __align__(16) double As[2][G2K][GT + 1];
-  __shared__ __align__(16) double Bs[2][G2K][GT + 1];
+  __shared__ __align__(16) double As[2][GSTAGE];
+  __shared__ __align__(16) double Bs[2][GSTAGE];
   pdl_trigger();
   const GemmTask t = tasks[blockIdx.x];
   pdl_wait();
-  if (t.tnw == 32) gemm2_tile_dmma<4>(t, segs, As, Bs);
-  else gemm2_tile_dmma<8>(t, segs, As, Bs);
+  const int sel = (t.tnw == 32 ? 4 : 0) + (t.ta ? 2 : 0) + (t.tb ? 0 : 1);
+  switch (sel) {
+    case 0: gemm2_tile_dmma<8, false, false>(t, segs, As, Bs); break;
+    case 1: gemm2_tile_dmma<8, false, true>(t, segs, As, Bs); break;
+    case 2: gemm2_tile_dmma<8, true, false>(t, segs, As, Bs); break;
+    case 3: gemm2_tile_dmma<8, true, true>(t, segs, As, Bs); break;
+    case 4: gemm2_tile_dmma<4, false, false>(t, segs, As, Bs); break;
+    case 5: gemm2_tile_dmma<4, false, true>(t, segs, As, Bs); break;
+    case 6: gemm2_tile_dmma<4, true, false>(t, segs, As, Bs); break;
+    default: gemm2_tile_dmma<4, true, true>(t, segs, As, Bs); break;
+  }
 }
 
 struct EigTask {
