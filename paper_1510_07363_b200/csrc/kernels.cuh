@@ -4225,6 +4225,247 @@ __global__ void __launch_bounds__(256) k_apply_bwd(const ApNode *__restrict__ no
   }
 }
 
+// ---- dataflow apply (single GPU): one persistent launch per direction ------
+// Alg. 3 / Alg. 4 as a dependency graph instead of wave-synchronous launches:
+// CTAs claim nodes in elimination order (forward) or its reverse (backward)
+// from a global counter and start a node as soon as the nodes it depends on
+// have finished (per-node counters: a node's Z^T D y contributions, or its
+// targets' x, are complete) instead of waiting for the whole previous wave.
+// Forward contributions are not read-modify-written into the targets: each
+// node stores Z^T D y in its own slot of `zob`, and the reader subtracts its
+// contributions from its RHS in writer (= elimination) order -- the same
+// sequence of operations as the wave launches, so the result is bitwise
+// theirs.  A node only waits for nodes claimed before it, so the claimed
+// node of lowest index can always proceed (no residency assumption).  The
+// trailing waves whose few large records are split over CTAs (the wave path's
+// split kernels) stay wave launches: the forward pass then ends with flush
+// tasks that subtract the dataflow nodes' contributions from those readers'
+// RHS (in writer order), and the backward dataflow pass starts after them.
+struct ApDf {
+  int node;        // the apply node; a flush task (index >= the dataflow nodes) names the reader it updates
+  int fin, bin;    // notifications to wait for: forward (distinct writers), backward (distinct targets)
+  int c0, nc;      // contributions to this node's RHS, [c0, c0 + nc) of the contribution list (writer order)
+  int r0, nr;      // the nodes this node writes into (forward notifications), in dflist
+  int w0, nwr;     // the nodes writing into this node (backward notifications), in dflist
+  int64_t zo;      // this node's Z^T D y in zob (W doubles)
+};
+struct ApContrib {
+  int64_t src;     // zob offset of the first value
+  int off, w;      // offset inside the reader's RHS, width
+};
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void df_wait(const int *cnt, int need) {
+  if (threadIdx.x == 0)
+    while (ld_acquire(cnt) < need) __nanosleep(64);
+  __syncthreads();
+}
+__device__ __forceinline__ void df_notify(int *cnt, const int *list, int k0, int nk) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    for (int k = 0; k < nk; ++k) atomicAdd(cnt + list[k0 + k], 1);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_apply_fwd_df(const ApNode *__restrict__ nodes, const ApDf *__restrict__ dfs,
+                                                      const ApContrib *__restrict__ contr, const int *__restrict__ dfl,
+                                                      int nnodes, int ntasks, double *__restrict__ vec,
+                                                      double *__restrict__ zob, int *cnt, int *work, int chunk_doubles) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ int s_p;
+  const int tid = threadIdx.x;
+  double *stage0 = sh, *stage1 = sh + chunk_doubles, *rhs = stage1 + chunk_doubles;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t ph = 0;   // phase bit per stage
+  for (;;) {
+    if (tid == 0) s_p = atomicAdd(work, 1);
+    __syncthreads();
+    const int p = s_p;
+    if (p >= ntasks) break;
+    const ApDf df = dfs[p];
+    const ApNode nd = nodes[df.node];
+    if (p >= nnodes) {   // flush: a wave-launched reader's contributions from the dataflow nodes
+      df_wait(cnt + p, df.fin);
+      for (int i = tid; i < nd.m; i += blockDim.x) {
+        double v = __ldcg(vec + nd.off_s + i);
+        bool hit = false;
+        for (int c = 0; c < df.nc; ++c) {
+          const ApContrib C = contr[df.c0 + c];
+          if (i >= C.off && i < C.off + C.w) {
+            v -= __ldcg(zob + C.src + (i - C.off));
+            hit = true;
+          }
+        }
+        if (hit) vec[nd.off_s + i] = v;
+      }
+      __syncthreads();
+      continue;
+    }
+    const int n = nd.m + nd.r;
+    if (n == 0) {
+      df_wait(cnt + p, df.fin);
+      df_notify(cnt, dfl, df.r0, df.nr);
+      continue;
+    }
+    double *dy = rhs + nd.m, *part = dy + n;
+    const int ld = nd.ld;
+    const int cc = max(1, chunk_doubles / ld);
+    const double *Z = nd.F + nd.zf_off;
+    const int na = (nd.m + cc - 1) / cc, nb = (nd.W + cc - 1) / cc, ntot = na + nb;
+    auto issue = [&](int c) {
+      const double *src;
+      int c0, c1;
+      if (c < na) {
+        c0 = c * cc;
+        c1 = min(nd.m, c0 + cc);
+        src = nd.F + (int64_t)c0 * ld;
+      } else {
+        c0 = (c - na) * cc;
+        c1 = min(nd.W, c0 + cc);
+        src = Z + (int64_t)c0 * ld;
+      }
+      const uint32_t bytes = (uint32_t)((int64_t)(c1 - c0) * ld * 8);
+      fence_proxy_async();
+      mbar_expect_tx(&bars[c & 1], bytes);
+      bulk_g2s((c & 1) ? stage1 : stage0, src, bytes, &bars[c & 1]);
+    };
+    if (tid == 0) {   // the record is static: fetched before the dependencies are met
+      if (ntot > 0) issue(0);
+      if (ntot > 1) issue(1);
+    }
+    df_wait(cnt + p, df.fin);
+    // RHS = initial entries minus the contributions, in writer order per entry
+    for (int i = tid; i < nd.m; i += blockDim.x) {
+      double v = __ldcg(vec + nd.off_s + i);
+      for (int c = 0; c < df.nc; ++c) {
+        const ApContrib C = contr[df.c0 + c];
+        if (i >= C.off && i < C.off + C.w) v -= __ldcg(zob + C.src + (i - C.off));
+      }
+      rhs[i] = v;
+    }
+    for (int i = tid; i < n; i += blockDim.x) dy[i] = 0.0;
+    __syncthreads();
+    for (int c = 0; c < ntot; ++c) {
+      if (tid == 0 && c >= 1 && c + 1 < ntot) issue(c + 1);
+      mbar_wait(&bars[c & 1], (ph >> (c & 1)) & 1);
+      ph ^= 1u << (c & 1);
+      const double *buf = (c & 1) ? stage1 : stage0;
+      if (c < na) {
+        const int k0 = c * cc, k1 = min(nd.m, k0 + cc);
+        ap_row_sums<false>(buf, ld, k0, k1, n, !nd.full, rhs, dy, part);
+        if (c == na - 1) {
+          for (int i = tid; i < n; i += blockDim.x) {
+            const double y = dy[i];
+            nd.y[i] = y;
+            dy[i] = (i < nd.m || !nd.sym) ? y : -y;
+          }
+        }
+      } else {
+        const int j0 = (c - na) * cc, j1 = min(nd.W, j0 + cc);
+        ap_col_dots_n<false>(buf, ld, j0, j1, n, dy, zob + df.zo, 0);
+      }
+      __syncthreads();
+    }
+    if (na == 0)
+      for (int i = tid; i < n; i += blockDim.x) nd.y[i] = 0.0;
+    df_notify(cnt, dfl, df.r0, df.nr);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_apply_bwd_df(const ApNode *__restrict__ nodes, const ApDf *__restrict__ dfs,
+                                                      const ApSeg *__restrict__ segs, const int *__restrict__ dfl,
+                                                      int nnodes, double *__restrict__ vec, int *cnt, int *work,
+                                                      int chunk_doubles) {
+  extern __shared__ __align__(16) double sh[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ int s_p;
+  const int tid = threadIdx.x;
+  double *stage0 = sh, *stage1 = sh + chunk_doubles, *u = stage1 + chunk_doubles;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  uint32_t ph = 0;
+  for (;;) {
+    if (tid == 0) s_p = atomicAdd(work, 1);
+    __syncthreads();
+    const int p = nnodes - 1 - s_p;
+    if (p < 0) break;
+    const ApDf df = dfs[p];
+    const ApNode nd = nodes[df.node];
+    const int n = nd.m + nd.r;
+    if (n == 0) {
+      df_wait(cnt + p, df.bin);
+      df_notify(cnt, dfl, df.w0, df.nwr);
+      continue;
+    }
+    double *xt = u + n, *part = xt + nd.W;
+    const int ld = nd.ld;
+    const int cc = max(1, chunk_doubles / ld);
+    const double *Z = nd.F + nd.zb_off, *Lb = nd.F + nd.lb_off;
+    const int nb = (nd.W + cc - 1) / cc, na = (nd.m + cc - 1) / cc, ntot = nb + na;
+    auto issue = [&](int c) {
+      const double *src;
+      int c0, c1;
+      if (c < nb) {
+        c0 = c * cc;
+        c1 = min(nd.W, c0 + cc);
+        src = Z + (int64_t)c0 * ld;
+      } else {
+        c0 = (c - nb) * cc;
+        c1 = min(nd.m, c0 + cc);
+        src = Lb + (int64_t)c0 * ld;
+      }
+      const uint32_t bytes = (uint32_t)((int64_t)(c1 - c0) * ld * 8);
+      fence_proxy_async();
+      mbar_expect_tx(&bars[c & 1], bytes);
+      bulk_g2s((c & 1) ? stage1 : stage0, src, bytes, &bars[c & 1]);
+    };
+    if (tid == 0) {
+      if (ntot > 0) issue(0);
+      if (ntot > 1) issue(1);
+    }
+    df_wait(cnt + p, df.bin);
+    for (int sg = 0; sg < nd.nseg; ++sg) {
+      const ApSeg S = segs[nd.seg0 + sg];
+      for (int j = tid; j < S.w; j += blockDim.x) xt[S.zc + j] = __ldcg(vec + S.voff + j);
+    }
+    for (int i = tid; i < n; i += blockDim.x) u[i] = __ldcg(nd.y + i);
+    __syncthreads();
+    for (int c = 0; c < ntot; ++c) {
+      if (tid == 0 && c >= 1 && c + 1 < ntot) issue(c + 1);
+      mbar_wait(&bars[c & 1], (ph >> (c & 1)) & 1);
+      ph ^= 1u << (c & 1);
+      const double *buf = (c & 1) ? stage1 : stage0;
+      if (c < nb) {
+        const int j0 = c * cc, j1 = min(nd.W, j0 + cc);
+        ap_row_sums<true>(buf, ld, j0, j1, n, false, xt, u, part);
+        if (c == nb - 1 && nd.sym)
+          for (int i = nd.m + tid; i < n; i += blockDim.x) u[i] = -u[i];   // D u
+      } else {
+        if (nb == 0 && c == 0 && nd.sym) {
+          for (int i = nd.m + tid; i < n; i += blockDim.x) u[i] = -u[i];
+          __syncthreads();
+        }
+        const int i0 = (c - nb) * cc, i1 = min(nd.m, i0 + cc);
+        ap_col_dots_n<true>(buf, ld, i0, i1, n, u, vec + nd.off_s, 0);
+      }
+      __syncthreads();
+    }
+    df_notify(cnt, dfl, df.w0, df.nwr);
+  }
+}
+
 // ---- split apply (waves with few, large records) --------------------------
 // The fused kernels stream a node's whole record with one CTA; for the upper
 // levels (few nodes per wave, records of MBs) the Z columns are split over

@@ -357,6 +357,14 @@ struct lorasp_ctx {
   std::vector<size_t> ap_wave_fsm, ap_wave_bsm;
   DevBuf d_apparts, d_upart;
   bool no_split_apply = getenv("LORASP_NO_SPLIT_APPLY") != nullptr;
+  // dataflow apply (single GPU): one persistent launch per direction with
+  // per-node dependency counters (k_apply_fwd_df / k_apply_bwd_df); bitwise the
+  // wave launches' result (LORASP_NO_DF selects the wave launches, for the tests)
+  bool no_df = getenv("LORASP_NO_DF") != nullptr;
+  bool ap_df_ok = false;
+  DevBuf d_apdf, d_apcontr, d_apdfl, d_zob, d_dfcnt;
+  int ap_df_n = 0, ap_df_nt = 0, ap_df_wave = 0, ap_df_ch = 0, ap_df_gf = 0, ap_df_gb = 0;
+  size_t ap_df_fsm = 0, ap_df_bsm = 0;
   std::vector<double> ap_wave_flops, ap_wave_bytes;  // per wave, one pass (fwd or bwd)
   size_t ap_fwd_smem = 0, ap_bwd_smem = 0, ap_y_smem = 0;
   int ap_chunk = 0;
@@ -721,6 +729,8 @@ void ensure_mem(lorasp_ctx *h) {
   CK(cudaFuncSetAttribute(k_apply_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_fwd_y, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_apply_fwd_df, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_apply_bwd_df, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_fwd_z, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_bwd_z, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_bwd_l, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
@@ -2875,6 +2885,137 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         h->ap_wave_bsm[w] = wb * 8 + 2 * wc * 8 + 64;
       }
   }
+  // dataflow apply plan: the reader of every forward segment (the node whose RHS
+  // range contains it), per reader its contributions in writer order, per node
+  // the distinct readers / writers to notify
+  h->ap_df_ok = false;
+  if (!dist && !h->no_df && !an.empty()) {
+    // the dataflow part: every node before the first split wave
+    // (the top of the tree -- from the first wave holding a record of >= 1 MB of
+    // Z after which every wave has <= 64 nodes -- stays wave launches, whose
+    // split kernels spread such records over CTAs; one CTA would stream them)
+    const int nwv = (int)h->ap_wave_split.size();
+    int S = nwv;
+    {
+      int few = nwv;   // first wave of the suffix with <= 64 nodes per wave
+      while (few > 0 && h->ap_wave_begin[few] - h->ap_wave_begin[few - 1] <= 64) --few;
+      for (int w = few; w < nwv; ++w) {
+        double zmax = 0;
+        for (int q = h->ap_wave_begin[w]; q < h->ap_wave_begin[w + 1]; ++q)
+          zmax = std::max(zmax, 8.0 * (an[q].m + an[q].r) * an[q].W);
+        if (zmax >= 1024.0 * 1024) {
+          S = w;
+          break;
+        }
+      }
+    }
+    h->ap_df_wave = S;
+    const int NA = (int)an.size();
+    const int N = h->ap_wave_begin[S];
+    std::vector<std::pair<int64_t, int>> rng;
+    for (int q = 0; q < NA; ++q)
+      if (an[q].m > 0) rng.push_back({an[q].off_s, q});
+    std::sort(rng.begin(), rng.end());
+    std::vector<int64_t> zoff(N);
+    int64_t ztot = 0;
+    for (int q = 0; q < N; ++q) {
+      zoff[q] = ztot;
+      ztot += an[q].W;
+    }
+    // task index of a reader: a dataflow node itself, or the flush task of a
+    // wave-launched reader (indices N, N + 1, ...)
+    std::vector<int> task_of(NA, -1), flush_node;
+    for (int q = 0; q < N; ++q) task_of[q] = q;
+    std::vector<std::vector<int>> Rl(N), Wl;
+    std::vector<std::vector<ApContrib>> CT(N);
+    Wl.resize(N);
+    std::vector<int> nreal(N, 0);   // distinct dataflow readers (backward waits)
+    bool ok = true;
+    for (int p = 0; p < N && ok; ++p)
+      for (int k = an[p].seg0; k < an[p].seg0 + an[p].nseg; ++k) {
+        const ApSeg &Sg = as[k];
+        auto it = std::upper_bound(rng.begin(), rng.end(), std::make_pair(Sg.voff, INT32_MAX));
+        if (it == rng.begin()) { ok = false; break; }
+        const int q = std::prev(it)->second;
+        if (q <= p || Sg.voff + Sg.w > an[q].off_s + an[q].m) { ok = false; break; }
+        if (task_of[q] < 0) {
+          task_of[q] = N + (int)flush_node.size();
+          flush_node.push_back(q);
+          CT.emplace_back();
+          Wl.emplace_back();
+        }
+        const int tq = task_of[q];
+        CT[tq].push_back(ApContrib{zoff[p] + Sg.zc, (int)(Sg.voff - an[q].off_s), Sg.w});
+        if (std::find(Rl[p].begin(), Rl[p].end(), tq) == Rl[p].end()) {
+          Rl[p].push_back(tq);
+          if (tq < N) ++nreal[p];
+        }
+        if (std::find(Wl[tq].begin(), Wl[tq].end(), p) == Wl[tq].end()) Wl[tq].push_back(p);
+      }
+    const int NT = N + (int)flush_node.size();
+    if (ok && N > 0) {
+      std::vector<ApDf> df(NT);
+      std::vector<ApContrib> cl;
+      std::vector<int> dl;
+      size_t fmx = 0, bmx = 0;
+      for (int q = 0; q < NT; ++q) {
+        ApDf &d = df[q];
+        d.node = q < N ? q : flush_node[q - N];
+        d.fin = (int)Wl[q].size();
+        if (q >= N) {
+          d.c0 = (int)cl.size();
+          d.nc = (int)CT[q].size();
+          cl.insert(cl.end(), CT[q].begin(), CT[q].end());
+          continue;
+        }
+        d.bin = nreal[q];
+        d.c0 = (int)cl.size();
+        d.nc = (int)CT[q].size();
+        cl.insert(cl.end(), CT[q].begin(), CT[q].end());
+        d.r0 = (int)dl.size();
+        d.nr = (int)Rl[q].size();
+        dl.insert(dl.end(), Rl[q].begin(), Rl[q].end());
+        d.w0 = (int)dl.size();
+        d.nwr = (int)Wl[q].size();
+        dl.insert(dl.end(), Wl[q].begin(), Wl[q].end());
+        d.zo = zoff[q];
+        const size_t n = (size_t)an[q].m + an[q].r;
+        fmx = std::max(fmx, (size_t)an[q].m + n + 258);   // rhs, y, partials
+        bmx = std::max(bmx, n + (size_t)an[q].W + 258);   // u, x_T, partials
+      }
+      h->d_apdf.ensure(NT * sizeof(ApDf), st);
+      h->d_apcontr.ensure(std::max<size_t>(1, cl.size()) * sizeof(ApContrib), st);
+      h->d_apdfl.ensure(std::max<size_t>(1, dl.size()) * sizeof(int), st);
+      h2d_sync(h->d_apdf.p, df.data(), NT * sizeof(ApDf), st);
+      if (!cl.empty()) h2d_sync(h->d_apcontr.p, cl.data(), cl.size() * sizeof(ApContrib), st);
+      if (!dl.empty()) h2d_sync(h->d_apdfl.p, dl.data(), dl.size() * sizeof(int), st);
+      h->d_zob.ensure(std::max<int64_t>(ztot, 8) * 8, st);
+      h->d_dfcnt.ensure((NT + 8) * sizeof(int), st);
+      h->ap_df_nt = NT;
+      // 2-stage ring per CTA sized for ~3 CTAs per SM (>= 2 columns per stage)
+      size_t ch = ((size_t)SMEM_LIMIT / 3 > std::max(fmx, bmx) * 8 + 256)
+                      ? ((size_t)SMEM_LIMIT / 3 - std::max(fmx, bmx) * 8 - 256) / 16 : 0;
+      ch = std::max(ch, 2 * max_col + 2);
+      ch = std::min<size_t>(ch, 48 * 1024 / 8);
+      ch = std::max(ch, 2 * max_col + 2);
+      ch = (ch + 1) & ~size_t(1);
+      h->ap_df_ch = (int)ch;
+      h->ap_df_fsm = fmx * 8 + 2 * ch * 8 + 64;
+      h->ap_df_bsm = bmx * 8 + 2 * ch * 8 + 64;
+      if (h->ap_df_fsm <= (size_t)SMEM_LIMIT && h->ap_df_bsm <= (size_t)SMEM_LIMIT) {
+        int dev = 0, nsm = 148, of = 1, ob = 1;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, k_apply_fwd_df, 256, h->ap_df_fsm));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ob, k_apply_bwd_df, 256, h->ap_df_bsm));
+        h->ap_df_gf = std::max(1, std::min(NT, nsm * std::max(1, of)));
+        h->ap_df_gb = std::max(1, std::min(N, nsm * std::max(1, ob)));
+        h->ap_df_n = N;
+        h->ap_df_ok = true;
+      }
+    }
+    if (h->debug && !h->ap_df_ok) fprintf(stderr, "[lorasp] dataflow apply plan not built (ok=%d)\n", (int)ok);
+  }
   h->d_apnodes.ensure(std::max<size_t>(1, an.size()) * sizeof(ApNode), st);
   h->d_apsegs.ensure(std::max<size_t>(1, as.size()) * sizeof(ApSeg), st);
   h2d_sync(h->d_apnodes.p, an.data(), an.size() * sizeof(ApNode), st);
@@ -2915,6 +3056,24 @@ void apply_wave(lorasp_ctx *h, int w, bool fwd, cudaStream_t s) {
   } else {
     launch_k(k_apply_bwd_z, np, 256, h->ap_bwd_smem, s, nodes, parts, segs, vec, h->d_upart.as<double>(), h->ap_chunk);
     launch_k(k_apply_bwd_l, nl, 256, h->ap_bwd_smem, s, nodes, lparts, h->d_upart.as<double>(), vec);
+  }
+}
+
+// Alg. 3 (fwd) or Alg. 4 (bwd) as one persistent dataflow launch (single GPU)
+void apply_df(lorasp_ctx *h, bool fwd, cudaStream_t s) {
+  const int N = h->ap_df_n, NT = h->ap_df_nt, nw = (int)h->ap_wave_begin.size() - 1;
+  int *cnt = h->d_dfcnt.as<int>(), *work = cnt + NT;
+  if (fwd) {
+    CK(cudaMemsetAsync(cnt, 0, (NT + 1) * sizeof(int), s));
+    launch_k(k_apply_fwd_df, h->ap_df_gf, 256, h->ap_df_fsm, s, h->d_apnodes.as<ApNode>(), h->d_apdf.as<ApDf>(),
+             h->d_apcontr.as<ApContrib>(), h->d_apdfl.as<int>(), N, NT, h->d_vec.as<double>(),
+             h->d_zob.as<double>(), cnt, work, h->ap_df_ch);
+    for (int w = h->ap_df_wave; w < nw; ++w) apply_wave(h, w, true, s);
+  } else {
+    for (int w = nw - 1; w >= h->ap_df_wave; --w) apply_wave(h, w, false, s);
+    CK(cudaMemsetAsync(cnt, 0, (NT + 1) * sizeof(int), s));
+    launch_k(k_apply_bwd_df, h->ap_df_gb, 256, h->ap_df_bsm, s, h->d_apnodes.as<ApNode>(), h->d_apdf.as<ApDf>(),
+             h->d_apsegs.as<ApSeg>(), h->d_apdfl.as<int>(), N, h->d_vec.as<double>(), cnt, work, h->ap_df_ch);
   }
 }
 
@@ -2987,6 +3146,17 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
     for (size_t v : h->ap_wave_bsm) sig.push_back((int64_t)v);
     sig.push_back((int64_t)(intptr_t)h->d_apparts.p);
     sig.push_back((int64_t)(intptr_t)h->d_upart.p);
+    sig.push_back(h->ap_df_ok);
+    sig.push_back(h->ap_df_n);
+    sig.push_back(h->ap_df_nt);
+    sig.push_back(h->ap_df_wave);
+    sig.push_back(h->ap_df_ch);
+    sig.push_back(h->ap_df_gf);
+    sig.push_back(h->ap_df_gb);
+    sig.push_back((int64_t)h->ap_df_fsm);
+    sig.push_back((int64_t)h->ap_df_bsm);
+    for (DevBuf *b : {&h->d_apdf, &h->d_apcontr, &h->d_apdfl, &h->d_zob, &h->d_dfcnt})
+      sig.push_back((int64_t)(intptr_t)b->p);
     if (h->ap_graph && sig != h->ap_graph_sig) {
       CK(cudaGraphExecDestroy(h->ap_graph));
       h->ap_graph = nullptr;
@@ -2999,8 +3169,13 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
       CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       cudaGraph_t g;
       CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-      for (int w = 0; w < nw; ++w) apply_wave(h, w, true, cs);
-      for (int w = nw - 1; w >= 0; --w) apply_wave(h, w, false, cs);
+      if (h->ap_df_ok) {
+        apply_df(h, true, cs);
+        apply_df(h, false, cs);
+      } else {
+        for (int w = 0; w < nw; ++w) apply_wave(h, w, true, cs);
+        for (int w = nw - 1; w >= 0; --w) apply_wave(h, w, false, cs);
+      }
       const cudaError_t ce = cudaStreamEndCapture(cs, &g);
       cudaStreamDestroy(cs);
       CK(ce);
@@ -3022,6 +3197,18 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
       tend(h, evg, fl, by);
       h->pend[evg].nl = 2 * nw;
     }
+  } else if (h->ap_df_ok) {
+    double fl = 0, by = 0;
+    for (int w = 0; w < nw; ++w) {
+      fl += h->ap_wave_flops[w];
+      by += h->ap_wave_bytes[w];
+    }
+    ev = tbeg(h, K_APPLY_FWD);
+    apply_df(h, true, st);
+    tend(h, ev, fl, by);
+    ev = tbeg(h, K_APPLY_BWD);
+    apply_df(h, false, st);
+    tend(h, ev, fl, by);
   } else {
   for (int w = 0; w < nw; ++w) {
     ev = tbeg(h, K_APPLY_FWD);
@@ -3742,7 +3929,7 @@ int lorasp_get_stats(lorasp_handle h, char *buf, size_t cap, size_t *len) {
       << ",\"t_rank_sync_wait_ms\":" << h->t_sync_ms << ",\"launches_factor\":" << h->launches_factor
       << ",\"schedule_rank_predicted\":" << (h->replay_used ? "true" : "false")
       << ",\"rank_prediction_hits\":" << h->replay_hits << ",\"rank_prediction_misses\":" << h->replay_misses
-      << ",\"split_pivot_nodes\":" << h->split_nodes << ",\"factor_graph\":" << (h->fgraph_used ? "true" : "false")
+      << ",\"split_pivot_nodes\":" << h->split_nodes << ",\"factor_graph\":" << (h->fgraph_used ? "true" : "false") << ",\"apply_dataflow\":" << (h->ap_df_ok ? "true" : "false")
       << ",\"factor_graph_captures\":" << h->fg_captures << ",\"factor_graph_launches\":" << h->fg_launches
       << ",\"factor_graph_failures\":" << h->fg_failures << ",\"dist_world\":" << h->dist_world
       << ",\"dist_rank\":" << h->dist_rank << ",\"dist_exchange_calls\":" << h->dist_calls
@@ -4129,6 +4316,7 @@ void lorasp_destroy(lorasp_handle h) {
     h->ws_piv2.release();
     h->d_sp.release();
     h->d_apparts.release();
+    for (DevBuf *b : {&h->d_apdf, &h->d_apcontr, &h->d_apdfl, &h->d_zob, &h->d_dfcnt}) b->release();
     h->d_upart.release();
     h->fpool.release();
     h->stg.release();

@@ -31,14 +31,17 @@ def L():
 
 
 def _single(L, p):
-    # the distributed apply runs the fused one-CTA-per-node apply kernels; the
-    # single-GPU reference does the same (no split apply) so that x is bitwise comparable
+    # the distributed apply runs the fused one-CTA-per-node apply kernels wave by
+    # wave; the single-GPU reference does the same (no split apply, no dataflow
+    # apply) so that x is bitwise comparable
     import os
     os.environ["LORASP_NO_SPLIT_APPLY"] = "1"
+    os.environ["LORASP_NO_DF"] = "1"
     try:
         h = L.analyze_problem(p)
     finally:
         del os.environ["LORASP_NO_SPLIT_APPLY"]
+        del os.environ["LORASP_NO_DF"]
     h.factor(p.values)
     x = np.zeros(p.n)
     h.apply(p.b, x)
