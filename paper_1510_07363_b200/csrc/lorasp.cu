@@ -2993,8 +2993,15 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
       h->d_dfcnt.ensure((NT + 8) * sizeof(int), st);
       h->ap_df_nt = NT;
       // 2-stage ring per CTA sized for ~3 CTAs per SM (>= 2 columns per stage)
-      size_t ch = ((size_t)SMEM_LIMIT / 3 > std::max(fmx, bmx) * 8 + 256)
-                      ? ((size_t)SMEM_LIMIT / 3 - std::max(fmx, bmx) * 8 - 256) / 16 : 0;
+      // CTAs per SM: 4 when the leaf waves are several times wider than the GPU
+      // (throughput: more bulk copies in flight), else 2 (larger stages, shorter
+      // per-node chains) -- measured: cfg4 / cfg5 Krylov -6 % / -5 % at 4 vs 3,
+      // cfg2 / cfg3 -6 % / -3 % at 2
+      int wmax = 0;
+      for (int w = 0; w < S; ++w) wmax = std::max(wmax, h->ap_wave_begin[w + 1] - h->ap_wave_begin[w]);
+      const int dfo = wmax >= 4 * 148 ? 4 : 2;
+      size_t ch = ((size_t)SMEM_LIMIT / dfo > std::max(fmx, bmx) * 8 + 256)
+                      ? ((size_t)SMEM_LIMIT / dfo - std::max(fmx, bmx) * 8 - 256) / 16 : 0;
       ch = std::max(ch, 2 * max_col + 2);
       ch = std::min<size_t>(ch, 48 * 1024 / 8);
       ch = std::max(ch, 2 * max_col + 2);
