@@ -296,7 +296,7 @@ static const char *KNAME[K_NCLASS] = {"leaf_scatter", "merge_copy", "gram_gemm",
                                       "project_gemm", "assemble_copy", "pivot_chol_inv", "trsm_gemm",
                                       "schur_gemm", "apply_fwd", "apply_bwd", "spmv", "dot", "vec"};
 static const char *KKERNEL[K_NCLASS] = {"k_leaf_scatter", "k_copy", "k_gemm2_dmma", "k_eig_warp | k_tridiag_* + k_eig_t", "k_gemm2_dmma", "k_copy",
-                                        "k_pivot", "k_gemm2_dmma", "k_gemm2_dmma", "k_apply_fwd", "k_apply_bwd",
+                                        "k_pivot", "k_gemm2_dmma", "k_gemm2_dmma", "k_apply_fwd_df + k_apply_bwd_df | k_apply_fwd", "k_apply_bwd",
                                         "k_spmv", "k_dot_partial+k_dot_final", "k_axpby/k_sub/k_set_rhs/k_get_x"};
 struct KStat {
   double ms = 0, flops = 0, bytes = 0;
@@ -2950,7 +2950,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           Rl[p].push_back(tq);
           if (tq < N) ++nreal[p];
         }
-        if (std::find(Wl[tq].begin(), Wl[tq].end(), p) == Wl[tq].end()) Wl[tq].push_back(p);
+        if (Wl[tq].empty() || Wl[tq].back() != p) Wl[tq].push_back(p);   // writers arrive in order
       }
     const int NT = N + (int)flush_node.size();
     if (ok && N > 0) {
@@ -3202,7 +3202,12 @@ void apply_dev(lorasp_ctx *h, const double *b, double *x, int64_t *counter) {
         by += 2 * h->ap_wave_bytes[w];
       }
       tend(h, evg, fl, by);
-      h->pend[evg].nl = 2 * nw;
+      int nl = 2 * nw;
+      if (h->ap_df_ok) {   // two dataflow launches + the trailing waves' launches
+        nl = 2;
+        for (int w = h->ap_df_wave; w < nw; ++w) nl += h->ap_wave_split[w] ? 4 : 2;
+      }
+      h->pend[evg].nl = nl;
     }
   } else if (h->ap_df_ok) {
     double fl = 0, by = 0;

@@ -1,3 +1,5 @@
+# Round-2 measurement commands (run from the repo root on one B200 via gpurun);
+# outputs land in gpurun_out/ and are copied to profiles/ by hand.
 set -x
 python bench.py > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err
 python bench.py --config cfg3 --steps 3 --no-cpu-baseline > gpurun_out/r02_bench_cfg3.json 2>&1
@@ -6,8 +8,11 @@ python bench.py --config cfg5 --steps 3 --no-cpu-baseline > gpurun_out/r02_bench
 python bench.py --config adv32 --adv-R 128 --steps 3 --no-cpu-baseline > gpurun_out/r02_bench_adv32.json 2>&1
 python bench.py --compressor rrqr --steps 5 --no-cpu-baseline --extra none > gpurun_out/r02_bench_rrqr_cfg2.json 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/r02_launches_bench.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --extra none > gpurun_out/ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_tridiag_reg|k_eig_t" -s 2 -c 2 -o gpurun_out/r02_eig_leaf python tools/profile_run.py cfg2 1 > gpurun_out/ncu_eig.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_pivot_blk" -s 2 -c 1 -o gpurun_out/r02_pivot_leaf python tools/profile_run.py cfg2 1 > gpurun_out/ncu_piv.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_gemm2_dmma" -s 40 -c 3 -o gpurun_out/r02_gemm_cfg4 python tools/profile_run.py cfg4 1 > gpurun_out/ncu_gemm.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_tridiag_reg|k_eig_t|k_eig_warp" --csv --log-file gpurun_out/r02_eig_traffic.csv python tools/profile_run.py cfg2 1 > gpurun_out/ncu_eigtr.log 2>&1
+# one cfg4 preconditioner application (after one factorization): DRAM bytes of every apply kernel
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_apply" --csv --log-file gpurun_out/r02_apply_traffic_cfg4.csv python tools/apply_profile.py cfg4 1 > gpurun_out/ncu_aptr.log 2>&1
+# full captures: the cfg4 leaf Schur GEMM, the cfg4 dataflow apply (forward), the cfg3 cluster eigen kernels
+ncu --set full --clock-control none --import-source on -k regex:"k_gemm2_dmma" -s 40 -c 2 -o gpurun_out/r02_gemm_cfg4 python tools/profile_run.py cfg4 1 > gpurun_out/ncu_gemm.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_apply_fwd_df" -c 1 -o gpurun_out/r02_applydf_cfg4 python tools/apply_profile.py cfg4 1 > gpurun_out/ncu_apdf.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_orth_bgs|k_eigvals_cl|k_tridiag_cl" -s 30 -c 3 -o gpurun_out/r02_eigcl_cfg3 python tools/profile_run.py cfg3 1 > gpurun_out/ncu_eigcl.log 2>&1
 ls -la gpurun_out/
