@@ -448,6 +448,7 @@ struct lorasp_ctx {
   std::vector<std::vector<uint32_t>> slot_readers;
   std::vector<int64_t> a2a_counts;   // world x world, bytes, [src * world + dst]
   int piv_maxn_hint = 0;   // batch-independent pivot path choice (max n of the whole wave)
+  int piv_cnt_hint = 0;    // ... and its node count (distributed: every rank's nodes)
   // recorded factorization: a verified rank-predicted sweep captured once as a
   // CUDA graph (descriptors resident in fg_desc) and replayed while the ranks,
   // the allocations and the timing mask stay the same
@@ -1211,7 +1212,11 @@ void pivots(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, double 
   int ev = tbeg(h, K_PIVOT);
   if (!small.empty()) {
     PivTask *dp = push(h, small);
-    if (max_n <= PIVW_MAXN) {   // one warp per node
+    // one warp per node when the wave is wide (throughput: several nodes per SM);
+    // a few nodes run faster on the block kernel (measured per node: ~40-55 us for
+    // the warp kernel vs ~22 us for k_pivot_blk at n = 32)
+    const bool wide = (h->piv_cnt_hint > 0 ? (size_t)h->piv_cnt_hint : small.size()) > 2 * 148;
+    if (max_n <= PIVW_MAXN && wide) {
       constexpr int W = PivW<1>::WARPS;
       launch_k(k_pivot_warp<1>, (unsigned)((small.size() + W - 1) / W), 32 * W, PivW<1>::SMEM, st, (const PivTask *)dp,
                (int)small.size(), h->d_status.as<int>());
@@ -1253,7 +1258,8 @@ void pivots_lu(lorasp_ctx *h, const std::vector<PivTask> &pv, double f_piv, doub
   }
   PivTask *dp = push(h, h->lu_pivot ? pvp : pv);
   int ev = tbeg(h, K_PIVOT);
-  if (max_n <= PIVW_MAXN && !h->lu_pivot) {   // one warp per node
+  const bool wide = (h->piv_cnt_hint > 0 ? (size_t)h->piv_cnt_hint : pv.size()) > 2 * 148;
+  if (max_n <= PIVW_MAXN && !h->lu_pivot && wide) {   // one warp per node (wide waves)
     constexpr int W = PivW<1>::WARPS;
     launch_k(k_pivot_lu_warp<1>, (unsigned)((pv.size() + W - 1) / W), 32 * W, PivW<1>::SMEM, h->stream,
              (const PivTask *)dp, (int)pv.size(), h->d_status.as<int>());
@@ -1595,6 +1601,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
   h->dist_bytes = 0;
   h->dist_calls = 0;
   h->piv_maxn_hint = 0;
+  h->piv_cnt_hint = 0;
   h->launches_factor = 0;
   h->split_nodes = 0;
   h->flops_model = 0;
@@ -2063,7 +2070,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           h->ws_T1.ensure(yt * 8 + 256, st);
         }
       }
-      int max_n = 0, pv_max_small = 0, pv_max_all = 0;
+      int max_n = 0, pv_max_small = 0, pv_max_all = 0, pv_cnt_small = 0, pv_cnt_all = 0;
       double f_proj = 0, b_proj = 0, f_piv = 0, b_piv = 0, f_z = 0, b_z = 0, f_s = 0, b_s = 0;
       // neighbour push (dist): the blocks each node writes, their reader masks, the writer
       std::vector<DirtyList> wr_blocks;
@@ -2518,7 +2525,11 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
           for (size_t q = n_pv; q < pv.size(); ++q) {   // the pivot batch as one GPU would see it
             const int pn = pv[q].m + pv[q].r;
             pv_max_all = std::max(pv_max_all, pn);
-            if (pn <= PIV_SMALL_N) pv_max_small = std::max(pv_max_small, pn);
+            ++pv_cnt_all;
+            if (pn <= PIV_SMALL_N) {
+              pv_max_small = std::max(pv_max_small, pn);
+              ++pv_cnt_small;
+            }
           }
           // the record F stays on its owner (distributed apply); each written
           // block goes to the ranks that read or update it later
@@ -2550,6 +2561,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         h->recs.push_back(std::move(rec));
       }
       h->piv_maxn_hint = dist ? (sym ? pv_max_small : pv_max_all) : 0;
+      h->piv_cnt_hint = dist ? (sym ? pv_cnt_small : pv_cnt_all) : 0;
       // all descriptors of the wave travel in one H2D copy
       // descriptors in two groups: the pivot section below pushes its own task
       // lists, and a staging-ring wrap there (which reuses the ring after
@@ -3579,6 +3591,7 @@ void replan_general(lorasp_ctx *h, const char *why) {
   h->dest_ready = false;
   h->leaf_soff.clear();
   h->piv_maxn_hint = 0;
+  h->piv_cnt_hint = 0;
   h->eig_clmax_hint = h->eig_bigmax_hint = h->eig_regmax_hint = 0;
   h->rank_cache.clear();
   h->lu_pivot = true;
