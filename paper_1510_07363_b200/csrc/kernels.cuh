@@ -2395,7 +2395,8 @@ __global__ void __launch_bounds__((REG || PRE) ? EIG_REG_THREADS : EIG_THREADS)
 // (unscaled) to the record; CTA 0 also lam[0], ||T|| bound, ncomp and the trace.
 // The rank (Eq. cutOff1 / curOff6) is decided by k_invit_multi from these.
 constexpr int REC_NCOMP = 2, REC_TRACE = 3;   // record slots rec[3 m + .]
-__global__ void __launch_bounds__(512, 1) k_eigvals_cl(const EigTask *__restrict__ tasks, double eps, int nch) {
+__global__ void __launch_bounds__(512, 1) k_eigvals_cl(const EigTask *__restrict__ tasks, double eps, int nch,
+                                                       int egmax) {
   extern __shared__ double sh[];
   __shared__ double s_red[32], s_bc[8];
   __shared__ int s_int[4];
@@ -2501,11 +2502,21 @@ __global__ void __launch_bounds__(512, 1) k_eigvals_cl(const EigTask *__restrict
   }
   const int per = (ncomp - 1 + nch - 1) / nch, k1 = 1 + c * per, k2 = min(ncomp, k1 + per);
   if (k1 >= k2) return;
-  const int cnt = k2 - k1;
-  if (cnt <= 16) grp_multisect<32>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm);
-  else if (cnt <= 32) grp_multisect<16>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm);
-  else if (cnt <= 64) grp_multisect<8>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm);
-  else grp_multisect<4>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm);
+  // lanes per eigenvalue: many (few rounds) for the latency-bound cluster path;
+  // egmax = 2 for the throughput path (many nodes per SM: the fewest Sturm
+  // steps per eigenvalue)
+  const int cnt = k2 - k1, lanes = (int)blockDim.x;
+  int eg = cnt * 32 <= lanes ? 32 : (cnt * 16 <= lanes ? 16 : (cnt * 8 <= lanes ? 8 : 4));
+  if (eg > egmax) eg = egmax;
+  if (eg < 2 && egmax >= 2) eg = 2;
+  switch (eg) {
+    case 32: grp_multisect<32>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm); break;
+    case 16: grp_multisect<16>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm); break;
+    case 8: grp_multisect<8>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm); break;
+    case 4: grp_multisect<4>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm); break;
+    case 2: grp_multisect<2>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm); break;
+    default: grp_multisect<1>(d, e2, m, k1, k2, gl, gu, pivmin, lam, bnorm); break;
+  }
 }
 
 // Stage 1: the rank from the eigenvalues (Eq. cutOff1, or Eq. curOff6 with the
@@ -2575,6 +2586,35 @@ __global__ void __launch_bounds__(256) k_invit_multi(const EigTask *__restrict__
     unsigned char *pv = reinterpret_cast<unsigned char *>(ws + 5 * (int64_t)m * nbc) + kk;
     invit_one(d, e, m, sft, pertol, k, DL, Dv, DU, DU2, bb, pv, nbc, t.V + (int64_t)k * m);
   }
+}
+
+// Throughput path (waves of many nodes with m <= 128, after k_tridiag_reg,
+// k_eigvals_cl and k_invit_multi): MGS + back-transformation of one node per
+// 256-thread CTA, vectors in registers, the packed reflectors of the record
+// staged through shared memory; several nodes share an SM.
+template <int NV>
+__device__ __forceinline__ void orthbt_node(const EigTask &t, int m, int r, double *sh, int stg_cap) {
+  const double *rec = t.work + 6 * (int64_t)m * m;
+  double *tau = sh, *zb = sh + 136, *stg = zb + 256;
+  for (int i = threadIdx.x; i < m; i += blockDim.x) tau[i] = rec[2 * m + i];
+  __syncthreads();
+  orth_backtr<4, NV, true>(t.V, rec + 4 * (int64_t)m, tau, m, r, zb, nullptr, stg, stg_cap);
+}
+constexpr int ORTHBT_STG = 4096;   // reflector staging doubles per CTA
+constexpr size_t ORTHBT_SMEM = (size_t)(136 + 256 + ORTHBT_STG) * 8;
+__global__ void __launch_bounds__(256, 2) k_orthbt(const EigTask *__restrict__ tasks) {
+  extern __shared__ double sh[];
+  pdl_trigger();
+  const EigTask t = tasks[blockIdx.x];
+  pdl_wait();
+  const int m = t.m, r = *t.rank_out;
+  if (r <= 0 || m > 128) return;
+  const int per_w = (r + 7) / 8;
+  if (per_w <= 1) orthbt_node<1>(t, m, r, sh, ORTHBT_STG);
+  else if (per_w <= 2) orthbt_node<2>(t, m, r, sh, ORTHBT_STG);
+  else if (per_w <= 4) orthbt_node<4>(t, m, r, sh, ORTHBT_STG);
+  else if (per_w <= 8) orthbt_node<8>(t, m, r, sh, ORTHBT_STG);
+  else orthbt_node<16>(t, m, r, sh, ORTHBT_STG);
 }
 
 // Block Gram-Schmidt of the r inverse-iteration vectors over a cluster of CL

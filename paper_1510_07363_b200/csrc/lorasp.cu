@@ -569,6 +569,22 @@ static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps
   else if (c == 1) launch_k(k_tridiag_reg<false, 2, 8, 8>, (unsigned)n, 256, 0, st, ds, eps, (long long *)nullptr);
   else launch_k(k_tridiag_reg<false>, (unsigned)n, EIG_REG_THREADS, 0, st, ds, eps, (long long *)nullptr);
   CK(cudaGetLastError());
+  // waves of many nodes (several per SM) with m in (64, 128]: the one-CTA
+  // k_eig_t keeps a whole SM for one node through phases that use a fraction of
+  // it (lambda_0 in one warp, one thread per inverse-iteration vector); the
+  // throughput pipeline runs many nodes per SM instead: eigenvalues (128
+  // threads, 2 lanes per eigenvalue), rank + inverse iteration (one warp per 8
+  // vectors), MGS + back-transformation (256 threads per node)
+  if (c == 2 && wave_n > 2 * 148 && eps > 0.0) {
+    const int mp = (128 + 8) & ~7;
+    launch_k(k_eigvals_cl, (unsigned)n, 128, (size_t)3 * mp * 8, st, (const EigTask *)ds, eps, 1, 2);
+    const int64_t per = 5 * (int64_t)128 + (128 + 7) / 8;
+    const int cap = (int)(2 * mp + 8 * per);
+    launch_k(k_invit_multi, (unsigned)(n * 16), 32, (size_t)cap * 8, st, (const EigTask *)ds, 16, cap, eps);
+    launch_k(k_orthbt, (unsigned)n, 256, ORTHBT_SMEM, st, (const EigTask *)ds);
+    CK(cudaGetLastError());
+    return 4;
+  }
   // waves wider than the GPU are throughput bound: for m <= 64 half the shared
   // memory (still room for ~30 inverse-iteration vectors per batch) lets two
   // CTAs share an SM
@@ -595,7 +611,7 @@ static int launch_pre_post(cudaStream_t st, EigTask *dp, int n, int mmax, double
   // eigenvalues over several CTAs per node (about 40 candidates each)
   const int nev = std::max(1, std::min(16, (mmax + 39) / 40));
   launch_k(k_eigvals_cl, (unsigned)(n * nev), 512, (size_t)3 * ((mmax + 8) & ~7) * 8, st, (const EigTask *)dp, eps,
-           nev);
+           nev, 32);
   CK(cudaGetLastError());
   const int cap = SMEM_LIMIT / 8;
   const int64_t per = 5 * (int64_t)mmax + (mmax + 7) / 8;
@@ -731,6 +747,7 @@ void ensure_mem(lorasp_ctx *h) {
   CK(cudaFuncSetAttribute(k_apply_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_fwd_y, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_fwd_df, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+  CK(cudaFuncSetAttribute(k_orthbt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ORTHBT_SMEM));
   CK(cudaFuncSetAttribute(k_apply_bwd_df, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_fwd_z, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_apply_bwd_z, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
