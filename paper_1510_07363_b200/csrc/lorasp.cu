@@ -575,7 +575,7 @@ static int launch_eig_reg(cudaStream_t st, EigTask *ds, int n, int c, double eps
   // throughput pipeline runs many nodes per SM instead: eigenvalues (128
   // threads, 2 lanes per eigenvalue), rank + inverse iteration (one warp per 8
   // vectors), MGS + back-transformation (256 threads per node)
-  if (c == 2 && wave_n > 2 * 148 && eps > 0.0) {
+  if (c == 2 && wave_n > 148 && eps > 0.0) {
     const int mp = (128 + 8) & ~7;
     launch_k(k_eigvals_cl, (unsigned)n, 128, (size_t)3 * mp * 8, st, (const EigTask *)ds, eps, 1, 2);
     const int64_t per = 5 * (int64_t)128 + (128 + 7) / 8;
