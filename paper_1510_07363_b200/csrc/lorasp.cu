@@ -465,6 +465,7 @@ struct lorasp_ctx {
   int64_t fg_launches = 0;
   int eig_clmax_hint = 0, eig_bigmax_hint = 0, eig_regmax_hint = 0;   // the same for the eigen-solver classes
   int eig_reg_wave_n = 0;   // distributed: register-tile eigen tasks of the whole wave
+  int eig_cl_wave_n[5] = {0, 0, 0, 0, 0};   // distributed: cluster-class eigen tasks of the whole wave
 };
 
 namespace {
@@ -532,6 +533,34 @@ static int eig_cl_class(int m) {
   return 0;
 }
 
+// clusters of this shape that can be co-resident on the device (GPC-limited:
+// at most one 16-CTA cluster per GPC), queried once per shape
+template <int QR, int UC, int CL>
+static int tridiag_cl_fit() {
+  static int fit = -1;
+  if (fit < 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = (size_t)21 * 32 * QR * 8;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k_tridiag_cl<QR, UC, CL>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      nc = 0;
+    }
+    fit = nc;
+    if (getenv("LORASP_DEBUG")) fprintf(stderr, "[lorasp] k_tridiag_cl<%d, %d, %d>: %d co-resident clusters\n", QR, UC, CL, nc);
+  }
+  return fit;
+}
+
 template <int QR, int UC, int CL>
 static void launch_tridiag_cl_t(cudaStream_t st, const EigTask *dt, int n, double eps, long long *prof) {
   cudaLaunchConfig_t cfg = {};
@@ -549,15 +578,30 @@ static void launch_tridiag_cl_t(cudaStream_t st, const EigTask *dt, int n, doubl
   CK(cudaLaunchKernelEx(&cfg, k_tridiag_cl<QR, UC, CL>, dt, eps, prof));
 }
 
+// Cluster width per wave: the per-step latency falls with fewer columns per
+// warp (UC), so a wave whose nodes all fit on the device at once takes the
+// widest cluster that still fits (16 / 8 / 4 CTAs); wider waves keep the
+// narrower cluster (or, m <= 160, the one-CTA register-tile kernel).  wave_n:
+// the class's nodes in the whole wave, so that distributed ranks pick the
+// single-GPU shape.
 static void launch_tridiag_cl(cudaStream_t st, const EigTask *dt, int n, int cls, double eps,
-                              long long *prof = nullptr) {
-  if (cls == 4) {   // 128 < m <= 160: the register-tile tridiagonalisation in one CTA (the record format is shared)
-    launch_k(k_tridiag_reg<false, 5, 16, 10>, (unsigned)n, 512, 0, st, dt, eps, (long long *)nullptr);
+                              long long *prof = nullptr, int wave_n = 0) {
+  if (wave_n <= 0) wave_n = n;
+  if (cls == 4) {   // 128 < m <= 160
+    if (wave_n <= tridiag_cl_fit<5, 2, 8>()) launch_tridiag_cl_t<5, 2, 8>(st, dt, n, eps, prof);
+    else   // the register-tile tridiagonalisation in one CTA (the record format is shared)
+      launch_k(k_tridiag_reg<false, 5, 16, 10>, (unsigned)n, 512, 0, st, dt, eps, (long long *)nullptr);
     return;
   }
-  if (cls == 1) launch_tridiag_cl_t<8, 4, 4>(st, dt, n, eps, prof);
-  else if (cls == 2) launch_tridiag_cl_t<12, 3, 8>(st, dt, n, eps, prof);
-  else launch_tridiag_cl_t<16, 2, 16>(st, dt, n, eps, prof);
+  if (cls == 1) {
+    if (wave_n <= tridiag_cl_fit<8, 2, 8>()) launch_tridiag_cl_t<8, 2, 8>(st, dt, n, eps, prof);
+    else launch_tridiag_cl_t<8, 4, 4>(st, dt, n, eps, prof);
+  } else if (cls == 2) {
+    if (wave_n <= tridiag_cl_fit<12, 2, 16>()) launch_tridiag_cl_t<12, 2, 16>(st, dt, n, eps, prof);
+    else launch_tridiag_cl_t<12, 3, 8>(st, dt, n, eps, prof);
+  } else {
+    launch_tridiag_cl_t<16, 2, 16>(st, dt, n, eps, prof);
+  }
 }
 
 // Register-tile eigen path for m <= 128: tridiagonalisation (tile class c:
@@ -695,6 +739,11 @@ static void set_eig_attrs() {
   CK(cudaFuncSetAttribute(k_tridiag_cl<12, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 12 * 8));
   CK(cudaFuncSetAttribute(k_tridiag_cl<16, 2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 16 * 8));
   CK(cudaFuncSetAttribute(k_tridiag_cl<16, 2, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(k_tridiag_cl<8, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 8 * 8));
+  CK(cudaFuncSetAttribute(k_tridiag_cl<12, 2, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 12 * 8));
+  CK(cudaFuncSetAttribute(k_tridiag_cl<12, 2, 16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  CK(cudaFuncSetAttribute(k_tridiag_cl<5, 2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 21 * 32 * 5 * 8));
+
 }
 
 void ensure_mem(lorasp_ctx *h) {
@@ -896,7 +945,8 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
         cs = h->stream_cl[c - 2];
         CK(cudaStreamWaitEvent(cs, h->ev_cf, 0));
       }
-      launch_tridiag_cl(cs, dc[c], (int)clt[c].size(), c, h->plan.eps);
+      launch_tridiag_cl(cs, dc[c], (int)clt[c].size(), c, h->plan.eps, nullptr,
+                        h->eig_cl_wave_n[c] > 0 ? h->eig_cl_wave_n[c] : (int)clt[c].size());
       ++h->launches_factor;
       if (cs != h->stream) {
         CK(cudaEventRecord(h->ev_cj[c - 2], cs));
@@ -1894,6 +1944,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         int max_m = 0;
         double f_gram = 0, b_gram = 0, f_eig = 0, b_eig = 0;
         h->eig_clmax_hint = h->eig_bigmax_hint = h->eig_regmax_hint = h->eig_reg_wave_n = 0;
+        for (int &x : h->eig_cl_wave_n) x = 0;
         if (dist) {
           CK(cudaMemsetAsync(h->d_ranks.p, 0, comp.size() * sizeof(int), st));
           // launch-shape choices from the whole wave, so that every rank runs
@@ -1905,7 +1956,10 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
               ++h->eig_reg_wave_n;
               continue;
             }
-            if (eig_cl_class(mc)) h->eig_clmax_hint = std::max(h->eig_clmax_hint, mc);
+            if (const int k = eig_cl_class(mc)) {
+              h->eig_clmax_hint = std::max(h->eig_clmax_hint, mc);
+              ++h->eig_cl_wave_n[k];
+            }
             else h->eig_bigmax_hint = std::max(h->eig_bigmax_hint, mc);
           }
         }
@@ -3610,6 +3664,7 @@ void replan_general(lorasp_ctx *h, const char *why) {
   h->piv_maxn_hint = 0;
   h->piv_cnt_hint = 0;
   h->eig_clmax_hint = h->eig_bigmax_hint = h->eig_regmax_hint = 0;
+  for (int &x : h->eig_cl_wave_n) x = 0;
   h->rank_cache.clear();
   h->lu_pivot = true;
   ++h->spd_fallbacks;
