@@ -794,12 +794,18 @@ __device__ __forceinline__ void sturm_count_multi(const double *__restrict__ d, 
     if (zero[q]) c[q] = sturm_count(d, e2, m, x[q], 0.0);
 }
 
-__global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tasks, double eps, int *status) {
+// NW warps per node: warp 0 runs every phase; with NW > 1 the eigenvalue phase
+// (the longest: one lane per eigenvalue bisects ~50 Sturm counts deep) runs
+// on the whole block as a group multisection with NW lanes per eigenvalue
+// (log2(NW + 1) bits per round).  Waves of few nodes take NW = 8, wide waves
+// NW = 4 or 1 (throughput).
+template <int NW>
+__global__ void __launch_bounds__(32 * NW) k_eig_warp(const EigTask *__restrict__ tasks, double eps, int *status) {
   extern __shared__ double sh[];
   pdl_trigger();
   const EigTask t = tasks[blockIdx.x];
   pdl_wait();
-  const int m = t.m, lane = threadIdx.x;
+  const int m = t.m, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double *Hv = sh, *d = Hv + EIGW_M * EIGW_LD, *e = d + 40, *e2 = e + 40, *tau = e2 + 40, *lam = tau + 40;
   double *vs = lam + 40, *ws = vs + EIGW_M, *LU = ws + EIGW_M, *Z = LU + 5 * EIGW_M * EIGW_M;
   unsigned char *pv = reinterpret_cast<unsigned char *>(Z + EIGW_M * EIGW_LD);
@@ -820,6 +826,7 @@ __global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tas
   fro = warp_sum(fro);
   trace = warp_sum(trace);
   if (!(fro > 0.0) || eps == 0.0) {   // G = 0: r = 0 (Z4); eps = 0: V = I, r = m (Z3)
+    if (warp != 0) return;   // every warp computed the same fro: uniform exit
     const bool keep = fro > 0.0;
     if (keep)
       for (int k = 0; k < m; ++k)
@@ -828,7 +835,8 @@ __global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tas
     if (lane == 0) *t.rank_out = keep ? m : 0;
     return;
   }
-  if (t.dbg && lane == 0) t.dbg[0] = clock64();
+  if (t.dbg && threadIdx.x == 0) t.dbg[0] = clock64();
+  if (warp == 0) {
   // ---- 1. Householder tridiagonalisation (lower, dsytd2), lane = row; the step
   // loop is unrolled so that every register index is static; reciprocals by
   // frcp (an IEEE FP64 division is ~430 cycles of latency on this chain) ----
@@ -881,8 +889,10 @@ __global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tas
     if (lane < m) d[lane] = dl;
     if (m >= 2 && lane == m - 1) e[m - 2] = el;
   }
-  __syncwarp();
-  if (t.dbg && lane == 0) t.dbg[1] = clock64();
+  }   // warp 0
+  if constexpr (NW > 1) __syncthreads();
+  else __syncwarp();
+  if (t.dbg && threadIdx.x == 0) t.dbg[1] = clock64();
   // ---- 2. eigenvalues: lane l bisects the l-th largest (Sturm counts, T / bnorm) ----
   double gl = 1e300, gu = -1e300;
   for (int i = 0; i < m; ++i) {
@@ -893,12 +903,18 @@ __global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tas
   const double bnorm = fmax(fmax(fabs(gl), fabs(gu)), 1e-300);
   const double isc = frcp(bnorm);
   double *ds = LU, *e2s = LU + 40;   // scaled copies (padded: d = 4, e2 = 0 beyond m)
-  for (int i = lane; i < 40; i += 32) {
+  for (int i = threadIdx.x; i < 40; i += 32 * NW) {
     ds[i] = (i < m) ? d[i] * isc : 4.0;
     e2s[i] = (i < m - 1) ? (e[i] * isc) * (e[i] * isc) : 0.0;
   }
-  __syncwarp();
   double lo = gl * isc - 4.4e-16 * m - 1e-300, hi = gu * isc + 4.4e-16 * m + 1e-300;
+  if constexpr (NW > 1) {
+    __syncthreads();
+    grp_multisect<NW>(ds, e2s, m, 0, m, lo, hi, 0.0, lam, bnorm);
+    __syncthreads();
+    if (warp != 0) return;
+  } else {
+  __syncwarp();
   const int j = m - 1 - lane;   // ascending index of this lane's eigenvalue
   {   // common bracketing: the counts at 32 points (one per lane), 33 sub-intervals
     const double h = (hi - lo) * (1.0 / 33.0);
@@ -921,6 +937,7 @@ __global__ void __launch_bounds__(32) k_eig_warp(const EigTask *__restrict__ tas
     lam[lane] = 0.5 * (lo + hi) * bnorm;
   }
   __syncwarp();
+  }
   const double sig0 = sqrt(fmax(lam[0], 0.0));
   int r = 0;
   if (t.frob) {   // Eq. curOff6: smallest k with tail(k) = trace - sum_{t<k} lambda_t < budget

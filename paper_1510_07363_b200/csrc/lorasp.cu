@@ -465,6 +465,7 @@ struct lorasp_ctx {
   int64_t fg_launches = 0;
   int eig_clmax_hint = 0, eig_bigmax_hint = 0, eig_regmax_hint = 0;   // the same for the eigen-solver classes
   int eig_reg_wave_n = 0;   // distributed: register-tile eigen tasks of the whole wave
+  int eig_all_wave_n = 0;   // distributed: eigen tasks of the whole wave
   int eig_cl_wave_n[5] = {0, 0, 0, 0, 0};   // distributed: cluster-class eigen tasks of the whole wave
 };
 
@@ -731,7 +732,11 @@ static void set_eig_attrs() {
   CK(cudaFuncSetAttribute(k_backtr_multi<12, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_backtr_multi<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_eig_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EIG_REG_SMEM));
-  CK(cudaFuncSetAttribute(k_eig_warp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(k_eig_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(EIGW_SMEM_DOUBLES * sizeof(double))));
+  CK(cudaFuncSetAttribute(k_eig_warp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(EIGW_SMEM_DOUBLES * sizeof(double))));
+  CK(cudaFuncSetAttribute(k_eig_warp<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(EIGW_SMEM_DOUBLES * sizeof(double))));
   CK(cudaFuncSetAttribute(k_eig_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
   CK(cudaFuncSetAttribute(k_eig_t<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
@@ -882,8 +887,19 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
     for (const EigTask &e : et) mm = std::max(mm, e.m);
     if (h->eig_regmax_hint > 0) mm = std::max(mm, h->eig_regmax_hint);
     if (!et.empty() && mm <= EIGW_M) {
-      launch_k(k_eig_warp, (unsigned)et.size(), 32, EIGW_SMEM_DOUBLES * sizeof(double), h->stream,
-               (const EigTask *)de, h->plan.eps, h->d_status.as<int>());
+      // few nodes: 8 warps per node share the eigenvalue phase (latency);
+      // wide waves: 4 or 1 (throughput).  The whole wave decides (distributed).
+      const int nwave = h->eig_all_wave_n > 0 ? h->eig_all_wave_n : (int)et.size();
+      const size_t smem = EIGW_SMEM_DOUBLES * sizeof(double);
+      if (nwave <= 148)
+        launch_k(k_eig_warp<8>, (unsigned)et.size(), 256, smem, h->stream, (const EigTask *)de, h->plan.eps,
+                 h->d_status.as<int>());
+      else if (nwave <= 4 * 148)
+        launch_k(k_eig_warp<4>, (unsigned)et.size(), 128, smem, h->stream, (const EigTask *)de, h->plan.eps,
+                 h->d_status.as<int>());
+      else
+        launch_k(k_eig_warp<1>, (unsigned)et.size(), 32, smem, h->stream, (const EigTask *)de, h->plan.eps,
+                 h->d_status.as<int>());
       ++h->launches_factor;
       CK(cudaGetLastError());
       return;
@@ -1945,6 +1961,7 @@ bool factor_impl(lorasp_ctx *h, const double *values, bool replay, bool capture 
         double f_gram = 0, b_gram = 0, f_eig = 0, b_eig = 0;
         h->eig_clmax_hint = h->eig_bigmax_hint = h->eig_regmax_hint = h->eig_reg_wave_n = 0;
         for (int &x : h->eig_cl_wave_n) x = 0;
+        h->eig_all_wave_n = dist ? (int)comp.size() : 0;
         if (dist) {
           CK(cudaMemsetAsync(h->d_ranks.p, 0, comp.size() * sizeof(int), st));
           // launch-shape choices from the whole wave, so that every rank runs
@@ -4147,7 +4164,12 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     CK(cudaMalloc(&de, sizeof(EigTask)));
     CK(cudaMemcpy(de, &e, sizeof(EigTask), cudaMemcpyHostToDevice));
     if (m <= EIGW_M && !getenv("LORASP_EIG_GENERIC")) {   // the production path for m <= 32
-      k_eig_warp<<<1, 32, EIGW_SMEM_DOUBLES * sizeof(double)>>>(de, eps, dst);
+      // test hook: the warp count of the production variant (LORASP_TEST_EIGW_NW = 1 / 4 / 8)
+      const char *nwe = getenv("LORASP_TEST_EIGW_NW");
+      const int nw = nwe ? atoi(nwe) : 8;
+      if (nw == 1) k_eig_warp<1><<<1, 32, EIGW_SMEM_DOUBLES * sizeof(double)>>>(de, eps, dst);
+      else if (nw == 4) k_eig_warp<4><<<1, 128, EIGW_SMEM_DOUBLES * sizeof(double)>>>(de, eps, dst);
+      else k_eig_warp<8><<<1, 256, EIGW_SMEM_DOUBLES * sizeof(double)>>>(de, eps, dst);
     } else {
       if (m >= EIG_REG_MIN && m <= EIG_REG_M && !getenv("LORASP_EIG_GENERIC")) {
         if (ddbg) {

@@ -129,3 +129,23 @@ def test_eig_large_rank(L, m):
     _, _, Vt = np.linalg.svd(M)
     Pr = Vt[:r].T @ Vt[:r]
     assert np.max(np.abs(V @ V.T - Pr)) <= 1e-8
+
+
+@pytest.mark.parametrize("nw", ["1", "4", "8"])
+@pytest.mark.parametrize("m", [2, 3, 9, 24, 32])
+def test_eig_warp_variants_match_svd(L, m, nw, monkeypatch):
+    """k_eig_warp with 1 / 4 / 8 warps per node (the eigenvalue phase as a group
+    multisection over NW lanes per eigenvalue when NW > 1): same bar as above
+    against the SVD of the stack, and the three variants' sigma agree to 1e-13."""
+    M = stack(m, 2 * m + 3, 0.7, seed=100 + m)
+    G = M.T @ M
+    monkeypatch.setenv("LORASP_TEST_EIGW_NW", nw)
+    sig, V, r, st = L.test_eig(G, 1e-3)
+    assert st == 0
+    s_ref = np.linalg.svd(M, compute_uv=False)
+    r_ref = int(np.sum(s_ref >= 1e-3 * s_ref[0]))
+    assert r == r_ref
+    assert np.max(np.abs(sig[:r] - s_ref[:r])) <= 1e-12 * s_ref[0]
+    assert np.allclose(V.T @ V, np.eye(r), rtol=0, atol=1e-12)
+    _, _, Vt = np.linalg.svd(M)
+    assert np.max(np.abs(V @ V.T - Vt[:r].T @ Vt[:r])) <= 1e-8
