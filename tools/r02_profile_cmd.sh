@@ -15,4 +15,8 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --set full --clock-control none --import-source on -k regex:"k_gemm2_dmma" -s 40 -c 2 -o gpurun_out/r02_gemm_cfg4 python tools/profile_run.py cfg4 1 > gpurun_out/ncu_gemm.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_apply_fwd_df" -c 1 -o gpurun_out/r02_applydf_cfg4 python tools/apply_profile.py cfg4 1 > gpurun_out/ncu_apdf.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_orth_bgs|k_eigvals_cl|k_tridiag_cl" -s 30 -c 3 -o gpurun_out/r02_eigcl_cfg3 python tools/profile_run.py cfg3 1 > gpurun_out/ncu_eigcl.log 2>&1
+# full captures at the final state: the cfg3 cluster tridiagonalisation (16-CTA class 2), the cfg2 few-node k_eig_warp<8>
+ncu --set full --clock-control none --import-source on -k regex:"k_tridiag_cl" -s 20 -c 2 -o gpurun_out/r02_trcl_cfg3 python tools/profile_run.py cfg3 1 > gpurun_out/ncu_trcl.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_eig_warp|k_tridiag_reg" -s 4 -c 4 -o gpurun_out/r02_eigw_cfg2 python tools/profile_run.py cfg2 1 > gpurun_out/ncu_eigw.log 2>&1
+
 ls -la gpurun_out/
