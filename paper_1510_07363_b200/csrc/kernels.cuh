@@ -797,8 +797,8 @@ __device__ __forceinline__ void sturm_count_multi(const double *__restrict__ d, 
 // NW warps per node: warp 0 runs every phase; with NW > 1 the eigenvalue phase
 // (the longest: one lane per eigenvalue bisects ~50 Sturm counts deep) runs
 // on the whole block as a group multisection with NW lanes per eigenvalue
-// (log2(NW + 1) bits per round).  Waves of few nodes take NW = 8, wide waves
-// NW = 4 or 1 (throughput).
+// (log2(NW + 1) bits per round).  Waves of up to 4 nodes per SM take NW = 4,
+// wider waves NW = 1 (throughput); NW = 8 is kept for the unit tests.
 template <int NW>
 __global__ void __launch_bounds__(32 * NW) k_eig_warp(const EigTask *__restrict__ tasks, double eps, int *status) {
   extern __shared__ double sh[];
@@ -944,8 +944,8 @@ __global__ void __launch_bounds__(32 * NW) k_eig_warp(const EigTask *__restrict_
     const double fbud = eps * eps * (*t.frob) / t.frob_w;
     double pre = 0.0;
     while (r < m && !(trace - pre < fbud)) pre += fmax(lam[r++], 0.0);
-  } else if (sig0 > 0.0) {
-    for (int k = 0; k < m; ++k) r += (sqrt(fmax(lam[k], 0.0)) >= eps * sig0);
+  } else if (sig0 > 0.0) {   // lane k compares sigma_k (m <= 32)
+    r = __popc(__ballot_sync(0xffffffffu, lane < m && sqrt(fmax(lam[lane], 0.0)) >= eps * sig0));
   }
   if (lane < m) t.sig[lane] = sqrt(fmax(lam[lane], 0.0));
   if (lane == 0) *t.rank_out = r;
@@ -1376,7 +1376,12 @@ __device__ __forceinline__ int eig_values_phase(const EigTask &t, double eps, in
     __syncthreads();
     r = s_int[1];
   } else {
-    for (int k = 0; k < ncomp; ++k) r += (sqrt(fmax(lam[k], 0.0)) >= eps * sig0);
+    // the same comparison per candidate, one thread each (a serial loop of
+    // IEEE square roots was a ~100-cycle chain link per candidate)
+    for (int k0 = 0; k0 < ncomp; k0 += blockDim.x) {
+      const int k = k0 + tid;
+      r += __syncthreads_count(k < ncomp && sqrt(fmax(lam[k], 0.0)) >= eps * sig0);
+    }
   }
   for (int k = tid; k < m; k += blockDim.x) t.sig[k] = (k < ncomp) ? sqrt(fmax(lam[k], 0.0)) : 0.0;
   if (tid == 0) *t.rank_out = r;

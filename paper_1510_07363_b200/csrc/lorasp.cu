@@ -887,14 +887,13 @@ void launch_eig(lorasp_ctx *h, const std::vector<EigTask> &et, EigTask *de, int 
     for (const EigTask &e : et) mm = std::max(mm, e.m);
     if (h->eig_regmax_hint > 0) mm = std::max(mm, h->eig_regmax_hint);
     if (!et.empty() && mm <= EIGW_M) {
-      // few nodes: 8 warps per node share the eigenvalue phase (latency);
-      // wide waves: 4 or 1 (throughput).  The whole wave decides (distributed).
+      // waves of up to 4 nodes per SM: 4 warps per node share the eigenvalue
+      // phase (measured: 4 lanes per eigenvalue beat 8 at m = 24 / 32); wider
+      // waves: one warp per node (throughput).  The whole wave decides
+      // (distributed).
       const int nwave = h->eig_all_wave_n > 0 ? h->eig_all_wave_n : (int)et.size();
       const size_t smem = EIGW_SMEM_DOUBLES * sizeof(double);
-      if (nwave <= 148)
-        launch_k(k_eig_warp<8>, (unsigned)et.size(), 256, smem, h->stream, (const EigTask *)de, h->plan.eps,
-                 h->d_status.as<int>());
-      else if (nwave <= 4 * 148)
+      if (nwave <= 4 * 148)
         launch_k(k_eig_warp<4>, (unsigned)et.size(), 128, smem, h->stream, (const EigTask *)de, h->plan.eps,
                  h->d_status.as<int>());
       else
@@ -4166,7 +4165,7 @@ int lorasp_test_eig(int device, const double *G, int m, double eps, double *V, d
     if (m <= EIGW_M && !getenv("LORASP_EIG_GENERIC")) {   // the production path for m <= 32
       // test hook: the warp count of the production variant (LORASP_TEST_EIGW_NW = 1 / 4 / 8)
       const char *nwe = getenv("LORASP_TEST_EIGW_NW");
-      const int nw = nwe ? atoi(nwe) : 8;
+      const int nw = nwe ? atoi(nwe) : 4;
       if (nw == 1) k_eig_warp<1><<<1, 32, EIGW_SMEM_DOUBLES * sizeof(double)>>>(de, eps, dst);
       else if (nw == 4) k_eig_warp<4><<<1, 128, EIGW_SMEM_DOUBLES * sizeof(double)>>>(de, eps, dst);
       else k_eig_warp<8><<<1, 256, EIGW_SMEM_DOUBLES * sizeof(double)>>>(de, eps, dst);
