@@ -20,3 +20,5 @@ ncu --set full --clock-control none --import-source on -k regex:"k_tridiag_cl" -
 ncu --set full --clock-control none --import-source on -k regex:"k_eig_warp|k_tridiag_reg" -s 4 -c 4 -o gpurun_out/r02_eigw_cfg2 python tools/profile_run.py cfg2 1 > gpurun_out/ncu_eigw.log 2>&1
 
 ls -la gpurun_out/
+# final-state capture of the cfg2 leaf-wave eigen kernels (after the parallel rank test)
+python tools/profile_run.py cfg2 1 > gpurun_out/profrun.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:"k_eig_t|k_tridiag_reg" -s 0 -c 4 -o gpurun_out/r02_eigt_final_cfg2 -f python tools/profile_run.py cfg2 1 > gpurun_out/ncu_eigt.log 2>&1
